@@ -1,0 +1,339 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (CPU only).
+
+Each test names the pin of DESIGN.md §4 / SURVEY §8(c) it implements and the passage it follows.
+None of these re-type the oracle's formula: they use closed forms derived independently
+(constant flux, two-state chains, exact rationals), invariants, limits, numerical quadrature,
+an independent O(N) algorithm and a continuous-time Monte Carlo of the physical process.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+from scipy import integrate
+
+import oracle
+from workloads import Flux, config, random_flux
+
+RNG_SEED = 20250920
+
+
+def _rand_cases(n_cases, n_bins, seed=RNG_SEED):
+    rng = np.random.default_rng(seed)
+    out = []
+    for c in range(n_cases):
+        f = random_flux(rng, n_bins, 1 + c % 2)
+        out.append((f, float(rng.uniform(0.0, 3.0 * f.t_r))))
+    return out
+
+
+# ---------------------------------------------------------------- P1 row-stochastic
+@pytest.mark.parametrize("f,td", _rand_cases(4, 96))
+def test_p1_row_stochastic(oracle_lib, f, td):
+    P = oracle.build_eq4(f, td)
+    assert np.all(P > 0.0)                                   # B > 0 => every transition possible
+    assert np.max(np.abs(P.sum(axis=1) - 1.0)) <= 1e-12
+
+
+# ------------------------------------------- P2 permuted base == direct Eq. 4 (Thm 2)
+@pytest.mark.parametrize("f,td", _rand_cases(6, 80, seed=3) + [(config(1).items[0].flux, 75.0)])
+def test_p2_row_permutation_equals_direct(oracle_lib, f, td):
+    """Row i of P~(t_d) is row (i + l) mod N of P~(0), l = ceil(x_d / Delta).
+    Exact after normalisation, so the tolerance is rounding only; the opposite roll
+    direction must fail."""
+    P = oracle.build_eq4(f, td)
+    P0 = oracle.build_eq4(f, 0.0)
+    l = oracle.shift_l(f, td)
+    assert np.max(np.abs(np.roll(P0, -l, axis=0) - P)) <= 1e-15
+    if l % f.n_bins:
+        assert np.max(np.abs(np.roll(P0, +l, axis=0) - P)) > 1e-6
+
+
+# --------------------------------------------------- P3 whole periods (x_d = t_d mod t_r)
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_p3_whole_periods(oracle_lib, m):
+    f = config(1).items[0].flux
+    assert np.max(np.abs(oracle.build_eq4(f, m * f.t_r) - oracle.build_eq4(f, 0.0))) <= 1e-15
+    assert np.max(np.abs(oracle.build_eq4(f, 75.0 + m * f.t_r) - oracle.build_eq4(f, 75.0))) <= 1e-15
+
+
+# ------------------------------------------ P5 constant flux (S = 0): closed-form circulant chain
+@pytest.mark.parametrize("B,N,td", [(1.0, 64, 37.3), (3.0, 50, 75.0), (10.0, 33, 250.0), (0.5, 16, 0.0)])
+def test_p5_constant_flux_closed_form(oracle_lib, B, N, td):
+    """With S = 0 the flux is B / t_r everywhere, so the integral of Eq. 4 is B/t_r times the
+    distance from the re-arm bin centre to the next visit of s_j: P~_ij = r^d (1 - r) / (1 - r^N),
+    r = exp(-B/N), d = (j - i - l) mod N; pi is uniform and |lambda_2| follows from the DFT of a
+    circulant. Derived by hand from Eq. 3/4 for constant lambda (not from the oracle's code)."""
+    f = Flux(100.0, N, (50.0,), (1.0,), (0.0,), B)
+    P = oracle.build_eq4(f, td)
+    x_d = math.fmod(td, 100.0)
+    l = math.ceil(x_d / (100.0 / N) - 1e-9) % N    # the test's own shift: smallest bin offset >= x_d
+    r = math.exp(-B / N)
+    i = np.arange(N)[:, None]
+    j = np.arange(N)[None, :]
+    d = (j - i - l) % N
+    expect = r ** d * (1.0 - r) / (1.0 - r ** N)
+    assert np.max(np.abs(P - expect)) <= 1e-14
+    pi = oracle.stationary_dense(P)
+    assert np.max(np.abs(pi - 1.0 / N)) <= 1e-14
+    # circulant eigenvalues: sum_d c_d w^{kd}; the second largest magnitude
+    ev = np.abs(np.linalg.eigvals(P))
+    ev.sort()
+    k = np.arange(1, N)
+    lam = (1 - r) / (1 - r * np.exp(2j * np.pi * k / N))
+    assert abs(ev[-2] - np.max(np.abs(lam))) <= 1e-9
+
+
+def test_p5_abs_lambda2_values(oracle_lib):
+    """|lambda_2| of the S = 0 chain at N = 256: (1-r)/|1 - r e^{2 pi i/N}| for B = 1, 3, 10
+    (0.15718, 0.43088, 0.84675 to 5 digits)."""
+    N = 256
+    for B, want in ((1.0, 0.15718), (3.0, 0.43088), (10.0, 0.84675)):
+        f = Flux(100.0, N, (50.0,), (1.0,), (0.0,), B)
+        ev = np.sort(np.abs(np.linalg.eigvals(oracle.build_eq4(f, 75.0))))
+        assert abs(ev[-2] - want) < 5e-5
+
+
+# ------------------------------------------- P6 structure of E_base (diag = 1, range)
+def test_p6_exponent_structure(oracle_lib):
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        f = random_flux(rng, 40, 2)
+        Lam = oracle.Lambda(f)
+        d = f.t_r / f.n_bins
+        E = np.array([[oracle.entry_eq4_unnorm(f, 0.0, i, j) / oracle.lam(f, (j + 0.5) * d)
+                       for j in range(f.n_bins)] for i in range(f.n_bins)])
+        assert np.all(np.diag(E) == 1.0)                    # b = D(a) when j = i and t_d = 0
+        assert np.all(E <= 1.0) and np.all(E >= math.exp(-Lam) * (1 - 1e-14))
+        # along row i, E decays monotonically in the cyclic distance from s_i (the wrap term of
+        # Eq. 5/6 sits below the diagonal): E_i,(i+d) is non-increasing in d = 0..N-1
+        for i in range(f.n_bins):
+            cyc = E[i, (i + np.arange(f.n_bins)) % f.n_bins]
+            assert np.all(np.diff(cyc) <= 1e-15)
+        # and the full-period product closes: E_i,i-1 = e^{-Lambda} * E_i-1... via one period
+        assert abs(E[1, 0] - math.exp(-Lam) / E[0, 1]) <= 1e-13
+
+
+# ------------------------------------------------------------ P7 solver agreement
+@pytest.mark.parametrize("f,td", _rand_cases(3, 200, seed=11) + [(config(1).items[0].flux, 75.0)])
+def test_p7_dense_vs_power(oracle_lib, f, td):
+    P = oracle.build_eq4(f, td)
+    pd = oracle.stationary_dense(P)
+    pp, its, ch, ok = oracle.stationary_power(P, 1e-14)
+    assert ok and ch < 1e-14
+    assert np.sum(np.abs(pd - pp)) <= 1e-13
+    assert abs(pd.sum() - 1.0) <= 1e-14 and np.all(pd > 0)
+    assert np.sum(np.abs(pd @ P - pd)) <= 1e-14
+
+
+# ------------------------------------------------------------ P8 tiny analytic chains
+def test_p8_two_state(oracle_lib):
+    P = np.array([[0.9, 0.1], [0.2, 0.8]])
+    want = np.array([2.0 / 3.0, 1.0 / 3.0])
+    assert np.max(np.abs(oracle.stationary_dense(P) - want)) <= 1e-15
+    pp, its, ch, ok = oracle.stationary_power(P, 1e-15)
+    assert ok and np.max(np.abs(pp - want)) <= 1e-14
+
+
+def _exact_stationary(Pq):
+    """pi (P - I) = 0, sum pi = 1, in exact rationals (Gauss-Jordan)."""
+    n = len(Pq)
+    A = [[Pq[c][r] - (1 if r == c else 0) for c in range(n)] for r in range(n)]
+    b = [Fraction(0)] * n
+    A[-1] = [Fraction(1)] * n
+    b[-1] = Fraction(1)
+    for k in range(n):
+        p = next(r for r in range(k, n) if A[r][k] != 0)
+        A[k], A[p], b[k], b[p] = A[p], A[k], b[p], b[k]
+        for r in range(n):
+            if r != k and A[r][k] != 0:
+                m = A[r][k] / A[k][k]
+                A[r] = [x - m * y for x, y in zip(A[r], A[k])]
+                b[r] -= m * b[k]
+    return [b[k] / A[k][k] for k in range(n)]
+
+
+@pytest.mark.parametrize("N", [2, 3, 5])
+def test_p8_brute_force_rational(oracle_lib, N):
+    rng = np.random.default_rng(N)
+    f = random_flux(rng, N, 1)
+    P = oracle.build_eq4(f, float(rng.uniform(0, 150)))
+    Pq = [[Fraction(x) for x in row] for row in P]
+    # renormalise exactly so the rational chain is exactly stochastic
+    Pq = [[x / sum(row) for x in row] for row in Pq]
+    exact = np.array([float(x) for x in _exact_stationary(Pq)])
+    assert np.max(np.abs(oracle.stationary_dense(P) - exact)) <= 1e-15
+    pp, _, _, ok = oracle.stationary_power(P, 1e-15)
+    assert ok and np.max(np.abs(pp - exact)) <= 1e-14
+
+
+# ----------------------------- P9 / P12: the integral of Eq. 3/4 by quadrature (Thm 1)
+def _lam_tilde_integral(f, lo, hi):
+    """int_lo^hi lambda~ by adaptive quadrature of the oracle's pointwise lambda, split at period
+    boundaries and at the pulse centres (independent of the closed-form F)."""
+    total = 0.0
+    k0 = math.floor(lo / f.t_r)
+    k1 = math.floor(hi / f.t_r)
+    for k in range(k0, k1 + 1):
+        a = max(lo, k * f.t_r) - k * f.t_r
+        b = min(hi, (k + 1) * f.t_r) - k * f.t_r
+        if b <= a:
+            continue
+        pts = [p for p in f.tau if a < p < b]
+        v, _ = integrate.quad(lambda t: oracle.lam(f, t), a, b, points=pts or None, limit=400,
+                              epsabs=1e-13, epsrel=1e-12)
+        total += v
+    return total
+
+
+def test_p12_F_vs_quadrature(oracle_lib):
+    rng = np.random.default_rng(12)
+    for _ in range(5):
+        f = random_flux(rng, 100, 2)
+        for t in rng.uniform(0, f.t_r, 4):
+            assert abs(oracle.F(f, t) - _lam_tilde_integral(f, 0.0, t)) <= 1e-9 * max(1.0, oracle.Lambda(f))
+        # Lambda = S + B when the pulses sit well inside the period (reading R5)
+    f = config(1).items[0].flux
+    assert abs(oracle.Lambda(f) - 0.6) <= 1e-15
+
+
+def test_p9_theorem1_continuous(oracle_lib):
+    """Theorem 1 in continuous variables (Remark 1): with a = x_k + x_d and
+    b = ceil((a - x_{k+1}) / t_r) t_r + x_{k+1}, int_a^b lambda~ equals
+    Lambda 1{x_k' > x_{k+1}} + F(x_{k+1}) - F(x_k'), x_k' = (x_k + x_d) mod t_r.
+    The left side is quadrature; the right side uses the oracle's closed-form F."""
+    rng = np.random.default_rng(9)
+    f = random_flux(rng, 100, 1, sigma_bins=(5, 20))
+    Lam = oracle.Lambda(f)
+    for _ in range(60):
+        xk, xk1 = rng.uniform(0, f.t_r, 2)
+        td = rng.uniform(0, 3 * f.t_r)
+        xd = math.fmod(td, f.t_r)
+        a = xk + xd
+        b = math.ceil((a - xk1) / f.t_r) * f.t_r + xk1
+        lhs = _lam_tilde_integral(f, a, b)
+        xkp = math.fmod(xk + xd, f.t_r)
+        rhs = Lam * (xkp > xk1) + oracle.F(f, xk1) - oracle.F(f, xkp)
+        assert abs(lhs - rhs) <= 1e-8 * max(1.0, Lam)
+
+
+def test_p9_discrete_entries_are_integrals(oracle_lib):
+    """Each unnormalised oracle entry is lambda(s_j) exp(-int_{D(a)}^{D(b)} lambda~): recover the
+    integral and compare with quadrature between the bin-centre limits."""
+    rng = np.random.default_rng(19)
+    f = random_flux(rng, 24, 2, sigma_bins=(2, 8))
+    d = f.t_r / f.n_bins
+    for _ in range(40):
+        i, j = (int(x) for x in rng.integers(0, f.n_bins, 2))
+        td = float(rng.uniform(0, 2.5 * f.t_r))
+        x_d = math.fmod(td, f.t_r)
+        a = (i + 0.5) * d + x_d
+        Da = (math.ceil(a / d) - 0.5) * d
+        b = math.ceil((a - (j + 0.5) * d) / f.t_r) * f.t_r + (j + 0.5) * d
+        I = -math.log(oracle.entry_eq4_unnorm(f, td, i, j) / oracle.lam(f, (j + 0.5) * d))
+        assert abs(I - _lam_tilde_integral(f, Da, b)) <= 1e-8
+
+
+# ------------------------------------------------- P4 vanishing flux (t_d = 0 i.i.d. limit)
+def test_p4_vanishing_flux(oracle_lib):
+    """As S, B -> 0 every E_ij -> 1, so every row -> lambda / sum(lambda) and pi -> lambda/sum(lambda)
+    at any dead time, with an O(eps) error: L1/eps must be constant over decades of eps."""
+    base = config(1).items[0].flux
+    d = base.t_r / base.n_bins
+    ratios = []
+    for eps in (1e-2, 1e-3, 1e-4, 1e-5):
+        f = base.scaled(eps)
+        lam = np.array([oracle.lam(f, (j + 0.5) * d) for j in range(f.n_bins)])
+        pi = oracle.stationary_dense(oracle.build_eq4(f, 75.0))
+        ratios.append(np.sum(np.abs(pi - lam / lam.sum())) / eps)
+    assert ratios[-1] > 0
+    assert abs(ratios[2] / ratios[3] - 1) < 1e-3 and abs(ratios[1] / ratios[3] - 1) < 1e-2
+    assert 0.13 < ratios[-1] < 0.15      # SURVEY P4 scratch: c = 0.1384 for this shape
+
+
+# ---------------------------------------------------- P11 structured O(N) cross-check (F3)
+def test_p11_structured_matvec(oracle_lib):
+    """Independent O(N) algorithm: with w_j = lambda_j e^{-F_j} and D_r = sum_{j>=r} w_j +
+    e^{-Lambda} sum_{j<r} w_j, x^T P~0 = w * (cumsum(x/D) + e^{-Lambda} (sum - cumsum)(x/D))
+    (rank-1 semiseparable form of E_base). Built here from the oracle's pointwise
+    lambda and F only, then compared with the oracle's Eq. 4 matrix and its pi."""
+    f = config(2).items[3].flux.with_bins(512)
+    td = 50.0
+    N = f.n_bins
+    d = f.t_r / N
+    s = (np.arange(N) + 0.5) * d
+    lam = np.array([oracle.lam(f, t) for t in s])
+    Fv = np.array([oracle.F(f, t) for t in s])
+    Lam = oracle.Lambda(f)
+    w = lam * np.exp(-Fv)
+    U = np.cumsum(w[::-1])[::-1]
+    L = np.concatenate([[0.0], np.cumsum(w)[:-1]])
+    D = U + math.exp(-Lam) * L
+    l = oracle.shift_l(f, td)
+
+    def step(pi):
+        x = np.roll(pi, l)               # x_r = pi[(r - l) mod N]
+        z = x / D
+        c = np.cumsum(z)
+        y = w * (c + math.exp(-Lam) * (c[-1] - c))
+        return y / y.sum()
+
+    pi = np.full(N, 1.0 / N)
+    for _ in range(500):
+        nxt = step(pi)
+        if np.sum(np.abs(nxt - pi)) < 1e-15:
+            pi = nxt
+            break
+        pi = nxt
+    P = oracle.build_eq4(f, td)
+    x = np.random.default_rng(0).random(N)
+    x /= x.sum()
+    y_dense = x @ P
+    y_struct = step(x) * np.sum(x @ P)
+    assert np.max(np.abs(y_dense - y_struct)) <= 1e-15
+    assert np.sum(np.abs(oracle.stationary_dense(P) - pi)) <= 1e-13
+
+
+# ------------------------------------------------------------ P10 Monte Carlo
+def _bin_integrated_fa(f, n_hist):
+    edges = np.linspace(0.0, f.t_r, n_hist + 1)
+    Fe = np.array([oracle.F(f, e) for e in edges])
+    return np.diff(Fe) / Fe[-1]
+
+
+def _mc_freq(f, td, seed, n_hist, n_batches=20, per_batch=50000):
+    h = oracle.monte_carlo(f, td, seed, 1000, per_batch, n_batches, n_hist)
+    fr = h / per_batch
+    return fr.mean(axis=0), fr.std(axis=0, ddof=1) / math.sqrt(n_batches)
+
+
+def test_p10_mc_sampler_no_deadtime(oracle_lib):
+    """t_d = 0: registrations are i.i.d. f_a, so the MC histogram is the bin-integrated f_a."""
+    f = Flux(100.0, 16, (40.0,), (5.0,), (2.0,), 1.0)
+    m, se = _mc_freq(f, 0.0, 1, 16)
+    assert np.all(np.abs(m - _bin_integrated_fa(f, 16)) <= 4.5 * se + 1e-12)
+
+
+def test_p10_mc_constant_flux_uniform(oracle_lib):
+    f = Flux(100.0, 16, (40.0,), (5.0,), (0.0,), 2.0)
+    m, se = _mc_freq(f, 75.0, 2, 16)
+    assert np.all(np.abs(m - 1.0 / 16) <= 4.5 * se)
+
+
+@pytest.mark.parametrize("td", [75.0, 130.0])
+def test_p10_mc_vs_chain(oracle_lib, td):
+    """The chain's pi (fine N, aggregated to 16 comparison bins) against the continuous-time MC
+    of P:60: every bin within 4 SE (batch means) + 2 |pi_N - pi_2N| (first-order discretisation
+    bias)."""
+    f = Flux(100.0, 512, (40.0,), (5.0,), (2.0,), 1.0)
+    m, se = _mc_freq(f, td, 3, 16)
+    aggs = []
+    for n in (512, 1024):
+        P = oracle.build_eq4(f.with_bins(n), td)
+        pi, _, _, ok = oracle.stationary_power(P, 1e-14)
+        assert ok
+        aggs.append(pi.reshape(16, -1).sum(axis=1))
+    bias = np.abs(aggs[0] - aggs[1])
+    assert np.all(np.abs(m - aggs[1]) <= 4.0 * se + 2.0 * bias)
+    # and the dead-time distortion is real: the MC is far from the undistorted f_a
+    assert np.max(np.abs(m - _bin_integrated_fa(f, 16))) > 20 * np.max(se)
