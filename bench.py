@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the hot path of arXiv 2509.20500 on B200 (one JSON line on rank 0).
+
+A step = one pass of the whole hot path over one batch of synthetic input: step 1-2 (flux vectors,
+prefix sums, base matrix P~0 written to HBM) and step 3-4 (dead time folded into the gather,
+power iteration to L1 change < 1e-12 on the device) for every item of the workload.
+
+Default workload: BASELINE.json configs[4] ("c5"): N = 32768, t_r = 200 ns, two returns, fp64;
+one P~0, the t_d = 430 ns solve plus the 16-value dead-time sweep on the same P~0 (multi-vector GEMV)
+= 17 stationary solves per step. --workload c1..c5 selects another config (c2, c3: batched items).
+
+Metric (BASELINE.json): stationary solves/s (value, whole job), with transition-matrix entries/s,
+and the fraction of the HBM roofline of the dominant kernel (the power-iteration GEMV) and of the
+construction kernel. The 8.6 GB matrix is larger than the 126 MB L2, so no flush is needed between
+steps (config.l2 says so). Device time by CUDA events on the launching stream; max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--dtype f64|f32]
+                    [--mode factored|exp] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "stationary solves/s (with transition-matrix entries/s; % of HBM roofline)"
+UNIT = "solves/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    p.add_argument("--mode", default="factored", choices=["factored", "exp"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------- workload
+def workload_items(name):
+    from workloads import config
+    k = int(name[1])
+    w = config(k)
+    if k == 5:
+        groups = [(w.items[0].flux, [w.items[0].t_d]), (w.items[0].flux, [it.t_d for it in w.sweep])]
+    else:
+        groups = [(it.flux, [it.t_d]) for it in w.items]
+    return w, groups
+
+
+# ------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, dev_index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(dev_index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons, pw = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+                pw.append(float(f[6]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------------------------- our arm
+class OurStep:
+    def __init__(self, groups, dtype, mode):
+        import torch
+        import paper_2509_20500_b200 as spl
+        self.spl, self.torch = spl, torch
+        self.dt = torch.float64 if dtype == "f64" else torch.float32
+        self.mode = mode
+        self.N = groups[0][0].n_bins
+        # one base matrix per distinct flux; each group = (flux, dead times sharing that P~0)
+        fl, self.fluxes = [], []
+        for f, tds in groups:
+            if f not in fl:
+                fl.append(f)
+        self.fluxes = fl
+        M = len(fl)
+        self.P0 = spl.empty_matrix(self.N, self.dt, n_matrices=M)
+        self.ws_build = spl.workspace(self.N, M, 1)
+        self.plans = []
+        if len(groups) == M:     # one dead time per matrix (c1-c4): one plan over all M matrices
+            assert all(len(t) == 1 for _, t in groups)
+            tds = np.array([[t[0]] for _, t in groups])
+            self.plans.append(spl.Plan(self.P0, fl[0].t_r, tds, tol=1e-12))
+        else:                    # c5: several dead-time groups on one matrix
+            for f, tds in groups:
+                m = fl.index(f)
+                self.plans.append(spl.Plan(self.P0[m], f.t_r, np.array([tds]), tol=1e-12))
+        self.n_solves = sum(len(t) for _, t in groups)
+        self.entries = M * self.N * self.N
+
+    def build(self):
+        if len(self.fluxes) == 1:
+            self.spl.build_base(self.fluxes[0], self.dt, self.mode, out=self.P0[0], ws=self.ws_build)
+        else:
+            self.spl.build_base_batched(self.fluxes, self.dt, self.mode, out=self.P0, ws=self.ws_build)
+
+    def solve(self):
+        for p in self.plans:
+            p.launch()
+
+    def infos(self):
+        return [p.info() for p in self.plans]
+
+
+def run_ours(args, rank, world, dev):
+    import torch
+    import paper_2509_20500_b200 as spl
+    w, groups = workload_items(args.workload)
+    st = OurStep(groups, args.dtype, args.mode)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        st.build()
+        st.solve()
+    torch.cuda.synchronize()
+    infos = st.infos()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev)
+    time.sleep(0.25)
+    for e0, e1, e2 in ev:
+        e0.record(stream)
+        st.build()
+        e1.record(stream)
+        st.solve()
+        e2.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    t_build = sum(a.elapsed_time(b) for a, b, _ in ev) / 1e3
+    t_solve = sum(b.elapsed_time(c) for _, b, c in ev) / 1e3
+    t_total = sum(a.elapsed_time(c) for a, _, c in ev) / 1e3
+    infos = st.infos()
+    if world > 1:
+        t = torch.tensor([t_total, t_build, t_solve], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_total, t_build, t_solve = (float(x) for x in t.tolist())
+
+    b = 8 if args.dtype == "f64" else 4
+    N = st.N
+    # algorithmic GEMV bytes: every launch reads each still-active matrix once (N^2 b); launches =
+    # iterations of the longest vector in each plan; matrices whose vectors all converged are skipped
+    launches_gemv, gemv_bytes = 0, 0
+    for plan_info, p in zip(infos, st.plans):
+        per_m = np.array([i["iters"] for i in plan_info]).reshape(p.M, p.V).max(axis=1)
+        launches_gemv += int(per_m.max())
+        gemv_bytes += int(per_m.sum()) * N * N * b
+    per_step_launches = 3 + sum(2 + 2 * int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
+                                for pi, p in zip(infos, st.plans))
+    hbm, hbm_src = load_peaks()
+    K = args.steps
+    gemv_gbs = gemv_bytes * K / t_solve / 1e9
+    build_gbs = st.entries * b * K / t_build / 1e9
+    units = st.n_solves * K * world
+    value = units / t_total
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, w, groups, st, world)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": t_total / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic (seeded BASELINE.json flux parameters; inputs are theta only)",
+        "config": {"workload": f"{args.workload}: {w.description}", "n_bins": N,
+                   "matrices_per_step": len(st.fluxes), "solves_per_step": st.n_solves, "entry_mode": args.mode,
+                   "tol": 1e-12, "l2": "matrix (%.2f GB) > 126 MB L2: no flush needed" % (st.entries * b / 1e9)
+                   if st.entries * b > 126e6 else "matrix fits in L2 (latency-bound config); not flushed",
+                   "parallelism": f"replicas x{world} (independent items per rank, no collective)"},
+        "entries_per_s": st.entries * K * world / t_build,
+        "ms_build_per_step": t_build / K * 1e3, "ms_solve_per_step": t_solve / K * 1e3,
+        "iterations": [[i["iters"] for i in pi] for pi in infos],
+        "roofline": {"bound": "hbm", "kernel": "k_power_step (power-iteration GEMV)", "achieved": gemv_gbs,
+                     "peak": hbm, "unit": "GB/s", "frac": gemv_gbs / hbm, "traffic": None,
+                     "peak_source": hbm_src,
+                     "note": "achieved = algorithmic bytes (N^2 b per launch per active matrix) / solve-phase "
+                             "time, which also contains the convergence-check kernels and graph loop overhead"},
+        "roofline_build": {"bound": "hbm", "kernel": "k_build", "achieved": build_gbs, "peak": hbm, "unit": "GB/s",
+                           "frac": build_gbs / hbm, "note": "N^2 b bytes written per matrix / build-phase time "
+                                                            "(includes the flux-vector scan kernel)"},
+        "clocks": clk, "e2e": e2e, "gpu_launches": per_step_launches * K,
+        "impl": "ours", "lib": spl.lib_path(),
+    }
+    return line
+
+
+def run_e2e(args, w, groups, st, world):
+    """Same metric through the public API with host buffers: theta from the host, pi copied to pinned
+    host memory, every step; plans (CUDA graphs) created inside the timed region by splidar.sweep /
+    Plan as a user call would."""
+    import torch
+    import paper_2509_20500_b200 as spl
+    N = st.N
+    n_solves = st.n_solves
+    pi_host = torch.empty((n_solves, N), dtype=torch.float64, pin_memory=True)
+    dt = st.dt
+    h2d = 0
+    for f, tds in groups:
+        h2d += 8 * (3 * len(f.tau) + 3) + 8 * len(tds)
+
+    def one():
+        row = 0
+        if len(groups) == len(st.fluxes):
+            st.build()
+            T = np.array([[t[0]] for _, t in groups])
+            plan = spl.Plan(st.P0, groups[0][0].t_r, T, tol=1e-12, ws=None)
+            plan.execute()
+            pi_host[row:row + plan.M].copy_(plan.pi[:, 0], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            plan.close()
+        else:
+            st.build()
+            for f, tds in groups:
+                plan = spl.Plan(st.P0[0], f.t_r, np.array([tds]), tol=1e-12)
+                plan.execute()
+                pi_host[row:row + len(tds)].copy_(plan.pi[0], non_blocking=True)
+                row += len(tds)
+                torch.cuda.current_stream().synchronize()
+                plan.close()
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    torch.cuda.synchronize()
+    dt_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt_s], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt_s = float(t.item())
+    return {"value": n_solves * args.steps * world / dt_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": n_solves * N * 8,
+            "note": "host wall clock; includes plan (CUDA graph) instantiation, the theta upload and the pi "
+                    "copy to pinned host memory every step"}
+
+
+# ------------------------------------------------------------------------------- oracle arm
+def run_oracle_sample(args, iters_per_item=None):
+    """The CPU oracle as it stands on a bounded sample of the same workload: R rows of the Eq. 4
+    matrix (OpenMP over rows) and the oracle's long-double product over them; scaled to whole
+    solves. The oracle has no permutation trick, so it builds one Eq. 4 matrix per dead time."""
+    import oracle
+    w, groups = workload_items(args.workload)
+    N = groups[0][0].n_bins
+    R = min(N, 1024 if N >= 16384 else (2048 if N >= 4096 else N))
+    rng = np.random.default_rng(0)
+    t_build_row, t_mv_row = [], []
+    for f, tds in groups[:4]:
+        r0 = int(rng.integers(0, N - R + 1))
+        t0 = time.perf_counter()
+        rows = oracle.rows_eq4(f, tds[0], r0, r0 + R)
+        t_build_row.append((time.perf_counter() - t0) / R)
+        x = np.full(R, 1.0 / N)
+        t0 = time.perf_counter()
+        oracle.left_matvec(rows, x)
+        t_mv_row.append((time.perf_counter() - t0) / R)
+    tb, tm = statistics.median(t_build_row), statistics.median(t_mv_row)
+    total = 0.0
+    n = 0
+    for gi, (f, tds) in enumerate(groups):
+        for vi, _ in enumerate(tds):
+            its = iters_per_item[gi][vi] if iters_per_item else 25
+            total += N * tb + its * N * tm
+            n += 1
+    cores = os.cpu_count()
+    return {"value": n / total, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{args.workload}: {R} of {N} rows of Eq. 4 (OpenMP, {cores} threads) and one long-double "
+                      f"product over them (1 thread), for up to 4 items; scaled to {n} full solves "
+                      f"(N rows each, one Eq. 4 matrix per dead time, GPU iteration counts)",
+            "s_per_row_build": tb, "s_per_row_product": tm}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        samples = [run_oracle_sample(args) for _ in range(max(1, min(args.steps, 3)))]
+        v = statistics.median(s["value"] for s in samples)
+        w, _ = workload_items(args.workload)
+        cb = dict(samples[0])
+        cb["value"] = v
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": len(samples),
+                "warmup": 0, "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": args.dtype, "data": "synthetic", "impl": "reference",
+                "config": {"workload": f"{args.workload}: {w.description}", "n_bins": w.n_bins},
+                "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                                             "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import torch
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    line = run_ours(args, rank, world, dev)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = run_oracle_sample(args, line["iterations"])
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,178 @@
+/*
+ * splidar.h — C ABI of libsplidar.so, the B200 (sm_100a) hot path of arXiv 2509.20500
+ * ("non-sequential Markov modelling of asynchronous SP-LiDAR timestamps under dead time").
+ *
+ * Citations: "P:NN" is line NN of the paper's text, with its section/equation.
+ *
+ * The path:
+ *   1. flux vectors   lambda_j = lambda(s_j) (Eq. 1), the cumulative flux
+ *                     F_j = F(s_j) = int_0^{s_j} lambda (Thm 1) by a warp+block prefix sum of
+ *                     exact per-bin flux masses, Lambda = F(t_r), and the row normalisers.
+ *   2. base matrix    P~0 = rownorm((1 lambda^T) . exp.(-Lambda L - D))   (§3.4):
+ *                     P~0[r][j] = lambda_j exp(F_r - F_j - Lambda [r > j]) / Z_r.
+ *   3. dead time      P~ = J_l P~0, row i of P~ is row (i + l) mod N of P~0, l = ceil(x_d / Delta),
+ *                     x_d = t_d mod t_r (Thm 2). Folded into the solver's vector
+ *                     gather; materialised only by splidar_apply_deadtime.
+ *   4. stationary pdf pi P~ = pi by power iteration on the device.
+ *
+ * Conventions for every entry point:
+ *   - Times (t_r, t_d, tau, sigma) share one unit (ns in the benchmarks). S and B are mean photons
+ *     per laser period. Bins: Delta = t_r / n_bins, centres s_j = (j + 1/2) Delta,
+ *     j = 0..N-1.
+ *   - Matrices are row-major with leading dimension ld (elements), ld >= N, ld * sizeof(dtype) a
+ *     multiple of 16 bytes and the base pointer 16-byte aligned (else SPLIDAR_ENOSPACE).
+ *     Storage is fp64 or fp32 (splidar_dtype); every vector, every scan and every GEMV
+ *     accumulation is fp64 regardless.
+ *   - Device pointers are cudaMalloc'd / torch CUDA memory on the current device; host pointers
+ *     are ordinary host memory. The caller owns every buffer; the library allocates nothing on
+ *     the device, keeps no global state besides the last CUDA error code, and is re-entrant for
+ *     distinct (stream, workspace) pairs.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Argument errors are returned synchronously, before anything is enqueued.
+ *   - Entry points marked "async" only enqueue work on `stream`; the others synchronise `stream`
+ *     exactly once at their end.
+ */
+#ifndef SPLIDAR_H
+#define SPLIDAR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPLIDAR_OK = 0,
+    SPLIDAR_EINVAL = 1,   /* an argument violates an invariant (checked on the host, nothing enqueued) */
+    SPLIDAR_ENOCONV = 2,  /* max_iter reached before the L1 change fell below tol; pi holds the last
+                             iterate and info.l1_change the last change (not silently accepted) */
+    SPLIDAR_EZEROROW = 3, /* a row normaliser D_r was zero or non-finite on the device */
+    SPLIDAR_ENOSPACE = 4, /* workspace too small, ld < N, or a pointer / ld not 16-byte aligned */
+    SPLIDAR_ECUDA = 5     /* CUDA runtime error; splidar_last_cuda_error() returns its code */
+} splidar_status;
+
+typedef enum { SPLIDAR_F64 = 0, SPLIDAR_F32 = 1 } splidar_dtype;   /* storage of P~0 / P~ */
+
+/* How an entry of P~0 is evaluated (both compute the same matrix, §3.4):
+ *   SPLIDAR_ENTRY_EXP:      lambda_j * exp(F_r - F_j - Lambda [r > j]) * (1 / Z_r), one exp per
+ *                           entry (the paper's exp.(-Lambda L - D); fp64 exp for fp64 storage,
+ *                           ex2.approx for fp32 storage).
+ *   SPLIDAR_ENTRY_FACTORED: w_j * (r > j ? e^{-Lambda} : 1) * (1 / D_r), w_j = lambda_j e^{-F_j},
+ *                           D_r = Z_r e^{-F_r}: the same product with e^{F_r} cancelled by the
+ *                           row normalisation; no transcendental per entry. Default. */
+typedef enum { SPLIDAR_ENTRY_FACTORED = 0, SPLIDAR_ENTRY_EXP = 1 } splidar_entry;
+
+/* The problem statement theta without t_d: Eq. 1 generalised to K Gaussian pulses
+ * lambda(t) = sum_k S_k N(t; tau_k, sigma_k^2) + B / t_r on [0, t_r); K = 1 is the paper.
+ * All pointers are HOST pointers to K doubles. Invariants (else SPLIDAR_EINVAL): t_r > 0 finite;
+ * 2 <= n_bins <= 2^20; 0 <= n_pulses <= SPLIDAR_MAX_PULSES; sigma_k > 0; S_k >= 0;
+ * 0 <= tau_k < t_r; background B > 0 (a positive floor keeps the chain irreducible);
+ * sum_k S_k + B <= 600 (keeps e^{-F} representable in fp64). */
+#define SPLIDAR_MAX_PULSES 16
+typedef struct {
+    double t_r;            /* laser repetition period                  */
+    int32_t n_bins;        /* N = n_b; bin width Delta = t_r / N       */
+    int32_t n_pulses;      /* K                                               */
+    const double *tau;     /* host [K] pulse centres (depth delay)      */
+    const double *sigma;   /* host [K] pulse widths sigma_t            */
+    const double *signal;  /* host [K] S_k = alpha E, photons / period */
+    double background;     /* B = t_r lambda_b, photons / period       */
+} splidar_flux;
+
+typedef struct {
+    int32_t iters;        /* power-iteration products pi P~ taken                          */
+    int32_t converged;    /* 1 if the last L1 change was below tol                         */
+    int32_t shift_l;      /* l = ceil(x_d / Delta) mod N used for the dead time (Thm 2)    */
+    int32_t reserved;
+    double l1_change;     /* last || pi^k P~ - pi^k ||_1                                   */
+    double lambda_total;  /* Lambda = F(t_r) as computed on the device (0 if not computed) */
+} splidar_solve_info;
+
+/* Shift rule (Thm 2): l = ceil(u) mod N with u = fmod(t_d, t_r) * N / t_r in fp64
+ * (the single definition used everywhere; l = N is the same as 0). Host only, synchronous.
+ * t_r > 0, N >= 2, t_d >= 0, all finite, else SPLIDAR_EINVAL. */
+splidar_status splidar_shift(double t_r, int32_t n_bins, double t_d, int32_t *l_out);
+
+/* Device workspace (bytes) for n_matrices base matrices of N bins solved with up to n_vectors
+ * dead times each (n_vectors <= 16). Any workspace at least this large, 256-byte aligned, may
+ * be passed to every entry point below with the same or smaller sizes. */
+size_t splidar_workspace_bytes(int32_t n_bins, int32_t n_matrices, int32_t n_vectors);
+
+/* Steps 1a-1c of the path for one flux (async): writes the device vectors that the matrix is
+ * built from. Any output pointer may be NULL. F[j] = F(s_j) (prefix sum of exact bin masses,
+ * Thm 1), lam[j] = lambda(s_j) (Eq. 1), w[j] = lam[j] e^{-F[j]},
+ * inv_d[j] = 1 / D_j with D_r = sum_{j>=r} w_j + e^{-Lambda} sum_{j<r} w_j (row sum of
+ * exp.(-Lambda L - D) (1 lambda^T) divided by e^{F_r}), lambda_total[0] = Lambda = F(t_r).
+ * All outputs are device fp64 arrays of N (lambda_total: 1). */
+splidar_status splidar_flux_vectors(const splidar_flux *flux, double *F, double *lam, double *w,
+                                    double *inv_d, double *lambda_total, void *ws, size_t ws_bytes,
+                                    void *stream);
+
+/* Step 2 (async): the normalised dead-time-free base matrix P~0 (§3.4, normalisation
+ * P:79) into P0 (device, N x ld, dtype dt). Columns [N, ld) are not written. */
+splidar_status splidar_build_base(const splidar_flux *flux, splidar_dtype dt, splidar_entry mode,
+                                  void *P0, int64_t ld, void *ws, size_t ws_bytes, void *stream);
+
+/* Step 2 for n_matrices fluxes at once (async): matrix m goes to P0 + m * matrix_stride
+ * elements (matrix_stride >= N * ld, multiple of ld). All fluxes share n_bins. */
+splidar_status splidar_build_base_batched(const splidar_flux *fluxes, int32_t n_matrices,
+                                          splidar_dtype dt, splidar_entry mode, void *P0, int64_t ld,
+                                          int64_t matrix_stride, void *ws, size_t ws_bytes,
+                                          void *stream);
+
+/* Step 3 materialised (async): P[i][:] = P0[(i + l) mod N][:] with l = splidar_shift(t_r, N, t_d)
+ * (Thm 2). P and P0 are distinct device N x ld matrices of dtype dt (P == P0 is
+ * SPLIDAR_EINVAL). The solvers never need this: they fold l into their vector gather. */
+splidar_status splidar_apply_deadtime(const void *P0, void *P, int32_t n_bins, int64_t ld,
+                                      splidar_dtype dt, double t_r, double t_d, void *stream);
+
+/* Step 4 (synchronises stream once): pi P~ = pi for P~ = J_l P~0, by power iteration:
+ * pi^0 = 1/N; y = pi^k P~ (fp64 accumulation, the row permutation applied as the gather
+ * x_r = pi^k[(r - l) mod N] of a GEMV on P~0); pi^{k+1} = y / ||y||_1; stop after the first k with
+ * ||pi^{k+1} - pi^k||_1 < tol or after max_iter products. The loop runs on the device (CUDA
+ * graph with a conditional WHILE node): no host round trip per iteration.
+ * pi: device fp64 [N]. info: host, may be NULL. tol > 0, max_iter >= 1. */
+splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, splidar_dtype dt,
+                                  double t_r, double t_d, double tol, int32_t max_iter, double *pi,
+                                  void *ws, size_t ws_bytes, splidar_solve_info *info, void *stream);
+
+/* Steps 1-4 for a batch of (signal, background, dead-time) triples (synchronises stream once):
+ * item m has pulses (shape.tau, shape.sigma, S[m] * shape.signal[k]) and background B[m], dead time
+ * t_d[m]; shape.signal are relative weights and shape.background is ignored. Items with equal
+ * (S, B) share one P~0 (built once, solved with one multi-vector GEMV for all their dead times,
+ * up to 16 per pass). P0_store: device, room for n_store matrices of N x ld (dtype dt) with
+ * consecutive stride N * ld; unique (S, B) pairs are processed n_store at a time.
+ * pi: device fp64 [n_items * N] (item-major). info: host [n_items], may be NULL.
+ * Returns SPLIDAR_ENOCONV if any item did not converge (its pi is the last iterate). */
+splidar_status splidar_sweep(const splidar_flux *shape, int32_t n_items, const double *S,
+                             const double *B, const double *t_d, splidar_dtype dt, splidar_entry mode,
+                             double tol, int32_t max_iter, double *pi, void *P0_store,
+                             int32_t n_store, int64_t ld, void *ws, size_t ws_bytes,
+                             splidar_solve_info *info, void *stream);
+
+/* Plans: the solver of splidar_stationary / splidar_sweep captured once into an instantiated CUDA
+ * graph and replayed. A plan binds the matrices, shifts, workspace and pi pointers; executing it
+ * re-runs the whole power iteration from pi^0 (synchronises stream once). n_vectors dead times
+ * t_d[n_matrices * n_vectors] (matrix-major) share each matrix. Destroy with splidar_plan_destroy. */
+typedef struct splidar_plan_s *splidar_plan;
+splidar_status splidar_plan_create(splidar_plan *plan, const void *P0, int32_t n_matrices,
+                                   int64_t matrix_stride, int32_t n_bins, int64_t ld, splidar_dtype dt,
+                                   double t_r, const double *t_d, int32_t n_vectors, double tol,
+                                   int32_t max_iter, double *pi, void *ws, size_t ws_bytes,
+                                   void *stream);
+splidar_status splidar_plan_execute(splidar_plan plan, splidar_solve_info *info /* host [M*V] */,
+                                    void *stream);
+/* As execute, but only enqueues (async); read results later with splidar_plan_info. */
+splidar_status splidar_plan_launch(splidar_plan plan, void *stream);
+splidar_status splidar_plan_info(splidar_plan plan, splidar_solve_info *info, void *stream);
+void splidar_plan_destroy(splidar_plan plan);
+
+const char *splidar_strerror(splidar_status st);
+int splidar_last_cuda_error(void);     /* cudaError_t of the last SPLIDAR_ECUDA, else 0 */
+const char *splidar_build_info(void);  /* compile target and version string */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLIDAR_H */

@@ -62,6 +62,7 @@ def lib():
             "oracle_stationary_dense": (C.c_int, [i32, p, p]),
             "oracle_stationary_power": (C.c_int, [i32, p, d, i32, p, C.POINTER(i32), C.POINTER(d)]),
             "oracle_mc": (C.c_int, [fp, d, C.c_uint64, i64, i64, i32, i32, p]),
+            "oracle_left_matvec": (None, [i32, i32, p, p, p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -131,6 +132,15 @@ def left_matvec_streamed(flux, t_d: float, x: np.ndarray) -> np.ndarray:
     if lib().oracle_left_matvec_streamed(r.ref, float(t_d), x.ctypes.data, y.ctypes.data):
         raise ArithmeticError("oracle: streamed matvec failed")
     return y
+
+
+def left_matvec(rows: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """y = x^T rows (long double accumulation), the product inside stationary_power."""
+    rows = np.ascontiguousarray(rows, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty(rows.shape[1], dtype=np.longdouble)
+    lib().oracle_left_matvec(rows.shape[0], rows.shape[1], rows.ctypes.data, x.ctypes.data, y.ctypes.data)
+    return y.astype(np.float64)
 
 
 def stationary_dense(P: np.ndarray) -> np.ndarray:

@@ -196,6 +196,17 @@ int oracle_stationary_dense(int32_t n, const double *Pt, double *pi) {
     return 0;
 }
 
+/* y = x^T A for R rows of A (row-major, N columns), accumulated in long double (the product used by
+ * the power iteration below; exported so that bench.py can time a bounded sample of it). */
+void oracle_left_matvec(int32_t R, int32_t n, const double *A, const double *x, long double *y) {
+    for (int32_t j = 0; j < n; ++j) y[j] = 0.0L;
+    for (int32_t i = 0; i < R; ++i) {
+        long double xi = x[i];
+        const double *row = A + (int64_t)i * n;
+        for (int32_t j = 0; j < n; ++j) y[j] += xi * row[j];
+    }
+}
+
 /* Power iteration (the solver BASELINE.json names for P:79): pi^0 = 1/N; pi^{k+1} = y / ||y||_1 with
  * y = pi^k P~; stop when ||pi^{k+1} - pi^k||_1 < tol. Returns 0 converged, 3 if max_iter reached.
  * iters = number of products y = pi P~ taken. */
@@ -207,12 +218,7 @@ int oracle_stationary_power(int32_t n, const double *Pt, double tol, int32_t max
     double ch = INFINITY;
     int32_t it = 0;
     while (it < max_iter) {
-        for (int32_t j = 0; j < n; ++j) y[j] = 0.0L;
-        for (int32_t i = 0; i < n; ++i) {
-            long double xi = pi[i];
-            const double *row = Pt + (int64_t)i * n;
-            for (int32_t j = 0; j < n; ++j) y[j] += xi * row[j];
-        }
+        oracle_left_matvec(n, n, Pt, pi, y);
         long double s = 0.0L;
         for (int32_t j = 0; j < n; ++j) s += y[j];
         long double d = 0.0L;

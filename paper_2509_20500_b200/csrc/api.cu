@@ -1,0 +1,577 @@
+// The C ABI of include/splidar.h: host validation, the shift rule, workspace layout, kernel
+// dispatch and the CUDA-graph solver plans. No compute happens on the host: every step of the
+// path runs in the kernels of flux_vectors.cu, build.cu and power.cu.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace spl {
+
+static inline size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int pad_vectors(int V) {
+    int p = 1;
+    while (p < V) p <<= 1;
+    return p;
+}
+
+// Splits of the row range per column strip for the GEMV grid: about 2400 CTAs (two waves of
+// 8 resident 256-thread CTAs on 148 SMs), with 64 <= rows per split and at most 64 splits, so the
+// partial sums (splits x N fp64 per vector) stay small beside the N^2 matrix stream and the
+// strip reduction stays short.
+static int choose_splits(int N, int M, int strips) {
+    const long target = 2400;
+    long R = (target + (long)strips * M - 1) / ((long)strips * M);
+    const long hi = N / 64 > 1 ? N / 64 : 1;
+    if (R > hi) R = hi;
+    if (R > 64) R = 64;
+    if (R < 1) R = 1;
+    return (int)R;
+}
+
+WsLayout ws_layout(int N, int M, int V) {
+    WsLayout L;
+    memset(&L, 0, sizeof(L));
+    L.N = N;
+    L.M = M;
+    L.V = pad_vectors(V);
+    L.strips = (N + kStripCols - 1) / kStripCols;
+    int R = choose_splits(N, M, L.strips);
+    L.rows_per_split = (N + R - 1) / R;
+    L.splits = (N + L.rows_per_split - 1) / L.rows_per_split;
+    const size_t MV = (size_t)M * L.V;
+    size_t o = 0;
+    L.flux = o; o = a256(o + sizeof(FluxDev) * (size_t)M);
+    L.vec = o;  o = a256(o + sizeof(double) * ((size_t)M * N * 5 + (size_t)M * 8));
+    L.lsh = o;  o = a256(o + sizeof(int) * MV);
+    L.oidx = o; o = a256(o + sizeof(int) * MV);
+    L.y = o;    o = a256(o + sizeof(double) * MV * 2 * N);
+    L.part = o; o = a256(o + sizeof(double) * MV * L.splits * N);
+    L.ssum = o; o = a256(o + sizeof(double) * MV * L.strips);
+    L.chunks = (N + kCheckChunk - 1) / kCheckChunk;
+    L.l1part = o; o = a256(o + sizeof(double) * MV * L.chunks);
+    L.state = o; o = a256(o + sizeof(SolveState) * MV);
+    L.strip_cnt = o; o = a256(o + sizeof(unsigned) * (size_t)M * L.strips);
+    L.mv_cnt = o; o = a256(o + sizeof(unsigned) * MV);
+    L.glob = o; o = a256(o + sizeof(unsigned) * 4);
+    L.total = o;
+    return L;
+}
+
+static VecPtrs vec_ptrs(char *ws, const WsLayout &L) {
+    double *b = reinterpret_cast<double *>(ws + L.vec);
+    const size_t MN = (size_t)L.M * L.N;
+    VecPtrs v;
+    v.F = b;
+    v.lam = b + MN;
+    v.w = b + 2 * MN;
+    v.invD = b + 3 * MN;
+    v.invZ = b + 4 * MN;
+    v.scal = b + 5 * MN;
+    return v;
+}
+
+// Small host arrays reach the device as kernel parameters (async, stream-ordered, capturable;
+// no pageable-memcpy stream synchronisation).
+namespace {
+constexpr int kUpChunk = 3072;
+struct UpChunk {
+    unsigned char data[kUpChunk];
+    int n;
+};
+__global__ void k_upload(const UpChunk c, unsigned char *dst) {
+    for (int i = threadIdx.x; i < c.n; i += blockDim.x) dst[i] = c.data[i];
+}
+}  // namespace
+
+static cudaError_t upload_async(void *dst, const void *src, size_t n, cudaStream_t s) {
+    const unsigned char *p = static_cast<const unsigned char *>(src);
+    for (size_t o = 0; o < n; o += kUpChunk) {
+        UpChunk c;
+        c.n = (int)((n - o) < (size_t)kUpChunk ? (n - o) : (size_t)kUpChunk);
+        memcpy(c.data, p + o, (size_t)c.n);
+        k_upload<<<1, 256, 0, s>>>(c, static_cast<unsigned char *>(dst) + o);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace spl
+
+using namespace spl;
+
+static int g_last_cuda_error = 0;
+
+static splidar_status cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return SPLIDAR_OK;
+    g_last_cuda_error = (int)e;
+    return SPLIDAR_ECUDA;
+}
+#define SPL_CUDA(x)                                              \
+    do {                                                         \
+        cudaError_t e_ = (x);                                    \
+        if (e_ != cudaSuccess) return cuda_status(e_);           \
+    } while (0)
+
+static bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
+
+static splidar_status check_flux(const splidar_flux *f, int expect_n = -1) {
+    if (!f) return SPLIDAR_EINVAL;
+    if (!finite_pos(f->t_r)) return SPLIDAR_EINVAL;
+    if (f->n_bins < 2 || f->n_bins > (1 << 20)) return SPLIDAR_EINVAL;
+    if (expect_n >= 0 && f->n_bins != expect_n) return SPLIDAR_EINVAL;
+    if (f->n_pulses < 0 || f->n_pulses > kMaxPulses) return SPLIDAR_EINVAL;
+    if (f->n_pulses > 0 && (!f->tau || !f->sigma || !f->signal)) return SPLIDAR_EINVAL;
+    if (!finite_pos(f->background)) return SPLIDAR_EINVAL;
+    double tot = f->background;
+    for (int k = 0; k < f->n_pulses; ++k) {
+        if (!finite_pos(f->sigma[k])) return SPLIDAR_EINVAL;
+        if (!std::isfinite(f->signal[k]) || f->signal[k] < 0.0) return SPLIDAR_EINVAL;
+        if (!std::isfinite(f->tau[k]) || f->tau[k] < 0.0 || f->tau[k] >= f->t_r) return SPLIDAR_EINVAL;
+        tot += f->signal[k];
+    }
+    if (!(tot <= 600.0)) return SPLIDAR_EINVAL;
+    return SPLIDAR_OK;
+}
+
+static FluxDev to_dev(const splidar_flux *f, double s_scale = 1.0, double B = -1.0) {
+    FluxDev d;
+    memset(&d, 0, sizeof(d));
+    d.t_r = f->t_r;
+    d.n = f->n_bins;
+    d.k = f->n_pulses;
+    d.B = B >= 0.0 ? B : f->background;
+    for (int k = 0; k < f->n_pulses; ++k) {
+        d.tau[k] = f->tau[k];
+        d.sigma[k] = f->sigma[k];
+        d.S[k] = s_scale * f->signal[k];
+    }
+    return d;
+}
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+static splidar_status check_matrix(const void *P, int N, int64_t ld, int dt) {
+    if (!P) return SPLIDAR_EINVAL;
+    if (dt != SPLIDAR_F64 && dt != SPLIDAR_F32) return SPLIDAR_EINVAL;
+    const int esz = dt == SPLIDAR_F64 ? 8 : 4;
+    if (ld < N || ((ld * esz) & 15) != 0 || !aligned16(P)) return SPLIDAR_ENOSPACE;
+    return SPLIDAR_OK;
+}
+
+static splidar_status check_ws(const void *ws, size_t ws_bytes, const WsLayout &L) {
+    if (!ws || ((uintptr_t)ws & 255u) != 0 || ws_bytes < L.total) return SPLIDAR_ENOSPACE;
+    return SPLIDAR_OK;
+}
+
+extern "C" {
+
+splidar_status splidar_shift(double t_r, int32_t n_bins, double t_d, int32_t *l_out) {
+    if (!l_out || !finite_pos(t_r) || n_bins < 2 || !std::isfinite(t_d) || t_d < 0.0) return SPLIDAR_EINVAL;
+    const double u = std::fmod(t_d, t_r) * (double)n_bins / t_r;   // x_d / Delta (Thm 2)
+    long l = (long)std::ceil(u);
+    l %= n_bins;
+    *l_out = (int32_t)l;
+    return SPLIDAR_OK;
+}
+
+size_t splidar_workspace_bytes(int32_t n_bins, int32_t n_matrices, int32_t n_vectors) {
+    if (n_bins < 2 || n_matrices < 1 || n_vectors < 1 || n_vectors > kMaxVectors) return 0;
+    return ws_layout(n_bins, n_matrices, n_vectors).total;
+}
+
+const char *splidar_strerror(splidar_status st) {
+    switch (st) {
+        case SPLIDAR_OK: return "ok";
+        case SPLIDAR_EINVAL: return "invalid argument";
+        case SPLIDAR_ENOCONV: return "power iteration did not converge within max_iter";
+        case SPLIDAR_EZEROROW: return "zero or non-finite row normaliser";
+        case SPLIDAR_ENOSPACE: return "workspace too small, ld < N, or misaligned pointer / ld";
+        case SPLIDAR_ECUDA: return "CUDA runtime error";
+    }
+    return "unknown status";
+}
+
+int splidar_last_cuda_error(void) { return g_last_cuda_error; }
+
+const char *splidar_build_info(void) {
+    return "libsplidar sm_100a (nvcc " SPL_NVCC_VERSION "), fp64 vectors / fp64 accumulation";
+}
+
+// ---------------------------------------------------------------- steps 1-2 -----------------
+
+static splidar_status vectors_and_build(const FluxDev *fl, int M, int N, int dt, int mode, void *P0,
+                                        int64_t ld, int64_t mstride, char *ws, const WsLayout &L,
+                                        cudaStream_t s) {
+    SPL_CUDA(upload_async(ws + L.flux, fl, sizeof(FluxDev) * (size_t)M, s));
+    VecPtrs vp = vec_ptrs(ws, L);
+    SPL_CUDA(launch_flux_vectors(reinterpret_cast<const FluxDev *>(ws + L.flux), M, N, vp, N, s));
+    if (P0) SPL_CUDA(launch_build(vp, N, M, N, dt, mode, P0, ld, mstride, s));
+    return SPLIDAR_OK;
+}
+
+splidar_status splidar_flux_vectors(const splidar_flux *flux, double *F, double *lam, double *w,
+                                    double *inv_d, double *lambda_total, void *ws, size_t ws_bytes,
+                                    void *stream) {
+    splidar_status st = check_flux(flux);
+    if (st) return st;
+    const int N = flux->n_bins;
+    const WsLayout L = ws_layout(N, 1, 1);
+    if ((st = check_ws(ws, ws_bytes, L))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *wsb = static_cast<char *>(ws);
+    FluxDev d = to_dev(flux);
+    if ((st = vectors_and_build(&d, 1, N, SPLIDAR_F64, 0, nullptr, 0, 0, wsb, L, s))) return st;
+    VecPtrs vp = vec_ptrs(wsb, L);
+    const size_t nb = sizeof(double) * (size_t)N;
+    if (F) SPL_CUDA(cudaMemcpyAsync(F, vp.F, nb, cudaMemcpyDeviceToDevice, s));
+    if (lam) SPL_CUDA(cudaMemcpyAsync(lam, vp.lam, nb, cudaMemcpyDeviceToDevice, s));
+    if (w) SPL_CUDA(cudaMemcpyAsync(w, vp.w, nb, cudaMemcpyDeviceToDevice, s));
+    if (inv_d) SPL_CUDA(cudaMemcpyAsync(inv_d, vp.invD, nb, cudaMemcpyDeviceToDevice, s));
+    if (lambda_total) SPL_CUDA(cudaMemcpyAsync(lambda_total, vp.scal, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return SPLIDAR_OK;
+}
+
+splidar_status splidar_build_base_batched(const splidar_flux *fluxes, int32_t n_matrices, splidar_dtype dt,
+                                          splidar_entry mode, void *P0, int64_t ld, int64_t matrix_stride,
+                                          void *ws, size_t ws_bytes, void *stream) {
+    if (!fluxes || n_matrices < 1 || n_matrices > 65535) return SPLIDAR_EINVAL;
+    if (mode != SPLIDAR_ENTRY_FACTORED && mode != SPLIDAR_ENTRY_EXP) return SPLIDAR_EINVAL;
+    const int N = fluxes[0].n_bins;
+    splidar_status st;
+    for (int m = 0; m < n_matrices; ++m)
+        if ((st = check_flux(&fluxes[m], N))) return st;
+    if ((st = check_matrix(P0, N, ld, dt))) return st;
+    if (n_matrices > 1 && (matrix_stride < (int64_t)N * ld || matrix_stride % ld != 0)) return SPLIDAR_EINVAL;
+    const WsLayout L = ws_layout(N, n_matrices, 1);
+    if ((st = check_ws(ws, ws_bytes, L))) return st;
+    std::vector<FluxDev> d((size_t)n_matrices);
+    for (int m = 0; m < n_matrices; ++m) d[(size_t)m] = to_dev(&fluxes[m]);
+    return vectors_and_build(d.data(), n_matrices, N, dt, mode, P0, ld, matrix_stride,
+                             static_cast<char *>(ws), L, (cudaStream_t)stream);
+}
+
+splidar_status splidar_build_base(const splidar_flux *flux, splidar_dtype dt, splidar_entry mode, void *P0,
+                                  int64_t ld, void *ws, size_t ws_bytes, void *stream) {
+    return splidar_build_base_batched(flux, 1, dt, mode, P0, ld, flux ? (int64_t)flux->n_bins * ld : 0, ws,
+                                      ws_bytes, stream);
+}
+
+splidar_status splidar_apply_deadtime(const void *P0, void *P, int32_t n_bins, int64_t ld, splidar_dtype dt,
+                                      double t_r, double t_d, void *stream) {
+    int32_t l;
+    splidar_status st = splidar_shift(t_r, n_bins, t_d, &l);
+    if (st) return st;
+    if ((st = check_matrix(P0, n_bins, ld, dt))) return st;
+    if ((st = check_matrix(P, n_bins, ld, dt))) return st;
+    if (P == P0) return SPLIDAR_EINVAL;
+    return cuda_status(launch_apply_deadtime(P0, P, n_bins, ld, dt, l, (cudaStream_t)stream));
+}
+
+// ---------------------------------------------------------------- step 4: plans --------------
+
+struct splidar_plan_s {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    WsLayout L;
+    PowerArgs args;
+    int M = 0, V = 0, Vreal = 0;
+    std::vector<int> lsh;          // [M * V] (padded)
+    std::vector<SolveState> host;  // [M * V]
+    std::vector<int> out_idx;      // [M * V]
+};
+
+static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws, cudaStream_t s) {
+    const WsLayout &L = p->L;
+    PowerArgs &a = p->args;
+    a.y = reinterpret_cast<double *>(ws + L.y);
+    a.part = reinterpret_cast<double *>(ws + L.part);
+    a.ssum = reinterpret_cast<double *>(ws + L.ssum);
+    a.l1part = reinterpret_cast<double *>(ws + L.l1part);
+    a.st = reinterpret_cast<SolveState *>(ws + L.state);
+    a.lsh = reinterpret_cast<const int *>(ws + L.lsh);
+    a.strip_cnt = reinterpret_cast<unsigned *>(ws + L.strip_cnt);
+    a.mv_cnt = reinterpret_cast<unsigned *>(ws + L.mv_cnt);
+    a.glob = reinterpret_cast<unsigned *>(ws + L.glob);
+    a.N = L.N;
+    a.M = L.M;
+    a.V = L.V;
+    a.splits = L.splits;
+    a.strips = L.strips;
+    a.rows_per_split = L.rows_per_split;
+    a.chunks = L.chunks;
+
+    SPL_CUDA(spl::upload_async(ws + L.lsh, p->lsh.data(), sizeof(int) * p->lsh.size(), s));
+    SPL_CUDA(spl::upload_async(ws + L.oidx, p->out_idx.data(), sizeof(int) * p->out_idx.size(), s));
+
+    SPL_CUDA(cudaGraphCreate(&p->graph, 0));
+    cudaGraphConditionalHandle h;
+    SPL_CUDA(cudaGraphConditionalHandleCreate(&h, p->graph, 1, cudaGraphCondAssignDefault));
+    a.use_handle = 1;
+    a.handle = h;
+
+    SolverKernels k;
+    if (solver_kernels(dt, L.V, &k, a)) return SPLIDAR_EINVAL;
+
+    cudaKernelNodeParams kp;
+    memset(&kp, 0, sizeof(kp));
+    void *init_args[] = {&a};
+    kp.func = k.init_fn;
+    kp.gridDim = k.init_grid;
+    kp.blockDim = k.init_block;
+    kp.kernelParams = init_args;
+    cudaGraphNode_t n_init, n_while, n_step, n_fin;
+    SPL_CUDA(cudaGraphAddKernelNode(&n_init, p->graph, nullptr, 0, &kp));
+
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    SPL_CUDA(cudaGraphAddNode(&n_while, p->graph, &n_init, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+
+    void *step_args[] = {&a};
+    kp.func = k.step_fn;
+    kp.gridDim = k.step_grid;
+    kp.blockDim = k.step_block;
+    kp.sharedMemBytes = k.step_smem;
+    kp.kernelParams = step_args;
+    SPL_CUDA(cudaGraphAddKernelNode(&n_step, body, nullptr, 0, &kp));
+    void *check_args[] = {&a};
+    kp.func = k.check_fn;
+    kp.gridDim = k.check_grid;
+    kp.blockDim = k.check_block;
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = check_args;
+    cudaGraphNode_t n_check;
+    SPL_CUDA(cudaGraphAddKernelNode(&n_check, body, &n_step, 1, &kp));
+
+    std::vector<unsigned char> fa(finish_args_size());
+    make_finish_args(fa.data(), a, pi, reinterpret_cast<const int *>(ws + L.oidx));
+    void *fin_args[] = {fa.data()};
+    kp.func = k.finish_fn;
+    kp.gridDim = k.finish_grid;
+    kp.blockDim = k.finish_block;
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = fin_args;
+    SPL_CUDA(cudaGraphAddKernelNode(&n_fin, p->graph, &n_while, 1, &kp));
+
+    SPL_CUDA(cudaGraphInstantiate(&p->exec, p->graph, 0));
+    return SPLIDAR_OK;
+}
+
+void splidar_plan_destroy(splidar_plan plan) {
+    if (!plan) return;
+    if (plan->exec) cudaGraphExecDestroy(plan->exec);
+    if (plan->graph) cudaGraphDestroy(plan->graph);
+    delete plan;
+}
+
+// Internal: plan with explicit shifts (l < 0 = unused vector) and output rows.
+static splidar_status plan_create_l(splidar_plan *out, const void *P0, int M, int64_t mstride, int N, int64_t ld,
+                                    int dt, const int *l, int V, double tol, int max_iter, double *pi,
+                                    const int *out_idx, void *ws, size_t ws_bytes, cudaStream_t s) {
+    *out = nullptr;
+    splidar_status st;
+    if ((st = check_matrix(P0, N, ld, dt))) return st;
+    if (M < 1 || M > 65535 || V < 1 || V > kMaxVectors || !pi) return SPLIDAR_EINVAL;
+    if (M > 1 && (mstride < (int64_t)N * ld || mstride % ld != 0)) return SPLIDAR_EINVAL;
+    if (!(tol > 0.0) || !std::isfinite(tol) || max_iter < 1) return SPLIDAR_EINVAL;
+    splidar_plan_s *p = new splidar_plan_s();
+    p->L = ws_layout(N, M, V);
+    if ((st = check_ws(ws, ws_bytes, p->L))) { delete p; return st; }
+    p->M = M;
+    p->V = p->L.V;
+    p->Vreal = V;
+    p->lsh.assign((size_t)M * p->V, -1);
+    p->out_idx.assign((size_t)M * p->V, -1);
+    for (int m = 0; m < M; ++m)
+        for (int v = 0; v < V; ++v) {
+            p->lsh[(size_t)m * p->V + v] = l[(size_t)m * V + v];
+            p->out_idx[(size_t)m * p->V + v] = out_idx ? out_idx[(size_t)m * V + v] : m * V + v;
+        }
+    p->host.resize((size_t)M * p->V);
+    memset(&p->args, 0, sizeof(p->args));
+    p->args.P = P0;
+    p->args.ld = ld;
+    p->args.mstride = mstride;
+    p->args.tol = tol;
+    p->args.max_iter = max_iter;
+    if ((st = plan_build(p, dt, pi, static_cast<char *>(ws), s))) {
+        splidar_plan_destroy(p);
+        return st;
+    }
+    *out = p;
+    return SPLIDAR_OK;
+}
+
+splidar_status splidar_plan_create(splidar_plan *plan, const void *P0, int32_t n_matrices, int64_t matrix_stride,
+                                   int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r, const double *t_d,
+                                   int32_t n_vectors, double tol, int32_t max_iter, double *pi, void *ws,
+                                   size_t ws_bytes, void *stream) {
+    if (!plan || !t_d || n_matrices < 1 || n_vectors < 1 || n_vectors > kMaxVectors) return SPLIDAR_EINVAL;
+    std::vector<int> l((size_t)n_matrices * n_vectors);
+    for (size_t i = 0; i < l.size(); ++i) {
+        int32_t li;
+        splidar_status st = splidar_shift(t_r, n_bins, t_d[i], &li);
+        if (st) return st;
+        l[i] = li;
+    }
+    return plan_create_l(plan, P0, n_matrices, matrix_stride, n_bins, ld, dt, l.data(), n_vectors, tol, max_iter,
+                         pi, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+splidar_status splidar_plan_launch(splidar_plan plan, void *stream) {
+    if (!plan) return SPLIDAR_EINVAL;
+    return cuda_status(cudaGraphLaunch(plan->exec, (cudaStream_t)stream));
+}
+
+splidar_status splidar_plan_info(splidar_plan plan, splidar_solve_info *info, void *stream) {
+    if (!plan) return SPLIDAR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    SPL_CUDA(cudaMemcpyAsync(plan->host.data(), plan->args.st, sizeof(SolveState) * plan->host.size(),
+                             cudaMemcpyDeviceToHost, s));
+    SPL_CUDA(cudaStreamSynchronize(s));
+    bool all = true;
+    for (int m = 0; m < plan->M; ++m)
+        for (int v = 0; v < plan->Vreal; ++v) {
+            const SolveState &h = plan->host[(size_t)m * plan->V + v];
+            all = all && h.converged;
+            if (info) {
+                splidar_solve_info &o = info[(size_t)m * plan->Vreal + v];
+                o.iters = h.iters;
+                o.converged = h.converged;
+                o.shift_l = h.l;
+                o.reserved = 0;
+                o.l1_change = h.change;
+                o.lambda_total = 0.0;
+            }
+        }
+    return all ? SPLIDAR_OK : SPLIDAR_ENOCONV;
+}
+
+splidar_status splidar_plan_execute(splidar_plan plan, splidar_solve_info *info, void *stream) {
+    splidar_status st = splidar_plan_launch(plan, stream);
+    if (st) return st;
+    return splidar_plan_info(plan, info, stream);
+}
+
+splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r,
+                                  double t_d, double tol, int32_t max_iter, double *pi, void *ws,
+                                  size_t ws_bytes, splidar_solve_info *info, void *stream) {
+    splidar_plan p;
+    splidar_status st = splidar_plan_create(&p, P0, 1, (int64_t)n_bins * ld, n_bins, ld, dt, t_r, &t_d, 1, tol,
+                                            max_iter, pi, ws, ws_bytes, stream);
+    if (st) return st;
+    st = splidar_plan_execute(p, info, stream);
+    splidar_plan_destroy(p);
+    return st;
+}
+
+// ---------------------------------------------------------------- sweep ----------------------
+
+splidar_status splidar_sweep(const splidar_flux *shape, int32_t n_items, const double *S, const double *B,
+                             const double *t_d, splidar_dtype dt, splidar_entry mode, double tol, int32_t max_iter,
+                             double *pi, void *P0_store, int32_t n_store, int64_t ld, void *ws, size_t ws_bytes,
+                             splidar_solve_info *info, void *stream) {
+    if (!shape || n_items < 1 || !S || !B || !t_d || !pi || n_store < 1) return SPLIDAR_EINVAL;
+    if (mode != SPLIDAR_ENTRY_FACTORED && mode != SPLIDAR_ENTRY_EXP) return SPLIDAR_EINVAL;
+    const int N = shape->n_bins;
+    splidar_status st;
+    if ((st = check_matrix(P0_store, N, ld, dt))) return st;
+    // validate every item as a full flux and compute its shift
+    std::vector<int> l((size_t)n_items);
+    for (int i = 0; i < n_items; ++i) {
+        FluxDev d = to_dev(shape, S[i], B[i]);
+        splidar_flux f = *shape;
+        f.background = B[i];
+        std::vector<double> sig((size_t)shape->n_pulses);
+        for (int k = 0; k < shape->n_pulses; ++k) sig[(size_t)k] = d.S[k];
+        f.signal = sig.data();
+        if (!std::isfinite(S[i]) || S[i] < 0.0) return SPLIDAR_EINVAL;
+        if ((st = check_flux(&f))) return st;
+        int32_t li;
+        if ((st = splidar_shift(shape->t_r, N, t_d[i], &li))) return st;
+        l[(size_t)i] = li;
+    }
+    // group items by (S, B) in order of first appearance
+    std::vector<std::pair<double, double>> keys;
+    std::vector<std::vector<int>> members;
+    {
+        std::map<std::pair<double, double>, int> idx;
+        for (int i = 0; i < n_items; ++i) {
+            auto k = std::make_pair(S[i], B[i]);
+            auto it = idx.find(k);
+            if (it == idx.end()) {
+                idx[k] = (int)keys.size();
+                keys.push_back(k);
+                members.emplace_back();
+                members.back().push_back(i);
+            } else {
+                members[(size_t)it->second].push_back(i);
+            }
+        }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    char *wsb = static_cast<char *>(ws);
+    const int64_t mstride = (int64_t)N * ld;
+    const int G = (int)keys.size();
+    bool all_conv = true;
+    std::vector<splidar_solve_info> pinfo;
+    for (int g0 = 0; g0 < G; g0 += n_store) {
+        const int Mc = (G - g0) < n_store ? (G - g0) : n_store;
+        size_t maxv = 1;
+        for (int g = g0; g < g0 + Mc; ++g) maxv = members[(size_t)g].size() > maxv ? members[(size_t)g].size() : maxv;
+        const int passes = (int)((maxv + kMaxVectors - 1) / kMaxVectors);
+        const int Vp = (int)(maxv < (size_t)kMaxVectors ? maxv : (size_t)kMaxVectors);
+        const WsLayout L = ws_layout(N, Mc, Vp);
+        if ((st = check_ws(ws, ws_bytes, L))) return st;
+        std::vector<FluxDev> fl((size_t)Mc);
+        for (int g = 0; g < Mc; ++g) fl[(size_t)g] = to_dev(shape, keys[(size_t)(g0 + g)].first, keys[(size_t)(g0 + g)].second);
+        if ((st = vectors_and_build(fl.data(), Mc, N, dt, mode, P0_store, ld, mstride, wsb, L, s))) return st;
+        std::vector<double> lam_tot((size_t)Mc * 8);
+        SPL_CUDA(cudaMemcpyAsync(lam_tot.data(), vec_ptrs(wsb, L).scal, sizeof(double) * lam_tot.size(),
+                                 cudaMemcpyDeviceToHost, s));
+        for (int pass = 0; pass < passes; ++pass) {
+            std::vector<int> lp((size_t)Mc * Vp, -1), op((size_t)Mc * Vp, -1);
+            for (int g = 0; g < Mc; ++g) {
+                const std::vector<int> &mem = members[(size_t)(g0 + g)];
+                for (int v = 0; v < Vp; ++v) {
+                    const size_t k = (size_t)pass * kMaxVectors + v;
+                    if (k < mem.size()) {
+                        lp[(size_t)g * Vp + v] = l[(size_t)mem[k]];
+                        op[(size_t)g * Vp + v] = mem[k];
+                    }
+                }
+            }
+            splidar_plan p;
+            st = plan_create_l(&p, P0_store, Mc, mstride, N, ld, dt, lp.data(), Vp, tol, max_iter, pi, op.data(), ws,
+                               ws_bytes, s);
+            if (st) return st;
+            pinfo.assign((size_t)Mc * Vp, splidar_solve_info());
+            st = splidar_plan_execute(p, pinfo.data(), s);
+            splidar_plan_destroy(p);
+            if (st != SPLIDAR_OK && st != SPLIDAR_ENOCONV) return st;
+            for (int g = 0; g < Mc; ++g)
+                for (int v = 0; v < Vp; ++v) {
+                    const int item = op[(size_t)g * Vp + v];
+                    if (item < 0) continue;
+                    splidar_solve_info o = pinfo[(size_t)g * Vp + v];
+                    o.lambda_total = lam_tot[(size_t)g * 8];
+                    if (lam_tot[(size_t)g * 8 + 2] != 0.0) return SPLIDAR_EZEROROW;
+                    all_conv = all_conv && o.converged;
+                    if (info) info[item] = o;
+                }
+        }
+    }
+    return all_conv ? SPLIDAR_OK : SPLIDAR_ENOCONV;
+}
+
+}  // extern "C"

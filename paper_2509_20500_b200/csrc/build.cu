@@ -1,0 +1,134 @@
+// Step 2 (K4): the normalised base matrix P~0 and step 3 materialised (K5): the row permutation.
+//
+// P~0[r][j] = lambda_j exp(F_r - F_j - Lambda [r > j]) / Z_r            (mode EXP)
+//           = w_j (r > j ? e^{-Lambda} : 1) / D_r                        (mode FACTORED)
+// from E_base = exp.(-Lambda L - D), L_rj = 1{s_r > s_j}, D_rj = F(s_j) - F(s_r),
+// P = (1 lambda^T) . E, row-normalised (§3.4).
+//
+// Layout: a CTA owns a 512-column strip and a chunk of rows; each thread owns 16 bytes of columns
+// (2 fp64 or 4 fp32) for every row of the chunk, keeps its column vectors (w, w e^{-Lambda} or
+// lambda, F) in registers and streams 128-bit stores down the rows. Per row it reads one
+// broadcast scalar (1/D_r or 1/Z_r, F_r). The kernel is a pure HBM write stream: N^2 * b bytes.
+#include "common.cuh"
+
+namespace spl {
+namespace {
+
+constexpr int kRowsPerCta = 32;
+
+template <typename T> struct Vec16;
+template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
+template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kStripCols / Vec16<T>::n)
+k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t ld, int64_t mstride) {
+    constexpr int VEC = Vec16<T>::n;
+    using V = typename Vec16<T>::type;
+    const int m = blockIdx.z;
+    const double *__restrict__ w = base.w + m * vstride;
+    const double *__restrict__ lam = base.lam + m * vstride;
+    const double *__restrict__ F = base.F + m * vstride;
+    const double *__restrict__ invD = base.invD + m * vstride;
+    const double *__restrict__ invZ = base.invZ + m * vstride;
+    const double Lam = base.scal[m * 8 + 0];
+    const double eL = base.scal[m * 8 + 1];
+    T *__restrict__ out = P0 + m * mstride;
+
+    const int j0 = blockIdx.x * kStripCols + threadIdx.x * VEC;
+    if (j0 >= N) return;
+    const int r0 = blockIdx.y * kRowsPerCta;
+    const int r1 = min(N, r0 + kRowsPerCta);
+    const bool full = j0 + VEC <= N;
+
+    // column operands in registers
+    double a[VEC], b[VEC];   // FACTORED: a = w_j, b = w_j e^{-Lambda};  EXP: a = lambda_j, b = F_j
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+        const int j = j0 + e;
+        if (MODE == SPLIDAR_ENTRY_FACTORED) {
+            a[e] = j < N ? w[j] : 0.0;
+            b[e] = a[e] * eL;
+        } else {
+            a[e] = j < N ? lam[j] : 0.0;
+            b[e] = j < N ? F[j] : 0.0;
+        }
+    }
+
+#pragma unroll 4
+    for (int r = r0; r < r1; ++r) {
+        T val[VEC];
+        if (MODE == SPLIDAR_ENTRY_FACTORED) {
+            const double inv = __ldg(invD + r);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) val[e] = (T)((j0 + e < r ? b[e] : a[e]) * inv);
+        } else {
+            const double iz = __ldg(invZ + r);
+            const double Fr = __ldg(F + r);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const double arg = Fr - b[e] - (j0 + e < r ? Lam : 0.0);   // in [-Lambda, 0]
+                if constexpr (sizeof(T) == 8) {
+                    val[e] = a[e] * exp(arg) * iz;
+                } else {
+                    // fp32 storage: ex2.approx on the fp64-formed exponent (|rel err| ~ 1e-6)
+                    val[e] = (float)(a[e] * iz) * __expf((float)arg);
+                }
+            }
+        }
+        T *row = out + (int64_t)r * ld + j0;
+        if (full) {
+            V v;
+            if constexpr (VEC == 2) { v.x = val[0]; v.y = val[1]; }
+            else { v.x = val[0]; v.y = val[1]; v.z = val[2]; v.w = val[3]; }
+            *reinterpret_cast<V *>(row) = v;
+        } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+                if (j0 + e < N) row[e] = val[e];
+        }
+    }
+}
+
+// P[i][:] = P0[(i + l) mod N][:] (Thm 2; J_l), 16-byte vectors, one row per CTA row.
+__global__ void __launch_bounds__(256) k_apply_deadtime(const uint4 *__restrict__ P0, uint4 *__restrict__ P,
+                                                        int N, int64_t ld_vec, int row_vecs, int l) {
+    const int i = blockIdx.x;
+    const int src = (int)(((int64_t)i + l) % N);
+    const uint4 *s = P0 + (int64_t)src * ld_vec;
+    uint4 *d = P + (int64_t)i * ld_vec;
+#pragma unroll 4
+    for (int c = threadIdx.x; c < row_vecs; c += blockDim.x) d[c] = __ldcs(s + c);
+}
+
+}  // namespace
+
+cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
+                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s) {
+    dim3 grid((N + kStripCols - 1) / kStripCols, (N + kRowsPerCta - 1) / kRowsPerCta, M);
+    if (dtype == SPLIDAR_F64) {
+        dim3 block(kStripCols / 2);
+        if (mode == SPLIDAR_ENTRY_EXP)
+            k_build<double, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride);
+        else
+            k_build<double, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride);
+    } else {
+        dim3 block(kStripCols / 4);
+        if (mode == SPLIDAR_ENTRY_EXP)
+            k_build<float, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride);
+        else
+            k_build<float, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, int dtype, int l,
+                                  cudaStream_t s) {
+    const int esz = dtype == SPLIDAR_F64 ? 8 : 4;
+    const int64_t ld_vec = ld * esz / 16;
+    const int row_vecs = (int)(((int64_t)N * esz + 15) / 16);
+    k_apply_deadtime<<<N, 256, 0, s>>>((const uint4 *)P0, (uint4 *)P, N, ld_vec, row_vecs, l);
+    return cudaGetLastError();
+}
+
+}  // namespace spl

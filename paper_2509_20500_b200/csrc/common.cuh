@@ -1,0 +1,106 @@
+// Internal definitions shared by the libsplidar translation units (not part of the C ABI).
+// Nothing here is shared with oracle/: the product and the oracle are independent.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/splidar.h"
+
+namespace spl {
+
+constexpr int kMaxPulses = SPLIDAR_MAX_PULSES;
+constexpr int kMaxVectors = 16;      // dead times per matrix in one multi-vector GEMV pass
+constexpr int kStripCols = 512;      // columns per GEMV / build CTA (4 KB of an fp64 row)
+constexpr int kNumSMs = 148;
+constexpr int kCheckChunk = 2048;   // elements per CTA of the convergence-check kernel
+
+// theta without t_d, device copy. Eq. 1 with K pulses.
+struct FluxDev {
+    double t_r;
+    int n;
+    int k;
+    double B;
+    double tau[kMaxPulses];
+    double sigma[kMaxPulses];
+    double S[kMaxPulses];
+};
+
+// Per-matrix vectors of step 1 (all fp64, length N) + scalars.
+struct VecPtrs {
+    double *F;      // F(s_j), prefix sum of bin masses (Thm 1)
+    double *lam;    // lambda(s_j)
+    double *w;      // lambda_j e^{-F_j}
+    double *invD;   // 1 / D_r
+    double *invZ;   // e^{-F_r} / D_r  (= 1 / Z_r, row sum of the exp form)
+    double *scal;   // [0] Lambda, [1] e^{-Lambda}, [2] bad-row flag (0 / 1)
+};
+
+// Per (matrix, vector) power-iteration state.
+struct __align__(16) SolveState {
+    int l;          // row shift (Thm 2); < 0 marks an unused (padding) vector
+    int iters;
+    int done;
+    int converged;
+    int cur;        // which y buffer holds the current iterate
+    int pad0, pad1, pad2;
+    double s;       // ||y[cur]||_1: pi^k = y[cur] / s
+    double change;  // last L1 change
+};
+
+// Workspace layout (offsets in bytes from the 256-aligned base).
+struct WsLayout {
+    int N, M, V;    // V padded to a power of two
+    int strips, splits, rows_per_split, chunks;
+    size_t flux, vec, lsh, oidx, y, part, ssum, l1part, state, strip_cnt, mv_cnt, glob, total;
+};
+
+WsLayout ws_layout(int N, int M, int V);
+int pad_vectors(int V);
+
+// ---- kernels launch wrappers (host) -------------------------------------------------------
+cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs base, int64_t vstride,
+                                cudaStream_t s);
+cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
+                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s);
+cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, int dtype, int l,
+                                  cudaStream_t s);
+
+struct PowerArgs {
+    const void *P;
+    int64_t ld;
+    int64_t mstride;
+    int N, M, V, splits, strips, rows_per_split, chunks;
+    double *y;               // [M][V][2][N]
+    double *part;            // [M][V][splits][N]
+    double *ssum;            // [M][V][strips]
+    double *l1part;          // [M][V][chunks]  per-chunk L1 changes (check kernel)
+    SolveState *st;          // [M][V]
+    const int *lsh;          // [M][V] row shifts l (< 0: unused vector)
+    unsigned *strip_cnt;     // [M][strips]
+    unsigned *mv_cnt;        // [M][V] check-kernel CTA counters
+    unsigned *glob;          // [0] check-kernel CTA counter, [1] any-active flag
+    double tol;
+    int max_iter;
+    int use_handle;
+    cudaGraphConditionalHandle handle;
+};
+
+// Kernel node parameters for the three solver kernels (for graph construction).
+struct SolverKernels {
+    void *init_fn;
+    void *step_fn;
+    void *check_fn;
+    void *finish_fn;
+    dim3 init_grid, init_block;
+    dim3 step_grid, step_block;
+    dim3 check_grid, check_block;
+    dim3 finish_grid, finish_block;
+    size_t step_smem;
+};
+int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a);
+size_t finish_args_size();
+// pi output: out_idx[mv] >= 0 selects row out_idx[mv] of pi ([*, N]); < 0 skips the vector.
+void make_finish_args(void *dst, const PowerArgs &a, double *pi, const int *out_idx);
+
+}  // namespace spl

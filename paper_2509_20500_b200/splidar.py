@@ -1,0 +1,335 @@
+"""Thin Python binding of libsplidar.so (include/splidar.h): argument marshalling only.
+
+Every step of the path runs in the library's sm_100a kernels; PyTorch supplies device memory,
+streams and the current device. There is no CPU fallback: if the library is missing or fails to
+load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsplidar.so")
+
+OK, EINVAL, ENOCONV, EZEROROW, ENOSPACE, ECUDA = range(6)
+F64, F32 = 0, 1
+ENTRY_FACTORED, ENTRY_EXP = 0, 1
+MAX_PULSES = 16
+MAX_VECTORS = 16
+
+_DTYPES = {torch.float64: F64, torch.float32: F32}
+_MODES = {"factored": ENTRY_FACTORED, "exp": ENTRY_EXP}
+
+
+class SplidarError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib().splidar_strerror(status).decode()
+        if status == ECUDA:
+            msg += f" (cudaError {_lib().splidar_last_cuda_error()})"
+        super().__init__(f"{where}: {msg} [status {status}]")
+
+
+class _Flux(C.Structure):
+    _fields_ = [("t_r", C.c_double), ("n_bins", C.c_int32), ("n_pulses", C.c_int32),
+                ("tau", C.POINTER(C.c_double)), ("sigma", C.POINTER(C.c_double)),
+                ("signal", C.POINTER(C.c_double)), ("background", C.c_double)]
+
+
+class SolveInfo(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("shift_l", C.c_int32),
+                ("reserved", C.c_int32), ("l1_change", C.c_double), ("lambda_total", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {"iters": self.iters, "converged": bool(self.converged), "shift_l": self.shift_l,
+                "l1_change": self.l1_change, "lambda_total": self.lambda_total}
+
+
+_LIB = None
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libsplidar.so not built ({LIB_PATH}); run "
+                               "`python -m paper_2509_20500_b200.build` (no CPU fallback exists)")
+        lib = C.CDLL(LIB_PATH)
+        st, i32, i64, d, p, sz = C.c_int, C.c_int32, C.c_int64, C.c_double, C.c_void_p, C.c_size_t
+        fp = C.POINTER(_Flux)
+        pinfo = C.POINTER(SolveInfo)
+        sig = {
+            "splidar_shift": (st, [d, i32, d, C.POINTER(i32)]),
+            "splidar_workspace_bytes": (sz, [i32, i32, i32]),
+            "splidar_flux_vectors": (st, [fp, p, p, p, p, p, p, sz, p]),
+            "splidar_build_base": (st, [fp, st, st, p, i64, p, sz, p]),
+            "splidar_build_base_batched": (st, [fp, i32, st, st, p, i64, i64, p, sz, p]),
+            "splidar_apply_deadtime": (st, [p, p, i32, i64, st, d, d, p]),
+            "splidar_stationary": (st, [p, i32, i64, st, d, d, d, i32, p, p, sz, pinfo, p]),
+            "splidar_sweep": (st, [fp, i32, p, p, p, st, st, d, i32, p, p, i32, i64, p, sz, pinfo, p]),
+            "splidar_plan_create": (st, [C.POINTER(p), p, i32, i64, i32, i64, st, d, p, i32, d, i32, p, p,
+                                         sz, p]),
+            "splidar_plan_execute": (st, [p, pinfo, p]),
+            "splidar_plan_launch": (st, [p, p]),
+            "splidar_plan_info": (st, [p, pinfo, p]),
+            "splidar_plan_destroy": (None, [p]),
+            "splidar_strerror": (C.c_char_p, [st]),
+            "splidar_last_cuda_error": (C.c_int, []),
+            "splidar_build_info": (C.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype, fn.argtypes = res, args
+        _LIB = lib
+    return _LIB
+
+
+def lib_path() -> str:
+    _lib()
+    return LIB_PATH
+
+
+def build_info() -> str:
+    return _lib().splidar_build_info().decode()
+
+
+def _check(status: int, where: str, allow=()):
+    if status != OK and status not in allow:
+        raise SplidarError(status, where)
+    return status
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class _FluxArg:
+    """Marshals any object with t_r, n_bins, tau, sigma, signal, background into splidar_flux."""
+
+    def __init__(self, flux):
+        self.tau = np.ascontiguousarray(flux.tau, dtype=np.float64).reshape(-1)
+        self.sigma = np.ascontiguousarray(flux.sigma, dtype=np.float64).reshape(-1)
+        self.signal = np.ascontiguousarray(flux.signal, dtype=np.float64).reshape(-1)
+        dp = C.POINTER(C.c_double)
+        self.s = _Flux(float(flux.t_r), int(flux.n_bins), int(self.tau.size),
+                       self.tau.ctypes.data_as(dp), self.sigma.ctypes.data_as(dp),
+                       self.signal.ctypes.data_as(dp), float(flux.background))
+
+
+def shift(t_r: float, n_bins: int, t_d: float) -> int:
+    """l = ceil((t_d mod t_r) N / t_r) mod N (Thm 2)."""
+    out = C.c_int32(0)
+    _check(_lib().splidar_shift(float(t_r), int(n_bins), float(t_d), C.byref(out)), "splidar_shift")
+    return out.value
+
+
+def workspace_bytes(n_bins: int, n_matrices: int = 1, n_vectors: int = 1) -> int:
+    return int(_lib().splidar_workspace_bytes(int(n_bins), int(n_matrices), int(n_vectors)))
+
+
+def workspace(n_bins: int, n_matrices: int = 1, n_vectors: int = 1, device=None) -> torch.Tensor:
+    n = workspace_bytes(n_bins, n_matrices, n_vectors)
+    if n == 0:
+        raise SplidarError(EINVAL, "splidar_workspace_bytes")
+    t = torch.empty(n + 256, dtype=torch.uint8, device=device or "cuda")
+    off = (-t.data_ptr()) % 256
+    return t[off:off + n]
+
+
+def leading_dim(n_bins: int, dtype=torch.float64) -> int:
+    """Smallest ld >= N with ld * sizeof(dtype) a multiple of 16 bytes."""
+    q = 16 // torch.tensor([], dtype=dtype).element_size()
+    return (n_bins + q - 1) // q * q
+
+
+def empty_matrix(n_bins: int, dtype=torch.float64, n_matrices: int | None = None, device=None) -> torch.Tensor:
+    """Device matrix storage [N, ld] (or [M, N, ld]) returned as the [.., N, N] view."""
+    ld = leading_dim(n_bins, dtype)
+    shape = (n_bins, ld) if n_matrices is None else (n_matrices, n_bins, ld)
+    return torch.empty(shape, dtype=dtype, device=device or "cuda")[..., :n_bins]
+
+
+def _matrix_args(P: torch.Tensor):
+    if not P.is_cuda or P.dtype not in _DTYPES or P.stride(-1) != 1:
+        raise SplidarError(EINVAL, "matrix argument (CUDA fp64/fp32 row-major tensor expected)")
+    return P.data_ptr(), P.shape[-1], P.stride(-2), _DTYPES[P.dtype]
+
+
+def flux_vectors(flux, ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Step 1 on the device: F(s_j), lambda(s_j), w_j, 1/D_j and Lambda (fp64 device tensors)."""
+    N = int(flux.n_bins)
+    ws = ws if ws is not None else workspace(N)
+    F, lam, w, invd = (torch.empty(N, dtype=torch.float64, device=ws.device) for _ in range(4))
+    L = torch.empty(1, dtype=torch.float64, device=ws.device)
+    fa = _FluxArg(flux)
+    _check(_lib().splidar_flux_vectors(C.byref(fa.s), F.data_ptr(), lam.data_ptr(), w.data_ptr(), invd.data_ptr(),
+                                       L.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)),
+           "splidar_flux_vectors")
+    return {"F": F, "lam": lam, "w": w, "inv_d": invd, "Lambda": L}
+
+
+def build_base(flux, dtype=torch.float64, mode: str = "factored", out: torch.Tensor | None = None,
+               ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Step 2: P~0 (N x N view of [N, ld] storage) on the current CUDA device (async)."""
+    N = int(flux.n_bins)
+    P = out if out is not None else empty_matrix(N, dtype)
+    ptr, n, ld, dt = _matrix_args(P)
+    ws = ws if ws is not None else workspace(N)
+    fa = _FluxArg(flux)
+    _check(_lib().splidar_build_base(C.byref(fa.s), dt, _MODES[mode], ptr, ld, ws.data_ptr(), ws.numel(),
+                                     _stream(stream)), "splidar_build_base")
+    return P
+
+
+def build_base_batched(fluxes, dtype=torch.float64, mode: str = "factored", out: torch.Tensor | None = None,
+                       ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Step 2 for M fluxes sharing N: P~0 [M, N, N] view of [M, N, ld] storage (async)."""
+    M = len(fluxes)
+    N = int(fluxes[0].n_bins)
+    P = out if out is not None else empty_matrix(N, dtype, n_matrices=M)
+    ptr, n, ld, dt = _matrix_args(P)
+    ws = ws if ws is not None else workspace(N, M)
+    fas = [_FluxArg(f) for f in fluxes]
+    arr = (_Flux * M)(*[fa.s for fa in fas])
+    _check(_lib().splidar_build_base_batched(arr, M, dt, _MODES[mode], ptr, ld, P.stride(0), ws.data_ptr(),
+                                             ws.numel(), _stream(stream)), "splidar_build_base_batched")
+    return P
+
+
+def apply_deadtime(P0: torch.Tensor, t_r: float, t_d: float, out: torch.Tensor | None = None,
+                   stream=None) -> torch.Tensor:
+    """Step 3 materialised: P[i] = P0[(i + l) mod N] (async)."""
+    ptr, n, ld, dt = _matrix_args(P0)
+    P = out if out is not None else empty_matrix(n, P0.dtype)
+    optr, on, old, odt = _matrix_args(P)
+    if old != ld or odt != dt or on != n:
+        raise SplidarError(EINVAL, "apply_deadtime: out must match P0's N, ld and dtype")
+    _check(_lib().splidar_apply_deadtime(ptr, optr, n, ld, dt, float(t_r), float(t_d), _stream(stream)),
+           "splidar_apply_deadtime")
+    return P
+
+
+def stationary(P0: torch.Tensor, t_r: float, t_d: float, tol: float = 1e-12, max_iter: int = 10 ** 6,
+               out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None,
+               check: bool = True):
+    """Step 4: pi with pi (J_l P~0) = pi by on-device power iteration. Returns (pi, info dict)."""
+    ptr, n, ld, dt = _matrix_args(P0)
+    pi = out if out is not None else torch.empty(n, dtype=torch.float64, device=P0.device)
+    ws = ws if ws is not None else workspace(n)
+    info = SolveInfo()
+    st = _lib().splidar_stationary(ptr, n, ld, dt, float(t_r), float(t_d), float(tol), int(max_iter),
+                                   pi.data_ptr(), ws.data_ptr(), ws.numel(), C.byref(info), _stream(stream))
+    _check(st, "splidar_stationary", allow=() if check else (ENOCONV,))
+    return pi, info.as_dict()
+
+
+def sweep(shape, S, B, t_d, dtype=torch.float64, mode: str = "factored", tol: float = 1e-12,
+          max_iter: int = 10 ** 6, n_store: int | None = None, P0_store: torch.Tensor | None = None,
+          ws: torch.Tensor | None = None, stream=None, check: bool = True):
+    """Steps 1-4 for (S[m], B[m], t_d[m]) items; shape.signal are relative pulse weights.
+    Returns (pi [M, N] fp64 device tensor, list of info dicts)."""
+    S = np.ascontiguousarray(S, dtype=np.float64).reshape(-1)
+    B = np.ascontiguousarray(B, dtype=np.float64).reshape(-1)
+    T = np.ascontiguousarray(t_d, dtype=np.float64).reshape(-1)
+    M = S.size
+    if B.size != M or T.size != M:
+        raise SplidarError(EINVAL, "sweep: S, B, t_d must have equal length")
+    N = int(shape.n_bins)
+    n_unique = len({(float(s), float(b)) for s, b in zip(S, B)})
+    if P0_store is None:
+        n_store = n_store or n_unique
+        P0_store = empty_matrix(N, dtype, n_matrices=n_store)
+    else:
+        n_store = P0_store.shape[0] if P0_store.dim() == 3 else 1
+    ptr, n, ld, dt = _matrix_args(P0_store)
+    if ws is None:
+        max_items = 1
+        counts = {}
+        for s, b in zip(S, B):
+            counts[(float(s), float(b))] = counts.get((float(s), float(b)), 0) + 1
+        max_items = min(MAX_VECTORS, max(counts.values()))
+        ws = workspace(N, min(n_store, n_unique), max_items, device=P0_store.device)
+    pi = torch.empty((M, N), dtype=torch.float64, device=P0_store.device)
+    infos = (SolveInfo * M)()
+    fa = _FluxArg(shape)
+    st = _lib().splidar_sweep(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data, dt, _MODES[mode],
+                              float(tol), int(max_iter), pi.data_ptr(), ptr, int(n_store), ld, ws.data_ptr(),
+                              ws.numel(), infos, _stream(stream))
+    _check(st, "splidar_sweep", allow=() if check else (ENOCONV,))
+    return pi, [i.as_dict() for i in infos]
+
+
+class Plan:
+    """An instantiated CUDA-graph power-iteration solver for M matrices x V dead times.
+
+    P0: [N, N] or [M, N, N] view (row-major, ld = stride); t_d: array [M, V]. pi: [M, V, N] fp64.
+    execute() reruns the solve from pi^0 and returns the infos; launch() only enqueues."""
+
+    def __init__(self, P0: torch.Tensor, t_r: float, t_d, tol: float = 1e-12, max_iter: int = 10 ** 6,
+                 ws: torch.Tensor | None = None, stream=None):
+        ptr, n, ld, dt = _matrix_args(P0)
+        M = P0.shape[0] if P0.dim() == 3 else 1
+        mstride = P0.stride(0) if P0.dim() == 3 else n * ld
+        T = np.ascontiguousarray(t_d, dtype=np.float64).reshape(M, -1)
+        V = T.shape[1]
+        self.M, self.V, self.N = M, V, n
+        self.P0 = P0
+        self.pi = torch.empty((M, V, n), dtype=torch.float64, device=P0.device)
+        self.ws = ws if ws is not None else workspace(n, M, V, device=P0.device)
+        self._T = T
+        self._h = C.c_void_p(None)
+        _check(_lib().splidar_plan_create(C.byref(self._h), ptr, M, mstride, n, ld, dt, float(t_r), T.ctypes.data,
+                                          V, float(tol), int(max_iter), self.pi.data_ptr(), self.ws.data_ptr(),
+                                          self.ws.numel(), _stream(stream)), "splidar_plan_create")
+
+    def launch(self, stream=None):
+        _check(_lib().splidar_plan_launch(self._h, _stream(stream)), "splidar_plan_launch")
+
+    def info(self, stream=None, check: bool = True) -> list:
+        infos = (SolveInfo * (self.M * self.V))()
+        st = _lib().splidar_plan_info(self._h, infos, _stream(stream))
+        _check(st, "splidar_plan_info", allow=() if check else (ENOCONV,))
+        return [i.as_dict() for i in infos]
+
+    def execute(self, stream=None, check: bool = True) -> list:
+        self.launch(stream)
+        return self.info(stream, check)
+
+    def close(self):
+        if self._h:
+            _lib().splidar_plan_destroy(self._h)
+            self._h = C.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class HostResult:
+    pi: np.ndarray
+    info: dict
+
+
+def solve_host(flux, t_d: float, dtype=torch.float64, mode: str = "factored", tol: float = 1e-12,
+               max_iter: int = 10 ** 6, P0: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+               pi_host: torch.Tensor | None = None) -> HostResult:
+    """End-to-end public call with host inputs and host output: theta (host) -> device build of P~0
+    -> on-device power iteration -> pi copied into (pinned) host memory."""
+    N = int(flux.n_bins)
+    P0 = build_base(flux, dtype, mode, out=P0, ws=ws)
+    pi, info = stationary(P0, flux.t_r, t_d, tol, max_iter, ws=ws)
+    if pi_host is None:
+        pi_host = torch.empty(N, dtype=torch.float64, pin_memory=True)
+    pi_host.copy_(pi, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return HostResult(pi_host.numpy(), info)

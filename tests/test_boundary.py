@@ -1,0 +1,204 @@
+"""The C-ABI boundary on the CPU: the library loads without a GPU, exports every symbol that
+include/splidar.h declares, and its host-side logic (shift rule, workspace sizing, argument
+validation, status strings) behaves as documented. No compute is launched here."""
+import ctypes as C
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import config, parity_cases
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "splidar.h")
+
+
+@pytest.fixture(scope="module")
+def spl():
+    from paper_2509_20500_b200 import build
+    build.build()
+    import paper_2509_20500_b200.splidar as s
+    s._lib()
+    return s
+
+
+def _declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(splidar_[a-z_]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_header_declares_the_path():
+    names = _declared_functions()
+    for must in ("splidar_build_base", "splidar_apply_deadtime", "splidar_stationary", "splidar_sweep",
+                 "splidar_flux_vectors", "splidar_shift", "splidar_workspace_bytes"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(spl):
+    lib = C.CDLL(spl.LIB_PATH)
+    missing = [n for n in _declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_build_info(spl):
+    assert "sm_100a" in spl.build_info()
+
+
+def test_status_strings(spl):
+    for st in range(6):
+        assert spl._lib().splidar_strerror(st).decode()
+    assert spl._lib().splidar_strerror(99).decode() == "unknown status"
+
+
+# ------------------------------------------------------------------ shift rule (Thm 2)
+def test_shift_rule_config_values(spl):
+    """l = ceil(x_d / Delta) mod N at the BASELINE configs."""
+    want = {1: 192, 2: 512, 3: 3277, 4: 3277, 5: 4916}
+    for k, l in want.items():
+        w = config(k)
+        f = w.items[0].flux
+        assert spl.shift(f.t_r, f.n_bins, w.items[0].t_d) == l
+    w = config(5)
+    f = w.items[0].flux
+    got = [spl.shift(f.t_r, f.n_bins, it.t_d) for it in w.sweep]
+    assert got == [1639, 6991, 12343, 17695, 23047, 28399, 984, 6336, 11688, 17040, 22392, 27744,
+                   328, 5680, 11032, 16384]
+
+
+def test_shift_rule_matches_oracle_and_edges(spl):
+    rng = np.random.default_rng(4)
+    for _ in range(500):
+        n = int(rng.integers(2, 70000))
+        t_r = float(rng.uniform(1, 300))
+        td = float(rng.uniform(0, 4 * t_r))
+        assert spl.shift(t_r, n, td) == oracle.shift_l(_F(t_r, n), td)
+    assert spl.shift(100.0, 256, 0.0) == 0
+    assert spl.shift(100.0, 256, 100.0) == 0           # whole period
+    assert spl.shift(100.0, 256, 300.0) == 0
+    assert spl.shift(100.0, 4, 99.0) == 0               # l = N wraps to 0
+    assert spl.shift(100.0, 4, 25.0) == 1               # exact integer: ceil(1) = 1
+    assert spl.shift(100.0, 4, 25.0001) == 2
+
+
+class _F:
+    def __init__(self, t_r, n):
+        self.t_r, self.n_bins = t_r, n
+
+
+@pytest.mark.parametrize("args", [(0.0, 16, 1.0), (-1.0, 16, 1.0), (100.0, 1, 1.0), (100.0, 16, -1.0),
+                                  (math.inf, 16, 1.0), (100.0, 16, math.nan)])
+def test_shift_rejects(spl, args):
+    out = C.c_int32(0)
+    assert spl._lib().splidar_shift(*args, C.byref(out)) == spl.EINVAL
+
+
+# ------------------------------------------------------------------ workspace sizing
+def test_workspace_bytes(spl):
+    assert spl.workspace_bytes(1, 1, 1) == 0
+    assert spl.workspace_bytes(256, 0, 1) == 0
+    assert spl.workspace_bytes(256, 1, 17) == 0
+    a = spl.workspace_bytes(32768, 1, 1)
+    b = spl.workspace_bytes(32768, 1, 16)
+    assert 0 < a < b
+    assert b < 1 << 30                     # < 1 GiB beside an 8.6 GB matrix
+    assert spl.workspace_bytes(4096, 64, 1) > spl.workspace_bytes(4096, 1, 1)
+    for n in (2, 3, 255, 1537, 32768):
+        assert spl.workspace_bytes(n, 1, 1) % 256 == 0
+
+
+# ------------------------------------------------------------------ argument validation (no launch)
+def _flux_struct(spl, **kw):
+    f = config(1).items[0].flux
+    d = dict(t_r=f.t_r, n_bins=f.n_bins, tau=f.tau, sigma=f.sigma, signal=f.signal, background=f.background)
+    d.update(kw)
+
+    class Obj:
+        pass
+    o = Obj()
+    for k, v in d.items():
+        setattr(o, k, v)
+    return spl._FluxArg(o)
+
+
+FAKE = 1 << 20          # 256-aligned fake device address: validation must fail before any access
+
+
+@pytest.mark.parametrize("kw", [dict(t_r=0.0), dict(n_bins=1), dict(n_bins=(1 << 20) + 1), dict(sigma=(0.0,)),
+                                dict(signal=(-1.0,)), dict(tau=(100.0,)), dict(tau=(-0.1,)),
+                                dict(background=0.0), dict(background=math.nan), dict(signal=(700.0,)),
+                                dict(tau=tuple([1.0] * 17), sigma=tuple([1.0] * 17), signal=tuple([0.1] * 17))])
+def test_build_base_rejects_bad_flux(spl, kw):
+    fa = _flux_struct(spl, **kw)
+    st = spl._lib().splidar_build_base(C.byref(fa.s), spl.F64, 0, FAKE, 256, FAKE, 1 << 30, None)
+    assert st == spl.EINVAL
+
+
+def test_build_base_rejects_layout(spl):
+    fa = _flux_struct(spl)
+    lib = spl._lib()
+    assert lib.splidar_build_base(C.byref(fa.s), spl.F64, 0, FAKE, 255, FAKE, 1 << 30, None) == spl.ENOSPACE
+    assert lib.splidar_build_base(C.byref(fa.s), spl.F64, 0, FAKE + 8, 256, FAKE, 1 << 30, None) == spl.ENOSPACE
+    assert lib.splidar_build_base(C.byref(fa.s), spl.F32, 0, FAKE, 258, FAKE, 1 << 30, None) == spl.ENOSPACE
+    assert lib.splidar_build_base(C.byref(fa.s), spl.F64, 0, FAKE, 256, FAKE, 16, None) == spl.ENOSPACE
+    assert lib.splidar_build_base(C.byref(fa.s), spl.F64, 0, FAKE, 256, FAKE + 64, 1 << 30, None) == spl.ENOSPACE
+    assert lib.splidar_build_base(C.byref(fa.s), spl.F64, 7, FAKE, 256, FAKE, 1 << 30, None) == spl.EINVAL
+    assert lib.splidar_build_base(C.byref(fa.s), 3, 0, FAKE, 256, FAKE, 1 << 30, None) == spl.EINVAL
+    assert lib.splidar_build_base(C.byref(fa.s), spl.F64, 0, None, 256, FAKE, 1 << 30, None) == spl.EINVAL
+
+
+def test_apply_deadtime_rejects(spl):
+    lib = spl._lib()
+    assert lib.splidar_apply_deadtime(FAKE, FAKE, 256, 256, spl.F64, 100.0, 75.0, None) == spl.EINVAL
+    assert lib.splidar_apply_deadtime(FAKE, FAKE * 2, 256, 256, spl.F64, 100.0, -1.0, None) == spl.EINVAL
+    assert lib.splidar_apply_deadtime(FAKE, FAKE * 2, 256, 250, spl.F64, 100.0, 1.0, None) == spl.ENOSPACE
+
+
+def test_stationary_rejects(spl):
+    lib = spl._lib()
+    info = spl.SolveInfo()
+    ws = spl.workspace_bytes(256, 1, 1)
+    args = dict(P0=FAKE, n=256, ld=256, dt=spl.F64, t_r=100.0, t_d=75.0, tol=1e-12, it=100, pi=FAKE, ws=FAKE,
+                wsb=ws)
+
+    def call(**kw):
+        a = dict(args)
+        a.update(kw)
+        return lib.splidar_stationary(a["P0"], a["n"], a["ld"], a["dt"], a["t_r"], a["t_d"], a["tol"], a["it"],
+                                      a["pi"], a["ws"], a["wsb"], C.byref(info), None)
+    assert call(tol=0.0) == spl.EINVAL
+    assert call(tol=math.nan) == spl.EINVAL
+    assert call(it=0) == spl.EINVAL
+    assert call(pi=None) == spl.EINVAL
+    assert call(t_d=-5.0) == spl.EINVAL
+    assert call(wsb=ws - 1) == spl.ENOSPACE
+    assert call(ld=100) == spl.ENOSPACE
+
+
+def test_sweep_rejects(spl):
+    lib = spl._lib()
+    fa = _flux_struct(spl)
+    S = np.array([0.5, 1.0])
+    B = np.array([0.1, 0.0])          # B = 0 is invalid (irreducibility)
+    T = np.array([75.0, 75.0])
+    st = lib.splidar_sweep(C.byref(fa.s), 2, S.ctypes.data, B.ctypes.data, T.ctypes.data, spl.F64, 0, 1e-12, 100,
+                           FAKE, FAKE, 2, 256, FAKE, 1 << 30, None, None)
+    assert st == spl.EINVAL
+    B = np.array([0.1, 0.2])
+    st = lib.splidar_sweep(C.byref(fa.s), 0, S.ctypes.data, B.ctypes.data, T.ctypes.data, spl.F64, 0, 1e-12, 100,
+                           FAKE, FAKE, 2, 256, FAKE, 1 << 30, None, None)
+    assert st == spl.EINVAL
+
+
+def test_parity_cases_are_well_formed():
+    """The seeded parity workload spans tiny N, ragged tails (N not a multiple of the 512-column
+    strip), several strips, K = 1 and 2 pulses, zero / whole-period / multi-period dead times."""
+    cases = parity_cases()
+    ns = {c.flux.n_bins for c in cases}
+    assert {2, 3, 1000, 1537, 2048} <= ns
+    assert any(c.t_d == 0.0 for c in cases) and any(c.t_d > 2 * c.flux.t_r for c in cases)
+    assert any(c.flux.n_pulses == 2 for c in cases)

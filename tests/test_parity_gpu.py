@@ -1,0 +1,314 @@
+"""GPU path vs the CPU oracle, element by element, through the C ABI (pytest -m gpu).
+
+Tolerances (BASELINE.json north_star): fp64 entries <= 1e-12 max-abs, row sums within 1e-12 of 1,
+pi <= 1e-10 in L1; fp32 storage <= 1e-5 (entries and pi). The oracle builds P~ entry by entry from
+Eq. 4 with the dead time inside the integral bounds; the GPU builds the base matrix from
+the paper's reparameterised form (§3.4) and applies the dead time as the row permutation of
+Theorem 2, so every comparison below also checks Theorem 2 (exact after normalisation, R1).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workloads import Flux, config, parity_cases, random_flux
+
+from ._structured import oracle_vectors, sampled_rows, structured_pi
+
+pytestmark = pytest.mark.gpu
+
+TOL_E64, TOL_ROW, TOL_PI64 = 1e-12, 1e-12, 1e-10
+TOL_E32, TOL_PI32 = 1e-5, 1e-5
+
+
+@pytest.fixture(scope="module")
+def spl():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2509_20500_b200 import build
+    build.build()
+    import paper_2509_20500_b200 as s
+    return s
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _oracle_pi(P):
+    n = P.shape[0]
+    if n <= 1100:
+        return oracle.stationary_dense(P)
+    pi, _, _, ok = oracle.stationary_power(P, 1e-15)
+    assert ok
+    return pi
+
+
+CASES = parity_cases()
+IDS = [f"N{c.flux.n_bins}-K{c.flux.n_pulses}-td{c.t_d:.2f}" for c in CASES]
+
+
+# ------------------------------------------------------------- a1-a2: flux vectors and the scan
+@pytest.mark.parametrize("case", CASES + [config(k).items[0] for k in range(1, 6)],
+                         ids=IDS + [f"config{k}" for k in range(1, 6)])
+def test_flux_vectors(spl, case):
+    f = case.flux
+    v = spl.flux_vectors(f)
+    lam, F, Lam = oracle_vectors(f)
+    tolF = 1e-13 * max(1.0, Lam)
+    assert abs(_np(v["Lambda"])[0] - Lam) <= tolF
+    assert np.max(np.abs(_np(v["F"]) - F)) <= tolF
+    assert np.max(np.abs(_np(v["lam"]) - lam) / lam) <= 1e-13
+
+
+# ------------------------------------------------------------- a3-a4: base matrix
+@pytest.mark.parametrize("mode", ["factored", "exp"])
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_build_base_f64(spl, case, mode):
+    f = case.flux
+    P0 = spl.build_base(f, torch.float64, mode)
+    got = _np(P0)
+    want = oracle.build_eq4(f, 0.0)
+    assert np.max(np.abs(got - want)) <= TOL_E64
+    assert np.max(np.abs(got.sum(axis=1) - 1.0)) <= TOL_ROW
+
+
+@pytest.mark.parametrize("mode", ["factored", "exp"])
+@pytest.mark.parametrize("case", CASES[::3], ids=IDS[::3])
+def test_build_base_f32(spl, case, mode):
+    f = case.flux
+    got = _np(spl.build_base(f, torch.float32, mode)).astype(np.float64)
+    want = oracle.build_eq4(f, 0.0)
+    assert np.max(np.abs(got - want)) <= TOL_E32
+    assert np.max(np.abs(got.sum(axis=1) - 1.0)) <= 1e-4
+
+
+# ------------------------------------------------------------- a5: dead time as row permutation
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_apply_deadtime_equals_eq4(spl, case):
+    """J_l P~0 on the GPU == the oracle's direct Eq. 4 with t_d inside the bounds."""
+    f = case.flux
+    P0 = spl.build_base(f, torch.float64)
+    P = spl.apply_deadtime(P0, f.t_r, case.t_d)
+    assert np.max(np.abs(_np(P) - oracle.build_eq4(f, case.t_d))) <= TOL_E64
+
+
+def test_apply_deadtime_f32_exact_copy(spl):
+    f = CASES[10].flux
+    P0 = spl.build_base(f, torch.float32)
+    P = spl.apply_deadtime(P0, f.t_r, 37.0)
+    l = spl.shift(f.t_r, f.n_bins, 37.0)
+    assert torch.equal(P, torch.roll(P0, -l, dims=0))
+
+
+# ------------------------------------------------------------- a6: power iteration
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_stationary_f64(spl, case):
+    f = case.flux
+    P0 = spl.build_base(f, torch.float64)
+    pi, info = spl.stationary(P0, f.t_r, case.t_d, tol=1e-12)
+    assert info["converged"] and info["l1_change"] < 1e-12
+    assert info["shift_l"] == oracle.shift_l(f, case.t_d)
+    want = _oracle_pi(oracle.build_eq4(f, case.t_d))
+    got = _np(pi)
+    assert np.sum(np.abs(got - want)) <= TOL_PI64
+    assert abs(got.sum() - 1.0) <= 1e-13 and np.all(got > 0)
+
+
+@pytest.mark.parametrize("case", CASES[1::3], ids=IDS[1::3])
+def test_stationary_f32(spl, case):
+    f = case.flux
+    P0 = spl.build_base(f, torch.float32)
+    pi, info = spl.stationary(P0, f.t_r, case.t_d, tol=1e-12, max_iter=100000, check=False)
+    want = _oracle_pi(oracle.build_eq4(f, case.t_d))
+    assert np.sum(np.abs(_np(pi) - want)) <= TOL_PI32
+
+
+def test_stationary_noconv_reported(spl):
+    f = config(1).items[0].flux
+    P0 = spl.build_base(f)
+    with pytest.raises(spl.SplidarError) as e:
+        spl.stationary(P0, f.t_r, 75.0, tol=1e-12, max_iter=2)
+    assert e.value.status == spl.ENOCONV
+    pi, info = spl.stationary(P0, f.t_r, 75.0, tol=1e-12, max_iter=2, check=False)
+    assert info["iters"] == 2 and not info["converged"] and info["l1_change"] > 1e-12
+    # pi holds the second iterate: compare with two oracle power steps
+    P = oracle.build_eq4(f, 75.0)
+    x = np.full(f.n_bins, 1.0 / f.n_bins)
+    for _ in range(2):
+        x = x @ P
+        x /= x.sum()
+    assert np.sum(np.abs(_np(pi) - x)) <= 1e-13
+
+
+def test_deterministic(spl):
+    f = config(2).items[5].flux
+    P0a = spl.build_base(f)
+    P0b = spl.build_base(f)
+    assert torch.equal(P0a, P0b)
+    pa, _ = spl.stationary(P0a, f.t_r, 50.0)
+    pb, _ = spl.stationary(P0b, f.t_r, 50.0)
+    assert torch.equal(pa, pb)
+
+
+def test_plan_reuse_and_multivector(spl):
+    """One P~0, several dead times in one multi-vector plan, executed twice: identical results,
+    each vector equal to its single-vector solve and to the oracle."""
+    f = random_flux(np.random.default_rng(3), 777, 2)
+    tds = [0.0, 13.0, 55.5, 130.0, 299.0]
+    P0 = spl.build_base(f)
+    plan = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-12)
+    i1 = plan.execute()
+    p1 = plan.pi.clone()
+    i2 = plan.execute()
+    assert torch.equal(p1, plan.pi) and i1 == i2
+    for v, td in enumerate(tds):
+        single, info = spl.stationary(P0, f.t_r, td)
+        assert info["iters"] == i1[v]["iters"]
+        assert np.sum(np.abs(_np(plan.pi[0, v]) - _np(single))) <= 1e-14
+        want = oracle.stationary_dense(oracle.build_eq4(f, td))
+        assert np.sum(np.abs(_np(plan.pi[0, v]) - want)) <= TOL_PI64
+    plan.close()
+
+
+# ------------------------------------------------------------- BASELINE configs 1-3 (full)
+def test_config1_full(spl):
+    it = config(1).items[0]
+    f = it.flux
+    P0 = spl.build_base(f)
+    P = spl.apply_deadtime(P0, f.t_r, it.t_d)
+    want = oracle.build_eq4(f, it.t_d)
+    assert np.max(np.abs(_np(P) - want)) <= TOL_E64
+    pi, info = spl.stationary(P0, f.t_r, it.t_d)
+    assert np.sum(np.abs(_np(pi) - oracle.stationary_dense(want))) <= TOL_PI64
+    assert info["shift_l"] == 192
+
+
+def test_config2_sweep(spl):
+    w = config(2)
+    # per-item pulse centres differ, so each item is its own shape: solve them through the batched
+    # builder + one plan over 6 matrices
+    fl = [it.flux for it in w.items]
+    P0 = spl.build_base_batched(fl)
+    plan = spl.Plan(P0, 100.0, np.array([[it.t_d] for it in w.items]), tol=1e-12)
+    infos = plan.execute()
+    for m, it in enumerate(w.items):
+        want_P = oracle.build_eq4(it.flux, 0.0)
+        assert np.max(np.abs(_np(P0[m]) - want_P)) <= TOL_E64
+        want = oracle.stationary_dense(oracle.build_eq4(it.flux, it.t_d))
+        assert np.sum(np.abs(_np(plan.pi[m, 0]) - want)) <= TOL_PI64
+        assert infos[m]["converged"]
+    plan.close()
+
+
+def test_config3_sweep(spl):
+    """64 (S, B) items at N = 4096 through splidar_sweep: all 64 vs the structured cross-check,
+    4 of them element-wise against the oracle's Eq. 4 matrix and power iteration."""
+    w = config(3)
+    base = w.items[0].flux
+    shape = Flux(base.t_r, base.n_bins, base.tau, base.sigma, (1.0,), 1.0)
+    S = np.array([it.flux.signal[0] for it in w.items])
+    B = np.array([it.flux.background for it in w.items])
+    T = np.array([it.t_d for it in w.items])
+    pi, infos = spl.sweep(shape, S, B, T, n_store=64)
+    got = _np(pi)
+    for m, it in enumerate(w.items):
+        assert infos[m]["converged"]
+        ref, _ = structured_pi(it.flux, it.t_d)
+        assert np.sum(np.abs(got[m] - ref)) <= TOL_PI64, m
+    for m in (0, 17, 42, 63):
+        it = w.items[m]
+        P = oracle.build_eq4(it.flux, it.t_d)
+        want, _, _, ok = oracle.stationary_power(P, 1e-15)
+        assert np.sum(np.abs(got[m] - want)) <= TOL_PI64
+
+
+# ------------------------------------------------------------- configs 4-5 at full size
+def _full_size_check(spl, flux, t_d, dtype, mode, tol_e, tol_pi, rows=None):
+    N = flux.n_bins
+    P0 = spl.build_base(flux, dtype, mode)
+    torch.cuda.synchronize()
+    l = oracle.shift_l(flux, t_d)
+    rng = np.random.default_rng(N)
+    rows = rows if rows is not None else sorted({0, 1, N - 1, l, (l + 1) % N, (N - l) % N, *rng.integers(0, N, 10)})
+    # sampled rows of P~ = J_l P~0 against the oracle's Eq. 4 rows
+    want = sampled_rows(flux, t_d, rows)
+    got = np.stack([_np(P0[(r + l) % N]).astype(np.float64) for r in rows])
+    assert np.max(np.abs(got - want)) <= tol_e
+    # all row sums of P~0 on the device
+    rs = _np(P0.sum(dim=1, dtype=torch.float64))
+    assert np.max(np.abs(rs - 1.0)) <= (TOL_ROW if dtype == torch.float64 else 1e-4)
+    pi, info = spl.stationary(P0, flux.t_r, t_d, tol=1e-12, check=dtype == torch.float64)
+    got_pi = _np(pi)
+    ref, _ = structured_pi(flux, t_d)
+    assert np.sum(np.abs(got_pi - ref)) <= tol_pi
+    del P0
+    torch.cuda.empty_cache()
+    return got_pi, info
+
+
+def test_config4_full(spl):
+    it = config(4).items[0]
+    pi, info = _full_size_check(spl, it.flux, it.t_d, torch.float64, "factored", TOL_E64, TOL_PI64)
+    assert info["converged"] and info["shift_l"] == 3277
+    # residual against the oracle's own rows, streamed (pi P~ = pi)
+    y = oracle.left_matvec_streamed(it.flux, it.t_d, pi)
+    assert np.sum(np.abs(y - pi)) <= 1e-11
+
+
+def test_config4_exp_mode(spl):
+    it = config(4).items[0]
+    _full_size_check(spl, it.flux, it.t_d, torch.float64, "exp", TOL_E64, TOL_PI64)
+
+
+def test_config5_full_f64(spl):
+    it = config(5).items[0]
+    pi, info = _full_size_check(spl, it.flux, it.t_d, torch.float64, "factored", TOL_E64, TOL_PI64)
+    assert info["converged"] and info["shift_l"] == 4916
+
+
+@pytest.mark.parametrize("mode", ["factored", "exp"])
+def test_config5_full_f32(spl, mode):
+    it = config(5).items[0]
+    _full_size_check(spl, it.flux, it.t_d, torch.float32, mode, TOL_E32, TOL_PI32)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_config5_deadtime_sweep(spl, dtype):
+    """16 dead times on one P~0 in one multi-vector plan (the a7 sweep), each vs the structured pi."""
+    w = config(5)
+    f = w.items[0].flux
+    tds = [it.t_d for it in w.sweep]
+    P0 = spl.build_base(f, dtype)
+    plan = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-12)
+    infos = plan.execute(check=dtype == torch.float64)
+    vec = oracle_vectors(f)
+    tol = TOL_PI64 if dtype == torch.float64 else TOL_PI32
+    for v, td in enumerate(tds):
+        ref, _ = structured_pi(f, td, vectors=vec)
+        assert np.sum(np.abs(_np(plan.pi[0, v]) - ref)) <= tol, td
+        assert infos[v]["shift_l"] == oracle.shift_l(f, td)
+    plan.close()
+    del P0
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------- degenerate cases
+def test_constant_flux_uniform_pi(spl):
+    """S = 0: circulant chain, pi = 1/N exactly, converges after one product (P5)."""
+    f = Flux(100.0, 1000, (50.0,), (1.0,), (0.0,), 3.0)
+    P0 = spl.build_base(f)
+    pi, info = spl.stationary(P0, f.t_r, 75.0)
+    assert np.max(np.abs(_np(pi) - 1e-3)) <= 1e-15
+    assert info["iters"] <= 2
+
+
+def test_tiny_n(spl):
+    for n in (2, 3):
+        f = random_flux(np.random.default_rng(n), n, 1)
+        for td in (0.0, 10.0, 150.0):
+            P0 = spl.build_base(f)
+            pi, _ = spl.stationary(P0, f.t_r, td)
+            want = oracle.stationary_dense(oracle.build_eq4(f, td))
+            assert np.sum(np.abs(_np(pi) - want)) <= 1e-13
