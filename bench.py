@@ -163,7 +163,6 @@ def run_ours(args, rank, world, dev):
         st.build()
         st.solve()
     torch.cuda.synchronize()
-    infos = st.infos()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]

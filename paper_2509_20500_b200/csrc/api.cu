@@ -20,20 +20,6 @@ int pad_vectors(int V) {
     return p;
 }
 
-// Splits of the row range per column strip for the GEMV grid: about 2400 CTAs (two waves of
-// 8 resident 256-thread CTAs on 148 SMs), with 64 <= rows per split and at most 64 splits, so the
-// partial sums (splits x N fp64 per vector) stay small beside the N^2 matrix stream and the
-// strip reduction stays short.
-static int choose_splits(int N, int M, int strips) {
-    const long target = 2400;
-    long R = (target + (long)strips * M - 1) / ((long)strips * M);
-    const long hi = N / 64 > 1 ? N / 64 : 1;
-    if (R > hi) R = hi;
-    if (R > 64) R = 64;
-    if (R < 1) R = 1;
-    return (int)R;
-}
-
 WsLayout ws_layout(int N, int M, int V) {
     WsLayout L;
     memset(&L, 0, sizeof(L));
@@ -41,9 +27,9 @@ WsLayout ws_layout(int N, int M, int V) {
     L.M = M;
     L.V = pad_vectors(V);
     L.strips = (N + kStripCols - 1) / kStripCols;
-    int R = choose_splits(N, M, L.strips);
-    L.rows_per_split = (N + R - 1) / R;
-    L.splits = (N + L.rows_per_split - 1) / L.rows_per_split;
+    L.chunks = (N + kCheckChunk - 1) / kCheckChunk;
+    L.xstride = L.V < 2 ? 2 : L.V;
+    L.pieces = kGemvCtas + M * L.strips;     // a CTA's k-th piece of strip g uses slot cta + g
     const size_t MV = (size_t)M * L.V;
     size_t o = 0;
     L.flux = o; o = a256(o + sizeof(FluxDev) * (size_t)M);
@@ -51,13 +37,14 @@ WsLayout ws_layout(int N, int M, int V) {
     L.lsh = o;  o = a256(o + sizeof(int) * MV);
     L.oidx = o; o = a256(o + sizeof(int) * MV);
     L.y = o;    o = a256(o + sizeof(double) * MV * 2 * N);
-    L.part = o; o = a256(o + sizeof(double) * MV * L.splits * N);
+    L.X = o;    o = a256(o + sizeof(double) * (size_t)M * N * L.xstride);
+    L.part = o; o = a256(o + sizeof(double) * (size_t)L.pieces * L.V * kStripCols);
     L.ssum = o; o = a256(o + sizeof(double) * MV * L.strips);
-    L.chunks = (N + kCheckChunk - 1) / kCheckChunk;
     L.l1part = o; o = a256(o + sizeof(double) * MV * L.chunks);
     L.state = o; o = a256(o + sizeof(SolveState) * MV);
     L.strip_cnt = o; o = a256(o + sizeof(unsigned) * (size_t)M * L.strips);
     L.mv_cnt = o; o = a256(o + sizeof(unsigned) * MV);
+    L.act = o; o = a256(o + sizeof(int) * (size_t)M);
     L.glob = o; o = a256(o + sizeof(unsigned) * 4);
     L.total = o;
     return L;
@@ -285,12 +272,21 @@ struct splidar_plan_s {
     std::vector<int> lsh;          // [M * V] (padded)
     std::vector<SolveState> host;  // [M * V]
     std::vector<int> out_idx;      // [M * V]
+    // eager mode (SPLIDAR_EAGER=1 at plan creation): the same kernels launched from a host loop that
+    // reads the any-active flag after each iteration; for profilers that do not descend into
+    // conditional graph bodies. Control only: every step still runs in the kernels.
+    bool eager = false;
+    SolverKernels k;
+    PowerArgs eager_args;
+    std::vector<unsigned char> fin_args;
+    unsigned *host_flag = nullptr;
 };
 
 static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws, cudaStream_t s) {
     const WsLayout &L = p->L;
     PowerArgs &a = p->args;
     a.y = reinterpret_cast<double *>(ws + L.y);
+    a.X = reinterpret_cast<double *>(ws + L.X);
     a.part = reinterpret_cast<double *>(ws + L.part);
     a.ssum = reinterpret_cast<double *>(ws + L.ssum);
     a.l1part = reinterpret_cast<double *>(ws + L.l1part);
@@ -298,14 +294,14 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     a.lsh = reinterpret_cast<const int *>(ws + L.lsh);
     a.strip_cnt = reinterpret_cast<unsigned *>(ws + L.strip_cnt);
     a.mv_cnt = reinterpret_cast<unsigned *>(ws + L.mv_cnt);
+    a.act = reinterpret_cast<int *>(ws + L.act);
     a.glob = reinterpret_cast<unsigned *>(ws + L.glob);
     a.N = L.N;
     a.M = L.M;
     a.V = L.V;
-    a.splits = L.splits;
     a.strips = L.strips;
-    a.rows_per_split = L.rows_per_split;
     a.chunks = L.chunks;
+    a.xstride = L.xstride;
 
     SPL_CUDA(spl::upload_async(ws + L.lsh, p->lsh.data(), sizeof(int) * p->lsh.size(), s));
     SPL_CUDA(spl::upload_async(ws + L.oidx, p->out_idx.data(), sizeof(int) * p->out_idx.size(), s));
@@ -316,8 +312,14 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     a.use_handle = 1;
     a.handle = h;
 
-    SolverKernels k;
+    SolverKernels &k = p->k;
     if (solver_kernels(dt, L.V, &k, a)) return SPLIDAR_EINVAL;
+    p->eager_args = a;
+    p->eager_args.use_handle = 0;
+    {
+        const char *e = getenv("SPLIDAR_EAGER");
+        p->eager = e && e[0] == '1';
+    }
 
     cudaKernelNodeParams kp;
     memset(&kp, 0, sizeof(kp));
@@ -353,7 +355,8 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     cudaGraphNode_t n_check;
     SPL_CUDA(cudaGraphAddKernelNode(&n_check, body, &n_step, 1, &kp));
 
-    std::vector<unsigned char> fa(finish_args_size());
+    std::vector<unsigned char> &fa = p->fin_args;
+    fa.resize(finish_args_size());
     make_finish_args(fa.data(), a, pi, reinterpret_cast<const int *>(ws + L.oidx));
     void *fin_args[] = {fa.data()};
     kp.func = k.finish_fn;
@@ -370,6 +373,7 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
 void splidar_plan_destroy(splidar_plan plan) {
     if (!plan) return;
     if (plan->exec) cudaGraphExecDestroy(plan->exec);
+    if (plan->host_flag) cudaFreeHost(plan->host_flag);
     if (plan->graph) cudaGraphDestroy(plan->graph);
     delete plan;
 }
@@ -428,8 +432,26 @@ splidar_status splidar_plan_create(splidar_plan *plan, const void *P0, int32_t n
                          pi, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
+    if (!p->host_flag) SPL_CUDA(cudaMallocHost(&p->host_flag, sizeof(unsigned)));
+    const SolverKernels &k = p->k;
+    void *args[] = {&p->eager_args};
+    SPL_CUDA(cudaLaunchKernel(k.init_fn, k.init_grid, k.init_block, args, 0, s));
+    for (int it = 0; it < p->args.max_iter; ++it) {
+        SPL_CUDA(cudaLaunchKernel(k.step_fn, k.step_grid, k.step_block, args, k.step_smem, s));
+        SPL_CUDA(cudaLaunchKernel(k.check_fn, k.check_grid, k.check_block, args, 0, s));
+        SPL_CUDA(cudaMemcpyAsync(p->host_flag, p->eager_args.glob + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        SPL_CUDA(cudaStreamSynchronize(s));
+        if (!*p->host_flag) break;
+    }
+    void *fargs[] = {p->fin_args.data()};
+    SPL_CUDA(cudaLaunchKernel(k.finish_fn, k.finish_grid, k.finish_block, fargs, 0, s));
+    return SPLIDAR_OK;
+}
+
 splidar_status splidar_plan_launch(splidar_plan plan, void *stream) {
     if (!plan) return SPLIDAR_EINVAL;
+    if (plan->eager) return plan_launch_eager(plan, (cudaStream_t)stream);
     return cuda_status(cudaGraphLaunch(plan->exec, (cudaStream_t)stream));
 }
 

@@ -14,6 +14,8 @@ constexpr int kMaxVectors = 16;      // dead times per matrix in one multi-vecto
 constexpr int kStripCols = 512;      // columns per GEMV / build CTA (4 KB of an fp64 row)
 constexpr int kNumSMs = 148;
 constexpr int kCheckChunk = 2048;   // elements per CTA of the convergence-check kernel
+constexpr int kGemvCtas = 2 * kNumSMs;  // persistent GEMV grid: two 256-thread CTAs per SM
+constexpr int kMinRowsPerCta = 64;      // smallest row range a GEMV CTA is given
 
 // theta without t_d, device copy. Eq. 1 with K pulses.
 struct FluxDev {
@@ -51,8 +53,8 @@ struct __align__(16) SolveState {
 // Workspace layout (offsets in bytes from the 256-aligned base).
 struct WsLayout {
     int N, M, V;    // V padded to a power of two
-    int strips, splits, rows_per_split, chunks;
-    size_t flux, vec, lsh, oidx, y, part, ssum, l1part, state, strip_cnt, mv_cnt, glob, total;
+    int strips, chunks, xstride, pieces;
+    size_t flux, vec, lsh, oidx, y, X, part, ssum, l1part, state, strip_cnt, mv_cnt, act, glob, total;
 };
 
 WsLayout ws_layout(int N, int M, int V);
@@ -70,16 +72,18 @@ struct PowerArgs {
     const void *P;
     int64_t ld;
     int64_t mstride;
-    int N, M, V, splits, strips, rows_per_split, chunks;
-    double *y;               // [M][V][2][N]
-    double *part;            // [M][V][splits][N]
-    double *ssum;            // [M][V][strips]
-    double *l1part;          // [M][V][chunks]  per-chunk L1 changes (check kernel)
+    int N, M, V, strips, chunks, xstride;
+    double *y;               // [M][V][2][N]       unnormalised iterates (ping-pong)
+    double *X;               // [M][N][xstride]    gathered, normalised x_v[r] = pi_v[(r - l_v) mod N]
+    double *part;            // [pieces][V][512]   per-CTA partial column sums
+    double *ssum;            // [M][V][strips]     strip sums of y
+    double *l1part;          // [M][V][chunks]     per-chunk L1 changes (check kernel)
     SolveState *st;          // [M][V]
     const int *lsh;          // [M][V] row shifts l (< 0: unused vector)
-    unsigned *strip_cnt;     // [M][strips]
-    unsigned *mv_cnt;        // [M][V] check-kernel CTA counters
-    unsigned *glob;          // [0] check-kernel CTA counter, [1] any-active flag
+    unsigned *strip_cnt;     // [M * strips]       pieces finished per strip (active order)
+    unsigned *mv_cnt;        // [M][V]             check-kernel CTA counters
+    int *act;                // [M]                active matrices (any vector still running)
+    unsigned *glob;          // [0] check CTA counter, [1] any-active flag, [2] number of active matrices
     double tol;
     int max_iter;
     int use_handle;

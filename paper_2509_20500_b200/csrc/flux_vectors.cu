@@ -1,5 +1,7 @@
 // Step 1 of the path (K1-K3): discretised flux, warp+block prefix sums, row
-// normalisers. One 1024-thread CTA per flux profile; everything fp64 and tree-shaped.
+// normalisers; everything fp64, the sums tree-shaped. The transcendental work (erfc differences,
+// exp) runs grid-wide in pointwise kernels (A, C, E); the scans (B, D) run one 1024-thread CTA per
+// profile (warp __shfl_up_sync scan + block scan of warp totals + a carry across 8192-element tiles).
 //
 //   masses   m_0 = int_0^{s_0} lambda, m_j = int_{s_{j-1}}^{s_j} lambda (1 <= j < N),
 //            m_N = int_{s_{N-1}}^{t_r} lambda, each exact (erfc differences, Eq. 1)
@@ -90,77 +92,88 @@ __device__ double block_scan_tile(double (&v)[kEPT], double *warp_tot, double ca
     return total;
 }
 
-__global__ void __launch_bounds__(kThreads) k_flux_vectors(const FluxDev *__restrict__ fluxes, int N,
-                                                           VecPtrs base, int64_t vstride) {
-    __shared__ double warp_tot[kWarps];
-    __shared__ FluxDev f;
-    const int m = blockIdx.x;
-    if (threadIdx.x == 0) f = fluxes[m];
-    __syncthreads();
-    double *F = base.F + m * vstride, *lam = base.lam + m * vstride, *w = base.w + m * vstride;
-    double *invD = base.invD + m * vstride, *invZ = base.invZ + m * vstride;
-    double *scal = base.scal + m * 8;
+// (A) pointwise, grid-wide: bin masses m_e (e = 0..N) into F[] (m_N into scal[3]) and lambda_j.
+__global__ void __launch_bounds__(256) k_vec_pointwise(const FluxDev *__restrict__ fluxes, int N, VecPtrs base,
+                                                       int64_t vstride) {
+    const int m = blockIdx.y;
+    const FluxDev &f = fluxes[m];
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e > N) return;
+    const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
+    const double hi = e == N ? f.t_r : bin_centre(f, e);
+    const double mass = flux_mass(f, lo, hi);
+    if (e < N) {
+        base.F[m * vstride + e] = mass;
+        base.lam[m * vstride + e] = flux_rate(f, bin_centre(f, e));
+    } else {
+        base.scal[m * 8 + 3] = mass;
+    }
+}
 
-    // ---- pass 1: masses -> F (inclusive), lambda(s_j); Lambda = total of the N + 1 masses
+// (B) one CTA per profile: F = inclusive prefix sum of the masses (in place), Lambda = F_{N-1} + m_N.
+__global__ void __launch_bounds__(kThreads) k_vec_scan_F(int N, VecPtrs base, int64_t vstride) {
+    __shared__ double warp_tot[kWarps];
+    const int m = blockIdx.x;
+    double *F = base.F + m * vstride;
+    double *scal = base.scal + m * 8;
     double carry = 0.0;
-    for (int t0 = 0; t0 <= N; t0 += kTile) {
+    for (int t0 = 0; t0 < N; t0 += kTile) {
         double v[kEPT];
         const int e0 = t0 + threadIdx.x * kEPT;
 #pragma unroll
-        for (int i = 0; i < kEPT; ++i) {
-            const int e = e0 + i;
-            if (e <= N) {
-                const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
-                const double hi = e == N ? f.t_r : bin_centre(f, e);
-                v[i] = flux_mass(f, lo, hi);
-            } else {
-                v[i] = 0.0;
-            }
-        }
+        for (int i = 0; i < kEPT; ++i) v[i] = e0 + i < N ? F[e0 + i] : 0.0;
         const double tot = block_scan_tile(v, warp_tot, carry);
 #pragma unroll
-        for (int i = 0; i < kEPT; ++i) {
-            const int e = e0 + i;
-            if (e < N) {
-                F[e] = v[i];
-                lam[e] = flux_rate(f, bin_centre(f, e));
-            }
-        }
+        for (int i = 0; i < kEPT; ++i)
+            if (e0 + i < N) F[e0 + i] = v[i];
         carry += tot;
     }
-    const double Lam = carry;
-    const double eL = exp(-Lam);
-    __syncthreads();  // F, lam visible to the whole block
+    if (threadIdx.x == 0) {
+        const double Lam = carry + scal[3];   // the tail mass int_{s_{N-1}}^{t_r} lambda closes the period
+        scal[0] = Lam;
+        scal[1] = exp(-Lam);
+    }
+}
 
-    // ---- pass 2: w_j, exclusive prefix L_r (scan of w shifted by one), stored in invD for now
-    carry = 0.0;
+// (C) pointwise: w_j = lambda_j e^{-F_j}.
+__global__ void __launch_bounds__(256) k_vec_w(int N, VecPtrs base, int64_t vstride) {
+    const int m = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < N) base.w[m * vstride + j] = base.lam[m * vstride + j] * exp(-base.F[m * vstride + j]);
+}
+
+// (D) one CTA per profile: L_r = sum_{j<r} w_j (exclusive prefix), U_r = sum_{j>=r} w_j (suffix),
+// D_r = U_r + e^{-Lambda} L_r, invD_r = 1 / D_r; a bad-row flag if some D_r is not positive and finite.
+__global__ void __launch_bounds__(kThreads) k_vec_scan_D(int N, VecPtrs base, int64_t vstride) {
+    __shared__ double warp_tot[kWarps];
+    const int m = blockIdx.x;
+    const double *w = base.w + m * vstride;
+    double *invD = base.invD + m * vstride;
+    double *scal = base.scal + m * 8;
+    const double eL = scal[1];
+    // prefix: scan of w shifted by one (element r holds w_{r-1}) = exclusive prefix L_r, kept in invD
+    double carry = 0.0;
     for (int t0 = 0; t0 < N; t0 += kTile) {
         double v[kEPT];
         const int e0 = t0 + threadIdx.x * kEPT;
 #pragma unroll
         for (int i = 0; i < kEPT; ++i) {
             const int e = e0 + i;
-            v[i] = (e >= 1 && e < N) ? lam[e - 1] * exp(-F[e - 1]) : 0.0;
+            v[i] = (e >= 1 && e < N) ? w[e - 1] : 0.0;
         }
         const double tot = block_scan_tile(v, warp_tot, carry);
 #pragma unroll
-        for (int i = 0; i < kEPT; ++i) {
-            const int e = e0 + i;
-            if (e < N) {
-                invD[e] = v[i];                      // L_e
-                w[e] = lam[e] * exp(-F[e]);
-            }
-        }
+        for (int i = 0; i < kEPT; ++i)
+            if (e0 + i < N) invD[e0 + i] = v[i];
         carry += tot;
     }
     __syncthreads();
-
-    // ---- pass 3: suffix U_r = sum_{j >= r} w_j (scan of the reversed sequence), D_r, 1/D_r, 1/Z_r
+    // suffix: scan of the reversed sequence, element e holds w_{N-1-e}
     carry = 0.0;
     int bad = 0;
     for (int t0 = 0; t0 < N; t0 += kTile) {
         double v[kEPT];
-        const int e0 = t0 + threadIdx.x * kEPT;   // reversed index: r = N - 1 - e
+        const int e0 = t0 + threadIdx.x * kEPT;
 #pragma unroll
         for (int i = 0; i < kEPT; ++i) {
             const int e = e0 + i;
@@ -172,29 +185,34 @@ __global__ void __launch_bounds__(kThreads) k_flux_vectors(const FluxDev *__rest
             const int e = e0 + i;
             if (e < N) {
                 const int r = N - 1 - e;
-                const double D = v[i] + eL * invD[r];  // U_r + e^{-Lambda} L_r
-                const bool ok = D > 0.0 && isfinite(D);
-                bad |= !ok;
-                const double id = 1.0 / D;
-                invD[r] = id;
-                invZ[r] = id * exp(-F[r]);
+                const double D = v[i] + eL * invD[r];   // U_r + e^{-Lambda} L_r
+                bad |= !(D > 0.0 && isfinite(D));
+                invD[r] = 1.0 / D;
             }
         }
         carry += tot;
     }
     bad = __syncthreads_or(bad);
-    if (threadIdx.x == 0) {
-        scal[0] = Lam;
-        scal[1] = eL;
-        scal[2] = bad ? 1.0 : 0.0;
-    }
+    if (threadIdx.x == 0) scal[2] = bad ? 1.0 : 0.0;
+}
+
+// (E) pointwise: invZ_r = e^{-F_r} / D_r (row normaliser of the exp form).
+__global__ void __launch_bounds__(256) k_vec_invz(int N, VecPtrs base, int64_t vstride) {
+    const int m = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < N) base.invZ[m * vstride + j] = base.invD[m * vstride + j] * exp(-base.F[m * vstride + j]);
 }
 
 }  // namespace
 
 cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs base, int64_t vstride,
                                 cudaStream_t s) {
-    k_flux_vectors<<<M, kThreads, 0, s>>>(d_flux, N, base, vstride);
+    const dim3 gp((N + 1 + 255) / 256, M), gv((N + 255) / 256, M);
+    k_vec_pointwise<<<gp, 256, 0, s>>>(d_flux, N, base, vstride);
+    k_vec_scan_F<<<M, kThreads, 0, s>>>(N, base, vstride);
+    k_vec_w<<<gv, 256, 0, s>>>(N, base, vstride);
+    k_vec_scan_D<<<M, kThreads, 0, s>>>(N, base, vstride);
+    k_vec_invz<<<gv, 256, 0, s>>>(N, base, vstride);
     return cudaGetLastError();
 }
 

@@ -1,43 +1,70 @@
 // Step 4 (K6 + K7): power iteration for pi P~ = pi with P~ = J_l P~0 (Thm 2),
-// one kernel per iteration, looped on the device by a CUDA-graph conditional WHILE node.
+// looped on the device by a CUDA-graph conditional WHILE node whose body is two kernels.
 //
-// One iteration for NV dead times sharing one P~0 (NV = 1 for a single solve):
-//   x_v[r]   = pi_v^k[(r - l_v) mod N]              (row permutation folded into the gather)
+// One iteration for V dead times sharing one P~0 (V = 1 for a single solve):
+//   x_v[r]   = pi_v^k[(r - l_v) mod N]              (row permutation folded into the gather; the
+//                                                     check kernel writes x in this gathered form)
 //   y_v[j]   = sum_r x_v[r] P~0[r][j]               (left GEMV, fp64 accumulation)
 //   s_v = sum_j y_v[j],  pi_v^{k+1} = y_v / s_v,  change_v = ||pi_v^{k+1} - pi_v^k||_1
-//   (pi is kept as (y, s): the next iteration gathers y_v * (1 / s_v))
 //
-// Grid (strips, splits, matrices). CTA (c, s, m) reads the 512-column strip c of rows
-// [s * rows_per_split, ...) of matrix m once (128-bit loads, 8 rows in flight per thread), multiplies by
-// the NV gathered vectors staged in shared memory, and writes fp64 partial sums [v][s][j].
-// The last CTA of a strip (atomic counter) adds the splits' partials in fixed order
-// (deterministic) and writes y and the strip's sum of y. A second, small kernel (k_power_check)
-// forms s, the normalised L1 change and the per-vector state, and its last CTA sets the WHILE
-// condition (any vector still running and below max_iter). Converged vectors are frozen; a matrix
-// whose vectors are all done is skipped by all of its CTAs.
+// k_power_step (the GEMV, the dominant kernel): a persistent grid of kGemvCtas CTAs splits the
+// row-segments (matrix, 512-column strip, row) of all still-active matrices into equal contiguous
+// ranges (stream-K style, so the grid stays full when only a few matrices of a batch are still
+// iterating). Each CTA streams its rows through a 3-stage shared-memory ring filled by TMA bulk
+// copies (cp.async.bulk + mbarrier complete_tx): per stage, RS row segments of 4 KB (fp64) or 2 KB
+// (fp32) plus the matching RS rows of gathered x. Threads read their 2 columns per row from
+// shared memory and accumulate all running vectors in fp64 registers; x of converged vectors is
+// compacted away per stage so frozen vectors cost no FMAs. At the end of a strip piece a CTA writes
+// its partial column sums; the last piece of a strip (atomic counter) adds the pieces in fixed order
+// (deterministic), writes y and the strip's sum of y.
+// k_power_check: s, the normalised L1 change, the state, the next gathered x, the active-matrix
+// list, and (last CTA) the WHILE condition.
 #include "common.cuh"
 
 namespace spl {
 namespace {
 
-constexpr int kSub = 64;      // rows of x staged in shared memory at a time
-constexpr int kUnroll = 8;    // rows of P~0 in flight per thread
+constexpr int kStages = 3;
+constexpr int kThreads = 256;           // 2 columns per thread across a 512-column strip
 
-template <typename T> struct Ld16;
-template <> struct Ld16<double> {
-    static constexpr int n = 2;
-    __device__ static __forceinline__ void load(const double *p, double (&o)[2]) {
-        const double2 v = __ldg(reinterpret_cast<const double2 *>(p));
-        o[0] = v.x; o[1] = v.y;
+// RS rows per stage; SROW = shared-memory row stride in elements (512 + pad, 16-byte multiple) so that
+// the k-rows of an MMA B fragment fall in different banks.
+template <typename T> struct GemvCfg;
+template <> struct GemvCfg<double> { static constexpr int RS = 8, SROW = kStripCols + 4; };   // 8 x 4 KB
+template <> struct GemvCfg<float> { static constexpr int RS = 16, SROW = kStripCols + 8; };   // 16 x 2 KB
+
+// ------------------------------------------------------------------ PTX helpers (sm_90+ / sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
     }
-};
-template <> struct Ld16<float> {
-    static constexpr int n = 4;
-    __device__ static __forceinline__ void load(const float *p, double (&o)[4]) {
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
-        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
-    }
-};
+}
+// 1-D TMA bulk copy global -> shared, completion counted on the mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
@@ -45,167 +72,319 @@ __device__ __forceinline__ double warp_sum(double x) {
     return x;
 }
 
-template <typename T, int NV>
-__global__ void __launch_bounds__(kStripCols / Ld16<T>::n) k_power_step(const PowerArgs a) {
-    constexpr int VEC = Ld16<T>::n;
-    constexpr int THREADS = kStripCols / VEC;
-    constexpr int NWARPS = THREADS / 32;
-    __shared__ double xs[kSub * NV];
-    __shared__ double s_inv[NV];
-    __shared__ int s_l[NV], s_cur[NV], s_done[NV];
-    __shared__ int s_active, s_last_strip;
-    __shared__ double red_sum[NWARPS][NV];
+template <typename T> __device__ __forceinline__ void lds2(const T *p, double &a, double &b);
+template <> __device__ __forceinline__ void lds2<double>(const double *p, double &a, double &b) {
+    const double2 v = *reinterpret_cast<const double2 *>(p);
+    a = v.x; b = v.y;
+}
+template <> __device__ __forceinline__ void lds2<float>(const float *p, double &a, double &b) {
+    const float2 v = *reinterpret_cast<const float2 *>(p);
+    a = v.x; b = v.y;
+}
 
-    const int m = blockIdx.z, split = blockIdx.y, strip = blockIdx.x, tid = threadIdx.x;
-    const int N = a.N;
-    SolveState *st = a.st + (size_t)m * NV;
-    if (tid < NV) {
-        const SolveState s = st[tid];
-        s_inv[tid] = 1.0 / s.s;
-        s_l[tid] = s.l < 0 ? 0 : s.l;
-        s_cur[tid] = s.cur;
-        s_done[tid] = s.done;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        int act = 0;
+// acc[a][0..1] += sum_{rr < nr} xs[rr][a] * seg[rr][2 tid .. 2 tid + 1] for slots a < NA.
+template <typename T, int NV, int NA, int RS>
+__device__ __forceinline__ void stage_fma(double (&acc)[NV][2], const T *seg, const double *xs, int xst, int nr,
+                                          int tid) {
+    constexpr int SROW = GemvCfg<T>::SROW;   // shared-memory row stride
+    if (nr == RS) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) act |= !s_done[v];
-        s_active = act;
-    }
-    __syncthreads();
-
-    if (s_active) {
-        const T *__restrict__ P = reinterpret_cast<const T *>(a.P) + (size_t)m * a.mstride;
-        double *ybase = a.y + (size_t)m * NV * 2 * N;
-        const int j0 = strip * kStripCols + tid * VEC;
-        const bool full = j0 + VEC <= N;
-        double acc[NV][VEC];
+        for (int rr = 0; rr < RS; ++rr) {
+            double p0, p1;
+            lds2<T>(seg + rr * SROW + 2 * tid, p0, p1);
+            const double *xr = xs + rr * xst;
+            if constexpr (NA == 1) {
+                const double x = xr[0];
+                acc[0][0] = fma(x, p0, acc[0][0]);
+                acc[0][1] = fma(x, p1, acc[0][1]);
+            } else {
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) acc[v][e] = 0.0;
-
-        const int r0 = split * a.rows_per_split;
-        const int r1 = min(N, r0 + a.rows_per_split);
-        for (int rb = r0; rb < r1; rb += kSub) {
-            const int nr = min(kSub, r1 - rb);
-            for (int idx = tid; idx < nr * NV; idx += THREADS) {
-                const int rr = idx / NV, v = idx % NV;
-                int src = rb + rr - s_l[v];
-                if (src < 0) src += N;
-                xs[idx] = ybase[(size_t)(v * 2 + s_cur[v]) * N + src] * s_inv[v];
-            }
-            __syncthreads();
-            if (full) {
-                const T *prow = P + (size_t)rb * a.ld + j0;
-                int rr = 0;
-                for (; rr + kUnroll <= nr; rr += kUnroll) {
-                    double p[kUnroll][VEC];
-#pragma unroll
-                    for (int u = 0; u < kUnroll; ++u) Ld16<T>::load(prow + (size_t)(rr + u) * a.ld, p[u]);
-#pragma unroll
-                    for (int u = 0; u < kUnroll; ++u)
-#pragma unroll
-                        for (int v = 0; v < NV; ++v) {
-                            const double x = xs[(rr + u) * NV + v];
-#pragma unroll
-                            for (int e = 0; e < VEC; ++e) acc[v][e] = fma(x, p[u][e], acc[v][e]);
-                        }
-                }
-                for (; rr < nr; ++rr) {
-                    double p[VEC];
-                    Ld16<T>::load(prow + (size_t)rr * a.ld, p);
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-                        const double x = xs[rr * NV + v];
-#pragma unroll
-                        for (int e = 0; e < VEC; ++e) acc[v][e] = fma(x, p[e], acc[v][e]);
-                    }
-                }
-            } else if (j0 < N) {
-                for (int rr = 0; rr < nr; ++rr) {
-                    const T *prow = P + (size_t)(rb + rr) * a.ld + j0;
-#pragma unroll
-                    for (int e = 0; e < VEC; ++e) {
-                        if (j0 + e < N) {
-                            const double pe = (double)prow[e];
-#pragma unroll
-                            for (int v = 0; v < NV; ++v) acc[v][e] = fma(xs[rr * NV + v], pe, acc[v][e]);
-                        }
-                    }
+                for (int v = 0; v < NA; v += 2) {
+                    const double2 x = *reinterpret_cast<const double2 *>(xr + v);
+                    acc[v][0] = fma(x.x, p0, acc[v][0]);
+                    acc[v][1] = fma(x.x, p1, acc[v][1]);
+                    acc[v + 1][0] = fma(x.y, p0, acc[v + 1][0]);
+                    acc[v + 1][1] = fma(x.y, p1, acc[v + 1][1]);
                 }
             }
-            __syncthreads();
         }
-
-        // partial sums of this split: part[m][v][split][j]
-        double *part = a.part + (size_t)m * NV * a.splits * N;
+    } else {
+        for (int rr = 0; rr < nr; ++rr) {
+            double p0, p1;
+            lds2<T>(seg + rr * SROW + 2 * tid, p0, p1);
+            const double *xr = xs + rr * xst;
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int e = 0; e < VEC; ++e)
-                if (j0 + e < N) part[((size_t)v * a.splits + split) * N + j0 + e] = acc[v][e];
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) {
-            const unsigned prev = atomicAdd(&a.strip_cnt[(size_t)m * a.strips + strip], 1u);
-            s_last_strip = prev == (unsigned)(a.splits - 1);
-        }
-        __syncthreads();
-
-        if (s_last_strip) {
-            // ---- strip finalisation: y = sum over splits (fixed order) and the strip's sum of y
-            __threadfence();
-            double lsum[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) lsum[v] = 0.0;
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                const int j = j0 + e;
-                if (j < N) {
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-                        const double *pp = part + (size_t)v * a.splits * N + j;
-                        // fixed-order sum over splits: 4 interleaved partial sums, then (a0+a1)+(a2+a3)
-                        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                        int s = 0;
-                        for (; s + 4 <= a.splits; s += 4) {
-                            a0 += __ldcg(pp + (size_t)(s + 0) * N);
-                            a1 += __ldcg(pp + (size_t)(s + 1) * N);
-                            a2 += __ldcg(pp + (size_t)(s + 2) * N);
-                            a3 += __ldcg(pp + (size_t)(s + 3) * N);
-                        }
-                        for (; s < a.splits; ++s) a0 += __ldcg(pp + (size_t)s * N);
-                        const double y = (a0 + a1) + (a2 + a3);
-                        ybase[((size_t)v * 2 + (1 - s_cur[v])) * N + j] = y;
-                        lsum[v] += y;
-                    }
-                }
+            for (int v = 0; v < NA; ++v) {
+                acc[v][0] = fma(xr[v], p0, acc[v][0]);
+                acc[v][1] = fma(xr[v], p1, acc[v][1]);
             }
-            const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const double t = warp_sum(lsum[v]);
-                if (lane == 0) red_sum[warp][v] = t;
-            }
-            __syncthreads();
-            if (tid < NV) {
-                double ssum = 0.0;
-#pragma unroll
-                for (int w = 0; w < NWARPS; ++w) ssum += red_sum[w][tid];
-                a.ssum[((size_t)m * NV + tid) * a.strips + strip] = ssum;
-            }
-            if (tid == 0) a.strip_cnt[(size_t)m * a.strips + strip] = 0u;
         }
     }
 }
 
-// Convergence check of one iteration (runs after k_power_step in the WHILE body).
-// CTA (c, mv): s = sum of the strip sums (fixed order), then the chunk's part of
-// ||y / s - pi^k||_1; the last CTA of each (matrix, vector) adds the chunks in fixed order and updates
-// the state (iters, s, change, cur, converged / done); the last CTA of the grid sets the WHILE
-// condition. Done vectors are skipped (their pi stays frozen).
+template <typename T, int NV, int RS>
+__device__ __forceinline__ void stage_fma_active(int na, double (&acc)[NV][2], const T *seg, const double *xs,
+                                                 int xst, int nr, int tid) {
+    if constexpr (NV <= 2) {
+        stage_fma<T, NV, NV, RS>(acc, seg, xs, xst, nr, tid);
+    } else {
+        if (na <= 4) stage_fma<T, NV, 4, RS>(acc, seg, xs, xst, nr, tid);
+        else if constexpr (NV >= 8) {
+            if (na <= 8) stage_fma<T, NV, 8, RS>(acc, seg, xs, xst, nr, tid);
+            else if constexpr (NV >= 16) {
+                if (na <= 12) stage_fma<T, NV, 12, RS>(acc, seg, xs, xst, nr, tid);
+                else stage_fma<T, NV, 16, RS>(acc, seg, xs, xst, nr, tid);
+            }
+        }
+    }
+}
+
+// DMMA (FP64 tensor core, mma.sync) form of a stage for MT = 16 or 8 vectors: per warp, the
+// 64-column slice [64 w, 64 w + 64) as 8 n-tiles; D[v][col] += sum_k X[k][v] P[k][col] with
+// A = X^T (MT x 4), B = P rows (4 x 8), D in registers: acc[nt][q] holds
+// (v, col) = (g + 8 (q >> 1), 64 w + 8 nt + 2 t + (q & 1)), g = lane / 4, t = lane % 4.
+// Rows k >= nr of a partial stage are zeroed in both operands (stale shared memory may hold NaN).
+template <typename T, int MT, int RS>
+__device__ __forceinline__ void stage_mma(double (&acc)[8][MT / 4], const T *seg, const double *xs, int nr,
+                                          int lane, int warp) {
+    constexpr int SROW = GemvCfg<T>::SROW;
+    const int g = lane >> 2, t = lane & 3;
+    const T *sb = seg + warp * 64 + g;
+#pragma unroll
+    for (int kb = 0; kb < RS; kb += 4) {
+        const int k = kb + t;
+        const bool kin = k < nr;
+        const double a0 = kin ? xs[k * MT + g] : 0.0;
+        double a1 = 0.0;
+        if constexpr (MT == 16) a1 = kin ? xs[k * MT + g + 8] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+            const double bv = kin ? (double)sb[k * SROW + nt * 8] : 0.0;
+            if constexpr (MT == 16) {
+                asm volatile(
+                    "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                    : "+d"(acc[nt][0]), "+d"(acc[nt][1]), "+d"(acc[nt][2]), "+d"(acc[nt][3])
+                    : "d"(a0), "d"(a1), "d"(bv));
+            } else {
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(acc[nt][0]), "+d"(acc[nt][1])
+                             : "d"(a0), "d"(bv));
+            }
+        }
+    }
+}
+
+template <typename T, int NV>
+struct StepSmem {
+    static constexpr int RS = GemvCfg<T>::RS;
+    static constexpr int XST = NV < 2 ? 2 : NV;                         // == PowerArgs::xstride
+    static constexpr int SROW = GemvCfg<T>::SROW;
+    static constexpr size_t SEG = (size_t)RS * SROW * sizeof(T);        // matrix bytes per stage
+    static constexpr size_t XB = (size_t)RS * XST * sizeof(double);     // x bytes per stage
+    static constexpr bool MMA = NV >= 8;                                 // DMMA path for 8 / 16 vectors
+    static constexpr size_t XC = (NV >= 4 && !MMA) ? (size_t)2 * RS * NV * sizeof(double) : 0;
+    static constexpr size_t BYTES = kStages * (SEG + XB) + XC + kStages * sizeof(uint64_t);
+};
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(kThreads, 2) k_power_step(const PowerArgs a) {
+    using SM = StepSmem<T, NV>;
+    constexpr int RS = SM::RS;
+    constexpr int NWARPS = kThreads / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T *segs = reinterpret_cast<T *>(smem);                                             // [S][RS][512]
+    double *xbuf = reinterpret_cast<double *>(smem + kStages * SM::SEG);               // [S][RS][XST]
+    double *xcmp = reinterpret_cast<double *>(smem + kStages * (SM::SEG + SM::XB));    // [2][RS][NV]
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * (SM::SEG + SM::XB) + SM::XC);
+    __shared__ int s_vmap[NV], s_cur[NV], s_nact, s_last;
+    __shared__ double red_sum[NWARPS][NV];
+
+    const int tid = threadIdx.x, b = blockIdx.x, G = gridDim.x;
+    const int N = a.N, S = a.strips;
+    const int n_act = (int)a.glob[2];
+    const int64_t T_units = (int64_t)n_act * S * N;
+    if (T_units == 0) return;
+    int64_t U = (T_units + G - 1) / G;
+    if (U < kMinRowsPerCta) U = kMinRowsPerCta;
+    const int64_t u_begin = (int64_t)b * U;
+    if (u_begin >= T_units) return;
+    const int64_t u_end = u_begin + U < T_units ? u_begin + U : T_units;
+
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    uint32_t q_issue = 0, q_cons = 0;   // stage sequence numbers (buffer q % S, parity (q / S) & 1)
+    int64_t u = u_begin;
+    while (u < u_end) {
+        const int64_t g64 = u / N;                       // strip index in active order
+        const int g = (int)g64;
+        const int ai = g / S, c = g % S;
+        const int m = a.act[ai];
+        const int r_lo = (int)(u - g64 * N);
+        const int64_t strip_end = (g64 + 1) * N;
+        const int r_hi = (int)((u_end < strip_end ? u_end : strip_end) - g64 * N);
+        u = g64 * N + r_hi;
+
+        // running vectors of matrix m, compacted into slots
+        if (tid == 0) {
+            int n = 0;
+            for (int v = 0; v < NV; ++v) {
+                const SolveState s = a.st[(size_t)m * NV + v];
+                if (!s.done) { s_vmap[n] = v; s_cur[n] = s.cur; ++n; }
+            }
+            s_nact = n;
+        }
+        __syncthreads();
+        const int nact = s_nact;
+        const int na_r = NV >= 4 ? ((nact + 3) & ~3) : NV;
+
+        const int cols = min(kStripCols, N - c * kStripCols);
+        const uint32_t seg_bytes = (uint32_t)(((size_t)cols * sizeof(T) + 15) & ~(size_t)15);
+        const T *pbase = reinterpret_cast<const T *>(a.P) + (size_t)m * a.mstride + (size_t)c * kStripCols;
+        const double *xg = a.X + (size_t)m * N * SM::XST;
+        const int nstages = (r_hi - r_lo + RS - 1) / RS;
+
+        auto issue = [&](int k) {   // stage k of this piece into buffer q_issue % S (thread 0)
+            const int rs = r_lo + k * RS;
+            const int nr = min(RS, r_hi - rs);
+            const int buf = q_issue % kStages;
+            mbar_expect_tx(&full[buf], nr * seg_bytes + (uint32_t)(nr * SM::XST * sizeof(double)));
+            for (int rr = 0; rr < nr; ++rr)
+                bulk_g2s(segs + ((size_t)buf * RS + rr) * SM::SROW, pbase + (size_t)(rs + rr) * a.ld, seg_bytes,
+                         &full[buf]);
+            bulk_g2s(xbuf + (size_t)buf * RS * SM::XST, xg + (size_t)rs * SM::XST,
+                     (uint32_t)(nr * SM::XST * sizeof(double)), &full[buf]);
+            ++q_issue;
+        };
+        if (tid == 0)
+            for (int k = 0; k < kStages - 1 && k < nstages; ++k) issue(k);
+        else
+            q_issue += min(kStages - 1, nstages);
+
+        constexpr int NACC = SM::MMA ? 8 : NV;          // MMA: 8 n-tiles x NV/4 values; else NV x 2
+        constexpr int QACC = SM::MMA ? NV / 4 : 2;
+        double acc[NACC][QACC];
+#pragma unroll
+        for (int i = 0; i < NACC; ++i)
+#pragma unroll
+            for (int q = 0; q < QACC; ++q) acc[i][q] = 0.0;
+
+        for (int k = 0; k < nstages; ++k) {
+            const int buf = q_cons % kStages;
+            mbar_wait(&full[buf], (q_cons / kStages) & 1);
+            const int nr = min(RS, r_hi - (r_lo + k * RS));
+            const double *xs;
+            int xst;
+            if constexpr (NV >= 4 && !SM::MMA) {
+                double *xc = xcmp + (size_t)(k & 1) * RS * NV;
+                for (int i = tid; i < RS * NV; i += kThreads) {
+                    const int rr = i / NV, sl = i % NV;
+                    xc[i] = (sl < nact && rr < nr) ? xbuf[((size_t)buf * RS + rr) * SM::XST + s_vmap[sl]] : 0.0;
+                }
+                xs = xc;
+                xst = NV;
+            } else {
+                xs = xbuf + (size_t)buf * RS * SM::XST;
+                xst = SM::XST;
+            }
+            __syncthreads();   // x compacted; every thread is done with the previous stage's buffer
+            if (tid == 0) {
+                if (k + kStages - 1 < nstages) issue(k + kStages - 1);
+            } else if (k + kStages - 1 < nstages) {
+                ++q_issue;
+            }
+            const T *segb = segs + (size_t)buf * RS * SM::SROW;
+            if constexpr (SM::MMA) {
+                (void)xst;
+                stage_mma<T, NV, RS>(acc, segb, xs, nr, tid & 31, tid >> 5);
+            } else {
+                if (2 * tid < cols) stage_fma_active<T, NV, RS>(na_r, acc, segb, xs, xst, nr, tid);
+            }
+            ++q_cons;
+        }
+
+        // ---- piece done: partial column sums into slot (b + g); the last piece of the strip reduces
+        const int64_t gN = g64 * N;
+        const int first = (int)(gN / U);
+        const int last = (int)((gN + N - 1) / U);
+        double *part = a.part + (size_t)(b + g) * NV * kStripCols;
+        if constexpr (SM::MMA) {
+            // all NV rows of D (converged vectors are never read back)
+            const int lane = tid & 31, w = tid >> 5, gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                const int col = w * 64 + nt * 8 + 2 * tq;
+#pragma unroll
+                for (int h = 0; h < NV / 8; ++h)
+                    *reinterpret_cast<double2 *>(part + (size_t)(gq + 8 * h) * kStripCols + col) =
+                        make_double2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+            }
+        } else if (2 * tid < cols) {
+#pragma unroll
+            for (int sl = 0; sl < NV; ++sl)
+                if (sl < nact)
+                    *reinterpret_cast<double2 *>(part + (size_t)s_vmap[sl] * kStripCols + 2 * tid) =
+                        make_double2(acc[sl][0], acc[sl][1]);
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned prev = atomicAdd(&a.strip_cnt[g], 1u);
+            s_last = prev == (unsigned)(last - first);
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            double lsum[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) lsum[v] = 0.0;
+            if (2 * tid < cols) {
+#pragma unroll
+                for (int sl = 0; sl < NV; ++sl) {
+                    if (sl >= nact) break;
+                    const int v = s_vmap[sl];
+                    double y0 = 0.0, y1 = 0.0;
+                    for (int pc = first; pc <= last; ++pc) {   // fixed order over the pieces
+                        const double2 t = __ldcg(reinterpret_cast<const double2 *>(
+                            a.part + ((size_t)(pc + g) * NV + v) * kStripCols + 2 * tid));
+                        y0 += t.x;
+                        y1 += t.y;
+                    }
+                    double *yv = a.y + (((size_t)m * NV + v) * 2 + (1 - s_cur[sl])) * N + c * kStripCols + 2 * tid;
+                    yv[0] = y0;
+                    if (2 * tid + 1 < cols) yv[1] = y1;
+                    else y1 = 0.0;
+                    lsum[sl] = y0 + y1;
+                }
+            }
+            const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+            for (int sl = 0; sl < NV; ++sl) {
+                if (sl >= nact) break;
+                const double t = warp_sum(lsum[sl]);
+                if (lane == 0) red_sum[warp][sl] = t;
+            }
+            __syncthreads();
+            if (tid < nact) {
+                double ssum = 0.0;
+#pragma unroll
+                for (int w = 0; w < NWARPS; ++w) ssum += red_sum[w][tid];
+                a.ssum[((size_t)m * NV + s_vmap[tid]) * S + c] = ssum;
+            }
+            if (tid == 0) a.strip_cnt[g] = 0u;
+        }
+        __syncthreads();
+    }
+}
+
+// Convergence check of one iteration (after k_power_step in the WHILE body). CTA (chunk, mv):
+// s = sum of strip sums (fixed order); the chunk's part of ||y / s - pi^k||_1; the next gathered
+// x: X[m][(j + l) mod N][v] = y_j / s; the last CTA of each (matrix, vector) adds the chunks in
+// fixed order and updates the state; the last CTA of the grid rebuilds the active-matrix list and
+// sets the WHILE condition. Done vectors are skipped (their pi stays frozen).
 __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
     __shared__ double red[8];
     __shared__ int s_last;
@@ -213,15 +392,24 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
     const int N = a.N;
     const SolveState st = a.st[mv];
     if (!st.done) {
+        const int m = mv / a.V, v = mv % a.V;
         double S = 0.0;
         const double *ss = a.ssum + (size_t)mv * a.strips;
         for (int k = 0; k < a.strips; ++k) S += __ldcg(ss + k);
         const double inv_new = 1.0 / S, inv_old = 1.0 / st.s;
         const double *yn = a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
         const double *yo = a.y + ((size_t)mv * 2 + st.cur) * N;
+        double *X = a.X + (size_t)m * N * a.xstride + v;
+        const int l = st.l < 0 ? 0 : st.l;
         double l1 = 0.0;
         const int j1 = min(N, (c + 1) * kCheckChunk);
-        for (int j = c * kCheckChunk + tid; j < j1; j += 256) l1 += fabs(__ldcg(yn + j) * inv_new - yo[j] * inv_old);
+        for (int j = c * kCheckChunk + tid; j < j1; j += 256) {
+            const double pn = __ldcg(yn + j) * inv_new;
+            l1 += fabs(pn - yo[j] * inv_old);
+            int r = j + l;
+            if (r >= N) r -= N;
+            X[(size_t)r * a.xstride] = pn;
+        }
         l1 = warp_sum(l1);
         if ((tid & 31) == 0) red[tid >> 5] = l1;
         __syncthreads();
@@ -251,30 +439,39 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
             __threadfence();
         }
     }
-    // grid completion: the last CTA decides whether the WHILE loop runs again
     if (tid == 0) {
         __threadfence();
         const unsigned total = gridDim.x * gridDim.y;
         const unsigned prev = atomicAdd(&a.glob[0], 1u);
         if (prev == total - 1) {
             __threadfence();
-            int any = 0;
-            const int n = a.M * a.V;
-            for (int i = 0; i < n; ++i) any |= !__ldcg(&a.st[i].done);
+            int n_act = 0;
+            for (int m = 0; m < a.M; ++m) {
+                int any = 0;
+                for (int v = 0; v < a.V; ++v) any |= !__ldcg(&a.st[(size_t)m * a.V + v].done);
+                if (any) a.act[n_act++] = m;
+            }
             a.glob[0] = 0u;
-            a.glob[1] = (unsigned)any;
-            if (a.use_handle) cudaGraphSetConditional(a.handle, any ? 1u : 0u);
+            a.glob[1] = n_act > 0 ? 1u : 0u;
+            a.glob[2] = (unsigned)n_act;
+            if (a.use_handle) cudaGraphSetConditional(a.handle, n_act > 0 ? 1u : 0u);
         }
     }
 }
 
-// pi^0 = 1/N for every (matrix, vector); state reset; counters zeroed.
+// pi^0 = 1/N (y and gathered x), state reset, counters zeroed, all matrices with a real vector active.
 __global__ void k_power_init(const PowerArgs a) {
     const int mv = blockIdx.y;
+    const int m = mv / a.V, v = mv % a.V;
     const int N = a.N;
     double *y = a.y + (size_t)mv * 2 * N;
+    double *X = a.X + (size_t)m * N * a.xstride;
     const double u = 1.0 / (double)N;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) y[j] = u;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+        y[j] = u;
+        X[(size_t)j * a.xstride + v] = u;
+        if (a.V == 1) X[(size_t)j * a.xstride + 1] = 0.0;   // padding column of the 16-byte x row
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         SolveState s;
         const int l = a.lsh[mv];
@@ -287,14 +484,23 @@ __global__ void k_power_init(const PowerArgs a) {
         s.s = 1.0;
         s.change = __longlong_as_double(0x7ff0000000000000ll);  // +inf
         a.st[mv] = s;
+        a.mv_cnt[mv] = 0u;
     }
     if (mv == 0) {
         const int ncnt = a.M * a.strips;
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ncnt; i += gridDim.x * blockDim.x)
             a.strip_cnt[i] = 0u;
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.M * a.V; i += gridDim.x * blockDim.x)
-            a.mv_cnt[i] = 0u;
-        if (blockIdx.x == 0 && threadIdx.x == 0) { a.glob[0] = 0u; a.glob[1] = 1u; }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            int n = 0;
+            for (int mm = 0; mm < a.M; ++mm) {
+                int any = 0;
+                for (int vv = 0; vv < a.V; ++vv) any |= a.lsh[(size_t)mm * a.V + vv] >= 0;
+                if (any) a.act[n++] = mm;
+            }
+            a.glob[0] = 0u;
+            a.glob[1] = n > 0 ? 1u : 0u;
+            a.glob[2] = (unsigned)n;
+        }
     }
 }
 
@@ -316,24 +522,41 @@ __global__ void k_power_finish(const FinishArgs f) {
         out[j] = y[j] / s.s;
 }
 
-template <typename T>
-void *step_fn(int V) {
-    switch (V) {
-        case 1: return (void *)k_power_step<T, 1>;
-        case 2: return (void *)k_power_step<T, 2>;
-        case 4: return (void *)k_power_step<T, 4>;
-        case 8: return (void *)k_power_step<T, 8>;
-        case 16: return (void *)k_power_step<T, 16>;
-        default: return nullptr;
+template <typename T, int NV>
+void *step_entry(size_t *smem) {
+    *smem = StepSmem<T, NV>::BYTES;
+    void *fn = (void *)k_power_step<T, NV>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+    return fn;
+}
+
+void *step_fn(int dtype, int V, size_t *smem) {
+    if (dtype == SPLIDAR_F64) {
+        switch (V) {
+            case 1: return step_entry<double, 1>(smem);
+            case 2: return step_entry<double, 2>(smem);
+            case 4: return step_entry<double, 4>(smem);
+            case 8: return step_entry<double, 8>(smem);
+            case 16: return step_entry<double, 16>(smem);
+        }
+    } else {
+        switch (V) {
+            case 1: return step_entry<float, 1>(smem);
+            case 2: return step_entry<float, 2>(smem);
+            case 4: return step_entry<float, 4>(smem);
+            case 8: return step_entry<float, 8>(smem);
+            case 16: return step_entry<float, 16>(smem);
+        }
     }
+    return nullptr;
 }
 
 }  // namespace
 
-// Describes the three solver kernels (function, grid, block) for graph construction.
+// Describes the solver kernels (function, grid, block, shared memory) for graph construction.
 int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a) {
     out->init_fn = (void *)k_power_init;
-    out->step_fn = dtype == SPLIDAR_F64 ? step_fn<double>(V) : step_fn<float>(V);
+    out->step_fn = step_fn(dtype, V, &out->step_smem);
     out->check_fn = (void *)k_power_check;
     out->finish_fn = (void *)k_power_finish;
     if (!out->step_fn) return 1;
@@ -342,9 +565,8 @@ int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a) {
     out->init_block = dim3(256);
     out->finish_grid = dim3(gx, a.M * a.V);
     out->finish_block = dim3(256);
-    out->step_grid = dim3(a.strips, a.splits, a.M);
-    out->step_block = dim3(dtype == SPLIDAR_F64 ? kStripCols / 2 : kStripCols / 4);
-    out->step_smem = 0;
+    out->step_grid = dim3(kGemvCtas);
+    out->step_block = dim3(kThreads);
     out->check_grid = dim3(a.chunks, a.M * a.V);
     out->check_block = dim3(256);
     return 0;
