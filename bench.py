@@ -60,15 +60,31 @@ def load_peaks():
 
 
 # ------------------------------------------------------------------------------- workload
-def workload_items(name):
+def workload_items(name, rank=0, world=1):
+    """(Workload, groups): groups = [(flux, [dead times sharing that flux's P~0]), ...] for this rank.
+    c5: every rank solves t_d = 430 and its 16-value shard of a 16 * world-point dead-time sweep over
+    [10, 500] (world = 1: the config's own linspace(10, 500, 16)); other configs: every rank solves
+    an independent replica of the config's items (weak scaling, no collective)."""
     from workloads import config
+    from paper_2509_20500_b200.shard import shard
     k = int(name[1])
     w = config(k)
     if k == 5:
-        groups = [(w.items[0].flux, [w.items[0].t_d]), (w.items[0].flux, [it.t_d for it in w.sweep])]
+        f = w.items[0].flux
+        sweep = [float(t) for t in np.linspace(10.0, 500.0, 16 * world)]
+        groups = [(f, [w.items[0].t_d]), (f, shard(sweep, rank, world))]
     else:
         groups = [(it.flux, [it.t_d]) for it in w.items]
     return w, groups
+
+
+def load_traffic(workload, dtype):
+    """dram bytes per launch of the dominant kernels from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(f"{workload}_{dtype}")
+    except Exception:
+        return None
 
 
 # ------------------------------------------------------------------------------- clocks
@@ -156,7 +172,7 @@ class OurStep:
 def run_ours(args, rank, world, dev):
     import torch
     import paper_2509_20500_b200 as spl
-    w, groups = workload_items(args.workload)
+    w, groups = workload_items(args.workload, rank, world)
     st = OurStep(groups, args.dtype, args.mode)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -185,10 +201,8 @@ def run_ours(args, rank, world, dev):
     t_solve = sum(b.elapsed_time(c) for _, b, c in ev) / 1e3
     t_total = sum(a.elapsed_time(c) for a, _, c in ev) / 1e3
     infos = st.infos()
-    if world > 1:
-        t = torch.tensor([t_total, t_build, t_solve], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_total, t_build, t_solve = (float(x) for x in t.tolist())
+    from paper_2509_20500_b200.shard import max_over_ranks
+    t_total, t_build, t_solve = max_over_ranks([t_total, t_build, t_solve], device="cuda")
 
     b = 8 if args.dtype == "f64" else 4
     N = st.N
@@ -202,6 +216,7 @@ def run_ours(args, rank, world, dev):
     per_step_launches = 3 + sum(2 + 2 * int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
                                 for pi, p in zip(infos, st.plans))
     hbm, hbm_src = load_peaks()
+    traffic = load_traffic(args.workload, args.dtype)
     K = args.steps
     gemv_gbs = gemv_bytes * K / t_solve / 1e9
     build_gbs = st.entries * b * K / t_build / 1e9
@@ -220,17 +235,22 @@ def run_ours(args, rank, world, dev):
                    "matrices_per_step": len(st.fluxes), "solves_per_step": st.n_solves, "entry_mode": args.mode,
                    "tol": 1e-12, "l2": "matrix (%.2f GB) > 126 MB L2: no flush needed" % (st.entries * b / 1e9)
                    if st.entries * b > 126e6 else "matrix fits in L2 (latency-bound config); not flushed",
-                   "parallelism": f"replicas x{world} (independent items per rank, no collective)"},
+                   "parallelism": (f"dp{world}: items sharded over {world} ranks, no collective on the data path"
+                                   if world > 1 else "single GPU")},
         "entries_per_s": st.entries * K * world / t_build,
         "ms_build_per_step": t_build / K * 1e3, "ms_solve_per_step": t_solve / K * 1e3,
         "iterations": [[i["iters"] for i in pi] for pi in infos],
         "roofline": {"bound": "hbm", "kernel": "k_power_step (power-iteration GEMV)", "achieved": gemv_gbs,
-                     "peak": hbm, "unit": "GB/s", "frac": gemv_gbs / hbm, "traffic": None,
+                     "peak": hbm, "unit": "GB/s", "frac": gemv_gbs / hbm,
+                     "traffic": traffic.get("k_power_step") if traffic else None,
+                     "algorithmic_bytes_per_launch": N * N * b,
+                     "traffic_source": traffic.get("source") if traffic else None,
                      "peak_source": hbm_src,
                      "note": "achieved = algorithmic bytes (N^2 b per launch per active matrix) / solve-phase "
                              "time, which also contains the convergence-check kernels and graph loop overhead"},
         "roofline_build": {"bound": "hbm", "kernel": "k_build", "achieved": build_gbs, "peak": hbm, "unit": "GB/s",
-                           "frac": build_gbs / hbm, "note": "N^2 b bytes written per matrix / build-phase time "
+                           "frac": build_gbs / hbm, "traffic": traffic.get("k_build") if traffic else None,
+                           "note": "N^2 b bytes written per matrix / build-phase time "
                                                             "(includes the flux-vector scan kernel)"},
         "clocks": clk, "e2e": e2e, "gpu_launches": per_step_launches * K,
         "impl": "ours", "lib": spl.lib_path(),
@@ -282,10 +302,8 @@ def run_e2e(args, w, groups, st, world):
         one()
     torch.cuda.synchronize()
     dt_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([dt_s], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        dt_s = float(t.item())
+    from paper_2509_20500_b200.shard import max_over_ranks
+    dt_s = max_over_ranks([dt_s], device="cuda")[0]
     return {"value": n_solves * args.steps * world / dt_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": n_solves * N * 8,
             "note": "host wall clock; includes plan (CUDA graph) instantiation, the theta upload and the pi "

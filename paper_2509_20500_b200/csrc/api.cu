@@ -33,7 +33,8 @@ WsLayout ws_layout(int N, int M, int V) {
     const size_t MV = (size_t)M * L.V;
     size_t o = 0;
     L.flux = o; o = a256(o + sizeof(FluxDev) * (size_t)M);
-    L.vec = o;  o = a256(o + sizeof(double) * ((size_t)M * N * 5 + (size_t)M * 8));
+    const size_t ntile = ((size_t)N + 1 + kScanTile - 1) / kScanTile;
+    L.vec = o;  o = a256(o + sizeof(double) * ((size_t)M * N * 5 + (size_t)M * 8 + 5 * (size_t)M * ntile));
     L.lsh = o;  o = a256(o + sizeof(int) * MV);
     L.oidx = o; o = a256(o + sizeof(int) * MV);
     L.y = o;    o = a256(o + sizeof(double) * MV * 2 * N);
@@ -60,6 +61,8 @@ static VecPtrs vec_ptrs(char *ws, const WsLayout &L) {
     v.invD = b + 3 * MN;
     v.invZ = b + 4 * MN;
     v.scal = b + 5 * MN;
+    v.ntile = (L.N + 1 + kScanTile - 1) / kScanTile;
+    v.tiles = v.scal + (size_t)L.M * 8;
     return v;
 }
 

@@ -35,8 +35,11 @@ struct VecPtrs {
     double *w;      // lambda_j e^{-F_j}
     double *invD;   // 1 / D_r
     double *invZ;   // e^{-F_r} / D_r  (= 1 / Z_r, row sum of the exp form)
-    double *scal;   // [0] Lambda, [1] e^{-Lambda}, [2] bad-row flag (0 / 1)
+    double *scal;   // [0] Lambda, [1] e^{-Lambda}, [2] bad-row flag (0 / 1), [3] tail mass m_N
+    double *tiles;  // [5][M][ntile] per-1024-element-tile totals / offsets of the two-level scans
+    int ntile;      // ceil((N + 1) / 1024)
 };
+constexpr int kScanTile = 1024;      // elements per tile of the two-level scans (256 threads x 4)
 
 // Per (matrix, vector) power-iteration state.
 struct __align__(16) SolveState {

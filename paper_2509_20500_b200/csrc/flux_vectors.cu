@@ -1,7 +1,7 @@
-// Step 1 of the path (K1-K3): discretised flux, warp+block prefix sums, row
-// normalisers; everything fp64, the sums tree-shaped. The transcendental work (erfc differences,
-// exp) runs grid-wide in pointwise kernels (A, C, E); the scans (B, D) run one 1024-thread CTA per
-// profile (warp __shfl_up_sync scan + block scan of warp totals + a carry across 8192-element tiles).
+// Step 1 of the path (K1-K3): discretised flux, prefix sums, row normalisers.
+// Everything fp64; every sum is tree-shaped (thread-local run of 4, warp __shfl_up_sync scan,
+// fixed-order combination of the 8 warp totals, then a scan of the 1024-element tile totals),
+// never a long sequential chain (a sequential fp64 cumsum drifts ~1e-12 at N = 32768).
 //
 //   masses   m_0 = int_0^{s_0} lambda, m_j = int_{s_{j-1}}^{s_j} lambda (1 <= j < N),
 //            m_N = int_{s_{N-1}}^{t_r} lambda, each exact (erfc differences, Eq. 1)
@@ -13,15 +13,22 @@
 //   D_r      = U_r + e^{-Lambda} L_r = e^{-F_r} sum_j lambda_j exp(F_r - F_j - Lambda [r > j])
 //            (the row sum of (1 lambda^T) . exp.(-Lambda L - D), §3.4, over e^{F_r})
 //   invD_r   = 1 / D_r, invZ_r = e^{-F_r} / D_r (normalisation)
+//
+// Five grid-wide launches per batch of profiles (grid = tiles x profiles):
+//   A  masses + lambda, tile-local inclusive scan of the masses, tile totals
+//   B  exclusive scan of the tile totals (one CTA per profile) -> tile offsets, Lambda
+//   C  F = local + offset, w, tile-local exclusive prefix / inclusive suffix of w, tile totals of w
+//   D  exclusive prefix and suffix of the w tile totals (one CTA per profile)
+//   E  L, U, D, 1/D, 1/Z
+// tiles[5][M][ntile]: 0 mass tile totals, 1 mass tile offsets, 2 w tile totals, 3 w tile
+// prefix offsets, 4 w tile suffix offsets.
 #include "common.cuh"
 
 namespace spl {
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kWarps = kThreads / 32;
-constexpr int kEPT = 8;                       // consecutive elements per thread per tile
-constexpr int kTile = kThreads * kEPT;        // 8192 elements per tile
+constexpr int kT = 256;                 // threads per tile CTA
+constexpr int kE = kScanTile / kT;      // 4 consecutive elements per thread
 
 __device__ __forceinline__ double bin_centre(const FluxDev &f, int j) {
     return ((double)j + 0.5) * (f.t_r / (double)f.n);
@@ -57,15 +64,13 @@ __device__ double flux_rate(const FluxDev &f, double t) {
     return v;
 }
 
-// Block-wide inclusive scan of a tile: each thread holds kEPT consecutive values in v[].
-// Thread-local running sums, then a warp scan of thread totals (__shfl_up_sync, 5 steps), then
-// a scan of the 32 warp totals by warp 0, then offsets. `carry` (the sum of all previous
-// tiles) is added. Returns the tile total. Summation depth: kEPT + 5 + 5 + 1 per tile.
-__device__ double block_scan_tile(double (&v)[kEPT], double *warp_tot, double carry) {
+// Inclusive scan of a 1024-element tile held as 4 consecutive values per thread (256 threads);
+// returns the tile total. warp_tot: 8 doubles of shared memory.
+__device__ double tile_scan(double (&v)[kE], double *warp_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int i = 1; i < kEPT; ++i) v[i] += v[i - 1];
-    const double t = v[kEPT - 1];
+    for (int i = 1; i < kE; ++i) v[i] += v[i - 1];
+    const double t = v[kE - 1];
     double x = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -74,145 +79,207 @@ __device__ double block_scan_tile(double (&v)[kEPT], double *warp_tot, double ca
     }
     if (lane == 31) warp_tot[warp] = x;
     __syncthreads();
-    if (warp == 0) {
-        double s = warp_tot[lane];  // kWarps == 32
+    double wex = 0.0, total = 0.0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, s, o);
-            if (lane >= o) s += y;
-        }
-        warp_tot[lane] = s;
+    for (int w2 = 0; w2 < kT / 32; ++w2) {       // 8 warp totals: a short fixed-order sum
+        const double wt = warp_tot[w2];
+        if (w2 < warp) wex += wt;
+        total += wt;
     }
-    __syncthreads();
-    const double excl = (x - t) + (warp > 0 ? warp_tot[warp - 1] : 0.0);
-    const double total = warp_tot[kWarps - 1];
+    const double ex = (x - t) + wex;
 #pragma unroll
-    for (int i = 0; i < kEPT; ++i) v[i] = carry + (excl + v[i]);
-    __syncthreads();  // warp_tot is reused by the next tile
+    for (int i = 0; i < kE; ++i) v[i] += ex;
+    __syncthreads();
     return total;
 }
 
-// (A) pointwise, grid-wide: bin masses m_e (e = 0..N) into F[] (m_N into scal[3]) and lambda_j.
-__global__ void __launch_bounds__(256) k_vec_pointwise(const FluxDev *__restrict__ fluxes, int N, VecPtrs base,
-                                                       int64_t vstride) {
-    const int m = blockIdx.y;
-    const FluxDev &f = fluxes[m];
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e > N) return;
-    const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
-    const double hi = e == N ? f.t_r : bin_centre(f, e);
-    const double mass = flux_mass(f, lo, hi);
-    if (e < N) {
-        base.F[m * vstride + e] = mass;
-        base.lam[m * vstride + e] = flux_rate(f, bin_centre(f, e));
-    } else {
-        base.scal[m * 8 + 3] = mass;
-    }
-}
-
-// (B) one CTA per profile: F = inclusive prefix sum of the masses (in place), Lambda = F_{N-1} + m_N.
-__global__ void __launch_bounds__(kThreads) k_vec_scan_F(int N, VecPtrs base, int64_t vstride) {
-    __shared__ double warp_tot[kWarps];
-    const int m = blockIdx.x;
-    double *F = base.F + m * vstride;
-    double *scal = base.scal + m * 8;
-    double carry = 0.0;
-    for (int t0 = 0; t0 < N; t0 += kTile) {
-        double v[kEPT];
-        const int e0 = t0 + threadIdx.x * kEPT;
+// Exclusive prefix and suffix scans of n <= 4096 tile totals by one 1024-thread CTA, fixed tree
+// order: pre[i] = sum_{k<i} in[k], suf[i] = sum_{k>i} in[k]; returns the total (pre or suf may
+// be null).
+__device__ double totals_scan(const double *in, int n, double *pre, double *suf) {
+    __shared__ double wt_f[32], wt_b[32];
+    constexpr int EPT = 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double f[EPT], bk[EPT];
+    const int e0 = threadIdx.x * EPT;
 #pragma unroll
-        for (int i = 0; i < kEPT; ++i) v[i] = e0 + i < N ? F[e0 + i] : 0.0;
-        const double tot = block_scan_tile(v, warp_tot, carry);
-#pragma unroll
-        for (int i = 0; i < kEPT; ++i)
-            if (e0 + i < N) F[e0 + i] = v[i];
-        carry += tot;
+    for (int i = 0; i < EPT; ++i) {
+        f[i] = e0 + i < n ? in[e0 + i] : 0.0;
+        bk[i] = e0 + i < n ? in[n - 1 - (e0 + i)] : 0.0;   // reversed sequence for the suffix
     }
-    if (threadIdx.x == 0) {
-        const double Lam = carry + scal[3];   // the tail mass int_{s_{N-1}}^{t_r} lambda closes the period
-        scal[0] = Lam;
-        scal[1] = exp(-Lam);
-    }
-}
-
-// (C) pointwise: w_j = lambda_j e^{-F_j}.
-__global__ void __launch_bounds__(256) k_vec_w(int N, VecPtrs base, int64_t vstride) {
-    const int m = blockIdx.y;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < N) base.w[m * vstride + j] = base.lam[m * vstride + j] * exp(-base.F[m * vstride + j]);
-}
-
-// (D) one CTA per profile: L_r = sum_{j<r} w_j (exclusive prefix), U_r = sum_{j>=r} w_j (suffix),
-// D_r = U_r + e^{-Lambda} L_r, invD_r = 1 / D_r; a bad-row flag if some D_r is not positive and finite.
-__global__ void __launch_bounds__(kThreads) k_vec_scan_D(int N, VecPtrs base, int64_t vstride) {
-    __shared__ double warp_tot[kWarps];
-    const int m = blockIdx.x;
-    const double *w = base.w + m * vstride;
-    double *invD = base.invD + m * vstride;
-    double *scal = base.scal + m * 8;
-    const double eL = scal[1];
-    // prefix: scan of w shifted by one (element r holds w_{r-1}) = exclusive prefix L_r, kept in invD
-    double carry = 0.0;
-    for (int t0 = 0; t0 < N; t0 += kTile) {
-        double v[kEPT];
-        const int e0 = t0 + threadIdx.x * kEPT;
+    const double f0[EPT] = {f[0], f[1], f[2], f[3]};
+    const double b0[EPT] = {bk[0], bk[1], bk[2], bk[3]};
 #pragma unroll
-        for (int i = 0; i < kEPT; ++i) {
-            const int e = e0 + i;
-            v[i] = (e >= 1 && e < N) ? w[e - 1] : 0.0;
+    for (int i = 1; i < EPT; ++i) { f[i] += f[i - 1]; bk[i] += bk[i - 1]; }
+    double xf = f[EPT - 1], xb = bk[EPT - 1];
+    const double tf = xf, tb = xb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double yf = __shfl_up_sync(0xffffffffu, xf, o);
+        const double yb = __shfl_up_sync(0xffffffffu, xb, o);
+        if (lane >= o) { xf += yf; xb += yb; }
+    }
+    if (lane == 31) { wt_f[warp] = xf; wt_b[warp] = xb; }
+    __syncthreads();
+    if (warp == 0) {
+        double sf = wt_f[lane], sb = wt_b[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double yf = __shfl_up_sync(0xffffffffu, sf, o);
+            const double yb = __shfl_up_sync(0xffffffffu, sb, o);
+            if (lane >= o) { sf += yf; sb += yb; }
         }
-        const double tot = block_scan_tile(v, warp_tot, carry);
-#pragma unroll
-        for (int i = 0; i < kEPT; ++i)
-            if (e0 + i < N) invD[e0 + i] = v[i];
-        carry += tot;
+        wt_f[lane] = sf;
+        wt_b[lane] = sb;
     }
     __syncthreads();
-    // suffix: scan of the reversed sequence, element e holds w_{N-1-e}
-    carry = 0.0;
-    int bad = 0;
-    for (int t0 = 0; t0 < N; t0 += kTile) {
-        double v[kEPT];
-        const int e0 = t0 + threadIdx.x * kEPT;
+    const double exf = (xf - tf) + (warp > 0 ? wt_f[warp - 1] : 0.0);
+    const double exb = (xb - tb) + (warp > 0 ? wt_b[warp - 1] : 0.0);
 #pragma unroll
-        for (int i = 0; i < kEPT; ++i) {
-            const int e = e0 + i;
-            v[i] = e < N ? w[N - 1 - e] : 0.0;
+    for (int i = 0; i < EPT; ++i) {
+        const int e = e0 + i;
+        if (e < n) {
+            if (pre) pre[e] = exf + (f[i] - f0[i]);              // exclusive prefix
+            if (suf) suf[n - 1 - e] = exb + (bk[i] - b0[i]);     // exclusive suffix
         }
-        const double tot = block_scan_tile(v, warp_tot, carry);
-#pragma unroll
-        for (int i = 0; i < kEPT; ++i) {
-            const int e = e0 + i;
-            if (e < N) {
-                const int r = N - 1 - e;
-                const double D = v[i] + eL * invD[r];   // U_r + e^{-Lambda} L_r
-                bad |= !(D > 0.0 && isfinite(D));
-                invD[r] = 1.0 / D;
-            }
-        }
-        carry += tot;
     }
-    bad = __syncthreads_or(bad);
-    if (threadIdx.x == 0) scal[2] = bad ? 1.0 : 0.0;
+    return wt_f[31];
 }
 
-// (E) pointwise: invZ_r = e^{-F_r} / D_r (row normaliser of the exp form).
-__global__ void __launch_bounds__(256) k_vec_invz(int N, VecPtrs base, int64_t vstride) {
-    const int m = blockIdx.y;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < N) base.invZ[m * vstride + j] = base.invD[m * vstride + j] * exp(-base.F[m * vstride + j]);
+__device__ __forceinline__ double *tile_row(const VecPtrs &b, int M, int which, int m) {
+    return b.tiles + ((size_t)which * M + m) * b.ntile;
+}
+
+// (A) masses + lambda; tile-local inclusive scan of the masses -> F (local), tile total.
+__global__ void __launch_bounds__(kT) k_vec_a(const FluxDev *__restrict__ fluxes, int N, int M, VecPtrs b,
+                                              int64_t vstride) {
+    __shared__ double warp_tot[kT / 32];
+    const int m = blockIdx.y, tile = blockIdx.x;
+    const FluxDev &f = fluxes[m];
+    const int e0 = tile * kScanTile + threadIdx.x * kE;
+    double v[kE];
+#pragma unroll
+    for (int i = 0; i < kE; ++i) {
+        const int e = e0 + i;
+        if (e <= N) {
+            const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
+            const double hi = e == N ? f.t_r : bin_centre(f, e);
+            v[i] = flux_mass(f, lo, hi);
+        } else {
+            v[i] = 0.0;
+        }
+    }
+    const double tot = tile_scan(v, warp_tot);
+    double *F = b.F + m * vstride, *lam = b.lam + m * vstride;
+#pragma unroll
+    for (int i = 0; i < kE; ++i) {
+        const int e = e0 + i;
+        if (e < N) {
+            F[e] = v[i];
+            lam[e] = flux_rate(f, bin_centre(f, e));
+        }
+    }
+    if (threadIdx.x == 0) tile_row(b, M, 0, m)[tile] = tot;
+}
+
+// (B) exclusive scan of the mass tile totals -> tile offsets; Lambda = the total; e^{-Lambda}.
+__global__ void __launch_bounds__(1024) k_vec_b(int M, int nt, VecPtrs b) {
+    const int m = blockIdx.x;
+    const double Lam = totals_scan(tile_row(b, M, 0, m), nt, tile_row(b, M, 1, m), nullptr);
+    if (threadIdx.x == 0) {
+        b.scal[m * 8 + 0] = Lam;
+        b.scal[m * 8 + 1] = exp(-Lam);
+        b.scal[m * 8 + 2] = 0.0;
+    }
+}
+
+// (C) F = local + offset; w = lambda e^{-F}; tile-local exclusive prefix of w (into invD, temp)
+// and inclusive suffix of w (into invZ, temp); tile total of w.
+__global__ void __launch_bounds__(kT) k_vec_c(int N, int M, VecPtrs b, int64_t vstride) {
+    __shared__ double warp_tot[kT / 32];
+    __shared__ double rev[kScanTile];
+    const int m = blockIdx.y, tile = blockIdx.x;
+    const double off = tile_row(b, M, 1, m)[tile];
+    double *F = b.F + m * vstride, *lam = b.lam + m * vstride, *w = b.w + m * vstride;
+    double *Lt = b.invD + m * vstride, *Ut = b.invZ + m * vstride;
+    const int e0 = tile * kScanTile + threadIdx.x * kE;
+    double wv[kE], pf[kE], sf[kE];
+#pragma unroll
+    for (int i = 0; i < kE; ++i) {
+        const int e = e0 + i;
+        if (e < N) {
+            const double Fe = F[e] + off;
+            F[e] = Fe;
+            wv[i] = lam[e] * exp(-Fe);
+            w[e] = wv[i];
+        } else {
+            wv[i] = 0.0;
+        }
+        pf[i] = wv[i];
+        rev[threadIdx.x * kE + i] = wv[i];
+    }
+    const double tot = tile_scan(pf, warp_tot);   // (its barriers also publish rev[])
+#pragma unroll
+    for (int i = 0; i < kE; ++i) {
+        const int e = e0 + i;
+        if (e < N) Lt[e] = pf[i] - wv[i];          // exclusive prefix within the tile
+    }
+    // inclusive suffix within the tile = inclusive scan of the reversed tile
+#pragma unroll
+    for (int i = 0; i < kE; ++i) sf[i] = rev[kScanTile - 1 - (threadIdx.x * kE + i)];
+    tile_scan(sf, warp_tot);
+#pragma unroll
+    for (int i = 0; i < kE; ++i) {
+        const int e = tile * kScanTile + kScanTile - 1 - (threadIdx.x * kE + i);
+        if (e < N) Ut[e] = sf[i];
+    }
+    if (threadIdx.x == 0) tile_row(b, M, 2, m)[tile] = tot;
+}
+
+// (D) exclusive prefix and suffix of the w tile totals.
+__global__ void __launch_bounds__(1024) k_vec_d(int M, int nt, VecPtrs b) {
+    const int m = blockIdx.x;
+    totals_scan(tile_row(b, M, 2, m), nt, tile_row(b, M, 3, m), tile_row(b, M, 4, m));
+}
+
+// (E) L_r, U_r, D_r = U_r + e^{-Lambda} L_r, 1/D_r, 1/Z_r; flags a non-positive / non-finite D_r.
+__global__ void __launch_bounds__(kT) k_vec_e(int N, int M, VecPtrs b, int64_t vstride) {
+    const int m = blockIdx.y, tile = blockIdx.x;
+    const double lpre = tile_row(b, M, 3, m)[tile];
+    const double usuf = tile_row(b, M, 4, m)[tile];
+    const double eL = b.scal[m * 8 + 1];
+    const double *F = b.F + m * vstride;
+    double *invD = b.invD + m * vstride, *invZ = b.invZ + m * vstride;
+    int bad = 0;
+    const int e0 = tile * kScanTile + threadIdx.x * kE;
+#pragma unroll
+    for (int i = 0; i < kE; ++i) {
+        const int r = e0 + i;
+        if (r < N) {
+            const double L = invD[r] + lpre;
+            const double U = invZ[r] + usuf;
+            const double D = U + eL * L;
+            bad |= !(D > 0.0 && isfinite(D));
+            const double id = 1.0 / D;
+            invD[r] = id;
+            invZ[r] = id * exp(-F[r]);
+        }
+    }
+    if (bad) b.scal[m * 8 + 2] = 1.0;
 }
 
 }  // namespace
 
 cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs base, int64_t vstride,
                                 cudaStream_t s) {
-    const dim3 gp((N + 1 + 255) / 256, M), gv((N + 255) / 256, M);
-    k_vec_pointwise<<<gp, 256, 0, s>>>(d_flux, N, base, vstride);
-    k_vec_scan_F<<<M, kThreads, 0, s>>>(N, base, vstride);
-    k_vec_w<<<gv, 256, 0, s>>>(N, base, vstride);
-    k_vec_scan_D<<<M, kThreads, 0, s>>>(N, base, vstride);
-    k_vec_invz<<<gv, 256, 0, s>>>(N, base, vstride);
+    const int nt = base.ntile;                         // tiles over the N + 1 masses
+    const int ntN = (N + kScanTile - 1) / kScanTile;   // tiles over the N bins
+    if (nt > 4096) return cudaErrorInvalidValue;
+    k_vec_a<<<dim3(nt, M), kT, 0, s>>>(d_flux, N, M, base, vstride);
+    k_vec_b<<<M, 1024, 0, s>>>(M, nt, base);
+    k_vec_c<<<dim3(ntN, M), kT, 0, s>>>(N, M, base, vstride);
+    k_vec_d<<<M, 1024, 0, s>>>(M, ntN, base);
+    k_vec_e<<<dim3(ntN, M), kT, 0, s>>>(N, M, base, vstride);
     return cudaGetLastError();
 }
 

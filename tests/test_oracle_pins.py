@@ -337,3 +337,15 @@ def test_p10_mc_vs_chain(oracle_lib, td):
     assert np.all(np.abs(m - aggs[1]) <= 4.0 * se + 2.0 * bias)
     # and the dead-time distortion is real: the MC is far from the undistorted f_a
     assert np.max(np.abs(m - _bin_integrated_fa(f, 16))) > 20 * np.max(se)
+
+
+# ------------------------------------------------------------ regression fixture (not a pin)
+def test_golden_config1_regression(oracle_lib):
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config1_oracle.json")))
+    it = config(1).items[0]
+    P = oracle.build_eq4(it.flux, it.t_d)
+    for r, row in g["rows"].items():
+        assert np.max(np.abs(P[int(r)] - np.array(row))) <= 1e-15
+    assert np.sum(np.abs(oracle.stationary_dense(P) - np.array(g["pi"]))) <= 1e-14
