@@ -6,8 +6,8 @@ prefix sums, base matrix P~0 written to HBM) and step 3-4 (dead time folded into
 power iteration to L1 change < 1e-12 on the device) for every item of the workload.
 
 Default workload: BASELINE.json configs[4] ("c5"): N = 32768, t_r = 200 ns, two returns, fp64;
-one P~0, the t_d = 430 ns solve plus the 16-value dead-time sweep on the same P~0 (multi-vector GEMV)
-= 17 stationary solves per step. --workload c1..c5 selects another config (c2, c3: batched items).
+one P~0, the 16-value dead-time sweep plus the t_d = 430 ns solve on the same P~0, all 17 in one
+multi-vector GEMV plan (each dead time its own gathered vector, Thm 2) = 17 stationary solves per step. --workload c1..c5 selects another config (c2, c3: batched items).
 
 Metric (BASELINE.json): stationary solves/s (value, whole job), with transition-matrix entries/s,
 and the fraction of the HBM roofline of the dominant kernel (the power-iteration GEMV) and of the
@@ -72,7 +72,7 @@ def workload_items(name, rank=0, world=1):
     if k == 5:
         f = w.items[0].flux
         sweep = [float(t) for t in np.linspace(10.0, 500.0, 16 * world)]
-        groups = [(f, [w.items[0].t_d]), (f, shard(sweep, rank, world))]
+        groups = [(f, shard(sweep, rank, world) + [w.items[0].t_d])]   # 17 dead times, one P~0, one plan
     else:
         groups = [(it.flux, [it.t_d]) for it in w.items]
     return w, groups
@@ -144,11 +144,11 @@ class OurStep:
         self.P0 = spl.empty_matrix(self.N, self.dt, n_matrices=M)
         self.ws_build = spl.workspace(self.N, M, 1)
         self.plans = []
-        if len(groups) == M:     # one dead time per matrix (c1-c4): one plan over all M matrices
-            assert all(len(t) == 1 for _, t in groups)
+        if len(groups) == M and all(len(t) == 1 for _, t in groups):
+            # one dead time per matrix (c1-c4): one plan over all M matrices
             tds = np.array([[t[0]] for _, t in groups])
             self.plans.append(spl.Plan(self.P0, fl[0].t_r, tds, tol=1e-12))
-        else:                    # c5: several dead-time groups on one matrix
+        else:                    # c5: dead-time groups sharing a matrix, one multi-vector plan each
             for f, tds in groups:
                 m = fl.index(f)
                 self.plans.append(spl.Plan(self.P0[m], f.t_r, np.array([tds]), tol=1e-12))
@@ -274,18 +274,17 @@ def run_e2e(args, w, groups, st, world):
 
     def one():
         row = 0
-        if len(groups) == len(st.fluxes):
-            st.build()
+        st.build()
+        if len(groups) == len(st.fluxes) and all(len(t) == 1 for _, t in groups):
             T = np.array([[t[0]] for _, t in groups])
-            plan = spl.Plan(st.P0, groups[0][0].t_r, T, tol=1e-12, ws=None)
+            plan = spl.Plan(st.P0, groups[0][0].t_r, T, tol=1e-12)
             plan.execute()
-            pi_host[row:row + plan.M].copy_(plan.pi[:, 0], non_blocking=True)
+            pi_host[0:plan.M].copy_(plan.pi[:, 0], non_blocking=True)
             torch.cuda.current_stream().synchronize()
             plan.close()
         else:
-            st.build()
             for f, tds in groups:
-                plan = spl.Plan(st.P0[0], f.t_r, np.array([tds]), tol=1e-12)
+                plan = spl.Plan(st.P0[st.fluxes.index(f)], f.t_r, np.array([tds]), tol=1e-12)
                 plan.execute()
                 pi_host[row:row + len(tds)].copy_(plan.pi[0], non_blocking=True)
                 row += len(tds)

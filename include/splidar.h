@@ -95,7 +95,7 @@ typedef struct {
 splidar_status splidar_shift(double t_r, int32_t n_bins, double t_d, int32_t *l_out);
 
 /* Device workspace (bytes) for n_matrices base matrices of N bins solved with up to n_vectors
- * dead times each (n_vectors <= 16). Any workspace at least this large, 256-byte aligned, may
+ * dead times each (n_vectors <= 32). Any workspace at least this large, 256-byte aligned, may
  * be passed to every entry point below with the same or smaller sizes. */
 size_t splidar_workspace_bytes(int32_t n_bins, int32_t n_matrices, int32_t n_vectors);
 
@@ -141,7 +141,7 @@ splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, sp
  * item m has pulses (shape.tau, shape.sigma, S[m] * shape.signal[k]) and background B[m], dead time
  * t_d[m]; shape.signal are relative weights and shape.background is ignored. Items with equal
  * (S, B) share one P~0 (built once, solved with one multi-vector GEMV for all their dead times,
- * up to 16 per pass). P0_store: device, room for n_store matrices of N x ld (dtype dt) with
+ * up to 32 per pass). P0_store: device, room for n_store matrices of N x ld (dtype dt) with
  * consecutive stride N * ld; unique (S, B) pairs are processed n_store at a time.
  * pi: device fp64 [n_items * N] (item-major). info: host [n_items], may be NULL.
  * Returns SPLIDAR_ENOCONV if any item did not converge (its pi is the last iterate). */

@@ -14,10 +14,14 @@ namespace spl {
 
 static inline size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// Vector counts with a compiled GEMV: 1, 2, 4, 8, 16, 17, 18, 24, 32.
 int pad_vectors(int V) {
-    int p = 1;
-    while (p < V) p <<= 1;
-    return p;
+    if (V <= 2) return V < 1 ? 1 : V;
+    if (V <= 4) return 4;
+    if (V <= 8) return 8;
+    if (V <= 16) return 16;
+    if (V <= 18) return V;   // 16 on tensor cores + 1-2 on DFMA
+    return V <= 24 ? 24 : 32;
 }
 
 WsLayout ws_layout(int N, int M, int V) {
@@ -28,7 +32,7 @@ WsLayout ws_layout(int N, int M, int V) {
     L.V = pad_vectors(V);
     L.strips = (N + kStripCols - 1) / kStripCols;
     L.chunks = (N + kCheckChunk - 1) / kCheckChunk;
-    L.xstride = L.V < 2 ? 2 : L.V;
+    L.xstride = L.V < 2 ? 2 : (L.V + 1) / 2 * 2;
     L.pieces = kGemvCtas + M * L.strips;     // a CTA's k-th piece of strip g uses slot cta + g
     const size_t MV = (size_t)M * L.V;
     size_t o = 0;

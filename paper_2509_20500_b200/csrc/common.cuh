@@ -10,11 +10,11 @@
 namespace spl {
 
 constexpr int kMaxPulses = SPLIDAR_MAX_PULSES;
-constexpr int kMaxVectors = 16;      // dead times per matrix in one multi-vector GEMV pass
+constexpr int kMaxVectors = 32;      // dead times per matrix in one multi-vector GEMV pass
 constexpr int kStripCols = 512;      // columns per GEMV / build CTA (4 KB of an fp64 row)
 constexpr int kNumSMs = 148;
 constexpr int kCheckChunk = 2048;   // elements per CTA of the convergence-check kernel
-constexpr int kGemvCtas = 2 * kNumSMs;  // persistent GEMV grid: two 256-thread CTAs per SM
+constexpr int kGemvCtas = 2 * kNumSMs;  // largest persistent GEMV grid (two 256-thread CTAs per SM)
 constexpr int kMinRowsPerCta = 64;      // smallest row range a GEMV CTA is given
 
 // theta without t_d, device copy. Eq. 1 with K pulses.

@@ -24,7 +24,6 @@
 namespace spl {
 namespace {
 
-constexpr int kStages = 3;
 constexpr int kThreads = 256;           // 2 columns per thread across a 512-column strip
 
 // RS rows per stage; SROW = shared-memory row stride in elements (512 + pad, 16-byte multiple) so that
@@ -139,57 +138,94 @@ __device__ __forceinline__ void stage_fma_active(int na, double (&acc)[NV][2], c
     }
 }
 
-// DMMA (FP64 tensor core, mma.sync) form of a stage for MT = 16 or 8 vectors: per warp, the
-// 64-column slice [64 w, 64 w + 64) as 8 n-tiles; D[v][col] += sum_k X[k][v] P[k][col] with
-// A = X^T (MT x 4), B = P rows (4 x 8), D in registers: acc[nt][q] holds
-// (v, col) = (g + 8 (q >> 1), 64 w + 8 nt + 2 t + (q & 1)), g = lane / 4, t = lane % 4.
+// DMMA (FP64 tensor core, mma.sync) form of a stage for NV = 8, 16, 24, 32 vectors held as NV/8
+// groups of 8. Per warp, the 64-column slice [64 w, 64 w + 64) as 8 n-tiles of 8 columns;
+// D[v][col] += sum_k X[k][v] P[k][col] with A = X^T, B = 4 rows of P (4 x 8), D in registers:
+// acc[q][nt][e] = D[8 q + g][64 w + 8 nt + 2 t + e] (g = lane / 4, t = lane % 4). A pair of active
+// groups is one m16n8k4; a single active group is one m8n8k4; a converged group costs nothing.
 // Rows k >= nr of a partial stage are zeroed in both operands (stale shared memory may hold NaN).
-template <typename T, int MT, int RS>
-__device__ __forceinline__ void stage_mma(double (&acc)[8][MT / 4], const T *seg, const double *xs, int nr,
-                                          int lane, int warp) {
+// One n-tile for vector groups Q, Q+1 of the compile-time running mask GM: one m16n8k4 when both
+// run, one m8n8k4 when one does, nothing when neither does; then the next pair.
+template <int NG, int Q, unsigned GM>
+__device__ __forceinline__ void mma_groups(double (&acc)[NG][8][2], const double (&a)[NG], double bv, int nt) {
+    if constexpr (Q < NG) {
+        constexpr bool lo = (GM >> Q) & 1u;
+        constexpr bool hi = Q + 1 < NG && ((GM >> (Q + 1)) & 1u);
+        if constexpr (lo && hi) {
+            asm volatile(
+                "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                : "+d"(acc[Q][nt][0]), "+d"(acc[Q][nt][1]), "+d"(acc[Q + 1][nt][0]), "+d"(acc[Q + 1][nt][1])
+                : "d"(a[Q]), "d"(a[Q + 1]), "d"(bv));
+        } else if constexpr (lo) {
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[Q][nt][0]), "+d"(acc[Q][nt][1])
+                         : "d"(a[Q]), "d"(bv));
+        } else if constexpr (hi) {
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[Q + 1][nt][0]), "+d"(acc[Q + 1][nt][1])
+                         : "d"(a[Q + 1]), "d"(bv));
+        }
+        mma_groups<NG, Q + 2, GM>(acc, a, bv, nt);
+    }
+}
+
+template <typename T, int NV, int RS, int XST, unsigned GM>
+__device__ __forceinline__ void stage_mma_fixed(double (&acc)[NV / 8][8][2], const T *seg, const double *xs, int nr,
+                                                int lane, int warp) {
     constexpr int SROW = GemvCfg<T>::SROW;
+    constexpr int NG = NV / 8;
     const int g = lane >> 2, t = lane & 3;
     const T *sb = seg + warp * 64 + g;
 #pragma unroll
     for (int kb = 0; kb < RS; kb += 4) {
         const int k = kb + t;
         const bool kin = k < nr;
-        const double a0 = kin ? xs[k * MT + g] : 0.0;
-        double a1 = 0.0;
-        if constexpr (MT == 16) a1 = kin ? xs[k * MT + g + 8] : 0.0;
+        double a[NG];                                   // A fragments: X[k][8 q + g]
+#pragma unroll
+        for (int q = 0; q < NG; ++q) a[q] = (kin && ((GM >> q) & 1u)) ? xs[k * XST + q * 8 + g] : 0.0;
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt) {
             const double bv = kin ? (double)sb[k * SROW + nt * 8] : 0.0;
-            if constexpr (MT == 16) {
-                asm volatile(
-                    "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
-                    : "+d"(acc[nt][0]), "+d"(acc[nt][1]), "+d"(acc[nt][2]), "+d"(acc[nt][3])
-                    : "d"(a0), "d"(a1), "d"(bv));
-            } else {
-                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                             : "+d"(acc[nt][0]), "+d"(acc[nt][1])
-                             : "d"(a0), "d"(bv));
-            }
+            mma_groups<NG, 0, GM>(acc, a, bv, nt);
         }
+    }
+}
+
+// Runtime running-group mask -> the compile-time specialisation (2^NG - 1 cases; uniform branch).
+template <typename T, int NV, int RS, int XST, unsigned GM = 1>
+__device__ __forceinline__ void stage_mma(double (&acc)[NV / 8][8][2], const T *seg, const double *xs, int nr,
+                                          int lane, int warp, unsigned gmask) {
+    if constexpr (GM < (1u << (NV / 8))) {
+        if (gmask == GM) stage_mma_fixed<T, NV, RS, XST, GM>(acc, seg, xs, nr, lane, warp);
+        else stage_mma<T, NV, RS, XST, GM + 1>(acc, seg, xs, nr, lane, warp, gmask);
     }
 }
 
 template <typename T, int NV>
 struct StepSmem {
+    // DMMA path for NV >= 8: NVM = the multiple of 8 on FP64 tensor cores, NVF = 0..2 leftover
+    // vectors on plain DFMA (so 17 dead times cost 17 FMAs per entry, not 24)
+    static constexpr int NVM = NV >= 8 ? NV / 8 * 8 : 0;
+    static constexpr int NVF = NV - NVM;
+    static constexpr bool MMA = NVM > 0;
+    // up to 16 vectors: 2 CTAs per SM with a 3-stage ring; 24 / 32 vectors need the registers of one
+    // CTA per SM, which gets a 5-stage ring instead
+    static constexpr int STAGES = NV >= 32 ? 5 : 3;
+    static constexpr int MINB = NV >= 32 ? 1 : 2;
     static constexpr int RS = GemvCfg<T>::RS;
-    static constexpr int XST = NV < 2 ? 2 : NV;                         // == PowerArgs::xstride
+    static constexpr int XST = NV < 2 ? 2 : (NV + 1) / 2 * 2;           // == PowerArgs::xstride (16-B rows)
     static constexpr int SROW = GemvCfg<T>::SROW;
     static constexpr size_t SEG = (size_t)RS * SROW * sizeof(T);        // matrix bytes per stage
     static constexpr size_t XB = (size_t)RS * XST * sizeof(double);     // x bytes per stage
-    static constexpr bool MMA = NV >= 8;                                 // DMMA path for 8 / 16 vectors
     static constexpr size_t XC = (NV >= 4 && !MMA) ? (size_t)2 * RS * NV * sizeof(double) : 0;
-    static constexpr size_t BYTES = kStages * (SEG + XB) + XC + kStages * sizeof(uint64_t);
+    static constexpr size_t BYTES = STAGES * (SEG + XB) + XC + STAGES * sizeof(uint64_t);
 };
 
 template <typename T, int NV>
-__global__ void __launch_bounds__(kThreads, 2) k_power_step(const PowerArgs a) {
+__global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(const PowerArgs a) {
     using SM = StepSmem<T, NV>;
     constexpr int RS = SM::RS;
+    constexpr int kStages = SM::STAGES;
     constexpr int NWARPS = kThreads / 32;
     extern __shared__ __align__(128) unsigned char smem[];
     T *segs = reinterpret_cast<T *>(smem);                                             // [S][RS][512]
@@ -197,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_power_step(const PowerArgs a) {
     double *xcmp = reinterpret_cast<double *>(smem + kStages * (SM::SEG + SM::XB));    // [2][RS][NV]
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * (SM::SEG + SM::XB) + SM::XC);
     __shared__ int s_vmap[NV], s_cur[NV], s_nact, s_last;
+    __shared__ unsigned s_gmask;
     __shared__ double red_sum[NWARPS][NV];
 
     const int tid = threadIdx.x, b = blockIdx.x, G = gridDim.x;
@@ -231,14 +268,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_power_step(const PowerArgs a) {
         // running vectors of matrix m, compacted into slots
         if (tid == 0) {
             int n = 0;
+            unsigned gm = 0;
             for (int v = 0; v < NV; ++v) {
                 const SolveState s = a.st[(size_t)m * NV + v];
-                if (!s.done) { s_vmap[n] = v; s_cur[n] = s.cur; ++n; }
+                if (!s.done) {
+                    s_vmap[n] = v; s_cur[n] = s.cur; ++n;
+                    gm |= (SM::MMA && v >= SM::NVM) ? (1u << (16 + v - SM::NVM)) : (1u << (v >> 3));
+                }
             }
             s_nact = n;
+            s_gmask = gm;
         }
         __syncthreads();
         const int nact = s_nact;
+        const unsigned gmask = s_gmask & 0xffffu;   // running 8-vector MMA groups
+        const unsigned fmask = s_gmask >> 16;       // running DFMA leftover vectors (NVM + i)
         const int na_r = NV >= 4 ? ((nact + 3) & ~3) : NV;
 
         const int cols = min(kStripCols, N - c * kStripCols);
@@ -264,13 +308,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_power_step(const PowerArgs a) {
         else
             q_issue += min(kStages - 1, nstages);
 
-        constexpr int NACC = SM::MMA ? 8 : NV;          // MMA: 8 n-tiles x NV/4 values; else NV x 2
-        constexpr int QACC = SM::MMA ? NV / 4 : 2;
-        double acc[NACC][QACC];
+        // MMA path: accm[group][n-tile][2]; FMA path: acc[vector slot][2] (the other one is unused)
+        constexpr int NG = SM::MMA ? SM::NVM / 8 : 1;
+        constexpr int NF = SM::MMA ? (SM::NVF > 0 ? SM::NVF : 1) : NV;
+        double accm[NG][8][2];
+        double acc[NF][2];   // FMA path: one per vector slot; MMA path: the DFMA leftover vectors
 #pragma unroll
-        for (int i = 0; i < NACC; ++i)
+        for (int q = 0; q < NG; ++q)
 #pragma unroll
-            for (int q = 0; q < QACC; ++q) acc[i][q] = 0.0;
+            for (int i = 0; i < 8; ++i) accm[q][i][0] = accm[q][i][1] = 0.0;
+#pragma unroll
+        for (int v = 0; v < NF; ++v) acc[v][0] = acc[v][1] = 0.0;
 
         for (int k = 0; k < nstages; ++k) {
             const int buf = q_cons % kStages;
@@ -299,7 +347,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_power_step(const PowerArgs a) {
             const T *segb = segs + (size_t)buf * RS * SM::SROW;
             if constexpr (SM::MMA) {
                 (void)xst;
-                stage_mma<T, NV, RS>(acc, segb, xs, nr, tid & 31, tid >> 5);
+                stage_mma<T, SM::NVM, RS, SM::XST>(accm, segb, xs, nr, tid & 31, tid >> 5, gmask);
+                if constexpr (SM::NVF > 0) {
+                    if (fmask && 2 * tid < cols) {
+                        for (int rr = 0; rr < nr; ++rr) {
+                            double p0, p1;
+                            lds2<T>(segb + rr * SM::SROW + 2 * tid, p0, p1);
+#pragma unroll
+                            for (int i = 0; i < SM::NVF; ++i) {
+                                const double x = xs[rr * SM::XST + SM::NVM + i];
+                                acc[i][0] = fma(x, p0, acc[i][0]);
+                                acc[i][1] = fma(x, p1, acc[i][1]);
+                            }
+                        }
+                    }
+                }
             } else {
                 if (2 * tid < cols) stage_fma_active<T, NV, RS>(na_r, acc, segb, xs, xst, nr, tid);
             }
@@ -312,15 +374,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_power_step(const PowerArgs a) {
         const int last = (int)((gN + N - 1) / U);
         double *part = a.part + (size_t)(b + g) * NV * kStripCols;
         if constexpr (SM::MMA) {
-            // all NV rows of D (converged vectors are never read back)
+            // rows of D of the running groups (converged vectors are never read back)
             const int lane = tid & 31, w = tid >> 5, gq = lane >> 2, tq = lane & 3;
 #pragma unroll
-            for (int nt = 0; nt < 8; ++nt) {
-                const int col = w * 64 + nt * 8 + 2 * tq;
+            for (int q = 0; q < NG; ++q) {
+                if (!((gmask >> q) & 1u)) continue;
 #pragma unroll
-                for (int h = 0; h < NV / 8; ++h)
-                    *reinterpret_cast<double2 *>(part + (size_t)(gq + 8 * h) * kStripCols + col) =
-                        make_double2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+                for (int nt = 0; nt < 8; ++nt)
+                    *reinterpret_cast<double2 *>(part + (size_t)(q * 8 + gq) * kStripCols + w * 64 + nt * 8 + 2 * tq) =
+                        make_double2(accm[q][nt][0], accm[q][nt][1]);
+            }
+            if constexpr (SM::NVF > 0) {
+                if (2 * tid < cols) {
+#pragma unroll
+                    for (int i = 0; i < SM::NVF; ++i)
+                        if ((fmask >> i) & 1u)
+                            *reinterpret_cast<double2 *>(part + (size_t)(SM::NVM + i) * kStripCols + 2 * tid) =
+                                make_double2(acc[i][0], acc[i][1]);
+                }
             }
         } else if (2 * tid < cols) {
 #pragma unroll
@@ -523,29 +594,38 @@ __global__ void k_power_finish(const FinishArgs f) {
 }
 
 template <typename T, int NV>
-void *step_entry(size_t *smem) {
+void *step_entry(size_t *smem, int *ctas_per_sm) {
     *smem = StepSmem<T, NV>::BYTES;
+    *ctas_per_sm = StepSmem<T, NV>::MINB;
     void *fn = (void *)k_power_step<T, NV>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
     return fn;
 }
 
-void *step_fn(int dtype, int V, size_t *smem) {
+void *step_fn(int dtype, int V, size_t *smem, int *cps) {
     if (dtype == SPLIDAR_F64) {
         switch (V) {
-            case 1: return step_entry<double, 1>(smem);
-            case 2: return step_entry<double, 2>(smem);
-            case 4: return step_entry<double, 4>(smem);
-            case 8: return step_entry<double, 8>(smem);
-            case 16: return step_entry<double, 16>(smem);
+            case 1: return step_entry<double, 1>(smem, cps);
+            case 2: return step_entry<double, 2>(smem, cps);
+            case 4: return step_entry<double, 4>(smem, cps);
+            case 8: return step_entry<double, 8>(smem, cps);
+            case 16: return step_entry<double, 16>(smem, cps);
+            case 17: return step_entry<double, 17>(smem, cps);
+            case 18: return step_entry<double, 18>(smem, cps);
+            case 24: return step_entry<double, 24>(smem, cps);
+            case 32: return step_entry<double, 32>(smem, cps);
         }
     } else {
         switch (V) {
-            case 1: return step_entry<float, 1>(smem);
-            case 2: return step_entry<float, 2>(smem);
-            case 4: return step_entry<float, 4>(smem);
-            case 8: return step_entry<float, 8>(smem);
-            case 16: return step_entry<float, 16>(smem);
+            case 1: return step_entry<float, 1>(smem, cps);
+            case 2: return step_entry<float, 2>(smem, cps);
+            case 4: return step_entry<float, 4>(smem, cps);
+            case 8: return step_entry<float, 8>(smem, cps);
+            case 16: return step_entry<float, 16>(smem, cps);
+            case 17: return step_entry<float, 17>(smem, cps);
+            case 18: return step_entry<float, 18>(smem, cps);
+            case 24: return step_entry<float, 24>(smem, cps);
+            case 32: return step_entry<float, 32>(smem, cps);
         }
     }
     return nullptr;
@@ -556,7 +636,8 @@ void *step_fn(int dtype, int V, size_t *smem) {
 // Describes the solver kernels (function, grid, block, shared memory) for graph construction.
 int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a) {
     out->init_fn = (void *)k_power_init;
-    out->step_fn = step_fn(dtype, V, &out->step_smem);
+    int cps = 2;
+    out->step_fn = step_fn(dtype, V, &out->step_smem, &cps);
     out->check_fn = (void *)k_power_check;
     out->finish_fn = (void *)k_power_finish;
     if (!out->step_fn) return 1;
@@ -565,7 +646,7 @@ int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a) {
     out->init_block = dim3(256);
     out->finish_grid = dim3(gx, a.M * a.V);
     out->finish_block = dim3(256);
-    out->step_grid = dim3(kGemvCtas);
+    out->step_grid = dim3(kNumSMs * cps);   // persistent: every resident CTA slot, once
     out->step_block = dim3(kThreads);
     out->check_grid = dim3(a.chunks, a.M * a.V);
     out->check_block = dim3(256);

@@ -21,7 +21,7 @@ OK, EINVAL, ENOCONV, EZEROROW, ENOSPACE, ECUDA = range(6)
 F64, F32 = 0, 1
 ENTRY_FACTORED, ENTRY_EXP = 0, 1
 MAX_PULSES = 16
-MAX_VECTORS = 16
+MAX_VECTORS = 32
 
 _DTYPES = {torch.float64: F64, torch.float32: F32}
 _MODES = {"factored": ENTRY_FACTORED, "exp": ENTRY_EXP}

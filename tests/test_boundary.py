@@ -101,9 +101,9 @@ def test_shift_rejects(spl, args):
 def test_workspace_bytes(spl):
     assert spl.workspace_bytes(1, 1, 1) == 0
     assert spl.workspace_bytes(256, 0, 1) == 0
-    assert spl.workspace_bytes(256, 1, 17) == 0
+    assert spl.workspace_bytes(256, 1, 33) == 0
     a = spl.workspace_bytes(32768, 1, 1)
-    b = spl.workspace_bytes(32768, 1, 16)
+    b = spl.workspace_bytes(32768, 1, 32)
     assert 0 < a < b
     assert b < 1 << 30                     # < 1 GiB beside an 8.6 GB matrix
     assert spl.workspace_bytes(4096, 64, 1) > spl.workspace_bytes(4096, 1, 1)

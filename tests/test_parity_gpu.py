@@ -274,12 +274,14 @@ def test_config5_full_f32(spl, mode):
     _full_size_check(spl, it.flux, it.t_d, torch.float32, mode, TOL_E32, TOL_PI32)
 
 
-@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
-def test_config5_deadtime_sweep(spl, dtype):
-    """16 dead times on one P~0 in one multi-vector plan (the a7 sweep), each vs the structured pi."""
+@pytest.mark.parametrize("dtype,extra", [(torch.float64, False), (torch.float32, False), (torch.float64, True),
+                                         (torch.float32, True)])
+def test_config5_deadtime_sweep(spl, dtype, extra):
+    """16 dead times on one P~0 in one multi-vector plan (the a7 sweep), each vs the structured pi;
+    extra=True adds the t_d = 430 solve as a 17th vector (24-vector DMMA path, the bench's step)."""
     w = config(5)
     f = w.items[0].flux
-    tds = [it.t_d for it in w.sweep]
+    tds = [it.t_d for it in w.sweep] + ([w.items[0].t_d] if extra else [])
     P0 = spl.build_base(f, dtype)
     plan = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-12)
     infos = plan.execute(check=dtype == torch.float64)
@@ -312,3 +314,24 @@ def test_tiny_n(spl):
             pi, _ = spl.stationary(P0, f.t_r, td, tol=1e-14)
             want = oracle.stationary_dense(oracle.build_eq4(f, td))
             assert np.sum(np.abs(_np(pi) - want)) <= 1e-12
+
+
+@pytest.mark.parametrize("nv", [3, 8, 9, 12, 17, 18, 24, 30, 32])
+def test_multivector_counts(spl, nv):
+    """Every compiled vector count (1..32 padded to 4/8/16/24/32), ragged N, each vector equal to its
+    single-vector solve and to the oracle."""
+    rng = np.random.default_rng(100 + nv)
+    f = random_flux(rng, 601, 2)
+    tds = [float(x) for x in rng.uniform(0, 3 * f.t_r, nv)]
+    P0 = spl.build_base(f)
+    plan = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-13)
+    infos = plan.execute()
+    for v in range(nv):
+        assert infos[v]["converged"]
+        single, info = spl.stationary(P0, f.t_r, tds[v], tol=1e-13)
+        assert info["iters"] == infos[v]["iters"]
+        assert np.sum(np.abs(_np(plan.pi[0, v]) - _np(single))) <= 1e-13
+    for v in (0, nv - 1):
+        want = oracle.stationary_dense(oracle.build_eq4(f, tds[v]))
+        assert np.sum(np.abs(_np(plan.pi[0, v]) - want)) <= TOL_PI64
+    plan.close()
