@@ -121,23 +121,6 @@ __device__ __forceinline__ void stage_fma(double (&acc)[NV][2], const T *seg, co
     }
 }
 
-template <typename T, int NV, int RS>
-__device__ __forceinline__ void stage_fma_active(int na, double (&acc)[NV][2], const T *seg, const double *xs,
-                                                 int xst, int nr, int tid) {
-    if constexpr (NV <= 2) {
-        stage_fma<T, NV, NV, RS>(acc, seg, xs, xst, nr, tid);
-    } else {
-        if (na <= 4) stage_fma<T, NV, 4, RS>(acc, seg, xs, xst, nr, tid);
-        else if constexpr (NV >= 8) {
-            if (na <= 8) stage_fma<T, NV, 8, RS>(acc, seg, xs, xst, nr, tid);
-            else if constexpr (NV >= 16) {
-                if (na <= 12) stage_fma<T, NV, 12, RS>(acc, seg, xs, xst, nr, tid);
-                else stage_fma<T, NV, 16, RS>(acc, seg, xs, xst, nr, tid);
-            }
-        }
-    }
-}
-
 // DMMA (FP64 tensor core, mma.sync) form of a stage for NV = 8, 16, 24, 32 vectors held as NV/8
 // groups of 8. Per warp, the 64-column slice [64 w, 64 w + 64) as 8 n-tiles of 8 columns;
 // D[v][col] += sum_k X[k][v] P[k][col] with A = X^T, B = 4 rows of P (4 x 8), D in registers:
@@ -169,11 +152,15 @@ __device__ __forceinline__ void mma_groups(double (&acc)[NG][8][2], const double
     }
 }
 
-template <typename T, int NV, int RS, int XST, unsigned GM>
-__device__ __forceinline__ void stage_mma_fixed(double (&acc)[NV / 8][8][2], const T *seg, const double *xs, int nr,
-                                                int lane, int warp) {
+// NVM vectors on tensor cores (groups of 8, running mask GM bits [0, NVM/8)) and NVF <= 2 leftover
+// vectors on DFMA (running mask bits [NVM/8, NVM/8 + NVF)) that reuse the B fragments already in
+// registers: lane (g, t) accumulates x_f[k = t] * P[t][64 w + 8 nt + g] into accf[f][nt]; the 4 t-lanes
+// of a column are added with shuffles when the piece ends.
+template <typename T, int NVM, int NVF, int RS, int XST, unsigned GM>
+__device__ __forceinline__ void stage_mma_fixed(double (&acc)[NVM / 8][8][2], double (&accf)[NVF > 0 ? NVF : 1][8],
+                                                const T *seg, const double *xs, int nr, int lane, int warp) {
     constexpr int SROW = GemvCfg<T>::SROW;
-    constexpr int NG = NV / 8;
+    constexpr int NG = NVM / 8;
     const int g = lane >> 2, t = lane & 3;
     const T *sb = seg + warp * 64 + g;
 #pragma unroll
@@ -183,21 +170,27 @@ __device__ __forceinline__ void stage_mma_fixed(double (&acc)[NV / 8][8][2], con
         double a[NG];                                   // A fragments: X[k][8 q + g]
 #pragma unroll
         for (int q = 0; q < NG; ++q) a[q] = (kin && ((GM >> q) & 1u)) ? xs[k * XST + q * 8 + g] : 0.0;
+        double xf[NVF > 0 ? NVF : 1];
+#pragma unroll
+        for (int f = 0; f < NVF; ++f) xf[f] = kin ? xs[k * XST + NVM + f] : 0.0;
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt) {
             const double bv = kin ? (double)sb[k * SROW + nt * 8] : 0.0;
             mma_groups<NG, 0, GM>(acc, a, bv, nt);
+#pragma unroll
+            for (int f = 0; f < NVF; ++f)
+                if ((GM >> (NG + f)) & 1u) accf[f][nt] = fma(xf[f], bv, accf[f][nt]);
         }
     }
 }
 
-// Runtime running-group mask -> the compile-time specialisation (2^NG - 1 cases; uniform branch).
-template <typename T, int NV, int RS, int XST, unsigned GM = 1>
-__device__ __forceinline__ void stage_mma(double (&acc)[NV / 8][8][2], const T *seg, const double *xs, int nr,
-                                          int lane, int warp, unsigned gmask) {
-    if constexpr (GM < (1u << (NV / 8))) {
-        if (gmask == GM) stage_mma_fixed<T, NV, RS, XST, GM>(acc, seg, xs, nr, lane, warp);
-        else stage_mma<T, NV, RS, XST, GM + 1>(acc, seg, xs, nr, lane, warp, gmask);
+// Runtime running mask -> the compile-time specialisation (2^(NG + NVF) - 1 cases; uniform branch).
+template <typename T, int NVM, int NVF, int RS, int XST, unsigned GM = 1>
+__device__ __forceinline__ void stage_mma(double (&acc)[NVM / 8][8][2], double (&accf)[NVF > 0 ? NVF : 1][8],
+                                          const T *seg, const double *xs, int nr, int lane, int warp, unsigned mask) {
+    if constexpr (GM < (1u << (NVM / 8 + NVF))) {
+        if (mask == GM) stage_mma_fixed<T, NVM, NVF, RS, XST, GM>(acc, accf, seg, xs, nr, lane, warp);
+        else stage_mma<T, NVM, NVF, RS, XST, GM + 1>(acc, accf, seg, xs, nr, lane, warp, mask);
     }
 }
 
@@ -217,8 +210,7 @@ struct StepSmem {
     static constexpr int SROW = GemvCfg<T>::SROW;
     static constexpr size_t SEG = (size_t)RS * SROW * sizeof(T);        // matrix bytes per stage
     static constexpr size_t XB = (size_t)RS * XST * sizeof(double);     // x bytes per stage
-    static constexpr size_t XC = (NV >= 4 && !MMA) ? (size_t)2 * RS * NV * sizeof(double) : 0;
-    static constexpr size_t BYTES = STAGES * (SEG + XB) + XC + STAGES * sizeof(uint64_t);
+    static constexpr size_t BYTES = STAGES * (SEG + XB) + STAGES * sizeof(uint64_t);
 };
 
 template <typename T, int NV>
@@ -230,10 +222,9 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
     extern __shared__ __align__(128) unsigned char smem[];
     T *segs = reinterpret_cast<T *>(smem);                                             // [S][RS][512]
     double *xbuf = reinterpret_cast<double *>(smem + kStages * SM::SEG);               // [S][RS][XST]
-    double *xcmp = reinterpret_cast<double *>(smem + kStages * (SM::SEG + SM::XB));    // [2][RS][NV]
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * (SM::SEG + SM::XB) + SM::XC);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * (SM::SEG + SM::XB));   // TMA landed
     __shared__ int s_vmap[NV], s_cur[NV], s_nact, s_last;
-    __shared__ unsigned s_gmask;
+    __shared__ unsigned s_gmask, s_vmask;
     __shared__ double red_sum[NWARPS][NV];
 
     const int tid = threadIdx.x, b = blockIdx.x, G = gridDim.x;
@@ -248,7 +239,9 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
     const int64_t u_end = u_begin + U < T_units ? u_begin + U : T_units;
 
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -268,22 +261,24 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
         // running vectors of matrix m, compacted into slots
         if (tid == 0) {
             int n = 0;
-            unsigned gm = 0;
+            unsigned gm = 0, vm = 0;
             for (int v = 0; v < NV; ++v) {
                 const SolveState s = a.st[(size_t)m * NV + v];
                 if (!s.done) {
                     s_vmap[n] = v; s_cur[n] = s.cur; ++n;
-                    gm |= (SM::MMA && v >= SM::NVM) ? (1u << (16 + v - SM::NVM)) : (1u << (v >> 3));
+                    vm |= 1u << v;
+                    // MMA groups of 8 in bits [0, NVM/8), DFMA leftovers in the bits after them
+                    gm |= (SM::MMA && v >= SM::NVM) ? (1u << (SM::NVM / 8 + v - SM::NVM)) : (1u << (v >> 3));
                 }
             }
             s_nact = n;
             s_gmask = gm;
+            s_vmask = vm;
         }
         __syncthreads();
         const int nact = s_nact;
-        const unsigned gmask = s_gmask & 0xffffu;   // running 8-vector MMA groups
-        const unsigned fmask = s_gmask >> 16;       // running DFMA leftover vectors (NVM + i)
-        const int na_r = NV >= 4 ? ((nact + 3) & ~3) : NV;
+        const unsigned gmask = s_gmask;             // running MMA groups + DFMA leftovers
+        const unsigned vmask = s_vmask;             // running vectors
 
         const int cols = min(kStripCols, N - c * kStripCols);
         const uint32_t seg_bytes = (uint32_t)(((size_t)cols * sizeof(T) + 15) & ~(size_t)15);
@@ -305,65 +300,40 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
         };
         if (tid == 0)
             for (int k = 0; k < kStages - 1 && k < nstages; ++k) issue(k);
-        else
-            q_issue += min(kStages - 1, nstages);
 
-        // MMA path: accm[group][n-tile][2]; FMA path: acc[vector slot][2] (the other one is unused)
+        // MMA path: accm[group][n-tile][2]; FMA path: acc[vector][2]; MMA leftovers: acc[i][2]
         constexpr int NG = SM::MMA ? SM::NVM / 8 : 1;
-        constexpr int NF = SM::MMA ? (SM::NVF > 0 ? SM::NVF : 1) : NV;
+        constexpr int NF = SM::MMA ? 1 : NV;
+        constexpr int NL = SM::NVF > 0 ? SM::NVF : 1;
         double accm[NG][8][2];
-        double acc[NF][2];   // FMA path: one per vector slot; MMA path: the DFMA leftover vectors
+        double accf[NL][8];   // MMA path leftovers: per lane, columns 64 w + 8 nt + g, rows k = t
+        double acc[NF][2];    // FMA path (NV <= 4): vector v, columns 2 tid, 2 tid + 1
 #pragma unroll
         for (int q = 0; q < NG; ++q)
 #pragma unroll
             for (int i = 0; i < 8; ++i) accm[q][i][0] = accm[q][i][1] = 0.0;
 #pragma unroll
         for (int v = 0; v < NF; ++v) acc[v][0] = acc[v][1] = 0.0;
+#pragma unroll
+        for (int f = 0; f < NL; ++f)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) accf[f][i] = 0.0;
 
+        const int lane = tid & 31, warp = tid >> 5;
         for (int k = 0; k < nstages; ++k) {
             const int buf = q_cons % kStages;
             mbar_wait(&full[buf], (q_cons / kStages) & 1);
             const int nr = min(RS, r_hi - (r_lo + k * RS));
-            const double *xs;
-            int xst;
-            if constexpr (NV >= 4 && !SM::MMA) {
-                double *xc = xcmp + (size_t)(k & 1) * RS * NV;
-                for (int i = tid; i < RS * NV; i += kThreads) {
-                    const int rr = i / NV, sl = i % NV;
-                    xc[i] = (sl < nact && rr < nr) ? xbuf[((size_t)buf * RS + rr) * SM::XST + s_vmap[sl]] : 0.0;
-                }
-                xs = xc;
-                xst = NV;
-            } else {
-                xs = xbuf + (size_t)buf * RS * SM::XST;
-                xst = SM::XST;
-            }
-            __syncthreads();   // x compacted; every thread is done with the previous stage's buffer
-            if (tid == 0) {
-                if (k + kStages - 1 < nstages) issue(k + kStages - 1);
-            } else if (k + kStages - 1 < nstages) {
-                ++q_issue;
-            }
+            const double *xs = xbuf + (size_t)buf * RS * SM::XST;
             const T *segb = segs + (size_t)buf * RS * SM::SROW;
+            // every warp is done with stage k - 1: its ring slot takes stage k + S - 1 (measured
+            // faster here than per-warp empty mbarriers: the block barrier keeps warps in step)
+            __syncthreads();
+            if (tid == 0 && k + kStages - 1 < nstages) issue(k + kStages - 1);
             if constexpr (SM::MMA) {
-                (void)xst;
-                stage_mma<T, SM::NVM, RS, SM::XST>(accm, segb, xs, nr, tid & 31, tid >> 5, gmask);
-                if constexpr (SM::NVF > 0) {
-                    if (fmask && 2 * tid < cols) {
-                        for (int rr = 0; rr < nr; ++rr) {
-                            double p0, p1;
-                            lds2<T>(segb + rr * SM::SROW + 2 * tid, p0, p1);
-#pragma unroll
-                            for (int i = 0; i < SM::NVF; ++i) {
-                                const double x = xs[rr * SM::XST + SM::NVM + i];
-                                acc[i][0] = fma(x, p0, acc[i][0]);
-                                acc[i][1] = fma(x, p1, acc[i][1]);
-                            }
-                        }
-                    }
-                }
+                stage_mma<T, SM::NVM, SM::NVF, RS, SM::XST>(accm, accf, segb, xs, nr, lane, warp, gmask);
             } else {
-                if (2 * tid < cols) stage_fma_active<T, NV, RS>(na_r, acc, segb, xs, xst, nr, tid);
+                if (2 * tid < cols) stage_fma<T, NV, NV, RS>(acc, segb, xs, SM::XST, nr, tid);
             }
             ++q_cons;
         }
@@ -385,20 +355,25 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
                         make_double2(accm[q][nt][0], accm[q][nt][1]);
             }
             if constexpr (SM::NVF > 0) {
-                if (2 * tid < cols) {
+                // leftovers: add the 4 k-lanes (t) of each column, lane t = 0 writes
 #pragma unroll
-                    for (int i = 0; i < SM::NVF; ++i)
-                        if ((fmask >> i) & 1u)
-                            *reinterpret_cast<double2 *>(part + (size_t)(SM::NVM + i) * kStripCols + 2 * tid) =
-                                make_double2(acc[i][0], acc[i][1]);
+                for (int f = 0; f < SM::NVF; ++f) {
+                    if (!((gmask >> (SM::NVM / 8 + f)) & 1u)) continue;
+#pragma unroll
+                    for (int nt = 0; nt < 8; ++nt) {
+                        double v = accf[f][nt];
+                        v += __shfl_xor_sync(0xffffffffu, v, 1);
+                        v += __shfl_xor_sync(0xffffffffu, v, 2);
+                        if (tq == 0) part[(size_t)(SM::NVM + f) * kStripCols + w * 64 + nt * 8 + gq] = v;
+                    }
                 }
             }
         } else if (2 * tid < cols) {
 #pragma unroll
-            for (int sl = 0; sl < NV; ++sl)
-                if (sl < nact)
-                    *reinterpret_cast<double2 *>(part + (size_t)s_vmap[sl] * kStripCols + 2 * tid) =
-                        make_double2(acc[sl][0], acc[sl][1]);
+            for (int v = 0; v < NV; ++v)
+                if ((vmask >> v) & 1u)
+                    *reinterpret_cast<double2 *>(part + (size_t)v * kStripCols + 2 * tid) =
+                        make_double2(acc[v][0], acc[v][1]);
         }
         __threadfence();
         __syncthreads();
