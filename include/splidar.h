@@ -168,6 +168,74 @@ splidar_status splidar_plan_launch(splidar_plan plan, void *stream);
 splidar_status splidar_plan_info(splidar_plan plan, splidar_solve_info *info, void *stream);
 void splidar_plan_destroy(splidar_plan plan);
 
+/* ---------------------------------------------------------------------------------------------
+ * Matrix-free (structured) operator: SURVEY §8(f) rows f2 and f1.
+ *
+ * From §3.4 (E_base = exp.(-Lambda L - D); P = (1 lambda^T) . E; row
+ * normalisation P:79) every row of P~0 is the same column profile w_j = lambda_j e^{-F_j}
+ * times a step (e^{-Lambda} below the diagonal, 1 on and above it) over the row normaliser D_r, so
+ *     (x^T P~0)_j = w_j (C_j + e^{-Lambda} (T - C_j)),  C_j = sum_{r<=j} x_r / D_r,  T = C_{N-1}:
+ * one prefix scan per product instead of a pass over N^2 stored entries. The dead time is the same
+ * row permutation (Thm 2), x_r = v[(r - l) mod N]. These entry points never store P~0; they
+ * compute exactly the matrix that splidar_build_base writes (up to rounding), so their results are
+ * compared with the same oracle. N <= 65536 (a cluster of <= 16 CTAs x 4096 bins per item), else
+ * SPLIDAR_EINVAL. Items follow splidar_sweep: item m has pulses (shape.tau, shape.sigma,
+ * S[m] * shape.signal[k]), background B[m], dead time t_d[m]; items with equal (S, B) share their
+ * step-1 vectors. All calls synchronise `stream` once at their end.
+ *
+ * Workspace: splidar_structured_workspace_bytes(N, n_profiles, n_items) bytes, 256-byte aligned
+ * (n_profiles = number of distinct (S, B) pairs; n_items = items, or N for splidar_mixing_steps);
+ * 0 if the sizes are invalid. */
+size_t splidar_structured_workspace_bytes(int32_t n_bins, int32_t n_profiles, int32_t n_items);
+
+/* f2: pi P~ = pi for every item by power iteration on the structured operator, with the same
+ * definition as splidar_stationary (pi^0 = 1/N, 1-norm renormalisation, stop after the first product
+ * with ||pi^{k+1} - pi^k||_1 < tol, or max_iter products -> SPLIDAR_ENOCONV with the last iterate).
+ * pi: device fp64 [n_items * N]; info: host [n_items] or NULL. */
+splidar_status splidar_stationary_structured(const splidar_flux *shape, int32_t n_items, const double *S,
+                                             const double *B, const double *t_d, double tol, int32_t max_iter,
+                                             double *pi, void *ws, size_t ws_bytes, splidar_solve_info *info,
+                                             void *stream);
+
+typedef struct {
+    double lambda2_re, lambda2_im;  /* second eigenvalue of P~ (lambda2_im >= 0: the member of a
+                                       conjugate pair with phase in [0, pi])                     */
+    double modulus;                 /* |lambda_2| (§4)                                    */
+    double phase;                   /* arg lambda_2 in [0, pi] (§4.2)                     */
+    double gap;                     /* spectral gap 1 - |lambda_2| (§4.1)                 */
+    double change;                  /* last move of the Ritz value                                */
+    int32_t iters, converged;
+} splidar_spectral_info;
+
+/* f1: the second eigenvalue of P~ = J_l P~0 per item (§4). The leading pair (left pi,
+ * right 1) is deflated, A = P~ - 1 pi, and a 2-D real subspace is iterated under v -> v A with Ritz
+ * values from H = (W Q^T)(Q Q^T)^{-1} (a complex pair spans a real 2-D invariant subspace); stop
+ * when the dominant Ritz value moves less than tol, else SPLIDAR_ENOCONV after max_iter products.
+ * pi: device fp64 [n_items * N], the stationary vectors of the items (e.g. from
+ * splidar_stationary_structured; accurate to << tol). info: host [n_items]. */
+splidar_status splidar_second_eigenvalue(const splidar_flux *shape, int32_t n_items, const double *S,
+                                         const double *B, const double *t_d, const double *pi, double tol,
+                                         int32_t max_iter, void *ws, size_t ws_bytes, splidar_spectral_info *info,
+                                         void *stream);
+
+/* f1: mixing steps (§4.1: "the number of steps n such that P~^n approaches the stationary
+ * distribution"): the smallest n >= 1 with max_i 1/2 ||e_i^T P~^n - pi||_1 <= eps over all start
+ * bins i (every row of P~^n), found per start as its first n_i (TV to stationarity is
+ * non-increasing) and reduced as max_i n_i. pi: device fp64 [N]. steps_per_start: device int32 [N]
+ * (n_i, -1 if max_steps was not enough) or NULL. mixing_steps: host, -1 with SPLIDAR_ENOCONV if
+ * some start needs more than max_steps. Workspace: splidar_structured_workspace_bytes(N, 1, N). */
+splidar_status splidar_mixing_steps(const splidar_flux *flux, double t_d, const double *pi, double eps,
+                                    int32_t max_steps, int32_t *steps_per_start, int32_t *mixing_steps, void *ws,
+                                    size_t ws_bytes, void *stream);
+
+/* f1: the trajectory of one histogram bin (§4.2): traj[n] = (start^T P~^n)[bin] for
+ * n = 0..steps (no renormalisation), and final_vec = start^T P~^steps (device [N], may be NULL).
+ * start: device fp64 [N]; traj: device fp64 [steps + 1]. 0 <= bin < N, steps >= 0.
+ * Workspace: splidar_structured_workspace_bytes(N, 1, 1). */
+splidar_status splidar_bin_trajectory(const splidar_flux *flux, double t_d, const double *start, int32_t bin,
+                                      int32_t steps, double *traj, double *final_vec, void *ws, size_t ws_bytes,
+                                      void *stream);
+
 const char *splidar_strerror(splidar_status st);
 int splidar_last_cuda_error(void);     /* cudaError_t of the last SPLIDAR_ECUDA, else 0 */
 const char *splidar_build_info(void);  /* compile target and version string */

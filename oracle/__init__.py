@@ -12,6 +12,7 @@ Functions (each follows the passage cited in oracle.c):
   left_matvec_streamed(flux, t_d, x)         x^T P~ with P~ recomputed row by row (large N)
   stationary_dense(P~), stationary_power(P~) pi P~ = pi
   monte_carlo(flux, t_d, ...)                continuous-time detection process of P:60
+  second_eigenvalue(P), mixing_steps(P, pi), bin_trajectory(P, start, bin, steps)   §4
 """
 from __future__ import annotations
 
@@ -182,3 +183,54 @@ def shift_l(flux, t_d: float) -> int:
     import math
     u = math.fmod(float(t_d), flux.t_r) * flux.n_bins / flux.t_r
     return int(math.ceil(u)) % flux.n_bins
+
+
+# ------------------------------------------------------------------ spectral analysis (§4)
+# Plain definitions on a dense transition matrix (the oracle's Eq. 4 P~, or any row-stochastic
+# matrix); numpy.linalg.eigvals and matmul are the library steps. SURVEY §8(f) row f1.
+
+def second_eigenvalue(P: np.ndarray) -> complex:
+    """lambda_2 of P (§4: "the magnitude of the second largest eigenvalue |lambda_2| of P~"):
+    all eigenvalues by numpy.linalg.eigvals, drop the Perron root (the one closest to 1), return the
+    largest-modulus remaining one; of a conjugate pair the member with phase in [0, pi]."""
+    ev = np.linalg.eigvals(np.asarray(P, dtype=np.float64))
+    k = int(np.argmin(np.abs(ev - 1.0)))
+    rest = np.delete(ev, k)
+    if rest.size == 0:
+        return 0j
+    mod = np.abs(rest)
+    top = rest[np.abs(mod - mod.max()) <= 1e-12 * max(1.0, mod.max())]
+    lam = top[np.argmax(top.imag)]                      # conjugate pair -> im >= 0
+    return complex(lam.real, abs(lam.imag)) if abs(lam.imag) > 0 else complex(lam.real, 0.0)
+
+
+def mixing_steps(P: np.ndarray, pi: np.ndarray, eps: float = 1e-3, max_steps: int = 100000):
+    """§4.1: the smallest n >= 1 with max_i 1/2 ||e_i^T P^n - pi||_1 <= eps, by repeated
+    multiplication of the full matrix power (every row is one start e_i). Returns (n, per-start first
+    hits n_i) with n = -1 if max_steps is exceeded."""
+    P = np.asarray(P, dtype=np.float64)
+    pi = np.asarray(pi, dtype=np.float64)
+    n_rows = P.shape[0]
+    first = np.full(n_rows, -1, dtype=np.int64)
+    Pn = P.copy()
+    n_mix = -1
+    for n in range(1, max_steps + 1):
+        tv = 0.5 * np.abs(Pn - pi[None, :]).sum(axis=1)
+        first[(first < 0) & (tv <= eps)] = n
+        if n_mix < 0 and tv.max() <= eps:
+            n_mix = n
+        if np.all(first >= 0):
+            break
+        Pn = Pn @ P
+    return n_mix, first
+
+
+def bin_trajectory(P: np.ndarray, start: np.ndarray, bin: int, steps: int):
+    """§4.2: (start^T P^n)[bin] for n = 0..steps, and start^T P^steps."""
+    v = np.asarray(start, dtype=np.float64).copy()
+    P = np.asarray(P, dtype=np.float64)
+    out = [v[bin]]
+    for _ in range(steps):
+        v = v @ P
+        out.append(v[bin])
+    return np.array(out), v

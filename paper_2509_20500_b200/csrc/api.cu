@@ -604,3 +604,249 @@ splidar_status splidar_sweep(const splidar_flux *shape, int32_t n_items, const d
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- structured operator (f1, f2) --
+//
+// Workspace: FluxDev[M] | the step-1 vectors of M profiles (as ws_layout) | prof[I] | lsh[I] |
+// SolveState[I] | SpecOut[I] | nsteps[I] | nmax.
+
+namespace spl {
+struct SLayout {
+    int N, M, I;
+    size_t flux, vec, prof, lsh, st, spec, nsteps, nmax, total;
+};
+static SLayout struct_layout(int N, int M, int I) {
+    SLayout L;
+    L.N = N;
+    L.M = M;
+    L.I = I;
+    size_t o = 0;
+    L.flux = o; o = a256(o + sizeof(FluxDev) * (size_t)M);
+    const size_t ntile = ((size_t)N + 1 + kScanTile - 1) / kScanTile;
+    L.vec = o; o = a256(o + sizeof(double) * ((size_t)M * N * 5 + (size_t)M * 8 + 5 * (size_t)M * ntile));
+    L.prof = o; o = a256(o + sizeof(int) * (size_t)I);
+    L.lsh = o; o = a256(o + sizeof(int) * (size_t)I);
+    L.st = o; o = a256(o + sizeof(SolveState) * (size_t)I);
+    L.spec = o; o = a256(o + sizeof(SpecOut) * (size_t)I);
+    L.nsteps = o; o = a256(o + sizeof(int) * (size_t)I);
+    L.nmax = o; o = a256(o + sizeof(int) * 4);
+    L.total = o;
+    return L;
+}
+static VecPtrs svec_ptrs(char *ws, const SLayout &L) {
+    WsLayout W;
+    memset(&W, 0, sizeof(W));
+    W.N = L.N;
+    W.M = L.M;
+    W.vec = L.vec;
+    return vec_ptrs(ws, W);
+}
+}  // namespace spl
+
+// Validates items (shape x S[m], B[m], t_d[m]), groups them by (S, B), enqueues the step-1 vectors of
+// every distinct profile and uploads the per-item profile index and shift (n_items_ws: items the
+// workspace must hold, >= n_items). Fills the kernel arguments with pointers into ws.
+struct Prep {
+    StructArgs a;
+    SLayout L;
+    std::vector<int> prof, l;
+    std::vector<double> scal;   // [M][8] host copy (after read_scal)
+};
+
+static splidar_status struct_prepare(const splidar_flux *shape, int n_items, const double *S, const double *B,
+                                     const double *t_d, int n_items_ws, void *ws, size_t ws_bytes, cudaStream_t s,
+                                     Prep *p) {
+    if (!shape || n_items < 1 || !S || !B || !t_d) return SPLIDAR_EINVAL;
+    const int N = shape->n_bins;
+    int C, T;
+    if (N < 2 || struct_shape(N, &C, &T)) return SPLIDAR_EINVAL;
+    splidar_status st;
+    p->l.assign((size_t)n_items, 0);
+    p->prof.assign((size_t)n_items, 0);
+    std::vector<FluxDev> fl;
+    std::map<std::pair<double, double>, int> idx;
+    for (int i = 0; i < n_items; ++i) {
+        if (!std::isfinite(S[i]) || S[i] < 0.0) return SPLIDAR_EINVAL;
+        FluxDev d = to_dev(shape, S[i], B[i]);
+        splidar_flux f = *shape;
+        f.background = B[i];
+        std::vector<double> sig((size_t)shape->n_pulses);
+        for (int k = 0; k < shape->n_pulses; ++k) sig[(size_t)k] = d.S[k];
+        f.signal = sig.data();
+        if ((st = check_flux(&f))) return st;
+        int32_t li;
+        if ((st = splidar_shift(shape->t_r, N, t_d[i], &li))) return st;
+        p->l[(size_t)i] = li;
+        auto key = std::make_pair(S[i], B[i]);
+        auto it = idx.find(key);
+        if (it == idx.end()) {
+            idx[key] = (int)fl.size();
+            p->prof[(size_t)i] = (int)fl.size();
+            fl.push_back(d);
+        } else {
+            p->prof[(size_t)i] = it->second;
+        }
+    }
+    const int M = (int)fl.size();
+    if (M > 65535) return SPLIDAR_EINVAL;
+    p->L = struct_layout(N, M, n_items_ws > n_items ? n_items_ws : n_items);
+    const SLayout &L = p->L;
+    if (!ws || ((uintptr_t)ws & 255u) != 0 || ws_bytes < L.total) return SPLIDAR_ENOSPACE;
+    char *wsb = static_cast<char *>(ws);
+    SPL_CUDA(cudaMemcpyAsync(wsb + L.flux, fl.data(), sizeof(FluxDev) * (size_t)M, cudaMemcpyHostToDevice, s));
+    VecPtrs vp = svec_ptrs(wsb, L);
+    SPL_CUDA(launch_flux_vectors(reinterpret_cast<const FluxDev *>(wsb + L.flux), M, N, vp, N, s));
+    SPL_CUDA(cudaMemcpyAsync(wsb + L.prof, p->prof.data(), sizeof(int) * (size_t)n_items, cudaMemcpyHostToDevice, s));
+    SPL_CUDA(cudaMemcpyAsync(wsb + L.lsh, p->l.data(), sizeof(int) * (size_t)n_items, cudaMemcpyHostToDevice, s));
+    StructArgs *a = &p->a;
+    memset(a, 0, sizeof(*a));
+    a->N = N;
+    a->C = C;
+    a->threads = T;
+    a->vstride = N;
+    a->w = vp.w;
+    a->invD = vp.invD;
+    a->scal = vp.scal;
+    a->prof = reinterpret_cast<const int *>(wsb + L.prof);
+    a->lsh = reinterpret_cast<const int *>(wsb + L.lsh);
+    a->st = reinterpret_cast<SolveState *>(wsb + L.st);
+    a->spec = reinterpret_cast<SpecOut *>(wsb + L.spec);
+    a->nsteps = reinterpret_cast<int *>(wsb + L.nsteps);
+    a->nmax = reinterpret_cast<int *>(wsb + L.nmax);
+    return SPLIDAR_OK;
+}
+
+// After the kernels: the per-profile scalars (Lambda, e^{-Lambda}, bad-row flag) to the host; syncs s.
+static splidar_status read_scal(Prep *p, cudaStream_t s) {
+    p->scal.assign((size_t)p->L.M * 8, 0.0);
+    SPL_CUDA(cudaMemcpyAsync(p->scal.data(), p->a.scal, sizeof(double) * p->scal.size(), cudaMemcpyDeviceToHost, s));
+    SPL_CUDA(cudaStreamSynchronize(s));
+    for (int m = 0; m < p->L.M; ++m)
+        if (p->scal[(size_t)m * 8 + 2] != 0.0) return SPLIDAR_EZEROROW;
+    return SPLIDAR_OK;
+}
+
+extern "C" {
+
+size_t splidar_structured_workspace_bytes(int32_t n_bins, int32_t n_profiles, int32_t n_items) {
+    int C, T;
+    if (n_bins < 2 || n_profiles < 1 || n_items < 1 || struct_shape(n_bins, &C, &T)) return 0;
+    return struct_layout(n_bins, n_profiles, n_items).total;
+}
+
+splidar_status splidar_stationary_structured(const splidar_flux *shape, int32_t n_items, const double *S,
+                                             const double *B, const double *t_d, double tol, int32_t max_iter,
+                                             double *pi, void *ws, size_t ws_bytes, splidar_solve_info *info,
+                                             void *stream) {
+    if (!pi || !(tol > 0.0) || !std::isfinite(tol) || max_iter < 1) return SPLIDAR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    Prep p;
+    splidar_status st = struct_prepare(shape, n_items, S, B, t_d, n_items, ws, ws_bytes, s, &p);
+    if (st) return st;
+    p.a.tol = tol;
+    p.a.max_iter = max_iter;
+    p.a.pi = pi;
+    SPL_CUDA(launch_struct(kStructSolve, p.a, n_items, s));
+    std::vector<SolveState> hs((size_t)n_items);
+    SPL_CUDA(cudaMemcpyAsync(hs.data(), p.a.st, sizeof(SolveState) * hs.size(), cudaMemcpyDeviceToHost, s));
+    if ((st = read_scal(&p, s))) return st;
+    bool all = true;
+    for (int i = 0; i < n_items; ++i) {
+        const SolveState &h = hs[(size_t)i];
+        all = all && h.converged;
+        if (info) {
+            splidar_solve_info &o = info[i];
+            o.iters = h.iters;
+            o.converged = h.converged;
+            o.shift_l = h.l;
+            o.reserved = 0;
+            o.l1_change = h.change;
+            o.lambda_total = p.scal[(size_t)p.prof[(size_t)i] * 8];
+        }
+    }
+    return all ? SPLIDAR_OK : SPLIDAR_ENOCONV;
+}
+
+splidar_status splidar_second_eigenvalue(const splidar_flux *shape, int32_t n_items, const double *S,
+                                         const double *B, const double *t_d, const double *pi, double tol,
+                                         int32_t max_iter, void *ws, size_t ws_bytes, splidar_spectral_info *info,
+                                         void *stream) {
+    if (!pi || !(tol > 0.0) || !std::isfinite(tol) || max_iter < 1) return SPLIDAR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    Prep p;
+    splidar_status st = struct_prepare(shape, n_items, S, B, t_d, n_items, ws, ws_bytes, s, &p);
+    if (st) return st;
+    p.a.tol = tol;
+    p.a.max_iter = max_iter;
+    p.a.pi = const_cast<double *>(pi);
+    SPL_CUDA(launch_struct(kStructLambda2, p.a, n_items, s));
+    std::vector<SpecOut> hs((size_t)n_items);
+    SPL_CUDA(cudaMemcpyAsync(hs.data(), p.a.spec, sizeof(SpecOut) * hs.size(), cudaMemcpyDeviceToHost, s));
+    if ((st = read_scal(&p, s))) return st;
+    bool all = true;
+    for (int i = 0; i < n_items; ++i) {
+        const SpecOut &h = hs[(size_t)i];
+        all = all && h.converged;
+        if (info) {
+            splidar_spectral_info &o = info[i];
+            o.lambda2_re = h.re;
+            o.lambda2_im = h.im;
+            o.modulus = std::hypot(h.re, h.im);
+            o.phase = std::atan2(h.im, h.re);
+            o.gap = 1.0 - o.modulus;
+            o.change = h.change;
+            o.iters = h.iters;
+            o.converged = h.converged;
+        }
+    }
+    return all ? SPLIDAR_OK : SPLIDAR_ENOCONV;
+}
+
+splidar_status splidar_mixing_steps(const splidar_flux *flux, double t_d, const double *pi, double eps,
+                                    int32_t max_steps, int32_t *steps_per_start, int32_t *mixing_steps, void *ws,
+                                    size_t ws_bytes, void *stream) {
+    if (!flux || !pi || !mixing_steps || !(eps > 0.0) || !std::isfinite(eps) || max_steps < 1) return SPLIDAR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const double one = 1.0, bg = flux->background;
+    const int N = flux->n_bins;
+    Prep p;
+    splidar_status st = struct_prepare(flux, 1, &one, &bg, &t_d, N, ws, ws_bytes, s, &p);
+    if (st) return st;
+    p.a.pi = const_cast<double *>(pi);
+    p.a.eps = eps;
+    p.a.max_iter = max_steps;
+    p.a.start_bin0 = 0;
+    SPL_CUDA(cudaMemsetAsync(p.a.nmax, 0, sizeof(int), s));
+    SPL_CUDA(launch_struct(kStructMixing, p.a, N, s));
+    if (steps_per_start)
+        SPL_CUDA(cudaMemcpyAsync(steps_per_start, p.a.nsteps, sizeof(int) * (size_t)N, cudaMemcpyDeviceToDevice, s));
+    int hmax = 0;
+    SPL_CUDA(cudaMemcpyAsync(&hmax, p.a.nmax, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if ((st = read_scal(&p, s))) return st;
+    if (hmax == 0x7fffffff) {
+        *mixing_steps = -1;
+        return SPLIDAR_ENOCONV;
+    }
+    *mixing_steps = hmax;
+    return SPLIDAR_OK;
+}
+
+splidar_status splidar_bin_trajectory(const splidar_flux *flux, double t_d, const double *start, int32_t bin,
+                                      int32_t steps, double *traj, double *final_vec, void *ws, size_t ws_bytes,
+                                      void *stream) {
+    if (!flux || !start || !traj || steps < 0 || bin < 0 || bin >= flux->n_bins) return SPLIDAR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const double one = 1.0, bg = flux->background;
+    Prep p;
+    splidar_status st = struct_prepare(flux, 1, &one, &bg, &t_d, 1, ws, ws_bytes, s, &p);
+    if (st) return st;
+    p.a.start = start;
+    p.a.bin = bin;
+    p.a.max_iter = steps;
+    p.a.traj = traj;
+    p.a.out = final_vec;
+    SPL_CUDA(launch_struct(kStructTraj, p.a, 1, s));
+    return read_scal(&p, s);
+}
+
+}  // extern "C"

@@ -110,4 +110,31 @@ size_t finish_args_size();
 // pi output: out_idx[mv] >= 0 selects row out_idx[mv] of pi ([*, N]); < 0 skips the vector.
 void make_finish_args(void *dst, const PowerArgs &a, double *pi, const int *out_idx);
 
+// ---- structured (matrix-free) operator kernels (structured.cu) -----------
+struct SpecOut {        // second eigenvalue of one item
+    double re, im;      // lambda_2 (im >= 0)
+    double change;      // last move of the dominant Ritz value
+    int iters, converged;
+};
+struct StructArgs {
+    int N, C, threads;          // cluster of C CTAs x threads, 8 positions per thread
+    int64_t vstride;            // profile stride of the vectors
+    const double *w, *invD, *scal;
+    const int *prof, *lsh;      // [items] profile index and shift l
+    double tol;
+    int max_iter;               // solve / lambda2: max products; mixing: step cap; traj: steps
+    double *pi;                 // solve: out [items][N]; lambda2: in [items][N]; mixing: in [N]
+    SolveState *st;             // solve: [items]
+    SpecOut *spec;              // lambda2: [items]
+    double eps;                 // mixing: TV threshold
+    int start_bin0;             // mixing: first start bin of this launch
+    int *nsteps, *nmax;         // mixing: [N] per start, max over starts
+    const double *start;        // traj: start distribution [N]
+    int bin;                    // traj: recorded bin
+    double *traj, *out;         // traj: [steps + 1], final vector [N] (may be null)
+};
+enum { kStructSolve = 0, kStructLambda2 = 1, kStructMixing = 2, kStructTraj = 3 };
+int struct_shape(int N, int *C, int *threads);
+cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s);
+
 }  // namespace spl

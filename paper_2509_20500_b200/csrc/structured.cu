@@ -1,0 +1,589 @@
+// SURVEY §8(f) rows f2 + f1: the structured (matrix-free) transition operator, with the stationary
+// solve, the second eigenvalue, the mixing steps and the bin trajectories built on it.
+//
+// The left product with the base matrix never needs the matrix. From §3.4 (E_base = exp.(-Lambda L - D),
+// P:172-174; P = (1 lambda^T) . E; row normalisation P:79):
+//   P~0[r][j] = w_j (r > j ? e^{-Lambda} : 1) / D_r,   w_j = lambda_j e^{-F_j}
+// so for a row vector x (already gathered by the dead-time permutation of Thm 2, x_r = v[(r - l) mod N]):
+//   y_j = sum_r x_r P~0[r][j] = w_j (C_j + e^{-Lambda} (T - C_j)),   z_r = x_r / D_r,
+//   C_j = sum_{r <= j} z_r (inclusive prefix), T = sum_r z_r.
+// One product is one prefix scan: O(N) instead of the N^2 b bytes of the dense GEMV.
+//
+// Layout: one thread-block cluster of C CTAs per item (C = ceil(N / 4096), <= 16). CTA c owns the
+// positions [c chunk, (c + 1) chunk), chunk = 8 x blockDim; a thread owns 8 consecutive positions (its
+// w, 1/D and iterate in registers). The gathered iterate lives in shared memory (xbuf); each product's
+// result is pushed straight into the owner CTA's xbuf at (j + l) mod N over DSMEM, so the permutation
+// costs one DSMEM store per element and no extra pass. Per product: block scan -> publish the CTA
+// totals to every CTA (DSMEM) -> barrier.cluster -> outputs + push + publish the next sums ->
+// barrier.cluster. Every CTA adds the published values in the same fixed order, so all CTAs take the
+// same control-flow decisions and the result does not depend on timing (deterministic).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace spl {
+namespace {
+
+constexpr int kSE = 8;                        // positions per thread
+constexpr int kSMaxT = 512;                   // threads per CTA
+constexpr int kSMaxWarps = kSMaxT / 32;
+constexpr int kSMaxC = 16;                    // cluster size (> 8 is non-portable)
+constexpr int kSExK = 8;                      // values published per CTA per exchange
+
+__device__ __forceinline__ int sidx(int p) { return p + (p >> 3); }   // padded xbuf index
+
+// Shared-memory scratch (static part): two exchange areas (each [kSExK][kSMaxC]) and block scratch.
+struct SShared {
+    double exA[kSExK * kSMaxC];
+    double exB[kSExK * kSMaxC];
+    double scr[kSExK * kSMaxWarps];
+};
+
+// Sum over the block of K values per thread; every thread gets the K totals (fixed order).
+template <int K>
+__device__ __forceinline__ void bsum(double (&v)[K], double *scr) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double x = v[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) scr[k * kSMaxWarps + warp] = x;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += scr[k * kSMaxWarps + w];
+        v[k] = s;
+    }
+    __syncthreads();
+}
+
+// Inclusive scan over the block of V vectors held as 8 consecutive values per thread; tot[a] = the
+// block total of vector a (every thread).
+template <int V>
+__device__ __forceinline__ void bscan(double (&v)[V][kSE], double (&tot)[V], double *scr) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double x[V], ex[V];
+#pragma unroll
+    for (int a = 0; a < V; ++a) {
+#pragma unroll
+        for (int i = 1; i < kSE; ++i) v[a][i] += v[a][i - 1];
+        x[a] = v[a][kSE - 1];
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+        for (int a = 0; a < V; ++a) {
+            const double y = __shfl_up_sync(0xffffffffu, x[a], o);
+            if (lane >= o) x[a] += y;
+        }
+#pragma unroll
+    for (int a = 0; a < V; ++a) {
+        ex[a] = __shfl_up_sync(0xffffffffu, x[a], 1);
+        if (lane == 0) ex[a] = 0.0;
+        if (lane == 31) scr[a * kSMaxWarps + warp] = x[a];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < V; ++a) {
+        double wex = 0.0, tt = 0.0;
+        for (int w = 0; w < nw; ++w) {
+            const double wt = scr[a * kSMaxWarps + w];
+            if (w < warp) wex += wt;
+            tt += wt;
+        }
+        tot[a] = tt;
+        const double e = wex + ex[a];
+#pragma unroll
+        for (int i = 0; i < kSE; ++i) v[a][i] += e;
+    }
+    __syncthreads();
+}
+
+// Publish K values of this CTA (rank c) into slot c of every CTA's exchange area (DSMEM stores).
+template <int K>
+__device__ __forceinline__ void publish(cg::cluster_group &cl, double *ex, const double (&v)[K], int c, int C) {
+    const int t = threadIdx.x;
+    if (t < C * K) {
+        const int dst = t / K, k = t - dst * K;
+        double *r = cl.map_shared_rank(ex, dst);
+        r[k * kSMaxC + c] = v[k];
+    }
+}
+
+// After the barrier: totals over all CTAs and the exclusive prefix up to CTA c (fixed order).
+__device__ __forceinline__ void gather_sum(const double *ex, int k, int c, int C, double &total, double &before) {
+    double t = 0.0, b = 0.0;
+    for (int cc = 0; cc < C; ++cc) {
+        const double v = ex[k * kSMaxC + cc];
+        if (cc < c) b += v;
+        t += v;
+    }
+    total = t;
+    before = b;
+}
+
+struct Pos {
+    int N, C, c, chunk, p0;   // p0: first global position of this thread
+    int l;
+    __device__ bool valid(int e) const { return p0 + e < N; }
+};
+
+__device__ __forceinline__ Pos make_pos(const StructArgs &a, int c, int l) {
+    Pos p;
+    p.N = a.N;
+    p.C = a.C;
+    p.c = c;
+    p.chunk = blockDim.x * kSE;
+    p.p0 = c * p.chunk + threadIdx.x * kSE;
+    p.l = l;
+    return p;
+}
+
+// The per-thread product core: given the gathered x (8 values), returns y at the thread's natural
+// positions after the cluster exchange of the scan totals. Publishes extra values (K - 1 of them
+// after the scan total at slot 0.. V-1) in the same exchange.
+// (Inlined into each kernel below; kept as code there for clarity of the barrier structure.)
+
+// Push y (natural positions p0 + e) into the gathered xbuf of the owner of (p + l) mod N.
+__device__ __forceinline__ void push(cg::cluster_group &cl, double *xbuf, const Pos &P, const double (&y)[kSE]) {
+#pragma unroll
+    for (int e = 0; e < kSE; ++e) {
+        const int p = P.p0 + e;
+        if (p < P.N) {
+            int r = p + P.l;
+            if (r >= P.N) r -= P.N;
+            const int dst = r / P.chunk;
+            const int li = r - dst * P.chunk;
+            double *remote = cl.map_shared_rank(xbuf, dst);
+            remote[sidx(li)] = y[e];
+        }
+    }
+}
+
+__device__ __forceinline__ void load8(const double *src, const Pos &P, double (&o)[kSE]) {
+#pragma unroll
+    for (int e = 0; e < kSE; ++e) o[e] = P.valid(e) ? __ldg(src + P.p0 + e) : 0.0;
+}
+
+// ---------------------------------------------------------------------------------------------
+// f2: stationary solve. pi^0 = 1/N; v^{k+1} = v^k P~ (unnormalised; P~ is stochastic so the scale
+// stays ~1); pi^k = v^k / ||v^k||_1; stop after the first k with ||pi^{k+1} - pi^k||_1 < tol (the change
+// of product k is published with the scan totals of product k + 1, one exchange fewer per product).
+__global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double xbuf[];
+    __shared__ SShared sh;
+    const int C = a.C, c = (int)cl.block_rank();
+    const int item = blockIdx.x / C;
+    const int m = a.prof[item], l = a.lsh[item];
+    const Pos P = make_pos(a, c, l);
+    const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
+    const double eL = a.scal[m * 8 + 1];
+    double wr[kSE], idr[kSE], yp[kSE];
+    load8(w, P, wr);
+    load8(invD, P, idr);
+    const double u = 1.0 / (double)P.N;
+#pragma unroll
+    for (int e = 0; e < kSE; ++e) {
+        yp[e] = P.valid(e) ? u : 0.0;
+        xbuf[sidx(threadIdx.x * kSE + e)] = yp[e];   // the gathered uniform vector is uniform
+    }
+    double s_prev = 1.0, dpart = 0.0, change = __longlong_as_double(0x7ff0000000000000ll);
+    int k = 0, conv = 0;
+    cl.sync();
+    for (;;) {
+        // phase 1: z = x / D, block scan; publish (scan total, change partial of product k - 1)
+        double v[1][kSE], tot[1];
+#pragma unroll
+        for (int e = 0; e < kSE; ++e) v[0][e] = xbuf[sidx(threadIdx.x * kSE + e)] * idr[e];
+        bscan<1>(v, tot, sh.scr);
+        {
+            const double pv[2] = {tot[0], dpart};
+            publish<2>(cl, sh.exA, pv, c, C);
+        }
+        cl.sync();   // A
+        double T, off, dummy;
+        gather_sum(sh.exA, 0, c, C, T, off);
+        if (k > 0) {
+            gather_sum(sh.exA, 1, c, C, change, dummy);
+            if (change < a.tol) { conv = 1; break; }
+            if (k >= a.max_iter || !(s_prev > 0.0) || !isfinite(change)) break;
+        }
+        // phase 2: y = w (C + e^{-Lambda} (T - C)) at the natural positions; push; publish sum(y)
+        double y[kSE];
+        double ps[1] = {0.0};
+#pragma unroll
+        for (int e = 0; e < kSE; ++e) {
+            const double Cj = off + v[0][e];
+            y[e] = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
+            ps[0] += y[e];
+        }
+        push(cl, xbuf, P, y);
+        bsum<1>(ps, sh.scr);
+        publish<1>(cl, sh.exB, ps, c, C);
+        cl.sync();   // B
+        double s, d2;
+        gather_sum(sh.exB, 0, c, C, s, d2);
+        double d[1] = {0.0};
+        const double is = 1.0 / s, ip = 1.0 / s_prev;
+#pragma unroll
+        for (int e = 0; e < kSE; ++e) {
+            d[0] += fabs(y[e] * is - yp[e] * ip);
+            yp[e] = y[e];
+        }
+        bsum<1>(d, sh.scr);
+        dpart = d[0];
+        s_prev = s;
+        ++k;
+    }
+    // pi^k = v^k / s_k at the natural positions
+    double *out = a.pi + (size_t)item * P.N;
+    const double is = 1.0 / s_prev;
+#pragma unroll
+    for (int e = 0; e < kSE; ++e)
+        if (P.valid(e)) out[P.p0 + e] = yp[e] * is;
+    if (c == 0 && threadIdx.x == 0) {
+        SolveState st;
+        st.l = l;
+        st.iters = k;
+        st.done = 1;
+        st.converged = conv;
+        st.cur = 0;
+        st.pad0 = st.pad1 = st.pad2 = 0;
+        st.s = s_prev;
+        st.change = change;
+        a.st[item] = st;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// f1: the second eigenvalue of P~ (§4). The known leading pair (left pi, right 1) is
+// deflated: A = P~ - 1 pi, v A = v P~ - (v 1) pi. A two-dimensional real subspace Q = [q1; q2] is
+// iterated, W = Q A, and the Ritz values are the eigenvalues of H = (W Q^T)(Q Q^T)^{-1}; a complex
+// pair lambda2, conj(lambda2) spans a real 2-D invariant subspace, so real arithmetic suffices. Basis
+// update: q1 = w1 / |w1|, q2 = (w2 - (w1.w2 / w1.w1) w1) / |w2| (applied as coefficients to the pushed
+// w, so the product needs two cluster exchanges). Stop when the dominant Ritz value moves < tol.
+
+__device__ __forceinline__ double hash_unit(uint32_t j, uint32_t salt) {   // deterministic in [-1, 1)
+    uint32_t x = j * 0x9E3779B1u + salt * 0x85EBCA77u + 0x165667B1u;
+    x ^= x >> 15; x *= 0x2C1B3C6Du; x ^= x >> 12; x *= 0x297A2D39u; x ^= x >> 15;
+    return (double)x * (2.0 / 4294967296.0) - 1.0;
+}
+
+__global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double xbuf[];    // [2][chunk + chunk / 8]: gathered w1, w2
+    __shared__ SShared sh;
+    const int C = a.C, c = (int)cl.block_rank();
+    const int item = blockIdx.x / C;
+    const int m = a.prof[item], l = a.lsh[item];
+    const Pos P = make_pos(a, c, l);
+    const int xs = P.chunk + P.chunk / 8;
+    double *xb0 = xbuf, *xb1 = xbuf + xs;
+    const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
+    const double *pi = a.pi + (size_t)item * P.N;
+    const double eL = a.scal[m * 8 + 1];
+    double wn[2][kSE];   // last W at the natural positions (q = combination of these)
+#pragma unroll
+    for (int e = 0; e < kSE; ++e) {
+        const int p = P.p0 + e;
+        wn[0][e] = P.valid(e) ? hash_unit((uint32_t)p, 1u) : 0.0;
+        wn[1][e] = P.valid(e) ? hash_unit((uint32_t)p, 2u) : 0.0;
+        // gathered copies: xbuf[r] = q[(r - l) mod N]
+        const int r = P.p0 + e;
+        double g0 = 0.0, g1 = 0.0;
+        if (r < P.N) {
+            int src = r - l;
+            if (src < 0) src += P.N;
+            g0 = hash_unit((uint32_t)src, 1u);
+            g1 = hash_unit((uint32_t)src, 2u);
+        }
+        xb0[sidx(threadIdx.x * kSE + e)] = g0;
+        xb1[sidx(threadIdx.x * kSE + e)] = g1;
+    }
+    double al = 1.0, be = 1.0, ga = 0.0;           // q1 = al w1, q2 = be (w2 - ga w1)
+    double mu_re = 0.0, mu_im = 0.0, dmu = __longlong_as_double(0x7ff0000000000000ll);
+    int k = 0, conv = 0;
+    cl.sync();
+    for (;;) {
+        // phase 1: current basis (gathered and natural), z = x / D, scans; sums and Gram Q Q^T
+        double v[2][kSE], tot[2];
+        double q[2][kSE];
+        double pp[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // sum q1, sum q2, q1.q1, q1.q2, q2.q2
+#pragma unroll
+        for (int e = 0; e < kSE; ++e) {
+            const double idr = P.valid(e) ? __ldg(invD + P.p0 + e) : 0.0;
+            const double g0 = xb0[sidx(threadIdx.x * kSE + e)], g1 = xb1[sidx(threadIdx.x * kSE + e)];
+            v[0][e] = al * g0 * idr;
+            v[1][e] = be * (g1 - ga * g0) * idr;
+            q[0][e] = al * wn[0][e];
+            q[1][e] = be * (wn[1][e] - ga * wn[0][e]);
+            pp[0] += q[0][e];
+            pp[1] += q[1][e];
+            pp[2] += q[0][e] * q[0][e];
+            pp[3] += q[0][e] * q[1][e];
+            pp[4] += q[1][e] * q[1][e];
+        }
+        bscan<2>(v, tot, sh.scr);
+        bsum<5>(pp, sh.scr);
+        {
+            const double pv[7] = {tot[0], tot[1], pp[0], pp[1], pp[2], pp[3], pp[4]};
+            publish<7>(cl, sh.exA, pv, c, C);
+        }
+        cl.sync();   // A
+        double T[2], off[2], sig[2], G11, G12, G22, dm;
+        gather_sum(sh.exA, 0, c, C, T[0], off[0]);
+        gather_sum(sh.exA, 1, c, C, T[1], off[1]);
+        gather_sum(sh.exA, 2, c, C, sig[0], dm);
+        gather_sum(sh.exA, 3, c, C, sig[1], dm);
+        gather_sum(sh.exA, 4, c, C, G11, dm);
+        gather_sum(sh.exA, 5, c, C, G12, dm);
+        gather_sum(sh.exA, 6, c, C, G22, dm);
+        // phase 2: W = Q P~ - (Q 1) pi; dots; push W
+        double hp[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // h11 h12 h21 h22 g11 g12 g22
+#pragma unroll
+        for (int e = 0; e < kSE; ++e) {
+            double y0 = 0.0, y1 = 0.0;
+            if (P.valid(e)) {
+                const double wj = __ldg(w + P.p0 + e), pj = __ldg(pi + P.p0 + e);
+                const double C0 = off[0] + v[0][e], C1 = off[1] + v[1][e];
+                y0 = wj * (C0 + eL * (T[0] - C0)) - sig[0] * pj;
+                y1 = wj * (C1 + eL * (T[1] - C1)) - sig[1] * pj;
+            }
+            wn[0][e] = y0;
+            wn[1][e] = y1;
+            hp[0] += y0 * q[0][e];
+            hp[1] += y0 * q[1][e];
+            hp[2] += y1 * q[0][e];
+            hp[3] += y1 * q[1][e];
+            hp[4] += y0 * y0;
+            hp[5] += y0 * y1;
+            hp[6] += y1 * y1;
+        }
+        push(cl, xb0, P, wn[0]);
+        push(cl, xb1, P, wn[1]);
+        bsum<7>(hp, sh.scr);
+        publish<7>(cl, sh.exB, hp, c, C);
+        cl.sync();   // B
+        double h[7];
+#pragma unroll
+        for (int i = 0; i < 7; ++i) gather_sum(sh.exB, i, c, C, h[i], dm);
+        ++k;
+        // Ritz values: H = M G^{-1}, M = W Q^T = [[h11, h12], [h21, h22]], G = Q Q^T
+        double nre, nim;
+        const double detG = G11 * G22 - G12 * G12;
+        const bool two = detG > 1e-24 * G11 * G22 && G11 > 0.0;
+        if (!(h[4] > 1e-280) || !(G11 > 0.0)) {        // the deflated operator annihilates the subspace
+            nre = 0.0; nim = 0.0;
+        } else if (two) {
+            const double id = 1.0 / detG;
+            const double H11 = (h[0] * G22 - h[1] * G12) * id, H12 = (-h[0] * G12 + h[1] * G11) * id;
+            const double H21 = (h[2] * G22 - h[3] * G12) * id, H22 = (-h[2] * G12 + h[3] * G11) * id;
+            const double tr = 0.5 * (H11 + H22);
+            const double det = H11 * H22 - H12 * H21;
+            const double disc = tr * tr - det;
+            if (disc < 0.0) {
+                nre = tr; nim = sqrt(-disc);
+            } else {
+                const double sq = sqrt(disc);
+                const double r1 = tr + sq, r2 = tr - sq;
+                nre = fabs(r1) >= fabs(r2) ? r1 : r2;
+                nim = 0.0;
+            }
+        } else {
+            nre = h[0] / G11;   // one-dimensional subspace: Rayleigh quotient
+            nim = 0.0;
+        }
+        dmu = hypot(nre - mu_re, nim - mu_im);
+        mu_re = nre;
+        mu_im = nim;
+        if (!(h[4] > 1e-280)) { conv = 1; break; }
+        if (k > 1 && dmu < a.tol) { conv = 1; break; }
+        if (k >= a.max_iter || !isfinite(dmu)) break;
+        // next basis as coefficients on the pushed W
+        al = 1.0 / sqrt(h[4]);
+        ga = h[5] / h[4];
+        be = h[6] > 1e-280 ? 1.0 / sqrt(h[6]) : 0.0;
+    }
+    if (c == 0 && threadIdx.x == 0) {
+        SpecOut o;
+        o.re = mu_re;
+        o.im = fabs(mu_im);   // the member of a conjugate pair with phase in [0, pi]
+        o.iters = k;
+        o.converged = conv;
+        o.change = dmu;
+        a.spec[item] = o;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// f1: mixing steps (§4.1): for each start bin i, the first n with
+// 1/2 || e_i P~^n - pi ||_1 <= eps (no renormalisation: P~ is stochastic). TV to stationarity is
+// non-increasing in n for every start, so the smallest n with max_i TV_i(n) <= eps is max_i n_i.
+// Item = one start bin; n_i written to a.nsteps[i] (-1: max_iter steps not enough).
+__global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double xbuf[];
+    __shared__ SShared sh;
+    const int C = a.C, c = (int)cl.block_rank();
+    const int start = a.start_bin0 + blockIdx.x / C;
+    const int m = a.prof[0], l = a.lsh[0];
+    const Pos P = make_pos(a, c, l);
+    const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
+    const double eL = a.scal[m * 8 + 1];
+    double wr[kSE], idr[kSE], pr[kSE];
+    load8(w, P, wr);
+    load8(invD, P, idr);
+    load8(a.pi, P, pr);
+    int r0 = start + l;
+    if (r0 >= P.N) r0 -= P.N;
+#pragma unroll
+    for (int e = 0; e < kSE; ++e) xbuf[sidx(threadIdx.x * kSE + e)] = (P.p0 + e == r0) ? 1.0 : 0.0;
+    int n = 0, hit = -1;
+    cl.sync();
+    for (;;) {
+        double v[1][kSE], tot[1];
+#pragma unroll
+        for (int e = 0; e < kSE; ++e) v[0][e] = xbuf[sidx(threadIdx.x * kSE + e)] * idr[e];
+        bscan<1>(v, tot, sh.scr);
+        publish<1>(cl, sh.exA, tot, c, C);
+        cl.sync();   // A
+        double T, off, dm;
+        gather_sum(sh.exA, 0, c, C, T, off);
+        double y[kSE], tv[1] = {0.0};
+#pragma unroll
+        for (int e = 0; e < kSE; ++e) {
+            const double Cj = off + v[0][e];
+            y[e] = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
+            tv[0] += fabs(y[e] - pr[e]);
+        }
+        push(cl, xbuf, P, y);
+        bsum<1>(tv, sh.scr);
+        publish<1>(cl, sh.exB, tv, c, C);
+        cl.sync();   // B
+        double TV;
+        gather_sum(sh.exB, 0, c, C, TV, dm);
+        ++n;
+        if (0.5 * TV <= a.eps) { hit = n; break; }
+        if (n >= a.max_iter) break;
+    }
+    if (c == 0 && threadIdx.x == 0) {
+        a.nsteps[start] = hit;
+        atomicMax(a.nmax, hit < 0 ? 0x7fffffff : hit);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// f1: bin trajectory (§4.2): (start P~^n)[bin] for n = 0..steps (no renormalisation),
+// and the final vector start P~^steps.
+__global__ void __launch_bounds__(kSMaxT, 1) k_struct_traj(const StructArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double xbuf[];
+    __shared__ SShared sh;
+    const int C = a.C, c = (int)cl.block_rank();
+    const int m = a.prof[0], l = a.lsh[0];
+    const Pos P = make_pos(a, c, l);
+    const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
+    const double eL = a.scal[m * 8 + 1];
+    double wr[kSE], idr[kSE];
+    load8(w, P, wr);
+    load8(invD, P, idr);
+#pragma unroll
+    for (int e = 0; e < kSE; ++e) {
+        const int r = P.p0 + e;
+        double g = 0.0;
+        if (r < P.N) {
+            int src = r - l;
+            if (src < 0) src += P.N;
+            g = a.start[src];
+        }
+        xbuf[sidx(threadIdx.x * kSE + e)] = g;
+    }
+    if (c == 0 && threadIdx.x == 0) a.traj[0] = a.start[a.bin];
+    cl.sync();
+    double y[kSE];
+    for (int n = 1; n <= a.max_iter; ++n) {
+        double v[1][kSE], tot[1];
+#pragma unroll
+        for (int e = 0; e < kSE; ++e) v[0][e] = xbuf[sidx(threadIdx.x * kSE + e)] * idr[e];
+        bscan<1>(v, tot, sh.scr);
+        publish<1>(cl, sh.exA, tot, c, C);
+        cl.sync();   // A
+        double T, off;
+        gather_sum(sh.exA, 0, c, C, T, off);
+#pragma unroll
+        for (int e = 0; e < kSE; ++e) {
+            const double Cj = off + v[0][e];
+            y[e] = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
+            if (P.p0 + e == a.bin) a.traj[n] = y[e];
+        }
+        if (n < a.max_iter) push(cl, xbuf, P, y);
+        cl.sync();   // B (pushes visible; xbuf reads of this product done everywhere)
+    }
+    if (a.out) {
+#pragma unroll
+        for (int e = 0; e < kSE; ++e)
+            if (P.valid(e)) a.out[P.p0 + e] = a.max_iter > 0 ? y[e] : a.start[P.p0 + e];
+    }
+}
+
+template <typename K>
+cudaError_t launch_cluster(K kernel, const StructArgs &a, int n_units, int V, cudaStream_t s) {
+    const int C = a.C;
+    const int nT = a.threads;
+    const int chunk = nT * kSE;
+    const size_t smem = sizeof(double) * (size_t)V * (chunk + chunk / 8);
+    cudaError_t e = cudaFuncSetAttribute((const void *)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (C > 8) {
+        e = cudaFuncSetAttribute((const void *)kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(n_units * C));
+    cfg.blockDim = dim3((unsigned)nT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
+}  // namespace
+
+// Cluster shape for N positions: C CTAs of `threads` threads, 8 positions per thread.
+int struct_shape(int N, int *C, int *threads) {
+    const int chunk_max = kSMaxT * kSE;
+    if (N <= chunk_max) {
+        int t = (N + kSE - 1) / kSE;
+        t = (t + 31) / 32 * 32;
+        *C = 1;
+        *threads = t < 32 ? 32 : t;
+    } else {
+        *threads = kSMaxT;
+        *C = (N + chunk_max - 1) / chunk_max;
+    }
+    return *C <= kSMaxC ? 0 : 1;
+}
+
+cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s) {
+    switch (kind) {
+        case kStructSolve: return launch_cluster(k_struct_solve, a, n_units, 1, s);
+        case kStructLambda2: return launch_cluster(k_struct_lambda2, a, n_units, 2, s);
+        case kStructMixing: return launch_cluster(k_struct_mixing, a, n_units, 1, s);
+        case kStructTraj: return launch_cluster(k_struct_traj, a, 1, 1, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace spl

@@ -51,6 +51,17 @@ class SolveInfo(C.Structure):
                 "l1_change": self.l1_change, "lambda_total": self.lambda_total}
 
 
+class SpectralInfo(C.Structure):
+    _fields_ = [("lambda2_re", C.c_double), ("lambda2_im", C.c_double), ("modulus", C.c_double),
+                ("phase", C.c_double), ("gap", C.c_double), ("change", C.c_double), ("iters", C.c_int32),
+                ("converged", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {"lambda2": complex(self.lambda2_re, self.lambda2_im), "modulus": self.modulus,
+                "phase": self.phase, "gap": self.gap, "change": self.change, "iters": self.iters,
+                "converged": bool(self.converged)}
+
+
 _LIB = None
 
 
@@ -79,6 +90,11 @@ def _lib():
             "splidar_plan_launch": (st, [p, p]),
             "splidar_plan_info": (st, [p, pinfo, p]),
             "splidar_plan_destroy": (None, [p]),
+            "splidar_structured_workspace_bytes": (sz, [i32, i32, i32]),
+            "splidar_stationary_structured": (st, [fp, i32, p, p, p, d, i32, p, p, sz, pinfo, p]),
+            "splidar_second_eigenvalue": (st, [fp, i32, p, p, p, p, d, i32, p, sz, C.POINTER(SpectralInfo), p]),
+            "splidar_mixing_steps": (st, [fp, d, p, d, i32, p, C.POINTER(i32), p, sz, p]),
+            "splidar_bin_trajectory": (st, [fp, d, p, i32, i32, p, p, p, sz, p]),
             "splidar_strerror": (C.c_char_p, [st]),
             "splidar_last_cuda_error": (C.c_int, []),
             "splidar_build_info": (C.c_char_p, []),
@@ -333,3 +349,95 @@ def solve_host(flux, t_d: float, dtype=torch.float64, mode: str = "factored", to
     pi_host.copy_(pi, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return HostResult(pi_host.numpy(), info)
+
+
+# ------------------------------------------------------------------ structured operator (f1, f2)
+def structured_workspace(n_bins: int, n_profiles: int = 1, n_items: int = 1, device=None) -> torch.Tensor:
+    n = int(_lib().splidar_structured_workspace_bytes(int(n_bins), int(n_profiles), int(n_items)))
+    if n == 0:
+        raise SplidarError(EINVAL, "splidar_structured_workspace_bytes")
+    t = torch.empty(n + 256, dtype=torch.uint8, device=device or "cuda")
+    off = (-t.data_ptr()) % 256
+    return t[off:off + n]
+
+
+def _items(shape, S, B, t_d):
+    S = np.ascontiguousarray(S, dtype=np.float64).reshape(-1)
+    B = np.ascontiguousarray(B, dtype=np.float64).reshape(-1)
+    T = np.ascontiguousarray(t_d, dtype=np.float64).reshape(-1)
+    if B.size != S.size or T.size != S.size or S.size < 1:
+        raise SplidarError(EINVAL, "S, B, t_d must have equal non-zero length")
+    n_prof = len({(float(a), float(b)) for a, b in zip(S, B)})
+    return S, B, T, n_prof
+
+
+def stationary_structured(shape, S, B, t_d, tol: float = 1e-12, max_iter: int = 10 ** 6,
+                          ws: torch.Tensor | None = None, stream=None, check: bool = True):
+    """f2: pi for (S[m], B[m], t_d[m]) items by power iteration on the matrix-free operator (no P~0 is
+    stored). shape.signal are relative pulse weights (as sweep). Returns (pi [M, N] fp64, infos)."""
+    S, B, T, n_prof = _items(shape, S, B, t_d)
+    M, N = S.size, int(shape.n_bins)
+    ws = ws if ws is not None else structured_workspace(N, n_prof, M)
+    pi = torch.empty((M, N), dtype=torch.float64, device=ws.device)
+    infos = (SolveInfo * M)()
+    fa = _FluxArg(shape)
+    st = _lib().splidar_stationary_structured(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data,
+                                              float(tol), int(max_iter), pi.data_ptr(), ws.data_ptr(), ws.numel(),
+                                              infos, _stream(stream))
+    _check(st, "splidar_stationary_structured", allow=() if check else (ENOCONV,))
+    return pi, [i.as_dict() for i in infos]
+
+
+def second_eigenvalue(shape, S, B, t_d, pi: torch.Tensor, tol: float = 1e-13, max_iter: int = 10 ** 5,
+                      ws: torch.Tensor | None = None, stream=None, check: bool = True) -> list:
+    """f1: lambda_2 of P~ per item (modulus, phase in [0, pi], gap); pi = the items' stationary vectors
+    [M, N] on the device."""
+    S, B, T, n_prof = _items(shape, S, B, t_d)
+    M, N = S.size, int(shape.n_bins)
+    if not pi.is_cuda or pi.dtype != torch.float64 or pi.numel() != M * N or not pi.is_contiguous():
+        raise SplidarError(EINVAL, "second_eigenvalue: pi must be a contiguous CUDA fp64 [M, N] tensor")
+    ws = ws if ws is not None else structured_workspace(N, n_prof, M, device=pi.device)
+    infos = (SpectralInfo * M)()
+    fa = _FluxArg(shape)
+    st = _lib().splidar_second_eigenvalue(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data,
+                                          pi.data_ptr(), float(tol), int(max_iter), ws.data_ptr(), ws.numel(),
+                                          infos, _stream(stream))
+    _check(st, "splidar_second_eigenvalue", allow=() if check else (ENOCONV,))
+    return [i.as_dict() for i in infos]
+
+
+def mixing_steps(flux, t_d: float, pi: torch.Tensor, eps: float = 1e-3, max_steps: int = 10 ** 5,
+                 ws: torch.Tensor | None = None, stream=None, check: bool = True):
+    """f1: smallest n with max_i 1/2 ||e_i P~^n - pi||_1 <= eps. Returns (n, per-start n_i int32 tensor)."""
+    N = int(flux.n_bins)
+    if not pi.is_cuda or pi.dtype != torch.float64 or pi.numel() != N or not pi.is_contiguous():
+        raise SplidarError(EINVAL, "mixing_steps: pi must be a contiguous CUDA fp64 [N] tensor")
+    ws = ws if ws is not None else structured_workspace(N, 1, N, device=pi.device)
+    per = torch.empty(N, dtype=torch.int32, device=pi.device)
+    out = C.c_int32(0)
+    fa = _FluxArg(flux)
+    st = _lib().splidar_mixing_steps(C.byref(fa.s), float(t_d), pi.data_ptr(), float(eps), int(max_steps),
+                                     per.data_ptr(), C.byref(out), ws.data_ptr(), ws.numel(), _stream(stream))
+    _check(st, "splidar_mixing_steps", allow=() if check else (ENOCONV,))
+    return out.value, per
+
+
+def bin_trajectory(flux, t_d: float, start: torch.Tensor, bin: int, steps: int, ws: torch.Tensor | None = None,
+                   stream=None):
+    """f1: (start P~^n)[bin] for n = 0..steps. Returns (traj [steps + 1], start P~^steps [N])."""
+    N = int(flux.n_bins)
+    if not start.is_cuda or start.dtype != torch.float64 or start.numel() != N or not start.is_contiguous():
+        raise SplidarError(EINVAL, "bin_trajectory: start must be a contiguous CUDA fp64 [N] tensor")
+    ws = ws if ws is not None else structured_workspace(N, 1, 1, device=start.device)
+    traj = torch.empty(int(steps) + 1, dtype=torch.float64, device=start.device)
+    fin = torch.empty(N, dtype=torch.float64, device=start.device)
+    fa = _FluxArg(flux)
+    _check(_lib().splidar_bin_trajectory(C.byref(fa.s), float(t_d), start.data_ptr(), int(bin), int(steps),
+                                         traj.data_ptr(), fin.data_ptr(), ws.data_ptr(), ws.numel(),
+                                         _stream(stream)), "splidar_bin_trajectory")
+    return traj, fin
+
+
+def flux_items(flux):
+    """(shape, S, B) for one flux in the items convention: shape = flux, S = 1, B = flux.background."""
+    return flux, np.array([1.0]), np.array([float(flux.background)])

@@ -349,3 +349,165 @@ def test_golden_config1_regression(oracle_lib):
     for r, row in g["rows"].items():
         assert np.max(np.abs(P[int(r)] - np.array(row))) <= 1e-15
     assert np.sum(np.abs(oracle.stationary_dense(P) - np.array(g["pi"]))) <= 1e-14
+
+
+# ===================================================== f1: spectral analysis (§4, P:207-222)
+# Pins of oracle.second_eigenvalue / mixing_steps / bin_trajectory against closed forms derived by
+# hand (two-state chain, a rotation-plus-teleport 3-state chain with a complex pair, the S = 0
+# circulant with its DFT spectrum incl. the phase the shift l adds), and against the dynamics they
+# describe (decay rate and oscillation of a trajectory on a model chain).
+
+@pytest.mark.parametrize("a,b", [(0.1, 0.2), (0.3, 0.45), (0.7, 0.9), (0.05, 0.95)])
+def test_f1_two_state_lambda2(a, b):
+    """[[1-a, a], [b, 1-b]]: eigenvalues 1 and 1 - a - b; phase 0 if positive, pi if negative."""
+    P = np.array([[1 - a, a], [b, 1 - b]])
+    lam = oracle.second_eigenvalue(P)
+    assert abs(lam - (1 - a - b)) <= 1e-14
+    ph = math.atan2(lam.imag, lam.real)
+    assert abs(ph - (0.0 if 1 - a - b >= 0 else math.pi)) <= 1e-14
+
+
+@pytest.mark.parametrize("alpha", [0.3, 0.8, 0.95])
+def test_f1_rotation_chain_complex_pair(alpha):
+    """P = alpha Cyc + (1 - alpha) J / 3 (Cyc the cyclic shift, J all ones): Cyc has eigenvalues
+    1, w, w^2 (w = e^{2 pi i / 3}) on eigenvectors orthogonal to 1 except the first, and J kills
+    those, so lambda_2 = alpha e^{2 pi i / 3}: modulus alpha, phase 2 pi / 3."""
+    Cyc = np.roll(np.eye(3), 1, axis=1)
+    P = alpha * Cyc + (1 - alpha) * np.ones((3, 3)) / 3
+    lam = oracle.second_eigenvalue(P)
+    assert abs(abs(lam) - alpha) <= 1e-13
+    assert abs(math.atan2(lam.imag, lam.real) - 2 * math.pi / 3) <= 1e-13
+
+
+@pytest.mark.parametrize("B,N,td", [(1.0, 64, 37.3), (3.0, 50, 75.0), (10.0, 33, 250.0), (0.5, 128, 10.0)])
+def test_f1_circulant_lambda2_with_phase(oracle_lib, B, N, td):
+    """S = 0: P~ is circulant with first-row entries a_m = c r^{(m - l) mod N} (pin P5), so its
+    eigenvalues are mu_k = sum_m a_m w^{mk} = w^{lk} (1 - r) / (1 - r w^k), w = e^{2 pi i / N}.
+    The modulus is largest at k = 1, N - 1 (a conjugate pair); its phase carries the shift l."""
+    f = Flux(100.0, N, (50.0,), (1.0,), (0.0,), B)
+    P = oracle.build_eq4(f, td)
+    l = math.ceil(math.fmod(td, 100.0) / (100.0 / N) - 1e-9) % N
+    r = math.exp(-B / N)
+    w = np.exp(2j * np.pi / N)
+    mu = w ** (l * 1) * (1 - r) / (1 - r * w)
+    want = complex(mu.real, abs(mu.imag))
+    lam = oracle.second_eigenvalue(P)
+    assert abs(abs(lam) - abs(mu)) <= 1e-12
+    assert abs(lam - want) <= 1e-10
+
+
+def test_f1_brute_force_char_poly():
+    """n = 8 random positive stochastic matrix: the characteristic polynomial in exact rationals
+    (Faddeev-LeVerrier) vanishes at the oracle's lambda_2, and no root of it other than 1 has a
+    larger modulus (roots located by the argument principle on a circle through |lambda_2|)."""
+    rng = np.random.default_rng(8)
+    n = 8
+    Q = [[Fraction(int(rng.integers(1, 50))) for _ in range(n)] for _ in range(n)]
+    for row in Q:
+        s = sum(row)
+        row[:] = [x / s for x in row]
+    P = np.array([[float(x) for x in row] for row in Q])
+    # Faddeev-LeVerrier: c_n = 1, M_k = A M_{k-1} + c_{n-k+1} I, c_{n-k} = -tr(A M_k) / k
+    I = [[Fraction(int(i == j)) for j in range(n)] for i in range(n)]
+    def mul(X, Y):
+        return [[sum(X[i][k] * Y[k][j] for k in range(n)) for j in range(n)] for i in range(n)]
+    c = [Fraction(0)] * (n + 1)
+    c[n] = Fraction(1)
+    Mk = [[Fraction(0)] * n for _ in range(n)]
+    for k in range(1, n + 1):
+        Mk = mul(Q, Mk)
+        for i in range(n):
+            Mk[i][i] += c[n - k + 1]
+        AM = mul(Q, Mk)
+        c[n - k] = -sum(AM[i][i] for i in range(n)) / k
+    coef = [float(x) for x in c]                        # ascending powers
+    def poly(z):
+        return sum(cf * z ** p for p, cf in enumerate(coef))
+    assert abs(poly(1.0)) <= 1e-12                      # stochastic: 1 is a root
+    lam = oracle.second_eigenvalue(P)
+    assert abs(poly(lam)) <= 1e-10
+    # number of roots inside |z| < rho by the argument principle (numerical winding number)
+    def n_roots_inside(rho):
+        t = np.linspace(0, 2 * np.pi, 20001)
+        z = rho * np.exp(1j * t)
+        v = np.array([poly(x) for x in z])
+        return int(round(np.sum(np.diff(np.unwrap(np.angle(v)))) / (2 * np.pi)))
+    rho = abs(lam)
+    mult = 2 if abs(lam.imag) > 1e-12 else 1
+    assert n_roots_inside(rho * (1 + 1e-6)) - n_roots_inside(rho * (1 - 1e-6)) == mult
+    assert n_roots_inside(min(0.999999, rho * (1 + 1e-6))) == n - 1   # only the Perron root is outside
+
+
+def test_f1_mixing_closed_forms():
+    """Rank-1 chain (every row = pi) mixes in one step. Two-state chain: e_i P^n - pi =
+    lambda^n (e_i - pi), so TV_i(n) = |lambda|^n (1 - pi_i) and n = ceil(log(eps / max_i(1 - pi_i)) /
+    log|lambda|)."""
+    pi = np.array([0.2, 0.5, 0.3])
+    n, first = oracle.mixing_steps(np.tile(pi, (3, 1)), pi, 1e-3)
+    assert n == 1 and np.all(first == 1)
+    for a, b, eps in ((0.1, 0.2, 1e-3), (0.6, 0.9, 1e-4), (0.05, 0.05, 1e-3)):
+        P = np.array([[1 - a, a], [b, 1 - b]])
+        p = np.array([b / (a + b), a / (a + b)])
+        lam = abs(1 - a - b)
+        want = math.ceil(math.log(eps / np.max(1 - p)) / math.log(lam))
+        n, first = oracle.mixing_steps(P, p, eps)
+        assert n == want
+        assert list(first) == [math.ceil(math.log(eps / (1 - p[i])) / math.log(lam)) for i in range(2)]
+
+
+def test_f1_mixing_circulant_symmetry_and_background_trend(oracle_lib):
+    """S = 0: every start mixes in the same number of steps (circulant symmetry). Paper §4.1:
+    mixing slows as B grows ("gap decreases as background B increases"): non-decreasing over
+    B in {0.1, 3, 6, 9} at fixed S."""
+    f = Flux(100.0, 64, (50.0,), (1.0,), (0.0,), 3.0)
+    P = oracle.build_eq4(f, 75.0)
+    n, first = oracle.mixing_steps(P, np.full(64, 1 / 64), 1e-3)
+    assert np.all(first == n)
+    steps = []
+    for B in (0.1, 3.0, 6.0, 9.0):
+        g = Flux(100.0, 128, (40.0,), (1.0,), (2.0,), B)
+        P = oracle.build_eq4(g, 75.0)
+        steps.append(oracle.mixing_steps(P, oracle.stationary_dense(P), 1e-3)[0])
+    assert steps == sorted(steps)
+
+
+def test_f1_trajectory_closed_forms():
+    """start = pi stays at pi[bin]; two-state chain from e_1: pi_1 + (1 - pi_1) lambda^n."""
+    a, b = 0.3, 0.5
+    P = np.array([[1 - a, a], [b, 1 - b]])
+    p = np.array([b / (a + b), a / (a + b)])
+    tr, _ = oracle.bin_trajectory(P, p, 0, 20)
+    assert np.max(np.abs(tr - p[0])) <= 1e-15
+    tr, _ = oracle.bin_trajectory(P, np.array([1.0, 0.0]), 0, 30)
+    n = np.arange(31)
+    assert np.max(np.abs(tr - (p[0] + (1 - p[0]) * (1 - a - b) ** n))) <= 1e-15
+
+
+@pytest.mark.parametrize("S,B,td", [(2.0, 3.0, 75.0), (1.0, 6.0, 75.0), (1.0, 9.0, 95.0)])
+def test_f1_trajectory_decay_matches_lambda2(oracle_lib, S, B, td):
+    """Fig. 4 caption: amplitude decays at |lambda_2| per step and oscillates with
+    arg(lambda_2). Checked on a model chain: the residual r_n = traj_n - pi[bin] from a point start
+    fits r_n ~ Re(c lambda_2^n) over the tail (least squares in (Re c, Im c) with the oracle's
+    lambda_2) to 1e-4 relative over 30 steps once the third mode has decayed, while the same fit with
+    |lambda_2| perturbed by 2% fails."""
+    f = Flux(100.0, 96, (40.0,), (0.8,), (S,), B)
+    P = oracle.build_eq4(f, td)
+    pi = oracle.stationary_dense(P)
+    lam = oracle.second_eigenvalue(P)
+    start = np.zeros(96)
+    start[5] = 1.0
+    mods = np.sort(np.abs(np.linalg.eigvals(P)))[::-1]
+    third = mods[3] if abs(mods[1] - mods[2]) < 1e-9 else mods[2]   # next mode after the pair / real root
+    n0 = int(math.ceil(math.log(1e-5) / math.log(third / abs(lam))))
+    n1 = n0 + 30
+    bin_ = int(np.argmax(pi))
+    tr, _ = oracle.bin_trajectory(P, start, bin_, n1)
+    r = tr[n0:n1 + 1] - pi[bin_]
+    n = np.arange(n0, n1 + 1)
+
+    def fit_err(lm):
+        A = np.stack([(lm ** n).real, -(lm ** n).imag], axis=1) if abs(lm.imag) > 0 else (lm.real ** n)[:, None]
+        coef, *_ = np.linalg.lstsq(A, r, rcond=None)
+        return np.max(np.abs(A @ coef - r)) / np.max(np.abs(r))
+    good, bad = fit_err(lam), fit_err(lam * 1.02)
+    assert good <= 1e-4 and bad > 1e-3 and bad > 30 * good, (good, bad)

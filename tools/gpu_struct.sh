@@ -1,0 +1,3 @@
+set -x
+python __graft_entry__.py > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests/test_structured_gpu.py -m gpu -q --timeout=240 -x > gpurun_out/pytest_struct.log 2>&1; tail -30 gpurun_out/pytest_struct.log
