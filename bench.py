@@ -41,7 +41,10 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "grid"])
+    p.add_argument("--path", default="dense", choices=["dense", "structured", "spectral"],
+                   help="dense: the north-star path (P~0 in HBM + GEMV power iteration); structured: "
+                        "SURVEY f2 matrix-free solve; spectral: SURVEY f1 solve + lambda_2")
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     p.add_argument("--mode", default="factored", choices=["factored", "exp"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -65,8 +68,11 @@ def workload_items(name, rank=0, world=1):
     c5: every rank solves t_d = 430 and its 16-value shard of a 16 * world-point dead-time sweep over
     [10, 500] (world = 1: the config's own linspace(10, 500, 16)); other configs: every rank solves
     an independent replica of the config's items (weak scaling, no collective)."""
-    from workloads import config
+    from workloads import config, spectral_grid
     from paper_2509_20500_b200.shard import shard
+    if name == "grid":
+        w = spectral_grid()
+        return w, [(it.flux, [it.t_d]) for it in shard(w.items, rank, world)]
     k = int(name[1])
     w = config(k)
     if k == 5:
@@ -309,6 +315,172 @@ def run_e2e(args, w, groups, st, world):
                     "copy to pinned host memory every step"}
 
 
+# ------------------------------------------------------------------------------- structured paths
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
+FLOPS_PER_ELEM = {"solve": 12, "lambda2": 48}      # algorithmic fp64 flops per bin per product
+
+
+def _shape_groups(groups):
+    """Items -> plans: one plan per pulse shape (t_r, N, tau, sigma, relative weights); items carry
+    (S = total signal, B, t_d)."""
+    from workloads import Flux
+    plans = {}
+    for f, tds in groups:
+        tot = float(sum(f.signal))
+        rel = tuple(x / tot for x in f.signal) if tot > 0 else tuple(f.signal)
+        key = (f.t_r, f.n_bins, tuple(f.tau), tuple(f.sigma), rel)
+        shape = Flux(f.t_r, f.n_bins, f.tau, f.sigma, rel, 1.0)
+        e = plans.setdefault(key, [shape, [], [], []])
+        for td in tds:
+            e[1].append(tot if tot > 0 else 1.0)
+            e[2].append(f.background)
+            e[3].append(td)
+    return list(plans.values())
+
+
+def run_struct(args, rank, world, dev):
+    import torch
+    import paper_2509_20500_b200 as spl
+    w, groups = workload_items(args.workload, rank, world)
+    kind = "solve" if args.path == "structured" else "lambda2"
+    sg = _shape_groups(groups)
+    N = groups[0][0].n_bins
+    solve_plans, l2_plans = [], []
+    for shape, S, B, T in sg:
+        sp = spl.StructPlan("solve", shape, S, B, T)
+        solve_plans.append(sp)
+        if kind == "lambda2":
+            l2_plans.append(spl.StructPlan("lambda2", shape, S, B, T, pi=sp.pi))
+    n_items = sum(len(g[1]) for g in sg)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for p in solve_plans:
+            p.launch()
+        for p in l2_plans:
+            p.launch()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev)
+    time.sleep(0.25)
+    t_total, k_ms, products = 0.0, [], 0
+    main_plans = l2_plans if kind == "lambda2" else solve_plans
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_total += e0.elapsed_time(e1) / 1e3
+        ms = 0.0
+        products = 0
+        for p in main_plans:
+            infos, kms = p.info()
+            ms += kms
+            products += sum(i["iters"] for i in infos)
+        k_ms.append(ms)
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    from paper_2509_20500_b200.shard import max_over_ranks
+    t_total = max_over_ranks([t_total], device="cuda")[0]
+    K = args.steps
+    kernel_s = statistics.mean(k_ms) / 1e3
+    flops = FLOPS_PER_ELEM[kind] * N * products
+    achieved = flops / kernel_s / 1e12
+    iters = [[i["iters"] for i in p.info()[0]] for p in main_plans]
+    conv = all(i["converged"] for p in main_plans for i in p.info()[0])
+    unit = "solves/s" if kind == "solve" else "spectral analyses/s"
+    metric = ("stationary solves/s, matrix-free structured operator (SURVEY f2)" if kind == "solve" else
+              "spectral analyses/s (pi + lambda_2, modulus and phase; SURVEY f1)")
+    e2e = None if args.no_e2e else run_struct_e2e(args, sg, kind, world)
+    return {
+        "metric": metric, "value": n_items * K * world / t_total, "unit": unit, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": t_total / K * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE.json flux parameters / (S, B) grid)",
+        "config": {"workload": f"{args.workload}: {w.description}", "n_bins": N, "items_per_step": n_items,
+                   "path": args.path, "tol": 1e-12 if kind == "solve" else 1e-13,
+                   "l2": "no matrix is stored; per-item state lives in shared memory / registers",
+                   "parallelism": "single GPU" if world == 1 else f"dp{world}: items sharded, no collective"},
+        "converged": conv, "products_per_step": products,
+        "iterations_max": max(max(x) for x in iters), "iterations_sum": sum(sum(x) for x in iters),
+        "roofline": {"bound": "alu", "kernel": "k_struct_lambda2" if kind == "lambda2" else "k_struct_solve",
+                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "algorithmic_flops_per_bin_product": FLOPS_PER_ELEM[kind],
+                     "kernel_ms_per_step": statistics.mean(k_ms),
+                     "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (probe: 35.8 TFLOP/s DFMA)",
+                     "note": "FP64 issue is not the limiter: per-product barriers and scan latency are (DESIGN.md)"},
+        "clocks": clk, "e2e": e2e,
+        "gpu_launches": (len(main_plans) + (len(solve_plans) if kind == "lambda2" else 0)) * 6 * K,
+        "impl": "ours", "lib": spl.lib_path(),
+    }
+
+
+def run_struct_e2e(args, sg, kind, world):
+    """Through the public one-shot calls with host theta and the results copied to pinned host memory."""
+    import torch
+    import paper_2509_20500_b200 as spl
+    n = sum(len(g[1]) for g in sg)
+    N = sg[0][0].n_bins
+    pi_host = torch.empty((n, N), dtype=torch.float64, pin_memory=True)
+
+    def one():
+        row = 0
+        for shape, S, B, T in sg:
+            pi, _ = spl.stationary_structured(shape, S, B, T)
+            if kind == "lambda2":
+                spl.second_eigenvalue(shape, S, B, T, pi)
+            pi_host[row:row + len(S)].copy_(pi, non_blocking=True)
+            row += len(S)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt_s = time.perf_counter() - t0
+    from paper_2509_20500_b200.shard import max_over_ranks
+    dt_s = max_over_ranks([dt_s], device="cuda")[0]
+    h2d = sum(8 * (3 * len(shape.tau) + 1) + 24 * len(S) for shape, S, B, T in sg)
+    return {"value": n * args.steps * world / dt_s, "unit": "solves/s" if kind == "solve" else "spectral analyses/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": n * N * 8 + (n * 48 if kind == "lambda2" else 0),
+            "note": "host wall clock; validation, grouping and upload of theta, kernels, pi to pinned host memory"}
+
+
+def run_oracle_spectral(args):
+    """Oracle for the spectral path: Eq. 4 matrix, dense pi and numpy eigvals, on a bounded sample."""
+    import oracle
+    w, groups = workload_items(args.workload)
+    N = groups[0][0].n_bins
+    if N > 2048:
+        return None
+    t0 = time.perf_counter()
+    n = 0
+    for f, tds in groups:
+        for td in tds:
+            P = oracle.build_eq4(f, td)
+            oracle.stationary_dense(P)
+            oracle.second_eigenvalue(P)
+            n += 1
+            if time.perf_counter() - t0 > 10.0:
+                break
+        if time.perf_counter() - t0 > 10.0:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "spectral analyses/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{args.workload}: {n} items (Eq. 4 matrix with OpenMP rows, dense Gaussian-elimination pi, "
+                      f"numpy.linalg.eigvals), about 10 s"}
+
+
 # ------------------------------------------------------------------------------- oracle arm
 def run_oracle_sample(args, iters_per_item=None):
     """The CPU oracle as it stands on a bounded sample of the same workload: R rows of the Eq. 4
@@ -375,9 +547,15 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    line = run_ours(args, rank, world, dev)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = run_oracle_sample(args, line["iterations"])
+    if args.path == "dense":
+        line = run_ours(args, rank, world, dev)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = run_oracle_sample(args, line["iterations"])
+    else:
+        line = run_struct(args, rank, world, dev)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = (run_oracle_sample(args) if args.path == "structured"
+                                    else run_oracle_spectral(args))
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

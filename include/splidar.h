@@ -218,6 +218,24 @@ splidar_status splidar_second_eigenvalue(const splidar_flux *shape, int32_t n_it
                                          int32_t max_iter, void *ws, size_t ws_bytes, splidar_spectral_info *info,
                                          void *stream);
 
+/* Structured plans: the items of splidar_stationary_structured (kind SPLIDAR_SPLAN_SOLVE) or
+ * splidar_second_eigenvalue (kind SPLIDAR_SPLAN_LAMBDA2; pi is then the input) validated and uploaded
+ * once; splidar_splan_launch only enqueues (step-1 vectors + the kernel, async, re-runnable);
+ * splidar_splan_info synchronises `stream`, fills the per-item info (either pointer may be NULL)
+ * and the device time of the last launch's kernel in ms (CUDA events recorded around it on
+ * `stream`; may be NULL); SPLIDAR_ENOCONV if an item did not converge. The two calls above are
+ * create + launch + info + destroy. */
+#define SPLIDAR_SPLAN_SOLVE 0
+#define SPLIDAR_SPLAN_LAMBDA2 1
+typedef struct splidar_splan_s *splidar_splan;
+splidar_status splidar_splan_create(splidar_splan *plan, int32_t kind, const splidar_flux *shape, int32_t n_items,
+                                    const double *S, const double *B, const double *t_d, double tol,
+                                    int32_t max_iter, double *pi, void *ws, size_t ws_bytes, void *stream);
+splidar_status splidar_splan_launch(splidar_splan plan, void *stream);
+splidar_status splidar_splan_info(splidar_splan plan, splidar_solve_info *solve_info,
+                                  splidar_spectral_info *spectral_info, float *kernel_ms, void *stream);
+void splidar_splan_destroy(splidar_splan plan);
+
 /* f1: mixing steps (§4.1: "the number of steps n such that P~^n approaches the stationary
  * distribution"): the smallest n >= 1 with max_i 1/2 ||e_i^T P~^n - pi||_1 <= eps over all start
  * bins i (every row of P~^n), found per start as its first n_i (TV to stationarity is

@@ -649,6 +649,8 @@ static VecPtrs svec_ptrs(char *ws, const SLayout &L) {
 struct Prep {
     StructArgs a;
     SLayout L;
+    const FluxDev *flux_dev;
+    VecPtrs vp;
     std::vector<int> prof, l;
     std::vector<double> scal;   // [M][8] host copy (after read_scal)
 };
@@ -695,7 +697,8 @@ static splidar_status struct_prepare(const splidar_flux *shape, int n_items, con
     char *wsb = static_cast<char *>(ws);
     SPL_CUDA(cudaMemcpyAsync(wsb + L.flux, fl.data(), sizeof(FluxDev) * (size_t)M, cudaMemcpyHostToDevice, s));
     VecPtrs vp = svec_ptrs(wsb, L);
-    SPL_CUDA(launch_flux_vectors(reinterpret_cast<const FluxDev *>(wsb + L.flux), M, N, vp, N, s));
+    p->flux_dev = reinterpret_cast<const FluxDev *>(wsb + L.flux);
+    p->vp = vp;
     SPL_CUDA(cudaMemcpyAsync(wsb + L.prof, p->prof.data(), sizeof(int) * (size_t)n_items, cudaMemcpyHostToDevice, s));
     SPL_CUDA(cudaMemcpyAsync(wsb + L.lsh, p->l.data(), sizeof(int) * (size_t)n_items, cudaMemcpyHostToDevice, s));
     StructArgs *a = &p->a;
@@ -726,6 +729,25 @@ static splidar_status read_scal(Prep *p, cudaStream_t s) {
     return SPLIDAR_OK;
 }
 
+// Structured plans: items validated and uploaded once; each launch recomputes the step-1 vectors
+// and runs the kernel (async); CUDA events around the kernel give its device time.
+struct splidar_splan_s {
+    Prep p;
+    int kind = 0;
+    int n_items = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<unsigned char> dummy;
+};
+
+static splidar_status splan_launch_impl(splidar_splan_s *pl, cudaStream_t s) {
+    const Prep &p = pl->p;
+    SPL_CUDA(launch_flux_vectors(p.flux_dev, p.L.M, p.a.N, p.vp, p.a.N, s));
+    SPL_CUDA(cudaEventRecord(pl->ev0, s));
+    SPL_CUDA(launch_struct(pl->kind == 0 ? kStructSolve : kStructLambda2, p.a, pl->n_items, s));
+    SPL_CUDA(cudaEventRecord(pl->ev1, s));
+    return SPLIDAR_OK;
+}
+
 extern "C" {
 
 size_t splidar_structured_workspace_bytes(int32_t n_bins, int32_t n_profiles, int32_t n_items) {
@@ -734,72 +756,119 @@ size_t splidar_structured_workspace_bytes(int32_t n_bins, int32_t n_profiles, in
     return struct_layout(n_bins, n_profiles, n_items).total;
 }
 
+void splidar_splan_destroy(splidar_splan plan) {
+    if (!plan) return;
+    if (plan->ev0) cudaEventDestroy(plan->ev0);
+    if (plan->ev1) cudaEventDestroy(plan->ev1);
+    delete plan;
+}
+
+splidar_status splidar_splan_create(splidar_splan *plan, int32_t kind, const splidar_flux *shape, int32_t n_items,
+                                    const double *S, const double *B, const double *t_d, double tol,
+                                    int32_t max_iter, double *pi, void *ws, size_t ws_bytes, void *stream) {
+    if (!plan) return SPLIDAR_EINVAL;
+    *plan = nullptr;
+    if ((kind != SPLIDAR_SPLAN_SOLVE && kind != SPLIDAR_SPLAN_LAMBDA2) || !pi || !(tol > 0.0) ||
+        !std::isfinite(tol) || max_iter < 1)
+        return SPLIDAR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    splidar_splan_s *pl = new splidar_splan_s();
+    splidar_status st = struct_prepare(shape, n_items, S, B, t_d, n_items, ws, ws_bytes, s, &pl->p);
+    if (st) { delete pl; return st; }
+    pl->kind = kind;
+    pl->n_items = n_items;
+    pl->p.a.tol = tol;
+    pl->p.a.max_iter = max_iter;
+    pl->p.a.pi = pi;
+    cudaError_t e = cudaEventCreate(&pl->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&pl->ev1);
+    if (e != cudaSuccess) { splidar_splan_destroy(pl); return cuda_status(e); }
+    *plan = pl;
+    return SPLIDAR_OK;
+}
+
+splidar_status splidar_splan_launch(splidar_splan plan, void *stream) {
+    if (!plan) return SPLIDAR_EINVAL;
+    return splan_launch_impl(plan, (cudaStream_t)stream);
+}
+
+splidar_status splidar_splan_info(splidar_splan plan, splidar_solve_info *solve_info,
+                                  splidar_spectral_info *spectral_info, float *kernel_ms, void *stream) {
+    if (!plan) return SPLIDAR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    Prep &p = plan->p;
+    const int n = plan->n_items;
+    std::vector<SolveState> hs;
+    std::vector<SpecOut> hp;
+    if (plan->kind == SPLIDAR_SPLAN_SOLVE) {
+        hs.resize((size_t)n);
+        SPL_CUDA(cudaMemcpyAsync(hs.data(), p.a.st, sizeof(SolveState) * hs.size(), cudaMemcpyDeviceToHost, s));
+    } else {
+        hp.resize((size_t)n);
+        SPL_CUDA(cudaMemcpyAsync(hp.data(), p.a.spec, sizeof(SpecOut) * hp.size(), cudaMemcpyDeviceToHost, s));
+    }
+    splidar_status st = read_scal(&p, s);
+    if (st) return st;
+    if (kernel_ms) SPL_CUDA(cudaEventElapsedTime(kernel_ms, plan->ev0, plan->ev1));
+    bool all = true;
+    for (int i = 0; i < n; ++i) {
+        if (plan->kind == SPLIDAR_SPLAN_SOLVE) {
+            const SolveState &h = hs[(size_t)i];
+            all = all && h.converged;
+            if (solve_info) {
+                splidar_solve_info &o = solve_info[i];
+                o.iters = h.iters;
+                o.converged = h.converged;
+                o.shift_l = h.l;
+                o.reserved = 0;
+                o.l1_change = h.change;
+                o.lambda_total = p.scal[(size_t)p.prof[(size_t)i] * 8];
+            }
+        } else {
+            const SpecOut &h = hp[(size_t)i];
+            all = all && h.converged;
+            if (spectral_info) {
+                splidar_spectral_info &o = spectral_info[i];
+                o.lambda2_re = h.re;
+                o.lambda2_im = h.im;
+                o.modulus = std::hypot(h.re, h.im);
+                o.phase = std::atan2(h.im, h.re);
+                o.gap = 1.0 - o.modulus;
+                o.change = h.change;
+                o.iters = h.iters;
+                o.converged = h.converged;
+            }
+        }
+    }
+    return all ? SPLIDAR_OK : SPLIDAR_ENOCONV;
+}
+
 splidar_status splidar_stationary_structured(const splidar_flux *shape, int32_t n_items, const double *S,
                                              const double *B, const double *t_d, double tol, int32_t max_iter,
                                              double *pi, void *ws, size_t ws_bytes, splidar_solve_info *info,
                                              void *stream) {
-    if (!pi || !(tol > 0.0) || !std::isfinite(tol) || max_iter < 1) return SPLIDAR_EINVAL;
-    cudaStream_t s = (cudaStream_t)stream;
-    Prep p;
-    splidar_status st = struct_prepare(shape, n_items, S, B, t_d, n_items, ws, ws_bytes, s, &p);
+    splidar_splan pl;
+    splidar_status st = splidar_splan_create(&pl, SPLIDAR_SPLAN_SOLVE, shape, n_items, S, B, t_d, tol, max_iter,
+                                             pi, ws, ws_bytes, stream);
     if (st) return st;
-    p.a.tol = tol;
-    p.a.max_iter = max_iter;
-    p.a.pi = pi;
-    SPL_CUDA(launch_struct(kStructSolve, p.a, n_items, s));
-    std::vector<SolveState> hs((size_t)n_items);
-    SPL_CUDA(cudaMemcpyAsync(hs.data(), p.a.st, sizeof(SolveState) * hs.size(), cudaMemcpyDeviceToHost, s));
-    if ((st = read_scal(&p, s))) return st;
-    bool all = true;
-    for (int i = 0; i < n_items; ++i) {
-        const SolveState &h = hs[(size_t)i];
-        all = all && h.converged;
-        if (info) {
-            splidar_solve_info &o = info[i];
-            o.iters = h.iters;
-            o.converged = h.converged;
-            o.shift_l = h.l;
-            o.reserved = 0;
-            o.l1_change = h.change;
-            o.lambda_total = p.scal[(size_t)p.prof[(size_t)i] * 8];
-        }
-    }
-    return all ? SPLIDAR_OK : SPLIDAR_ENOCONV;
+    st = splidar_splan_launch(pl, stream);
+    if (!st) st = splidar_splan_info(pl, info, nullptr, nullptr, stream);
+    splidar_splan_destroy(pl);
+    return st;
 }
 
 splidar_status splidar_second_eigenvalue(const splidar_flux *shape, int32_t n_items, const double *S,
                                          const double *B, const double *t_d, const double *pi, double tol,
                                          int32_t max_iter, void *ws, size_t ws_bytes, splidar_spectral_info *info,
                                          void *stream) {
-    if (!pi || !(tol > 0.0) || !std::isfinite(tol) || max_iter < 1) return SPLIDAR_EINVAL;
-    cudaStream_t s = (cudaStream_t)stream;
-    Prep p;
-    splidar_status st = struct_prepare(shape, n_items, S, B, t_d, n_items, ws, ws_bytes, s, &p);
+    splidar_splan pl;
+    splidar_status st = splidar_splan_create(&pl, SPLIDAR_SPLAN_LAMBDA2, shape, n_items, S, B, t_d, tol,
+                                             max_iter, const_cast<double *>(pi), ws, ws_bytes, stream);
     if (st) return st;
-    p.a.tol = tol;
-    p.a.max_iter = max_iter;
-    p.a.pi = const_cast<double *>(pi);
-    SPL_CUDA(launch_struct(kStructLambda2, p.a, n_items, s));
-    std::vector<SpecOut> hs((size_t)n_items);
-    SPL_CUDA(cudaMemcpyAsync(hs.data(), p.a.spec, sizeof(SpecOut) * hs.size(), cudaMemcpyDeviceToHost, s));
-    if ((st = read_scal(&p, s))) return st;
-    bool all = true;
-    for (int i = 0; i < n_items; ++i) {
-        const SpecOut &h = hs[(size_t)i];
-        all = all && h.converged;
-        if (info) {
-            splidar_spectral_info &o = info[i];
-            o.lambda2_re = h.re;
-            o.lambda2_im = h.im;
-            o.modulus = std::hypot(h.re, h.im);
-            o.phase = std::atan2(h.im, h.re);
-            o.gap = 1.0 - o.modulus;
-            o.change = h.change;
-            o.iters = h.iters;
-            o.converged = h.converged;
-        }
-    }
-    return all ? SPLIDAR_OK : SPLIDAR_ENOCONV;
+    st = splidar_splan_launch(pl, stream);
+    if (!st) st = splidar_splan_info(pl, nullptr, info, nullptr, stream);
+    splidar_splan_destroy(pl);
+    return st;
 }
 
 splidar_status splidar_mixing_steps(const splidar_flux *flux, double t_d, const double *pi, double eps,
@@ -812,6 +881,7 @@ splidar_status splidar_mixing_steps(const splidar_flux *flux, double t_d, const 
     Prep p;
     splidar_status st = struct_prepare(flux, 1, &one, &bg, &t_d, N, ws, ws_bytes, s, &p);
     if (st) return st;
+    SPL_CUDA(launch_flux_vectors(p.flux_dev, p.L.M, N, p.vp, N, s));
     p.a.pi = const_cast<double *>(pi);
     p.a.eps = eps;
     p.a.max_iter = max_steps;
@@ -840,6 +910,7 @@ splidar_status splidar_bin_trajectory(const splidar_flux *flux, double t_d, cons
     Prep p;
     splidar_status st = struct_prepare(flux, 1, &one, &bg, &t_d, 1, ws, ws_bytes, s, &p);
     if (st) return st;
+    SPL_CUDA(launch_flux_vectors(p.flux_dev, p.L.M, flux->n_bins, p.vp, flux->n_bins, s));
     p.a.start = start;
     p.a.bin = bin;
     p.a.max_iter = steps;

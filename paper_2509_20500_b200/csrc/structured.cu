@@ -31,136 +31,188 @@ constexpr int kSMaxT = 512;                   // threads per CTA
 constexpr int kSMaxWarps = kSMaxT / 32;
 constexpr int kSMaxC = 16;                    // cluster size (> 8 is non-portable)
 constexpr int kSExK = 8;                      // values published per CTA per exchange
+constexpr int kSChunk = kSMaxT * kSE;         // positions per CTA of a multi-CTA cluster
+
+// Teams: the threads that own one item's N positions.
+//   kWarp     one warp (N <= 256): shuffles only, __syncwarp orders the pushes
+//   kBlock    one CTA (N <= 4096): block scan / sums through shared memory, __syncthreads
+//   kCluster  C CTAs (N > 4096): as kBlock inside each CTA, CTA totals exchanged over DSMEM and
+//             barrier.cluster
+enum { kWarp = 0, kBlock = 1, kCluster = 2 };
 
 __device__ __forceinline__ int sidx(int p) { return p + (p >> 3); }   // padded xbuf index
 
-// Shared-memory scratch (static part): two exchange areas (each [kSExK][kSMaxC]) and block scratch.
 struct SShared {
     double exA[kSExK * kSMaxC];
     double exB[kSExK * kSMaxC];
     double scr[kSExK * kSMaxWarps];
 };
 
-// Sum over the block of K values per thread; every thread gets the K totals (fixed order).
-template <int K>
-__device__ __forceinline__ void bsum(double (&v)[K], double *scr) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+__device__ __forceinline__ double warp_allsum(double x) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double x = v[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (lane == 0) scr[k * kSMaxWarps + warp] = x;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double s = 0.0;
-        for (int w = 0; w < nw; ++w) s += scr[k * kSMaxWarps + w];
-        v[k] = s;
-    }
-    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
 }
 
-// Inclusive scan over the block of V vectors held as 8 consecutive values per thread; tot[a] = the
-// block total of vector a (every thread).
-template <int V>
-__device__ __forceinline__ void bscan(double (&v)[V][kSE], double (&tot)[V], double *scr) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double x[V], ex[V];
-#pragma unroll
-    for (int a = 0; a < V; ++a) {
-#pragma unroll
-        for (int i = 1; i < kSE; ++i) v[a][i] += v[a][i - 1];
-        x[a] = v[a][kSE - 1];
+template <int MODE>
+struct Team {
+    cg::cluster_group cl;
+    int c, C;          // CTA rank in the cluster, cluster size
+    double *exA, *exB, *scr;
+
+    __device__ Team(SShared &sh, int C_) : cl(cg::this_cluster()) {
+        c = MODE == kCluster ? (int)cl.block_rank() : 0;
+        C = MODE == kCluster ? C_ : 1;
+        exA = sh.exA;
+        exB = sh.exB;
+        scr = sh.scr;
     }
+    __device__ __forceinline__ void barrier() {
+        if constexpr (MODE == kWarp) __syncwarp();
+        else if constexpr (MODE == kBlock) __syncthreads();
+        else cl.sync();
+    }
+    // sum over the team-local threads (warp or CTA) of K values; every thread gets the totals
+    template <int K>
+    __device__ __forceinline__ void sum(double (&v)[K]) {
+        if constexpr (MODE == kWarp) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1)
+            for (int k = 0; k < K; ++k) v[k] = warp_allsum(v[k]);
+        } else {
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const double x = warp_allsum(v[k]);
+                if (lane == 0) scr[k * kSMaxWarps + warp] = x;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double s = 0.0;
+                for (int w = 0; w < nw; ++w) s += scr[k * kSMaxWarps + w];
+                v[k] = s;
+            }
+            __syncthreads();
+        }
+    }
+    // inclusive scan over the team-local positions of V vectors (8 consecutive per thread);
+    // tot[a] = team-local total
+    template <int V>
+    __device__ __forceinline__ void scan(double (&v)[V][kSE], double (&tot)[V]) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        double x[V], ex[V];
 #pragma unroll
         for (int a = 0; a < V; ++a) {
-            const double y = __shfl_up_sync(0xffffffffu, x[a], o);
-            if (lane >= o) x[a] += y;
+#pragma unroll
+            for (int i = 1; i < kSE; ++i) v[a][i] += v[a][i - 1];
+            x[a] = v[a][kSE - 1];
         }
 #pragma unroll
-    for (int a = 0; a < V; ++a) {
-        ex[a] = __shfl_up_sync(0xffffffffu, x[a], 1);
-        if (lane == 0) ex[a] = 0.0;
-        if (lane == 31) scr[a * kSMaxWarps + warp] = x[a];
-    }
-    __syncthreads();
+        for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
-    for (int a = 0; a < V; ++a) {
-        double wex = 0.0, tt = 0.0;
-        for (int w = 0; w < nw; ++w) {
-            const double wt = scr[a * kSMaxWarps + w];
-            if (w < warp) wex += wt;
-            tt += wt;
+            for (int a = 0; a < V; ++a) {
+                const double y = __shfl_up_sync(0xffffffffu, x[a], o);
+                if (lane >= o) x[a] += y;
+            }
+#pragma unroll
+        for (int a = 0; a < V; ++a) {
+            ex[a] = __shfl_up_sync(0xffffffffu, x[a], 1);
+            if (lane == 0) ex[a] = 0.0;
         }
-        tot[a] = tt;
-        const double e = wex + ex[a];
+        if constexpr (MODE == kWarp) {
 #pragma unroll
-        for (int i = 0; i < kSE; ++i) v[a][i] += e;
+            for (int a = 0; a < V; ++a) {
+                tot[a] = __shfl_sync(0xffffffffu, x[a], 31);
+#pragma unroll
+                for (int i = 0; i < kSE; ++i) v[a][i] += ex[a];
+            }
+        } else {
+            const int nw = blockDim.x >> 5;
+#pragma unroll
+            for (int a = 0; a < V; ++a)
+                if (lane == 31) scr[a * kSMaxWarps + warp] = x[a];
+            __syncthreads();
+#pragma unroll
+            for (int a = 0; a < V; ++a) {
+                double wex = 0.0, tt = 0.0;
+                for (int w = 0; w < nw; ++w) {
+                    const double wt = scr[a * kSMaxWarps + w];
+                    if (w < warp) wex += wt;
+                    tt += wt;
+                }
+                tot[a] = tt;
+                const double e = wex + ex[a];
+#pragma unroll
+                for (int i = 0; i < kSE; ++i) v[a][i] += e;
+            }
+            __syncthreads();
+        }
     }
-    __syncthreads();
-}
-
-// Publish K values of this CTA (rank c) into slot c of every CTA's exchange area (DSMEM stores).
-template <int K>
-__device__ __forceinline__ void publish(cg::cluster_group &cl, double *ex, const double (&v)[K], int c, int C) {
-    const int t = threadIdx.x;
-    if (t < C * K) {
-        const int dst = t / K, k = t - dst * K;
-        double *r = cl.map_shared_rank(ex, dst);
-        r[k * kSMaxC + c] = v[k];
+    // exchange K per-CTA values through area ex (A or B) and synchronise the team; afterwards
+    // total(k) gives the sum over all CTAs and over the CTAs before this one. For a single-CTA
+    // team only the barrier remains (and the values are already the totals).
+    template <int K>
+    __device__ __forceinline__ void exchange(double *ex, const double (&v)[K]) {
+        if constexpr (MODE == kCluster) {
+            const int t = threadIdx.x;
+            if (t < C * K) {
+                const int dst = t / K, k = t - dst * K;
+                cl.map_shared_rank(ex, dst)[k * kSMaxC + c] = v[k];
+            }
+            cl.sync();
+        } else {
+            barrier();
+        }
     }
-}
-
-// After the barrier: totals over all CTAs and the exclusive prefix up to CTA c (fixed order).
-__device__ __forceinline__ void gather_sum(const double *ex, int k, int c, int C, double &total, double &before) {
-    double t = 0.0, b = 0.0;
-    for (int cc = 0; cc < C; ++cc) {
-        const double v = ex[k * kSMaxC + cc];
-        if (cc < c) b += v;
-        t += v;
+    __device__ __forceinline__ void total(const double *ex, int k, double own, double &tot, double &before) const {
+        if constexpr (MODE == kCluster) {
+            double t = 0.0, b = 0.0;
+            for (int cc = 0; cc < C; ++cc) {
+                const double v = ex[k * kSMaxC + cc];
+                if (cc < c) b += v;
+                t += v;
+            }
+            tot = t;
+            before = b;
+        } else {
+            tot = own;
+            before = 0.0;
+        }
     }
-    total = t;
-    before = b;
-}
+    __device__ __forceinline__ double *xdst(double *xbuf, int dst) {
+        if constexpr (MODE == kCluster) return cl.map_shared_rank(xbuf, dst);
+        else return xbuf;
+    }
+};
 
 struct Pos {
-    int N, C, c, chunk, p0;   // p0: first global position of this thread
-    int l;
+    int N, p0, l;   // p0: first global position of this thread
     __device__ bool valid(int e) const { return p0 + e < N; }
 };
 
+template <int MODE>
 __device__ __forceinline__ Pos make_pos(const StructArgs &a, int c, int l) {
     Pos p;
     p.N = a.N;
-    p.C = a.C;
-    p.c = c;
-    p.chunk = blockDim.x * kSE;
-    p.p0 = c * p.chunk + threadIdx.x * kSE;
+    p.p0 = (MODE == kCluster ? c * kSChunk : 0) + threadIdx.x * kSE;
     p.l = l;
     return p;
 }
 
-// The per-thread product core: given the gathered x (8 values), returns y at the thread's natural
-// positions after the cluster exchange of the scan totals. Publishes extra values (K - 1 of them
-// after the scan total at slot 0.. V-1) in the same exchange.
-// (Inlined into each kernel below; kept as code there for clarity of the barrier structure.)
-
 // Push y (natural positions p0 + e) into the gathered xbuf of the owner of (p + l) mod N.
-__device__ __forceinline__ void push(cg::cluster_group &cl, double *xbuf, const Pos &P, const double (&y)[kSE]) {
+template <int MODE>
+__device__ __forceinline__ void push(Team<MODE> &tm, double *xbuf, const Pos &P, const double (&y)[kSE]) {
 #pragma unroll
     for (int e = 0; e < kSE; ++e) {
         const int p = P.p0 + e;
         if (p < P.N) {
             int r = p + P.l;
             if (r >= P.N) r -= P.N;
-            const int dst = r / P.chunk;
-            const int li = r - dst * P.chunk;
-            double *remote = cl.map_shared_rank(xbuf, dst);
-            remote[sidx(li)] = y[e];
+            if constexpr (MODE == kCluster) {
+                tm.xdst(xbuf, r / kSChunk)[sidx(r % kSChunk)] = y[e];
+            } else {
+                xbuf[sidx(r)] = y[e];
+            }
         }
     }
 }
@@ -170,18 +222,24 @@ __device__ __forceinline__ void load8(const double *src, const Pos &P, double (&
     for (int e = 0; e < kSE; ++e) o[e] = P.valid(e) ? __ldg(src + P.p0 + e) : 0.0;
 }
 
+template <int MODE>
+__device__ __forceinline__ int item_index(int C) {
+    if constexpr (MODE == kCluster) return blockIdx.x / C;
+    else return blockIdx.x;
+}
+
 // ---------------------------------------------------------------------------------------------
 // f2: stationary solve. pi^0 = 1/N; v^{k+1} = v^k P~ (unnormalised; P~ is stochastic so the scale
 // stays ~1); pi^k = v^k / ||v^k||_1; stop after the first k with ||pi^{k+1} - pi^k||_1 < tol (the change
 // of product k is published with the scan totals of product k + 1, one exchange fewer per product).
+template <int MODE>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) {
-    cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
-    const int C = a.C, c = (int)cl.block_rank();
-    const int item = blockIdx.x / C;
+    Team<MODE> tm(sh, a.C);
+    const int item = item_index<MODE>(a.C);
     const int m = a.prof[item], l = a.lsh[item];
-    const Pos P = make_pos(a, c, l);
+    const Pos P = make_pos<MODE>(a, tm.c, l);
     const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
     const double eL = a.scal[m * 8 + 1];
     double wr[kSE], idr[kSE], yp[kSE];
@@ -195,22 +253,21 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
     }
     double s_prev = 1.0, dpart = 0.0, change = __longlong_as_double(0x7ff0000000000000ll);
     int k = 0, conv = 0;
-    cl.sync();
+    tm.barrier();
     for (;;) {
-        // phase 1: z = x / D, block scan; publish (scan total, change partial of product k - 1)
+        // phase 1: z = x / D, scan; publish (scan total, change partial of product k - 1)
         double v[1][kSE], tot[1];
 #pragma unroll
         for (int e = 0; e < kSE; ++e) v[0][e] = xbuf[sidx(threadIdx.x * kSE + e)] * idr[e];
-        bscan<1>(v, tot, sh.scr);
+        tm.template scan<1>(v, tot);
         {
             const double pv[2] = {tot[0], dpart};
-            publish<2>(cl, sh.exA, pv, c, C);
+            tm.template exchange<2>(tm.exA, pv);
         }
-        cl.sync();   // A
         double T, off, dummy;
-        gather_sum(sh.exA, 0, c, C, T, off);
+        tm.total(tm.exA, 0, tot[0], T, off);
         if (k > 0) {
-            gather_sum(sh.exA, 1, c, C, change, dummy);
+            tm.total(tm.exA, 1, dpart, change, dummy);
             if (change < a.tol) { conv = 1; break; }
             if (k >= a.max_iter || !(s_prev > 0.0) || !isfinite(change)) break;
         }
@@ -223,12 +280,11 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
             y[e] = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
             ps[0] += y[e];
         }
-        push(cl, xbuf, P, y);
-        bsum<1>(ps, sh.scr);
-        publish<1>(cl, sh.exB, ps, c, C);
-        cl.sync();   // B
+        push<MODE>(tm, xbuf, P, y);
+        tm.template sum<1>(ps);
+        tm.template exchange<1>(tm.exB, ps);
         double s, d2;
-        gather_sum(sh.exB, 0, c, C, s, d2);
+        tm.total(tm.exB, 0, ps[0], s, d2);
         double d[1] = {0.0};
         const double is = 1.0 / s, ip = 1.0 / s_prev;
 #pragma unroll
@@ -236,18 +292,17 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
             d[0] += fabs(y[e] * is - yp[e] * ip);
             yp[e] = y[e];
         }
-        bsum<1>(d, sh.scr);
+        tm.template sum<1>(d);
         dpart = d[0];
         s_prev = s;
         ++k;
     }
-    // pi^k = v^k / s_k at the natural positions
     double *out = a.pi + (size_t)item * P.N;
     const double is = 1.0 / s_prev;
 #pragma unroll
     for (int e = 0; e < kSE; ++e)
         if (P.valid(e)) out[P.p0 + e] = yp[e] * is;
-    if (c == 0 && threadIdx.x == 0) {
+    if (tm.c == 0 && threadIdx.x == 0) {
         SolveState st;
         st.l = l;
         st.iters = k;
@@ -267,7 +322,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
 // iterated, W = Q A, and the Ritz values are the eigenvalues of H = (W Q^T)(Q Q^T)^{-1}; a complex
 // pair lambda2, conj(lambda2) spans a real 2-D invariant subspace, so real arithmetic suffices. Basis
 // update: q1 = w1 / |w1|, q2 = (w2 - (w1.w2 / w1.w1) w1) / |w2| (applied as coefficients to the pushed
-// w, so the product needs two cluster exchanges). Stop when the dominant Ritz value moves < tol.
+// w, so the product needs two team exchanges). Stop when the dominant Ritz value moves < tol.
 
 __device__ __forceinline__ double hash_unit(uint32_t j, uint32_t salt) {   // deterministic in [-1, 1)
     uint32_t x = j * 0x9E3779B1u + salt * 0x85EBCA77u + 0x165667B1u;
@@ -275,15 +330,16 @@ __device__ __forceinline__ double hash_unit(uint32_t j, uint32_t salt) {   // de
     return (double)x * (2.0 / 4294967296.0) - 1.0;
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a) {
-    cg::cluster_group cl = cg::this_cluster();
-    extern __shared__ double xbuf[];    // [2][chunk + chunk / 8]: gathered w1, w2
+    extern __shared__ double xbuf[];    // [2][xs]: gathered w1, w2
     __shared__ SShared sh;
-    const int C = a.C, c = (int)cl.block_rank();
-    const int item = blockIdx.x / C;
+    Team<MODE> tm(sh, a.C);
+    const int item = item_index<MODE>(a.C);
     const int m = a.prof[item], l = a.lsh[item];
-    const Pos P = make_pos(a, c, l);
-    const int xs = P.chunk + P.chunk / 8;
+    const Pos P = make_pos<MODE>(a, tm.c, l);
+    const int chunk = MODE == kCluster ? kSChunk : (int)blockDim.x * kSE;
+    const int xs = chunk + chunk / 8;
     double *xb0 = xbuf, *xb1 = xbuf + xs;
     const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
     const double *pi = a.pi + (size_t)item * P.N;
@@ -294,11 +350,9 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
         const int p = P.p0 + e;
         wn[0][e] = P.valid(e) ? hash_unit((uint32_t)p, 1u) : 0.0;
         wn[1][e] = P.valid(e) ? hash_unit((uint32_t)p, 2u) : 0.0;
-        // gathered copies: xbuf[r] = q[(r - l) mod N]
-        const int r = P.p0 + e;
-        double g0 = 0.0, g1 = 0.0;
-        if (r < P.N) {
-            int src = r - l;
+        double g0 = 0.0, g1 = 0.0;       // gathered copies: xbuf[r] = q[(r - l) mod N]
+        if (p < P.N) {
+            int src = p - l;
             if (src < 0) src += P.N;
             g0 = hash_unit((uint32_t)src, 1u);
             g1 = hash_unit((uint32_t)src, 2u);
@@ -309,7 +363,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
     double al = 1.0, be = 1.0, ga = 0.0;           // q1 = al w1, q2 = be (w2 - ga w1)
     double mu_re = 0.0, mu_im = 0.0, dmu = __longlong_as_double(0x7ff0000000000000ll);
     int k = 0, conv = 0;
-    cl.sync();
+    tm.barrier();
     for (;;) {
         // phase 1: current basis (gathered and natural), z = x / D, scans; sums and Gram Q Q^T
         double v[2][kSE], tot[2];
@@ -329,21 +383,20 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
             pp[3] += q[0][e] * q[1][e];
             pp[4] += q[1][e] * q[1][e];
         }
-        bscan<2>(v, tot, sh.scr);
-        bsum<5>(pp, sh.scr);
+        tm.template scan<2>(v, tot);
+        tm.template sum<5>(pp);
         {
             const double pv[7] = {tot[0], tot[1], pp[0], pp[1], pp[2], pp[3], pp[4]};
-            publish<7>(cl, sh.exA, pv, c, C);
+            tm.template exchange<7>(tm.exA, pv);
         }
-        cl.sync();   // A
         double T[2], off[2], sig[2], G11, G12, G22, dm;
-        gather_sum(sh.exA, 0, c, C, T[0], off[0]);
-        gather_sum(sh.exA, 1, c, C, T[1], off[1]);
-        gather_sum(sh.exA, 2, c, C, sig[0], dm);
-        gather_sum(sh.exA, 3, c, C, sig[1], dm);
-        gather_sum(sh.exA, 4, c, C, G11, dm);
-        gather_sum(sh.exA, 5, c, C, G12, dm);
-        gather_sum(sh.exA, 6, c, C, G22, dm);
+        tm.total(tm.exA, 0, tot[0], T[0], off[0]);
+        tm.total(tm.exA, 1, tot[1], T[1], off[1]);
+        tm.total(tm.exA, 2, pp[0], sig[0], dm);
+        tm.total(tm.exA, 3, pp[1], sig[1], dm);
+        tm.total(tm.exA, 4, pp[2], G11, dm);
+        tm.total(tm.exA, 5, pp[3], G12, dm);
+        tm.total(tm.exA, 6, pp[4], G22, dm);
         // phase 2: W = Q P~ - (Q 1) pi; dots; push W
         double hp[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // h11 h12 h21 h22 g11 g12 g22
 #pragma unroll
@@ -365,14 +418,13 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
             hp[5] += y0 * y1;
             hp[6] += y1 * y1;
         }
-        push(cl, xb0, P, wn[0]);
-        push(cl, xb1, P, wn[1]);
-        bsum<7>(hp, sh.scr);
-        publish<7>(cl, sh.exB, hp, c, C);
-        cl.sync();   // B
+        push<MODE>(tm, xb0, P, wn[0]);
+        push<MODE>(tm, xb1, P, wn[1]);
+        tm.template sum<7>(hp);
+        tm.template exchange<7>(tm.exB, hp);
         double h[7];
 #pragma unroll
-        for (int i = 0; i < 7; ++i) gather_sum(sh.exB, i, c, C, h[i], dm);
+        for (int i = 0; i < 7; ++i) tm.total(tm.exB, i, hp[i], h[i], dm);
         ++k;
         // Ritz values: H = M G^{-1}, M = W Q^T = [[h11, h12], [h21, h22]], G = Q Q^T
         double nre, nim;
@@ -405,12 +457,11 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
         if (!(h[4] > 1e-280)) { conv = 1; break; }
         if (k > 1 && dmu < a.tol) { conv = 1; break; }
         if (k >= a.max_iter || !isfinite(dmu)) break;
-        // next basis as coefficients on the pushed W
         al = 1.0 / sqrt(h[4]);
         ga = h[5] / h[4];
         be = h[6] > 1e-280 ? 1.0 / sqrt(h[6]) : 0.0;
     }
-    if (c == 0 && threadIdx.x == 0) {
+    if (tm.c == 0 && threadIdx.x == 0) {
         SpecOut o;
         o.re = mu_re;
         o.im = fabs(mu_im);   // the member of a conjugate pair with phase in [0, pi]
@@ -426,14 +477,14 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
 // 1/2 || e_i P~^n - pi ||_1 <= eps (no renormalisation: P~ is stochastic). TV to stationarity is
 // non-increasing in n for every start, so the smallest n with max_i TV_i(n) <= eps is max_i n_i.
 // Item = one start bin; n_i written to a.nsteps[i] (-1: max_iter steps not enough).
+template <int MODE>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a) {
-    cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
-    const int C = a.C, c = (int)cl.block_rank();
-    const int start = a.start_bin0 + blockIdx.x / C;
+    Team<MODE> tm(sh, a.C);
+    const int start = a.start_bin0 + item_index<MODE>(a.C);
     const int m = a.prof[0], l = a.lsh[0];
-    const Pos P = make_pos(a, c, l);
+    const Pos P = make_pos<MODE>(a, tm.c, l);
     const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
     const double eL = a.scal[m * 8 + 1];
     double wr[kSE], idr[kSE], pr[kSE];
@@ -445,16 +496,15 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a)
 #pragma unroll
     for (int e = 0; e < kSE; ++e) xbuf[sidx(threadIdx.x * kSE + e)] = (P.p0 + e == r0) ? 1.0 : 0.0;
     int n = 0, hit = -1;
-    cl.sync();
+    tm.barrier();
     for (;;) {
         double v[1][kSE], tot[1];
 #pragma unroll
         for (int e = 0; e < kSE; ++e) v[0][e] = xbuf[sidx(threadIdx.x * kSE + e)] * idr[e];
-        bscan<1>(v, tot, sh.scr);
-        publish<1>(cl, sh.exA, tot, c, C);
-        cl.sync();   // A
+        tm.template scan<1>(v, tot);
+        tm.template exchange<1>(tm.exA, tot);
         double T, off, dm;
-        gather_sum(sh.exA, 0, c, C, T, off);
+        tm.total(tm.exA, 0, tot[0], T, off);
         double y[kSE], tv[1] = {0.0};
 #pragma unroll
         for (int e = 0; e < kSE; ++e) {
@@ -462,17 +512,16 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a)
             y[e] = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
             tv[0] += fabs(y[e] - pr[e]);
         }
-        push(cl, xbuf, P, y);
-        bsum<1>(tv, sh.scr);
-        publish<1>(cl, sh.exB, tv, c, C);
-        cl.sync();   // B
+        push<MODE>(tm, xbuf, P, y);
+        tm.template sum<1>(tv);
+        tm.template exchange<1>(tm.exB, tv);
         double TV;
-        gather_sum(sh.exB, 0, c, C, TV, dm);
+        tm.total(tm.exB, 0, tv[0], TV, dm);
         ++n;
         if (0.5 * TV <= a.eps) { hit = n; break; }
         if (n >= a.max_iter) break;
     }
-    if (c == 0 && threadIdx.x == 0) {
+    if (tm.c == 0 && threadIdx.x == 0) {
         a.nsteps[start] = hit;
         atomicMax(a.nmax, hit < 0 ? 0x7fffffff : hit);
     }
@@ -481,13 +530,13 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a)
 // ---------------------------------------------------------------------------------------------
 // f1: bin trajectory (§4.2): (start P~^n)[bin] for n = 0..steps (no renormalisation),
 // and the final vector start P~^steps.
+template <int MODE>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_traj(const StructArgs a) {
-    cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
-    const int C = a.C, c = (int)cl.block_rank();
+    Team<MODE> tm(sh, a.C);
     const int m = a.prof[0], l = a.lsh[0];
-    const Pos P = make_pos(a, c, l);
+    const Pos P = make_pos<MODE>(a, tm.c, l);
     const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
     const double eL = a.scal[m * 8 + 1];
     double wr[kSE], idr[kSE];
@@ -504,26 +553,25 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_traj(const StructArgs a) {
         }
         xbuf[sidx(threadIdx.x * kSE + e)] = g;
     }
-    if (c == 0 && threadIdx.x == 0) a.traj[0] = a.start[a.bin];
-    cl.sync();
+    if (tm.c == 0 && threadIdx.x == 0) a.traj[0] = a.start[a.bin];
+    tm.barrier();
     double y[kSE];
     for (int n = 1; n <= a.max_iter; ++n) {
         double v[1][kSE], tot[1];
 #pragma unroll
         for (int e = 0; e < kSE; ++e) v[0][e] = xbuf[sidx(threadIdx.x * kSE + e)] * idr[e];
-        bscan<1>(v, tot, sh.scr);
-        publish<1>(cl, sh.exA, tot, c, C);
-        cl.sync();   // A
+        tm.template scan<1>(v, tot);
+        tm.template exchange<1>(tm.exA, tot);
         double T, off;
-        gather_sum(sh.exA, 0, c, C, T, off);
+        tm.total(tm.exA, 0, tot[0], T, off);
 #pragma unroll
         for (int e = 0; e < kSE; ++e) {
             const double Cj = off + v[0][e];
             y[e] = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
             if (P.p0 + e == a.bin) a.traj[n] = y[e];
         }
-        if (n < a.max_iter) push(cl, xbuf, P, y);
-        cl.sync();   // B (pushes visible; xbuf reads of this product done everywhere)
+        if (n < a.max_iter) push<MODE>(tm, xbuf, P, y);
+        tm.barrier();   // pushes visible; the xbuf reads of this product are done everywhere
     }
     if (a.out) {
 #pragma unroll
@@ -533,7 +581,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_traj(const StructArgs a) {
 }
 
 template <typename K>
-cudaError_t launch_cluster(K kernel, const StructArgs &a, int n_units, int V, cudaStream_t s) {
+cudaError_t launch_team(K kernel, const StructArgs &a, int n_units, int V, cudaStream_t s) {
     const int C = a.C;
     const int nT = a.threads;
     const int chunk = nT * kSE;
@@ -555,33 +603,37 @@ cudaError_t launch_cluster(K kernel, const StructArgs &a, int n_units, int V, cu
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = C > 1 ? 1 : 0;   // single-CTA teams launch without a cluster (no residency cap)
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
 }  // namespace
 
-// Cluster shape for N positions: C CTAs of `threads` threads, 8 positions per thread.
+// Team shape for N positions: C CTAs of `threads` threads, 8 positions per thread.
 int struct_shape(int N, int *C, int *threads) {
-    const int chunk_max = kSMaxT * kSE;
-    if (N <= chunk_max) {
+    if (N <= kSChunk) {
         int t = (N + kSE - 1) / kSE;
         t = (t + 31) / 32 * 32;
         *C = 1;
         *threads = t < 32 ? 32 : t;
     } else {
         *threads = kSMaxT;
-        *C = (N + chunk_max - 1) / chunk_max;
+        *C = (N + kSChunk - 1) / kSChunk;
     }
     return *C <= kSMaxC ? 0 : 1;
 }
 
+#define SPL_TEAM_LAUNCH(KERNEL, V)                                                              \
+    (a.C > 1 ? launch_team(KERNEL<kCluster>, a, n_units, V, s)                                  \
+             : (a.threads == 32 ? launch_team(KERNEL<kWarp>, a, n_units, V, s)                  \
+                                : launch_team(KERNEL<kBlock>, a, n_units, V, s)))
+
 cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s) {
     switch (kind) {
-        case kStructSolve: return launch_cluster(k_struct_solve, a, n_units, 1, s);
-        case kStructLambda2: return launch_cluster(k_struct_lambda2, a, n_units, 2, s);
-        case kStructMixing: return launch_cluster(k_struct_mixing, a, n_units, 1, s);
-        case kStructTraj: return launch_cluster(k_struct_traj, a, 1, 1, s);
+        case kStructSolve: return SPL_TEAM_LAUNCH(k_struct_solve, 1);
+        case kStructLambda2: return SPL_TEAM_LAUNCH(k_struct_lambda2, 2);
+        case kStructMixing: return SPL_TEAM_LAUNCH(k_struct_mixing, 1);
+        case kStructTraj: n_units = 1; return SPL_TEAM_LAUNCH(k_struct_traj, 1);
     }
     return cudaErrorInvalidValue;
 }

@@ -95,6 +95,10 @@ def _lib():
             "splidar_second_eigenvalue": (st, [fp, i32, p, p, p, p, d, i32, p, sz, C.POINTER(SpectralInfo), p]),
             "splidar_mixing_steps": (st, [fp, d, p, d, i32, p, C.POINTER(i32), p, sz, p]),
             "splidar_bin_trajectory": (st, [fp, d, p, i32, i32, p, p, p, sz, p]),
+            "splidar_splan_create": (st, [C.POINTER(p), i32, fp, i32, p, p, p, d, i32, p, p, sz, p]),
+            "splidar_splan_launch": (st, [p, p]),
+            "splidar_splan_info": (st, [p, pinfo, C.POINTER(SpectralInfo), C.POINTER(C.c_float), p]),
+            "splidar_splan_destroy": (None, [p]),
             "splidar_strerror": (C.c_char_p, [st]),
             "splidar_last_cuda_error": (C.c_int, []),
             "splidar_build_info": (C.c_char_p, []),
@@ -441,3 +445,56 @@ def bin_trajectory(flux, t_d: float, start: torch.Tensor, bin: int, steps: int, 
 def flux_items(flux):
     """(shape, S, B) for one flux in the items convention: shape = flux, S = 1, B = flux.background."""
     return flux, np.array([1.0]), np.array([float(flux.background)])
+
+
+class StructPlan:
+    """Structured (matrix-free) solver plan: kind "solve" (f2, pi out) or "lambda2" (f1, pi in).
+    launch() only enqueues (step-1 vectors + kernel); info() syncs and returns (infos, kernel_ms)."""
+
+    def __init__(self, kind: str, shape, S, B, t_d, pi: torch.Tensor | None = None, tol: float | None = None,
+                 max_iter: int | None = None, ws: torch.Tensor | None = None, stream=None):
+        S, B, T, n_prof = _items(shape, S, B, t_d)
+        self.kind = {"solve": 0, "lambda2": 1}[kind]
+        self.M, self.N = S.size, int(shape.n_bins)
+        if tol is None:
+            tol = 1e-12 if self.kind == 0 else 1e-13
+        if max_iter is None:
+            max_iter = 10 ** 6 if self.kind == 0 else 10 ** 5
+        if self.kind == 0 and pi is None:
+            pi = torch.empty((self.M, self.N), dtype=torch.float64, device="cuda")
+        if pi is None or not pi.is_cuda or pi.dtype != torch.float64 or pi.numel() != self.M * self.N:
+            raise SplidarError(EINVAL, "StructPlan: pi must be a CUDA fp64 [M, N] tensor")
+        self.pi = pi
+        self.ws = ws if ws is not None else structured_workspace(self.N, n_prof, self.M, device=pi.device)
+        self._keep = (S, B, T)
+        self._h = C.c_void_p(None)
+        fa = _FluxArg(shape)
+        _check(_lib().splidar_splan_create(C.byref(self._h), self.kind, C.byref(fa.s), self.M, S.ctypes.data,
+                                           B.ctypes.data, T.ctypes.data, float(tol), int(max_iter), pi.data_ptr(),
+                                           self.ws.data_ptr(), self.ws.numel(), _stream(stream)),
+               "splidar_splan_create")
+
+    def launch(self, stream=None):
+        _check(_lib().splidar_splan_launch(self._h, _stream(stream)), "splidar_splan_launch")
+
+    def info(self, stream=None, check: bool = True):
+        ms = C.c_float(0.0)
+        if self.kind == 0:
+            infos = (SolveInfo * self.M)()
+            st = _lib().splidar_splan_info(self._h, infos, None, C.byref(ms), _stream(stream))
+        else:
+            infos = (SpectralInfo * self.M)()
+            st = _lib().splidar_splan_info(self._h, None, infos, C.byref(ms), _stream(stream))
+        _check(st, "splidar_splan_info", allow=() if check else (ENOCONV,))
+        return [i.as_dict() for i in infos], float(ms.value)
+
+    def close(self):
+        if self._h:
+            _lib().splidar_splan_destroy(self._h)
+            self._h = C.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -126,3 +126,18 @@ def parity_cases(seed: int = 7) -> list:
     f = random_flux(rng, 512, 1)
     cases += [Item(f, 0.0), Item(f, f.t_r), Item(f, 2.0 * f.t_r), Item(f, 75.0), Item(f, 37.5 + f.t_r)]
     return cases
+
+
+def spectral_grid(n_bins: int = 256, n_side: int = 64, t_ds=(75.0, 95.0)) -> Workload:
+    """Stand-in for the paper's (S, B) grids (Fig. 3c: S, B in [0, 10] at 2^8 bins; Fig. 4,
+    P:187-191 and §4.2: t_d = 75 and 95): n_side x n_side (S, B) pairs on linspace(0.05, 10)
+    (B > 0 keeps the chain irreducible, R16), one Gaussian return at 40 ns with
+    sigma 0.5 ns (config 1's pulse), t_r = 100 ns, each pair at every t_d. Inputs only."""
+    v = np.linspace(0.05, 10.0, n_side)
+    items = []
+    for td in t_ds:
+        for s in v:
+            for b in v:
+                items.append(Item(_gauss(100.0, n_bins, 40.0, 0.5, float(s), float(b)), float(td)))
+    return Workload("grid", f"(S,B) grid {n_side}x{n_side} on [0.05,10]^2 x t_d {list(t_ds)}, N={n_bins}, "
+                            f"pulse 40/0.5, t_r=100", items)
