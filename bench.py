@@ -42,9 +42,10 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "grid"])
-    p.add_argument("--path", default="dense", choices=["dense", "structured", "spectral"],
+    p.add_argument("--path", default="dense", choices=["dense", "structured", "spectral", "eq4"],
                    help="dense: the north-star path (P~0 in HBM + GEMV power iteration); structured: "
-                        "SURVEY f2 matrix-free solve; spectral: SURVEY f1 solve + lambda_2")
+                        "SURVEY f2 matrix-free solve; spectral: SURVEY f1 solve + lambda_2; eq4: SURVEY f4 "
+                        "element-wise Eq. 4 construction (with Theorem 2's construction timed beside it)")
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     p.add_argument("--mode", default="factored", choices=["factored", "exp"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -456,6 +457,81 @@ def run_struct_e2e(args, sg, kind, world):
             "note": "host wall clock; validation, grouping and upload of theta, kernels, pi to pinned host memory"}
 
 
+def run_eq4(args, rank, world, dev):
+    """P~ element by element from Eq. 4 for every item of the workload (its own dead time), and
+    in the same run Theorem 2's construction of the same matrices (base matrix + materialised row
+    permutation) for the same-hardware speed-up (the paper's Fig. 3a comparison)."""
+    import torch
+    import paper_2509_20500_b200 as spl
+    w, groups = workload_items(args.workload, rank, world)
+    items = [(f, td) for f, tds in groups for td in tds][:4 if args.workload == "c5" else None]
+    N = items[0][0].n_bins
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    b = 8 if args.dtype == "f64" else 4
+    P = spl.empty_matrix(N, dt)
+    P0 = spl.empty_matrix(N, dt)
+    ws = spl.workspace(N)
+    stream = torch.cuda.current_stream()
+
+    def eq4_step():
+        for f, td in items:
+            spl.build_eq4(f, td, dt, out=P)
+
+    def thm2_step():
+        for f, td in items:
+            spl.build_base(f, dt, args.mode, out=P0, ws=ws)
+            spl.apply_deadtime(P0, f.t_r, td, out=P)
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        evs = []
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(c) for a, c in evs) / 1e3
+
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(dev)
+    time.sleep(0.25)
+    t_eq4 = timed(eq4_step)
+    clk = clocks.stop()
+    t_thm2 = timed(thm2_step)
+    from paper_2509_20500_b200.shard import max_over_ranks
+    t_eq4, t_thm2 = max_over_ranks([t_eq4, t_thm2], device="cuda")
+    K = args.steps
+    entries = len(items) * N * N
+    traffic = load_traffic(args.workload + "_eq4", args.dtype) or {}
+    flops_per_entry = traffic.get("fp64_flops_per_entry")
+    achieved = flops_per_entry * entries * K / t_eq4 / 1e12 if flops_per_entry else None
+    return {
+        "metric": "transition-matrix entries/s, element-wise Eq. 4 construction (SURVEY f4)",
+        "value": entries * K * world / t_eq4, "unit": "entries/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": t_eq4 / K * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded BASELINE.json flux parameters)",
+        "config": {"workload": f"{args.workload}: {w.description}", "n_bins": N, "matrices_per_step": len(items),
+                   "path": "eq4", "l2": "matrix > L2 for N >= 4096 (not flushed otherwise)",
+                   "parallelism": "single GPU" if world == 1 else f"dp{world}"},
+        "theorem2_same_gpu": {"entries_per_s": entries * K * world / t_thm2, "ms_per_step": t_thm2 / K * 1e3,
+                              "what": "splidar_build_base + splidar_apply_deadtime (materialised J_l) per item",
+                              "speedup_vs_eq4": t_eq4 / t_thm2},
+        "paper_speedup_context": "up to 1000x vs Rapp's element-wise construction (P:5, P:199; hardware not stated)",
+        "roofline": {"bound": "alu", "kernel": "k_build_eq4", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
+                     "traffic": traffic.get("dram_bytes"),
+                     "algorithmic_flops_per_entry": flops_per_entry,
+                     "flops_source": traffic.get("source"),
+                     "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (probe: 35.8 TFLOP/s DFMA)"},
+        "clocks": clk, "e2e": None, "gpu_launches": len(items) * K, "impl": "ours", "lib": spl.lib_path(),
+    }
+
+
 def run_oracle_spectral(args):
     """Oracle for the spectral path: Eq. 4 matrix, dense pi and numpy eigvals, on a bounded sample."""
     import oracle
@@ -551,6 +627,15 @@ def main():
         line = run_ours(args, rank, world, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = run_oracle_sample(args, line["iterations"])
+    elif args.path == "eq4":
+        line = run_eq4(args, rank, world, dev)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            cb = run_oracle_sample(args)
+            w_, g_ = workload_items(args.workload)
+            Nn = g_[0][0].n_bins
+            cb = {"value": Nn / cb["s_per_row_build"], "unit": "entries/s", "cores": cb["cores"], "kind": "oracle",
+                  "sample": cb["sample"].split(" and one")[0] + " (build only)"}
+            line["cpu_baseline"] = cb
     else:
         line = run_struct(args, rank, world, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:

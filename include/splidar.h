@@ -127,6 +127,16 @@ splidar_status splidar_build_base_batched(const splidar_flux *fluxes, int32_t n_
 splidar_status splidar_apply_deadtime(const void *P0, void *P, int32_t n_bins, int64_t ld,
                                       splidar_dtype dt, double t_r, double t_d, void *stream);
 
+/* P~ built ELEMENT BY ELEMENT from Eq. 4 -- the sequential
+ * construction that Theorem 2 replaces -- for same-hardware comparisons: for every (i, j) on its own,
+ * a = s_i + x_d, D(a) = (ceil(a / Delta) - 1/2) Delta, b = ceil((a - s_j) / t_r) t_r + s_j
+ * (P:102), P_ij = lambda(s_j) exp(-int_{D(a)}^{b} lambda~) with the integral of the periodic replica in
+ * closed form (erfc at both limits, no reuse between entries), then rows divided by their sums.
+ * Same matrix as splidar_build_base + splidar_apply_deadtime up to rounding. P: device N x ld, dtype
+ * dt. t_d >= 0 finite, flux as splidar_build_base, else SPLIDAR_EINVAL / SPLIDAR_ENOSPACE. */
+splidar_status splidar_build_eq4(const splidar_flux *flux, double t_d, splidar_dtype dt, void *P, int64_t ld,
+                                 void *stream);
+
 /* Step 4 (synchronises stream once): pi P~ = pi for P~ = J_l P~0, by power iteration:
  * pi^0 = 1/N; y = pi^k P~ (fp64 accumulation, the row permutation applied as the gather
  * x_r = pi^k[(r - l) mod N] of a GEMV on P~0); pi^{k+1} = y / ||y||_1; stop after the first k with

@@ -268,6 +268,17 @@ splidar_status splidar_apply_deadtime(const void *P0, void *P, int32_t n_bins, i
     return cuda_status(launch_apply_deadtime(P0, P, n_bins, ld, dt, l, (cudaStream_t)stream));
 }
 
+// f4: the element-wise Eq. 4 construction, for same-hardware comparisons.
+splidar_status splidar_build_eq4(const splidar_flux *flux, double t_d, splidar_dtype dt, void *P, int64_t ld,
+                                 void *stream) {
+    splidar_status st = check_flux(flux);
+    if (st) return st;
+    if (!std::isfinite(t_d) || t_d < 0.0) return SPLIDAR_EINVAL;
+    if ((st = check_matrix(P, flux->n_bins, ld, dt))) return st;
+    const double u = std::fmod(t_d, flux->t_r) * (double)flux->n_bins / flux->t_r;   // x_d / Delta (R4)
+    return cuda_status(launch_build_eq4(to_dev(flux), u, dt, P, ld, (cudaStream_t)stream));
+}
+
 // ---------------------------------------------------------------- step 4: plans --------------
 
 struct splidar_plan_s {

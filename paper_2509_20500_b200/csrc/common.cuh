@@ -70,6 +70,7 @@ cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int 
                          void *P0, int64_t ld, int64_t mstride, cudaStream_t s);
 cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, int dtype, int l,
                                   cudaStream_t s);
+cudaError_t launch_build_eq4(const FluxDev &f, double u, int dtype, void *P, int64_t ld, cudaStream_t s);
 
 struct PowerArgs {
     const void *P;

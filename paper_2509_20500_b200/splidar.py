@@ -99,6 +99,7 @@ def _lib():
             "splidar_splan_launch": (st, [p, p]),
             "splidar_splan_info": (st, [p, pinfo, C.POINTER(SpectralInfo), C.POINTER(C.c_float), p]),
             "splidar_splan_destroy": (None, [p]),
+            "splidar_build_eq4": (st, [fp, d, st, p, i64, p]),
             "splidar_strerror": (C.c_char_p, [st]),
             "splidar_last_cuda_error": (C.c_int, []),
             "splidar_build_info": (C.c_char_p, []),
@@ -220,6 +221,16 @@ def build_base_batched(fluxes, dtype=torch.float64, mode: str = "factored", out:
     arr = (_Flux * M)(*[fa.s for fa in fas])
     _check(_lib().splidar_build_base_batched(arr, M, dt, _MODES[mode], ptr, ld, P.stride(0), ws.data_ptr(),
                                              ws.numel(), _stream(stream)), "splidar_build_base_batched")
+    return P
+
+
+def build_eq4(flux, t_d: float, dtype=torch.float64, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """P~ element by element from Eq. 4 (the construction Theorem 2 replaces), async."""
+    N = int(flux.n_bins)
+    P = out if out is not None else empty_matrix(N, dtype)
+    ptr, n, ld, dt = _matrix_args(P)
+    fa = _FluxArg(flux)
+    _check(_lib().splidar_build_eq4(C.byref(fa.s), float(t_d), dt, ptr, ld, _stream(stream)), "splidar_build_eq4")
     return P
 
 
