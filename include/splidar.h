@@ -264,6 +264,29 @@ splidar_status splidar_bin_trajectory(const splidar_flux *flux, double t_d, cons
                                       int32_t steps, double *traj, double *final_vec, void *ws, size_t ws_bytes,
                                       void *stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Monte Carlo of the asynchronous detection process, the paper's ground
+ * truth for the Markov model. Items as splidar_sweep (shape x S[m], B[m], t_d[m]); each
+ * item runs n_runs independent chains ("runs", one histogram each). A chain starts at T = 0 as if a
+ * photon had just been registered; after each registration at T_k the detector is dead for t_d and
+ * the next registration is T_{k+1} = Ftilde^{-1}(Ftilde(T_k + t_d) - log U) (the first arrival of the
+ * inhomogeneous Poisson process with rate lambda~, Eq. 1 replicated), U uniform on (0, 1]
+ * from splitmix64 started at seed + c * 0xD1B54A32D192ED03 (mod 2^64) for chain c = m * n_runs + run
+ * and advanced once per registration (the generator the CPU oracle implements, so chains can be
+ * replayed). The first n_burn registrations are discarded; then X_k = T_k mod t_r goes into the
+ * run's histogram of n_hist bins ((k-1) t_r/n_hist, k t_r/n_hist] (X = 0 read as t_r) until n_regs
+ * registrations are counted, or, when n_cycles > 0 (n_regs ignored), until the first registration
+ * n_cycles laser periods after the burn-in (the paper's "histograms of 50,000 laser cycles").
+ * hist: device uint64 [n_items][n_runs][n_hist] (zeroed by the call). n_record > 0 also stores the
+ * first n_record registrations of every chain: q_rec (period index) and t_rec (offset in [0, t_r)),
+ * device [n_items * n_runs][n_record]. Synchronises `stream` once.
+ * Workspace: splidar_mc_workspace_bytes(n_profiles, n_items) (n_profiles = distinct (S, B) pairs). */
+size_t splidar_mc_workspace_bytes(int32_t n_profiles, int32_t n_items);
+splidar_status splidar_monte_carlo(const splidar_flux *shape, int32_t n_items, const double *S, const double *B,
+                                   const double *t_d, uint64_t seed, int32_t n_runs, int64_t n_burn, int64_t n_regs,
+                                   int64_t n_cycles, int32_t n_hist, uint64_t *hist, int32_t n_record,
+                                   int64_t *q_rec, double *t_rec, void *ws, size_t ws_bytes, void *stream);
+
 const char *splidar_strerror(splidar_status st);
 int splidar_last_cuda_error(void);     /* cudaError_t of the last SPLIDAR_ECUDA, else 0 */
 const char *splidar_build_info(void);  /* compile target and version string */

@@ -63,6 +63,7 @@ def lib():
             "oracle_stationary_dense": (C.c_int, [i32, p, p]),
             "oracle_stationary_power": (C.c_int, [i32, p, d, i32, p, C.POINTER(i32), C.POINTER(d)]),
             "oracle_mc": (C.c_int, [fp, d, C.c_uint64, i64, i64, i32, i32, p]),
+            "oracle_mc_timestamps": (C.c_int, [fp, d, C.c_uint64, i64, p, p]),
             "oracle_left_matvec": (None, [i32, i32, p, p, p]),
         }
         for name, (res, args) in sig.items():
@@ -175,6 +176,17 @@ def monte_carlo(flux, t_d: float, seed: int, n_burn: int, n_per_batch: int, n_ba
                        int(n_hist), h.ctypes.data):
         raise ValueError("oracle_mc: zero total flux")
     return h
+
+
+def mc_timestamps(flux, t_d: float, seed: int, n: int):
+    """The first n registrations (period q, offset t = T mod t_r) of one detection chain whose
+    splitmix64 generator starts at `seed` (time starts at q = 0, t = 0)."""
+    q = np.zeros(n, dtype=np.int64)
+    t = np.zeros(n, dtype=np.float64)
+    r = _FluxRef(flux)
+    if lib().oracle_mc_timestamps(r.ref, float(t_d), int(seed) & (2 ** 64 - 1), int(n), q.ctypes.data, t.ctypes.data):
+        raise ValueError("oracle_mc_timestamps: zero total flux")
+    return q, t
 
 
 def shift_l(flux, t_d: float) -> int:

@@ -259,38 +259,58 @@ static double F_inverse(const oracle_flux *f, double y) {
     return 0.5 * (lo + hi);
 }
 
-/* Continuous-time simulation of asynchronous detection: photons arrive as an inhomogeneous
- * Poisson process with the periodic rate lambda~ (Eq. 1 replicated); after each
- * registration at T_k the SPAD is dead for t_d and re-arms at T_k + t_d; the next
- * registration is the first arrival after re-arming, T_{k+1} = Ftilde^{-1}(Ftilde(T_k + t_d) + E),
- * E ~ Exp(1) (time change of a Poisson process). The timestamp is X_k = T_k mod t_r, binned
- * into n_hist bins ((k-1) Delta_h, k Delta_h] with X = 0 read as t_r. The first n_burn registrations
- * are discarded; the rest are split into n_batches consecutive batches, hist[b * n_hist + k]. */
+/* One registration of the continuous-time detection process: photons arrive as an
+ * inhomogeneous Poisson process with the periodic rate lambda~ (Eq. 1 replicated); after
+ * the registration at T_k = q t_r + t the SPAD is dead for t_d and re-arms at T_k + t_d; the
+ * next registration is the first arrival after re-arming, T_{k+1} = Ftilde^{-1}(Ftilde(T_k + t_d) + E),
+ * E ~ Exp(1) = -log U, U uniform on (0, 1] from splitmix64 (time change of a Poisson process). Time is
+ * carried as (period q, offset t in [0, t_r)) to keep precision. */
+static void mc_next(const oracle_flux *f, double Lam, double t_d, uint64_t *st, int64_t *q, double *t) {
+    double tt = *t + t_d;
+    int64_t qq = *q + (int64_t)floor(tt / f->t_r);
+    tt = fmod(tt, f->t_r);
+    if (tt < 0.0) tt += f->t_r;
+    double target = oracle_F(f, tt) - log(unif01_open(st));
+    int64_t extra = (int64_t)floor(target / Lam);
+    double rem = target - (double)extra * Lam;
+    if (rem < 0.0) { rem += Lam; extra -= 1; }
+    if (rem >= Lam) { rem -= Lam; extra += 1; }
+    *q = qq + extra;
+    *t = F_inverse(f, rem);
+    if (*t >= f->t_r) { *t -= f->t_r; *q += 1; }
+}
+
+/* The first n registrations of one chain started at (q, t) = (0, 0) with generator state `seed`:
+ * q_out[k], t_out[k] (X_k = t_out[k] = T_k mod t_r). */
+int oracle_mc_timestamps(const oracle_flux *f, double t_d, uint64_t seed, int64_t n, int64_t *q_out,
+                         double *t_out) {
+    const double Lam = oracle_Lambda(f);
+    if (!(Lam > 0.0)) return 1;
+    uint64_t st = seed;
+    int64_t q = 0;
+    double t = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+        mc_next(f, Lam, t_d, &st, &q, &t);
+        q_out[k] = q;
+        t_out[k] = t;
+    }
+    return 0;
+}
+
+/* Histogram of the timestamps X_k = T_k mod t_r of one chain: n_hist bins
+ * ((k-1) Delta_h, k Delta_h] with X = 0 read as t_r. The first n_burn registrations are discarded;
+ * the rest are split into n_batches consecutive batches, hist[b * n_hist + k]. */
 int oracle_mc(const oracle_flux *f, double t_d, uint64_t seed, int64_t n_burn, int64_t n_per_batch,
               int32_t n_batches, int32_t n_hist, int64_t *hist) {
     const double Lam = oracle_Lambda(f);
     if (!(Lam > 0.0)) return 1;
     uint64_t st = seed;
-    /* time is carried as (period q, offset t in [0, t_r)) to keep precision */
     int64_t q = 0;
     double t = 0.0;
     memset(hist, 0, sizeof(int64_t) * (size_t)n_batches * n_hist);
     const int64_t total = n_burn + n_per_batch * n_batches;
     for (int64_t k = 0; k < total; ++k) {
-        /* re-arm at T + t_d */
-        double tt = t + t_d;
-        int64_t qq = q + (int64_t)floor(tt / f->t_r);
-        tt = fmod(tt, f->t_r);
-        if (tt < 0.0) tt += f->t_r;
-        /* cumulative flux at the re-arm time, then add an Exp(1) increment */
-        double target = oracle_F(f, tt) - log(unif01_open(&st));
-        int64_t extra = (int64_t)floor(target / Lam);
-        double rem = target - (double)extra * Lam;
-        if (rem < 0.0) { rem += Lam; extra -= 1; }
-        if (rem >= Lam) { rem -= Lam; extra += 1; }
-        q = qq + extra;
-        t = F_inverse(f, rem);
-        if (t >= f->t_r) { t -= f->t_r; q += 1; }
+        mc_next(f, Lam, t_d, &st, &q, &t);
         if (k >= n_burn) {
             int64_t b = (k - n_burn) / n_per_batch;
             double dh = f->t_r / n_hist;

@@ -932,3 +932,82 @@ splidar_status splidar_bin_trajectory(const splidar_flux *flux, double t_d, cons
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- Monte Carlo (f3) -------------
+static size_t mc_layout(int M, int I, size_t *o_prof, size_t *o_td) {
+    size_t o = a256(sizeof(FluxDev) * (size_t)M);
+    *o_prof = o;
+    o = a256(o + sizeof(int) * (size_t)I);
+    *o_td = o;
+    return a256(o + sizeof(double) * (size_t)I);
+}
+
+extern "C" {
+
+size_t splidar_mc_workspace_bytes(int32_t n_profiles, int32_t n_items) {
+    if (n_profiles < 1 || n_items < 1) return 0;
+    size_t a, b;
+    return mc_layout(n_profiles, n_items, &a, &b);
+}
+
+splidar_status splidar_monte_carlo(const splidar_flux *shape, int32_t n_items, const double *S, const double *B,
+                                   const double *t_d, uint64_t seed, int32_t n_runs, int64_t n_burn, int64_t n_regs,
+                                   int64_t n_cycles, int32_t n_hist, uint64_t *hist, int32_t n_record,
+                                   int64_t *q_rec, double *t_rec, void *ws, size_t ws_bytes, void *stream) {
+    if (!shape || n_items < 1 || n_items > 65535 || !S || !B || !t_d || !hist) return SPLIDAR_EINVAL;
+    if (n_runs < 1 || n_hist < 1 || n_burn < 0 || n_record < 0 || (n_regs < 1 && n_cycles < 1)) return SPLIDAR_EINVAL;
+    if (n_record > 0 && (!q_rec || !t_rec)) return SPLIDAR_EINVAL;
+    splidar_status st;
+    std::vector<FluxDev> fl;
+    std::vector<int> prof((size_t)n_items);
+    std::map<std::pair<double, double>, int> idx;
+    for (int i = 0; i < n_items; ++i) {
+        if (!std::isfinite(S[i]) || S[i] < 0.0 || !std::isfinite(t_d[i]) || t_d[i] < 0.0) return SPLIDAR_EINVAL;
+        FluxDev d = to_dev(shape, S[i], B[i]);
+        splidar_flux f = *shape;
+        f.background = B[i];
+        std::vector<double> sig((size_t)shape->n_pulses);
+        for (int k = 0; k < shape->n_pulses; ++k) sig[(size_t)k] = d.S[k];
+        f.signal = sig.data();
+        if ((st = check_flux(&f))) return st;
+        auto key = std::make_pair(S[i], B[i]);
+        auto it = idx.find(key);
+        if (it == idx.end()) {
+            idx[key] = (int)fl.size();
+            prof[(size_t)i] = (int)fl.size();
+            fl.push_back(d);
+        } else {
+            prof[(size_t)i] = it->second;
+        }
+    }
+    size_t o_prof, o_td;
+    const size_t need = mc_layout((int)fl.size(), n_items, &o_prof, &o_td);
+    if (!ws || ((uintptr_t)ws & 255u) != 0 || ws_bytes < need) return SPLIDAR_ENOSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *wsb = static_cast<char *>(ws);
+    SPL_CUDA(cudaMemcpyAsync(wsb, fl.data(), sizeof(FluxDev) * fl.size(), cudaMemcpyHostToDevice, s));
+    SPL_CUDA(cudaMemcpyAsync(wsb + o_prof, prof.data(), sizeof(int) * prof.size(), cudaMemcpyHostToDevice, s));
+    SPL_CUDA(cudaMemcpyAsync(wsb + o_td, t_d, sizeof(double) * (size_t)n_items, cudaMemcpyHostToDevice, s));
+    SPL_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint64_t) * (size_t)n_items * n_runs * n_hist, s));
+    McArgs a;
+    memset(&a, 0, sizeof(a));
+    a.flux = reinterpret_cast<const FluxDev *>(wsb);
+    a.prof = reinterpret_cast<const int *>(wsb + o_prof);
+    a.td = reinterpret_cast<const double *>(wsb + o_td);
+    a.n_items = n_items;
+    a.n_runs = n_runs;
+    a.n_hist = n_hist;
+    a.n_record = n_record;
+    a.n_burn = n_burn;
+    a.n_regs = n_regs;
+    a.n_cycles = n_cycles;
+    a.seed = seed;
+    a.hist = reinterpret_cast<unsigned long long *>(hist);
+    a.q_rec = reinterpret_cast<long long *>(q_rec);
+    a.t_rec = t_rec;
+    SPL_CUDA(launch_mc(a, s));
+    SPL_CUDA(cudaStreamSynchronize(s));
+    return SPLIDAR_OK;
+}
+
+}  // extern "C"

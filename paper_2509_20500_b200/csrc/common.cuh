@@ -138,4 +138,18 @@ enum { kStructSolve = 0, kStructLambda2 = 1, kStructMixing = 2, kStructTraj = 3 
 int struct_shape(int N, int *C, int *threads);
 cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s);
 
+// ---- Monte Carlo of the detection process (mc.cu) ------------------------------
+struct McArgs {
+    const FluxDev *flux;        // [profiles]
+    const int *prof;            // [items]
+    const double *td;           // [items]
+    int n_items, n_runs, n_hist, n_record;
+    long long n_burn, n_regs, n_cycles;
+    uint64_t seed;
+    unsigned long long *hist;   // [items][runs][n_hist]
+    long long *q_rec;           // [items * runs][n_record]
+    double *t_rec;
+};
+cudaError_t launch_mc(const McArgs &a, cudaStream_t s);
+
 }  // namespace spl
