@@ -42,14 +42,16 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "grid"])
-    p.add_argument("--path", default="dense", choices=["dense", "structured", "spectral", "eq4"],
+    p.add_argument("--path", default="dense", choices=["dense", "structured", "spectral", "eq4", "mc"],
                    help="dense: the north-star path (P~0 in HBM + GEMV power iteration); structured: "
                         "SURVEY f2 matrix-free solve; spectral: SURVEY f1 solve + lambda_2; eq4: SURVEY f4 "
-                        "element-wise Eq. 4 construction (with Theorem 2's construction timed beside it)")
+                        "element-wise Eq. 4 construction (with Theorem 2's construction timed beside it); mc: "
+                        "SURVEY f3 Monte Carlo of the detection process (paper protocol, P:202)")
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     p.add_argument("--mode", default="factored", choices=["factored", "exp"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--mc-split", type=int, default=None, help="--path mc: sub-chains per run (default: auto)")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
 
@@ -532,6 +534,107 @@ def run_eq4(args, rank, world, dev):
     }
 
 
+def run_mc(args, rank, world, dev):
+    """the paper's Monte Carlo protocol on the GPU. c1..c5: every item, 100 runs of 50,000
+    laser cycles each, histograms at 2^10 bins; grid: a 16 x 16 (S, B) x {75, 95} grid at 2^8
+    bins, 25 runs of 50,000 cycles per item. Metric: registrations/s."""
+    import torch
+    import paper_2509_20500_b200 as spl
+    from workloads import spectral_grid
+    if args.workload == "grid":
+        w = spectral_grid(256, 16)
+        groups = [(it.flux, [it.t_d]) for it in w.items]
+        n_runs, n_hist = 25, 256
+    else:
+        w, groups = workload_items(args.workload, rank, world)
+        n_runs, n_hist = 100, 1024
+    sg = _shape_groups(groups)
+    n_cycles, n_burn = 50000, 100
+    n_items = sum(len(g[1]) for g in sg)
+    # sub-chains per run for occupancy (~200k threads), each >= 3000 cycles; 1 = one chain per histogram
+    n_split = max([d for d in range(1, 51) if n_cycles % d == 0 and n_cycles // d >= 3000
+                   and d * n_items * n_runs <= max(200000, n_items * n_runs)] or [1])
+    if args.mc_split is not None:
+        n_split = args.mc_split
+    stream = torch.cuda.current_stream()
+    seed = [1000 + 7919 * rank]
+
+    def step():
+        regs = 0
+        for shape, S, B, T in sg:
+            h = spl.monte_carlo(shape, S, B, T, seed[0], n_runs, n_hist, n_burn=n_burn, n_cycles=n_cycles,
+                                n_split=n_split)
+            regs += h.sum()
+        seed[0] += 1
+        return regs
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(dev)
+    time.sleep(0.25)
+    regs_t = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        regs_t.append(step())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    t_total = e0.elapsed_time(e1) / 1e3
+    from paper_2509_20500_b200.shard import max_over_ranks
+    t_total = max_over_ranks([t_total], device="cuda")[0]
+    regs = int(sum(int(r) for r in regs_t))
+    K = args.steps
+    traffic = load_traffic(args.workload + "_mc", "f64") or {}
+    fpr = traffic.get("fp64_flops_per_registration")
+    achieved = fpr * regs / t_total / 1e12 if fpr else None
+    return {
+        "metric": "simulated registrations/s, Monte Carlo of the detection process (SURVEY f3)",
+        "value": regs * world / t_total, "unit": "registrations/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": t_total / K * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based generator)",
+        "config": {"workload": f"{args.workload}: {w.description}", "items": n_items, "runs_per_item": n_runs,
+                   "laser_cycles_per_run": n_cycles, "n_hist": n_hist, "burn_in": n_burn, "path": "mc",
+                   "n_split": n_split, "split_note": "each run = n_split independent sub-chains of n_cycles / n_split "
+                                                     "cycles after their own burn-in, into one histogram",
+                   "protocol": "P:202 (100 x 50,000 cycles, 2^10 bins)" if args.workload != "grid"
+                   else "P:205 (25 x 50,000 cycles per (S, B), 2^8 bins)",
+                   "parallelism": "single GPU" if world == 1 else f"dp{world}: chains seeded per rank"},
+        "laser_cycles_per_s": n_items * n_runs * n_cycles * K * world / t_total,
+        "registrations_per_step": regs / K,
+        "roofline": {"bound": "alu", "kernel": "k_mc", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
+                     "traffic": traffic.get("dram_bytes"), "algorithmic_flops_per_registration": fpr,
+                     "flops_source": traffic.get("source"),
+                     "note": "time includes the host call (validation, uploads, histogram zeroing)",
+                     "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (probe: 35.8 TFLOP/s DFMA)"},
+        "clocks": clk, "e2e": None, "gpu_launches": len(sg) * K, "impl": "ours", "lib": spl.lib_path(),
+    }
+
+
+def run_oracle_mc(args):
+    """The oracle's single-chain Monte Carlo for about 10 s on one core of the host."""
+    import oracle
+    from workloads import spectral_grid
+    if args.workload == "grid":
+        f, td = spectral_grid(256, 16).items[0].flux, 75.0
+    else:
+        w, groups = workload_items(args.workload)
+        f, td = groups[0][0], groups[0][1][0]
+    n = 20000
+    t0 = time.perf_counter()
+    done = 0
+    while time.perf_counter() - t0 < 10.0:
+        oracle.monte_carlo(f, td, 1 + done, 0, n, 1, 256)
+        done += n
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "registrations/s", "cores": 1, "kind": "oracle",
+            "sample": f"{args.workload}: chains of {n} registrations (oracle_mc, bisection inversion), ~10 s"}
+
+
 def run_oracle_spectral(args):
     """Oracle for the spectral path: Eq. 4 matrix, dense pi and numpy eigvals, on a bounded sample."""
     import oracle
@@ -627,6 +730,10 @@ def main():
         line = run_ours(args, rank, world, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = run_oracle_sample(args, line["iterations"])
+    elif args.path == "mc":
+        line = run_mc(args, rank, world, dev)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = run_oracle_mc(args)
     elif args.path == "eq4":
         line = run_eq4(args, rank, world, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:

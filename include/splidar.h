@@ -279,12 +279,17 @@ splidar_status splidar_bin_trajectory(const splidar_flux *flux, double t_d, cons
  * n_cycles laser periods after the burn-in (the paper's "histograms of 50,000 laser cycles").
  * hist: device uint64 [n_items][n_runs][n_hist] (zeroed by the call). n_record > 0 also stores the
  * first n_record registrations of every chain: q_rec (period index) and t_rec (offset in [0, t_r)),
- * device [n_items * n_runs][n_record]. Synchronises `stream` once.
+ * device [n_items * n_runs * n_split][n_record].
+ * n_split >= 1: each run is n_split independent sub-chains (chain c = (m * n_runs + run) * n_split + sub,
+ * seeded as above), each with its own n_burn and 1/n_split of the run's n_regs or n_cycles (which
+ * must then be a multiple of n_split), all adding into the run's histogram: the same stationary
+ * estimate with n_split times the parallelism; n_split = 1 is the paper's one-chain-per-histogram
+ * protocol. Synchronises `stream` once.
  * Workspace: splidar_mc_workspace_bytes(n_profiles, n_items) (n_profiles = distinct (S, B) pairs). */
 size_t splidar_mc_workspace_bytes(int32_t n_profiles, int32_t n_items);
 splidar_status splidar_monte_carlo(const splidar_flux *shape, int32_t n_items, const double *S, const double *B,
-                                   const double *t_d, uint64_t seed, int32_t n_runs, int64_t n_burn, int64_t n_regs,
-                                   int64_t n_cycles, int32_t n_hist, uint64_t *hist, int32_t n_record,
+                                   const double *t_d, uint64_t seed, int32_t n_runs, int32_t n_split, int64_t n_burn,
+                                   int64_t n_regs, int64_t n_cycles, int32_t n_hist, uint64_t *hist, int32_t n_record,
                                    int64_t *q_rec, double *t_rec, void *ws, size_t ws_bytes, void *stream);
 
 const char *splidar_strerror(splidar_status st);

@@ -951,11 +951,14 @@ size_t splidar_mc_workspace_bytes(int32_t n_profiles, int32_t n_items) {
 }
 
 splidar_status splidar_monte_carlo(const splidar_flux *shape, int32_t n_items, const double *S, const double *B,
-                                   const double *t_d, uint64_t seed, int32_t n_runs, int64_t n_burn, int64_t n_regs,
-                                   int64_t n_cycles, int32_t n_hist, uint64_t *hist, int32_t n_record,
+                                   const double *t_d, uint64_t seed, int32_t n_runs, int32_t n_split, int64_t n_burn,
+                                   int64_t n_regs, int64_t n_cycles, int32_t n_hist, uint64_t *hist, int32_t n_record,
                                    int64_t *q_rec, double *t_rec, void *ws, size_t ws_bytes, void *stream) {
     if (!shape || n_items < 1 || n_items > 65535 || !S || !B || !t_d || !hist) return SPLIDAR_EINVAL;
-    if (n_runs < 1 || n_hist < 1 || n_burn < 0 || n_record < 0 || (n_regs < 1 && n_cycles < 1)) return SPLIDAR_EINVAL;
+    if (n_runs < 1 || n_split < 1 || (int64_t)n_runs * n_split > (1 << 30) || n_hist < 1 || n_burn < 0 ||
+        n_record < 0 || (n_regs < 1 && n_cycles < 1))
+        return SPLIDAR_EINVAL;
+    if ((n_cycles > 0 && n_cycles % n_split) || (n_cycles < 1 && n_regs % n_split)) return SPLIDAR_EINVAL;
     if (n_record > 0 && (!q_rec || !t_rec)) return SPLIDAR_EINVAL;
     splidar_status st;
     std::vector<FluxDev> fl;
@@ -996,11 +999,12 @@ splidar_status splidar_monte_carlo(const splidar_flux *shape, int32_t n_items, c
     a.td = reinterpret_cast<const double *>(wsb + o_td);
     a.n_items = n_items;
     a.n_runs = n_runs;
+    a.n_split = n_split;
     a.n_hist = n_hist;
     a.n_record = n_record;
     a.n_burn = n_burn;
-    a.n_regs = n_regs;
-    a.n_cycles = n_cycles;
+    a.n_regs = n_cycles > 0 ? 0 : n_regs / n_split;
+    a.n_cycles = n_cycles > 0 ? n_cycles / n_split : 0;
     a.seed = seed;
     a.hist = reinterpret_cast<unsigned long long *>(hist);
     a.q_rec = reinterpret_cast<long long *>(q_rec);

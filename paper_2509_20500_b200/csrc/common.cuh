@@ -143,11 +143,11 @@ struct McArgs {
     const FluxDev *flux;        // [profiles]
     const int *prof;            // [items]
     const double *td;           // [items]
-    int n_items, n_runs, n_hist, n_record;
-    long long n_burn, n_regs, n_cycles;
+    int n_items, n_runs, n_split, n_hist, n_record;
+    long long n_burn, n_regs, n_cycles;   // per chain (a run's budget / n_split)
     uint64_t seed;
     unsigned long long *hist;   // [items][runs][n_hist]
-    long long *q_rec;           // [items * runs][n_record]
+    long long *q_rec;           // [items * runs * n_split][n_record]
     double *t_rec;
 };
 cudaError_t launch_mc(const McArgs &a, cudaStream_t s);

@@ -8,15 +8,18 @@
 // (time change of a Poisson process), with Ftilde(q t_r + t) = q Lambda + F(t) and F in closed form
 // (erfc; Thm 1). U comes from splitmix64 advanced once per registration from the chain seed
 // seed + c * 0xD1B54A32D192ED03 (c = item * n_runs + run): a counter-based stream, the same algorithm
-// the CPU oracle implements, so a chain can be replayed on the CPU draw for draw.
+// the CPU oracle implements, so a chain can be replayed on the CPU draw for draw. With n_split > 1 a
+// run is n_split independent sub-chains (chain c = (item * n_runs + run) * n_split + sub), each with
+// its own burn-in and 1/n_split of the run's budget, adding into the run's histogram: the same
+// stationary estimate with n_split times the parallelism (n_split = 1 is the paper's protocol).
 // The timestamp X_k = T_k mod t_r goes into the run's n_hist-bin histogram ((k-1) Delta_h,
 // k Delta_h] (X = 0 read as t_r) once k >= n_burn; a run stops after n_regs counted registrations, or
 // (n_cycles > 0) at the first registration n_cycles laser periods after the end of the burn-in.
 //
 // Inversion of F on [0, t_r): a CTA serves runs of one item; it tabulates F at 512 + 1 uniform nodes
 // in shared memory, brackets the root by binary search in the table, then runs Newton steps (F' =
-// lambda > 0 since B > 0) safeguarded by bisection of the bracket until the step is below
-// 1e-15 t_r.
+// lambda > 0 since B > 0) safeguarded by bisection of the bracket until F(t) - y reaches the rounding
+// floor of F or the step is below 1e-15 t_r.
 #include "common.cuh"
 
 namespace spl {
@@ -68,14 +71,17 @@ __device__ double mc_finv(const FluxDev &f, const McConst &q, const double *tab,
     double lo = lo_i * h, hi = hi_i == kMcTable ? f.t_r : hi_i * h;
     const double flo = tab[lo_i], fhi = tab[hi_i];
     double t = fhi > flo ? lo + (y - flo) / (fhi - flo) * (hi - lo) : 0.5 * (lo + hi);
+    // stop when the step is below 1e-15 t_r, the bracket is that narrow, or F(t) - y is at the
+    // rounding floor of F (|g| <= 4 eps Lambda): below it the Newton step is rounding noise
     const double eps = 1e-15 * f.t_r;
+    const double gfloor = 4.0 * 2.220446049250313e-16 * q.Lam;
     for (int it = 0; it < 200; ++it) {
         const double g = mc_F(f, q, t) - y;
         if (g > 0.0) hi = t; else lo = t;
         double tn = t - g / mc_lambda(f, q, t);
         if (!(tn > lo && tn < hi)) tn = 0.5 * (lo + hi);
-        const bool done = fabs(tn - t) <= eps || hi - lo <= eps;
-        t = tn;
+        const bool done = fabs(g) <= gfloor || fabs(tn - t) <= eps || hi - lo <= eps;
+        t = fabs(g) <= gfloor ? t : tn;
         if (done) break;
     }
     return t;
@@ -86,7 +92,7 @@ __global__ void __launch_bounds__(kMcThreads) k_mc(const McArgs a) {
     __shared__ FluxDev fs;
     __shared__ McConst qs;                                  // per-flux constants, shared by the CTA
     const int item = blockIdx.y;
-    const int run = blockIdx.x * kMcThreads + threadIdx.x;
+    const int chain = blockIdx.x * kMcThreads + threadIdx.x;   // run * n_split + sub-chain
     if (threadIdx.x == 0) {
         fs = a.flux[a.prof[item]];
         qs.rate_b = fs.B / fs.t_r;
@@ -104,11 +110,12 @@ __global__ void __launch_bounds__(kMcThreads) k_mc(const McArgs a) {
     if (threadIdx.x == 0) qs.Lam = tab[kMcTable];           // Lambda = F(t_r) (reading R5)
     __syncthreads();
     const McConst &q = qs;
-    if (run >= a.n_runs) return;
+    if (chain >= a.n_runs * a.n_split) return;
+    const int run = chain / a.n_split;
     const double t_d = a.td[item];
-    const long long c = (long long)item * a.n_runs + run;
+    const long long c = (long long)item * a.n_runs * a.n_split + chain;   // chain index (seed, records)
     uint64_t st = a.seed + (uint64_t)c * 0xD1B54A32D192ED03ull;
-    unsigned long long *hist = a.hist + (size_t)c * a.n_hist;
+    unsigned long long *hist = a.hist + ((size_t)item * a.n_runs + run) * a.n_hist;
     const double dh = f.t_r / a.n_hist;
     long long qp = 0, q_end = -1;
     double t = 0.0;
@@ -147,7 +154,7 @@ __global__ void __launch_bounds__(kMcThreads) k_mc(const McArgs a) {
 }  // namespace
 
 cudaError_t launch_mc(const McArgs &a, cudaStream_t s) {
-    dim3 grid((unsigned)((a.n_runs + kMcThreads - 1) / kMcThreads), (unsigned)a.n_items);
+    dim3 grid((unsigned)((a.n_runs * a.n_split + kMcThreads - 1) / kMcThreads), (unsigned)a.n_items);
     k_mc<<<grid, kMcThreads, 0, s>>>(a);
     return cudaGetLastError();
 }

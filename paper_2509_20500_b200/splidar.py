@@ -101,8 +101,8 @@ def _lib():
             "splidar_splan_destroy": (None, [p]),
             "splidar_build_eq4": (st, [fp, d, st, p, i64, p]),
             "splidar_mc_workspace_bytes": (sz, [i32, i32]),
-            "splidar_monte_carlo": (st, [fp, i32, p, p, p, C.c_uint64, i32, i64, i64, i64, i32, p, i32, p, p, p, sz,
-                                         p]),
+            "splidar_monte_carlo": (st, [fp, i32, p, p, p, C.c_uint64, i32, i32, i64, i64, i64, i32, p, i32, p, p,
+                                         p, sz, p]),
             "splidar_strerror": (C.c_char_p, [st]),
             "splidar_last_cuda_error": (C.c_int, []),
             "splidar_build_info": (C.c_char_p, []),
@@ -515,7 +515,7 @@ class StructPlan:
 
 
 def monte_carlo(shape, S, B, t_d, seed: int, n_runs: int, n_hist: int, n_burn: int = 100, n_regs: int = 0,
-                n_cycles: int = 0, n_record: int = 0, stream=None):
+                n_cycles: int = 0, n_record: int = 0, n_split: int = 1, stream=None):
     """histograms [M, n_runs, n_hist] (int64 CUDA tensor) of simulated detection timestamps
      per item; with n_record > 0 also (q_rec, t_rec) [M * n_runs, n_record] of every chain."""
     S, B, T, n_prof = _items(shape, S, B, t_d)
@@ -527,11 +527,11 @@ def monte_carlo(shape, S, B, t_d, seed: int, n_runs: int, n_hist: int, n_burn: i
     ws = torch.empty(nb + 256, dtype=torch.uint8, device="cuda")
     ws = ws[(-ws.data_ptr()) % 256:][:nb]
     nr = max(0, int(n_record))
-    q_rec = torch.empty((M * int(n_runs), max(nr, 1)), dtype=torch.int64, device="cuda")
-    t_rec = torch.empty((M * int(n_runs), max(nr, 1)), dtype=torch.float64, device="cuda")
+    q_rec = torch.empty((M * int(n_runs) * int(n_split), max(nr, 1)), dtype=torch.int64, device="cuda")
+    t_rec = torch.empty((M * int(n_runs) * int(n_split), max(nr, 1)), dtype=torch.float64, device="cuda")
     fa = _FluxArg(shape)
     _check(_lib().splidar_monte_carlo(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data,
-                                      int(seed) & (2 ** 64 - 1), int(n_runs), int(n_burn), int(n_regs),
+                                      int(seed) & (2 ** 64 - 1), int(n_runs), int(n_split), int(n_burn), int(n_regs),
                                       int(n_cycles), int(n_hist), hist.data_ptr(), nr,
                                       q_rec.data_ptr() if nr else None, t_rec.data_ptr() if nr else None,
                                       ws.data_ptr(), ws.numel(), _stream(stream)), "splidar_monte_carlo")

@@ -151,3 +151,27 @@ def test_mc_rejects(spl):
         spl.monte_carlo(f, [1.0], [0.1], [75.0], 1, 4, 16)                   # neither n_regs nor n_cycles
     with pytest.raises(spl.SplidarError):
         spl.monte_carlo(f, [1.0], [0.1], [-1.0], 1, 4, 16, n_regs=10)        # negative dead time
+
+
+def test_mc_split_subchains(spl):
+    """n_split = 4: chain c = (m * n_runs + run) * 4 + sub is replayed by the oracle from its own seed,
+    and run r's histogram is exactly the binning of its 4 sub-chains' counted registrations."""
+    f = Flux(100.0, 64, (30.0, 70.0), (2.0, 4.0), (1.5, 0.7), 0.6)
+    shape, tot = _items_of(f)
+    n_runs, n_split, n_burn, n_regs, n_hist, seed = 8, 4, 20, 400, 24, 99
+    hist, q, t = spl.monte_carlo(shape, [tot], [f.background], [57.0], seed, n_runs, n_hist, n_burn=n_burn,
+                                 n_regs=n_regs, n_record=n_burn + n_regs // n_split, n_split=n_split)
+    q, t = _np(q), _np(t)
+    assert q.shape[0] == n_runs * n_split
+    c = 1 * n_split + 2
+    qo, to = oracle.mc_timestamps(f, 57.0, _seed(seed, c), n_burn + n_regs // n_split)
+    assert np.max(np.abs((q[c] * f.t_r + t[c]) - (qo * f.t_r + to))) <= 1e-9 * f.t_r
+    dh = f.t_r / n_hist
+    for run in range(n_runs):
+        tt = t[run * n_split:(run + 1) * n_split, n_burn:].ravel()
+        b = np.ceil(tt / dh).astype(np.int64) - 1
+        b[b < 0] = n_hist - 1
+        b[b >= n_hist] = n_hist - 1
+        assert np.array_equal(_np(hist[0, run]), np.bincount(b, minlength=n_hist))
+    with pytest.raises(spl.SplidarError):    # budget not divisible by n_split
+        spl.monte_carlo(shape, [tot], [f.background], [57.0], seed, 2, 8, n_regs=401, n_split=4)
