@@ -53,6 +53,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--mc-split", type=int, default=None, help="--path mc: sub-chains per run (default: auto)")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="dense path: never replay the step as a CUDA graph")
     return p.parse_args()
 
 
@@ -164,6 +165,29 @@ class OurStep:
         self.n_solves = sum(len(t) for _, t in groups)
         self.entries = M * self.N * self.N
 
+    def step(self):
+        self.build()
+        self.solve()
+
+    def capture(self):
+        """Small N (every plan fused = single launches): the whole step captured once as a CUDA graph and
+        replayed, so a step is one cudaGraphLaunch instead of ~5 host API calls. Returns False otherwise."""
+        torch = self.torch
+        if not all(p.fused for p in self.plans):
+            return False
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.step()
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            self.step()
+        self.graph_build = torch.cuda.CUDAGraph()      # the build alone, for the build / solve split
+        with torch.cuda.graph(self.graph_build, capture_error_mode="thread_local"):
+            self.build()
+        return True
+
     def build(self):
         if len(self.fluxes) == 1:
             self.spl.build_base(self.fluxes[0], self.dt, self.mode, out=self.P0[0], ws=self.ws_build)
@@ -184,9 +208,13 @@ def run_ours(args, rank, world, dev):
     w, groups = workload_items(args.workload, rank, world)
     st = OurStep(groups, args.dtype, args.mode)
     stream = torch.cuda.current_stream()
+    graphed = (not args.no_graph) and st.capture()
     for _ in range(args.warmup):
-        st.build()
-        st.solve()
+        if graphed:
+            st.graph.replay()
+        else:
+            st.build()
+            st.solve()
     torch.cuda.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -198,17 +226,33 @@ def run_ours(args, rank, world, dev):
     time.sleep(0.25)
     for e0, e1, e2 in ev:
         e0.record(stream)
-        st.build()
-        e1.record(stream)
-        st.solve()
+        if graphed:                      # one replay = build + solve; the split is not observable
+            st.graph.replay()
+        else:
+            st.build()
+            e1.record(stream)
+            st.solve()
         e2.record(stream)
     torch.cuda.synchronize()
+    if graphed:                          # build share: replays of the build-only graph (build roofline)
+        st.graph_build.replay()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(len(ev)):
+            st.graph_build.replay()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        t_b = b0.elapsed_time(b1) / 1e3 / len(ev)
     if world > 1:
         torch.distributed.barrier()
     clk = clocks.stop()
-    t_build = sum(a.elapsed_time(b) for a, b, _ in ev) / 1e3
-    t_solve = sum(b.elapsed_time(c) for _, b, c in ev) / 1e3
     t_total = sum(a.elapsed_time(c) for a, _, c in ev) / 1e3
+    if graphed:
+        t_build = min(t_b * len(ev), t_total)
+        t_solve = t_total - t_build
+    else:
+        t_build = sum(a.elapsed_time(b) for a, b, _ in ev) / 1e3
+        t_solve = sum(b.elapsed_time(c) for _, b, c in ev) / 1e3
     infos = st.infos()
     from paper_2509_20500_b200.shard import max_over_ranks
     t_total, t_build, t_solve = max_over_ranks([t_total, t_build, t_solve], device="cuda")
@@ -222,8 +266,11 @@ def run_ours(args, rank, world, dev):
         per_m = np.array([i["iters"] for i in plan_info]).reshape(p.M, p.V).max(axis=1)
         launches_gemv += int(per_m.max())
         gemv_bytes += int(per_m.sum()) * N * N * b
-    per_step_launches = 3 + sum(2 + 2 * int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
-                                for pi, p in zip(infos, st.plans))
+    if graphed:
+        per_step_launches = 3 + len(st.plans)
+    else:
+        per_step_launches = 3 + sum(2 + 2 * int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
+                                    for pi, p in zip(infos, st.plans))
     hbm, hbm_src = load_peaks()
     traffic = load_traffic(args.workload, args.dtype)
     K = args.steps
@@ -245,7 +292,10 @@ def run_ours(args, rank, world, dev):
                    "tol": 1e-12, "l2": "matrix (%.2f GB) > 126 MB L2: no flush needed" % (st.entries * b / 1e9)
                    if st.entries * b > 126e6 else "matrix fits in L2 (latency-bound config); not flushed",
                    "parallelism": (f"dp{world}: items sharded over {world} ranks, no collective on the data path"
-                                   if world > 1 else "single GPU")},
+                                   if world > 1 else "single GPU"),
+                   "solver": "fused (one clustered launch per plan, N <= 2048)" if all(p.fused for p in st.plans)
+                   else "graph (GEMV + check in a conditional WHILE node)",
+                   "step_as_cuda_graph": bool(graphed)},
         "entries_per_s": st.entries * K * world / t_build,
         "ms_build_per_step": t_build / K * 1e3, "ms_solve_per_step": t_solve / K * 1e3,
         "iterations": [[i["iters"] for i in pi] for pi in infos],
@@ -729,7 +779,10 @@ def main():
     if args.path == "dense":
         line = run_ours(args, rank, world, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = run_oracle_sample(args, line["iterations"])
+            its = line["iterations"]
+            if len(its) == 1 and len(its[0]) > 1 and args.workload != "c5":
+                its = [[x] for x in its[0]]          # one plan over M matrices -> one list per item
+            line["cpu_baseline"] = run_oracle_sample(args, its)
     elif args.path == "mc":
         line = run_mc(args, rank, world, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:

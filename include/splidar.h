@@ -177,6 +177,14 @@ splidar_status splidar_plan_execute(splidar_plan plan, splidar_solve_info *info 
 splidar_status splidar_plan_launch(splidar_plan plan, void *stream);
 splidar_status splidar_plan_info(splidar_plan plan, splidar_solve_info *info, void *stream);
 void splidar_plan_destroy(splidar_plan plan);
+/* How a plan runs: SPLIDAR_PLAN_GRAPH (instantiated CUDA graph: [GEMV -> check] in a conditional WHILE
+ * node; N > 2048) or SPLIDAR_PLAN_FUSED (N <= 2048: one clustered launch runs every iteration of every
+ * (matrix, dead time) pair, P~0 rows staged in shared memory or streamed from L2; a single kernel
+ * launch, so splidar_plan_launch may be captured into a caller's CUDA graph). -1 for NULL.
+ * SPLIDAR_FUSED=0 in the environment at plan creation forces the graph form. */
+#define SPLIDAR_PLAN_GRAPH 0
+#define SPLIDAR_PLAN_FUSED 1
+int splidar_plan_kind(splidar_plan plan);
 
 /* ---------------------------------------------------------------------------------------------
  * Matrix-free (structured) operator: SURVEY §8(f) rows f2 and f1.

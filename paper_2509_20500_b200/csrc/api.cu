@@ -298,6 +298,10 @@ struct splidar_plan_s {
     PowerArgs eager_args;
     std::vector<unsigned char> fin_args;
     unsigned *host_flag = nullptr;
+    // small N: every iteration of every (matrix, vector) in one clustered launch (fused.cu)
+    bool fused = false;
+    int dt = 0;
+    FusedArgs fargs;
 };
 
 static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws, cudaStream_t s) {
@@ -323,6 +327,33 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
 
     SPL_CUDA(spl::upload_async(ws + L.lsh, p->lsh.data(), sizeof(int) * p->lsh.size(), s));
     SPL_CUDA(spl::upload_async(ws + L.oidx, p->out_idx.data(), sizeof(int) * p->out_idx.size(), s));
+
+    {   // small N: the fused single-launch solver (SPLIDAR_FUSED=0 forces the general path)
+        const char *e = getenv("SPLIDAR_FUSED");
+        int C, R;
+        if (!(e && e[0] == '0') && !fused_shape(L.N, &C, &R)) {
+            p->fused = true;
+            p->dt = dt;
+            FusedArgs &f = p->fargs;
+            memset(&f, 0, sizeof(f));
+            f.P = a.P;
+            f.ld = a.ld;
+            f.mstride = a.mstride;
+            f.N = L.N;
+            f.M = L.M;
+            f.V = L.V;
+            f.C = C;
+            f.R = R;
+            f.resident = fused_resident(L.N, R, dt);
+            f.lsh = reinterpret_cast<const int *>(ws + L.lsh);
+            f.out_idx = reinterpret_cast<const int *>(ws + L.oidx);
+            f.pi = pi;
+            f.st = a.st;
+            f.tol = a.tol;
+            f.max_iter = a.max_iter;
+            return SPLIDAR_OK;
+        }
+    }
 
     SPL_CUDA(cudaGraphCreate(&p->graph, 0));
     cudaGraphConditionalHandle h;
@@ -467,8 +498,11 @@ static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
     return SPLIDAR_OK;
 }
 
+int splidar_plan_kind(splidar_plan plan) { return !plan ? -1 : plan->fused ? SPLIDAR_PLAN_FUSED : SPLIDAR_PLAN_GRAPH; }
+
 splidar_status splidar_plan_launch(splidar_plan plan, void *stream) {
     if (!plan) return SPLIDAR_EINVAL;
+    if (plan->fused) return cuda_status(launch_fused(plan->dt, plan->fargs, (cudaStream_t)stream));
     if (plan->eager) return plan_launch_eager(plan, (cudaStream_t)stream);
     return cuda_status(cudaGraphLaunch(plan->exec, (cudaStream_t)stream));
 }

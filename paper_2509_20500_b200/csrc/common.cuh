@@ -138,6 +138,23 @@ enum { kStructSolve = 0, kStructLambda2 = 1, kStructMixing = 2, kStructTraj = 3 
 int struct_shape(int N, int *C, int *threads);
 cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s);
 
+// ---- fused small-N dense solve (fused.cu): all iterations of one (matrix, vector) in one cluster
+struct FusedArgs {
+    const void *P;
+    int64_t ld, mstride;
+    int N, M, V, C, R;
+    int resident;               // rows of P~0 copied to shared memory once
+    const int *lsh;             // [M][V]
+    const int *out_idx;         // [M][V]
+    double *pi;
+    SolveState *st;             // [M][V]
+    double tol;
+    int max_iter;
+};
+int fused_shape(int N, int *C, int *R);
+int fused_resident(int N, int R, int dtype);
+cudaError_t launch_fused(int dtype, const FusedArgs &a, cudaStream_t s);
+
 // ---- Monte Carlo of the detection process (mc.cu) ------------------------------
 struct McArgs {
     const FluxDev *flux;        // [profiles]

@@ -14,7 +14,8 @@
 //            (the row sum of (1 lambda^T) . exp.(-Lambda L - D), §3.4, over e^{F_r})
 //   invD_r   = 1 / D_r, invZ_r = e^{-F_r} / D_r (normalisation)
 //
-// Five grid-wide launches per batch of profiles (grid = tiles x profiles):
+// N < 8192: one launch, one 1024-thread CTA per profile (k_vec_small, the same three scans in one CTA).
+// Larger N: five grid-wide launches per batch of profiles (grid = tiles x profiles):
 //   A  masses + lambda, tile-local inclusive scan of the masses, tile totals
 //   B  exclusive scan of the tile totals (one CTA per profile) -> tile offsets, Lambda
 //   C  F = local + offset, w, tile-local exclusive prefix / inclusive suffix of w, tile totals of w
@@ -268,6 +269,120 @@ __global__ void __launch_bounds__(kT) k_vec_e(int N, int M, VecPtrs b, int64_t v
     if (bad) b.scal[m * 8 + 2] = 1.0;
 }
 
+// ---- N < 8192: the five launches above as ONE CTA per profile (1024 threads x 8 consecutive slots;
+// same sums: thread-local run, warp __shfl_up_sync scan, scan of the 32 warp totals).
+constexpr int kST = 1024, kSEl = 8;
+
+// inclusive scan of 8 consecutive values per thread over the block; returns the block total
+__device__ double small_scan(double (&v)[kSEl], double *wt) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 1; i < kSEl; ++i) v[i] += v[i - 1];
+    const double t = v[kSEl - 1];
+    double x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    double ex = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) ex = 0.0;
+    if (lane == 31) wt[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const double a = wt[lane];
+        double z = a;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += y;
+        }
+        wt[32 + lane] = z - a;            // exclusive prefix of the warp totals
+        if (lane == 31) wt[64] = z;       // block total
+    }
+    __syncthreads();
+    const double off = wt[32 + warp] + ex;
+#pragma unroll
+    for (int i = 0; i < kSEl; ++i) v[i] += off;
+    const double tot = wt[64];
+    __syncthreads();
+    return tot;
+}
+
+__global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ fluxes, int N, VecPtrs b,
+                                                   int64_t vstride) {
+    __shared__ double wt[65];
+    extern __shared__ double rev[];      // [kST * kSEl]: w reversed, then its inclusive scan
+    const int m = blockIdx.x;
+    const FluxDev &f = fluxes[m];
+    const int e0 = threadIdx.x * kSEl;
+    double *F = b.F + m * vstride, *lam = b.lam + m * vstride, *w = b.w + m * vstride;
+    double *invD = b.invD + m * vstride, *invZ = b.invZ + m * vstride;
+    // masses (N + 1 of them) and their inclusive scan: F_j = F(s_j), Lambda = F(t_r)
+    double wv[kSEl];
+#pragma unroll
+    for (int i = 0; i < kSEl; ++i) {
+        const int e = e0 + i;
+        wv[i] = 0.0;
+        if (e <= N) {
+            const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
+            const double hi = e == N ? f.t_r : bin_centre(f, e);
+            wv[i] = flux_mass(f, lo, hi);
+        }
+    }
+    const double Lam = small_scan(wv, wt);
+    const double eL = exp(-Lam);
+    // lambda_j, w_j = lambda_j e^{-F_j}
+#pragma unroll
+    for (int i = 0; i < kSEl; ++i) {
+        const int e = e0 + i;
+        if (e < N) {
+            const double lm = flux_rate(f, bin_centre(f, e));
+            F[e] = wv[i];
+            lam[e] = lm;
+            wv[i] = lm * exp(-wv[i]);
+            w[e] = wv[i];
+        } else {
+            wv[i] = 0.0;
+        }
+        rev[kST * kSEl - 1 - e] = wv[i];
+    }
+    double pf[kSEl];
+#pragma unroll
+    for (int i = 0; i < kSEl; ++i) pf[i] = wv[i];
+    small_scan(pf, wt);                          // prefix of w (its barriers publish rev[])
+    {
+        double sf[kSEl];
+#pragma unroll
+        for (int i = 0; i < kSEl; ++i) sf[i] = rev[e0 + i];
+        small_scan(sf, wt);                      // inclusive scan of the reversed w
+#pragma unroll
+        for (int i = 0; i < kSEl; ++i) rev[e0 + i] = sf[i];
+    }
+    __syncthreads();
+    int bad = 0;
+#pragma unroll
+    for (int i = 0; i < kSEl; ++i) {
+        const int r = e0 + i;
+        if (r < N) {
+            const double L = pf[i] - wv[i];                   // sum_{j < r} w_j (exclusive prefix)
+            const double U = rev[kST * kSEl - 1 - r];         // sum_{j >= r} w_j (inclusive suffix)
+            const double D = U + eL * L;
+            bad |= !(D > 0.0 && isfinite(D));
+            const double id = 1.0 / D;
+            invD[r] = id;
+            invZ[r] = id * (wv[i] / lam[r]);                  // e^{-F_r} / D_r
+        }
+    }
+    if (threadIdx.x == 0) {
+        b.scal[m * 8 + 0] = Lam;
+        b.scal[m * 8 + 1] = eL;
+        b.scal[m * 8 + 2] = 0.0;
+    }
+    __syncthreads();
+    if (bad) b.scal[m * 8 + 2] = 1.0;
+}
+
 }  // namespace
 
 cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs base, int64_t vstride,
@@ -275,6 +390,17 @@ cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs bas
     const int nt = base.ntile;                         // tiles over the N + 1 masses
     const int ntN = (N + kScanTile - 1) / kScanTile;   // tiles over the N bins
     if (nt > 4096) return cudaErrorInvalidValue;
+    if (N + 1 <= kST * kSEl) {                         // one CTA per profile, one launch
+        const int smem = (int)(sizeof(double) * kST * kSEl);
+        static bool attr = false;           // once per process (not inside every captured launch)
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute((const void *)k_vec_small, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        k_vec_small<<<M, kST, smem, s>>>(d_flux, N, base, vstride);
+        return cudaGetLastError();
+    }
     k_vec_a<<<dim3(nt, M), kT, 0, s>>>(d_flux, N, M, base, vstride);
     k_vec_b<<<M, 1024, 0, s>>>(M, nt, base);
     k_vec_c<<<dim3(ntN, M), kT, 0, s>>>(N, M, base, vstride);

@@ -1,0 +1,307 @@
+// Step 4 for small N (N <= 2048): the whole power iteration of one (matrix, dead time) pair in ONE
+// launch, on one thread-block cluster, reading the STORED P~0 (the same GEMV as k_power_step, without
+// its per-iteration launches). At these sizes the matrices are L2-resident and the general path is
+// bound by launch and graph latency (c1: ~30 us per iteration), not by bandwidth.
+//
+// Cluster of C CTAs (C = min(16, ceil(N / 32))): CTA c owns the rows [c R, (c + 1) R) of P~0 and the
+// output columns [c W, (c + 1) W) (R = W = ceil(N / C)). Its rows of P~0 are copied to shared memory
+// once when they fit in 96 KB (N <= 384 fp64 / 512 fp32 at R = 32), else streamed from L2 (4 rows per
+// step, their loads in flight together). One product pi P~ = x P~0 with the gathered
+// x_r = v[(r - l) mod N] (Thm 2):
+//   A  partial y over the CTA's rows (x_r from shared memory, fp64 FMA) ->
+//      each partial column slice pushed to its owner over DSMEM; barrier.cluster
+//   B  owners add the C partials in fixed order -> y_j; sum of y; y_j pushed (unnormalised) to the
+//      x buffer of the CTA owning row (j + l) mod N; barrier.cluster
+//   C  s = sum y, the L1 change of the normalised iterates (published with the next A)
+// Same definition as the general path: pi^0 = 1/N, pi^{k+1} = y / ||y||_1, stop after the first
+// product with ||pi^{k+1} - pi^k||_1 < tol (decided one exchange later, on identical sums in every
+// CTA), or after max_iter products. Deterministic: fixed-order sums, no atomics.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace spl {
+namespace {
+
+constexpr int kFT = 256;          // threads per CTA
+constexpr int kFMaxC = 16;
+constexpr int kFMaxCols = 8;      // columns per thread: N <= 2 * 256 * 4 = 2048
+
+struct FusedShared {
+    double exA[2 * kFMaxC];       // scan of nothing: [0] unused, change partials
+    double exB[kFMaxC];           // sum partials
+    double red[kFT / 32];
+};
+
+__device__ __forceinline__ uint32_t fsmem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void fmbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(fsmem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fmbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fsmem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void fmbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(fsmem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+// 1-D TMA bulk copy global -> shared (bytes % 16 == 0), completion counted on the mbarrier
+__device__ __forceinline__ void fbulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(fsmem_u32(dst)), "l"(src), "r"(bytes), "r"(fsmem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ double fwarp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// block sum, every thread gets the total (fixed order)
+__device__ __forceinline__ double fblock_sum(double v, double *red) {
+    v = fwarp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kFT / 32; ++w) s += red[w];
+    __syncthreads();
+    return s;
+}
+
+// Q = column pairs per thread (N <= 512 Q), RS = rows whose loads are in flight together.
+template <typename T, int Q>
+__global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
+    constexpr int NC = 2 * Q;
+    constexpr int RS = Q <= 2 ? 8 : 4;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double fsm[];
+    __shared__ FusedShared sh;
+    const int C = a.C, c = (int)cl.block_rank();
+    const int mv = blockIdx.x / C;
+    const int N = a.N, R = a.R;                      // rows / owned columns per CTA
+    const int m = mv / a.V;
+    const int l = a.lsh[mv];
+    double *xb = fsm;                                // [R]      gathered x of my rows
+    double *recv = fsm + R;                          // [C][R]   partials of my columns from every CTA
+    double *yp = recv + (size_t)C * R;               // [R]      previous y of my columns
+    const int NP = (N + 3) & ~3;                     // row stride: 16-byte aligned rows for both dtypes
+    T *slice = reinterpret_cast<T *>(fsm + (((size_t)R * (C + 2) + 1) & ~(size_t)1));   // [R][NP] (a.resident)
+    if (l < 0) {                                     // padding vector: nothing to solve
+        if (c == 0 && threadIdx.x == 0) {
+            SolveState st = {};
+            st.l = -1;
+            st.done = 1;
+            a.st[mv] = st;
+        }
+        return;
+    }
+    const int r0 = c * R, r1 = min(N, r0 + R);
+    const T *P = reinterpret_cast<const T *>(a.P) + (size_t)m * a.mstride;
+    const int nrow = r1 - r0;
+    if (a.resident) {                                // my rows, once, by TMA bulk copies; then smem only
+        __shared__ uint64_t bar;
+        const uint32_t row_bytes = (uint32_t)(((size_t)N * sizeof(T) + 15) & ~(size_t)15);   // <= ld bytes
+        if (threadIdx.x == 0) {
+            fmbar_init(&bar, 1);
+            fmbar_expect_tx(&bar, row_bytes * (uint32_t)nrow);
+            for (int r = 0; r < nrow; ++r) fbulk_g2s(slice + (size_t)r * NP, P + (size_t)(r0 + r) * a.ld, row_bytes, &bar);
+        }
+        __syncthreads();
+        fmbar_wait(&bar, 0);
+    }
+    const double u = 1.0 / (double)N;
+    for (int i = threadIdx.x; i < R; i += kFT) {
+        xb[i] = r0 + i < N ? u : 0.0;                // gathered uniform vector
+        yp[i] = c * R + i < N ? u : 0.0;
+    }
+    double s_prev = 1.0, dpart = 0.0, change = __longlong_as_double(0x7ff0000000000000ll);
+    int k = 0, conv = 0;
+    cl.sync();
+    for (;;) {
+        // ---- A: partial y over my rows; column j = 2 t + 512 q + e; 4 rows per step, all their
+        // loads issued before the FMAs (shared memory when resident, else L2)
+        double acc[NC];
+#pragma unroll
+        for (int i = 0; i < NC; ++i) acc[i] = 0.0;
+        const T *base = a.resident ? slice : P + (size_t)r0 * a.ld;
+        const int64_t rs = a.resident ? NP : a.ld;
+        for (int r = 0; r < nrow; r += RS) {
+            double xr[RS];
+            double pv[RS][NC];
+#pragma unroll
+            for (int rr = 0; rr < RS; ++rr) {
+                const bool rin = r + rr < nrow;
+                xr[rr] = rin ? xb[r + rr] : 0.0;
+                const T *row = base + (size_t)(rin ? r + rr : r) * rs;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const int j = 2 * threadIdx.x + 2 * kFT * q;
+                    pv[rr][2 * q] = pv[rr][2 * q + 1] = 0.0;
+                    if (j < N) {
+                        if constexpr (sizeof(T) == 8) {
+                            const double2 v = a.resident ? *reinterpret_cast<const double2 *>(row + j)
+                                                         : __ldg(reinterpret_cast<const double2 *>(row + j));
+                            pv[rr][2 * q] = v.x; pv[rr][2 * q + 1] = v.y;
+                        } else {
+                            const float2 v = a.resident ? *reinterpret_cast<const float2 *>(row + j)
+                                                        : __ldg(reinterpret_cast<const float2 *>(row + j));
+                            pv[rr][2 * q] = v.x; pv[rr][2 * q + 1] = v.y;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int rr = 0; rr < RS; ++rr)
+#pragma unroll
+                for (int i = 0; i < NC; ++i) acc[i] = fma(xr[rr], pv[rr][i], acc[i]);
+        }
+        // push partials to the owners of the columns: recv[c][j - owner R] in the owner's smem
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = 2 * threadIdx.x + 2 * kFT * q + e;
+                if (j < N) {
+                    const int ow = j / R;
+                    cl.map_shared_rank(recv, ow)[(size_t)c * R + (j - ow * R)] = acc[2 * q + e];
+                }
+            }
+        }
+        if (threadIdx.x < C) cl.map_shared_rank(sh.exA, threadIdx.x)[kFMaxC + c] = dpart;
+        cl.sync();   // A
+        if (k > 0) {
+            double t = 0.0;
+            for (int cc = 0; cc < C; ++cc) t += sh.exA[kFMaxC + cc];
+            change = t;
+            if (change < a.tol) { conv = 1; break; }
+            if (k >= a.max_iter || !(s_prev > 0.0) || !isfinite(change)) break;
+        }
+        // ---- B: owners add the partials (fixed order); push y to the x buffers; publish sum(y)
+        double ys = 0.0, yj = 0.0;
+        const int j = c * R + (int)threadIdx.x;
+        const bool own = (int)threadIdx.x < R && j < N;
+        if (own) {
+            for (int cc = 0; cc < C; ++cc) yj += recv[(size_t)cc * R + threadIdx.x];
+            ys = yj;
+            int r = j + l;
+            if (r >= N) r -= N;
+            const int ow = r / R;
+            cl.map_shared_rank(xb, ow)[r - ow * R] = yj;
+        }
+        ys = fblock_sum(ys, sh.red);
+        if (threadIdx.x < C) cl.map_shared_rank(sh.exB, threadIdx.x)[c] = ys;
+        cl.sync();   // B
+        double s = 0.0;
+        for (int cc = 0; cc < C; ++cc) s += sh.exB[cc];
+        // ---- C: L1 change of the normalised iterates over my columns
+        double d = 0.0;
+        if (own) {
+            d = fabs(yj / s - yp[threadIdx.x] / s_prev);
+            yp[threadIdx.x] = yj;
+        }
+        dpart = fblock_sum(d, sh.red);
+        s_prev = s;
+        ++k;
+    }
+    // pi^k = y / s over my columns
+    const int o = a.out_idx[mv];
+    if (o >= 0) {
+        const int j = c * R + (int)threadIdx.x;
+        if ((int)threadIdx.x < R && j < N) a.pi[(size_t)o * N + j] = yp[threadIdx.x] / s_prev;
+    }
+    if (c == 0 && threadIdx.x == 0) {
+        SolveState st;
+        st.l = l;
+        st.iters = k;
+        st.done = 1;
+        st.converged = conv;
+        st.cur = 0;
+        st.pad0 = st.pad1 = st.pad2 = 0;
+        st.s = s_prev;
+        st.change = change;
+        a.st[mv] = st;
+    }
+}
+
+}  // namespace
+
+int fused_shape(int N, int *C, int *R) {
+    if (N > kFMaxCols * kFT) return 1;
+    int c = (N + 31) / 32;
+    if (c > kFMaxC) c = kFMaxC;
+    if (c < 1) c = 1;
+    int r = (N + c - 1) / c;
+    if (r > kFT) return 1;
+    *C = c;
+    *R = r;
+    return 0;
+}
+
+constexpr size_t kFResidentMax = 96 * 1024;   // largest row slice kept in shared memory
+
+size_t fused_slice_bytes(int N, int R, int dtype) {
+    return (size_t)R * ((N + 3) & ~3) * (dtype == SPLIDAR_F64 ? 8 : 4);
+}
+size_t fused_smem(const FusedArgs &a, int dtype) {
+    return sizeof(double) * (((size_t)a.R * (a.C + 2) + 1) & ~(size_t)1) +
+           (a.resident ? fused_slice_bytes(a.N, a.R, dtype) : 0);
+}
+
+template <typename T>
+void *fused_fn_q(int N) {
+    const int q = (N + 2 * kFT - 1) / (2 * kFT);
+    if (q <= 1) return (void *)k_power_fused<T, 1>;
+    if (q <= 2) return (void *)k_power_fused<T, 2>;
+    return (void *)k_power_fused<T, 4>;
+}
+
+void *fused_fn(int dtype, int N) {
+    void *fn = dtype == SPLIDAR_F64 ? fused_fn_q<double>(N) : fused_fn_q<float>(N);
+    static void *done[8] = {};              // attributes set once per kernel instance
+    for (int i = 0; i < 8; ++i) {
+        if (done[i] == fn) return fn;
+        if (!done[i]) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            done[i] = fn;
+            return fn;
+        }
+    }
+    return fn;
+}
+
+int fused_resident(int N, int R, int dtype) { return fused_slice_bytes(N, R, dtype) <= kFResidentMax; }
+
+cudaError_t launch_fused(int dtype, const FusedArgs &a, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.M * a.V * a.C));
+    cfg.blockDim = dim3(kFT);
+    cfg.dynamicSmemBytes = fused_smem(a, dtype);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)a.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    void *fn = fused_fn(dtype, a.N);
+    void *args[] = {const_cast<FusedArgs *>(&a)};
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+}  // namespace spl

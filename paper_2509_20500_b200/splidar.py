@@ -90,6 +90,7 @@ def _lib():
             "splidar_plan_launch": (st, [p, p]),
             "splidar_plan_info": (st, [p, pinfo, p]),
             "splidar_plan_destroy": (None, [p]),
+            "splidar_plan_kind": (C.c_int, [p]),
             "splidar_structured_workspace_bytes": (sz, [i32, i32, i32]),
             "splidar_stationary_structured": (st, [fp, i32, p, p, p, d, i32, p, p, sz, pinfo, p]),
             "splidar_second_eigenvalue": (st, [fp, i32, p, p, p, p, d, i32, p, sz, C.POINTER(SpectralInfo), p]),
@@ -325,6 +326,11 @@ class Plan:
 
     def launch(self, stream=None):
         _check(_lib().splidar_plan_launch(self._h, _stream(stream)), "splidar_plan_launch")
+
+    @property
+    def fused(self) -> bool:
+        """True when the plan is one clustered launch (N <= 2048), capturable into a CUDA graph."""
+        return _lib().splidar_plan_kind(self._h) == 1
 
     def info(self, stream=None, check: bool = True) -> list:
         infos = (SolveInfo * (self.M * self.V))()

@@ -335,3 +335,26 @@ def test_multivector_counts(spl, nv):
         want = oracle.stationary_dense(oracle.build_eq4(f, tds[v]))
         assert np.sum(np.abs(_np(plan.pi[0, v]) - want)) <= TOL_PI64
     plan.close()
+
+
+# ------------------------------------------------------------- small-N fused solver vs the general path
+@pytest.mark.parametrize("case", CASES[::2] + [config(1).items[0], config(2).items[3]],
+                         ids=IDS[::2] + ["config1", "config2-item3"])
+def test_fused_equals_general_path(spl, case, monkeypatch):
+    """N <= 2048 plans run the fused cluster solver; the same plan forced onto the general graph path
+    (SPLIDAR_FUSED=0) gives the same pi (<= 1e-14 L1) and iteration count (+-1), for fp64 and fp32."""
+    f = case.flux
+    for dt in (torch.float64, torch.float32):
+        P0 = spl.build_base(f, dt)
+        tds = [case.t_d, case.t_d + 7.3]
+        fused = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-12)
+        i_f = fused.execute(check=False)
+        monkeypatch.setenv("SPLIDAR_FUSED", "0")
+        general = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-12)
+        monkeypatch.delenv("SPLIDAR_FUSED")
+        i_g = general.execute(check=False)
+        for v in range(2):
+            assert abs(i_f[v]["iters"] - i_g[v]["iters"]) <= 1
+            assert np.sum(np.abs(_np(fused.pi[0, v]) - _np(general.pi[0, v]))) <= 1e-13
+        fused.close()
+        general.close()
