@@ -202,3 +202,90 @@ def test_parity_cases_are_well_formed():
     assert {2, 3, 1000, 1537, 2048} <= ns
     assert any(c.t_d == 0.0 for c in cases) and any(c.t_d > 2 * c.flux.t_r for c in cases)
     assert any(c.flux.n_pulses == 2 for c in cases)
+
+
+# ------------------------------------------------------------------ §8(f) entry points: host validation
+def _items(S=(0.5,), B=(0.1,), T=(75.0,)):
+    return (np.ascontiguousarray(S, dtype=np.float64), np.ascontiguousarray(B, dtype=np.float64),
+            np.ascontiguousarray(T, dtype=np.float64))
+
+
+def test_structured_workspace_bytes(spl):
+    lib = spl._lib()
+    assert lib.splidar_structured_workspace_bytes(65536, 1, 1) > 0          # a cluster of 16 CTAs
+    assert lib.splidar_structured_workspace_bytes(65537, 1, 1) == 0         # beyond 16 x 4096 bins
+    assert lib.splidar_structured_workspace_bytes(1, 1, 1) == 0
+    assert lib.splidar_structured_workspace_bytes(256, 0, 1) == 0
+    a = lib.splidar_structured_workspace_bytes(4096, 3, 10)
+    assert a % 256 == 0 and lib.splidar_structured_workspace_bytes(4096, 3, 20) > a
+    assert lib.splidar_mc_workspace_bytes(2, 5) > 0 and lib.splidar_mc_workspace_bytes(0, 5) == 0
+
+
+def test_structured_rejects(spl):
+    lib = spl._lib()
+    fa = _flux_struct(spl)
+    S, B, T = _items()
+    ws = lib.splidar_structured_workspace_bytes(256, 1, 1)
+
+    def solve(S=S, B=B, T=T, tol=1e-12, it=100, pi=FAKE, wsb=ws, n=1):
+        return lib.splidar_stationary_structured(C.byref(fa.s), n, S.ctypes.data, B.ctypes.data, T.ctypes.data, tol,
+                                                 it, pi, FAKE, wsb, None, None)
+    assert solve(tol=0.0) == spl.EINVAL
+    assert solve(it=0) == spl.EINVAL
+    assert solve(pi=None) == spl.EINVAL
+    assert solve(n=0) == spl.EINVAL
+    assert solve(T=np.array([-1.0])) == spl.EINVAL
+    assert solve(B=np.array([0.0])) == spl.EINVAL                           # B = 0: reducible chain (R16)
+    assert solve(S=np.array([-0.5])) == spl.EINVAL
+    assert solve(wsb=ws - 1) == spl.ENOSPACE
+    info = spl.SpectralInfo()
+    assert lib.splidar_second_eigenvalue(C.byref(fa.s), 1, S.ctypes.data, B.ctypes.data, T.ctypes.data, None, 1e-13,
+                                         100, FAKE, ws, C.byref(info), None) == spl.EINVAL
+    h = C.c_void_p(None)
+    assert lib.splidar_splan_create(C.byref(h), 7, C.byref(fa.s), 1, S.ctypes.data, B.ctypes.data, T.ctypes.data,
+                                    1e-12, 100, FAKE, FAKE, ws, None) == spl.EINVAL
+    assert not h.value
+    out = C.c_int32(0)
+    wsm = lib.splidar_structured_workspace_bytes(256, 1, 256)
+    assert lib.splidar_mixing_steps(C.byref(fa.s), 75.0, FAKE, 0.0, 100, None, C.byref(out), FAKE, wsm,
+                                    None) == spl.EINVAL
+    assert lib.splidar_mixing_steps(C.byref(fa.s), 75.0, FAKE, 1e-3, 100, None, C.byref(out), FAKE, wsm - 1,
+                                    None) == spl.ENOSPACE
+    assert lib.splidar_bin_trajectory(C.byref(fa.s), 75.0, FAKE, 256, 10, FAKE, None, FAKE, ws, None) == spl.EINVAL
+    assert lib.splidar_bin_trajectory(C.byref(fa.s), 75.0, FAKE, 0, -1, FAKE, None, FAKE, ws, None) == spl.EINVAL
+
+
+def test_monte_carlo_rejects(spl):
+    lib = spl._lib()
+    fa = _flux_struct(spl)
+    S, B, T = _items()
+    ws = lib.splidar_mc_workspace_bytes(1, 1)
+
+    def mc(runs=4, split=1, burn=10, regs=100, cycles=0, nh=16, hist=FAKE, nrec=0, wsb=ws, T=T):
+        return lib.splidar_monte_carlo(C.byref(fa.s), 1, S.ctypes.data, B.ctypes.data, T.ctypes.data, 1, runs, split,
+                                       burn, regs, cycles, nh, hist, nrec, None, None, FAKE, wsb, None)
+    assert mc(runs=0) == spl.EINVAL
+    assert mc(split=0) == spl.EINVAL
+    assert mc(regs=0, cycles=0) == spl.EINVAL
+    assert mc(split=3, regs=100) == spl.EINVAL                              # budget not divisible by n_split
+    assert mc(split=4, regs=0, cycles=50001) == spl.EINVAL
+    assert mc(nh=0) == spl.EINVAL
+    assert mc(hist=None) == spl.EINVAL
+    assert mc(nrec=5) == spl.EINVAL                                         # records requested, no buffers
+    assert mc(T=np.array([-2.0])) == spl.EINVAL
+    assert mc(wsb=ws - 1) == spl.ENOSPACE
+
+
+def test_build_eq4_rejects(spl):
+    lib = spl._lib()
+    fa = _flux_struct(spl)
+    assert lib.splidar_build_eq4(C.byref(fa.s), -1.0, spl.F64, FAKE, 256, None) == spl.EINVAL
+    assert lib.splidar_build_eq4(C.byref(fa.s), math.inf, spl.F64, FAKE, 256, None) == spl.EINVAL
+    assert lib.splidar_build_eq4(C.byref(fa.s), 75.0, spl.F64, FAKE, 250, None) == spl.ENOSPACE
+    assert lib.splidar_build_eq4(C.byref(fa.s), 75.0, spl.F64, None, 256, None) == spl.EINVAL
+    bad = _flux_struct(spl, background=0.0)
+    assert lib.splidar_build_eq4(C.byref(bad.s), 75.0, spl.F64, FAKE, 256, None) == spl.EINVAL
+
+
+def test_plan_kind_null(spl):
+    assert spl._lib().splidar_plan_kind(None) == -1
