@@ -1,7 +1,7 @@
 // Step 2 (K4): the normalised base matrix P~0 and step 3 materialised (K5): the row permutation.
 //
 // P~0[r][j] = lambda_j exp(F_r - F_j - Lambda [r > j]) / Z_r            (mode EXP)
-//           = w_j (r > j ? e^{-Lambda} : 1) / D_r                        (mode FACTORED)
+//           = w_j (r > j ? e^{-Lambda} / D_r : 1 / D_r)                  (mode FACTORED)
 // from E_base = exp.(-Lambda L - D), L_rj = 1{s_r > s_j}, D_rj = F(s_j) - F(s_r),
 // P = (1 lambda^T) . E, row-normalised (§3.4).
 //
@@ -42,13 +42,13 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
     const bool full = j0 + VEC <= N;
 
     // column operands in registers
-    double a[VEC], b[VEC];   // FACTORED: a = w_j, b = w_j e^{-Lambda};  EXP: a = lambda_j, b = F_j
+    double a[VEC], b[VEC];   // FACTORED: a = w_j;  EXP: a = lambda_j, b = F_j
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
         const int j = j0 + e;
         if (MODE == SPLIDAR_ENTRY_FACTORED) {
             a[e] = j < N ? w[j] : 0.0;
-            b[e] = a[e] * eL;
+            b[e] = 0.0;
         } else {
             a[e] = j < N ? lam[j] : 0.0;
             b[e] = j < N ? F[j] : 0.0;
@@ -59,9 +59,12 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
     for (int r = r0; r < r1; ++r) {
         T val[VEC];
         if (MODE == SPLIDAR_ENTRY_FACTORED) {
-            const double inv = __ldg(invD + r);
+            // row multipliers 1/D_r (j >= r) and e^{-Lambda}/D_r (j < r): forming w_j e^{-Lambda} first
+            // would underflow (~e^{-2 Lambda}) for Lambda > ~350, while e^{-Lambda}/D_r stays O(1)
+            const double inv_hi = __ldg(invD + r);
+            const double inv_lo = eL * inv_hi;
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) val[e] = (T)((j0 + e < r ? b[e] : a[e]) * inv);
+            for (int e = 0; e < VEC; ++e) val[e] = (T)(a[e] * (j0 + e < r ? inv_lo : inv_hi));
         } else {
             const double iz = __ldg(invZ + r);
             const double Fr = __ldg(F + r);

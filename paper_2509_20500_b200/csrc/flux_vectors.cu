@@ -78,6 +78,11 @@ __device__ double tile_scan(double (&v)[kE], double *warp_tot) {
         const double y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
+    // exclusive prefix of the thread totals by a shuffle, never as (inclusive - own): with values
+    // spanning hundreds of decades (w = lambda e^{-F} at large Lambda) the subtraction would leave
+    // an error of ulp(own) on a much smaller prefix
+    double xe = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) xe = 0.0;
     if (lane == 31) warp_tot[warp] = x;
     __syncthreads();
     double wex = 0.0, total = 0.0;
@@ -87,7 +92,8 @@ __device__ double tile_scan(double (&v)[kE], double *warp_tot) {
         if (w2 < warp) wex += wt;
         total += wt;
     }
-    const double ex = (x - t) + wex;
+    (void)t;
+    const double ex = xe + wex;
 #pragma unroll
     for (int i = 0; i < kE; ++i) v[i] += ex;
     __syncthreads();
@@ -98,7 +104,7 @@ __device__ double tile_scan(double (&v)[kE], double *warp_tot) {
 // order: pre[i] = sum_{k<i} in[k], suf[i] = sum_{k>i} in[k]; returns the total (pre or suf may
 // be null).
 __device__ double totals_scan(const double *in, int n, double *pre, double *suf) {
-    __shared__ double wt_f[32], wt_b[32];
+    __shared__ double wt_f[65], wt_b[65];
     constexpr int EPT = 4;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double f[EPT], bk[EPT];
@@ -108,18 +114,21 @@ __device__ double totals_scan(const double *in, int n, double *pre, double *suf)
         f[i] = e0 + i < n ? in[e0 + i] : 0.0;
         bk[i] = e0 + i < n ? in[n - 1 - (e0 + i)] : 0.0;   // reversed sequence for the suffix
     }
-    const double f0[EPT] = {f[0], f[1], f[2], f[3]};
-    const double b0[EPT] = {bk[0], bk[1], bk[2], bk[3]};
+    // thread-local EXCLUSIVE running sums (no subtraction anywhere: see tile_scan)
+    double fe[EPT], be[EPT];
+    fe[0] = 0.0;
+    be[0] = 0.0;
 #pragma unroll
-    for (int i = 1; i < EPT; ++i) { f[i] += f[i - 1]; bk[i] += bk[i - 1]; }
-    double xf = f[EPT - 1], xb = bk[EPT - 1];
-    const double tf = xf, tb = xb;
+    for (int i = 1; i < EPT; ++i) { fe[i] = fe[i - 1] + f[i - 1]; be[i] = be[i - 1] + bk[i - 1]; }
+    double xf = fe[EPT - 1] + f[EPT - 1], xb = be[EPT - 1] + bk[EPT - 1];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const double yf = __shfl_up_sync(0xffffffffu, xf, o);
         const double yb = __shfl_up_sync(0xffffffffu, xb, o);
         if (lane >= o) { xf += yf; xb += yb; }
     }
+    double xfe = __shfl_up_sync(0xffffffffu, xf, 1), xbe = __shfl_up_sync(0xffffffffu, xb, 1);
+    if (lane == 0) { xfe = 0.0; xbe = 0.0; }
     if (lane == 31) { wt_f[warp] = xf; wt_b[warp] = xb; }
     __syncthreads();
     if (warp == 0) {
@@ -130,21 +139,24 @@ __device__ double totals_scan(const double *in, int n, double *pre, double *suf)
             const double yb = __shfl_up_sync(0xffffffffu, sb, o);
             if (lane >= o) { sf += yf; sb += yb; }
         }
-        wt_f[lane] = sf;
-        wt_b[lane] = sb;
+        double sfe = __shfl_up_sync(0xffffffffu, sf, 1), sbe = __shfl_up_sync(0xffffffffu, sb, 1);
+        if (lane == 0) { sfe = 0.0; sbe = 0.0; }
+        wt_f[32 + lane] = sfe;                  // exclusive prefix of the warp totals
+        wt_b[32 + lane] = sbe;
+        if (lane == 31) { wt_f[64] = sf; wt_b[64] = sb; }
     }
     __syncthreads();
-    const double exf = (xf - tf) + (warp > 0 ? wt_f[warp - 1] : 0.0);
-    const double exb = (xb - tb) + (warp > 0 ? wt_b[warp - 1] : 0.0);
+    const double exf = xfe + wt_f[32 + warp];
+    const double exb = xbe + wt_b[32 + warp];
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
         const int e = e0 + i;
         if (e < n) {
-            if (pre) pre[e] = exf + (f[i] - f0[i]);              // exclusive prefix
-            if (suf) suf[n - 1 - e] = exb + (bk[i] - b0[i]);     // exclusive suffix
+            if (pre) pre[e] = exf + fe[i];                       // exclusive prefix
+            if (suf) suf[n - 1 - e] = exb + be[i];               // exclusive suffix
         }
     }
-    return wt_f[31];
+    return wt_f[64];
 }
 
 __device__ __forceinline__ double *tile_row(const VecPtrs &b, int M, int which, int m) {
@@ -297,7 +309,10 @@ __device__ double small_scan(double (&v)[kSEl], double *wt) {
             const double y = __shfl_up_sync(0xffffffffu, z, o);
             if (lane >= o) z += y;
         }
-        wt[32 + lane] = z - a;            // exclusive prefix of the warp totals
+        double ze = __shfl_up_sync(0xffffffffu, z, 1);   // exclusive prefix, not z - a (see tile_scan)
+        if (lane == 0) ze = 0.0;
+        (void)a;
+        wt[32 + lane] = ze;
         if (lane == 31) wt[64] = z;       // block total
     }
     __syncthreads();

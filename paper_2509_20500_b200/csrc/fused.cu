@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -34,35 +35,6 @@ struct FusedShared {
     double exB[kFMaxC];           // sum partials
     double red[kFT / 32];
 };
-
-__device__ __forceinline__ uint32_t fsmem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void fmbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(fsmem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fmbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fsmem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void fmbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(fsmem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
-// 1-D TMA bulk copy global -> shared (bytes % 16 == 0), completion counted on the mbarrier
-__device__ __forceinline__ void fbulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(fsmem_u32(dst)), "l"(src), "r"(bytes), "r"(fsmem_u32(bar))
-                 : "memory");
-}
 
 __device__ __forceinline__ double fwarp_sum(double x) {
 #pragma unroll
@@ -116,12 +88,13 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
         __shared__ uint64_t bar;
         const uint32_t row_bytes = (uint32_t)(((size_t)N * sizeof(T) + 15) & ~(size_t)15);   // <= ld bytes
         if (threadIdx.x == 0) {
-            fmbar_init(&bar, 1);
-            fmbar_expect_tx(&bar, row_bytes * (uint32_t)nrow);
-            for (int r = 0; r < nrow; ++r) fbulk_g2s(slice + (size_t)r * NP, P + (size_t)(r0 + r) * a.ld, row_bytes, &bar);
+            mbar_init(&bar, 1);
+            fence_mbar_init();
+            mbar_expect_tx(&bar, row_bytes * (uint32_t)nrow);
+            for (int r = 0; r < nrow; ++r) bulk_g2s(slice + (size_t)r * NP, P + (size_t)(r0 + r) * a.ld, row_bytes, &bar);
         }
         __syncthreads();
-        fmbar_wait(&bar, 0);
+        mbar_wait(&bar, 0);
     }
     const double u = 1.0 / (double)N;
     for (int i = threadIdx.x; i < R; i += kFT) {

@@ -20,6 +20,7 @@
 // k_power_check: s, the normalised L1 change, the state, the next gathered x, the active-matrix
 // list, and (last CTA) the WHILE condition.
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace spl {
 namespace {
@@ -31,39 +32,6 @@ constexpr int kThreads = 256;           // 2 columns per thread across a 512-col
 template <typename T> struct GemvCfg;
 template <> struct GemvCfg<double> { static constexpr int RS = 8, SROW = kStripCols + 4; };   // 8 x 4 KB
 template <> struct GemvCfg<float> { static constexpr int RS = 16, SROW = kStripCols + 8; };   // 16 x 2 KB
-
-// ------------------------------------------------------------------ PTX helpers (sm_90+ / sm_100a)
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
-// 1-D TMA bulk copy global -> shared, completion counted on the mbarrier (bytes % 16 == 0).
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll

@@ -281,3 +281,30 @@ def test_bin_trajectory_vs_oracle(spl, f, td):
     assert np.max(np.abs(_np(fin) - want_v)) <= 1e-13
     tr0, fin0 = spl.bin_trajectory(f, td, torch.tensor(start, device="cuda"), bin_, 0)
     assert _np(tr0)[0] == start[bin_] and np.array_equal(_np(fin0), start)
+
+
+# ------------------------------------------------------------- extreme flux (Lambda near the 600 guard)
+@pytest.mark.parametrize("S,B,N", [(450.0, 120.0, 512), (0.0, 590.0, 300), (30.0, 1e-6, 1024)],
+                         ids=["Lambda570", "const590", "tinyB"])
+def test_extreme_flux_all_paths(spl, S, B, N):
+    """Lambda = 570 / 590 (e^{-Lambda} ~ 1e-250: the factored entries span ~250 decades) and a vanishing
+    floor B = 1e-6: the dense fused path, the dense graph path and the structured path all match the
+    oracle's Eq. 4 pi."""
+    f = Flux(100.0, N, (42.0,), (0.7,), (S,), B)
+    td = 63.3
+    want = oracle.stationary_dense(oracle.build_eq4(f, td))
+    P0 = spl.build_base(f)
+    got_e = _np(P0)
+    assert np.max(np.abs(got_e - oracle.build_eq4(f, 0.0))) <= 1e-12
+    pi_d, info = spl.stationary(P0, f.t_r, td, max_iter=10 ** 6)
+    assert np.sum(np.abs(_np(pi_d) - want)) <= TOL_PI64
+    pi_s, _ = _one(spl, f, td, max_iter=10 ** 6)
+    assert np.sum(np.abs(_np(pi_s) - want)) <= TOL_PI64
+
+
+def test_extreme_flux_rejected_beyond_guard(spl):
+    f = Flux(100.0, 256, (42.0,), (0.7,), (500.0,), 101.0)      # Lambda = 601 > 600 (reading R15)
+    with pytest.raises(spl.SplidarError):
+        spl.build_base(f)
+    with pytest.raises(spl.SplidarError):
+        _one(spl, f, 10.0)
