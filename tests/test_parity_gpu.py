@@ -358,3 +358,28 @@ def test_fused_equals_general_path(spl, case, monkeypatch):
             assert np.sum(np.abs(_np(fused.pi[0, v]) - _np(general.pi[0, v]))) <= 1e-13
         fused.close()
         general.close()
+
+
+def test_ragged_large_n(spl):
+    """N = 9001 (> 8192: the tiled flux-vector scans; a ragged last 512-column strip for the build and
+    the graph-path GEMV; a 3-CTA cluster with a ragged last CTA for the structured solve): sampled rows
+    of J_l P~0 vs the oracle's Eq. 4 rows, and pi from both solvers vs the long-double cross-check."""
+    f = random_flux(np.random.default_rng(9001), 9001, 2)
+    td = 157.25
+    N = f.n_bins
+    lam, F, Lam = oracle_vectors(f)
+    v = spl.flux_vectors(f)
+    assert np.max(np.abs(_np(v["F"]) - F)) <= 1e-13 * max(1.0, Lam)
+    P0 = spl.build_base(f)
+    l = oracle.shift_l(f, td)
+    rows = [0, 1, 511, 512, 8999, 9000, l, (N - l) % N, 4500]
+    want = sampled_rows(f, td, rows)
+    got = np.stack([_np(P0[(r + l) % N]) for r in rows])
+    assert np.max(np.abs(got - want)) <= TOL_E64
+    pi, info = spl.stationary(P0, f.t_r, td)
+    assert info["converged"]
+    ref, _ = structured_pi(f, td, vectors=(lam, F, Lam))
+    assert np.sum(np.abs(_np(pi) - ref)) <= TOL_PI64
+    shape, S, B = spl.flux_items(f)
+    pis, _ = spl.stationary_structured(shape, S, B, [td])
+    assert np.sum(np.abs(_np(pis[0]) - ref)) <= TOL_PI64
