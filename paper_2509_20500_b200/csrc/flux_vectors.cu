@@ -302,7 +302,7 @@ __device__ double small_scan(double (&v)[kSEl], double *wt) {
     if (lane == 31) wt[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        const double a = wt[lane];
+        const double a = lane < (int)(blockDim.x >> 5) ? wt[lane] : 0.0;   // blockDim may be < 1024
         double z = a;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -327,7 +327,8 @@ __device__ double small_scan(double (&v)[kSEl], double *wt) {
 __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ fluxes, int N, VecPtrs b,
                                                    int64_t vstride) {
     __shared__ double wt[65];
-    extern __shared__ double rev[];      // [kST * kSEl]: w reversed, then its inclusive scan
+    extern __shared__ double rev[];      // [blockDim * 8]: w reversed, then its inclusive scan
+    const int nslot = (int)blockDim.x * kSEl;
     const int m = blockIdx.x;
     const FluxDev &f = fluxes[m];
     const int e0 = threadIdx.x * kSEl;
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
         } else {
             wv[i] = 0.0;
         }
-        rev[kST * kSEl - 1 - e] = wv[i];
+        rev[nslot - 1 - e] = wv[i];
     }
     double pf[kSEl];
 #pragma unroll
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
         const int r = e0 + i;
         if (r < N) {
             const double L = pf[i] - wv[i];                   // sum_{j < r} w_j (exclusive prefix)
-            const double U = rev[kST * kSEl - 1 - r];         // sum_{j >= r} w_j (inclusive suffix)
+            const double U = rev[nslot - 1 - r];              // sum_{j >= r} w_j (inclusive suffix)
             const double D = U + eL * L;
             bad |= !(D > 0.0 && isfinite(D));
             const double id = 1.0 / D;
@@ -406,14 +407,17 @@ cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs bas
     const int ntN = (N + kScanTile - 1) / kScanTile;   // tiles over the N bins
     if (nt > 4096) return cudaErrorInvalidValue;
     if (N + 1 <= kST * kSEl) {                         // one CTA per profile, one launch
-        const int smem = (int)(sizeof(double) * kST * kSEl);
+        int threads = (N + 1 + kSEl - 1) / kSEl;     // just enough threads for the N + 1 slots
+        threads = (threads + 31) / 32 * 32;
+        const int smem = (int)(sizeof(double) * threads * kSEl);
         static bool attr = false;           // once per process (not inside every captured launch)
         if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute((const void *)k_vec_small, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaError_t e = cudaFuncSetAttribute((const void *)k_vec_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)(sizeof(double) * kST * kSEl));
             if (e != cudaSuccess) return e;
             attr = true;
         }
-        k_vec_small<<<M, kST, smem, s>>>(d_flux, N, base, vstride);
+        k_vec_small<<<M, threads, smem, s>>>(d_flux, N, base, vstride);
         return cudaGetLastError();
     }
     k_vec_a<<<dim3(nt, M), kT, 0, s>>>(d_flux, N, M, base, vstride);

@@ -9,14 +9,21 @@
 //   C_j = sum_{r <= j} z_r (inclusive prefix), T = sum_r z_r.
 // One product is one prefix scan: O(N) instead of the N^2 b bytes of the dense GEMV.
 //
-// Layout: one thread-block cluster of C CTAs per item (C = ceil(N / 4096), <= 16). CTA c owns the
-// positions [c chunk, (c + 1) chunk), chunk = 8 x blockDim; a thread owns 8 consecutive positions (its
-// w, 1/D and iterate in registers). The gathered iterate lives in shared memory (xbuf); each product's
-// result is pushed straight into the owner CTA's xbuf at (j + l) mod N over DSMEM, so the permutation
-// costs one DSMEM store per element and no extra pass. Per product: block scan -> publish the CTA
-// totals to every CTA (DSMEM) -> barrier.cluster -> outputs + push + publish the next sums ->
-// barrier.cluster. Every CTA adds the published values in the same fixed order, so all CTAs take the
-// same control-flow decisions and the result does not depend on timing (deterministic).
+// Teams: the threads that own one item's N positions, E consecutive positions per thread:
+//   kWarp     one warp, E = 8 (N <= 256): shuffles only, __syncwarp orders the pushes
+//   kBlock    one CTA, E = 8 (N <= 4096): block scan / sums through shared memory, __syncthreads
+//   kCluster  a thread-block cluster of C CTAs x 512 threads, E = 8 (C = ceil(N / 4096)) for the solve
+//             and lambda_2, E = 16 (C = ceil(N / 8192)) for mixing and trajectories; CTA totals
+//             exchanged over DSMEM, barrier.cluster between phases. (E = 16 solves fit c5's 17 items in
+//             one wave of 4-CTA clusters but measured slower: 460 vs 361 us; per-CTA work dominates.)
+// w and 1/D of a thread's positions stay in registers (solve) or are staged once in shared memory;
+// the gathered iterate lives in
+// shared memory (xbuf) and each product's result is pushed straight into the owner's xbuf at
+// (j + l) mod N (DSMEM across CTAs), so the permutation costs one store per element and no extra pass.
+// Per product: scan -> publish the CTA totals -> barrier -> outputs + push + publish the next sums ->
+// barrier. Every CTA adds the published values in the same fixed order, so all CTAs take the same
+// control-flow decisions and the result does not depend on timing (deterministic). Exclusive prefixes
+// are formed by shuffles, never by subtraction.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -26,21 +33,17 @@ namespace cg = cooperative_groups;
 namespace spl {
 namespace {
 
-constexpr int kSE = 8;                        // positions per thread
 constexpr int kSMaxT = 512;                   // threads per CTA
 constexpr int kSMaxWarps = kSMaxT / 32;
 constexpr int kSMaxC = 16;                    // cluster size (> 8 is non-portable)
 constexpr int kSExK = 8;                      // values published per CTA per exchange
-constexpr int kSChunk = kSMaxT * kSE;         // positions per CTA of a multi-CTA cluster
+constexpr int kSChunkB = kSMaxT * 8;          // positions per CTA at E = 8 (one-CTA limit)
 
-// Teams: the threads that own one item's N positions.
-//   kWarp     one warp (N <= 256): shuffles only, __syncwarp orders the pushes
-//   kBlock    one CTA (N <= 4096): block scan / sums through shared memory, __syncthreads
-//   kCluster  C CTAs (N > 4096): as kBlock inside each CTA, CTA totals exchanged over DSMEM and
-//             barrier.cluster
 enum { kWarp = 0, kBlock = 1, kCluster = 2 };
 
-__device__ __forceinline__ int sidx(int p) { return p + (p >> 3); }   // padded xbuf index
+// padded shared-memory index of a position (E consecutive per thread: <= 2-way bank conflicts)
+template <int E>
+__device__ __forceinline__ int sidx(int p) { return p + p / E; }
 
 struct SShared {
     double exA[kSExK * kSMaxC];
@@ -95,17 +98,17 @@ struct Team {
             __syncthreads();
         }
     }
-    // inclusive scan over the team-local positions of V vectors (8 consecutive per thread);
+    // inclusive scan over the team-local positions of V vectors (E consecutive per thread);
     // tot[a] = team-local total
-    template <int V>
-    __device__ __forceinline__ void scan(double (&v)[V][kSE], double (&tot)[V]) {
+    template <int V, int E>
+    __device__ __forceinline__ void scan(double (&v)[V][E], double (&tot)[V]) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         double x[V], ex[V];
 #pragma unroll
         for (int a = 0; a < V; ++a) {
 #pragma unroll
-            for (int i = 1; i < kSE; ++i) v[a][i] += v[a][i - 1];
-            x[a] = v[a][kSE - 1];
+            for (int i = 1; i < E; ++i) v[a][i] += v[a][i - 1];
+            x[a] = v[a][E - 1];
         }
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1)
@@ -124,7 +127,7 @@ struct Team {
             for (int a = 0; a < V; ++a) {
                 tot[a] = __shfl_sync(0xffffffffu, x[a], 31);
 #pragma unroll
-                for (int i = 0; i < kSE; ++i) v[a][i] += ex[a];
+                for (int i = 0; i < E; ++i) v[a][i] += ex[a];
             }
         } else {
             const int nw = blockDim.x >> 5;
@@ -143,7 +146,7 @@ struct Team {
                 tot[a] = tt;
                 const double e = wex + ex[a];
 #pragma unroll
-                for (int i = 0; i < kSE; ++i) v[a][i] += e;
+                for (int i = 0; i < E; ++i) v[a][i] += e;
             }
             __syncthreads();
         }
@@ -179,47 +182,44 @@ struct Team {
             before = 0.0;
         }
     }
-    __device__ __forceinline__ double *xdst(double *xbuf, int dst) {
-        if constexpr (MODE == kCluster) return cl.map_shared_rank(xbuf, dst);
-        else return xbuf;
-    }
 };
 
+// Positions of this thread: p0 .. p0 + E - 1 (global), local index tid * E + e in its CTA's chunk.
+template <int MODE, int E>
 struct Pos {
-    int N, p0, l;   // p0: first global position of this thread
+    int N, p0, l;
+    __device__ Pos(int N_, int c, int l_) : N(N_), l(l_) {
+        p0 = (MODE == kCluster ? c * (int)blockDim.x * E : 0) + (int)threadIdx.x * E;
+    }
     __device__ bool valid(int e) const { return p0 + e < N; }
+    __device__ int loc(int e) const { return sidx<E>((int)threadIdx.x * E + e); }
 };
-
-template <int MODE>
-__device__ __forceinline__ Pos make_pos(const StructArgs &a, int c, int l) {
-    Pos p;
-    p.N = a.N;
-    p.p0 = (MODE == kCluster ? c * kSChunk : 0) + threadIdx.x * kSE;
-    p.l = l;
-    return p;
-}
 
 // Push y (natural positions p0 + e) into the gathered xbuf of the owner of (p + l) mod N.
-template <int MODE>
-__device__ __forceinline__ void push(Team<MODE> &tm, double *xbuf, const Pos &P, const double (&y)[kSE]) {
+template <int MODE, int E>
+__device__ __forceinline__ void push(Team<MODE> &tm, double *xbuf, const Pos<MODE, E> &P, const double (&y)[E]) {
+    const int chunk = (int)blockDim.x * E;
 #pragma unroll
-    for (int e = 0; e < kSE; ++e) {
+    for (int e = 0; e < E; ++e) {
         const int p = P.p0 + e;
         if (p < P.N) {
             int r = p + P.l;
             if (r >= P.N) r -= P.N;
             if constexpr (MODE == kCluster) {
-                tm.xdst(xbuf, r / kSChunk)[sidx(r % kSChunk)] = y[e];
+                const int dst = r / chunk;
+                tm.cl.map_shared_rank(xbuf, dst)[sidx<E>(r - dst * chunk)] = y[e];
             } else {
-                xbuf[sidx(r)] = y[e];
+                xbuf[sidx<E>(r)] = y[e];
             }
         }
     }
 }
 
-__device__ __forceinline__ void load8(const double *src, const Pos &P, double (&o)[kSE]) {
+// stage the thread's E values of src (global) in shared memory at its padded local indices
+template <int MODE, int E>
+__device__ __forceinline__ void stage(double *dst, const double *src, const Pos<MODE, E> &P) {
 #pragma unroll
-    for (int e = 0; e < kSE; ++e) o[e] = P.valid(e) ? __ldg(src + P.p0 + e) : 0.0;
+    for (int e = 0; e < E; ++e) dst[P.loc(e)] = P.valid(e) ? __ldg(src + P.p0 + e) : 0.0;
 }
 
 template <int MODE>
@@ -228,38 +228,54 @@ __device__ __forceinline__ int item_index(int C) {
     else return blockIdx.x;
 }
 
+template <int E>
+__device__ __forceinline__ int xsize(int threads) { const int ch = threads * E; return ch + ch / E; }
+
 // ---------------------------------------------------------------------------------------------
 // f2: stationary solve. pi^0 = 1/N; v^{k+1} = v^k P~ (unnormalised; P~ is stochastic so the scale
 // stays ~1); pi^k = v^k / ||v^k||_1; stop after the first k with ||pi^{k+1} - pi^k||_1 < tol (the change
 // of product k is published with the scan totals of product k + 1, one exchange fewer per product).
-template <int MODE>
+// Shared memory: xbuf | w | 1/D (each xsize).
+template <int MODE, int E>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) {
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
     Team<MODE> tm(sh, a.C);
     const int item = item_index<MODE>(a.C);
     const int m = a.prof[item], l = a.lsh[item];
-    const Pos P = make_pos<MODE>(a, tm.c, l);
-    const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
+    const Pos<MODE, E> P(a.N, tm.c, l);
+    // w and 1/D: registers at E = 8 (measured faster), shared memory at E = 16
+    constexpr bool REG = E == 8;
+    const int xs = xsize<E>(blockDim.x);
+    double *ws = xbuf + xs, *ids = xbuf + 2 * xs;
+    double wr[REG ? E : 1], idr[REG ? E : 1];
+    if constexpr (REG) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            wr[e] = P.valid(e) ? __ldg(a.w + (size_t)m * a.vstride + P.p0 + e) : 0.0;
+            idr[e] = P.valid(e) ? __ldg(a.invD + (size_t)m * a.vstride + P.p0 + e) : 0.0;
+        }
+    } else {
+        stage(ws, a.w + (size_t)m * a.vstride, P);
+        stage(ids, a.invD + (size_t)m * a.vstride, P);
+    }
     const double eL = a.scal[m * 8 + 1];
-    double wr[kSE], idr[kSE], yp[kSE];
-    load8(w, P, wr);
-    load8(invD, P, idr);
+    double yp[E];
     const double u = 1.0 / (double)P.N;
 #pragma unroll
-    for (int e = 0; e < kSE; ++e) {
+    for (int e = 0; e < E; ++e) {
         yp[e] = P.valid(e) ? u : 0.0;
-        xbuf[sidx(threadIdx.x * kSE + e)] = yp[e];   // the gathered uniform vector is uniform
+        xbuf[P.loc(e)] = yp[e];                        // the gathered uniform vector is uniform
     }
     double s_prev = 1.0, dpart = 0.0, change = __longlong_as_double(0x7ff0000000000000ll);
     int k = 0, conv = 0;
     tm.barrier();
     for (;;) {
         // phase 1: z = x / D, scan; publish (scan total, change partial of product k - 1)
-        double v[1][kSE], tot[1];
+        double v[1][E], tot[1];
 #pragma unroll
-        for (int e = 0; e < kSE; ++e) v[0][e] = xbuf[sidx(threadIdx.x * kSE + e)] * idr[e];
-        tm.template scan<1>(v, tot);
+        for (int e = 0; e < E; ++e) v[0][e] = xbuf[P.loc(e)] * (REG ? idr[REG ? e : 0] : ids[P.loc(e)]);
+        tm.template scan<1, E>(v, tot);
         {
             const double pv[2] = {tot[0], dpart};
             tm.template exchange<2>(tm.exA, pv);
@@ -271,16 +287,16 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
             if (change < a.tol) { conv = 1; break; }
             if (k >= a.max_iter || !(s_prev > 0.0) || !isfinite(change)) break;
         }
-        // phase 2: y = w (C + e^{-Lambda} (T - C)) at the natural positions; push; publish sum(y)
-        double y[kSE];
+        // phase 2: y = w (C + e^{-Lambda} (T - C)) at the natural positions (in place of the scan);
+        // push; publish sum(y)
         double ps[1] = {0.0};
 #pragma unroll
-        for (int e = 0; e < kSE; ++e) {
+        for (int e = 0; e < E; ++e) {
             const double Cj = off + v[0][e];
-            y[e] = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
-            ps[0] += y[e];
+            v[0][e] = P.valid(e) ? (REG ? wr[REG ? e : 0] : ws[P.loc(e)]) * (Cj + eL * (T - Cj)) : 0.0;
+            ps[0] += v[0][e];
         }
-        push<MODE>(tm, xbuf, P, y);
+        push<MODE, E>(tm, xbuf, P, v[0]);
         tm.template sum<1>(ps);
         tm.template exchange<1>(tm.exB, ps);
         double s, d2;
@@ -288,9 +304,9 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
         double d[1] = {0.0};
         const double is = 1.0 / s, ip = 1.0 / s_prev;
 #pragma unroll
-        for (int e = 0; e < kSE; ++e) {
-            d[0] += fabs(y[e] * is - yp[e] * ip);
-            yp[e] = y[e];
+        for (int e = 0; e < E; ++e) {
+            d[0] += fabs(v[0][e] * is - yp[e] * ip);
+            yp[e] = v[0][e];
         }
         tm.template sum<1>(d);
         dpart = d[0];
@@ -300,7 +316,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
     double *out = a.pi + (size_t)item * P.N;
     const double is = 1.0 / s_prev;
 #pragma unroll
-    for (int e = 0; e < kSE; ++e)
+    for (int e = 0; e < E; ++e)
         if (P.valid(e)) out[P.p0 + e] = yp[e] * is;
     if (tm.c == 0 && threadIdx.x == 0) {
         SolveState st;
@@ -323,6 +339,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
 // pair lambda2, conj(lambda2) spans a real 2-D invariant subspace, so real arithmetic suffices. Basis
 // update: q1 = w1 / |w1|, q2 = (w2 - (w1.w2 / w1.w1) w1) / |w2| (applied as coefficients to the pushed
 // w, so the product needs two team exchanges). Stop when the dominant Ritz value moves < tol.
+// Shared memory: xbuf0 | xbuf1 | w | 1/D | pi.
 
 __device__ __forceinline__ double hash_unit(uint32_t j, uint32_t salt) {   // deterministic in [-1, 1)
     uint32_t x = j * 0x9E3779B1u + salt * 0x85EBCA77u + 0x165667B1u;
@@ -330,23 +347,23 @@ __device__ __forceinline__ double hash_unit(uint32_t j, uint32_t salt) {   // de
     return (double)x * (2.0 / 4294967296.0) - 1.0;
 }
 
-template <int MODE>
+template <int MODE, int E>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a) {
-    extern __shared__ double xbuf[];    // [2][xs]: gathered w1, w2
+    extern __shared__ double xbuf[];
     __shared__ SShared sh;
     Team<MODE> tm(sh, a.C);
     const int item = item_index<MODE>(a.C);
     const int m = a.prof[item], l = a.lsh[item];
-    const Pos P = make_pos<MODE>(a, tm.c, l);
-    const int chunk = MODE == kCluster ? kSChunk : (int)blockDim.x * kSE;
-    const int xs = chunk + chunk / 8;
-    double *xb0 = xbuf, *xb1 = xbuf + xs;
-    const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
-    const double *pi = a.pi + (size_t)item * P.N;
+    const Pos<MODE, E> P(a.N, tm.c, l);
+    const int xs = xsize<E>(blockDim.x);
+    double *xb0 = xbuf, *xb1 = xbuf + xs, *ws = xbuf + 2 * xs, *ids = xbuf + 3 * xs, *pis = xbuf + 4 * xs;
+    stage(ws, a.w + (size_t)m * a.vstride, P);
+    stage(ids, a.invD + (size_t)m * a.vstride, P);
+    stage(pis, a.pi + (size_t)item * P.N, P);
     const double eL = a.scal[m * 8 + 1];
-    double wn[2][kSE];   // last W at the natural positions (q = combination of these)
+    double wn[2][E];   // last W at the natural positions (q = combination of these)
 #pragma unroll
-    for (int e = 0; e < kSE; ++e) {
+    for (int e = 0; e < E; ++e) {
         const int p = P.p0 + e;
         wn[0][e] = P.valid(e) ? hash_unit((uint32_t)p, 1u) : 0.0;
         wn[1][e] = P.valid(e) ? hash_unit((uint32_t)p, 2u) : 0.0;
@@ -357,8 +374,8 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
             g0 = hash_unit((uint32_t)src, 1u);
             g1 = hash_unit((uint32_t)src, 2u);
         }
-        xb0[sidx(threadIdx.x * kSE + e)] = g0;
-        xb1[sidx(threadIdx.x * kSE + e)] = g1;
+        xb0[P.loc(e)] = g0;
+        xb1[P.loc(e)] = g1;
     }
     double al = 1.0, be = 1.0, ga = 0.0;           // q1 = al w1, q2 = be (w2 - ga w1)
     double mu_re = 0.0, mu_im = 0.0, dmu = __longlong_as_double(0x7ff0000000000000ll);
@@ -366,24 +383,23 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
     tm.barrier();
     for (;;) {
         // phase 1: current basis (gathered and natural), z = x / D, scans; sums and Gram Q Q^T
-        double v[2][kSE], tot[2];
-        double q[2][kSE];
+        double v[2][E], tot[2];
         double pp[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // sum q1, sum q2, q1.q1, q1.q2, q2.q2
 #pragma unroll
-        for (int e = 0; e < kSE; ++e) {
-            const double idr = P.valid(e) ? __ldg(invD + P.p0 + e) : 0.0;
-            const double g0 = xb0[sidx(threadIdx.x * kSE + e)], g1 = xb1[sidx(threadIdx.x * kSE + e)];
+        for (int e = 0; e < E; ++e) {
+            const double idr = ids[P.loc(e)];
+            const double g0 = xb0[P.loc(e)], g1 = xb1[P.loc(e)];
             v[0][e] = al * g0 * idr;
             v[1][e] = be * (g1 - ga * g0) * idr;
-            q[0][e] = al * wn[0][e];
-            q[1][e] = be * (wn[1][e] - ga * wn[0][e]);
-            pp[0] += q[0][e];
-            pp[1] += q[1][e];
-            pp[2] += q[0][e] * q[0][e];
-            pp[3] += q[0][e] * q[1][e];
-            pp[4] += q[1][e] * q[1][e];
+            wn[1][e] = be * (wn[1][e] - ga * wn[0][e]);   // q2 (natural)
+            wn[0][e] = al * wn[0][e];                      // q1
+            pp[0] += wn[0][e];
+            pp[1] += wn[1][e];
+            pp[2] += wn[0][e] * wn[0][e];
+            pp[3] += wn[0][e] * wn[1][e];
+            pp[4] += wn[1][e] * wn[1][e];
         }
-        tm.template scan<2>(v, tot);
+        tm.template scan<2, E>(v, tot);
         tm.template sum<5>(pp);
         {
             const double pv[7] = {tot[0], tot[1], pp[0], pp[1], pp[2], pp[3], pp[4]};
@@ -397,29 +413,29 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
         tm.total(tm.exA, 4, pp[2], G11, dm);
         tm.total(tm.exA, 5, pp[3], G12, dm);
         tm.total(tm.exA, 6, pp[4], G22, dm);
-        // phase 2: W = Q P~ - (Q 1) pi; dots; push W
+        // phase 2: W = Q P~ - (Q 1) pi; dots with Q (held in wn) and W; push W (into v)
         double hp[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // h11 h12 h21 h22 g11 g12 g22
 #pragma unroll
-        for (int e = 0; e < kSE; ++e) {
+        for (int e = 0; e < E; ++e) {
             double y0 = 0.0, y1 = 0.0;
             if (P.valid(e)) {
-                const double wj = __ldg(w + P.p0 + e), pj = __ldg(pi + P.p0 + e);
+                const double wj = ws[P.loc(e)], pj = pis[P.loc(e)];
                 const double C0 = off[0] + v[0][e], C1 = off[1] + v[1][e];
                 y0 = wj * (C0 + eL * (T[0] - C0)) - sig[0] * pj;
                 y1 = wj * (C1 + eL * (T[1] - C1)) - sig[1] * pj;
             }
-            wn[0][e] = y0;
-            wn[1][e] = y1;
-            hp[0] += y0 * q[0][e];
-            hp[1] += y0 * q[1][e];
-            hp[2] += y1 * q[0][e];
-            hp[3] += y1 * q[1][e];
+            hp[0] += y0 * wn[0][e];
+            hp[1] += y0 * wn[1][e];
+            hp[2] += y1 * wn[0][e];
+            hp[3] += y1 * wn[1][e];
             hp[4] += y0 * y0;
             hp[5] += y0 * y1;
             hp[6] += y1 * y1;
+            wn[0][e] = y0;
+            wn[1][e] = y1;
         }
-        push<MODE>(tm, xb0, P, wn[0]);
-        push<MODE>(tm, xb1, P, wn[1]);
+        push<MODE, E>(tm, xb0, P, wn[0]);
+        push<MODE, E>(tm, xb1, P, wn[1]);
         tm.template sum<7>(hp);
         tm.template exchange<7>(tm.exB, hp);
         double h[7];
@@ -477,42 +493,43 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
 // 1/2 || e_i P~^n - pi ||_1 <= eps (no renormalisation: P~ is stochastic). TV to stationarity is
 // non-increasing in n for every start, so the smallest n with max_i TV_i(n) <= eps is max_i n_i.
 // Item = one start bin; n_i written to a.nsteps[i] (-1: max_iter steps not enough).
-template <int MODE>
+// Shared memory: xbuf | w | 1/D | pi.
+template <int MODE, int E>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a) {
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
     Team<MODE> tm(sh, a.C);
     const int start = a.start_bin0 + item_index<MODE>(a.C);
     const int m = a.prof[0], l = a.lsh[0];
-    const Pos P = make_pos<MODE>(a, tm.c, l);
-    const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
+    const Pos<MODE, E> P(a.N, tm.c, l);
+    const int xs = xsize<E>(blockDim.x);
+    double *ws = xbuf + xs, *ids = xbuf + 2 * xs, *pis = xbuf + 3 * xs;
+    stage(ws, a.w + (size_t)m * a.vstride, P);
+    stage(ids, a.invD + (size_t)m * a.vstride, P);
+    stage(pis, a.pi, P);
     const double eL = a.scal[m * 8 + 1];
-    double wr[kSE], idr[kSE], pr[kSE];
-    load8(w, P, wr);
-    load8(invD, P, idr);
-    load8(a.pi, P, pr);
     int r0 = start + l;
     if (r0 >= P.N) r0 -= P.N;
 #pragma unroll
-    for (int e = 0; e < kSE; ++e) xbuf[sidx(threadIdx.x * kSE + e)] = (P.p0 + e == r0) ? 1.0 : 0.0;
+    for (int e = 0; e < E; ++e) xbuf[P.loc(e)] = (P.p0 + e == r0) ? 1.0 : 0.0;
     int n = 0, hit = -1;
     tm.barrier();
     for (;;) {
-        double v[1][kSE], tot[1];
+        double v[1][E], tot[1];
 #pragma unroll
-        for (int e = 0; e < kSE; ++e) v[0][e] = xbuf[sidx(threadIdx.x * kSE + e)] * idr[e];
-        tm.template scan<1>(v, tot);
+        for (int e = 0; e < E; ++e) v[0][e] = xbuf[P.loc(e)] * ids[P.loc(e)];
+        tm.template scan<1, E>(v, tot);
         tm.template exchange<1>(tm.exA, tot);
         double T, off, dm;
         tm.total(tm.exA, 0, tot[0], T, off);
-        double y[kSE], tv[1] = {0.0};
+        double tv[1] = {0.0};
 #pragma unroll
-        for (int e = 0; e < kSE; ++e) {
+        for (int e = 0; e < E; ++e) {
             const double Cj = off + v[0][e];
-            y[e] = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
-            tv[0] += fabs(y[e] - pr[e]);
+            v[0][e] = P.valid(e) ? ws[P.loc(e)] * (Cj + eL * (T - Cj)) : 0.0;
+            tv[0] += fabs(v[0][e] - pis[P.loc(e)]);
         }
-        push<MODE>(tm, xbuf, P, y);
+        push<MODE, E>(tm, xbuf, P, v[0]);
         tm.template sum<1>(tv);
         tm.template exchange<1>(tm.exB, tv);
         double TV;
@@ -529,21 +546,21 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a)
 
 // ---------------------------------------------------------------------------------------------
 // f1: bin trajectory (§4.2): (start P~^n)[bin] for n = 0..steps (no renormalisation),
-// and the final vector start P~^steps.
-template <int MODE>
+// and the final vector start P~^steps. Shared memory: xbuf | w | 1/D.
+template <int MODE, int E>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_traj(const StructArgs a) {
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
     Team<MODE> tm(sh, a.C);
     const int m = a.prof[0], l = a.lsh[0];
-    const Pos P = make_pos<MODE>(a, tm.c, l);
-    const double *w = a.w + (size_t)m * a.vstride, *invD = a.invD + (size_t)m * a.vstride;
+    const Pos<MODE, E> P(a.N, tm.c, l);
+    const int xs = xsize<E>(blockDim.x);
+    double *ws = xbuf + xs, *ids = xbuf + 2 * xs;
+    stage(ws, a.w + (size_t)m * a.vstride, P);
+    stage(ids, a.invD + (size_t)m * a.vstride, P);
     const double eL = a.scal[m * 8 + 1];
-    double wr[kSE], idr[kSE];
-    load8(w, P, wr);
-    load8(invD, P, idr);
 #pragma unroll
-    for (int e = 0; e < kSE; ++e) {
+    for (int e = 0; e < E; ++e) {
         const int r = P.p0 + e;
         double g = 0.0;
         if (r < P.N) {
@@ -551,41 +568,58 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_traj(const StructArgs a) {
             if (src < 0) src += P.N;
             g = a.start[src];
         }
-        xbuf[sidx(threadIdx.x * kSE + e)] = g;
+        xbuf[P.loc(e)] = g;
     }
     if (tm.c == 0 && threadIdx.x == 0) a.traj[0] = a.start[a.bin];
     tm.barrier();
-    double y[kSE];
+    double v[1][E];
     for (int n = 1; n <= a.max_iter; ++n) {
-        double v[1][kSE], tot[1];
+        double tot[1];
 #pragma unroll
-        for (int e = 0; e < kSE; ++e) v[0][e] = xbuf[sidx(threadIdx.x * kSE + e)] * idr[e];
-        tm.template scan<1>(v, tot);
+        for (int e = 0; e < E; ++e) v[0][e] = xbuf[P.loc(e)] * ids[P.loc(e)];
+        tm.template scan<1, E>(v, tot);
         tm.template exchange<1>(tm.exA, tot);
         double T, off;
         tm.total(tm.exA, 0, tot[0], T, off);
 #pragma unroll
-        for (int e = 0; e < kSE; ++e) {
+        for (int e = 0; e < E; ++e) {
             const double Cj = off + v[0][e];
-            y[e] = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
-            if (P.p0 + e == a.bin) a.traj[n] = y[e];
+            v[0][e] = P.valid(e) ? ws[P.loc(e)] * (Cj + eL * (T - Cj)) : 0.0;
+            if (P.p0 + e == a.bin) a.traj[n] = v[0][e];
         }
-        if (n < a.max_iter) push<MODE>(tm, xbuf, P, y);
+        if (n < a.max_iter) push<MODE, E>(tm, xbuf, P, v[0]);
         tm.barrier();   // pushes visible; the xbuf reads of this product are done everywhere
     }
     if (a.out) {
 #pragma unroll
-        for (int e = 0; e < kSE; ++e)
-            if (P.valid(e)) a.out[P.p0 + e] = a.max_iter > 0 ? y[e] : a.start[P.p0 + e];
+        for (int e = 0; e < E; ++e)
+            if (P.valid(e)) a.out[P.p0 + e] = a.max_iter > 0 ? v[0][e] : a.start[P.p0 + e];
     }
 }
 
+// Team shape for N positions and E positions per thread: C CTAs of `threads` threads.
+int shape_for(int N, int E, int *C, int *threads) {
+    if (N <= kSChunkB) {                         // one warp or one CTA (E = 8)
+        int t = (N + 7) / 8;
+        t = (t + 31) / 32 * 32;
+        *C = 1;
+        *threads = t < 32 ? 32 : t;
+        return 0;
+    }
+    *threads = kSMaxT;
+    *C = (N + kSMaxT * E - 1) / (kSMaxT * E);
+    return *C <= kSMaxC ? 0 : 1;
+}
+
+// nbuf = shared-memory vectors of xsize doubles the kernel uses
 template <typename K>
-cudaError_t launch_team(K kernel, const StructArgs &a, int n_units, int V, cudaStream_t s) {
-    const int C = a.C;
-    const int nT = a.threads;
-    const int chunk = nT * kSE;
-    const size_t smem = sizeof(double) * (size_t)V * (chunk + chunk / 8);
+cudaError_t launch_team(K kernel, StructArgs a, int n_units, int E, int nbuf, cudaStream_t s) {
+    int C, T;
+    if (shape_for(a.N, E, &C, &T)) return cudaErrorInvalidValue;
+    a.C = C;
+    a.threads = T;
+    const int chunk = T * E;
+    const size_t smem = sizeof(double) * (size_t)nbuf * (chunk + chunk / E);
     cudaError_t e = cudaFuncSetAttribute((const void *)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (C > 8) {
@@ -594,7 +628,7 @@ cudaError_t launch_team(K kernel, const StructArgs &a, int n_units, int V, cudaS
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(n_units * C));
-    cfg.blockDim = dim3((unsigned)nT);
+    cfg.blockDim = dim3((unsigned)T);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -609,31 +643,23 @@ cudaError_t launch_team(K kernel, const StructArgs &a, int n_units, int V, cudaS
 
 }  // namespace
 
-// Team shape for N positions: C CTAs of `threads` threads, 8 positions per thread.
+// Valid N for every structured kernel (the lambda_2 kernel, at 4096 bins per CTA, is the tightest).
 int struct_shape(int N, int *C, int *threads) {
-    if (N <= kSChunk) {
-        int t = (N + kSE - 1) / kSE;
-        t = (t + 31) / 32 * 32;
-        *C = 1;
-        *threads = t < 32 ? 32 : t;
-    } else {
-        *threads = kSMaxT;
-        *C = (N + kSChunk - 1) / kSChunk;
-    }
-    return *C <= kSMaxC ? 0 : 1;
+    if (N < 2) return 1;
+    return shape_for(N, 8, C, threads);
 }
 
-#define SPL_TEAM_LAUNCH(KERNEL, V)                                                              \
-    (a.C > 1 ? launch_team(KERNEL<kCluster>, a, n_units, V, s)                                  \
-             : (a.threads == 32 ? launch_team(KERNEL<kWarp>, a, n_units, V, s)                  \
-                                : launch_team(KERNEL<kBlock>, a, n_units, V, s)))
+#define SPL_TEAM_LAUNCH(KERNEL, EC, NBUF)                                                       \
+    (a.N > kSChunkB ? launch_team(KERNEL<kCluster, EC>, a, n_units, EC, NBUF, s)                \
+                    : (a.N <= 256 ? launch_team(KERNEL<kWarp, 8>, a, n_units, 8, NBUF, s)       \
+                                  : launch_team(KERNEL<kBlock, 8>, a, n_units, 8, NBUF, s)))
 
 cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s) {
     switch (kind) {
-        case kStructSolve: return SPL_TEAM_LAUNCH(k_struct_solve, 1);
-        case kStructLambda2: return SPL_TEAM_LAUNCH(k_struct_lambda2, 2);
-        case kStructMixing: return SPL_TEAM_LAUNCH(k_struct_mixing, 1);
-        case kStructTraj: n_units = 1; return SPL_TEAM_LAUNCH(k_struct_traj, 1);
+        case kStructSolve: return SPL_TEAM_LAUNCH(k_struct_solve, 8, 3);
+        case kStructLambda2: return SPL_TEAM_LAUNCH(k_struct_lambda2, 8, 5);
+        case kStructMixing: return SPL_TEAM_LAUNCH(k_struct_mixing, 16, 4);
+        case kStructTraj: n_units = 1; return SPL_TEAM_LAUNCH(k_struct_traj, 16, 3);
     }
     return cudaErrorInvalidValue;
 }
