@@ -578,6 +578,7 @@ def run_eq4(args, rank, world, dev):
                      "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
                      "traffic": traffic.get("dram_bytes"),
                      "algorithmic_flops_per_entry": flops_per_entry,
+                     "fp64_pipe_pct_ncu": traffic.get("fp64_pipe_pct"),
                      "flops_source": traffic.get("source"),
                      "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (probe: 35.8 TFLOP/s DFMA)"},
         "clocks": clk, "e2e": None, "gpu_launches": len(items) * K, "impl": "ours", "lib": spl.lib_path(),
@@ -658,6 +659,7 @@ def run_mc(args, rank, world, dev):
         "roofline": {"bound": "alu", "kernel": "k_mc", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
                      "traffic": traffic.get("dram_bytes"), "algorithmic_flops_per_registration": fpr,
+                     "fp64_pipe_pct_ncu": traffic.get("fp64_pipe_pct"),
                      "flops_source": traffic.get("source"),
                      "note": "time includes the host call (validation, uploads, histogram zeroing)",
                      "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (probe: 35.8 TFLOP/s DFMA)"},
