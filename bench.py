@@ -370,7 +370,7 @@ def run_e2e(args, w, groups, st, world):
 
 # ------------------------------------------------------------------------------- structured paths
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
-FLOPS_PER_ELEM = {"solve": 12, "lambda2": 48}      # algorithmic fp64 flops per bin per product
+FLOPS_PER_ELEM = {"solve": 9, "lambda2": 48}      # algorithmic fp64 flops per bin per product
 
 
 def _shape_groups(groups):

@@ -151,6 +151,45 @@ struct Team {
             __syncthreads();
         }
     }
+    // as scan<1, E>, and in the same barrier the per-warp partials warp_part[w] (written by lane 0 of
+    // each warp before the call) are added in fixed order: part = their sum over the team-local warps
+    template <int E>
+    __device__ __forceinline__ void scan_and_sum(double (&v)[1][E], double &tot, double *warp_part, double &part) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int i = 1; i < E; ++i) v[0][i] += v[0][i - 1];
+        double x = v[0][E - 1];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        double ex = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 0) ex = 0.0;
+        if constexpr (MODE == kWarp) {
+            tot = __shfl_sync(0xffffffffu, x, 31);
+#pragma unroll
+            for (int i = 0; i < E; ++i) v[0][i] += ex;
+            part = warp_part[0];
+        } else {
+            const int nw = blockDim.x >> 5;
+            if (lane == 31) scr[warp] = x;
+            __syncthreads();
+            double wex = 0.0, tt = 0.0, pt = 0.0;
+            for (int w = 0; w < nw; ++w) {
+                const double wt = scr[w];
+                if (w < warp) wex += wt;
+                tt += wt;
+                pt += warp_part[w];
+            }
+            tot = tt;
+            part = pt;
+            const double e = wex + ex;
+#pragma unroll
+            for (int i = 0; i < E; ++i) v[0][i] += e;
+            __syncthreads();
+        }
+    }
     // exchange K per-CTA values through area ex (A or B) and synchronise the team; afterwards
     // total(k) gives the sum over all CTAs and over the CTAs before this one. For a single-CTA
     // team only the barrier remains (and the values are already the totals).
@@ -232,14 +271,18 @@ template <int E>
 __device__ __forceinline__ int xsize(int threads) { const int ch = threads * E; return ch + ch / E; }
 
 // ---------------------------------------------------------------------------------------------
-// f2: stationary solve. pi^0 = 1/N; v^{k+1} = v^k P~ (unnormalised; P~ is stochastic so the scale
-// stays ~1); pi^k = v^k / ||v^k||_1; stop after the first k with ||pi^{k+1} - pi^k||_1 < tol (the change
-// of product k is published with the scan totals of product k + 1, one exchange fewer per product).
-// Shared memory: xbuf | w | 1/D (each xsize).
+// f2: stationary solve. pi^0 = 1/N; v^{k+1} = v^k P~; pi^k = v^k / ||v^k||_1; stop after the first k
+// with ||pi^{k+1} - pi^k||_1 < tol. P~ is row-stochastic, so ||v^k||_1 = ||v^0||_1 = 1 up to rounding
+// (|1 - ||v^k||| ~ sqrt(k) eps): the iterates are not renormalised, the change is ||v^{k+1} - v^k||_1
+// (differs from the normalised change by ~1e-15 << tol) and pi is normalised once at the end
+// (R25). Per product: scan (its first barrier also adds the previous product's change
+// partials) -> publish (scan total, change) -> barrier -> y, push, change partial -> barrier.
+// Shared memory: xbuf | w | 1/D (each xsize; w and 1/D in registers at E = 8).
 template <int MODE, int E>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) {
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
+    __shared__ double dwarp[kSMaxWarps];              // per-warp change partials of the last product
     Team<MODE> tm(sh, a.C);
     const int item = item_index<MODE>(a.C);
     const int m = a.prof[item], l = a.lsh[item];
@@ -267,54 +310,53 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
         yp[e] = P.valid(e) ? u : 0.0;
         xbuf[P.loc(e)] = yp[e];                        // the gathered uniform vector is uniform
     }
-    double s_prev = 1.0, dpart = 0.0, change = __longlong_as_double(0x7ff0000000000000ll);
+    if ((threadIdx.x & 31) == 0) dwarp[threadIdx.x >> 5] = 0.0;
+    double change = __longlong_as_double(0x7ff0000000000000ll);
     int k = 0, conv = 0;
     tm.barrier();
     for (;;) {
-        // phase 1: z = x / D, scan; publish (scan total, change partial of product k - 1)
-        double v[1][E], tot[1];
+        // phase 1: z = x / D, scan (+ the change partials of product k - 1); publish both
+        double v[1][E], tot, dpart;
 #pragma unroll
         for (int e = 0; e < E; ++e) v[0][e] = xbuf[P.loc(e)] * (REG ? idr[REG ? e : 0] : ids[P.loc(e)]);
-        tm.template scan<1, E>(v, tot);
+        tm.template scan_and_sum<E>(v, tot, dwarp, dpart);
         {
-            const double pv[2] = {tot[0], dpart};
+            const double pv[2] = {tot, dpart};
             tm.template exchange<2>(tm.exA, pv);
         }
         double T, off, dummy;
-        tm.total(tm.exA, 0, tot[0], T, off);
+        tm.total(tm.exA, 0, tot, T, off);
         if (k > 0) {
             tm.total(tm.exA, 1, dpart, change, dummy);
             if (change < a.tol) { conv = 1; break; }
-            if (k >= a.max_iter || !(s_prev > 0.0) || !isfinite(change)) break;
+            if (k >= a.max_iter || !isfinite(change)) break;
         }
         // phase 2: y = w (C + e^{-Lambda} (T - C)) at the natural positions (in place of the scan);
-        // push; publish sum(y)
-        double ps[1] = {0.0};
+        // push; the change partial ||y - y_prev||_1 of this warp
+        double d = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const double Cj = off + v[0][e];
             v[0][e] = P.valid(e) ? (REG ? wr[REG ? e : 0] : ws[P.loc(e)]) * (Cj + eL * (T - Cj)) : 0.0;
-            ps[0] += v[0][e];
-        }
-        push<MODE, E>(tm, xbuf, P, v[0]);
-        tm.template sum<1>(ps);
-        tm.template exchange<1>(tm.exB, ps);
-        double s, d2;
-        tm.total(tm.exB, 0, ps[0], s, d2);
-        double d[1] = {0.0};
-        const double is = 1.0 / s, ip = 1.0 / s_prev;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            d[0] += fabs(v[0][e] * is - yp[e] * ip);
+            d += fabs(v[0][e] - yp[e]);
             yp[e] = v[0][e];
         }
-        tm.template sum<1>(d);
-        dpart = d[0];
-        s_prev = s;
+        push<MODE, E>(tm, xbuf, P, v[0]);
+        d = warp_allsum(d);
+        if ((threadIdx.x & 31) == 0) dwarp[threadIdx.x >> 5] = d;
+        tm.barrier();   // pushes complete (and dwarp written) before the next product reads them
         ++k;
     }
+    // pi^k = v^k / ||v^k||_1 at the natural positions
+    double sv[1] = {0.0};
+#pragma unroll
+    for (int e = 0; e < E; ++e) sv[0] += yp[e];
+    tm.template sum<1>(sv);
+    tm.template exchange<1>(tm.exB, sv);
+    double s_k, dm;
+    tm.total(tm.exB, 0, sv[0], s_k, dm);
     double *out = a.pi + (size_t)item * P.N;
-    const double is = 1.0 / s_prev;
+    const double is = 1.0 / s_k;
 #pragma unroll
     for (int e = 0; e < E; ++e)
         if (P.valid(e)) out[P.p0 + e] = yp[e] * is;
@@ -323,10 +365,10 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
         st.l = l;
         st.iters = k;
         st.done = 1;
-        st.converged = conv;
+        st.converged = conv && s_k > 0.0;
         st.cur = 0;
         st.pad0 = st.pad1 = st.pad2 = 0;
-        st.s = s_prev;
+        st.s = s_k;
         st.change = change;
         a.st[item] = st;
     }
@@ -498,6 +540,7 @@ template <int MODE, int E>
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a) {
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
+    __shared__ double twarp[kSMaxWarps];              // per-warp TV partials of the last product
     Team<MODE> tm(sh, a.C);
     const int start = a.start_bin0 + item_index<MODE>(a.C);
     const int m = a.prof[0], l = a.lsh[0];
@@ -512,31 +555,39 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a)
     if (r0 >= P.N) r0 -= P.N;
 #pragma unroll
     for (int e = 0; e < E; ++e) xbuf[P.loc(e)] = (P.p0 + e == r0) ? 1.0 : 0.0;
+    if ((threadIdx.x & 31) == 0) twarp[threadIdx.x >> 5] = 0.0;
     int n = 0, hit = -1;
     tm.barrier();
     for (;;) {
-        double v[1][E], tot[1];
+        // phase 1: scan of x / D (+ the TV partials of product n, decided one exchange later)
+        double v[1][E], tot, tvpart;
 #pragma unroll
         for (int e = 0; e < E; ++e) v[0][e] = xbuf[P.loc(e)] * ids[P.loc(e)];
-        tm.template scan<1, E>(v, tot);
-        tm.template exchange<1>(tm.exA, tot);
-        double T, off, dm;
-        tm.total(tm.exA, 0, tot[0], T, off);
-        double tv[1] = {0.0};
+        tm.template scan_and_sum<E>(v, tot, twarp, tvpart);
+        {
+            const double pv[2] = {tot, tvpart};
+            tm.template exchange<2>(tm.exA, pv);
+        }
+        double T, off, TV, dm;
+        tm.total(tm.exA, 0, tot, T, off);
+        if (n > 0) {
+            tm.total(tm.exA, 1, tvpart, TV, dm);
+            if (0.5 * TV <= a.eps) { hit = n; break; }
+            if (n >= a.max_iter) break;
+        }
+        // phase 2: product n + 1, push, its TV partial
+        double tv = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const double Cj = off + v[0][e];
             v[0][e] = P.valid(e) ? ws[P.loc(e)] * (Cj + eL * (T - Cj)) : 0.0;
-            tv[0] += fabs(v[0][e] - pis[P.loc(e)]);
+            tv += fabs(v[0][e] - pis[P.loc(e)]);
         }
         push<MODE, E>(tm, xbuf, P, v[0]);
-        tm.template sum<1>(tv);
-        tm.template exchange<1>(tm.exB, tv);
-        double TV;
-        tm.total(tm.exB, 0, tv[0], TV, dm);
+        tv = warp_allsum(tv);
+        if ((threadIdx.x & 31) == 0) twarp[threadIdx.x >> 5] = tv;
+        tm.barrier();
         ++n;
-        if (0.5 * TV <= a.eps) { hit = n; break; }
-        if (n >= a.max_iter) break;
     }
     if (tm.c == 0 && threadIdx.x == 0) {
         a.nsteps[start] = hit;
