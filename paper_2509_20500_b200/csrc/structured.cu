@@ -151,43 +151,77 @@ struct Team {
             __syncthreads();
         }
     }
-    // as scan<1, E>, and in the same barrier the per-warp partials warp_part[w] (written by lane 0 of
-    // each warp before the call) are added in fixed order: part = their sum over the team-local warps
-    template <int E>
-    __device__ __forceinline__ void scan_and_sum(double (&v)[1][E], double &tot, double *warp_part, double &part) {
+    // as scan<V, E>, and in the same barrier the per-warp partials wp[k * kSMaxWarps + w] (written by
+    // lane 0 of each warp before the call) are added in fixed order: part[k] = their sum over the
+    // team-local warps
+    template <int V, int E, int K>
+    __device__ __forceinline__ void scan_sum(double (&v)[V][E], double (&tot)[V], const double *wp, double (&part)[K]) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        double x[V], ex[V];
 #pragma unroll
-        for (int i = 1; i < E; ++i) v[0][i] += v[0][i - 1];
-        double x = v[0][E - 1];
+        for (int a = 0; a < V; ++a) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            for (int i = 1; i < E; ++i) v[a][i] += v[a][i - 1];
+            x[a] = v[a][E - 1];
         }
-        double ex = __shfl_up_sync(0xffffffffu, x, 1);
-        if (lane == 0) ex = 0.0;
-        if constexpr (MODE == kWarp) {
-            tot = __shfl_sync(0xffffffffu, x, 31);
 #pragma unroll
-            for (int i = 0; i < E; ++i) v[0][i] += ex;
-            part = warp_part[0];
+        for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+            for (int a = 0; a < V; ++a) {
+                const double y = __shfl_up_sync(0xffffffffu, x[a], o);
+                if (lane >= o) x[a] += y;
+            }
+#pragma unroll
+        for (int a = 0; a < V; ++a) {
+            ex[a] = __shfl_up_sync(0xffffffffu, x[a], 1);
+            if (lane == 0) ex[a] = 0.0;
+        }
+        if constexpr (MODE == kWarp) {
+#pragma unroll
+            for (int a = 0; a < V; ++a) {
+                tot[a] = __shfl_sync(0xffffffffu, x[a], 31);
+#pragma unroll
+                for (int i = 0; i < E; ++i) v[a][i] += ex[a];
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) part[k] = wp[k * kSMaxWarps];
         } else {
             const int nw = blockDim.x >> 5;
-            if (lane == 31) scr[warp] = x;
-            __syncthreads();
-            double wex = 0.0, tt = 0.0, pt = 0.0;
-            for (int w = 0; w < nw; ++w) {
-                const double wt = scr[w];
-                if (w < warp) wex += wt;
-                tt += wt;
-                pt += warp_part[w];
-            }
-            tot = tt;
-            part = pt;
-            const double e = wex + ex;
 #pragma unroll
-            for (int i = 0; i < E; ++i) v[0][i] += e;
+            for (int a = 0; a < V; ++a)
+                if (lane == 31) scr[a * kSMaxWarps + warp] = x[a];
             __syncthreads();
+#pragma unroll
+            for (int a = 0; a < V; ++a) {
+                double wex = 0.0, tt = 0.0;
+                for (int w = 0; w < nw; ++w) {
+                    const double wt = scr[a * kSMaxWarps + w];
+                    if (w < warp) wex += wt;
+                    tt += wt;
+                }
+                tot[a] = tt;
+                const double e = wex + ex[a];
+#pragma unroll
+                for (int i = 0; i < E; ++i) v[a][i] += e;
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double pt = 0.0;
+                for (int w = 0; w < nw; ++w) pt += wp[k * kSMaxWarps + w];
+                part[k] = pt;
+            }
+            __syncthreads();
+        }
+    }
+    // sum over the team-local warps of per-warp partials (after a barrier that ordered their writes)
+    template <int K>
+    __device__ __forceinline__ void warp_partials(const double *wp, double (&part)[K]) const {
+        const int nw = MODE == kWarp ? 1 : (int)(blockDim.x >> 5);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double pt = 0.0;
+            for (int w = 0; w < nw; ++w) pt += wp[k * kSMaxWarps + w];
+            part[k] = pt;
         }
     }
     // exchange K per-CTA values through area ex (A or B) and synchronise the team; afterwards
@@ -316,10 +350,11 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
     tm.barrier();
     for (;;) {
         // phase 1: z = x / D, scan (+ the change partials of product k - 1); publish both
-        double v[1][E], tot, dpart;
+        double v[1][E], tt[1], dp[1];
 #pragma unroll
         for (int e = 0; e < E; ++e) v[0][e] = xbuf[P.loc(e)] * (REG ? idr[REG ? e : 0] : ids[P.loc(e)]);
-        tm.template scan_and_sum<E>(v, tot, dwarp, dpart);
+        tm.template scan_sum<1, E, 1>(v, tt, dwarp, dp);
+        const double tot = tt[0], dpart = dp[0];
         {
             const double pv[2] = {tot, dpart};
             tm.template exchange<2>(tm.exA, pv);
@@ -399,6 +434,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
     const Pos<MODE, E> P(a.N, tm.c, l);
     const int xs = xsize<E>(blockDim.x);
     double *xb0 = xbuf, *xb1 = xbuf + xs, *ws = xbuf + 2 * xs, *ids = xbuf + 3 * xs, *pis = xbuf + 4 * xs;
+    __shared__ double wpart[7 * kSMaxWarps];          // per-warp partial dot products
     stage(ws, a.w + (size_t)m * a.vstride, P);
     stage(ids, a.invD + (size_t)m * a.vstride, P);
     stage(pis, a.pi + (size_t)item * P.N, P);
@@ -441,8 +477,13 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
             pp[3] += wn[0][e] * wn[1][e];
             pp[4] += wn[1][e] * wn[1][e];
         }
-        tm.template scan<2, E>(v, tot);
-        tm.template sum<5>(pp);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            const double t = warp_allsum(pp[i]);
+            if ((threadIdx.x & 31) == 0) wpart[i * kSMaxWarps + (threadIdx.x >> 5)] = t;
+        }
+        if constexpr (MODE == kWarp) __syncwarp();
+        tm.template scan_sum<2, E, 5>(v, tot, wpart, pp);   // its first barrier also adds the pp partials
         {
             const double pv[7] = {tot[0], tot[1], pp[0], pp[1], pp[2], pp[3], pp[4]};
             tm.template exchange<7>(tm.exA, pv);
@@ -478,11 +519,22 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
         }
         push<MODE, E>(tm, xb0, P, wn[0]);
         push<MODE, E>(tm, xb1, P, wn[1]);
-        tm.template sum<7>(hp);
-        tm.template exchange<7>(tm.exB, hp);
         double h[7];
+        if constexpr (MODE == kCluster) {
+            tm.template sum<7>(hp);
+            tm.template exchange<7>(tm.exB, hp);
 #pragma unroll
-        for (int i = 0; i < 7; ++i) tm.total(tm.exB, i, hp[i], h[i], dm);
+            for (int i = 0; i < 7; ++i) tm.total(tm.exB, i, hp[i], h[i], dm);
+        } else {                                      // one barrier orders the pushes and the partials
+#pragma unroll
+            for (int i = 0; i < 7; ++i) {
+                const double t = warp_allsum(hp[i]);
+                if ((threadIdx.x & 31) == 0) wpart[i * kSMaxWarps + (threadIdx.x >> 5)] = t;
+            }
+            tm.barrier();
+            tm.template warp_partials<7>(wpart, h);
+            tm.barrier();                             // wpart is rewritten in the next phase 1
+        }
         ++k;
         // Ritz values: H = M G^{-1}, M = W Q^T = [[h11, h12], [h21, h22]], G = Q Q^T
         double nre, nim;
@@ -560,10 +612,11 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a)
     tm.barrier();
     for (;;) {
         // phase 1: scan of x / D (+ the TV partials of product n, decided one exchange later)
-        double v[1][E], tot, tvpart;
+        double v[1][E], tt[1], tp[1];
 #pragma unroll
         for (int e = 0; e < E; ++e) v[0][e] = xbuf[P.loc(e)] * ids[P.loc(e)];
-        tm.template scan_and_sum<E>(v, tot, twarp, tvpart);
+        tm.template scan_sum<1, E, 1>(v, tt, twarp, tp);
+        const double tot = tt[0], tvpart = tp[0];
         {
             const double pv[2] = {tot, tvpart};
             tm.template exchange<2>(tm.exA, pv);
