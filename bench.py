@@ -435,7 +435,7 @@ def run_struct(args, rank, world, dev):
         for p in main_plans:
             infos, kms = p.info()
             ms += kms
-            products += sum(i["iters"] for i in infos)
+            products += int(infos["iters"].sum())
         k_ms.append(ms)
     if world > 1:
         torch.distributed.barrier()
@@ -446,8 +446,8 @@ def run_struct(args, rank, world, dev):
     kernel_s = statistics.mean(k_ms) / 1e3
     flops = FLOPS_PER_ELEM[kind] * N * products
     achieved = flops / kernel_s / 1e12
-    iters = [[i["iters"] for i in p.info()[0]] for p in main_plans]
-    conv = all(i["converged"] for p in main_plans for i in p.info()[0])
+    iters = [[int(x) for x in p.info()[0]["iters"]] for p in main_plans]
+    conv = bool(all(int(x) for p in main_plans for x in p.info(check=False)[0]["converged"]))
     unit = "solves/s" if kind == "solve" else "spectral analyses/s"
     metric = ("stationary solves/s, matrix-free structured operator (SURVEY f2)" if kind == "solve" else
               "spectral analyses/s (pi + lambda_2, modulus and phase; SURVEY f1)")

@@ -11,5 +11,5 @@ from .splidar import (  # noqa: F401
     apply_deadtime, build_base, build_base_batched, build_info, empty_matrix, flux_vectors, leading_dim,
     lib_path, shift, solve_host, stationary, sweep, workspace, workspace_bytes,
     SpectralInfo, bin_trajectory, flux_items, mixing_steps, second_eigenvalue, stationary_structured,
-    structured_workspace, StructPlan, build_eq4, monte_carlo,
+    structured_workspace, StructPlan, build_eq4, monte_carlo, lambda2_of,
 )

@@ -88,14 +88,15 @@ def main(argv=None) -> int:
                 info = infos[0]
             if not info["converged"]:
                 status = EXIT_NOCONV
-            out = {"n_bins": f.n_bins, "shift_l": info["shift_l"], "iters": info["iters"],
-                   "converged": info["converged"], "l1_change": info["l1_change"], "path": a.path,
+            out = {"n_bins": f.n_bins, "shift_l": int(info["shift_l"]), "iters": int(info["iters"]),
+                   "converged": bool(info["converged"]), "l1_change": float(info["l1_change"]), "path": a.path,
                    "pi": pi[0].cpu().tolist()}
             if a.spectral and status == EXIT_OK:
                 shape, S, B = spl.flux_items(f)
                 l2 = spl.second_eigenvalue(shape, S, B, [a.t_d], pi.contiguous(), check=False)[0]
-                out["lambda2"] = {"re": l2["lambda2"].real, "im": l2["lambda2"].imag, "modulus": l2["modulus"],
-                                  "phase": l2["phase"], "gap": l2["gap"], "converged": l2["converged"]}
+                out["lambda2"] = {"re": float(l2["lambda2_re"]), "im": float(l2["lambda2_im"]),
+                                  "modulus": float(l2["modulus"]), "phase": float(l2["phase"]),
+                                  "gap": float(l2["gap"]), "converged": bool(l2["converged"])}
             if a.mixing and status == EXIT_OK:
                 n, _ = spl.mixing_steps(f, a.t_d, pi[0].contiguous(), check=False)
                 out["mixing_steps"] = n

@@ -149,6 +149,33 @@ static FluxDev to_dev(const splidar_flux *f, double s_scale = 1.0, double B = -1
     return d;
 }
 
+// Items (shape x S[m], B[m]): the shape's period, bins, pulse positions / widths and (non-negative)
+// relative signal weights are validated once; each item then only needs S finite >= 0, B finite > 0
+// and S * sum(weights) + B <= 600 -- the same conditions check_flux applies to the item's own flux,
+// without building it (batches of 10^4 items are validated in microseconds).
+static splidar_status check_shape(const splidar_flux *shape, double *sig_sum) {
+    if (!shape || shape->n_pulses < 0 || shape->n_pulses > kMaxPulses) return SPLIDAR_EINVAL;
+    if (shape->n_pulses > 0 && !shape->signal) return SPLIDAR_EINVAL;
+    double zeros[kMaxPulses] = {0.0};
+    splidar_flux f = *shape;
+    f.background = 1.0;
+    f.signal = zeros;                    // positions and widths only; weights checked below
+    splidar_status st = check_flux(&f);
+    if (st) return st;
+    double sum = 0.0;
+    for (int k = 0; k < shape->n_pulses; ++k) {
+        if (!std::isfinite(shape->signal[k]) || shape->signal[k] < 0.0) return SPLIDAR_EINVAL;
+        sum += shape->signal[k];
+    }
+    *sig_sum = sum;
+    return SPLIDAR_OK;
+}
+static splidar_status check_item(double sig_sum, double S, double B) {
+    if (!std::isfinite(S) || S < 0.0 || !finite_pos(B)) return SPLIDAR_EINVAL;
+    if (!(S * sig_sum + B <= 600.0)) return SPLIDAR_EINVAL;
+    return SPLIDAR_OK;
+}
+
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
 static splidar_status check_matrix(const void *P, int N, int64_t ld, int dt) {
@@ -567,17 +594,12 @@ splidar_status splidar_sweep(const splidar_flux *shape, int32_t n_items, const d
     const int N = shape->n_bins;
     splidar_status st;
     if ((st = check_matrix(P0_store, N, ld, dt))) return st;
-    // validate every item as a full flux and compute its shift
+    // validate every item and compute its shift
     std::vector<int> l((size_t)n_items);
+    double sig_sum;
+    if ((st = check_shape(shape, &sig_sum))) return st;
     for (int i = 0; i < n_items; ++i) {
-        FluxDev d = to_dev(shape, S[i], B[i]);
-        splidar_flux f = *shape;
-        f.background = B[i];
-        std::vector<double> sig((size_t)shape->n_pulses);
-        for (int k = 0; k < shape->n_pulses; ++k) sig[(size_t)k] = d.S[k];
-        f.signal = sig.data();
-        if (!std::isfinite(S[i]) || S[i] < 0.0) return SPLIDAR_EINVAL;
-        if ((st = check_flux(&f))) return st;
+        if ((st = check_item(sig_sum, S[i], B[i]))) return st;
         int32_t li;
         if ((st = splidar_shift(shape->t_r, N, t_d[i], &li))) return st;
         l[(size_t)i] = li;
@@ -719,24 +741,23 @@ static splidar_status struct_prepare(const splidar_flux *shape, int n_items, con
     p->prof.assign((size_t)n_items, 0);
     std::vector<FluxDev> fl;
     std::map<std::pair<double, double>, int> idx;
+    double sig_sum;
+    if ((st = check_shape(shape, &sig_sum))) return st;
     for (int i = 0; i < n_items; ++i) {
-        if (!std::isfinite(S[i]) || S[i] < 0.0) return SPLIDAR_EINVAL;
-        FluxDev d = to_dev(shape, S[i], B[i]);
-        splidar_flux f = *shape;
-        f.background = B[i];
-        std::vector<double> sig((size_t)shape->n_pulses);
-        for (int k = 0; k < shape->n_pulses; ++k) sig[(size_t)k] = d.S[k];
-        f.signal = sig.data();
-        if ((st = check_flux(&f))) return st;
+        if ((st = check_item(sig_sum, S[i], B[i]))) return st;
         int32_t li;
         if ((st = splidar_shift(shape->t_r, N, t_d[i], &li))) return st;
         p->l[(size_t)i] = li;
-        auto key = std::make_pair(S[i], B[i]);
+        const auto key = std::make_pair(S[i], B[i]);
+        if (i > 0 && S[i] == S[i - 1] && B[i] == B[i - 1]) {        // runs of equal (S, B): no lookup
+            p->prof[(size_t)i] = p->prof[(size_t)i - 1];
+            continue;
+        }
         auto it = idx.find(key);
         if (it == idx.end()) {
-            idx[key] = (int)fl.size();
+            idx.emplace(key, (int)fl.size());
             p->prof[(size_t)i] = (int)fl.size();
-            fl.push_back(d);
+            fl.push_back(to_dev(shape, S[i], B[i]));
         } else {
             p->prof[(size_t)i] = it->second;
         }
@@ -1005,21 +1026,17 @@ splidar_status splidar_monte_carlo(const splidar_flux *shape, int32_t n_items, c
     std::vector<FluxDev> fl;
     std::vector<int> prof((size_t)n_items);
     std::map<std::pair<double, double>, int> idx;
+    double sig_sum;
+    if ((st = check_shape(shape, &sig_sum))) return st;
     for (int i = 0; i < n_items; ++i) {
-        if (!std::isfinite(S[i]) || S[i] < 0.0 || !std::isfinite(t_d[i]) || t_d[i] < 0.0) return SPLIDAR_EINVAL;
-        FluxDev d = to_dev(shape, S[i], B[i]);
-        splidar_flux f = *shape;
-        f.background = B[i];
-        std::vector<double> sig((size_t)shape->n_pulses);
-        for (int k = 0; k < shape->n_pulses; ++k) sig[(size_t)k] = d.S[k];
-        f.signal = sig.data();
-        if ((st = check_flux(&f))) return st;
-        auto key = std::make_pair(S[i], B[i]);
+        if ((st = check_item(sig_sum, S[i], B[i]))) return st;
+        if (!std::isfinite(t_d[i]) || t_d[i] < 0.0) return SPLIDAR_EINVAL;
+        const auto key = std::make_pair(S[i], B[i]);
         auto it = idx.find(key);
         if (it == idx.end()) {
-            idx[key] = (int)fl.size();
+            idx.emplace(key, (int)fl.size());
             prof[(size_t)i] = (int)fl.size();
-            fl.push_back(d);
+            fl.push_back(to_dev(shape, S[i], B[i]));
         } else {
             prof[(size_t)i] = it->second;
         }

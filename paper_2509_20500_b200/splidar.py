@@ -391,8 +391,21 @@ def _items(shape, S, B, t_d):
     T = np.ascontiguousarray(t_d, dtype=np.float64).reshape(-1)
     if B.size != S.size or T.size != S.size or S.size < 1:
         raise SplidarError(EINVAL, "S, B, t_d must have equal non-zero length")
-    n_prof = len({(float(a), float(b)) for a, b in zip(S, B)})
+    # distinct (S, B) pairs, compared numerically as the library groups them: the workspace size
+    n_prof = int(np.unique(S + 1j * B).size)
     return S, B, T, n_prof
+
+
+def _records(ctypes_array) -> np.ndarray:
+    """Per-item infos as a numpy structured array (a zero-copy view of the ctypes array; fields as the
+    C struct: infos[m]["iters"], infos["converged"], ...). Used by the batched structured calls, whose
+    item counts make a list of dicts the dominant host cost."""
+    return np.ctypeslib.as_array(ctypes_array)
+
+
+def lambda2_of(rec) -> complex:
+    """lambda_2 of one spectral record (lambda2_re + i lambda2_im)."""
+    return complex(float(rec["lambda2_re"]), float(rec["lambda2_im"]))
 
 
 def stationary_structured(shape, S, B, t_d, tol: float = 1e-12, max_iter: int = 10 ** 6,
@@ -409,13 +422,14 @@ def stationary_structured(shape, S, B, t_d, tol: float = 1e-12, max_iter: int = 
                                               float(tol), int(max_iter), pi.data_ptr(), ws.data_ptr(), ws.numel(),
                                               infos, _stream(stream))
     _check(st, "splidar_stationary_structured", allow=() if check else (ENOCONV,))
-    return pi, [i.as_dict() for i in infos]
+    return pi, _records(infos)
 
 
 def second_eigenvalue(shape, S, B, t_d, pi: torch.Tensor, tol: float = 1e-13, max_iter: int = 10 ** 5,
                       ws: torch.Tensor | None = None, stream=None, check: bool = True) -> list:
     """f1: lambda_2 of P~ per item (modulus, phase in [0, pi], gap); pi = the items' stationary vectors
-    [M, N] on the device."""
+    [M, N] on the device. Returns a numpy structured array with the fields of SpectralInfo
+    (lambda2_of(rec) gives the complex value)."""
     S, B, T, n_prof = _items(shape, S, B, t_d)
     M, N = S.size, int(shape.n_bins)
     if not pi.is_cuda or pi.dtype != torch.float64 or pi.numel() != M * N or not pi.is_contiguous():
@@ -427,7 +441,7 @@ def second_eigenvalue(shape, S, B, t_d, pi: torch.Tensor, tol: float = 1e-13, ma
                                           pi.data_ptr(), float(tol), int(max_iter), ws.data_ptr(), ws.numel(),
                                           infos, _stream(stream))
     _check(st, "splidar_second_eigenvalue", allow=() if check else (ENOCONV,))
-    return [i.as_dict() for i in infos]
+    return _records(infos)
 
 
 def mixing_steps(flux, t_d: float, pi: torch.Tensor, eps: float = 1e-3, max_steps: int = 10 ** 5,
@@ -506,7 +520,7 @@ class StructPlan:
             infos = (SpectralInfo * self.M)()
             st = _lib().splidar_splan_info(self._h, None, infos, C.byref(ms), _stream(stream))
         _check(st, "splidar_splan_info", allow=() if check else (ENOCONV,))
-        return [i.as_dict() for i in infos], float(ms.value)
+        return _records(infos), float(ms.value)
 
     def close(self):
         if self._h:

@@ -207,7 +207,7 @@ def test_lambda2_large_n_vs_trajectory(spl):
     pi, _ = _one(spl, f, it.t_d)
     got = _lambda2(spl, f, it.t_d, pi)
     assert got["converged"] and 0 < got["modulus"] < 1
-    lam = got["lambda2"]
+    lam = spl.lambda2_of(got)
     start = torch.zeros(f.n_bins, dtype=torch.float64, device="cuda")
     start[100] = 1.0
     bin_ = int(torch.argmax(pi))
