@@ -297,6 +297,10 @@ def run_ours(args, rank, world, dev):
                    else "graph (GEMV + check in a conditional WHILE node)",
                    "step_as_cuda_graph": bool(graphed)},
         "entries_per_s": st.entries * K * world / t_build,
+        "solves_per_s_solve_only": st.n_solves * K * world / t_solve,
+        "paper_context": {"claim": "up to 1000x faster construction than Rapp's element-wise method",
+                          "where": "abstract P:5, §3.5 P:199", "hardware": "not stated in the paper",
+                          "same_gpu_ratio": "bench.py --path eq4 (Theorem 2 vs element-wise Eq. 4 on this B200)"},
         "ms_build_per_step": t_build / K * 1e3, "ms_solve_per_step": t_solve / K * 1e3,
         "iterations": [[i["iters"] for i in pi] for pi in infos],
         "roofline": {"bound": "hbm", "kernel": "k_power_step (power-iteration GEMV)", "achieved": gemv_gbs,
@@ -713,6 +717,23 @@ def run_oracle_spectral(args):
 
 
 # ------------------------------------------------------------------------------- oracle arm
+def host_info() -> dict:
+    """CPU model, logical cores and RAM of the host the oracle runs on."""
+    model, ram = None, None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                ram = f"{int(line.split()[1]) / 1048576:.0f} GiB"
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cores": os.cpu_count(), "ram": ram}
+
+
 def run_oracle_sample(args, iters_per_item=None):
     """The CPU oracle as it stands on a bounded sample of the same workload: R rows of the Eq. 4
     matrix (OpenMP over rows) and the oracle's long-double product over them; scaled to whole
@@ -733,6 +754,13 @@ def run_oracle_sample(args, iters_per_item=None):
         oracle.left_matvec(rows, x)
         t_mv_row.append((time.perf_counter() - t0) / R)
     tb, tm = statistics.median(t_build_row), statistics.median(t_mv_row)
+    # the build's rows again on one thread (the OpenMP figure above uses every core)
+    f0, tds0 = groups[0]
+    oracle.set_threads(1)
+    t0 = time.perf_counter()
+    oracle.rows_eq4(f0, tds0[0], 0, min(R, 256))
+    tb1 = (time.perf_counter() - t0) / min(R, 256)
+    oracle.set_threads(os.cpu_count() or 1)
     total = 0.0
     n = 0
     for gi, (f, tds) in enumerate(groups):
@@ -745,7 +773,9 @@ def run_oracle_sample(args, iters_per_item=None):
             "sample": f"{args.workload}: {R} of {N} rows of Eq. 4 (OpenMP, {cores} threads) and one long-double "
                       f"product over them (1 thread), for up to 4 items; scaled to {n} full solves "
                       f"(N rows each, one Eq. 4 matrix per dead time, GPU iteration counts)",
-            "s_per_row_build": tb, "s_per_row_product": tm}
+            "s_per_row_build": tb, "s_per_row_product": tm,
+            "build_entries_per_s_all_cores": N / tb, "build_entries_per_s_one_core": N / tb1,
+            "solve_products_entries_per_s_one_core": N / tm, "host": host_info()}
 
 
 def main():

@@ -65,6 +65,8 @@ def lib():
             "oracle_mc": (C.c_int, [fp, d, C.c_uint64, i64, i64, i32, i32, p]),
             "oracle_mc_timestamps": (C.c_int, [fp, d, C.c_uint64, i64, p, p]),
             "oracle_left_matvec": (None, [i32, i32, p, p, p]),
+            "oracle_set_threads": (None, [i32]),
+            "oracle_max_threads": (i32, []),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -187,6 +189,15 @@ def mc_timestamps(flux, t_d: float, seed: int, n: int):
     if lib().oracle_mc_timestamps(r.ref, float(t_d), int(seed) & (2 ** 64 - 1), int(n), q.ctypes.data, t.ctypes.data):
         raise ValueError("oracle_mc_timestamps: zero total flux")
     return q, t
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the row loops (timing only)."""
+    lib().oracle_set_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())
 
 
 def shift_l(flux, t_d: float) -> int:

@@ -27,6 +27,7 @@
  *   Parity pins: none unpinned (see tests/test_oracle_pins.py); the MC pin is statistical.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -42,6 +43,10 @@ typedef struct {
 } oracle_flux;
 
 static const double kPi = 3.14159265358979323846;
+
+/* Threads of the OpenMP row loops (timing only: the arithmetic does not depend on it). */
+void oracle_set_threads(int32_t n) { omp_set_num_threads(n > 0 ? n : 1); }
+int32_t oracle_max_threads(void) { return omp_get_max_threads(); }
 
 /* Phi(z) standard normal CDF via erfc. */
 static double std_cdf(double z) { return 0.5 * erfc(-z / sqrt(2.0)); }
