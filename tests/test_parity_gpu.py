@@ -383,3 +383,28 @@ def test_ragged_large_n(spl):
     shape, S, B = spl.flux_items(f)
     pis, _ = spl.stationary_structured(shape, S, B, [td])
     assert np.sum(np.abs(_np(pis[0]) - ref)) <= TOL_PI64
+
+
+def test_sweep_chunked_store_and_many_dead_times(spl):
+    """splidar_sweep with n_store = 3 for 7 distinct (S, B) profiles (three rounds of builds) and 40
+    dead times on one profile (two multi-vector passes of <= 32), N = 700 (fused solver) and 3000
+    (graph path): every item vs its own single solve and a sample vs the oracle."""
+    rng = np.random.default_rng(44)
+    for N in (700, 3000):
+        base = random_flux(rng, N, 1)
+        shape = Flux(base.t_r, N, base.tau, base.sigma, (1.0,), 1.0)
+        S = list(rng.uniform(0.1, 5.0, 6)) + [2.0] * 40
+        B = list(rng.uniform(0.05, 1.5, 6)) + [0.7] * 40
+        T = list(rng.uniform(0.0, 250.0, 6)) + list(np.linspace(1.0, 290.0, 40))
+        pi, infos = spl.sweep(shape, S, B, T, n_store=3)
+        got = _np(pi)
+        for m in list(range(6)) + [6, 25, 45]:
+            f = Flux(shape.t_r, N, shape.tau, shape.sigma, (S[m],), B[m])
+            assert infos[m]["converged"] and infos[m]["shift_l"] == oracle.shift_l(f, T[m])
+            P0 = spl.build_base(f)
+            single, _ = spl.stationary(P0, f.t_r, T[m])
+            assert np.sum(np.abs(got[m] - _np(single))) <= 1e-13, (N, m)
+        for m in (0, 45):
+            f = Flux(shape.t_r, N, shape.tau, shape.sigma, (S[m],), B[m])
+            want = _oracle_pi(oracle.build_eq4(f, T[m]))
+            assert np.sum(np.abs(got[m] - want)) <= TOL_PI64
