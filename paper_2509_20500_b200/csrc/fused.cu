@@ -5,8 +5,8 @@
 //
 // Cluster of C CTAs (C = min(16, ceil(N / 32))): CTA c owns the rows [c R, (c + 1) R) of P~0 and the
 // output columns [c W, (c + 1) W) (R = W = ceil(N / C)). Its rows of P~0 are copied to shared memory
-// once when they fit in 96 KB (N <= 384 fp64 / 512 fp32 at R = 32), else streamed from L2 (4 rows per
-// step, their loads in flight together). One product pi P~ = x P~0 with the gathered
+// once when they fit in 96 KB (N <= 384 fp64 / 512 fp32 at R = 32), else streamed from L2 through a
+// 3-stage shared-memory ring of TMA bulk copies (64 KB per stage, issued by one thread). One product pi P~ = x P~0 with the gathered
 // x_r = v[(r - l) mod N] (Thm 2):
 //   A  partial y over the CTA's rows (x_r from shared memory, fp64 FMA) ->
 //      each partial column slice pushed to its owner over DSMEM; barrier.cluster
@@ -27,6 +27,8 @@ namespace spl {
 namespace {
 
 constexpr int kFT = 256;          // threads per CTA
+constexpr int kRing = 3;          // stages of the TMA row ring (rows not resident in shared memory)
+constexpr int kRingBytes = 64 * 1024;   // per stage
 constexpr int kFMaxC = 16;
 constexpr int kFMaxCols = 8;      // columns per thread: N <= 2 * 256 * 4 = 2048
 
@@ -84,9 +86,20 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     const int r0 = c * R, r1 = min(N, r0 + R);
     const T *P = reinterpret_cast<const T *>(a.P) + (size_t)m * a.mstride;
     const int nrow = r1 - r0;
+    // non-resident rows: the TMA ring (after the small buffers, where the resident slice would be)
+    T *ring = slice;
+    const uint32_t row_bytes = (uint32_t)(((size_t)N * sizeof(T) + 15) & ~(size_t)15);   // <= ld bytes
+    int ring_rows = kRingBytes / (int)(NP * sizeof(T));
+    ring_rows = ring_rows < 1 ? 1 : (ring_rows > 8 ? 8 : ring_rows);
+    __shared__ uint64_t rbar[kRing];
+    uint32_t q_issue = 0, q_cons = 0;
+    const double *xrow = nullptr;
+    if (!a.resident && threadIdx.x == 0) {
+        for (int i = 0; i < kRing; ++i) mbar_init(&rbar[i], 1);
+        fence_mbar_init();
+    }
     if (a.resident) {                                // my rows, once, by TMA bulk copies; then smem only
         __shared__ uint64_t bar;
-        const uint32_t row_bytes = (uint32_t)(((size_t)N * sizeof(T) + 15) & ~(size_t)15);   // <= ld bytes
         if (threadIdx.x == 0) {
             mbar_init(&bar, 1);
             fence_mbar_init();
@@ -105,42 +118,68 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     int k = 0, conv = 0;
     cl.sync();
     for (;;) {
-        // ---- A: partial y over my rows; column j = 2 t + 512 q + e; 4 rows per step, all their
-        // loads issued before the FMAs (shared memory when resident, else L2)
+        // ---- A: partial y over my rows; column j = 2 t + 512 q + e. Resident rows: from shared
+        // memory, RS rows per step. Otherwise rows stream through a 3-stage shared-memory ring filled by
+        // TMA bulk copies (thread 0 issues, mbarrier complete_tx), so ~kRing x 64 KB are in flight.
         double acc[NC];
 #pragma unroll
         for (int i = 0; i < NC; ++i) acc[i] = 0.0;
-        const T *base = a.resident ? slice : P + (size_t)r0 * a.ld;
-        const int64_t rs = a.resident ? NP : a.ld;
-        for (int r = 0; r < nrow; r += RS) {
-            double xr[RS];
-            double pv[RS][NC];
+        auto rows_fma = [&](const T *base, int64_t rs, int n) {
+            for (int r = 0; r < n; r += RS) {
+                double xr[RS];
+                double pv[RS][NC];
 #pragma unroll
-            for (int rr = 0; rr < RS; ++rr) {
-                const bool rin = r + rr < nrow;
-                xr[rr] = rin ? xb[r + rr] : 0.0;
-                const T *row = base + (size_t)(rin ? r + rr : r) * rs;
+                for (int rr = 0; rr < RS; ++rr) {
+                    const bool rin = r + rr < n;
+                    xr[rr] = rin ? xrow[r + rr] : 0.0;
+                    const T *row = base + (size_t)(rin ? r + rr : r) * rs;
 #pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const int j = 2 * threadIdx.x + 2 * kFT * q;
-                    pv[rr][2 * q] = pv[rr][2 * q + 1] = 0.0;
-                    if (j < N) {
-                        if constexpr (sizeof(T) == 8) {
-                            const double2 v = a.resident ? *reinterpret_cast<const double2 *>(row + j)
-                                                         : __ldg(reinterpret_cast<const double2 *>(row + j));
-                            pv[rr][2 * q] = v.x; pv[rr][2 * q + 1] = v.y;
-                        } else {
-                            const float2 v = a.resident ? *reinterpret_cast<const float2 *>(row + j)
-                                                        : __ldg(reinterpret_cast<const float2 *>(row + j));
-                            pv[rr][2 * q] = v.x; pv[rr][2 * q + 1] = v.y;
+                    for (int q = 0; q < Q; ++q) {
+                        const int j = 2 * threadIdx.x + 2 * kFT * q;
+                        pv[rr][2 * q] = pv[rr][2 * q + 1] = 0.0;
+                        if (j < N) {
+                            if constexpr (sizeof(T) == 8) {
+                                const double2 v = *reinterpret_cast<const double2 *>(row + j);
+                                pv[rr][2 * q] = v.x; pv[rr][2 * q + 1] = v.y;
+                            } else {
+                                const float2 v = *reinterpret_cast<const float2 *>(row + j);
+                                pv[rr][2 * q] = v.x; pv[rr][2 * q + 1] = v.y;
+                            }
                         }
                     }
                 }
+#pragma unroll
+                for (int rr = 0; rr < RS; ++rr)
+#pragma unroll
+                    for (int i = 0; i < NC; ++i) acc[i] = fma(xr[rr], pv[rr][i], acc[i]);
             }
-#pragma unroll
-            for (int rr = 0; rr < RS; ++rr)
-#pragma unroll
-                for (int i = 0; i < NC; ++i) acc[i] = fma(xr[rr], pv[rr][i], acc[i]);
+        };
+        if (a.resident) {
+            xrow = xb;
+            rows_fma(slice, NP, nrow);
+        } else {
+            const int nst = (nrow + ring_rows - 1) / ring_rows;
+            auto issue = [&](int st) {                 // thread 0: stage st into buffer q_issue % kRing
+                const int rs0 = st * ring_rows;
+                const int nr = min(ring_rows, nrow - rs0);
+                const int buf = (int)(q_issue % kRing);
+                mbar_expect_tx(&rbar[buf], row_bytes * (uint32_t)nr);
+                for (int rr = 0; rr < nr; ++rr)
+                    bulk_g2s(ring + ((size_t)buf * ring_rows + rr) * NP, P + (size_t)(r0 + rs0 + rr) * a.ld, row_bytes,
+                             &rbar[buf]);
+                ++q_issue;
+            };
+            if (threadIdx.x == 0)
+                for (int st = 0; st < kRing - 1 && st < nst; ++st) issue(st);
+            for (int st = 0; st < nst; ++st) {
+                const int buf = (int)(q_cons % kRing);
+                mbar_wait(&rbar[buf], (q_cons / kRing) & 1u);
+                __syncthreads();                       // every thread is done with stage st - 1's buffer
+                if (threadIdx.x == 0 && st + kRing - 1 < nst) issue(st + kRing - 1);
+                xrow = xb + st * ring_rows;
+                rows_fma(ring + (size_t)buf * ring_rows * NP, NP, min(ring_rows, nrow - st * ring_rows));
+                ++q_cons;
+            }
         }
         // push partials to the owners of the columns: recv[c][j - owner R] in the owner's smem
 #pragma unroll
@@ -229,9 +268,15 @@ constexpr size_t kFResidentMax = 96 * 1024;   // largest row slice kept in share
 size_t fused_slice_bytes(int N, int R, int dtype) {
     return (size_t)R * ((N + 3) & ~3) * (dtype == SPLIDAR_F64 ? 8 : 4);
 }
+size_t fused_ring_bytes(int N, int dtype) {
+    const size_t row = (size_t)((N + 3) & ~3) * (dtype == SPLIDAR_F64 ? 8 : 4);
+    size_t rows = kRingBytes / row;
+    rows = rows < 1 ? 1 : (rows > 8 ? 8 : rows);
+    return kRing * rows * row;
+}
 size_t fused_smem(const FusedArgs &a, int dtype) {
     return sizeof(double) * (((size_t)a.R * (a.C + 2) + 1) & ~(size_t)1) +
-           (a.resident ? fused_slice_bytes(a.N, a.R, dtype) : 0);
+           (a.resident ? fused_slice_bytes(a.N, a.R, dtype) : fused_ring_bytes(a.N, dtype));
 }
 
 template <typename T>
@@ -249,7 +294,7 @@ void *fused_fn(int dtype, int N) {
         if (done[i] == fn) return fn;
         if (!done[i]) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
             done[i] = fn;
             return fn;
         }
