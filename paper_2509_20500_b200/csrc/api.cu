@@ -809,7 +809,6 @@ struct splidar_splan_s {
     int kind = 0;
     int n_items = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    std::vector<unsigned char> dummy;
 };
 
 static splidar_status splan_launch_impl(splidar_splan_s *pl, cudaStream_t s) {

@@ -23,6 +23,8 @@
 //   E  L, U, D, 1/D, 1/Z
 // tiles[5][M][ntile]: 0 mass tile totals, 1 mass tile offsets, 2 w tile totals, 3 w tile
 // prefix offsets, 4 w tile suffix offsets.
+#include <mutex>
+
 #include "common.cuh"
 
 namespace spl {
@@ -71,8 +73,7 @@ __device__ double tile_scan(double (&v)[kE], double *warp_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int i = 1; i < kE; ++i) v[i] += v[i - 1];
-    const double t = v[kE - 1];
-    double x = t;
+    double x = v[kE - 1];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const double y = __shfl_up_sync(0xffffffffu, x, o);
@@ -92,7 +93,6 @@ __device__ double tile_scan(double (&v)[kE], double *warp_tot) {
         if (w2 < warp) wex += wt;
         total += wt;
     }
-    (void)t;
     const double ex = xe + wex;
 #pragma unroll
     for (int i = 0; i < kE; ++i) v[i] += ex;
@@ -311,7 +311,6 @@ __device__ double small_scan(double (&v)[kSEl], double *wt) {
         }
         double ze = __shfl_up_sync(0xffffffffu, z, 1);   // exclusive prefix, not z - a (see tile_scan)
         if (lane == 0) ze = 0.0;
-        (void)a;
         wt[32 + lane] = ze;
         if (lane == 31) wt[64] = z;       // block total
     }
@@ -410,13 +409,13 @@ cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs bas
         int threads = (N + 1 + kSEl - 1) / kSEl;     // just enough threads for the N + 1 slots
         threads = (threads + 31) / 32 * 32;
         const int smem = (int)(sizeof(double) * threads * kSEl);
-        static bool attr = false;           // once per process (not inside every captured launch)
-        if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute((const void *)k_vec_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)(sizeof(double) * kST * kSEl));
-            if (e != cudaSuccess) return e;
-            attr = true;
-        }
+        static std::once_flag once;         // once per process (thread-safe; not in captured launches)
+        static cudaError_t attr = cudaSuccess;
+        std::call_once(once, [] {
+            attr = cudaFuncSetAttribute((const void *)k_vec_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(sizeof(double) * kST * kSEl));
+        });
+        if (attr != cudaSuccess) return attr;
         k_vec_small<<<M, threads, smem, s>>>(d_flux, N, base, vstride);
         return cudaGetLastError();
     }

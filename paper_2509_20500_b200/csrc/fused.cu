@@ -18,6 +18,8 @@
 // CTA), or after max_iter products. Deterministic: fixed-order sums, no atomics.
 #include <cooperative_groups.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -30,7 +32,7 @@ constexpr int kFT = 256;          // threads per CTA
 constexpr int kRing = 3;          // stages of the TMA row ring (rows not resident in shared memory)
 constexpr int kRingBytes = 64 * 1024;   // per stage
 constexpr int kFMaxC = 16;
-constexpr int kFMaxCols = 8;      // columns per thread: N <= 2 * 256 * 4 = 2048
+constexpr int kFMaxN = 2 * kFT * 4;   // N <= 2048: at most 4 column pairs per thread
 
 struct FusedShared {
     double exA[2 * kFMaxC];       // scan of nothing: [0] unused, change partials
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
 }  // namespace
 
 int fused_shape(int N, int *C, int *R) {
-    if (N > kFMaxCols * kFT) return 1;
+    if (N > kFMaxN) return 1;
     int c = (N + 31) / 32;
     if (c > kFMaxC) c = kFMaxC;
     if (c < 1) c = 1;
@@ -287,19 +289,23 @@ void *fused_fn_q(int N) {
     return (void *)k_power_fused<T, 4>;
 }
 
-void *fused_fn(int dtype, int N) {
-    void *fn = dtype == SPLIDAR_F64 ? fused_fn_q<double>(N) : fused_fn_q<float>(N);
-    static void *done[8] = {};              // attributes set once per kernel instance
-    for (int i = 0; i < 8; ++i) {
-        if (done[i] == fn) return fn;
-        if (!done[i]) {
-            cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            done[i] = fn;
-            return fn;
+// the kernel instance for (dtype, N); its attributes are set once per process for all instances
+// (thread-safe; never inside a captured launch)
+cudaError_t fused_fn(int dtype, int N, void **fn) {
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] {
+        void *all[] = {(void *)k_power_fused<double, 1>, (void *)k_power_fused<double, 2>,
+                       (void *)k_power_fused<double, 4>, (void *)k_power_fused<float, 1>,
+                       (void *)k_power_fused<float, 2>, (void *)k_power_fused<float, 4>};
+        for (void *f : all) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            if (e != cudaSuccess) { attr = e; return; }
         }
-    }
-    return fn;
+    });
+    *fn = dtype == SPLIDAR_F64 ? fused_fn_q<double>(N) : fused_fn_q<float>(N);
+    return attr;
 }
 
 int fused_resident(int N, int R, int dtype) { return fused_slice_bytes(N, R, dtype) <= kFResidentMax; }
@@ -317,7 +323,9 @@ cudaError_t launch_fused(int dtype, const FusedArgs &a, cudaStream_t s) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    void *fn = fused_fn(dtype, a.N);
+    void *fn = nullptr;
+    cudaError_t e = fused_fn(dtype, a.N, &fn);
+    if (e != cudaSuccess) return e;
     void *args[] = {const_cast<FusedArgs *>(&a)};
     return cudaLaunchKernelExC(&cfg, fn, args);
 }

@@ -12,8 +12,8 @@
 // Teams: the threads that own one item's N positions, E consecutive positions per thread:
 //   kWarp     one warp, E = 8 (N <= 256): shuffles only, __syncwarp orders the pushes
 //   kBlock    one CTA, E = 8 (N <= 4096): block scan / sums through shared memory, __syncthreads
-//   kCluster  a thread-block cluster of C CTAs x 512 threads, E = 8 (C = ceil(N / 4096)) for the solve
-//             and lambda_2, E = 16 (C = ceil(N / 8192)) for mixing and trajectories; CTA totals
+//   kCluster  a thread-block cluster of C CTAs x 512 threads, E = 8 (C = ceil(N / 4096)) for the solve,
+//             lambda_2 and mixing, E = 16 (C = ceil(N / 8192)) for trajectories; CTA totals
 //             exchanged over DSMEM, barrier.cluster between phases. (E = 16 solves fit c5's 17 items in
 //             one wave of 4-CTA clusters but measured slower: 460 vs 361 us; per-CTA work dominates.)
 // w and 1/D of a thread's positions stay in registers (solve) or are staged once in shared memory;
@@ -25,6 +25,9 @@
 // control-flow decisions and the result does not depend on timing (deterministic). Exclusive prefixes
 // are formed by shuffles, never by subtraction.
 #include <cooperative_groups.h>
+
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -716,6 +719,20 @@ int shape_for(int N, int E, int *C, int *threads) {
 }
 
 // nbuf = shared-memory vectors of xsize doubles the kernel uses
+// Kernel attributes once per kernel (keyed by its address: every team kernel has the same type), at
+// the largest dynamic shared memory it can request; thread-safe, never inside a captured launch.
+cudaError_t team_attrs_once(const void *fn, size_t max_smem) {
+    static std::mutex mu;
+    static std::vector<const void *> done;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const void *d : done)
+        if (d == fn) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) done.push_back(fn);
+    return e;
+}
+
 template <typename K>
 cudaError_t launch_team(K kernel, StructArgs a, int n_units, int E, int nbuf, cudaStream_t s) {
     int C, T;
@@ -724,12 +741,9 @@ cudaError_t launch_team(K kernel, StructArgs a, int n_units, int E, int nbuf, cu
     a.threads = T;
     const int chunk = T * E;
     const size_t smem = sizeof(double) * (size_t)nbuf * (chunk + chunk / E);
-    cudaError_t e = cudaFuncSetAttribute((const void *)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int cmax = kSMaxT * E;
+    cudaError_t e = team_attrs_once((const void *)kernel, sizeof(double) * (size_t)nbuf * (cmax + cmax / E));
     if (e != cudaSuccess) return e;
-    if (C > 8) {
-        e = cudaFuncSetAttribute((const void *)kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(n_units * C));
     cfg.blockDim = dim3((unsigned)T);
@@ -762,7 +776,7 @@ cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream
     switch (kind) {
         case kStructSolve: return SPL_TEAM_LAUNCH(k_struct_solve, 8, 3);
         case kStructLambda2: return SPL_TEAM_LAUNCH(k_struct_lambda2, 8, 5);
-        case kStructMixing: return SPL_TEAM_LAUNCH(k_struct_mixing, 16, 4);
+        case kStructMixing: return SPL_TEAM_LAUNCH(k_struct_mixing, 8, 4);     // 4 vectors: 147 KB at E = 8
         case kStructTraj: n_units = 1; return SPL_TEAM_LAUNCH(k_struct_traj, 16, 3);
     }
     return cudaErrorInvalidValue;

@@ -308,3 +308,26 @@ def test_extreme_flux_rejected_beyond_guard(spl):
         spl.build_base(f)
     with pytest.raises(spl.SplidarError):
         _one(spl, f, 10.0)
+
+
+def test_mixing_steps_cluster_team(spl):
+    """N = 6000 (> 4096: a 2-CTA cluster per start bin, DSMEM pushes): per-start first hits of three
+    starts against repeated products with the oracle's Eq. 4 matrix."""
+    f = random_flux(np.random.default_rng(6000), 6000, 2)
+    td = 71.0
+    pi, _ = _one(spl, f, td, tol=1e-14)
+    n_gpu, per = spl.mixing_steps(f, td, pi, eps=1e-3)
+    per = _np(per)
+    assert n_gpu == per.max() and np.all(per >= 1)
+    P = oracle.build_eq4(f, td)
+    pi_np = _np(pi)
+    for i in (0, 2999, int(np.argmax(per))):
+        v = np.zeros(f.n_bins)
+        v[i] = 1.0
+        n = 0
+        while True:
+            v = v @ P
+            n += 1
+            if 0.5 * np.abs(v - pi_np).sum() <= 1e-3:
+                break
+        assert per[i] == n, i
