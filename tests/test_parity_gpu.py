@@ -408,3 +408,22 @@ def test_sweep_chunked_store_and_many_dead_times(spl):
             f = Flux(shape.t_r, N, shape.tau, shape.sigma, (S[m],), B[m])
             want = _oracle_pi(oracle.build_eq4(f, T[m]))
             assert np.sum(np.abs(got[m] - want)) <= TOL_PI64
+
+
+@pytest.mark.parametrize("dtype,nv", [(torch.float64, 1), (torch.float64, 5), (torch.float32, 1)])
+def test_eager_mode_equals_graph(spl, monkeypatch, dtype, nv):
+    """SPLIDAR_EAGER=1 (host loop over the same kernels, for profilers) gives bit-identical pi and the same
+    infos as the CUDA-graph plan: fp64 single vector (check fused into the GEMV), fp64 multi-vector and
+    fp32 (separate check kernel); N = 3000 (graph path)."""
+    f = random_flux(np.random.default_rng(3000 + nv), 3000, 2)
+    tds = [float(x) for x in np.linspace(5.0, 280.0, nv)]
+    P0 = spl.build_base(f, dtype)
+    g = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-12)
+    ig = g.execute(check=False)
+    monkeypatch.setenv("SPLIDAR_EAGER", "1")
+    e = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-12)
+    monkeypatch.delenv("SPLIDAR_EAGER")
+    ie = e.execute(check=False)
+    assert torch.equal(g.pi, e.pi) and ig == ie
+    g.close()
+    e.close()
