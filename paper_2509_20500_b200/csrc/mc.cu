@@ -16,10 +16,11 @@
 // k Delta_h] (X = 0 read as t_r) once k >= n_burn; a run stops after n_regs counted registrations, or
 // (n_cycles > 0) at the first registration n_cycles laser periods after the end of the burn-in.
 //
-// Inversion of F on [0, t_r): a CTA serves runs of one item; it tabulates F at 512 + 1 uniform nodes
-// in shared memory, brackets the root by binary search in the table, then runs Newton steps (F' =
-// lambda > 0 since B > 0) safeguarded by bisection of the bracket until F(t) - y reaches the rounding
-// floor of F or the step is below 1e-15 t_r.
+// Inversion of F on [0, t_r): a CTA serves runs of one item; it tabulates F and lambda = dF/dt at
+// 512 + 1 uniform nodes in shared memory, brackets the root by binary search in the table, starts from
+// the root of the cubic Hermite interpolant on the bracket, then runs Newton steps on the closed form
+// (dF/dt = lambda > 0 since B > 0) safeguarded by bisection of the bracket until F(t) - y reaches the
+// rounding floor of F or the step is below 1e-15 t_r.
 #include "common.cuh"
 
 namespace spl {
@@ -60,8 +61,8 @@ __device__ __forceinline__ double unif01_open(uint64_t &s) {   // (0, 1]
     return ((double)(splitmix64(s) >> 11) + 1.0) * (1.0 / 9007199254740992.0);
 }
 
-// F(t) = y on [0, t_r], 0 <= y < Lambda.
-__device__ double mc_finv(const FluxDev &f, const McConst &q, const double *tab, double y) {
+// F(t) = y on [0, t_r], 0 <= y < Lambda. tab = F at the 513 nodes, dtab = lambda = dF/dt at the nodes.
+__device__ double mc_finv(const FluxDev &f, const McConst &q, const double *tab, const double *dtab, double y) {
     const double h = f.t_r / kMcTable;
     int lo_i = 0, hi_i = kMcTable;            // tab[lo_i] <= y < tab[hi_i]
     while (hi_i - lo_i > 1) {
@@ -70,7 +71,24 @@ __device__ double mc_finv(const FluxDev &f, const McConst &q, const double *tab,
     }
     double lo = lo_i * h, hi = hi_i == kMcTable ? f.t_r : hi_i * h;
     const double flo = tab[lo_i], fhi = tab[hi_i];
-    double t = fhi > flo ? lo + (y - flo) / (fhi - flo) * (hi - lo) : 0.5 * (lo + hi);
+    // initial guess: root of the cubic Hermite interpolant of F on the bracket (F and lambda at its ends;
+    // error ~h^4), by Newton on the polynomial from the linear guess (no transcendentals)
+    double t;
+    if (fhi > flo) {
+        const double hh = hi - lo, d0 = dtab[lo_i] * hh, d1 = dtab[hi_i] * hh, df = fhi - flo;
+        double u = (y - flo) / df;
+        for (int it = 0; it < 3; ++it) {
+            const double u2 = u * u, u3 = u2 * u;
+            const double H = flo + df * (3.0 * u2 - 2.0 * u3) + d0 * (u3 - 2.0 * u2 + u) + d1 * (u3 - u2);
+            const double dH = df * (6.0 * u - 6.0 * u2) + d0 * (3.0 * u2 - 4.0 * u + 1.0) + d1 * (3.0 * u2 - 2.0 * u);
+            if (!(dH > 0.0)) break;
+            u -= (H - y) / dH;
+            u = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u);
+        }
+        t = lo + u * hh;
+    } else {
+        t = 0.5 * (lo + hi);
+    }
     // stop when the step is below 1e-15 t_r, the bracket is that narrow, or F(t) - y is at the
     // rounding floor of F (|g| <= 4 eps Lambda): below it the Newton step is rounding noise
     const double eps = 1e-15 * f.t_r;
@@ -88,7 +106,7 @@ __device__ double mc_finv(const FluxDev &f, const McConst &q, const double *tab,
 }
 
 __global__ void __launch_bounds__(kMcThreads) k_mc(const McArgs a) {
-    __shared__ double tab[kMcTable + 1];
+    __shared__ double tab[kMcTable + 1], dtab[kMcTable + 1];
     __shared__ FluxDev fs;
     __shared__ McConst qs;                                  // per-flux constants, shared by the CTA
     const int item = blockIdx.y;
@@ -104,8 +122,11 @@ __global__ void __launch_bounds__(kMcThreads) k_mc(const McArgs a) {
     }
     __syncthreads();
     const FluxDev &f = fs;
-    for (int g = threadIdx.x; g <= kMcTable; g += kMcThreads)
-        tab[g] = mc_F(f, qs, g == kMcTable ? f.t_r : g * (f.t_r / kMcTable));
+    for (int g = threadIdx.x; g <= kMcTable; g += kMcThreads) {
+        const double tg = g == kMcTable ? f.t_r : g * (f.t_r / kMcTable);
+        tab[g] = mc_F(f, qs, tg);
+        dtab[g] = mc_lambda(f, qs, tg);
+    }
     __syncthreads();
     if (threadIdx.x == 0) qs.Lam = tab[kMcTable];           // Lambda = F(t_r) (reading R5)
     __syncthreads();
@@ -131,7 +152,7 @@ __global__ void __launch_bounds__(kMcThreads) k_mc(const McArgs a) {
         if (rem < 0.0) { rem += q.Lam; extra -= 1; }
         if (rem >= q.Lam) { rem -= q.Lam; extra += 1; }
         qp = qq + extra;
-        t = mc_finv(f, q, tab, rem);
+        t = mc_finv(f, q, tab, dtab, rem);
         if (t >= f.t_r) { t -= f.t_r; qp += 1; }
         if (k < a.n_record) {
             a.q_rec[(size_t)c * a.n_record + k] = qp;
