@@ -3,6 +3,11 @@ set -u
 O=gpurun_out
 python __graft_entry__.py > $O/build.log 2>&1
 run() { local name=$1; shift; timeout 900 python bench.py "$@" > $O/$name.json 2> $O/$name.err; echo "$name rc=$?"; }
+# FP64 op counts and DRAM bytes of the ALU-bound kernels first (-> profiles/traffic.json, used below)
+M=smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active
+for w in c5 c3; do ncu --metrics $M --clock-control none -k regex:k_build_eq4 -c 1 --csv python bench.py --path eq4 --workload $w --steps 1 --warmup 0 --no-cpu-baseline > $O/ncu_eq4_metrics_$w.csv 2>/dev/null; done
+for w in c1 grid; do ncu --metrics $M --clock-control none -k regex:k_mc -c 1 --csv python bench.py --path mc --workload $w --steps 1 --warmup 0 --no-cpu-baseline > $O/ncu_mc_metrics_$w.csv 2>/dev/null; done
+python tools/update_traffic.py > $O/traffic_update.log 2>&1; echo "traffic rc=$?"
 run bench_c5                                        # default line (N=1): c5 fp64, dense path
 for w in c1 c2 c3 c4; do run bench_$w --workload $w --no-cpu-baseline; done
 run bench_c5_f32 --dtype f32 --no-cpu-baseline
