@@ -11,10 +11,12 @@ t = json.load(open(path))
 
 def parse(fname, kernel):
     rows, line = [], None
-    for r in csv.reader(open(fname)):
-        if r and r[0].startswith("{"):
-            line = json.loads(",".join(r))
-        elif len(r) > 14 and kernel in r[4]:
+    for raw in open(fname):
+        if raw.startswith("{"):
+            line = json.loads(raw)
+            continue
+        r = next(csv.reader([raw]), [])
+        if len(r) > 14 and kernel in r[4]:
             rows.append(r)
     m = {r[12]: float(r[14].replace(",", "")) for r in rows}
     return m, line
