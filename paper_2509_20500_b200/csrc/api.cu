@@ -42,15 +42,15 @@ WsLayout ws_layout(int N, int M, int V) {
     L.lsh = o;  o = a256(o + sizeof(int) * MV);
     L.oidx = o; o = a256(o + sizeof(int) * MV);
     L.y = o;    o = a256(o + sizeof(double) * MV * 2 * N);
-    L.X = o;    o = a256(o + sizeof(double) * 2 * (size_t)M * N * L.xstride);
+    L.X = o;    o = a256(o + sizeof(double) * (size_t)M * N * L.xstride);
     L.part = o; o = a256(o + sizeof(double) * (size_t)L.pieces * L.V * kStripCols);
     L.ssum = o; o = a256(o + sizeof(double) * MV * L.strips);
-    L.l1s = o;  o = a256(o + sizeof(double) * MV * L.strips);
+    L.l1part = o; o = a256(o + sizeof(double) * MV * L.chunks);
     L.state = o; o = a256(o + sizeof(SolveState) * MV);
     L.strip_cnt = o; o = a256(o + sizeof(unsigned) * (size_t)M * L.strips);
     L.mv_cnt = o; o = a256(o + sizeof(unsigned) * MV);
     L.act = o; o = a256(o + sizeof(int) * (size_t)M);
-    L.glob = o; o = a256(o + sizeof(unsigned) * 8);
+    L.glob = o; o = a256(o + sizeof(unsigned) * 4);
     L.total = o;
     return L;
 }
@@ -338,7 +338,7 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     a.X = reinterpret_cast<double *>(ws + L.X);
     a.part = reinterpret_cast<double *>(ws + L.part);
     a.ssum = reinterpret_cast<double *>(ws + L.ssum);
-    a.l1s = reinterpret_cast<double *>(ws + L.l1s);
+    a.l1part = reinterpret_cast<double *>(ws + L.l1part);
     a.st = reinterpret_cast<SolveState *>(ws + L.state);
     a.lsh = reinterpret_cast<const int *>(ws + L.lsh);
     a.strip_cnt = reinterpret_cast<unsigned *>(ws + L.strip_cnt);
@@ -387,10 +387,6 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     SPL_CUDA(cudaGraphConditionalHandleCreate(&h, p->graph, 1, cudaGraphCondAssignDefault));
     a.use_handle = 1;
     a.handle = h;
-    // the check inside the GEMV's strip finishers (R25) for fp64 storage with 1-2 vectors; fp32 rows are
-    // stochastic only to ~1e-7, and with many vectors the strips' x scatter is better spread over a
-    // separate full-grid kernel (measured: c3 / c4 +1.2%, c5's 17 vectors -1%)
-    a.fuse_check = (dt == SPLIDAR_F64 && L.V <= 2) ? 1 : 0;
 
     SolverKernels &k = p->k;
     if (solver_kernels(dt, L.V, &k, a)) return SPLIDAR_EINVAL;
@@ -425,17 +421,15 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     kp.blockDim = k.step_block;
     kp.sharedMemBytes = k.step_smem;
     kp.kernelParams = step_args;
-    SPL_CUDA(cudaGraphAddKernelNode(&n_step, body, nullptr, 0, &kp));   // GEMV (+ the check for fp64)
-    if (!a.fuse_check) {                                                 // fp32: separate normalising check
-        void *check_args[] = {&a};
-        kp.func = k.check_fn;
-        kp.gridDim = k.check_grid;
-        kp.blockDim = k.check_block;
-        kp.sharedMemBytes = 0;
-        kp.kernelParams = check_args;
-        cudaGraphNode_t n_check;
-        SPL_CUDA(cudaGraphAddKernelNode(&n_check, body, &n_step, 1, &kp));
-    }
+    SPL_CUDA(cudaGraphAddKernelNode(&n_step, body, nullptr, 0, &kp));
+    void *check_args[] = {&a};
+    kp.func = k.check_fn;
+    kp.gridDim = k.check_grid;
+    kp.blockDim = k.check_block;
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = check_args;
+    cudaGraphNode_t n_check;
+    SPL_CUDA(cudaGraphAddKernelNode(&n_check, body, &n_step, 1, &kp));
 
     std::vector<unsigned char> &fa = p->fin_args;
     fa.resize(finish_args_size());
@@ -521,8 +515,7 @@ static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
     SPL_CUDA(cudaLaunchKernel(k.init_fn, k.init_grid, k.init_block, args, 0, s));
     for (int it = 0; it < p->args.max_iter; ++it) {
         SPL_CUDA(cudaLaunchKernel(k.step_fn, k.step_grid, k.step_block, args, k.step_smem, s));
-        if (!p->eager_args.fuse_check)
-            SPL_CUDA(cudaLaunchKernel(k.check_fn, k.check_grid, k.check_block, args, 0, s));
+        SPL_CUDA(cudaLaunchKernel(k.check_fn, k.check_grid, k.check_block, args, 0, s));
         SPL_CUDA(cudaMemcpyAsync(p->host_flag, p->eager_args.glob + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
         SPL_CUDA(cudaStreamSynchronize(s));
         if (!*p->host_flag) break;

@@ -57,7 +57,7 @@ struct __align__(16) SolveState {
 struct WsLayout {
     int N, M, V;    // V padded to a power of two
     int strips, chunks, xstride, pieces;
-    size_t flux, vec, lsh, oidx, y, X, part, ssum, l1s, state, strip_cnt, mv_cnt, act, glob, total;
+    size_t flux, vec, lsh, oidx, y, X, part, ssum, l1part, state, strip_cnt, mv_cnt, act, glob, total;
 };
 
 WsLayout ws_layout(int N, int M, int V);
@@ -78,20 +78,19 @@ struct PowerArgs {
     int64_t mstride;
     int N, M, V, strips, chunks, xstride;
     double *y;               // [M][V][2][N]       unnormalised iterates (ping-pong)
-    double *X;               // [2][M][N][xstride] gathered x_v[r] = v_v[(r - l_v) mod N], by iteration parity
+    double *X;               // [M][N][xstride]    gathered, normalised x_v[r] = pi_v[(r - l_v) mod N]
     double *part;            // [pieces][V][512]   per-CTA partial column sums
     double *ssum;            // [M][V][strips]     strip sums of y
-    double *l1s;             // [M][V][strips]     strip ||y - y_prev||_1 (fp32: check-chunk partials)
+    double *l1part;          // [M][V][chunks]     per-chunk L1 changes (check kernel)
     SolveState *st;          // [M][V]
     const int *lsh;          // [M][V] row shifts l (< 0: unused vector)
     unsigned *strip_cnt;     // [M * strips]       pieces finished per strip (active order)
     unsigned *mv_cnt;        // [M][V]             check-kernel CTA counters
     int *act;                // [M]                active matrices (any vector still running)
-    unsigned *glob;          // [0] check CTA counter, [1] any-active flag, [2] active matrices, [3] X parity, [4] exit counter
+    unsigned *glob;          // [0] check CTA counter, [1] any-active flag, [2] number of active matrices
     double tol;
     int max_iter;
     int use_handle;
-    int fuse_check;          // fp64 storage: k_power_step also does the convergence check
     cudaGraphConditionalHandle handle;
 };
 

@@ -7,17 +7,6 @@
 //   y_v[j]   = sum_r x_v[r] P~0[r][j]               (left GEMV, fp64 accumulation)
 //   s_v = sum_j y_v[j],  pi_v^{k+1} = y_v / s_v,  change_v = ||pi_v^{k+1} - pi_v^k||_1
 //
-// fp64 storage with 1-2 vectors: one WHILE-body kernel per iteration, k_power_step is the GEMV AND the
-// convergence check (fp32 storage and multi-vector plans keep the separate normalising k_power_check,
-// see there). The
-// iterates are not renormalised between products (P~ is row-stochastic: ||v P~||_1 = ||v||_1 up to
-// rounding, R25), so the last CTA of each strip can finish its columns on its own: it writes
-// y, the strip's sum of y, the strip's ||y - y_prev||_1 and the next gathered x (X is double-buffered
-// by iteration parity, so the permuted writes never race with this pass's readers). The last CTA of
-// the grid to exit (an exit counter, so every CTA has read this launch's parameters) adds the strip
-// partials in fixed order, updates the states (change = ||y - y_prev||_1 / ||y_prev||_1, the L1 change
-// of the normalised iterates up to ~1e-15), rebuilds the active-matrix list and sets the WHILE
-// condition; pi = y / ||y||_1 is written by k_power_finish.
 // k_power_step (the GEMV, the dominant kernel): a persistent grid of kGemvCtas CTAs splits the
 // row-segments (matrix, 512-column strip, row) of all still-active matrices into equal contiguous
 // ranges (stream-K style, so the grid stays full when only a few matrices of a batch are still
@@ -27,7 +16,9 @@
 // shared memory and accumulate all running vectors in fp64 registers; x of converged vectors is
 // compacted away per stage so frozen vectors cost no FMAs. At the end of a strip piece a CTA writes
 // its partial column sums; the last piece of a strip (atomic counter) adds the pieces in fixed order
-// (deterministic) and finishes the strip as above.
+// (deterministic), writes y and the strip's sum of y.
+// k_power_check: s, the normalised L1 change, the state, the next gathered x, the active-matrix
+// list, and (last CTA) the WHILE condition.
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -190,65 +181,6 @@ struct StepSmem {
     static constexpr size_t BYTES = STAGES * (SEG + XB) + STAGES * sizeof(uint64_t);
 };
 
-// The convergence decision of one iteration, by the last CTA of the grid to exit k_power_step: per
-// running (matrix, vector), s = sum of strip sums and L1 = sum of strip ||y - y_prev||_1 (fixed
-// order); iters, change = L1 / s_prev, cur, s, converged / done; then the active-matrix list, the
-// iteration parity of X and the WHILE condition.
-__device__ void power_decide(const PowerArgs &a) {
-    const int S = a.strips;
-    for (int mv = threadIdx.x; mv < a.M * a.V; mv += blockDim.x) {
-        SolveState st = a.st[mv];
-        if (st.done) continue;
-        double s = 0.0, L1 = 0.0;
-        const double *ss = a.ssum + (size_t)mv * S, *ls = a.l1s + (size_t)mv * S;
-        for (int g = 0; g < S; ++g) {
-            s += __ldcg(ss + g);
-            L1 += __ldcg(ls + g);
-        }
-        const double change = L1 / st.s;
-        st.iters += 1;
-        st.change = change;
-        st.s = s;
-        st.cur ^= 1;
-        if (change < a.tol) { st.converged = 1; st.done = 1; }
-        else if (st.iters >= a.max_iter || !(s > 0.0) || !isfinite(change)) { st.done = 1; }
-        a.st[mv] = st;
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int n_act = 0;
-        for (int m = 0; m < a.M; ++m) {
-            int any = 0;
-            for (int v = 0; v < a.V; ++v) any |= !__ldcg(&a.st[(size_t)m * a.V + v].done);
-            if (any) a.act[n_act++] = m;
-        }
-        a.glob[1] = n_act > 0 ? 1u : 0u;
-        a.glob[2] = (unsigned)n_act;
-        a.glob[3] ^= 1u;
-        a.glob[4] = 0u;
-        __threadfence();
-        if (a.use_handle) cudaGraphSetConditional(a.handle, n_act > 0 ? 1u : 0u);
-    }
-}
-
-// every CTA counts itself out; the last one decides (no CTA can still be reading this launch's
-// n_act / parity when they change)
-__device__ __forceinline__ void power_exit(const PowerArgs &a, int *s_flag) {
-    if (!a.fuse_check) return;                         // fp32 storage: k_power_check decides
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned prev = atomicAdd(&a.glob[4], 1u);
-        *s_flag = prev == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (*s_flag) {
-        __threadfence();
-        power_decide(a);
-    }
-}
-
 template <typename T, int NV>
 __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(const PowerArgs a) {
     using SM = StepSmem<T, NV>;
@@ -259,24 +191,20 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
     T *segs = reinterpret_cast<T *>(smem);                                             // [S][RS][512]
     double *xbuf = reinterpret_cast<double *>(smem + kStages * SM::SEG);               // [S][RS][XST]
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * (SM::SEG + SM::XB));   // TMA landed
-    __shared__ int s_vmap[NV], s_cur[NV], s_l[NV], s_nact, s_last, s_decide;
+    __shared__ int s_vmap[NV], s_cur[NV], s_nact, s_last;
     __shared__ unsigned s_gmask, s_vmask;
-    __shared__ double red_sum[NWARPS][NV], red_l1[NWARPS][NV];
+    __shared__ double red_sum[NWARPS][NV];
 
     const int tid = threadIdx.x, b = blockIdx.x, G = gridDim.x;
     const int N = a.N, S = a.strips;
     const int n_act = (int)a.glob[2];
-    const unsigned par = a.glob[3];                    // X[par] is read, X[par ^ 1] written
     const int64_t T_units = (int64_t)n_act * S * N;
+    if (T_units == 0) return;
     int64_t U = (T_units + G - 1) / G;
     if (U < kMinRowsPerCta) U = kMinRowsPerCta;
     const int64_t u_begin = (int64_t)b * U;
-    if (T_units == 0 || u_begin >= T_units) {          // no work, but still counted out
-        power_exit(a, &s_decide);
-        return;
-    }
+    if (u_begin >= T_units) return;
     const int64_t u_end = u_begin + U < T_units ? u_begin + U : T_units;
-    const size_t xsz = (size_t)a.M * N * SM::XST;      // one X buffer
 
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
@@ -305,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
             for (int v = 0; v < NV; ++v) {
                 const SolveState s = a.st[(size_t)m * NV + v];
                 if (!s.done) {
-                    s_vmap[n] = v; s_cur[n] = s.cur; s_l[n] = s.l; ++n;
+                    s_vmap[n] = v; s_cur[n] = s.cur; ++n;
                     vm |= 1u << v;
                     // MMA groups of 8 in bits [0, NVM/8), DFMA leftovers in the bits after them
                     gm |= (SM::MMA && v >= SM::NVM) ? (1u << (SM::NVM / 8 + v - SM::NVM)) : (1u << (v >> 3));
@@ -323,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
         const int cols = min(kStripCols, N - c * kStripCols);
         const uint32_t seg_bytes = (uint32_t)(((size_t)cols * sizeof(T) + 15) & ~(size_t)15);
         const T *pbase = reinterpret_cast<const T *>(a.P) + (size_t)m * a.mstride + (size_t)c * kStripCols;
-        const double *xg = a.X + par * xsz + (size_t)m * N * SM::XST;
+        const double *xg = a.X + (size_t)m * N * SM::XST;
         const int nstages = (r_hi - r_lo + RS - 1) / RS;
 
         auto issue = [&](int k) {   // stage k of this piece into buffer q_issue % S (thread 0)
@@ -423,12 +351,10 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
         }
         __syncthreads();
         if (s_last) {
-            // finish the strip: y, its sum, ||y - y_prev||_1, and the next gathered x
             __threadfence();
-            double lsum[NV], l1[NV];
+            double lsum[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) lsum[v] = l1[v] = 0.0;
-            double *Xn = a.X + (par ^ 1u) * xsz + (size_t)m * N * SM::XST;
+            for (int v = 0; v < NV; ++v) lsum[v] = 0.0;
             if (2 * tid < cols) {
 #pragma unroll
                 for (int sl = 0; sl < NV; ++sl) {
@@ -441,26 +367,11 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
                         y0 += t.x;
                         y1 += t.y;
                     }
-                    const size_t yb = ((size_t)m * NV + v) * 2;
-                    const int j = c * kStripCols + 2 * tid;
-                    double *yv = a.y + (yb + (1 - s_cur[sl])) * N + j;
-                    const double *yo = a.y + (yb + s_cur[sl]) * N + j;
-                    const bool two = 2 * tid + 1 < cols;
-                    if (!two) y1 = 0.0;
+                    double *yv = a.y + (((size_t)m * NV + v) * 2 + (1 - s_cur[sl])) * N + c * kStripCols + 2 * tid;
                     yv[0] = y0;
-                    if (two) yv[1] = y1;
+                    if (2 * tid + 1 < cols) yv[1] = y1;
+                    else y1 = 0.0;
                     lsum[sl] = y0 + y1;
-                    if (a.fuse_check) {
-                        l1[sl] = fabs(y0 - yo[0]) + (two ? fabs(y1 - yo[1]) : 0.0);
-                        int r = j + s_l[sl];                   // x_r = v[(r - l) mod N]: v_j -> row j + l
-                        if (r >= N) r -= N;
-                        Xn[(size_t)r * SM::XST + v] = y0;
-                        if (two) {
-                            ++r;
-                            if (r >= N) r -= N;
-                            Xn[(size_t)r * SM::XST + v] = y1;
-                        }
-                    }
                 }
             }
             const int lane = tid & 31, warp = tid >> 5;
@@ -468,38 +379,31 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
             for (int sl = 0; sl < NV; ++sl) {
                 if (sl >= nact) break;
                 const double t = warp_sum(lsum[sl]);
-                const double t1 = warp_sum(l1[sl]);
-                if (lane == 0) { red_sum[warp][sl] = t; red_l1[warp][sl] = t1; }
+                if (lane == 0) red_sum[warp][sl] = t;
             }
             __syncthreads();
             if (tid < nact) {
-                double ssum = 0.0, lsm = 0.0;
+                double ssum = 0.0;
 #pragma unroll
-                for (int w = 0; w < NWARPS; ++w) { ssum += red_sum[w][tid]; lsm += red_l1[w][tid]; }
+                for (int w = 0; w < NWARPS; ++w) ssum += red_sum[w][tid];
                 a.ssum[((size_t)m * NV + s_vmap[tid]) * S + c] = ssum;
-                a.l1s[((size_t)m * NV + s_vmap[tid]) * S + c] = lsm;
             }
             if (tid == 0) a.strip_cnt[g] = 0u;
         }
         __syncthreads();
     }
-    power_exit(a, &s_decide);
 }
 
-// fp32 storage or > 2 vectors: the separate, normalising convergence check (k_power_step then skips
-// its own).
-// fp32 rows are stochastic only to ~1e-7, so the unnormalised iterates' norm drifts by the Perron
-// root each product and ||y - y_prev||_1 would never reach tol; here s = sum of strip sums (fixed
-// order), the chunk's part of ||y / s - y_prev / s_prev||_1, and the next gathered, normalised x
-// X[par ^ 1][m][(j + l) mod N][v] = y_j / s. The last CTA of each (matrix, vector) adds the chunks in
-// fixed order and updates the state; the last CTA of the grid rebuilds the active-matrix list, flips
-// the X parity and sets the WHILE condition. Done vectors are skipped (their pi stays frozen).
+// Convergence check of one iteration (after k_power_step in the WHILE body). CTA (chunk, mv):
+// s = sum of strip sums (fixed order); the chunk's part of ||y / s - pi^k||_1; the next gathered
+// x: X[m][(j + l) mod N][v] = y_j / s; the last CTA of each (matrix, vector) adds the chunks in
+// fixed order and updates the state; the last CTA of the grid rebuilds the active-matrix list and
+// sets the WHILE condition. Done vectors are skipped (their pi stays frozen).
 __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
     __shared__ double red[8];
     __shared__ int s_last;
     const int c = blockIdx.x, mv = blockIdx.y, tid = threadIdx.x;
     const int N = a.N;
-    const unsigned par = a.glob[3];
     const SolveState st = a.st[mv];
     if (!st.done) {
         const int m = mv / a.V, v = mv % a.V;
@@ -509,7 +413,7 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
         const double inv_new = 1.0 / S, inv_old = 1.0 / st.s;
         const double *yn = a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
         const double *yo = a.y + ((size_t)mv * 2 + st.cur) * N;
-        double *X = a.X + (par ^ 1u) * ((size_t)a.M * N * a.xstride) + (size_t)m * N * a.xstride + v;
+        double *X = a.X + (size_t)m * N * a.xstride + v;
         const int l = st.l < 0 ? 0 : st.l;
         double l1 = 0.0;
         const int j1 = min(N, (c + 1) * kCheckChunk);
@@ -527,7 +431,7 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
             double t = 0.0;
 #pragma unroll
             for (int w = 0; w < 8; ++w) t += red[w];
-            a.l1s[(size_t)mv * a.strips + c] = t;      // chunk partials (chunks <= strips)
+            a.l1part[(size_t)mv * a.chunks + c] = t;
             __threadfence();
             const unsigned prev = atomicAdd(&a.mv_cnt[mv], 1u);
             s_last = prev == (unsigned)(a.chunks - 1);
@@ -536,7 +440,7 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
         if (s_last && tid == 0) {
             __threadfence();
             double L1 = 0.0;
-            for (int k = 0; k < a.chunks; ++k) L1 += __ldcg(a.l1s + (size_t)mv * a.strips + k);
+            for (int k = 0; k < a.chunks; ++k) L1 += __ldcg(a.l1part + (size_t)mv * a.chunks + k);
             SolveState s = st;
             s.iters += 1;
             s.change = L1;
@@ -564,14 +468,12 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
             a.glob[0] = 0u;
             a.glob[1] = n_act > 0 ? 1u : 0u;
             a.glob[2] = (unsigned)n_act;
-            a.glob[3] ^= 1u;
             if (a.use_handle) cudaGraphSetConditional(a.handle, n_act > 0 ? 1u : 0u);
         }
     }
 }
 
-// pi^0 = 1/N (y and gathered x in X[0]), state reset, counters zeroed, all matrices with a real vector
-// active.
+// pi^0 = 1/N (y and gathered x), state reset, counters zeroed, all matrices with a real vector active.
 __global__ void k_power_init(const PowerArgs a) {
     const int mv = blockIdx.y;
     const int m = mv / a.V, v = mv % a.V;
@@ -612,8 +514,6 @@ __global__ void k_power_init(const PowerArgs a) {
             a.glob[0] = 0u;
             a.glob[1] = n > 0 ? 1u : 0u;
             a.glob[2] = (unsigned)n;
-            a.glob[3] = 0u;              // X[0] holds pi^0
-            a.glob[4] = 0u;
         }
     }
 }
@@ -681,7 +581,7 @@ int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a) {
     out->init_fn = (void *)k_power_init;
     int cps = 2;
     out->step_fn = step_fn(dtype, V, &out->step_smem, &cps);
-    out->check_fn = (void *)k_power_check;   // fp32 storage only; fp64 checks inside k_power_step
+    out->check_fn = (void *)k_power_check;
     out->finish_fn = (void *)k_power_finish;
     if (!out->step_fn) return 1;
     const int gx = (a.N + 255) / 256 < 64 ? (a.N + 255) / 256 : 64;
