@@ -1,0 +1,76 @@
+"""Rewrites DESIGN.md §6's tables from the committed bench lines in profiles/r01/ (run after
+tools/gpu_bench_all.sh and copying its outputs)."""
+import json, os
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+def L(n): return json.load(open(os.path.join(ROOT, 'profiles', 'r01', f'{n}.json')))
+p = os.path.join(ROOT, 'DESIGN.md')
+s = open(p).read()
+i = s.index('**Headline (north-star dense path; default bench line')
+j = s.index('## 7. Multi-GPU')
+names = ['bench_c5', 'bench_c5_f32', 'bench_c5_exp', 'bench_c4', 'bench_c3', 'bench_c2', 'bench_c1', 'bench_ref_c5',
+         'bench_struct_c5', 'bench_struct_c3', 'bench_struct_c4', 'bench_struct_grid', 'bench_spec_grid', 'bench_spec_c5',
+         'bench_spec_c1', 'bench_eq4_c5', 'bench_eq4_c3', 'bench_mc_c1', 'bench_mc_grid']
+d = {n: L(n) for n in names}
+def dense_row(name, label):
+    x = d[name]; r = x['roofline']; b = x['roofline_build']
+    return (f"| {label} | {x['value']:.1f} | {x['ms_per_step']:.3f} | {b['achieved']:.0f} ({b['frac']:.3f}) | "
+            f"{r['achieved']:.0f} ({r['frac']:.3f}) | {x['e2e']['value']:.1f} | {x['clocks']['sm_mhz']:.0f} |")
+c5 = d['bench_c5']
+def g(n, k='value'): return d[n][k]
+def rf(n, k): return d[n]['roofline'][k]
+new = f'''**Headline (north-star dense path; default bench line, `profiles/r01/bench_c5.json`)** = c5 fp64, one
+step = build P~0 + the t_d = 430 solve + the 16-dead-time sweep on the same P~0, all 17 vectors in one
+multi-vector plan (max 40 iterations) = 17 stationary solves. Peak = MEASURED_PEAKS.json hbm_gbs of the
+pod ({rf('bench_c5','peak'):.1f} GB/s, a copy: read + write); a pure write stream (build) or read stream (GEMV)
+can exceed a copy by ~6% (probe: 6.86 / 6.95 TB/s), so fractions slightly above 1 mean "at the HBM limit".
+
+| workload | solves/s | ms/step | build GB/s (frac) | GEMV GB/s (frac) | e2e solves/s | SM MHz |
+|---|---|---|---|---|---|---|
+{dense_row('bench_c5','c5 fp64 (default)')}
+{dense_row('bench_c5_f32','c5 fp32 storage (17-vector sweep FP64-tensor-bound)')}
+{dense_row('bench_c5_exp','c5 fp64, exp entry mode')}
+{dense_row('bench_c4','c4 fp64')}
+{dense_row('bench_c3','c3 fp64 (64 items)')}
+{dense_row('bench_c2','c2 fp64 (6 items, L2-resident; fused solver, CUDA-graph step)')}
+{dense_row('bench_c1','c1 fp64 (L2-resident; fused solver, CUDA-graph step)')}
+
+Box to box the default line moved between 291 and 316 solves/s this round at identical code: the
+17-vector pass is at the DMMA / HBM balance point (ncu: tensor DMMA subpipe 74% busy, DRAM 80%), so it
+follows the power-capped SM clock, unlike a pure read stream. Before this round's small-N work c1 / c2 ran
+at 3321 / 12110 solves/s (0.30 / 0.50 ms per step). The c5 step is close to its floor: 40 passes x
+max(8.59 GB / 6.95 TB/s, 16 x 2 x N^2 flops / 37 TFLOP/s) = 40 x 1.24 ms = 49.4 ms of the
+{c5['ms_per_step']:.1f} ms step. The GEMV `achieved` divides algorithmic bytes (N^2 b per launch per active
+matrix) by the whole solve phase (GEMV + check kernels + graph overhead), a lower bound on the kernel's own
+rate; ncu: 8.656 GB DRAM read per 8.590 GB algorithmic (`traffic`), and the launch list of the default
+command (`profiles/r01/launches_c5_eager.csv`, eager mode, cold cache) gives `k_power_step<double, 17>`
+~96% of device time (1.27 ms per pass), `k_build` ~2.3%, `k_power_check` ~1.5%, the flux-vector kernels
+0.1%. Clocks under load: {c5['clocks']['sm_mhz']:.0f} MHz ({', '.join(c5['clocks']['reasons']) or 'no throttle'}).
+CPU baseline (the oracle as it stands, {c5['cpu_baseline']['cores']} host cores, {c5['cpu_baseline']['host']['cpu_model']}): {c5['cpu_baseline']['value']:.4f} solves/s on c5 (bounded
+sample, see the line's `cpu_baseline.sample`; one core builds {c5['cpu_baseline']['build_entries_per_s_one_core']:.3g} Eq. 4 entries/s, all cores
+{c5['cpu_baseline']['build_entries_per_s_all_cores']:.3g}); `--impl reference` (the same oracle as the reference arm): {g('bench_ref_c5'):.4f} solves/s.
+
+**§8(f) rows** (`bench.py --path structured|spectral|eq4|mc`; lines in `profiles/r01/bench_{{struct,spec,eq4,mc}}_*.json`):
+
+| row | workload | throughput | ms/step | dominant kernel vs roofline | oracle on the host |
+|---|---|---|---|---|---|
+| f2 structured solve | c5 (17 items, N = 32768) | {g('bench_struct_c5'):,.0f} solves/s (dense path: {c5['value']:.0f}) | {g('bench_struct_c5','ms_per_step'):.3f} | `k_struct_solve`, {rf('bench_struct_c5','achieved'):.2f} TFLOP/s ({rf('bench_struct_c5','frac'):.3f} of FP64): barrier-bound, 15 co-resident 8-CTA clusters | {d['bench_struct_c5']['cpu_baseline']['value']:.4f} solves/s |
+| f2 | c3 (64 items, N = 4096) | {g('bench_struct_c3'):,.0f} solves/s | {g('bench_struct_c3','ms_per_step'):.3f} | {rf('bench_struct_c3','achieved'):.2f} TFLOP/s ({rf('bench_struct_c3','frac'):.3f}) | {d['bench_struct_c3']['cpu_baseline']['value']:.2f} |
+| f2 | c4 (1 item, N = 16384) | {g('bench_struct_c4'):,.0f} solves/s (dense: {g('bench_c4'):.0f}) | {g('bench_struct_c4','ms_per_step'):.3f} | latency (one 4-CTA cluster) | {d['bench_struct_c4']['cpu_baseline']['value']:.3f} |
+| f2 | grid (8192 items, N = 256) | {g('bench_struct_grid')/1e6:.1f} M solves/s | {g('bench_struct_grid','ms_per_step'):.3f} | {rf('bench_struct_grid','achieved'):.2f} TFLOP/s ({rf('bench_struct_grid','frac'):.3f}) | {d['bench_struct_grid']['cpu_baseline']['value']:.0f} |
+| f1 spectral (pi + lambda_2) | grid | {g('bench_spec_grid')/1e6:.2f} M analyses/s | {g('bench_spec_grid','ms_per_step'):.2f} | `k_struct_lambda2`, {rf('bench_spec_grid','achieved'):.2f} TFLOP/s ({rf('bench_spec_grid','frac'):.3f}) | {d['bench_spec_grid']['cpu_baseline']['value']:.1f} (dense eigvals) |
+| f1 | c5 (17 items) | {g('bench_spec_c5'):,.0f} analyses/s | {g('bench_spec_c5','ms_per_step'):.2f} | {rf('bench_spec_c5','achieved'):.2f} TFLOP/s | — (no dense spectrum at N = 32768) |
+| f4 element-wise Eq. 4 | c5 (4 matrices of N = 32768, K = 2) | {g('bench_eq4_c5'):.3g} entries/s; Theorem 2 on the same GPU {d['bench_eq4_c5']['theorem2_same_gpu']['entries_per_s']:.3g} ({d['bench_eq4_c5']['theorem2_same_gpu']['speedup_vs_eq4']:.1f}x with the permutation materialised; ~28x with it folded) | {g('bench_eq4_c5','ms_per_step'):.1f} | `k_build_eq4`, {rf('bench_eq4_c5','achieved'):.1f} TFLOP/s ({rf('bench_eq4_c5','frac'):.2f}), FP64 pipe {rf('bench_eq4_c5','fp64_pipe_pct_ncu'):.0f}% | {d['bench_eq4_c5']['cpu_baseline']['value']:.3g} entries/s |
+| f4 | c3 (64 matrices of N = 4096, K = 1) | {g('bench_eq4_c3'):.3g} entries/s; Theorem 2: {d['bench_eq4_c3']['theorem2_same_gpu']['entries_per_s']:.3g} ({d['bench_eq4_c3']['theorem2_same_gpu']['speedup_vs_eq4']:.1f}x) | {g('bench_eq4_c3','ms_per_step'):.1f} | {rf('bench_eq4_c3','achieved'):.1f} TFLOP/s ({rf('bench_eq4_c3','frac'):.2f}) | {d['bench_eq4_c3']['cpu_baseline']['value']:.3g} |
+| f3 Monte Carlo | grid 16 x 16 x 2 items x 25 runs x 50,000 cycles (P:205), n_split {d['bench_mc_grid']['config']['n_split']} | {g('bench_mc_grid'):.3g} registrations/s | {g('bench_mc_grid','ms_per_step'):.0f} | `k_mc`, FP64 pipe {rf('bench_mc_grid','fp64_pipe_pct_ncu'):.0f}% ({rf('bench_mc_grid','achieved'):.2f} TFLOP/s counting DFMA/DADD/DMUL only) | {d['bench_mc_grid']['cpu_baseline']['value']:.3g} (1 core) |
+| f3 | c1, 100 runs x 50,000 cycles, 2^10 bins (P:202), n_split {d['bench_mc_c1']['config']['n_split']} | {g('bench_mc_c1'):.3g} registrations/s | {g('bench_mc_c1','ms_per_step'):.1f} | latency (1600 chains) | {d['bench_mc_c1']['cpu_baseline']['value']:.3g} |
+
+The paper's "1000x" (P:5, P:199) compares its vectorised construction with Rapp's element-wise one on
+unstated hardware. On one B200 the element-wise Eq. 4 build is FP64-bound at about half the pipe's peak
+and Theorem 2's build is HBM-bound, so the same-hardware ratio is 2.5-28x: the GPU parallelises the
+element-wise method too; Theorem 2's value on B200 is that the construction becomes a pure write stream
+and every dead time a free permutation (the 17-dead-time sweep reuses one P~0).
+
+'''
+s = s[:i] + new + s[j:]
+open(p, 'w').write(s)
+print("DESIGN §6 updated")
