@@ -71,9 +71,10 @@ static VecPtrs vec_ptrs(char *ws, const WsLayout &L) {
 }
 
 // Small host arrays reach the device as kernel parameters (async, stream-ordered, capturable;
-// no pageable-memcpy stream synchronisation).
+// no pageable-memcpy stream synchronisation). CUDA >= 12.1 allows 32764 bytes of parameters, so up to
+// 32000 bytes (e.g. 76 flux records) go in one launch.
 namespace {
-constexpr int kUpChunk = 3072;
+constexpr int kUpChunk = 32000;
 struct UpChunk {
     unsigned char data[kUpChunk];
     int n;
