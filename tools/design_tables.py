@@ -36,7 +36,11 @@ can exceed a copy by ~6% (probe: 6.86 / 6.95 TB/s), so fractions slightly above 
 
 Box to box the default line moved between 291 and 316 solves/s this round at identical code: the
 17-vector pass is at the DMMA / HBM balance point (ncu: tensor DMMA subpipe 74% busy, DRAM 80%), so it
-follows the power-capped SM clock, unlike a pure read stream. Before this round's small-N work c1 / c2 ran
+follows the power-capped SM clock, unlike a pure read stream: a sustained run takes ~1.38 ms per
+iteration (GEMV + check) against 1.27 ms for the GEMV replayed alone under ncu, and the eager host loop
+adds only 41 us per iteration to the graph (`tools/graph_overhead.py`), so the graph loop itself costs
+little. Moving 9 of the 17 vectors to plain DFMA (8 on DMMA) to unload the tensor pipe was measured
+and rejected: 1.68 ms per pass, issue-bound (FP64 pipe 33%, DMMA 29%). Before this round's small-N work c1 / c2 ran
 at 3321 / 12110 solves/s (0.30 / 0.50 ms per step). The c5 step is close to its floor: 40 passes x
 max(8.59 GB / 6.95 TB/s, 16 x 2 x N^2 flops / 37 TFLOP/s) = 40 x 1.24 ms = 49.4 ms of the
 {c5['ms_per_step']:.1f} ms step. The GEMV `achieved` divides algorithmic bytes (N^2 b per launch per active
