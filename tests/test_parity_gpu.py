@@ -427,3 +427,31 @@ def test_eager_mode_equals_graph(spl, monkeypatch, dtype, nv):
     assert torch.equal(g.pi, e.pi) and ig == ie
     g.close()
     e.close()
+
+
+def test_max_size_dense(spl):
+    """A matrix sized for the 180 GB of one B200: N = 110000 (ragged: not a multiple of 512), fp64,
+    96.8 GB. Sampled rows of J_l P~0 vs the oracle's Eq. 4 rows, all row sums, and pi vs the
+    long-double structured cross-check."""
+    N = 110000
+    ld = spl.leading_dim(N)
+    need = N * ld * 8
+    free, _ = torch.cuda.mem_get_info()
+    if free < need + (6 << 30):
+        pytest.skip(f"needs {need / 2**30:.0f} GiB free, have {free / 2**30:.0f}")
+    f = Flux(100.0, N, (37.0, 71.0), (0.4, 0.9), (2.0, 0.6), 0.8)
+    td = 142.5
+    P0 = spl.build_base(f)
+    l = oracle.shift_l(f, td)
+    rows = [0, N - 1, l, (N - l) % N, 54321]
+    want = sampled_rows(f, td, rows)
+    got = np.stack([_np(P0[(r + l) % N]) for r in rows])
+    assert np.max(np.abs(got - want)) <= TOL_E64
+    rs = _np(P0.sum(dim=1, dtype=torch.float64))
+    assert np.max(np.abs(rs - 1.0)) <= TOL_ROW
+    pi, info = spl.stationary(P0, f.t_r, td)
+    assert info["converged"]
+    ref, _ = structured_pi(f, td)
+    assert np.sum(np.abs(_np(pi) - ref)) <= TOL_PI64
+    del P0
+    torch.cuda.empty_cache()
