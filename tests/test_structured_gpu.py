@@ -331,3 +331,21 @@ def test_mixing_steps_cluster_team(spl):
             if 0.5 * np.abs(v - pi_np).sum() <= 1e-3:
                 break
         assert per[i] == n, i
+
+
+@pytest.mark.parametrize("N", [255, 256, 257, 4095, 4096, 4097, 8191, 8192, 8193, 12289])
+def test_team_boundaries(spl, N):
+    """Each side of every team-shape boundary (warp <= 256 < CTA <= 4096 < cluster; cluster size steps
+    every 4096 bins): the structured pi equals the dense GEMV path's pi, and lambda_2 the oracle's."""
+    f = random_flux(np.random.default_rng(N), N, 2)
+    td = float(np.random.default_rng(N + 1).uniform(0.0, 3.0 * f.t_r))
+    pi_s, info_s = _one(spl, f, td)
+    P0 = spl.build_base(f)
+    pi_d, info_d = spl.stationary(P0, f.t_r, td)
+    assert info_s["converged"] and abs(int(info_s["iters"]) - info_d["iters"]) <= 1
+    assert np.sum(np.abs(_np(pi_s) - _np(pi_d))) <= 1e-13
+    del P0
+    if N <= 4097:
+        got = _lambda2(spl, f, td, pi_s)
+        want = oracle.second_eigenvalue(oracle.build_eq4(f, td))
+        assert got["converged"] and abs(got["modulus"] - abs(want)) <= 1e-8
