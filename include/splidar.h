@@ -236,6 +236,21 @@ splidar_status splidar_second_eigenvalue(const splidar_flux *shape, int32_t n_it
                                          int32_t max_iter, void *ws, size_t ws_bytes, splidar_spectral_info *info,
                                          void *stream);
 
+/* f1 on a STORED matrix (any row-stochastic P0 in HBM, fp64 or fp32: splidar_build_base's P~0,
+ * splidar_build_eq4's matrix, or a user's): the second eigenvalue of P~ = J_l P0, l from t_r, t_d as in
+ * splidar_shift (Thm 2; t_d = 0 gives P~ = P0), by the same deflated 2-D subspace iteration as
+ * splidar_second_eigenvalue, each product y = q^T P~ being one pass of the multi-vector GEMV over P0
+ * (two vectors, dead time folded into the gathered x). pi: device fp64 [N], the stationary vector of
+ * P~ (e.g. from splidar_stationary; sum 1, accurate to << tol). info: host, may be NULL. The stored
+ * matrix is read, never written. max_iter >= 2; SPLIDAR_ENOCONV if the Ritz value still moved by tol
+ * or more after max_iter products. Workspace: splidar_spectral_dense_workspace_bytes(N), 256-aligned.
+ * Synchronises `stream`. */
+size_t splidar_spectral_dense_workspace_bytes(int32_t n_bins);
+splidar_status splidar_second_eigenvalue_dense(const void *P0, int32_t n_bins, int64_t ld, splidar_dtype dt,
+                                               double t_r, double t_d, const double *pi, double tol,
+                                               int32_t max_iter, void *ws, size_t ws_bytes,
+                                               splidar_spectral_info *info, void *stream);
+
 /* Structured plans: the items of splidar_stationary_structured (kind SPLIDAR_SPLAN_SOLVE) or
  * splidar_second_eigenvalue (kind SPLIDAR_SPLAN_LAMBDA2; pi is then the input) validated and uploaded
  * once; splidar_splan_launch only enqueues (step-1 vectors + the kernel, async, re-runnable);

@@ -10,6 +10,7 @@ from .splidar import (  # noqa: F401
     ENOCONV, EINVAL, ENOSPACE, ECUDA, EZEROROW, OK, F32, F64, LIB_PATH, Plan, SolveInfo, SplidarError,
     apply_deadtime, build_base, build_base_batched, build_info, empty_matrix, flux_vectors, leading_dim,
     lib_path, shift, solve_host, stationary, sweep, workspace, workspace_bytes,
-    SpectralInfo, bin_trajectory, flux_items, mixing_steps, second_eigenvalue, stationary_structured,
+    SpectralInfo, bin_trajectory, flux_items, mixing_steps, second_eigenvalue, second_eigenvalue_dense,
+    stationary_structured,
     structured_workspace, StructPlan, build_eq4, monte_carlo, lambda2_of,
 )

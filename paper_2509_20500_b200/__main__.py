@@ -92,8 +92,12 @@ def main(argv=None) -> int:
                    "converged": bool(info["converged"]), "l1_change": float(info["l1_change"]), "path": a.path,
                    "pi": pi[0].cpu().tolist()}
             if a.spectral and status == EXIT_OK:
-                shape, S, B = spl.flux_items(f)
-                l2 = spl.second_eigenvalue(shape, S, B, [a.t_d], pi.contiguous(), check=False)[0]
+                if a.path == "dense":   # on the stored matrix (two-vector GEMV products)
+                    l2 = spl.second_eigenvalue_dense(P0, f.t_r, a.t_d, pi[0].contiguous(), check=False)
+                    l2 = dict(l2, lambda2_re=l2["lambda2"].real, lambda2_im=l2["lambda2"].imag)
+                else:
+                    shape, S, B = spl.flux_items(f)
+                    l2 = spl.second_eigenvalue(shape, S, B, [a.t_d], pi.contiguous(), check=False)[0]
                 out["lambda2"] = {"re": float(l2["lambda2_re"]), "im": float(l2["lambda2_im"]),
                                   "modulus": float(l2["modulus"]), "phase": float(l2["phase"]),
                                   "gap": float(l2["gap"]), "converged": bool(l2["converged"])}

@@ -577,6 +577,161 @@ splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, sp
     return st;
 }
 
+// ------------------------------------------------ f1 on a stored matrix (spectral_dense.cu) ---
+
+static size_t sd_extra(int N, size_t *o_part, size_t *o_qsum, size_t *o_state, size_t *o_cnt) {
+    size_t o = 0;
+    *o_part = o; o = a256(o + sizeof(double) * (size_t)sd_chunks(N) * kSdDotsPerChunk);
+    *o_qsum = o; o = a256(o + sizeof(double) * 2 * (size_t)sd_update_ctas(N));
+    *o_state = o; o = a256(o + sizeof(SdState));
+    *o_cnt = o; o = a256(o + sizeof(unsigned) * 4);
+    return o;
+}
+
+size_t splidar_spectral_dense_workspace_bytes(int32_t n_bins) {
+    if (n_bins < 2) return 0;
+    size_t a, b, c, d;
+    return ws_layout(n_bins, 1, 2).total + sd_extra(n_bins, &a, &b, &c, &d);
+}
+
+splidar_status splidar_second_eigenvalue_dense(const void *P0, int32_t n_bins, int64_t ld, splidar_dtype dt,
+                                               double t_r, double t_d, const double *pi, double tol,
+                                               int32_t max_iter, void *ws, size_t ws_bytes,
+                                               splidar_spectral_info *info, void *stream) {
+    splidar_status st;
+    if (n_bins < 2 || !pi) return SPLIDAR_EINVAL;
+    if ((st = check_matrix(P0, n_bins, ld, dt))) return st;
+    if (!(tol > 0.0) || !std::isfinite(tol) || max_iter < 2) return SPLIDAR_EINVAL;
+    int32_t l;
+    if ((st = splidar_shift(t_r, n_bins, t_d, &l))) return st;
+    const int N = n_bins;
+    const WsLayout L = ws_layout(N, 1, 2);
+    size_t o_part, o_qsum, o_state, o_cnt;
+    const size_t extra = sd_extra(N, &o_part, &o_qsum, &o_state, &o_cnt);
+    if (!ws || ((uintptr_t)ws & 255u) != 0 || ws_bytes < L.total + extra) return SPLIDAR_ENOSPACE;
+    char *wsb = static_cast<char *>(ws);
+    cudaStream_t s = (cudaStream_t)stream;
+
+    SdArgs a;
+    memset(&a, 0, sizeof(a));
+    PowerArgs &p = a.p;
+    p.P = P0;
+    p.ld = ld;
+    p.mstride = (int64_t)N * ld;
+    p.N = N;
+    p.M = 1;
+    p.V = L.V;
+    p.strips = L.strips;
+    p.chunks = L.chunks;
+    p.xstride = L.xstride;
+    p.y = reinterpret_cast<double *>(wsb + L.y);
+    p.X = reinterpret_cast<double *>(wsb + L.X);
+    p.part = reinterpret_cast<double *>(wsb + L.part);
+    p.ssum = reinterpret_cast<double *>(wsb + L.ssum);
+    p.l1part = reinterpret_cast<double *>(wsb + L.l1part);
+    p.st = reinterpret_cast<SolveState *>(wsb + L.state);
+    p.lsh = reinterpret_cast<const int *>(wsb + L.lsh);
+    p.strip_cnt = reinterpret_cast<unsigned *>(wsb + L.strip_cnt);
+    p.mv_cnt = reinterpret_cast<unsigned *>(wsb + L.mv_cnt);
+    p.act = reinterpret_cast<int *>(wsb + L.act);
+    p.glob = reinterpret_cast<unsigned *>(wsb + L.glob);
+    p.tol = tol;
+    p.max_iter = max_iter;
+    a.l = l;
+    a.pi = pi;
+    a.part = reinterpret_cast<double *>(wsb + L.total + o_part);
+    a.qsum = reinterpret_cast<double *>(wsb + L.total + o_qsum);
+    a.nq = sd_update_ctas(N);
+    a.sd = reinterpret_cast<SdState *>(wsb + L.total + o_state);
+    a.cnt = reinterpret_cast<unsigned *>(wsb + L.total + o_cnt);
+    a.tol = tol;
+    a.max_iter = max_iter;
+
+    SolverKernels k;
+    if (solver_kernels(dt, 2, &k, p)) return SPLIDAR_EINVAL;
+    SdKernels q;
+    sd_kernels(&q, N);
+    const char *e = getenv("SPLIDAR_EAGER");
+    if (e && e[0] == '1') {   // host loop (profilers); control only, every step runs in the kernels
+        SdArgs ea = a;
+        ea.use_handle = 0;
+        void *args[] = {&ea};
+        void *pargs[] = {&ea.p};
+        SPL_CUDA(cudaLaunchKernel(q.init_fn, dim3(1), q.block, args, 0, s));
+        SdState h;
+        for (int it = 0; it < max_iter; ++it) {
+            SPL_CUDA(cudaLaunchKernel(k.step_fn, k.step_grid, k.step_block, pargs, k.step_smem, s));
+            SPL_CUDA(cudaLaunchKernel(q.dots_fn, q.dots_grid, q.block, args, 0, s));
+            SPL_CUDA(cudaLaunchKernel(q.update_fn, q.update_grid, q.block, args, 0, s));
+            SPL_CUDA(cudaMemcpyAsync(&h, a.sd, sizeof(h), cudaMemcpyDeviceToHost, s));
+            SPL_CUDA(cudaStreamSynchronize(s));
+            if (h.done) break;
+        }
+    } else {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t x = nullptr;
+        cudaError_t err = cudaSuccess;
+        do {
+            if ((err = cudaGraphCreate(&g, 0))) break;
+            cudaGraphConditionalHandle h;
+            if ((err = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault))) break;
+            a.use_handle = 1;
+            a.handle = h;
+            cudaKernelNodeParams kp;
+            memset(&kp, 0, sizeof(kp));
+            void *args[] = {&a};
+            void *pargs[] = {&a.p};
+            cudaGraphNode_t n_init, n_while, n_step, n_dots, n_upd;
+            kp.func = q.init_fn;
+            kp.gridDim = dim3(1);
+            kp.blockDim = q.block;
+            kp.kernelParams = args;
+            if ((err = cudaGraphAddKernelNode(&n_init, g, nullptr, 0, &kp))) break;
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            if ((err = cudaGraphAddNode(&n_while, g, &n_init, 1, &cp))) break;
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            kp.func = k.step_fn;
+            kp.gridDim = k.step_grid;
+            kp.blockDim = k.step_block;
+            kp.sharedMemBytes = k.step_smem;
+            kp.kernelParams = pargs;
+            if ((err = cudaGraphAddKernelNode(&n_step, body, nullptr, 0, &kp))) break;
+            kp.func = q.dots_fn;
+            kp.gridDim = q.dots_grid;
+            kp.blockDim = q.block;
+            kp.sharedMemBytes = 0;
+            kp.kernelParams = args;
+            if ((err = cudaGraphAddKernelNode(&n_dots, body, &n_step, 1, &kp))) break;
+            kp.func = q.update_fn;
+            kp.gridDim = q.update_grid;
+            if ((err = cudaGraphAddKernelNode(&n_upd, body, &n_dots, 1, &kp))) break;
+            if ((err = cudaGraphInstantiate(&x, g, 0))) break;
+            if (!(err = cudaGraphLaunch(x, s))) err = cudaStreamSynchronize(s);   // before destroying
+        } while (0);
+        if (x) cudaGraphExecDestroy(x);
+        if (g) cudaGraphDestroy(g);
+        SPL_CUDA(err);
+    }
+    SdState h;
+    SPL_CUDA(cudaMemcpyAsync(&h, a.sd, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SPL_CUDA(cudaStreamSynchronize(s));
+    if (info) {
+        info->lambda2_re = h.mu_re;
+        info->lambda2_im = h.mu_im;
+        info->modulus = std::hypot(h.mu_re, h.mu_im);
+        info->phase = std::atan2(h.mu_im, h.mu_re);
+        info->gap = 1.0 - info->modulus;
+        info->change = h.dmu;
+        info->iters = h.iters;
+        info->converged = h.converged;
+    }
+    return h.converged ? SPLIDAR_OK : SPLIDAR_ENOCONV;
+}
+
 // ---------------------------------------------------------------- sweep ----------------------
 
 splidar_status splidar_sweep(const splidar_flux *shape, int32_t n_items, const double *S, const double *B,

@@ -155,6 +155,36 @@ int fused_shape(int N, int *C, int *R);
 int fused_resident(int N, int R, int dtype);
 cudaError_t launch_fused(int dtype, const FusedArgs &a, cudaStream_t s);
 
+// ---- second eigenvalue of a stored matrix (spectral_dense.cu; SURVEY §8(f) f1 on K6) -----------
+struct SdState {
+    double sig_w[2];            // the sigma the last w were formed with (update kernel)
+    double al, be, ga;          // q1' = al w1, q2' = be (w2 - ga w1)
+    double mu_re, mu_im, dmu;   // dominant Ritz value of the deflated operator, its last move
+    int iters, converged, done, pad;
+};
+struct SdArgs {
+    PowerArgs p;                // the GEMV's arguments (M = 1, V = 2; y buffer 0 holds q, 1 gets q P~)
+    int l;                      // row shift of P~ = J_l P0
+    const double *pi;           // [N]
+    double *part;               // [chunks][10]
+    double *qsum;               // [2][nq] per-CTA partial sums of the stored basis q_a
+    int nq;                     // = sd_update_ctas(N)
+    SdState *sd;
+    unsigned *cnt;
+    double tol;
+    int max_iter;
+    int use_handle;
+    cudaGraphConditionalHandle handle;
+};
+struct SdKernels {
+    void *init_fn, *dots_fn, *update_fn;
+    dim3 block, dots_grid, update_grid;
+};
+int sd_chunks(int N);
+int sd_update_ctas(int N);
+constexpr int kSdDotsPerChunk = 10;
+void sd_kernels(SdKernels *k, int N);
+
 // ---- Monte Carlo of the detection process (mc.cu) ------------------------------
 struct McArgs {
     const FluxDev *flux;        // [profiles]

@@ -94,6 +94,9 @@ def _lib():
             "splidar_structured_workspace_bytes": (sz, [i32, i32, i32]),
             "splidar_stationary_structured": (st, [fp, i32, p, p, p, d, i32, p, p, sz, pinfo, p]),
             "splidar_second_eigenvalue": (st, [fp, i32, p, p, p, p, d, i32, p, sz, C.POINTER(SpectralInfo), p]),
+            "splidar_spectral_dense_workspace_bytes": (sz, [i32]),
+            "splidar_second_eigenvalue_dense": (st, [p, i32, i64, st, d, d, p, d, i32, p, sz,
+                                                     C.POINTER(SpectralInfo), p]),
             "splidar_mixing_steps": (st, [fp, d, p, d, i32, p, C.POINTER(i32), p, sz, p]),
             "splidar_bin_trajectory": (st, [fp, d, p, i32, i32, p, p, p, sz, p]),
             "splidar_splan_create": (st, [C.POINTER(p), i32, fp, i32, p, p, p, d, i32, p, p, sz, p]),
@@ -442,6 +445,28 @@ def second_eigenvalue(shape, S, B, t_d, pi: torch.Tensor, tol: float = 1e-13, ma
                                           infos, _stream(stream))
     _check(st, "splidar_second_eigenvalue", allow=() if check else (ENOCONV,))
     return _records(infos)
+
+
+def second_eigenvalue_dense(P0: torch.Tensor, t_r: float, t_d: float, pi: torch.Tensor, tol: float = 1e-13,
+                            max_iter: int = 10 ** 5, ws: torch.Tensor | None = None, stream=None,
+                            check: bool = True) -> dict:
+    """f1 on a stored matrix: lambda_2 of P~ = J_l P0 (any row-stochastic P0 [N, >= N] fp64/fp32 on the
+    device, l from (t_r, t_d)); pi = the stationary vector of P~ [N] fp64 on the device. Every product
+    is a pass of the multi-vector GEMV over P0. Returns a dict with the fields of SpectralInfo."""
+    ptr, n, ld, dt = _matrix_args(P0)
+    if not pi.is_cuda or pi.dtype != torch.float64 or pi.numel() != n or not pi.is_contiguous():
+        raise SplidarError(EINVAL, "second_eigenvalue_dense: pi must be a contiguous CUDA fp64 [N] tensor")
+    if ws is None:
+        nb = _lib().splidar_spectral_dense_workspace_bytes(n)
+        t = torch.empty(nb + 256, dtype=torch.uint8, device=P0.device)
+        off = (-t.data_ptr()) % 256
+        ws = t[off:off + nb]
+    info = SpectralInfo()
+    st = _lib().splidar_second_eigenvalue_dense(ptr, n, ld, dt, float(t_r), float(t_d), pi.data_ptr(), float(tol),
+                                                int(max_iter), ws.data_ptr(), ws.numel(), C.byref(info),
+                                                _stream(stream))
+    _check(st, "splidar_second_eigenvalue_dense", allow=() if check else (ENOCONV,))
+    return info.as_dict()
 
 
 def mixing_steps(flux, t_d: float, pi: torch.Tensor, eps: float = 1e-3, max_steps: int = 10 ** 5,

@@ -179,6 +179,33 @@ def test_stationary_rejects(spl):
     assert call(ld=100) == spl.ENOSPACE
 
 
+def test_second_eigenvalue_dense_rejects(spl):
+    lib = spl._lib()
+    info = spl.SpectralInfo()
+    wsb = lib.splidar_spectral_dense_workspace_bytes(256)
+    assert wsb >= spl.workspace_bytes(256, 1, 2) and lib.splidar_spectral_dense_workspace_bytes(1) == 0
+    args = dict(P0=FAKE, n=256, ld=256, dt=spl.F64, t_r=100.0, t_d=75.0, pi=FAKE, tol=1e-13, it=100, ws=FAKE,
+                wsb=wsb)
+
+    def call(**kw):
+        a = dict(args)
+        a.update(kw)
+        return lib.splidar_second_eigenvalue_dense(a["P0"], a["n"], a["ld"], a["dt"], a["t_r"], a["t_d"], a["pi"],
+                                                   a["tol"], a["it"], a["ws"], a["wsb"], C.byref(info), None)
+    assert call(n=1) == spl.EINVAL
+    assert call(pi=None) == spl.EINVAL
+    assert call(P0=None) == spl.EINVAL
+    assert call(dt=7) == spl.EINVAL
+    assert call(tol=0.0) == spl.EINVAL
+    assert call(tol=math.inf) == spl.EINVAL
+    assert call(it=1) == spl.EINVAL
+    assert call(t_d=-1.0) == spl.EINVAL
+    assert call(t_r=0.0) == spl.EINVAL
+    assert call(ld=255) == spl.ENOSPACE
+    assert call(wsb=wsb - 1) == spl.ENOSPACE
+    assert call(ws=FAKE + 8) == spl.ENOSPACE
+
+
 def test_sweep_rejects(spl):
     lib = spl._lib()
     fa = _flux_struct(spl)
