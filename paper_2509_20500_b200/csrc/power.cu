@@ -407,9 +407,12 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
     const SolveState st = a.st[mv];
     if (!st.done) {
         const int m = mv / a.V, v = mv % a.V;
+        // s = the strip sums added by every warp in the same fixed order (lane-strided, xor tree), so
+        // all CTAs of (matrix, vector) hold the bitwise-same s
         double S = 0.0;
         const double *ss = a.ssum + (size_t)mv * a.strips;
-        for (int k = 0; k < a.strips; ++k) S += __ldcg(ss + k);
+        for (int k = tid & 31; k < a.strips; k += 32) S += __ldcg(ss + k);
+        S = warp_sum(S);
         const double inv_new = 1.0 / S, inv_old = 1.0 / st.s;
         const double *yn = a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
         const double *yo = a.y + ((size_t)mv * 2 + st.cur) * N;
@@ -437,38 +440,50 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
             s_last = prev == (unsigned)(a.chunks - 1);
         }
         __syncthreads();
-        if (s_last && tid == 0) {
+        if (s_last && tid < 32) {   // the last CTA: chunk partials added lane-strided, fixed xor tree
             __threadfence();
             double L1 = 0.0;
-            for (int k = 0; k < a.chunks; ++k) L1 += __ldcg(a.l1part + (size_t)mv * a.chunks + k);
-            SolveState s = st;
-            s.iters += 1;
-            s.change = L1;
-            s.s = S;
-            s.cur ^= 1;
-            if (L1 < a.tol) { s.converged = 1; s.done = 1; }
-            else if (s.iters >= a.max_iter || !(S > 0.0) || !isfinite(L1)) { s.done = 1; }
-            a.st[mv] = s;
-            a.mv_cnt[mv] = 0u;
-            __threadfence();
+            for (int k = tid; k < a.chunks; k += 32) L1 += __ldcg(a.l1part + (size_t)mv * a.chunks + k);
+            L1 = warp_sum(L1);
+            if (tid == 0) {
+                SolveState s = st;
+                s.iters += 1;
+                s.change = L1;
+                s.s = S;
+                s.cur ^= 1;
+                if (L1 < a.tol) { s.converged = 1; s.done = 1; }
+                else if (s.iters >= a.max_iter || !(S > 0.0) || !isfinite(L1)) { s.done = 1; }
+                a.st[mv] = s;
+                a.mv_cnt[mv] = 0u;
+                __threadfence();
+            }
         }
     }
-    if (tid == 0) {
-        __threadfence();
-        const unsigned total = gridDim.x * gridDim.y;
-        const unsigned prev = atomicAdd(&a.glob[0], 1u);
-        if (prev == total - 1) {
+    if (tid < 32) {   // the last CTA of the grid: active-matrix list (warp 0, 32 matrices per ballot)
+        unsigned prev = 0;
+        if (tid == 0) {
+            __threadfence();
+            prev = atomicAdd(&a.glob[0], 1u);
+        }
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == gridDim.x * gridDim.y - 1) {
             __threadfence();
             int n_act = 0;
-            for (int m = 0; m < a.M; ++m) {
+            for (int m0 = 0; m0 < a.M; m0 += 32) {
+                const int m = m0 + tid;
                 int any = 0;
-                for (int v = 0; v < a.V; ++v) any |= !__ldcg(&a.st[(size_t)m * a.V + v].done);
-                if (any) a.act[n_act++] = m;
+                if (m < a.M)
+                    for (int v = 0; v < a.V; ++v) any |= !__ldcg(&a.st[(size_t)m * a.V + v].done);
+                const unsigned b = __ballot_sync(0xffffffffu, any);
+                if (any) a.act[n_act + __popc(b & ((1u << tid) - 1u))] = m;
+                n_act += __popc(b);
             }
-            a.glob[0] = 0u;
-            a.glob[1] = n_act > 0 ? 1u : 0u;
-            a.glob[2] = (unsigned)n_act;
-            if (a.use_handle) cudaGraphSetConditional(a.handle, n_act > 0 ? 1u : 0u);
+            if (tid == 0) {
+                a.glob[0] = 0u;
+                a.glob[1] = n_act > 0 ? 1u : 0u;
+                a.glob[2] = (unsigned)n_act;
+                if (a.use_handle) cudaGraphSetConditional(a.handle, n_act > 0 ? 1u : 0u);
+            }
         }
     }
 }

@@ -26,7 +26,7 @@ namespace spl {
 namespace {
 
 constexpr int kSdT = 256;
-constexpr int kSdChunk = 4096;
+constexpr int kSdChunk = 512;     // 64 CTAs at N = 32768 (4096: 8 CTAs, 17.7 us per launch)
 constexpr int kSdDots = kSdDotsPerChunk;
 
 __device__ __forceinline__ double sd_hash(uint32_t j, uint32_t salt) {   // deterministic in [-1, 1)
@@ -147,14 +147,22 @@ __global__ void __launch_bounds__(kSdT) k_sd_dots(const SdArgs s) {
         s_last = atomicAdd(s.cnt, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
+    if (!s_last) return;
     __threadfence();
+    {   // the last CTA: dot k summed over the chunks by warp k % 8 (lanes strided, then a fixed tree)
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (int k = warp; k < kSdDots; k += kSdT / 32) {
+            double t = 0.0;
+            for (int cc = lane; cc < (int)gridDim.x; cc += 32) t += __ldcg(s.part + (size_t)cc * kSdDots + k);
+            t = sd_warp_sum(t);
+            if (lane == 0) red[k][0] = t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
     double h[kSdDots];
 #pragma unroll
-    for (int k = 0; k < kSdDots; ++k) h[k] = 0.0;
-    for (int cc = 0; cc < (int)gridDim.x; ++cc)
-#pragma unroll
-        for (int k = 0; k < kSdDots; ++k) h[k] += __ldcg(s.part + (size_t)cc * kSdDots + k);
+    for (int k = 0; k < kSdDots; ++k) h[k] = red[k][0];
     SdState n = st;
     n.iters += 1;
     // Ritz values: H = M G^{-1}, M = W Q^T = [[h11, h12], [h21, h22]], G = Q Q^T

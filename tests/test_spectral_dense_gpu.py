@@ -109,7 +109,7 @@ def test_dense_lambda2_circulant_closed_form(spl, B, N, td):
 
 @pytest.mark.parametrize("k", [4, 5])
 def test_dense_equals_structured_large(spl, k):
-    """N = 16384 / 32768 (configs 4, 5; 4 / 8 dots chunks, ragged GEMV pieces): the stored-matrix
+    """N = 16384 / 32768 (configs 4, 5; 32 / 64 dots chunks, ragged GEMV pieces): the stored-matrix
     lambda_2 equals the structured kernel's to far below the paper's reported precision."""
     it = config(k).items[0]
     f = it.flux
@@ -122,7 +122,7 @@ def test_dense_equals_structured_large(spl, k):
 
 
 def test_dense_ragged_multi_chunk(spl):
-    """N = 9001 (3 dots chunks, last one ragged; 18 GEMV strips, last ragged) vs structured."""
+    """N = 9001 (18 dots chunks and 18 GEMV strips, the last of each ragged) vs structured."""
     rng = np.random.default_rng(5)
     f = Flux(100.0, 9001, (40.0, 63.0), (0.5, 1.5), (0.8, 0.4), 0.6)
     td = float(rng.uniform(0, 300))
