@@ -291,6 +291,33 @@ __device__ __forceinline__ void push(Team<MODE> &tm, double *xbuf, const Pos<MOD
     }
 }
 
+// Cluster push through a staging buffer: the warp's 32 E consecutive y values are written to its
+// slice of ybuf (blocked, as held), then read back lane-contiguous, so every remote store instruction
+// of the warp writes 32 consecutive positions of the destination (the blocked layout scattered each
+// store over 32 lines of DSMEM; DSMEM moves ~20 B/clk per SM).
+template <int E>
+__device__ __forceinline__ void push_cl(Team<kCluster> &tm, double *xbuf, double *ybuf, const Pos<kCluster, E> &P,
+                                        const double (&y)[E]) {
+    const int chunk = (int)blockDim.x * E;
+    const int lane = threadIdx.x & 31, wbase = (int)(threadIdx.x & ~31u) * E;
+#pragma unroll
+    for (int e = 0; e < E; ++e) ybuf[P.loc(e)] = y[e];
+    __syncwarp();
+    const int cbase = tm.c * chunk;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const int q = wbase + k * 32 + lane;
+        const int p = cbase + q;
+        if (p < P.N) {
+            int r = p + P.l;
+            if (r >= P.N) r -= P.N;
+            const int dst = r / chunk;
+            tm.cl.map_shared_rank(xbuf, dst)[sidx<E>(r - dst * chunk)] = ybuf[sidx<E>(q)];
+        }
+    }
+    __syncwarp();   // the slice may be restaged at once (two vectors per product)
+}
+
 // stage the thread's E values of src (global) in shared memory at its padded local indices
 template <int MODE, int E>
 __device__ __forceinline__ void stage(double *dst, const double *src, const Pos<MODE, E> &P) {
@@ -379,7 +406,8 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
             d += fabs(v[0][e] - yp[e]);
             yp[e] = v[0][e];
         }
-        push<MODE, E>(tm, xbuf, P, v[0]);
+        if constexpr (MODE == kCluster && REG) push_cl<E>(tm, xbuf, ws, P, v[0]);   // ws is free at E = 8
+        else push<MODE, E>(tm, xbuf, P, v[0]);
         d = warp_allsum(d);
         if ((threadIdx.x & 31) == 0) dwarp[threadIdx.x >> 5] = d;
         tm.barrier();   // pushes complete (and dwarp written) before the next product reads them
@@ -520,8 +548,13 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
             wn[0][e] = y0;
             wn[1][e] = y1;
         }
-        push<MODE, E>(tm, xb0, P, wn[0]);
-        push<MODE, E>(tm, xb1, P, wn[1]);
+        if constexpr (MODE == kCluster) {            // staging buffer: the 6th (cluster launches only)
+            push_cl<E>(tm, xb0, xbuf + 5 * xs, P, wn[0]);
+            push_cl<E>(tm, xb1, xbuf + 5 * xs, P, wn[1]);
+        } else {
+            push<MODE, E>(tm, xb0, P, wn[0]);
+            push<MODE, E>(tm, xb1, P, wn[1]);
+        }
         double h[7];
         if constexpr (MODE == kCluster) {
             tm.template sum<7>(hp);
@@ -639,7 +672,8 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a)
             v[0][e] = P.valid(e) ? ws[P.loc(e)] * (Cj + eL * (T - Cj)) : 0.0;
             tv += fabs(v[0][e] - pis[P.loc(e)]);
         }
-        push<MODE, E>(tm, xbuf, P, v[0]);
+        if constexpr (MODE == kCluster) push_cl<E>(tm, xbuf, xbuf + 4 * xs, P, v[0]);   // 5th buffer (cluster)
+        else push<MODE, E>(tm, xbuf, P, v[0]);
         tv = warp_allsum(tv);
         if ((threadIdx.x & 31) == 0) twarp[threadIdx.x >> 5] = tv;
         tm.barrier();
@@ -767,17 +801,18 @@ int struct_shape(int N, int *C, int *threads) {
     return shape_for(N, 8, C, threads);
 }
 
-#define SPL_TEAM_LAUNCH(KERNEL, EC, NBUF)                                                       \
-    (a.N > kSChunkB ? launch_team(KERNEL<kCluster, EC>, a, n_units, EC, NBUF, s)                \
+// NBUF_CL: shared-memory vectors of the cluster variant (+1 staging buffer for push_cl)
+#define SPL_TEAM_LAUNCH(KERNEL, EC, NBUF, NBUF_CL)                                              \
+    (a.N > kSChunkB ? launch_team(KERNEL<kCluster, EC>, a, n_units, EC, NBUF_CL, s)             \
                     : (a.N <= 256 ? launch_team(KERNEL<kWarp, 8>, a, n_units, 8, NBUF, s)       \
                                   : launch_team(KERNEL<kBlock, 8>, a, n_units, 8, NBUF, s)))
 
 cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s) {
     switch (kind) {
-        case kStructSolve: return SPL_TEAM_LAUNCH(k_struct_solve, 8, 3);
-        case kStructLambda2: return SPL_TEAM_LAUNCH(k_struct_lambda2, 8, 5);
-        case kStructMixing: return SPL_TEAM_LAUNCH(k_struct_mixing, 8, 4);     // 4 vectors: 147 KB at E = 8
-        case kStructTraj: n_units = 1; return SPL_TEAM_LAUNCH(k_struct_traj, 16, 3);
+        case kStructSolve: return SPL_TEAM_LAUNCH(k_struct_solve, 8, 3, 3);       // stages in the free w slot
+        case kStructLambda2: return SPL_TEAM_LAUNCH(k_struct_lambda2, 8, 5, 6);   // 221 KB at E = 8
+        case kStructMixing: return SPL_TEAM_LAUNCH(k_struct_mixing, 8, 4, 5);     // 184 KB at E = 8
+        case kStructTraj: n_units = 1; return SPL_TEAM_LAUNCH(k_struct_traj, 16, 3, 3);
     }
     return cudaErrorInvalidValue;
 }
