@@ -26,6 +26,7 @@
 // are formed by shuffles, never by subtraction.
 #include <cooperative_groups.h>
 
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
     const int m = a.prof[item], l = a.lsh[item];
     const Pos<MODE, E> P(a.N, tm.c, l);
     // w and 1/D: registers at E = 8 (measured faster), shared memory at E = 16
-    constexpr bool REG = E == 8;
+    constexpr bool REG = E <= 8;
     const int xs = xsize<E>(blockDim.x);
     double *ws = xbuf + xs, *ids = xbuf + 2 * xs;
     double wr[REG ? E : 1], idr[REG ? E : 1];
@@ -793,6 +794,46 @@ cudaError_t launch_team(K kernel, StructArgs a, int n_units, int E, int nbuf, cu
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
+// Clusters of C CTAs x T threads with `smem` dynamic bytes resident at once (cached per kernel, C).
+int resident_clusters(const void *fn, int C, int T, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_pair(fn, C);
+    const auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)C);
+    cfg.blockDim = dim3((unsigned)T);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        n = 0;
+    }
+    cache[key] = n;
+    return n;
+}
+
+// Team width: 4 bins per thread (clusters of twice as many CTAs, half the DSMEM bytes per SM per
+// product: c4's single item -15%) when every item's cluster is resident at once; else 8 (c5's 17
+// items: two waves of 8-CTA clusters beat two of 16-CTA ones, 0.223 vs 0.356 ms).
+bool one_wave_at_e4(const void *fn, int N, int n_units, int nbuf) {
+    int C, T;
+    if (shape_for(N, 4, &C, &T) || C < 2) return false;
+    const size_t smem = sizeof(double) * (size_t)nbuf * (T * 4 + T);
+    if (team_attrs_once(fn, sizeof(double) * (size_t)nbuf * (kSMaxT * 4 + kSMaxT)) != cudaSuccess) return false;
+    const int cap = resident_clusters(fn, C, T, smem);
+    return cap > 0 && n_units <= cap;
+}
+
 }  // namespace
 
 // Valid N for every structured kernel (the lambda_2 kernel, at 4096 bins per CTA, is the tightest).
@@ -809,8 +850,14 @@ int struct_shape(int N, int *C, int *threads) {
 
 cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s) {
     switch (kind) {
-        case kStructSolve: return SPL_TEAM_LAUNCH(k_struct_solve, 8, 3, 3);       // stages in the free w slot
-        case kStructLambda2: return SPL_TEAM_LAUNCH(k_struct_lambda2, 8, 5, 6);   // 221 KB at E = 8
+        case kStructSolve:                                                         // stages in the free w slot
+            if (a.N > kSChunkB && one_wave_at_e4((const void *)k_struct_solve<kCluster, 4>, a.N, n_units, 3))
+                return launch_team(k_struct_solve<kCluster, 4>, a, n_units, 4, 3, s);
+            return SPL_TEAM_LAUNCH(k_struct_solve, 8, 3, 3);
+        case kStructLambda2:                                                       // 221 KB at E = 8
+            if (a.N > kSChunkB && one_wave_at_e4((const void *)k_struct_lambda2<kCluster, 4>, a.N, n_units, 6))
+                return launch_team(k_struct_lambda2<kCluster, 4>, a, n_units, 4, 6, s);
+            return SPL_TEAM_LAUNCH(k_struct_lambda2, 8, 5, 6);
         case kStructMixing: return SPL_TEAM_LAUNCH(k_struct_mixing, 8, 4, 5);     // 184 KB at E = 8
         case kStructTraj: n_units = 1; return SPL_TEAM_LAUNCH(k_struct_traj, 16, 3, 3);
     }

@@ -1,7 +1,7 @@
-# structured quick check: parity tests + struct bench lines (c5, c4, c3, grid)
+# structured quick check: parity tests + struct / spectral bench lines
 python __graft_entry__.py > gpurun_out/build.log 2>&1
-timeout 900 python -m pytest tests/test_structured_gpu.py -q -x 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_structured_gpu.py tests/test_spectral_dense_gpu.py -q -x 2>&1 | tail -1
 for w in c5 c4 c3 grid; do timeout 300 python bench.py --path structured --workload $w --no-cpu-baseline > gpurun_out/bench_struct_$w.json 2>/dev/null; python -c "
 import json; d=json.load(open('gpurun_out/bench_struct_$w.json')); r=d['roofline']; print('$w', round(d['value']), round(d['ms_per_step'],4), round(r.get('kernel_ms_per_step'),4), d['clocks']['sm_mhz'])"; done
-for w in c5 grid; do timeout 300 python bench.py --path spectral --workload $w --no-cpu-baseline > gpurun_out/bench_spec_$w.json 2>/dev/null; python -c "
+for w in c5 c4 grid; do timeout 300 python bench.py --path spectral --workload $w --no-cpu-baseline > gpurun_out/bench_spec_$w.json 2>/dev/null; python -c "
 import json; d=json.load(open('gpurun_out/bench_spec_$w.json')); r=d['roofline']; print('spec $w', round(d['value']), round(d['ms_per_step'],4), round(r.get('kernel_ms_per_step', 0) or 0,4))"; done
