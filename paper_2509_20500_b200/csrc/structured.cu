@@ -299,7 +299,7 @@ __device__ __forceinline__ void push(Team<MODE> &tm, double *xbuf, const Pos<MOD
 template <int E>
 __device__ __forceinline__ void push_cl(Team<kCluster> &tm, double *xbuf, double *ybuf, const Pos<kCluster, E> &P,
                                         const double (&y)[E]) {
-    const int chunk = (int)blockDim.x * E;
+    constexpr int chunk = kSMaxT * E;                   // cluster teams are 512 threads (power of two)
     const int lane = threadIdx.x & 31, wbase = (int)(threadIdx.x & ~31u) * E;
 #pragma unroll
     for (int e = 0; e < E; ++e) ybuf[P.loc(e)] = y[e];
@@ -312,8 +312,8 @@ __device__ __forceinline__ void push_cl(Team<kCluster> &tm, double *xbuf, double
         if (p < P.N) {
             int r = p + P.l;
             if (r >= P.N) r -= P.N;
-            const int dst = r / chunk;
-            tm.cl.map_shared_rank(xbuf, dst)[sidx<E>(r - dst * chunk)] = ybuf[sidx<E>(q)];
+            const int dst = r / chunk;                  // a shift: chunk is a compile-time power of two
+            tm.cl.map_shared_rank(xbuf, dst)[sidx<E>(r & (chunk - 1))] = ybuf[sidx<E>(q)];
         }
     }
     __syncwarp();   // the slice may be restaged at once (two vectors per product)
@@ -344,6 +344,7 @@ __device__ __forceinline__ int xsize(int threads) { const int ch = threads * E; 
 // partials) -> publish (scan total, change) -> barrier -> y, push, change partial -> barrier.
 // Shared memory: xbuf | w | 1/D (each xsize; w and 1/D in registers at E = 8).
 template <int MODE, int E>
+// Warp and CTA teams (cluster teams run k_struct_solve_c1 below).
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) {
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
@@ -428,6 +429,232 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
     for (int e = 0; e < E; ++e)
         if (P.valid(e)) out[P.p0 + e] = yp[e] * is;
     if (tm.c == 0 && threadIdx.x == 0) {
+        SolveState st;
+        st.l = l;
+        st.iters = k;
+        st.done = 1;
+        st.converged = conv && s_k > 0.0;
+        st.cur = 0;
+        st.pad0 = st.pad1 = st.pad2 = 0;
+        st.s = s_k;
+        st.change = change;
+        a.st[item] = st;
+    }
+}
+
+// f2 on a cluster team with ONE cluster barrier per product. The two-barrier order exchanges the CTA
+// totals of z = x / D after the scan (for every CTA's prefix offset and T), then pushes y. Here the
+// pushing CTA also sends, per destination CTA, the sum of the z values it delivers there,
+// z_r = y_j / D_r with r = (j + l) mod N (1/D at the shifted positions is staged once), and its change
+// partial. After one barrier every CTA has its gathered x AND every CTA total: it scans its own chunk
+// (one block barrier) and adds the offsets. Gathered x and the table are double-buffered by the
+// parity of the product: a CTA can only be one product ahead (its next write needs everyone's
+// arrival at the barrier that follows the current read).
+// A CTA's chunk maps to a contiguous range of r (mod N) of one chunk's length, so its pushes land in
+// at most 3 runs of destination CTAs (one chunk boundary and the wrap at N; the ragged last chunk ends
+// at N): run boundaries are per-CTA constants, each thread keeps one accumulator per run.
+// Issue-bound (~700 SASS instructions per warp per product in the first version): the table totals,
+// the run sums and the table rows are done by warp 0 only, warp offsets by a lane-parallel scan,
+// chunk = 512 E is a compile-time power of two (no integer division).
+constexpr int kSeg = 3;
+struct C1Shared {
+    double tab[2][kSMaxC][kSMaxC + 1];   // [parity][source CTA][destination CTA | change]
+    double wrun[kSMaxWarps][kSeg + 1];   // per warp: z delivered per run, change partial
+    double scr[kSMaxWarps];              // block scan: warp totals
+    double off, T, change;               // this product's offset of the CTA, total, last change
+};
+
+template <int E>
+__global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve_c1(const StructArgs a) {
+    constexpr int kChunk = kSMaxT * E;                  // cluster teams are 512 threads
+    constexpr int kLog = E == 4 ? 11 : (E == 8 ? 12 : 13);
+    static_assert((1 << kLog) == kChunk, "chunk must be a power of two");
+    extern __shared__ double dyn[];
+    __shared__ C1Shared sh;
+    __shared__ SShared shT;                             // epilogue sum (Team exchange)
+    Team<kCluster> tm(shT, a.C);
+    const int C = a.C, c = tm.c;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int item = blockIdx.x / C;
+    const int m = a.prof[item], l = a.lsh[item];
+    const Pos<kCluster, E> P(a.N, c, l);
+    const int N = P.N, cbase = c * kChunk;
+    const int nval = min(kChunk, N - cbase);            // valid positions of this CTA
+    const int xs = xsize<E>(blockDim.x);
+    double *xb[2] = {dyn, dyn + xs};
+    double *stg = dyn + 2 * xs, *idsh = dyn + 3 * xs;   // push staging; 1/D at (j + l) mod N, lane order
+    const double *wv = a.w + (size_t)m * a.vstride, *iv = a.invD + (size_t)m * a.vstride;
+    // destination runs of this CTA's pushes: local q in [0, q1) -> dst0, [q1, q2) -> dst1, [q2, ..) -> dst2
+    int q1, q2, dstr[kSeg];
+    {
+        int r = cbase + l;
+        r = r >= N ? r - N : r;
+        int q = 0;
+        int qb[kSeg];
+#pragma unroll
+        for (int s2 = 0; s2 < kSeg; ++s2) {
+            const int d = r >> kLog;
+            const int end = min((d + 1) << kLog, N);    // first r past this run
+            dstr[s2] = d;
+            q += end - r;
+            qb[s2] = q;
+            r = end >= N ? 0 : end;
+        }
+        q1 = qb[0];
+        q2 = qb[1];
+    }
+    double wr[E], idr[E], yp[E];
+    const double u = 1.0 / (double)N;
+    double own = 0.0;                                   // this CTA's total of z^0 = u / D
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const bool ok = P.valid(e);
+        wr[e] = ok ? __ldg(wv + P.p0 + e) : 0.0;
+        idr[e] = ok ? __ldg(iv + P.p0 + e) : 0.0;
+        yp[e] = ok ? u : 0.0;
+        xb[0][P.loc(e)] = yp[e];                        // x^0: the uniform vector is its own gather
+        xb[1][P.loc(e)] = 0.0;                          // positions >= N stay 0 in both buffers
+        own += yp[e] * idr[e];
+    }
+    const int wq = (int)(tid & ~31u) * E + lane;        // lane-order local index for kk = 0
+    int sgk[E];                                         // run of this lane's kk-th pushed position
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const int q = wq + k * 32;
+        int r = cbase + q + l;
+        if (r >= N) r -= N;
+        idsh[sidx<E>(q)] = q < nval ? __ldg(iv + r) : 0.0;
+        sgk[k] = (q >= q1) + (q >= q2);
+    }
+    const double eL = a.scal[m * 8 + 1];
+    {   // table of product 0: own total on the diagonal
+        double v[1] = {own};
+        tm.template sum<1>(v);
+        if (tid < C * (C + 1)) {
+            const int dst = tid / (C + 1), col = tid - dst * (C + 1);
+            tm.cl.map_shared_rank(&sh.tab[0][0][0], dst)[c * (kSMaxC + 1) + col] = col == c ? v[0] : 0.0;
+        }
+    }
+    tm.cl.sync();
+    double change = __longlong_as_double(0x7ff0000000000000ll);
+    int k = 0, conv = 0;
+    for (;;) {
+        const int b = k & 1;
+        if (warp == 0) {   // CTA totals (lane d: sum over sources, fixed order), offset, T, change
+            double tot_d = 0.0, chg = 0.0;
+            if (lane < C) {
+                for (int src = 0; src < C; ++src) tot_d += sh.tab[b][src][lane];
+                chg = sh.tab[b][lane][C];
+            }
+            double inc = tot_d;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const double exc = __shfl_up_sync(0xffffffffu, inc, 1);
+            chg = warp_allsum(chg);
+            if (lane == c) sh.off = c == 0 ? 0.0 : exc;
+            if (lane == C - 1) sh.T = inc;
+            if (lane == 0) sh.change = chg;
+        }
+        // local inclusive scan of z = x / D over the chunk
+        double v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = xb[b][P.loc(e)] * idr[e];
+#pragma unroll
+        for (int e = 1; e < E; ++e) v[e] += v[e - 1];
+        double x = v[E - 1];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        double ex = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 0) ex = 0.0;
+        if (lane == 31) sh.scr[warp] = x;
+        __syncthreads();
+        if (k > 0) {
+            change = sh.change;
+            if (change < a.tol) { conv = 1; break; }
+            if (k >= a.max_iter || !isfinite(change)) break;
+        }
+        double wt = lane < kSMaxWarps ? sh.scr[lane] : 0.0;   // exclusive prefix of the warp totals
+#pragma unroll
+        for (int o = 1; o < kSMaxWarps; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, wt, o);
+            if (lane >= o) wt += y;
+        }
+        const double wexc = __shfl_sync(0xffffffffu, wt, warp == 0 ? 0 : warp - 1);
+        const double base = sh.off + (warp == 0 ? 0.0 : wexc) + ex;
+        const double T = sh.T;
+        // y = w (C + e^{-Lambda} (T - C)); change partial
+        double d = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const double Cj = base + v[e];
+            const double y = P.valid(e) ? wr[e] * (Cj + eL * (T - Cj)) : 0.0;
+            d += fabs(y - yp[e]);
+            yp[e] = y;
+            stg[P.loc(e)] = y;
+        }
+        __syncwarp();
+        // push y (lane-contiguous) into the other buffer; z delivered per run
+        double acc[kSeg + 1] = {0.0, 0.0, 0.0, d};
+#pragma unroll
+        for (int kk = 0; kk < E; ++kk) {
+            const int q = wq + kk * 32;
+            if (q < nval) {
+                int r = cbase + q + l;
+                if (r >= N) r -= N;
+                const int dst = r >> kLog;
+                const double y = stg[sidx<E>(q)];
+                tm.cl.map_shared_rank(xb[b ^ 1], dst)[sidx<E>(r & (kChunk - 1))] = y;
+                const double z = y * idsh[sidx<E>(q)];
+                acc[0] += sgk[kk] == 0 ? z : 0.0;
+                acc[1] += sgk[kk] == 1 ? z : 0.0;
+                acc[2] += sgk[kk] == 2 ? z : 0.0;
+            }
+        }
+#pragma unroll
+        for (int s2 = 0; s2 <= kSeg; ++s2) acc[s2] = warp_allsum(acc[s2]);
+        if (lane == 0) {
+#pragma unroll
+            for (int s2 = 0; s2 <= kSeg; ++s2) sh.wrun[warp][s2] = acc[s2];
+        }
+        __syncthreads();
+        if (warp == 0) {   // run sums and change partial of the CTA; its table row to every CTA
+            double rs[kSeg + 1];
+#pragma unroll
+            for (int s2 = 0; s2 <= kSeg; ++s2) rs[s2] = warp_allsum(lane < kSMaxWarps ? sh.wrun[lane][s2] : 0.0);
+            if (lane <= C) {
+                double val = rs[kSeg];                           // column C: change partial
+                if (lane < C) {
+                    val = 0.0;
+#pragma unroll
+                    for (int s2 = 0; s2 < kSeg; ++s2) val += dstr[s2] == lane ? rs[s2] : 0.0;
+                }
+                for (int dst = 0; dst < C; ++dst)
+                    tm.cl.map_shared_rank(&sh.tab[b ^ 1][0][0], dst)[c * (kSMaxC + 1) + lane] = val;
+            }
+        }
+        tm.cl.sync();   // pushes and table rows visible; everyone is done reading buffer b
+        ++k;
+    }
+    // pi^k = v^k / ||v^k||_1 at the natural positions
+    double sv[1] = {0.0};
+#pragma unroll
+    for (int e = 0; e < E; ++e) sv[0] += yp[e];
+    tm.template sum<1>(sv);
+    tm.template exchange<1>(tm.exB, sv);
+    double s_k, dm;
+    tm.total(tm.exB, 0, sv[0], s_k, dm);
+    double *out = a.pi + (size_t)item * N;
+    const double is = 1.0 / s_k;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        if (P.valid(e)) out[P.p0 + e] = yp[e] * is;
+    if (c == 0 && tid == 0) {
         SolveState st;
         st.l = l;
         st.iters = k;
@@ -850,10 +1077,14 @@ int struct_shape(int N, int *C, int *threads) {
 
 cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s) {
     switch (kind) {
-        case kStructSolve:                                                         // stages in the free w slot
-            if (a.N > kSChunkB && one_wave_at_e4((const void *)k_struct_solve<kCluster, 4>, a.N, n_units, 3))
-                return launch_team(k_struct_solve<kCluster, 4>, a, n_units, 4, 3, s);
-            return SPL_TEAM_LAUNCH(k_struct_solve, 8, 3, 3);
+        case kStructSolve:
+            if (a.N > kSChunkB) {   // cluster teams: one barrier.cluster per product
+                if (one_wave_at_e4((const void *)k_struct_solve_c1<4>, a.N, n_units, 4))
+                    return launch_team(k_struct_solve_c1<4>, a, n_units, 4, 4, s);
+                return launch_team(k_struct_solve_c1<8>, a, n_units, 8, 4, s);
+            }
+            return a.N <= 256 ? launch_team(k_struct_solve<kWarp, 8>, a, n_units, 8, 3, s)
+                              : launch_team(k_struct_solve<kBlock, 8>, a, n_units, 8, 3, s);
         case kStructLambda2:                                                       // 221 KB at E = 8
             if (a.N > kSChunkB && one_wave_at_e4((const void *)k_struct_lambda2<kCluster, 4>, a.N, n_units, 6))
                 return launch_team(k_struct_lambda2<kCluster, 4>, a, n_units, 4, 6, s);

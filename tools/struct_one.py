@@ -14,6 +14,8 @@ if case.startswith("grid"):
     S = np.tile(S.ravel(), 2); B = np.tile(B.ravel(), 2)
     T = np.repeat([75.0, 95.0], 64 * 64)
     shape = base
+elif case == "c4":
+    it = config(4).items[0]; shape = it.flux; S = np.ones(1); B = np.array([shape.background]); T = np.array([it.t_d])
 elif case == "c3":
     it = config(3).items[0]; shape = it.flux; S = np.ones(1); B = np.array([shape.background]); T = np.array([it.t_d])
 else:
