@@ -30,8 +30,9 @@
 namespace spl {
 namespace {
 
-constexpr int kT = 256;                 // threads per tile CTA
-constexpr int kE = kScanTile / kT;      // 4 consecutive elements per thread
+constexpr int kT = 1024;                // threads per tile CTA (one element each: the erfc / exp chains of
+                                        // a tile run in parallel; 256 x 4 left 8 warps per tile, k_vec_a 19 us at N = 32768)
+constexpr int kE = kScanTile / kT;      // consecutive elements per thread
 
 __device__ __forceinline__ double bin_centre(const FluxDev &f, int j) {
     return ((double)j + 0.5) * (f.t_r / (double)f.n);
@@ -67,8 +68,8 @@ __device__ double flux_rate(const FluxDev &f, double t) {
     return v;
 }
 
-// Inclusive scan of a 1024-element tile held as 4 consecutive values per thread (256 threads);
-// returns the tile total. warp_tot: 8 doubles of shared memory.
+// Inclusive scan of a 1024-element tile held as kE consecutive values per thread (kT threads);
+// returns the tile total. warp_tot: kT / 32 doubles of shared memory.
 __device__ double tile_scan(double (&v)[kE], double *warp_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -88,7 +89,7 @@ __device__ double tile_scan(double (&v)[kE], double *warp_tot) {
     __syncthreads();
     double wex = 0.0, total = 0.0;
 #pragma unroll
-    for (int w2 = 0; w2 < kT / 32; ++w2) {       // 8 warp totals: a short fixed-order sum
+    for (int w2 = 0; w2 < kT / 32; ++w2) {       // the warp totals: a short fixed-order sum
         const double wt = warp_tot[w2];
         if (w2 < warp) wex += wt;
         total += wt;
