@@ -481,8 +481,9 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve_c1(const StructArgs 
     const int N = P.N, cbase = c * kChunk;
     const int nval = min(kChunk, N - cbase);            // valid positions of this CTA
     const int xs = xsize<E>(blockDim.x);
-    double *xb[2] = {dyn, dyn + xs};
     double *stg = dyn + 2 * xs, *idsh = dyn + 3 * xs;   // push staging; 1/D at (j + l) mod N, lane order
+    // gathered x of product parity b: dyn + b * xs (arithmetic, not a pointer array: a runtime-indexed
+    // array of pointers lives in local memory)
     const double *wv = a.w + (size_t)m * a.vstride, *iv = a.invD + (size_t)m * a.vstride;
     // destination runs of this CTA's pushes: local q in [0, q1) -> dst0, [q1, q2) -> dst1, [q2, ..) -> dst2
     int q1, q2, dstr[kSeg];
@@ -512,8 +513,8 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve_c1(const StructArgs 
         wr[e] = ok ? __ldg(wv + P.p0 + e) : 0.0;
         idr[e] = ok ? __ldg(iv + P.p0 + e) : 0.0;
         yp[e] = ok ? u : 0.0;
-        xb[0][P.loc(e)] = yp[e];                        // x^0: the uniform vector is its own gather
-        xb[1][P.loc(e)] = 0.0;                          // positions >= N stay 0 in both buffers
+        dyn[P.loc(e)] = yp[e];                          // x^0: the uniform vector is its own gather
+        dyn[xs + P.loc(e)] = 0.0;                       // positions >= N stay 0 in both buffers
         own += yp[e] * idr[e];
     }
     const int wq = (int)(tid & ~31u) * E + lane;        // lane-order local index for kk = 0
@@ -540,6 +541,8 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve_c1(const StructArgs 
     int k = 0, conv = 0;
     for (;;) {
         const int b = k & 1;
+        const double *xcur = dyn + b * xs;
+        double *xnext = dyn + (b ^ 1) * xs;
         if (warp == 0) {   // CTA totals (lane d: sum over sources, fixed order), offset, T, change
             double tot_d = 0.0, chg = 0.0;
             if (lane < C) {
@@ -561,7 +564,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve_c1(const StructArgs 
         // local inclusive scan of z = x / D over the chunk
         double v[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = xb[b][P.loc(e)] * idr[e];
+        for (int e = 0; e < E; ++e) v[e] = xcur[P.loc(e)] * idr[e];
 #pragma unroll
         for (int e = 1; e < E; ++e) v[e] += v[e - 1];
         double x = v[E - 1];
@@ -609,7 +612,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve_c1(const StructArgs 
                 if (r >= N) r -= N;
                 const int dst = r >> kLog;
                 const double y = stg[sidx<E>(q)];
-                tm.cl.map_shared_rank(xb[b ^ 1], dst)[sidx<E>(r & (kChunk - 1))] = y;
+                tm.cl.map_shared_rank(xnext, dst)[sidx<E>(r & (kChunk - 1))] = y;
                 const double z = y * idsh[sidx<E>(q)];
                 acc[0] += sgk[kk] == 0 ? z : 0.0;
                 acc[1] += sgk[kk] == 1 ? z : 0.0;
