@@ -237,7 +237,10 @@ struct Team {
             const int t = threadIdx.x;
             if (t < C * K) {
                 const int dst = t / K, k = t - dst * K;
-                cl.map_shared_rank(ex, dst)[k * kSMaxC + c] = v[k];
+                double val = v[0];                 // select by unrolled compares: v[k] with a runtime k
+#pragma unroll                                    // would put v in local memory
+                for (int kk = 1; kk < K; ++kk) val = k == kk ? v[kk] : val;
+                cl.map_shared_rank(ex, dst)[k * kSMaxC + c] = val;
             }
             cl.sync();
         } else {
