@@ -334,35 +334,48 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
     const int e0 = threadIdx.x * kSEl;
     double *F = b.F + m * vstride, *lam = b.lam + m * vstride, *w = b.w + m * vstride;
     double *invD = b.invD + m * vstride, *invZ = b.invZ + m * vstride;
+    // The erfc / exp evaluations run in ROLLED loops through the thread's own shared-memory slots:
+    // unrolled 8x with the inlined fp64 erfc / exp the kernel was ~12k SASS instructions and stalled
+    // on instruction fetch (ncu: no_instructions 33%, 52.6 us for c3's 64 profiles).
     // masses (N + 1 of them) and their inclusive scan: F_j = F(s_j), Lambda = F(t_r)
-    double wv[kSEl];
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < kSEl; ++i) {
         const int e = e0 + i;
-        wv[i] = 0.0;
+        double mv = 0.0;
         if (e <= N) {
             const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
             const double hi = e == N ? f.t_r : bin_centre(f, e);
-            wv[i] = flux_mass(f, lo, hi);
+            mv = flux_mass(f, lo, hi);
         }
+        rev[e0 + i] = mv;
     }
-    const double Lam = small_scan(wv, wt);
-    const double eL = exp(-Lam);
-    // lambda_j, w_j = lambda_j e^{-F_j}
+    double wv[kSEl];
 #pragma unroll
+    for (int i = 0; i < kSEl; ++i) wv[i] = rev[e0 + i];
+    const double Lam = small_scan(wv, wt);       // its barriers: every thread has read its slots
+    const double eL = exp(-Lam);
+#pragma unroll
+    for (int i = 0; i < kSEl; ++i) rev[e0 + i] = wv[i];   // F_j (own slots)
+    // lambda_j, w_j = lambda_j e^{-F_j}
+#pragma unroll 1
     for (int i = 0; i < kSEl; ++i) {
         const int e = e0 + i;
+        double wj = 0.0;
         if (e < N) {
+            const double Fe = rev[e0 + i];
             const double lm = flux_rate(f, bin_centre(f, e));
-            F[e] = wv[i];
+            F[e] = Fe;
             lam[e] = lm;
-            wv[i] = lm * exp(-wv[i]);
-            w[e] = wv[i];
-        } else {
-            wv[i] = 0.0;
+            wj = lm * exp(-Fe);
+            w[e] = wj;
         }
-        rev[nslot - 1 - e] = wv[i];
+        rev[e0 + i] = wj;
     }
+#pragma unroll
+    for (int i = 0; i < kSEl; ++i) wv[i] = rev[e0 + i];
+    __syncthreads();                             // own slots read: rev[] now takes w reversed
+#pragma unroll
+    for (int i = 0; i < kSEl; ++i) rev[nslot - 1 - (e0 + i)] = wv[i];
     double pf[kSEl];
 #pragma unroll
     for (int i = 0; i < kSEl; ++i) pf[i] = wv[i];
