@@ -466,15 +466,20 @@ def run_struct(args, rank, world, dev):
                    "parallelism": "single GPU" if world == 1 else f"dp{world}: items sharded, no collective"},
         "converged": conv, "products_per_step": products,
         "iterations_max": max(max(x) for x in iters), "iterations_sum": sum(sum(x) for x in iters),
-        "roofline": {"bound": "alu", "kernel": "k_struct_lambda2" if kind == "lambda2" else "k_struct_solve",
+        "roofline": {"bound": "alu", "kernel": "k_struct_lambda2" if kind == "lambda2" else
+                     ("k_struct_solve_c1" if N > 4096 else "k_struct_solve"),
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
                      "algorithmic_flops_per_bin_product": FLOPS_PER_ELEM[kind],
                      "kernel_ms_per_step": statistics.mean(k_ms),
                      "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (probe: 35.8 TFLOP/s DFMA)",
-                     "note": "FP64 issue is not the limiter: per-product barriers and scan latency are (DESIGN.md)"},
+                     "note": "FP64 issue is not the limiter: per-product barriers, scan latency and instruction "
+                             "issue are (DESIGN.md)"},
         "clocks": clk, "e2e": e2e,
-        "gpu_launches": (len(main_plans) + (len(solve_plans) if kind == "lambda2" else 0)) * 6 * K,
+        # per plan launch: the step-1 vector kernels (k_vec_small: 1 when N + 1 <= 8192, else k_vec_a..e: 5)
+        # and the team kernel
+        "gpu_launches": (len(main_plans) + (len(solve_plans) if kind == "lambda2" else 0))
+                        * ((1 if N + 1 <= 8192 else 5) + 1) * K,
         "impl": "ours", "lib": spl.lib_path(),
     }
 

@@ -36,8 +36,9 @@ can exceed a copy by ~6% (probe: 6.86 / 6.95 TB/s), so fractions slightly above 
 
 Box to box the default line moved between 291 and 316 solves/s this round at identical code: the
 17-vector pass is at the DMMA / HBM balance point (ncu: tensor DMMA subpipe 74% busy, DRAM 80%), so it
-follows the power-capped SM clock, unlike a pure read stream: a sustained run takes ~1.38 ms per
-iteration (GEMV + check) against 1.27 ms for the GEMV replayed alone under ncu, and the eager host loop
+follows the power-capped SM clock, unlike a pure read stream (this line's box held {c5['clocks']['sm_mhz']:.0f} MHz under load):
+one 17-vector solve launched after idle takes 1.278 ms per iteration (the ncu GEMV + check times),
+back-to-back steps ~1.38 ms, and the eager host loop
 adds only 41 us per iteration to the graph (`tools/graph_overhead.py`), so the graph loop itself costs
 little. Moving 9 of the 17 vectors to plain DFMA (8 on DMMA) to unload the tensor pipe was measured
 and rejected: 1.68 ms per pass, issue-bound (FP64 pipe 33%, DMMA 29%). Before this round's small-N work c1 / c2 ran
@@ -47,7 +48,7 @@ max(8.59 GB / 6.95 TB/s, 16 x 2 x N^2 flops / 37 TFLOP/s) = 40 x 1.24 ms = 49.4 
 matrix) by the whole solve phase (GEMV + check kernels + graph overhead), a lower bound on the kernel's own
 rate; ncu: 8.656 GB DRAM read per 8.590 GB algorithmic (`traffic`), and the launch list of the default
 command (`profiles/r01/launches_c5_eager.csv`, eager mode, cold cache) gives `k_power_step<double, 17>`
-~96% of device time (1.27 ms per pass), `k_build` ~2.3%, `k_power_check` ~1.5%, the flux-vector kernels
+~96% of device time (1.27 ms per pass), `k_build` ~2.3%, `k_power_check` ~1% (13.7 us), the flux-vector kernels
 0.1%. Clocks under load: {c5['clocks']['sm_mhz']:.0f} MHz ({', '.join(c5['clocks']['reasons']) or 'no throttle'}).
 CPU baseline (the oracle as it stands, {c5['cpu_baseline']['cores']} host cores, {c5['cpu_baseline']['host']['cpu_model']}): {c5['cpu_baseline']['value']:.4f} solves/s on c5 (bounded
 sample, see the line's `cpu_baseline.sample`; one core builds {c5['cpu_baseline']['build_entries_per_s_one_core']:.3g} Eq. 4 entries/s, all cores
@@ -57,9 +58,9 @@ sample, see the line's `cpu_baseline.sample`; one core builds {c5['cpu_baseline'
 
 | row | workload | throughput | ms/step | dominant kernel vs roofline | oracle on the host |
 |---|---|---|---|---|---|
-| f2 structured solve | c5 (17 items, N = 32768) | {g('bench_struct_c5'):,.0f} solves/s (dense path: {c5['value']:.0f}) | {g('bench_struct_c5','ms_per_step'):.3f} | `k_struct_solve`, {rf('bench_struct_c5','achieved'):.2f} TFLOP/s ({rf('bench_struct_c5','frac'):.3f} of FP64): barrier-bound, 15 co-resident 8-CTA clusters | {d['bench_struct_c5']['cpu_baseline']['value']:.4f} solves/s |
+| f2 structured solve | c5 (17 items, N = 32768) | {g('bench_struct_c5'):,.0f} solves/s (dense path: {c5['value']:.0f}) | {g('bench_struct_c5','ms_per_step'):.3f} | `k_struct_solve_c1`, {rf('bench_struct_c5','achieved'):.2f} TFLOP/s ({rf('bench_struct_c5','frac'):.3f} of FP64): latency / issue-bound (one barrier.cluster per product), two waves of at most 15 co-resident 8-CTA clusters | {d['bench_struct_c5']['cpu_baseline']['value']:.4f} solves/s |
 | f2 | c3 (64 items, N = 4096) | {g('bench_struct_c3'):,.0f} solves/s | {g('bench_struct_c3','ms_per_step'):.3f} | {rf('bench_struct_c3','achieved'):.2f} TFLOP/s ({rf('bench_struct_c3','frac'):.3f}) | {d['bench_struct_c3']['cpu_baseline']['value']:.2f} |
-| f2 | c4 (1 item, N = 16384) | {g('bench_struct_c4'):,.0f} solves/s (dense: {g('bench_c4'):.0f}) | {g('bench_struct_c4','ms_per_step'):.3f} | latency (one 4-CTA cluster) | {d['bench_struct_c4']['cpu_baseline']['value']:.3f} |
+| f2 | c4 (1 item, N = 16384) | {g('bench_struct_c4'):,.0f} solves/s (dense: {g('bench_c4'):.0f}) | {g('bench_struct_c4','ms_per_step'):.3f} | latency (one 8-CTA cluster of 4 bins per thread) | {d['bench_struct_c4']['cpu_baseline']['value']:.3f} |
 | f2 | grid (8192 items, N = 256) | {g('bench_struct_grid')/1e6:.1f} M solves/s | {g('bench_struct_grid','ms_per_step'):.3f} | {rf('bench_struct_grid','achieved'):.2f} TFLOP/s ({rf('bench_struct_grid','frac'):.3f}) | {d['bench_struct_grid']['cpu_baseline']['value']:.0f} |
 | f1 spectral (pi + lambda_2) | grid | {g('bench_spec_grid')/1e6:.2f} M analyses/s | {g('bench_spec_grid','ms_per_step'):.2f} | `k_struct_lambda2`, {rf('bench_spec_grid','achieved'):.2f} TFLOP/s ({rf('bench_spec_grid','frac'):.3f}) | {d['bench_spec_grid']['cpu_baseline']['value']:.1f} (dense eigvals) |
 | f1 | c5 (17 items) | {g('bench_spec_c5'):,.0f} analyses/s | {g('bench_spec_c5','ms_per_step'):.2f} | {rf('bench_spec_c5','achieved'):.2f} TFLOP/s | — (no dense spectrum at N = 32768) |
