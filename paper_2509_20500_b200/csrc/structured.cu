@@ -349,6 +349,7 @@ __device__ __forceinline__ int xsize(int threads) { const int ch = threads * E; 
 template <int MODE, int E>
 // Warp and CTA teams (cluster teams run k_struct_solve_c1 below).
 __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) {
+    static_assert(MODE != kCluster, "cluster teams: k_struct_solve_c1");
     extern __shared__ double xbuf[];
     __shared__ SShared sh;
     __shared__ double dwarp[kSMaxWarps];              // per-warp change partials of the last product
@@ -411,8 +412,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
             d += fabs(v[0][e] - yp[e]);
             yp[e] = v[0][e];
         }
-        if constexpr (MODE == kCluster && REG) push_cl<E>(tm, xbuf, ws, P, v[0]);   // ws is free at E = 8
-        else push<MODE, E>(tm, xbuf, P, v[0]);
+        push<MODE, E>(tm, xbuf, P, v[0]);
         d = warp_allsum(d);
         if ((threadIdx.x & 31) == 0) dwarp[threadIdx.x >> 5] = d;
         tm.barrier();   // pushes complete (and dwarp written) before the next product reads them
