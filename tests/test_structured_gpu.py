@@ -349,3 +349,34 @@ def test_team_boundaries(spl, N):
         got = _lambda2(spl, f, td, pi_s)
         want = oracle.second_eigenvalue(oracle.build_eq4(f, td))
         assert got["converged"] and abs(got["modulus"] - abs(want)) <= 1e-8
+
+
+@pytest.mark.parametrize("N", [12289, 32768])
+def test_cluster_shift_edges(spl, N):
+    """Cluster teams at the shifts where the pushes' destination runs change shape: l = 0 (every CTA
+    pushes to itself), l = 1, l at and next to a chunk boundary (2048 at 4 bins per thread, 4096 at 8),
+    l = N - 1 (wrap of all but one position); N = 12289 leaves a last CTA of 1 position. One item
+    (4 bins per thread, one cluster) and 17 items (8 bins per thread, two waves) against the dense GEMV
+    path's pi for the same P~0."""
+    f = random_flux(np.random.default_rng(N + 7), N, 2)
+    ls = [0, 1, 2047, 2048, 4095, 4096, N - 1]
+    tds = [0.0 if l == 0 else (l - 0.5) * f.t_r / N for l in ls]
+    assert [spl.shift(f.t_r, N, t) for t in tds] == ls
+    P0 = spl.build_base(f)
+    pis_d, infos_d = [], []
+    for td in tds:
+        p, i = spl.stationary(P0, f.t_r, td)
+        pis_d.append(_np(p))
+        infos_d.append(i)
+    del P0
+    shape, S, B = spl.flux_items(f)
+    for td, want, inf_d in zip(tds, pis_d, infos_d):                     # one item: E = 4
+        got, inf = _one(spl, f, td)
+        assert inf["converged"] and abs(int(inf["iters"]) - inf_d["iters"]) <= 1
+        assert np.sum(np.abs(_np(got) - want)) <= 1e-13, td
+    T = (tds * 3)[:17]                                                   # 17 items: E = 8, two waves
+    pis, infos = spl.stationary_structured(shape, np.repeat(S, 17), np.repeat(B, 17), T)
+    for m in range(17):
+        k = m % len(tds)
+        assert bool(infos[m]["converged"])
+        assert np.sum(np.abs(_np(pis[m]) - pis_d[k])) <= 1e-13, (m, ls[k])
