@@ -61,6 +61,31 @@ __device__ __forceinline__ double warp_allsum(double x) {
     return x;
 }
 
+// Lane-parallel sums over the (<= 16) warps of a CTA, replacing 16-long dependent loops that every
+// thread ran (ncu: ~860 of the lambda_2 kernel's ~2280 SASS instructions per warp per product).
+// Fixed trees: every warp of every CTA computes bitwise-identical results from the same values.
+// src[w] for w < nw (the CTA's warps); lanes >= nw contribute 0.
+__device__ __forceinline__ double lanes_total(const double *src, int nw) {
+    const int lane = threadIdx.x & 31;
+    double x = lane < nw ? src[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+// exclusive prefix over the warps before `warp` and the total, of src[w] (w < nw)
+__device__ __forceinline__ void lanes_scan(const double *src, int nw, int warp, double &before, double &total) {
+    const int lane = threadIdx.x & 31;
+    double inc = lane < nw ? src[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < kSMaxWarps; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const double exc = __shfl_up_sync(0xffffffffu, inc, 1);
+    before = __shfl_sync(0xffffffffu, lane == 0 ? 0.0 : exc, warp);
+    total = __shfl_sync(0xffffffffu, inc, kSMaxWarps - 1);
+}
+
 template <int MODE>
 struct Team {
     cg::cluster_group cl;
@@ -94,11 +119,7 @@ struct Team {
             }
             __syncthreads();
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                double s = 0.0;
-                for (int w = 0; w < nw; ++w) s += scr[k * kSMaxWarps + w];
-                v[k] = s;
-            }
+            for (int k = 0; k < K; ++k) v[k] = lanes_total(scr + k * kSMaxWarps, nw);
             __syncthreads();
         }
     }
@@ -141,12 +162,8 @@ struct Team {
             __syncthreads();
 #pragma unroll
             for (int a = 0; a < V; ++a) {
-                double wex = 0.0, tt = 0.0;
-                for (int w = 0; w < nw; ++w) {
-                    const double wt = scr[a * kSMaxWarps + w];
-                    if (w < warp) wex += wt;
-                    tt += wt;
-                }
+                double wex, tt;
+                lanes_scan(scr + a * kSMaxWarps, nw, warp, wex, tt);
                 tot[a] = tt;
                 const double e = wex + ex[a];
 #pragma unroll
@@ -197,35 +214,28 @@ struct Team {
             __syncthreads();
 #pragma unroll
             for (int a = 0; a < V; ++a) {
-                double wex = 0.0, tt = 0.0;
-                for (int w = 0; w < nw; ++w) {
-                    const double wt = scr[a * kSMaxWarps + w];
-                    if (w < warp) wex += wt;
-                    tt += wt;
-                }
+                double wex, tt;
+                lanes_scan(scr + a * kSMaxWarps, nw, warp, wex, tt);
                 tot[a] = tt;
                 const double e = wex + ex[a];
 #pragma unroll
                 for (int i = 0; i < E; ++i) v[a][i] += e;
             }
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                double pt = 0.0;
-                for (int w = 0; w < nw; ++w) pt += wp[k * kSMaxWarps + w];
-                part[k] = pt;
-            }
+            for (int k = 0; k < K; ++k) part[k] = lanes_total(wp + k * kSMaxWarps, nw);
             __syncthreads();
         }
     }
     // sum over the team-local warps of per-warp partials (after a barrier that ordered their writes)
     template <int K>
     __device__ __forceinline__ void warp_partials(const double *wp, double (&part)[K]) const {
-        const int nw = MODE == kWarp ? 1 : (int)(blockDim.x >> 5);
+        if constexpr (MODE == kWarp) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double pt = 0.0;
-            for (int w = 0; w < nw; ++w) pt += wp[k * kSMaxWarps + w];
-            part[k] = pt;
+            for (int k = 0; k < K; ++k) part[k] = wp[k * kSMaxWarps];
+        } else {
+            const int nw = (int)(blockDim.x >> 5);
+#pragma unroll
+            for (int k = 0; k < K; ++k) part[k] = lanes_total(wp + k * kSMaxWarps, nw);
         }
     }
     // exchange K per-CTA values through area ex (A or B) and synchronise the team; afterwards
