@@ -258,20 +258,23 @@ struct Team {
         }
     }
     __device__ __forceinline__ void total(const double *ex, int k, double own, double &tot, double &before) const {
-        if constexpr (MODE == kCluster) {
-            double t = 0.0, b = 0.0;
-            for (int cc = 0; cc < C; ++cc) {
-                const double v = ex[k * kSMaxC + cc];
-                if (cc < c) b += v;
-                t += v;
+        if constexpr (MODE == kCluster) {   // lane-parallel over the C <= 16 CTAs (fixed shfl-up tree)
+            const int lane = threadIdx.x & 31;
+            double inc = lane < C ? ex[k * kSMaxC + lane] : 0.0;
+#pragma unroll
+            for (int o = 1; o < kSMaxC; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
             }
-            tot = t;
-            before = b;
+            const double exc = __shfl_up_sync(0xffffffffu, inc, 1);
+            tot = __shfl_sync(0xffffffffu, inc, kSMaxC - 1);
+            before = __shfl_sync(0xffffffffu, lane == 0 ? 0.0 : exc, c);
         } else {
             tot = own;
             before = 0.0;
         }
     }
+
 };
 
 // Positions of this thread: p0 .. p0 + E - 1 (global), local index tid * E + e in its CTA's chunk.
