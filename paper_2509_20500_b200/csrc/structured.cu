@@ -86,6 +86,54 @@ __device__ __forceinline__ void lanes_scan(const double *src, int nw, int warp, 
     total = __shfl_sync(0xffffffffu, inc, kSMaxWarps - 1);
 }
 
+// Transposed butterfly: the warp sums of 8 values in 9 double shuffles (8 separate xor trees take 40).
+// Each xor step exchanges half of the lane's remaining values with its partner, so after offsets
+// 16, 8, 4 lane l holds one value index k8(l) = 4 b4 + 2 b3 + b2 (bits of l) summed over 8 lanes, and
+// offsets 2, 1 finish it. Fixed order: every warp gets bitwise-identical totals for the same inputs.
+__device__ __forceinline__ int k8_of_lane(int lane) { return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1); }
+__device__ __forceinline__ int lane_of_k8(int k) { return ((k >> 2) & 1) * 16 + ((k >> 1) & 1) * 8 + (k & 1) * 4; }
+__device__ __forceinline__ double warp_sum8(const double (&v)[8]) {
+    const int lane = threadIdx.x & 31;
+    const bool h4 = (lane >> 4) & 1, h3 = (lane >> 3) & 1, h2 = (lane >> 2) & 1;
+    double w4[4], w2[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double keep = h4 ? v[i + 4] : v[i], send = h4 ? v[i] : v[i + 4];
+        w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double keep = h3 ? w4[i + 2] : w4[i], send = h3 ? w4[i] : w4[i + 2];
+        w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    double x = (h2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, h2 ? w2[0] : w2[1], 4);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    return x;
+}
+// per-warp sums of K <= 8 values, written by lane lane_of_k8(k) to dst[k * kSMaxWarps + warp]
+template <int K>
+__device__ __forceinline__ void warp_sums_to(const double (&v)[K], double *dst) {
+    static_assert(K <= 8, "at most 8 values");
+    double u[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) u[k] = k < K ? v[k] : 0.0;
+    const double t = warp_sum8(u);
+    const int lane = threadIdx.x & 31, k = k8_of_lane(lane);
+    if ((lane & 3) == 0 && k < K) dst[k * kSMaxWarps + (threadIdx.x >> 5)] = t;
+}
+// totals over the nw warps of K <= 8 per-warp values src[k * kSMaxWarps + w], in every thread
+template <int K>
+__device__ __forceinline__ void lanes_totals(const double *src, int nw, double (&out)[K]) {
+    const int lane = threadIdx.x & 31;
+    double u[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) u[k] = (k < K && lane < nw) ? src[k * kSMaxWarps + lane] : 0.0;
+    const double t = warp_sum8(u);
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = __shfl_sync(0xffffffffu, t, lane_of_k8(k));
+}
+
 template <int MODE>
 struct Team {
     cg::cluster_group cl;
@@ -111,15 +159,22 @@ struct Team {
 #pragma unroll
             for (int k = 0; k < K; ++k) v[k] = warp_allsum(v[k]);
         } else {
-            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+            const int nw = blockDim.x >> 5;
+            if constexpr (K <= 8) {
+                warp_sums_to<K>(v, scr);
+                __syncthreads();
+                lanes_totals<K>(scr, nw, v);
+            } else {
+                const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const double x = warp_allsum(v[k]);
-                if (lane == 0) scr[k * kSMaxWarps + warp] = x;
+                for (int k = 0; k < K; ++k) {
+                    const double x = warp_allsum(v[k]);
+                    if (lane == 0) scr[k * kSMaxWarps + warp] = x;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < K; ++k) v[k] = lanes_total(scr + k * kSMaxWarps, nw);
             }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < K; ++k) v[k] = lanes_total(scr + k * kSMaxWarps, nw);
             __syncthreads();
         }
     }
@@ -221,8 +276,7 @@ struct Team {
 #pragma unroll
                 for (int i = 0; i < E; ++i) v[a][i] += e;
             }
-#pragma unroll
-            for (int k = 0; k < K; ++k) part[k] = lanes_total(wp + k * kSMaxWarps, nw);
+            lanes_totals<K>(wp, nw, part);
             __syncthreads();
         }
     }
@@ -234,8 +288,7 @@ struct Team {
             for (int k = 0; k < K; ++k) part[k] = wp[k * kSMaxWarps];
         } else {
             const int nw = (int)(blockDim.x >> 5);
-#pragma unroll
-            for (int k = 0; k < K; ++k) part[k] = lanes_total(wp + k * kSMaxWarps, nw);
+            lanes_totals<K>(wp, nw, part);
         }
     }
     // exchange K per-CTA values through area ex (A or B) and synchronise the team; afterwards
@@ -755,11 +808,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
             pp[3] += wn[0][e] * wn[1][e];
             pp[4] += wn[1][e] * wn[1][e];
         }
-#pragma unroll
-        for (int i = 0; i < 5; ++i) {
-            const double t = warp_allsum(pp[i]);
-            if ((threadIdx.x & 31) == 0) wpart[i * kSMaxWarps + (threadIdx.x >> 5)] = t;
-        }
+        warp_sums_to<5>(pp, wpart);
         if constexpr (MODE == kWarp) __syncwarp();
         tm.template scan_sum<2, E, 5>(v, tot, wpart, pp);   // its first barrier also adds the pp partials
         {
@@ -809,11 +858,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
 #pragma unroll
             for (int i = 0; i < 7; ++i) tm.total(tm.exB, i, hp[i], h[i], dm);
         } else {                                      // one barrier orders the pushes and the partials
-#pragma unroll
-            for (int i = 0; i < 7; ++i) {
-                const double t = warp_allsum(hp[i]);
-                if ((threadIdx.x & 31) == 0) wpart[i * kSMaxWarps + (threadIdx.x >> 5)] = t;
-            }
+            warp_sums_to<7>(hp, wpart);
             tm.barrier();
             tm.template warp_partials<7>(wpart, h);
             tm.barrier();                             // wpart is rewritten in the next phase 1
