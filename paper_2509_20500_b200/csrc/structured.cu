@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
 constexpr int kSeg = 3;
 struct C1Shared {
     double tab[2][kSMaxC][kSMaxC + 1];   // [parity][source CTA][destination CTA | change]
-    double wrun[kSMaxWarps][kSeg + 1];   // per warp: z delivered per run, change partial
+    double wrun[kSeg + 1][kSMaxWarps];   // per run (and change partial), per warp: z delivered
     double scr[kSMaxWarps];              // block scan: warp totals
     double off, T, change;               // this product's offset of the CTA, total, last change
 };
@@ -688,17 +688,11 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve_c1(const StructArgs 
                 acc[2] += sgk[kk] == 2 ? z : 0.0;
             }
         }
-#pragma unroll
-        for (int s2 = 0; s2 <= kSeg; ++s2) acc[s2] = warp_allsum(acc[s2]);
-        if (lane == 0) {
-#pragma unroll
-            for (int s2 = 0; s2 <= kSeg; ++s2) sh.wrun[warp][s2] = acc[s2];
-        }
+        warp_sums_to<kSeg + 1>(acc, &sh.wrun[0][0]);
         __syncthreads();
         if (warp == 0) {   // run sums and change partial of the CTA; its table row to every CTA
             double rs[kSeg + 1];
-#pragma unroll
-            for (int s2 = 0; s2 <= kSeg; ++s2) rs[s2] = warp_allsum(lane < kSMaxWarps ? sh.wrun[lane][s2] : 0.0);
+            lanes_totals<kSeg + 1>(&sh.wrun[0][0], kSMaxWarps, rs);
             if (lane <= C) {
                 double val = rs[kSeg];                           // column C: change partial
                 if (lane < C) {
