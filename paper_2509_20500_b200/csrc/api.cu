@@ -953,20 +953,48 @@ static splidar_status read_scal(Prep *p, cudaStream_t s) {
 
 // Structured plans: items validated and uploaded once; each launch recomputes the step-1 vectors
 // and runs the kernel (async); CUDA events around the kernel give its device time.
+// The first launch runs eagerly (it also sets the kernels' attributes and caches the cluster
+// residency query); a second launch captures the same sequence once into a CUDA graph, with the
+// events as external event-record nodes, and it and later launches replay it (one cudaGraphLaunch instead of up to 6 kernel
+// launches and 2 event records: the host gaps between them were ~1/4 of c5's structured step).
+// SPLIDAR_SPLAN_GRAPH=0 keeps every launch eager.
 struct splidar_splan_s {
     Prep p;
     int kind = 0;
     int n_items = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool graph_tried = false;
+    long launches = 0;
+    cudaGraphExec_t gexec = nullptr;
 };
 
-static splidar_status splan_launch_impl(splidar_splan_s *pl, cudaStream_t s) {
+static splidar_status splan_launch_impl(splidar_splan_s *pl, cudaStream_t s, bool capture = false) {
     const Prep &p = pl->p;
+    const unsigned fl = capture ? cudaEventRecordExternal : cudaEventRecordDefault;
     SPL_CUDA(launch_flux_vectors(p.flux_dev, p.L.M, p.a.N, p.vp, p.a.N, s));
-    SPL_CUDA(cudaEventRecord(pl->ev0, s));
+    SPL_CUDA(cudaEventRecordWithFlags(pl->ev0, s, fl));
     SPL_CUDA(launch_struct(pl->kind == 0 ? kStructSolve : kStructLambda2, p.a, pl->n_items, s));
-    SPL_CUDA(cudaEventRecord(pl->ev1, s));
+    SPL_CUDA(cudaEventRecordWithFlags(pl->ev1, s, fl));
     return SPLIDAR_OK;
+}
+
+// Capture the launch sequence on a private stream (nothing executes) and instantiate it.
+static cudaError_t splan_capture(splidar_splan_s *pl) {
+    cudaStream_t cs = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        const splidar_status st = splan_launch_impl(pl, cs, true);
+        const cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+        e = st != SPLIDAR_OK ? cudaErrorUnknown : e2;
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&pl->gexec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cs);
+    if (e != cudaSuccess) pl->gexec = nullptr;
+    return e;
 }
 
 extern "C" {
@@ -979,6 +1007,7 @@ size_t splidar_structured_workspace_bytes(int32_t n_bins, int32_t n_profiles, in
 
 void splidar_splan_destroy(splidar_splan plan) {
     if (!plan) return;
+    if (plan->gexec) cudaGraphExecDestroy(plan->gexec);
     if (plan->ev0) cudaEventDestroy(plan->ev0);
     if (plan->ev1) cudaEventDestroy(plan->ev1);
     delete plan;
@@ -1010,7 +1039,16 @@ splidar_status splidar_splan_create(splidar_splan *plan, int32_t kind, const spl
 
 splidar_status splidar_splan_launch(splidar_splan plan, void *stream) {
     if (!plan) return SPLIDAR_EINVAL;
-    return splan_launch_impl(plan, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!plan->gexec && plan->launches == 1 && !plan->graph_tried) {   // a reused plan: capture it once
+        plan->graph_tried = true;
+        const char *e = getenv("SPLIDAR_SPLAN_GRAPH");
+        if (!(e && e[0] == '0') && splan_capture(plan) != cudaSuccess)
+            (void)cudaGetLastError();   // stay eager: the graph is an optimisation only
+    }
+    ++plan->launches;
+    if (plan->gexec) return cuda_status(cudaGraphLaunch(plan->gexec, s));
+    return splan_launch_impl(plan, s);
 }
 
 splidar_status splidar_splan_info(splidar_splan plan, splidar_solve_info *solve_info,
