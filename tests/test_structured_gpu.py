@@ -380,3 +380,28 @@ def test_cluster_shift_edges(spl, N):
         k = m % len(tds)
         assert bool(infos[m]["converged"])
         assert np.sum(np.abs(_np(pis[m]) - pis_d[k])) <= 1e-13, (m, ls[k])
+
+
+@pytest.mark.parametrize("kind", ["solve", "lambda2"])
+def test_plan_graph_replay_equals_eager(spl, kind):
+    """A structured plan's first launch is eager, later ones replay a captured CUDA graph: identical
+    results (bitwise), iteration counts and a positive kernel time from the graph's event nodes."""
+    it = config(4).items[0]
+    shape, S, B = spl.flux_items(it.flux)
+    T = [it.t_d, 75.0, 430.0]
+    S3, B3 = np.repeat(S, 3), np.repeat(B, 3)
+    pi = None
+    if kind == "lambda2":
+        pi, _ = spl.stationary_structured(shape, S3, B3, T)
+    plan = spl.StructPlan(kind, shape, S3, B3, T, pi=pi)
+    outs = []
+    for _ in range(3):
+        plan.launch()
+        infos, ms = plan.info()
+        assert ms > 0.0
+        outs.append((plan.pi.clone() if kind == "solve" else None, infos.copy()))
+    plan.close()
+    for o in outs[1:]:
+        if kind == "solve":
+            assert torch.equal(o[0], outs[0][0])
+        assert np.array_equal(o[1], outs[0][1])
