@@ -310,6 +310,26 @@ struct Team {
             barrier();
         }
     }
+    // totals only (no prefix) of K exchange values k0 .. k0 + K - 1, two per pass (lanes 0-15 and
+    // 16-31, C <= 16, fixed xor trees); single-CTA teams: the own values
+    template <int K>
+    __device__ __forceinline__ void totals_only(const double *ex, int k0, const double (&own)[K], double (&tot)[K]) const {
+        if constexpr (MODE == kCluster) {
+            const int lane = threadIdx.x & 31, half = lane >> 4, sl = lane & 15;
+#pragma unroll
+            for (int k = 0; k < K; k += 2) {
+                const int kk = k + half;
+                double x = (sl < C && kk < K) ? ex[(k0 + kk) * kSMaxC + sl] : 0.0;
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                tot[k] = __shfl_sync(0xffffffffu, x, 0);
+                if (k + 1 < K) tot[k + 1] = __shfl_sync(0xffffffffu, x, 16);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) tot[k] = own[k];
+        }
+    }
     __device__ __forceinline__ void total(const double *ex, int k, double own, double &tot, double &before) const {
         if constexpr (MODE == kCluster) {   // lane-parallel over the C <= 16 CTAs (fixed shfl-up tree)
             const int lane = threadIdx.x & 31;
@@ -812,11 +832,11 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
         double T[2], off[2], sig[2], G11, G12, G22, dm;
         tm.total(tm.exA, 0, tot[0], T[0], off[0]);
         tm.total(tm.exA, 1, tot[1], T[1], off[1]);
-        tm.total(tm.exA, 2, pp[0], sig[0], dm);
-        tm.total(tm.exA, 3, pp[1], sig[1], dm);
-        tm.total(tm.exA, 4, pp[2], G11, dm);
-        tm.total(tm.exA, 5, pp[3], G12, dm);
-        tm.total(tm.exA, 6, pp[4], G22, dm);
+        {
+            double tt[5];
+            tm.template totals_only<5>(tm.exA, 2, pp, tt);
+            sig[0] = tt[0]; sig[1] = tt[1]; G11 = tt[2]; G12 = tt[3]; G22 = tt[4];
+        }
         // phase 2: W = Q P~ - (Q 1) pi; dots with Q (held in wn) and W; push W (into v)
         double hp[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // h11 h12 h21 h22 g11 g12 g22
 #pragma unroll
@@ -849,8 +869,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
         if constexpr (MODE == kCluster) {
             tm.template sum<7>(hp);
             tm.template exchange<7>(tm.exB, hp);
-#pragma unroll
-            for (int i = 0; i < 7; ++i) tm.total(tm.exB, i, hp[i], h[i], dm);
+            tm.template totals_only<7>(tm.exB, 0, hp, h);
         } else {                                      // one barrier orders the pushes and the partials
             warp_sums_to<7>(hp, wpart);
             tm.barrier();
