@@ -327,10 +327,15 @@ __device__ double small_scan(double (&v)[kSEl], double *wt) {
 __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ fluxes, int N, VecPtrs b,
                                                    int64_t vstride) {
     __shared__ double wt[65];
-    extern __shared__ double rev[];      // [blockDim * 8]: w reversed, then its inclusive scan
+    __shared__ FluxDev fs;               // the profile's parameters: shared-memory loads in the erfc loops
+    extern __shared__ double rev[];      // [blockDim * 8]: w reversed, then its inclusive scan; then
+                                         // [blockDim * 8]: lambda_j (own slots)
     const int nslot = (int)blockDim.x * kSEl;
+    double *lams = rev + nslot;
     const int m = blockIdx.x;
-    const FluxDev &f = fluxes[m];
+    if (threadIdx.x == 0) fs = fluxes[m];
+    __syncthreads();
+    const FluxDev &f = fs;
     const int e0 = threadIdx.x * kSEl;
     double *F = b.F + m * vstride, *lam = b.lam + m * vstride, *w = b.w + m * vstride;
     double *invD = b.invD + m * vstride, *invZ = b.invZ + m * vstride;
@@ -366,6 +371,7 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
             const double lm = flux_rate(f, bin_centre(f, e));
             F[e] = Fe;
             lam[e] = lm;
+            lams[e0 + i] = lm;
             wj = lm * exp(-Fe);
             w[e] = wj;
         }
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
             bad |= !(D > 0.0 && isfinite(D));
             const double id = 1.0 / D;
             invD[r] = id;
-            invZ[r] = id * (wv[i] / lam[r]);                  // e^{-F_r} / D_r
+            invZ[r] = id * (wv[i] / lams[e0 + i]);            // e^{-F_r} / D_r
         }
     }
     if (threadIdx.x == 0) {
@@ -422,12 +428,12 @@ cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs bas
     if (N + 1 <= kST * kSEl) {                         // one CTA per profile, one launch
         int threads = (N + 1 + kSEl - 1) / kSEl;     // just enough threads for the N + 1 slots
         threads = (threads + 31) / 32 * 32;
-        const int smem = (int)(sizeof(double) * threads * kSEl);
+        const int smem = (int)(sizeof(double) * threads * kSEl * 2);
         static std::once_flag once;         // once per process (thread-safe; not in captured launches)
         static cudaError_t attr = cudaSuccess;
         std::call_once(once, [] {
             attr = cudaFuncSetAttribute((const void *)k_vec_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)(sizeof(double) * kST * kSEl));
+                                        (int)(sizeof(double) * kST * kSEl * 2));
         });
         if (attr != cudaSuccess) return attr;
         k_vec_small<<<M, threads, smem, s>>>(d_flux, N, base, vstride);
