@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_lambda2(const StructArgs a
             const double pv[7] = {tot[0], tot[1], pp[0], pp[1], pp[2], pp[3], pp[4]};
             tm.template exchange<7>(tm.exA, pv);
         }
-        double T[2], off[2], sig[2], G11, G12, G22, dm;
+        double T[2], off[2], sig[2], G11, G12, G22;
         tm.total(tm.exA, 0, tot[0], T[0], off[0]);
         tm.total(tm.exA, 1, tot[1], T[1], off[1]);
         {
