@@ -339,21 +339,23 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
     const int e0 = threadIdx.x * kSEl;
     double *F = b.F + m * vstride, *lam = b.lam + m * vstride, *w = b.w + m * vstride;
     double *invD = b.invD + m * vstride, *invZ = b.invZ + m * vstride;
-    // The erfc / exp evaluations run in ROLLED loops through the thread's own shared-memory slots:
-    // unrolled 8x with the inlined fp64 erfc / exp the kernel was ~12k SASS instructions and stalled
-    // on instruction fetch (ncu: no_instructions 33%, 52.6 us for c3's 64 profiles).
+    // The erfc / exp evaluations run in rolled loops STRIDED over the CTA's threads (one element per
+    // thread and round, coalesced stores; the CTA has up to 1024 threads, more than the (N + 1) / 8 the
+    // scans need) through shared memory; the scans then take 8 consecutive slots per thread. Unrolled
+    // 8x per thread the inlined fp64 erfc / exp stalled on instruction fetch, and 8 serial evaluations
+    // per thread were the latency of the whole kernel (35 us for c3's profiles).
     // masses (N + 1 of them) and their inclusive scan: F_j = F(s_j), Lambda = F(t_r)
 #pragma unroll 1
-    for (int i = 0; i < kSEl; ++i) {
-        const int e = e0 + i;
+    for (int e = threadIdx.x; e < nslot; e += blockDim.x) {
         double mv = 0.0;
         if (e <= N) {
             const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
             const double hi = e == N ? f.t_r : bin_centre(f, e);
             mv = flux_mass(f, lo, hi);
         }
-        rev[e0 + i] = mv;
+        rev[e] = mv;
     }
+    __syncthreads();
     double wv[kSEl];
 #pragma unroll
     for (int i = 0; i < kSEl; ++i) wv[i] = rev[e0 + i];
@@ -361,22 +363,23 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
     const double eL = exp(-Lam);
 #pragma unroll
     for (int i = 0; i < kSEl; ++i) rev[e0 + i] = wv[i];   // F_j (own slots)
-    // lambda_j, w_j = lambda_j e^{-F_j}
+    __syncthreads();
+    // lambda_j, w_j = lambda_j e^{-F_j} (strided, as the masses)
 #pragma unroll 1
-    for (int i = 0; i < kSEl; ++i) {
-        const int e = e0 + i;
+    for (int e = threadIdx.x; e < nslot; e += blockDim.x) {
         double wj = 0.0;
         if (e < N) {
-            const double Fe = rev[e0 + i];
+            const double Fe = rev[e];
             const double lm = flux_rate(f, bin_centre(f, e));
             F[e] = Fe;
             lam[e] = lm;
-            lams[e0 + i] = lm;
+            lams[e] = lm;
             wj = lm * exp(-Fe);
             w[e] = wj;
         }
-        rev[e0 + i] = wj;
+        rev[e] = wj;
     }
+    __syncthreads();
 #pragma unroll
     for (int i = 0; i < kSEl; ++i) wv[i] = rev[e0 + i];
     __syncthreads();                             // own slots read: rev[] now takes w reversed
@@ -426,8 +429,8 @@ cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs bas
     const int ntN = (N + kScanTile - 1) / kScanTile;   // tiles over the N bins
     if (nt > 4096) return cudaErrorInvalidValue;
     if (N + 1 <= kST * kSEl) {                         // one CTA per profile, one launch
-        int threads = (N + 1 + kSEl - 1) / kSEl;     // just enough threads for the N + 1 slots
-        threads = (threads + 31) / 32 * 32;
+        int threads = N + 1 < kST ? N + 1 : kST;     // one element per thread for the transcendentals
+        threads = (threads + 31) / 32 * 32;          // (the scans need only (N + 1) / 8 of them)
         const int smem = (int)(sizeof(double) * threads * kSEl * 2);
         static std::once_flag once;         // once per process (thread-safe; not in captured launches)
         static cudaError_t attr = cudaSuccess;
