@@ -154,6 +154,9 @@ splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, sp
  * up to 32 per pass). P0_store: device, room for n_store matrices of N x ld (dtype dt) with
  * consecutive stride N * ld; unique (S, B) pairs are processed n_store at a time.
  * pi: device fp64 [n_items * N] (item-major). info: host [n_items], may be NULL.
+ * P0_store == NULL: matrix-free, the items go to splidar_stationary_structured (same items, same pi to
+ * rounding; dt, mode, n_store and ld are ignored; ws: splidar_structured_workspace_bytes(N, unique
+ * (S, B) pairs, n_items) bytes).
  * Returns SPLIDAR_ENOCONV if any item did not converge (its pi is the last iterate). */
 splidar_status splidar_sweep(const splidar_flux *shape, int32_t n_items, const double *S,
                              const double *B, const double *t_d, splidar_dtype dt, splidar_entry mode,

@@ -738,7 +738,11 @@ splidar_status splidar_sweep(const splidar_flux *shape, int32_t n_items, const d
                              const double *t_d, splidar_dtype dt, splidar_entry mode, double tol, int32_t max_iter,
                              double *pi, void *P0_store, int32_t n_store, int64_t ld, void *ws, size_t ws_bytes,
                              splidar_solve_info *info, void *stream) {
-    if (!shape || n_items < 1 || !S || !B || !t_d || !pi || n_store < 1) return SPLIDAR_EINVAL;
+    if (!shape || n_items < 1 || !S || !B || !t_d || !pi) return SPLIDAR_EINVAL;
+    if (!P0_store)   // matrix-free: the same items on the structured operator (f2), no N^2 storage
+        return splidar_stationary_structured(shape, n_items, S, B, t_d, tol, max_iter, pi, ws, ws_bytes, info,
+                                             stream);
+    if (n_store < 1) return SPLIDAR_EINVAL;
     if (mode != SPLIDAR_ENTRY_FACTORED && mode != SPLIDAR_ENTRY_EXP) return SPLIDAR_EINVAL;
     const int N = shape->n_bins;
     splidar_status st;

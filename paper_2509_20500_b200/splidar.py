@@ -270,8 +270,9 @@ def stationary(P0: torch.Tensor, t_r: float, t_d: float, tol: float = 1e-12, max
 
 def sweep(shape, S, B, t_d, dtype=torch.float64, mode: str = "factored", tol: float = 1e-12,
           max_iter: int = 10 ** 6, n_store: int | None = None, P0_store: torch.Tensor | None = None,
-          ws: torch.Tensor | None = None, stream=None, check: bool = True):
+          ws: torch.Tensor | None = None, stream=None, check: bool = True, matrix_free: bool = False):
     """Steps 1-4 for (S[m], B[m], t_d[m]) items; shape.signal are relative pulse weights.
+    matrix_free=True: no P~0 is stored (splidar_sweep with P0_store = NULL: the structured operator).
     Returns (pi [M, N] fp64 device tensor, list of info dicts)."""
     S = np.ascontiguousarray(S, dtype=np.float64).reshape(-1)
     B = np.ascontiguousarray(B, dtype=np.float64).reshape(-1)
@@ -280,6 +281,17 @@ def sweep(shape, S, B, t_d, dtype=torch.float64, mode: str = "factored", tol: fl
     if B.size != M or T.size != M:
         raise SplidarError(EINVAL, "sweep: S, B, t_d must have equal length")
     N = int(shape.n_bins)
+    if matrix_free:
+        n_unique = len({(float(s), float(b)) for s, b in zip(S, B)})
+        ws = ws if ws is not None else structured_workspace(N, n_unique, M)
+        pi = torch.empty((M, N), dtype=torch.float64, device=ws.device)
+        infos = (SolveInfo * M)()
+        fa = _FluxArg(shape)
+        st = _lib().splidar_sweep(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data, F64,
+                                  _MODES[mode], float(tol), int(max_iter), pi.data_ptr(), None, 0, 0,
+                                  ws.data_ptr(), ws.numel(), infos, _stream(stream))
+        _check(st, "splidar_sweep", allow=() if check else (ENOCONV,))
+        return pi, [i.as_dict() for i in infos]
     n_unique = len({(float(s), float(b)) for s, b in zip(S, B)})
     if P0_store is None:
         n_store = n_store or n_unique

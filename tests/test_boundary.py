@@ -219,6 +219,15 @@ def test_sweep_rejects(spl):
     st = lib.splidar_sweep(C.byref(fa.s), 0, S.ctypes.data, B.ctypes.data, T.ctypes.data, spl.F64, 0, 1e-12, 100,
                            FAKE, FAKE, 2, 256, FAKE, 1 << 30, None, None)
     assert st == spl.EINVAL
+    # P0_store = NULL: matrix-free (structured) path, validated as splidar_stationary_structured
+    need = lib.splidar_structured_workspace_bytes(256, 2, 2)
+    st = lib.splidar_sweep(C.byref(fa.s), 2, S.ctypes.data, B.ctypes.data, T.ctypes.data, spl.F64, 0, 1e-12, 100,
+                           FAKE, None, 0, 0, FAKE, need - 1, None, None)
+    assert st == spl.ENOSPACE
+    B0 = np.array([0.1, 0.0])
+    st = lib.splidar_sweep(C.byref(fa.s), 2, S.ctypes.data, B0.ctypes.data, T.ctypes.data, spl.F64, 0, 1e-12, 100,
+                           FAKE, None, 0, 0, FAKE, need, None, None)
+    assert st == spl.EINVAL
 
 
 def test_parity_cases_are_well_formed():

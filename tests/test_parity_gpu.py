@@ -410,6 +410,26 @@ def test_sweep_chunked_store_and_many_dead_times(spl):
             assert np.sum(np.abs(got[m] - want)) <= TOL_PI64
 
 
+@pytest.mark.parametrize("N", [700, 9001])
+def test_sweep_matrix_free_equals_dense(spl, N):
+    """splidar_sweep with P0_store = NULL (matrix-free: the structured operator) gives the dense sweep's
+    pi (<= 1e-13 L1), the same shifts and Lambda, iterations +-1 (R25), for mixed (S, B, t_d) items
+    including repeated profiles; N = 9001 takes cluster teams."""
+    rng = np.random.default_rng(N)
+    base = random_flux(rng, N, 2)
+    shape = Flux(base.t_r, N, base.tau, base.sigma, (0.7, 0.3), 1.0)
+    S = list(rng.uniform(0.1, 5.0, 5)) + [2.0] * 4
+    B = list(rng.uniform(0.05, 1.5, 5)) + [0.7] * 4
+    T = list(rng.uniform(0.0, 250.0, 5)) + [10.0, 75.0, 200.0, 310.0]
+    pd, infd = spl.sweep(shape, S, B, T)
+    pf, inff = spl.sweep(shape, S, B, T, matrix_free=True)
+    for m in range(len(S)):
+        assert inff[m]["converged"] and inff[m]["shift_l"] == infd[m]["shift_l"]
+        assert abs(inff[m]["iters"] - infd[m]["iters"]) <= 1
+        assert abs(inff[m]["lambda_total"] - infd[m]["lambda_total"]) <= 1e-13 * infd[m]["lambda_total"]
+        assert np.sum(np.abs(_np(pf[m]) - _np(pd[m]))) <= 1e-13, m
+
+
 @pytest.mark.parametrize("dtype,nv", [(torch.float64, 1), (torch.float64, 5), (torch.float32, 1)])
 def test_eager_mode_equals_graph(spl, monkeypatch, dtype, nv):
     """SPLIDAR_EAGER=1 (host loop over the same kernels, for profilers) gives bit-identical pi and the same
