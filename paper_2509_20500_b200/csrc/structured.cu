@@ -475,12 +475,8 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_solve(const StructArgs a) 
         double v[1][E], tt[1], dp[1];
 #pragma unroll
         for (int e = 0; e < E; ++e) v[0][e] = xbuf[P.loc(e)] * (REG ? idr[REG ? e : 0] : ids[P.loc(e)]);
-        tm.template scan_sum<1, E, 1>(v, tt, dwarp, dp);
-        const double tot = tt[0], dpart = dp[0];
-        {
-            const double pv[2] = {tot, dpart};
-            tm.template exchange<2>(tm.exA, pv);
-        }
+        tm.template scan_sum<1, E, 1>(v, tt, dwarp, dp);   // its closing barrier also orders the xbuf
+        const double tot = tt[0], dpart = dp[0];           // reads before this product's pushes
         double T, off, dummy;
         tm.total(tm.exA, 0, tot, T, off);
         if (k > 0) {
@@ -958,7 +954,7 @@ __global__ void __launch_bounds__(kSMaxT, 1) k_struct_mixing(const StructArgs a)
         for (int e = 0; e < E; ++e) v[0][e] = xbuf[P.loc(e)] * ids[P.loc(e)];
         tm.template scan_sum<1, E, 1>(v, tt, twarp, tp);
         const double tot = tt[0], tvpart = tp[0];
-        {
+        if constexpr (MODE == kCluster) {   // warp / CTA teams: scan_sum's closing barrier suffices
             const double pv[2] = {tot, tvpart};
             tm.template exchange<2>(tm.exA, pv);
         }
