@@ -34,7 +34,8 @@ can exceed a copy by ~6% (probe: 6.86 / 6.95 TB/s), so fractions slightly above 
 {dense_row('bench_c2','c2 fp64 (6 items, L2-resident; fused solver, CUDA-graph step)')}
 {dense_row('bench_c1','c1 fp64 (L2-resident; fused solver, CUDA-graph step)')}
 
-Box to box the default line moved between 291 and 316 solves/s this round at identical code: the
+Box to box the default line moved between 291 and 316 solves/s this round at identical code (the final
+code: 294.7 at 1717 MHz in the table above, 314.6 at 1957 MHz on another box, `profiles/r01/bench_c5_box2.json`): the
 17-vector pass is at the DMMA / HBM balance point (ncu: tensor DMMA subpipe 74% busy, DRAM 80%), so it
 follows the power-capped SM clock, unlike a pure read stream (this line's box held {c5['clocks']['sm_mhz']:.0f} MHz under load):
 one 17-vector solve launched after idle takes 1.278 ms per iteration (the ncu GEMV + check times),
