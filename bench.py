@@ -792,13 +792,19 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        samples = [run_oracle_sample(args) for _ in range(max(1, min(args.steps, 3)))]
+        # W untimed warm-up samples, then K timed ones (each a bounded sample of the workload, ~1 s at
+        # c5); the value is the median, ms_per_step the extrapolated time of one full step
+        for _ in range(max(0, args.warmup)):
+            run_oracle_sample(args)
+        samples = [run_oracle_sample(args) for _ in range(max(1, min(args.steps, 10)))]
         v = statistics.median(s["value"] for s in samples)
-        w, _ = workload_items(args.workload)
+        w, groups_ref = workload_items(args.workload)
+        n_step = sum(len(t) for _, t in groups_ref)
         cb = dict(samples[0])
         cb["value"] = v
         line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": len(samples),
-                "warmup": 0, "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "warmup": max(0, args.warmup), "ms_per_step": 1e3 * n_step / v, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
                 "dtype": args.dtype, "data": "synthetic", "impl": "reference",
                 "config": {"workload": f"{args.workload}: {w.description}", "n_bins": w.n_bins},
                 "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
