@@ -475,3 +475,40 @@ def test_max_size_dense(spl):
     assert np.sum(np.abs(_np(pi) - ref)) <= TOL_PI64
     del P0
     torch.cuda.empty_cache()
+
+
+def test_concurrent_streams_reentrant(spl):
+    """The library is re-entrant for distinct (stream, workspace) pairs: a dense plan (graph path), a
+    structured plan and a stored-matrix lambda_2 enqueued on three streams at once give bit-identical
+    results to the same calls run one after another on the default stream."""
+    f = random_flux(np.random.default_rng(77), 3000, 2)
+    tds = [20.0, 140.0, 260.0]
+    P0 = spl.build_base(f)
+    shape, S, B = spl.flux_items(f)
+    # sequential references
+    plan = spl.Plan(P0, f.t_r, [tds])
+    plan.execute()
+    ref_dense = plan.pi.clone()
+    plan.close()
+    ref_struct, _ = spl.stationary_structured(shape, np.repeat(S, 3), np.repeat(B, 3), tds)
+    ref_l2 = spl.second_eigenvalue_dense(P0, f.t_r, tds[0], ref_struct[0].contiguous())
+    torch.cuda.synchronize()
+    # concurrent: three streams, three workspaces
+    s1, s2, s3 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        p1 = spl.Plan(P0, f.t_r, [tds], stream=s1)
+        p1.launch(stream=s1)
+    with torch.cuda.stream(s2):
+        sp = spl.StructPlan("solve", shape, np.repeat(S, 3), np.repeat(B, 3), tds, stream=s2)
+        sp.launch(stream=s2)
+    with torch.cuda.stream(s3):
+        l2 = spl.second_eigenvalue_dense(P0, f.t_r, tds[0], ref_struct[0].contiguous(), stream=s3)
+    p1.info(stream=s1)
+    sp.info(stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(p1.pi, ref_dense)
+    assert torch.equal(sp.pi, ref_struct)
+    assert l2 == ref_l2
+    p1.close()
+    sp.close()
