@@ -155,3 +155,19 @@ def test_dense_lambda2_deterministic_and_noconv(spl):
     assert not c["converged"] and c["iters"] == 2
     with pytest.raises(spl.SplidarError):
         spl.second_eigenvalue_dense(P0, f.t_r, 75.0, pi, max_iter=2)
+
+
+def test_dense_equals_structured_max_n(spl):
+    """N = 65536 (a 34 GB fp64 matrix; the structured lambda_2 on a 16-CTA cluster, its largest team):
+    the two independent lambda_2 computations agree."""
+    f = Flux(100.0, 65536, (30.0, 70.0), (0.05, 0.2), (1.5, 0.7), 0.9)
+    td = 123.4
+    shape, S, B = spl.flux_items(f)
+    pi, _ = spl.stationary_structured(shape, S, B, [td])
+    ref = spl.second_eigenvalue(shape, S, B, [td], pi)[0]
+    P0 = spl.build_base(f)
+    got = spl.second_eigenvalue_dense(P0, f.t_r, td, pi[0].contiguous())
+    del P0
+    torch.cuda.empty_cache()
+    assert got["converged"] and ref["converged"]
+    assert abs(spl.lambda2_of(ref) - got["lambda2"]) <= 1e-10, (got, ref)
