@@ -266,11 +266,14 @@ def run_ours(args, rank, world, dev):
         per_m = np.array([i["iters"] for i in plan_info]).reshape(p.M, p.V).max(axis=1)
         launches_gemv += int(per_m.max())
         gemv_bytes += int(per_m.sum()) * N * N * b
+    # parameter upload + step-1 vector kernels (k_vec_small when N + 1 <= 8192, else k_vec_a..e) +
+    # k_build, then per plan: one fused launch, or init + (GEMV + check) per iteration + finish
+    prelude = 1 + (1 if N + 1 <= 8192 else 5) + 1
     if graphed:
-        per_step_launches = 3 + len(st.plans)
+        per_step_launches = prelude + len(st.plans)
     else:
-        per_step_launches = 3 + sum(2 + 2 * int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
-                                    for pi, p in zip(infos, st.plans))
+        per_step_launches = prelude + sum(2 + 2 * int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
+                                          for pi, p in zip(infos, st.plans))
     hbm, hbm_src = load_peaks()
     traffic = load_traffic(args.workload, args.dtype)
     K = args.steps
