@@ -256,7 +256,10 @@ splidar_status splidar_second_eigenvalue_dense(const void *P0, int32_t n_bins, i
 
 /* Structured plans: the items of splidar_stationary_structured (kind SPLIDAR_SPLAN_SOLVE) or
  * splidar_second_eigenvalue (kind SPLIDAR_SPLAN_LAMBDA2; pi is then the input) validated and uploaded
- * once; splidar_splan_launch only enqueues (step-1 vectors + the kernel, async, re-runnable);
+ * once; splidar_splan_launch only enqueues (step-1 vectors + the kernel, async, re-runnable; the
+ * first launch is eager, the second captures the sequence into a CUDA graph on a private stream and
+ * it and later launches replay it: one cudaGraphLaunch on `stream`; SPLIDAR_SPLAN_GRAPH=0 in the
+ * environment keeps every launch eager; launches of one plan must not overlap);
  * splidar_splan_info synchronises `stream`, fills the per-item info (either pointer may be NULL)
  * and the device time of the last launch's kernel in ms (CUDA events recorded around it on
  * `stream`; may be NULL); SPLIDAR_ENOCONV if an item did not converge. The two calls above are
