@@ -35,7 +35,9 @@ can exceed a copy by ~6% (probe: 6.86 / 6.95 TB/s), so fractions slightly above 
 {dense_row('bench_c1','c1 fp64 (L2-resident; fused solver, CUDA-graph step)')}
 
 Box to box the default line moved between 291 and 316 solves/s this round at identical code (the final
-code: 294.7 at 1717 MHz in the table above, 314.6 at 1957 MHz on another box, `profiles/r01/bench_c5_box2.json`): the
+code: 294.7 at 1717 MHz and 609 W peak board power in the table above, 314.6 at 1957 MHz and 515 W on
+another box, `profiles/r01/bench_c5_box2.json`; both report sw_power_cap, so the boxes differ in power
+draw per clock): the
 17-vector pass is at the DMMA / HBM balance point (ncu: tensor DMMA subpipe 74% busy, DRAM 80%), so it
 follows the power-capped SM clock, unlike a pure read stream (this line's box held {c5['clocks']['sm_mhz']:.0f} MHz under load):
 one 17-vector solve launched after idle takes 1.278 ms per iteration (the ncu GEMV + check times),
