@@ -11,6 +11,7 @@ names = ['bench_c5', 'bench_c5_f32', 'bench_c5_exp', 'bench_c4', 'bench_c3', 'be
          'bench_struct_c5', 'bench_struct_c3', 'bench_struct_c4', 'bench_struct_grid', 'bench_spec_grid', 'bench_spec_c5',
          'bench_spec_c1', 'bench_eq4_c5', 'bench_eq4_c3', 'bench_mc_c1', 'bench_mc_grid']
 d = {n: L(n) for n in names}
+d2 = L('bench_c5_box2')
 def dense_row(name, label):
     x = d[name]; r = x['roofline']; b = x['roofline_build']
     return (f"| {label} | {x['value']:.1f} | {x['ms_per_step']:.3f} | {b['achieved']:.0f} ({b['frac']:.3f}) | "
@@ -35,9 +36,9 @@ can exceed a copy by ~6% (probe: 6.86 / 6.95 TB/s), so fractions slightly above 
 {dense_row('bench_c1','c1 fp64 (L2-resident; fused solver, CUDA-graph step)')}
 
 Box to box the default line moved between 291 and 316 solves/s this round at identical code (the final
-code: 294.7 at 1717 MHz and 609 W peak board power in the table above, 314.6 at 1957 MHz and 515 W on
-another box, `profiles/r01/bench_c5_box2.json`; both report sw_power_cap, so the boxes differ in power
-draw per clock): the
+code: {c5['value']:.1f} at {c5['clocks']['sm_mhz']:.0f} MHz and {c5['clocks'].get('power_w_max', 0):.0f} W peak board power in the table above, {d2['value']:.1f} at
+{d2['clocks']['sm_mhz']:.0f} MHz and {d2['clocks'].get('power_w_max', 0):.0f} W on another box (`profiles/r01/bench_c5_box2.json`), 294.7 at 1717 MHz and
+609 W on a third; all report sw_power_cap, so the boxes differ in power draw per clock): the
 17-vector pass is at the DMMA / HBM balance point (ncu: tensor DMMA subpipe 74% busy, DRAM 80%), so it
 follows the power-capped SM clock, unlike a pure read stream (this line's box held {c5['clocks']['sm_mhz']:.0f} MHz under load):
 one 17-vector solve launched after idle takes 1.278 ms per iteration (the ncu GEMV + check times),
