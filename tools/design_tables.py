@@ -45,7 +45,9 @@ one 17-vector solve launched after idle takes 1.278 ms per iteration (the ncu GE
 back-to-back steps ~1.38 ms, and the eager host loop
 adds only 41 us per iteration to the graph (`tools/graph_overhead.py`), so the graph loop itself costs
 little. Moving 9 of the 17 vectors to plain DFMA (8 on DMMA) to unload the tensor pipe was measured
-and rejected: 1.68 ms per pass, issue-bound (FP64 pipe 33%, DMMA 29%). Before this round's small-N work c1 / c2 ran
+and rejected: 1.68 ms per pass, issue-bound (FP64 pipe 33%, DMMA 29%). Larger FP64 MMA shapes do not
+help either: ptxas lowers m16n8k4, m16n8k8 and m16n8k16 .f64 alike to the native DMMA.8x8x4 (SASS), and
+all three run at 37.1 TFLOP/s in `tools/probe/dmma_probe.cu`. Before this round's small-N work c1 / c2 ran
 at 3321 / 12110 solves/s (0.30 / 0.50 ms per step). The c5 step is close to its floor: 40 passes x
 max(8.59 GB / 6.95 TB/s, 16 x 2 x N^2 flops / 37 TFLOP/s) = 40 x 1.24 ms = 49.4 ms of the
 {c5['ms_per_step']:.1f} ms step. The GEMV `achieved` divides algorithmic bytes (N^2 b per launch per active
