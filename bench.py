@@ -42,7 +42,8 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "grid"])
-    p.add_argument("--path", default="dense", choices=["dense", "structured", "spectral", "eq4", "mc"],
+    p.add_argument("--path", default="dense", choices=["dense", "structured", "spectral", "spectral_dense", "eq4",
+                                                       "mc"],
                    help="dense: the north-star path (P~0 in HBM + GEMV power iteration); structured: "
                         "SURVEY f2 matrix-free solve; spectral: SURVEY f1 solve + lambda_2; eq4: SURVEY f4 "
                         "element-wise Eq. 4 construction (with Theorem 2's construction timed beside it); mc: "
@@ -373,6 +374,82 @@ def run_e2e(args, w, groups, st, world):
             "d2h_bytes_per_step": n_solves * N * 8,
             "note": "host wall clock; includes plan (CUDA graph) instantiation, the theta upload and the pi "
                     "copy to pinned host memory every step"}
+
+
+# ------------------------------------------------------------------------------- stored-matrix lambda_2
+def run_spectral_dense(args, rank, world, dev):
+    """f1 on a stored matrix: per step, build the workload's first P~0, its stationary pi (dense GEMV
+    plan) and lambda_2 by the two-vector GEMV subspace iteration (splidar_second_eigenvalue_dense).
+    Roofline: the two-vector GEMV, N^2 b bytes per product (timed by CUDA events around the lambda_2
+    call: products x bytes / that time, a lower bound on the kernel's own rate)."""
+    import torch
+    import paper_2509_20500_b200 as spl
+    w, groups = workload_items(args.workload, rank, world)
+    f, td = w.items[0].flux, w.items[0].t_d              # the workload's own item (c5: t_d = 430)
+    N = f.n_bins
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    b = 8 if args.dtype == "f64" else 4
+    P0 = spl.empty_matrix(N, dt)
+    ws_b = spl.workspace(N, 1, 1)
+    from paper_2509_20500_b200 import splidar as _binding
+    nb = _binding._lib().splidar_spectral_dense_workspace_bytes(N)
+    t_ws = torch.empty(nb + 256, dtype=torch.uint8, device="cuda")
+    ws_l2 = t_ws[(-t_ws.data_ptr()) % 256:][:nb]
+    plan = spl.Plan(P0, f.t_r, [[td]], tol=1e-12)
+    stream = torch.cuda.current_stream()
+    res = {}
+
+    def step():
+        spl.build_base(f, dt, out=P0, ws=ws_b)
+        plan.launch()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res["l2"] = spl.second_eigenvalue_dense(P0, f.t_r, td, plan.pi[0, 0], ws=ws_l2)
+        e1.record(stream)
+        res["ev"] = (e0, e1)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(dev)
+    time.sleep(0.25)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l2_ms = []
+    t_total = 0.0
+    for _ in range(args.steps):
+        t0.record(stream)
+        step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        t_total += t0.elapsed_time(t1) / 1e3
+        l2_ms.append(res["ev"][0].elapsed_time(res["ev"][1]))
+    clk = clocks.stop()
+    from paper_2509_20500_b200.shard import max_over_ranks
+    t_total = max_over_ranks([t_total], device="cuda")[0]
+    info = res["l2"]
+    K = args.steps
+    l2_s = statistics.mean(l2_ms) / 1e3
+    achieved = info["iters"] * N * N * b / l2_s / 1e9
+    hbm, hbm_src = load_peaks()
+    return {
+        "metric": "spectral analyses/s on a stored matrix (pi + lambda_2; SURVEY f1 via the multi-vector GEMV)",
+        "value": world * K / t_total, "unit": "analyses/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": t_total / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic (seeded BASELINE.json flux parameters)",
+        "config": {"workload": f"{args.workload}: {w.description}", "n_bins": N, "t_d": td,
+                   "step": "build P~0 + dense pi (GEMV plan) + lambda_2 (two-vector GEMV subspace iteration)",
+                   "l2": "matrix > L2 for N >= 4096" if N * N * b > 126e6 else "L2-resident"},
+        "lambda2": {"modulus": info["modulus"], "phase": info["phase"], "iters": info["iters"],
+                    "converged": info["converged"]},
+        "roofline": {"bound": "hbm", "kernel": "k_power_step<T, 2>", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": hbm_src,
+                     "algorithmic_bytes_per_launch": N * N * b, "lambda2_ms_per_step": statistics.mean(l2_ms)},
+        "clocks": clk, "e2e": None,
+        "gpu_launches": K * ((1 + (1 if N + 1 <= 8192 else 5) + 1) + 0 + 3 * int(info["iters"]) + 1),
+        "impl": "ours", "lib": spl.lib_path(),
+    }
 
 
 # ------------------------------------------------------------------------------- structured paths
@@ -833,6 +910,8 @@ def main():
         line = run_mc(args, rank, world, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = run_oracle_mc(args)
+    elif args.path == "spectral_dense":
+        line = run_spectral_dense(args, rank, world, dev)
     elif args.path == "eq4":
         line = run_eq4(args, rank, world, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:

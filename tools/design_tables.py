@@ -9,7 +9,7 @@ i = s.index('**Headline (north-star dense path; default bench line')
 j = s.index('## 7. Multi-GPU')
 names = ['bench_c5', 'bench_c5_f32', 'bench_c5_exp', 'bench_c4', 'bench_c3', 'bench_c2', 'bench_c1', 'bench_ref_c5',
          'bench_struct_c5', 'bench_struct_c3', 'bench_struct_c4', 'bench_struct_grid', 'bench_spec_grid', 'bench_spec_c5',
-         'bench_spec_c1', 'bench_eq4_c5', 'bench_eq4_c3', 'bench_mc_c1', 'bench_mc_grid']
+         'bench_spec_c1', 'bench_eq4_c5', 'bench_eq4_c3', 'bench_mc_c1', 'bench_mc_grid', 'bench_spec_dense_c5']
 d = {n: L(n) for n in names}
 d2 = L('bench_c5_box2')
 def dense_row(name, label):
@@ -70,6 +70,7 @@ sample, see the line's `cpu_baseline.sample`; one core builds {c5['cpu_baseline'
 | f2 | grid (8192 items, N = 256) | {g('bench_struct_grid')/1e6:.1f} M solves/s | {g('bench_struct_grid','ms_per_step'):.3f} | {rf('bench_struct_grid','achieved'):.2f} TFLOP/s ({rf('bench_struct_grid','frac'):.3f}) | {d['bench_struct_grid']['cpu_baseline']['value']:.0f} |
 | f1 spectral (pi + lambda_2) | grid | {g('bench_spec_grid')/1e6:.2f} M analyses/s | {g('bench_spec_grid','ms_per_step'):.2f} | `k_struct_lambda2`, {rf('bench_spec_grid','achieved'):.2f} TFLOP/s ({rf('bench_spec_grid','frac'):.3f}) | {d['bench_spec_grid']['cpu_baseline']['value']:.1f} (dense eigvals) |
 | f1 | c5 (17 items) | {g('bench_spec_c5'):,.0f} analyses/s | {g('bench_spec_c5','ms_per_step'):.2f} | {rf('bench_spec_c5','achieved'):.2f} TFLOP/s | — (no dense spectrum at N = 32768) |
+| f1 on the stored matrix (`--path spectral_dense`) | c5 item (t_d = 430): build + dense pi + lambda_2 | {g('bench_spec_dense_c5'):.1f} analyses/s | {g('bench_spec_dense_c5','ms_per_step'):.1f} | `k_power_step<double, 2>`, {rf('bench_spec_dense_c5','achieved'):.0f} GB/s ({rf('bench_spec_dense_c5','frac'):.2f} of copy HBM) | — |
 | f4 element-wise Eq. 4 | c5 (4 matrices of N = 32768, K = 2) | {g('bench_eq4_c5'):.3g} entries/s; Theorem 2 on the same GPU {d['bench_eq4_c5']['theorem2_same_gpu']['entries_per_s']:.3g} ({d['bench_eq4_c5']['theorem2_same_gpu']['speedup_vs_eq4']:.1f}x with the permutation materialised; ~28x with it folded) | {g('bench_eq4_c5','ms_per_step'):.1f} | `k_build_eq4`, {rf('bench_eq4_c5','achieved'):.1f} TFLOP/s ({rf('bench_eq4_c5','frac'):.2f}), FP64 pipe {rf('bench_eq4_c5','fp64_pipe_pct_ncu'):.0f}% | {d['bench_eq4_c5']['cpu_baseline']['value']:.3g} entries/s |
 | f4 | c3 (64 matrices of N = 4096, K = 1) | {g('bench_eq4_c3'):.3g} entries/s; Theorem 2: {d['bench_eq4_c3']['theorem2_same_gpu']['entries_per_s']:.3g} ({d['bench_eq4_c3']['theorem2_same_gpu']['speedup_vs_eq4']:.1f}x) | {g('bench_eq4_c3','ms_per_step'):.1f} | {rf('bench_eq4_c3','achieved'):.1f} TFLOP/s ({rf('bench_eq4_c3','frac'):.2f}) | {d['bench_eq4_c3']['cpu_baseline']['value']:.3g} |
 | f3 Monte Carlo | grid 16 x 16 x 2 items x 25 runs x 50,000 cycles (P:205), n_split {d['bench_mc_grid']['config']['n_split']} | {g('bench_mc_grid'):.3g} registrations/s | {g('bench_mc_grid','ms_per_step'):.0f} | `k_mc`, FP64 pipe {rf('bench_mc_grid','fp64_pipe_pct_ncu'):.0f}% ({rf('bench_mc_grid','achieved'):.2f} TFLOP/s counting DFMA/DADD/DMUL only) | {d['bench_mc_grid']['cpu_baseline']['value']:.3g} (1 core) |
