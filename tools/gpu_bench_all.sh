@@ -15,6 +15,7 @@ run bench_c5_exp --mode exp --no-cpu-baseline
 run bench_ref_c5 --impl reference --steps 1
 for w in c5 c3 c4 grid; do run bench_struct_$w --path structured --workload $w; done
 for w in grid c5 c1; do run bench_spec_$w --path spectral --workload $w; done
+for w in c5 c4; do run bench_spec_dense_$w --path spectral_dense --workload $w; done
 for w in c5 c3; do run bench_eq4_$w --path eq4 --workload $w; done
 for w in c1 grid; do run bench_mc_$w --path mc --workload $w --steps 3 --warmup 1; done
 # launch list of the default command (cold-cache, serialised: shares only)
