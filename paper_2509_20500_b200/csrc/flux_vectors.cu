@@ -344,16 +344,49 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
     // scans need) through shared memory; the scans then take 8 consecutive slots per thread. Unrolled
     // 8x per thread the inlined fp64 erfc / exp stalled on instruction fetch, and 8 serial evaluations
     // per thread were the latency of the whole kernel (35 us for c3's profiles).
-    // masses (N + 1 of them) and their inclusive scan: F_j = F(s_j), Lambda = F(t_r)
+    // masses (N + 1 of them) and their inclusive scan: F_j = F(s_j), Lambda = F(t_r).
+    // Each mass is flux_mass(lo, hi) (B term, then the pulses in order) with every bin edge's erfc
+    // evaluated once and shared by the two masses it bounds: per pulse, erfc(|z| / sqrt 2) of the upper
+    // edge of mass e goes to lams[e] (free until the lambda loop), and mass e adds the tail-aware
+    // difference of phi_diff from lams[e - 1] and lams[e] (the straddling mass calls erf as phi_diff
+    // does): bitwise the same masses with half the erfc evaluations.
 #pragma unroll 1
     for (int e = threadIdx.x; e < nslot; e += blockDim.x) {
         double mv = 0.0;
         if (e <= N) {
             const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
             const double hi = e == N ? f.t_r : bin_centre(f, e);
-            mv = flux_mass(f, lo, hi);
+            mv = f.B * ((hi - lo) / f.t_r);
         }
         rev[e] = mv;
+    }
+    const double r2 = 0.70710678118654752440;  // 1/sqrt(2)
+#pragma unroll 1
+    for (int k = 0; k < f.k; ++k) {
+        const double is = 1.0 / f.sigma[k];
+        __syncthreads();                         // lams[] of the previous pulse consumed
+#pragma unroll 1
+        for (int e = threadIdx.x; e <= N; e += blockDim.x) {
+            const double hi = e == N ? f.t_r : bin_centre(f, e);
+            const double zh = (hi - f.tau[k]) * is;
+            lams[e] = erfc((zh >= 0.0 ? zh : -zh) * r2);
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int e = threadIdx.x; e <= N; e += blockDim.x) {
+            const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
+            const double hi = e == N ? f.t_r : bin_centre(f, e);
+            const double zl = (lo - f.tau[k]) * is, zh = (hi - f.tau[k]) * is;
+            double ph;
+            if (zl >= 0.0) {
+                ph = 0.5 * ((e == 0 ? erfc(zl * r2) : lams[e - 1]) - lams[e]);
+            } else if (zh <= 0.0) {
+                ph = 0.5 * (lams[e] - (e == 0 ? erfc(-zl * r2) : lams[e - 1]));
+            } else {
+                ph = 0.5 * (erf(zh * r2) + erf(-zl * r2));
+            }
+            rev[e] += f.S[k] * ph;
+        }
     }
     __syncthreads();
     double wv[kSEl];
