@@ -167,20 +167,34 @@ __device__ __forceinline__ double *tile_row(const VecPtrs &b, int M, int which, 
 // (A) masses + lambda; tile-local inclusive scan of the masses -> F (local), tile total.
 __global__ void __launch_bounds__(kT) k_vec_a(const FluxDev *__restrict__ fluxes, int N, int M, VecPtrs b,
                                               int64_t vstride) {
+    static_assert(kE == 1, "one element per thread: the edge sharing below assumes it");
     __shared__ double warp_tot[kT / 32];
+    __shared__ double eh[kT];                  // erfc(|z| / sqrt 2) of each thread's upper bin edge
     const int m = blockIdx.y, tile = blockIdx.x;
     const FluxDev &f = fluxes[m];
     const int e0 = tile * kScanTile + threadIdx.x * kE;
+    // flux_mass(lo, hi) with each bin edge's erfc evaluated once and shared by the two masses it
+    // bounds (as k_vec_small; the tile's first mass evaluates its lower edge itself): bitwise the
+    // same masses with half the erfc evaluations
     double v[kE];
-#pragma unroll
-    for (int i = 0; i < kE; ++i) {
-        const int e = e0 + i;
+    const int e = e0;
+    const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
+    const double hi = e == N ? f.t_r : bin_centre(f, e);
+    v[0] = e <= N ? f.B * ((hi - lo) / f.t_r) : 0.0;
+    const double r2 = 0.70710678118654752440;  // 1/sqrt(2)
+    for (int k = 0; k < f.k; ++k) {
+        const double is = 1.0 / f.sigma[k];
+        const double zl = (lo - f.tau[k]) * is, zh = (hi - f.tau[k]) * is;
+        __syncthreads();                         // eh[] of the previous pulse consumed
+        eh[threadIdx.x] = e <= N ? erfc((zh >= 0.0 ? zh : -zh) * r2) : 0.0;
+        __syncthreads();
         if (e <= N) {
-            const double lo = e == 0 ? 0.0 : bin_centre(f, e - 1);
-            const double hi = e == N ? f.t_r : bin_centre(f, e);
-            v[i] = flux_mass(f, lo, hi);
-        } else {
-            v[i] = 0.0;
+            const double el = threadIdx.x > 0 ? eh[threadIdx.x - 1] : erfc((zl >= 0.0 ? zl : -zl) * r2);
+            double ph;
+            if (zl >= 0.0) ph = 0.5 * (el - eh[threadIdx.x]);
+            else if (zh <= 0.0) ph = 0.5 * (eh[threadIdx.x] - el);
+            else ph = 0.5 * (erf(zh * r2) + erf(-zl * r2));
+            v[0] += f.S[k] * ph;
         }
     }
     const double tot = tile_scan(v, warp_tot);
