@@ -10,6 +10,7 @@ Functions (each follows the passage cited in oracle.c):
   rows_eq4(flux, t_d, r0, r1)                rows [r0, r1) of the same
   entry_eq4_unnorm(flux, t_d, i, j)          one unnormalised Eq. 4 entry
   left_matvec_streamed(flux, t_d, x)         x^T P~ with P~ recomputed row by row (large N)
+  left_matvec_streamed_multi(flux, t_d, X)   the same for the rows of X, each P~ row computed once
   stationary_dense(P~), stationary_power(P~) pi P~ = pi
   monte_carlo(flux, t_d, ...)                continuous-time detection process of P:60
   second_eigenvalue(P), mixing_steps(P, pi), bin_trajectory(P, start, bin, steps)   §4
@@ -60,6 +61,7 @@ def lib():
             "oracle_rows_eq4": (C.c_int, [fp, d, i32, i32, p]),
             "oracle_build_eq4": (C.c_int, [fp, d, p]),
             "oracle_left_matvec_streamed": (C.c_int, [fp, d, p, p]),
+            "oracle_left_matvec_streamed_multi": (C.c_int, [fp, d, i32, p, p]),
             "oracle_stationary_dense": (C.c_int, [i32, p, p]),
             "oracle_stationary_power": (C.c_int, [i32, p, d, i32, p, C.POINTER(i32), C.POINTER(d)]),
             "oracle_mc": (C.c_int, [fp, d, C.c_uint64, i64, i64, i32, i32, p]),
@@ -127,6 +129,17 @@ def rows_eq4(flux, t_d: float, r0: int, r1: int) -> np.ndarray:
 
 def build_eq4(flux, t_d: float) -> np.ndarray:
     return rows_eq4(flux, t_d, 0, flux.n_bins)
+
+
+def left_matvec_streamed_multi(flux, t_d: float, X: np.ndarray) -> np.ndarray:
+    """Y[v] = X[v]^T P~ for the rows X[v] of X [k, N], every Eq. 4 row computed once."""
+    X = np.ascontiguousarray(np.atleast_2d(X), dtype=np.float64)
+    assert X.shape[1] == flux.n_bins
+    Y = np.empty_like(X)
+    r = _FluxRef(flux)
+    if lib().oracle_left_matvec_streamed_multi(r.ref, float(t_d), int(X.shape[0]), X.ctypes.data, Y.ctypes.data):
+        raise ArithmeticError("oracle: streamed matvec failed")
+    return Y
 
 
 def left_matvec_streamed(flux, t_d: float, x: np.ndarray) -> np.ndarray:

@@ -131,34 +131,46 @@ int oracle_build_eq4(const oracle_flux *f, double t_d, double *out) {
     return oracle_rows_eq4(f, t_d, 0, f->n_bins, out);
 }
 
-/* y = x^T P~ for a row-streamed P~ (P~ never stored): used to check pi P~ = pi at sizes where the
- * dense matrix does not fit; each row is recomputed from Eq. 4. y is accumulated in long double
- * per thread, then summed over threads in thread order. */
-int oracle_left_matvec_streamed(const oracle_flux *f, double t_d, const double *x, double *y) {
+/* Y[v] = X[v]^T P~ for k vectors X[v] (k rows of N, row-major) and a row-streamed P~ (P~ never
+ * stored): used to check pi P~ = pi at sizes where the dense matrix does not fit; each row
+ * of P~ is recomputed once from Eq. 4 and applied to all k vectors. Y is accumulated in long
+ * double per thread, then summed over threads in thread order. */
+int oracle_left_matvec_streamed_multi(const oracle_flux *f, double t_d, int32_t k, const double *x,
+                                      double *y) {
     const int32_t N = f->n_bins;
+    const size_t nk = (size_t)N * (size_t)k;
     int bad = 0;
-    long double *acc = (long double *)calloc((size_t)N, sizeof(long double));
+    long double *acc = (long double *)calloc(nk, sizeof(long double));
     if (!acc) return 2;
 #pragma omp parallel reduction(| : bad)
     {
-        long double *loc = (long double *)calloc((size_t)N, sizeof(long double));
+        long double *loc = (long double *)calloc(nk, sizeof(long double));
         double *row = (double *)malloc((size_t)N * sizeof(double));
         if (!loc || !row) bad |= 2;
         else {
 #pragma omp for schedule(dynamic, 8)
             for (int32_t i = 0; i < N; ++i) {
                 bad |= oracle_row_eq4(f, t_d, i, row);
-                for (int32_t j = 0; j < N; ++j) loc[j] += (long double)x[i] * row[j];
+                for (int32_t v = 0; v < k; ++v) {
+                    const long double xi = x[(size_t)v * N + i];
+                    long double *lv = loc + (size_t)v * N;
+                    for (int32_t j = 0; j < N; ++j) lv[j] += xi * row[j];
+                }
             }
 #pragma omp critical
-            for (int32_t j = 0; j < N; ++j) acc[j] += loc[j];
+            for (size_t t = 0; t < nk; ++t) acc[t] += loc[t];
         }
         free(loc);
         free(row);
     }
-    for (int32_t j = 0; j < N; ++j) y[j] = (double)acc[j];
+    for (size_t t = 0; t < nk; ++t) y[t] = (double)acc[t];
     free(acc);
     return bad;
+}
+
+/* y = x^T P~ (one vector). */
+int oracle_left_matvec_streamed(const oracle_flux *f, double t_d, const double *x, double *y) {
+    return oracle_left_matvec_streamed_multi(f, t_d, 1, x, y);
 }
 
 /* pi P~ = pi, sum(pi) = 1 (leading left eigenvector of the stochastic matrix), by Gaussian

@@ -49,12 +49,91 @@ def test_p2_row_permutation_equals_direct(oracle_lib, f, td):
         assert np.max(np.abs(np.roll(P0, +l, axis=0) - P)) > 1e-6
 
 
-# --------------------------------------------------- P3 whole periods (x_d = t_d mod t_r)
+# ------------------------------- P3 raw dead time in the bounds, whole periods (Eq. 4)
+def _raw_bound_integral(f, i, j, t_d):
+    """The physical definition: a registration at s_i re-arms the SPAD at the RAW time
+    a = s_i + t_d on the unrolled time line; the next registration in bin j happens at the first
+    later visit b = ceil((a - s_j) / t_r) t_r + s_j of s_j (Eq. 3's upper limit with the raw a,
+    P:102), and Eq. 4 discretises the lower limit to D(a) = (ceil(a / Delta) - 1/2) Delta.
+    Returns int_{D(a)}^{b} lambda~ by quadrature over however many periods [D(a), b] spans -- no
+    fmod of t_d anywhere, so a wrong period reduction in the oracle cannot cancel out."""
+    # the two ceilings in exact rational arithmetic (t_d and t_r are exact binary fractions), so a
+    # bound that lands exactly on a bin centre (t_d a whole number of periods) is not pushed a
+    # period further by rounding; the limits themselves are then plain floats
+    d = Fraction(f.t_r) / f.n_bins
+    a = (i + Fraction(1, 2)) * d + Fraction(t_d)
+    s_j = (j + Fraction(1, 2)) * d
+    Da = float((math.ceil(a / d) - Fraction(1, 2)) * d)
+    b = float(math.ceil((a - s_j) / Fraction(f.t_r)) * Fraction(f.t_r) + s_j)
+    return _lam_tilde_integral(f, Da, b)
+
+
 @pytest.mark.parametrize("m", [1, 2, 3])
-def test_p3_whole_periods(oracle_lib, m):
+def test_p3_raw_dead_time_and_whole_periods(oracle_lib, m):
+    """t_d = m t_r + x (m = 1..3): every unnormalised oracle entry equals lambda(s_j) exp(-I) with
+    I the quadrature of lambda~ between the RAW-dead-time bounds, and for
+    x = 0 those raw-bound entries equal the oracle's t_d = 0 entries (whole periods reduce to the
+    dead-time-free matrix, BASELINE north_star). The oracle itself reduces x_d = t_d mod t_r
+    first, so this pins that reduction and its period bookkeeping against the physics."""
+    rng = np.random.default_rng(300 + m)
+    for k in (1, 2):
+        f = random_flux(rng, 24, k, sigma_bins=(2, 8))
+        d = f.t_r / f.n_bins
+        for x in (0.0, float(rng.uniform(0.0, f.t_r)), float(rng.uniform(0.0, f.t_r))):
+            if x > 0.0 and abs(x / d - round(x / d)) < 1e-6:
+                continue          # keep a / Delta away from integers (the bin-edge tie, reading R4)
+            td = m * f.t_r + x
+            for i, j in [(int(i), j) for i in rng.integers(0, f.n_bins, 2) for j in range(f.n_bins)]:
+                lam_j = oracle.lam(f, (j + 0.5) * d)
+                I_raw = _raw_bound_integral(f, i, j, td)
+                got = oracle.entry_eq4_unnorm(f, td, i, j)
+                assert abs(-math.log(got / lam_j) - I_raw) <= 1e-8 * max(1.0, m * oracle.Lambda(f))
+                if x == 0.0:
+                    zero = oracle.entry_eq4_unnorm(f, 0.0, i, j)
+                    assert abs(-math.log(zero / lam_j) - I_raw) <= 1e-8 * max(1.0, m * oracle.Lambda(f))
+    # the raw bounds really sit m periods down the unrolled line (so the quadrature above never
+    # saw a reduced dead time), and span less than one period plus one bin
     f = config(1).items[0].flux
-    assert np.max(np.abs(oracle.build_eq4(f, m * f.t_r) - oracle.build_eq4(f, 0.0))) <= 1e-15
-    assert np.max(np.abs(oracle.build_eq4(f, 75.0 + m * f.t_r) - oracle.build_eq4(f, 75.0))) <= 1e-15
+    d = f.t_r / f.n_bins
+    a = 3.5 * d + m * f.t_r + 75.0
+    Da = (math.ceil(a / d) - 0.5) * d
+    b = math.ceil((a - 5.5 * d) / f.t_r) * f.t_r + 5.5 * d
+    assert m * f.t_r <= Da < b < Da + f.t_r + d
+
+
+# -------------------------- P13 streamed x^T P~ (the only oracle route to pi P~ at N >= 16384)
+@pytest.mark.parametrize("N,K,td_frac", [(97, 1, 0.37), (97, 2, 1.71), (256, 1, 2.42), (256, 2, 0.61)])
+def test_p13_streamed_left_matvec(oracle_lib, N, K, td_frac):
+    """oracle_left_matvec_streamed recomputes every row of Eq. 4 and accumulates x_i P~_i in long
+    double over OpenMP threads. Pinned against numpy's matmul of the dense oracle matrix (a library
+    product) for t_d below and above t_r, against single rows (x = e_i picks row i, so a transposed
+    operand fails), and for thread-count independence."""
+    rng = np.random.default_rng(1300 + N + K)
+    f = random_flux(rng, N, K)
+    td = td_frac * f.t_r
+    P = oracle.build_eq4(f, td)
+    Pl = P.astype(np.longdouble)           # the library product in extended precision, like the oracle's sum
+    for x in (rng.uniform(0.0, 1.0, N), np.full(N, 1.0 / N)):
+        y = oracle.left_matvec_streamed(f, td, x)
+        want = (x.astype(np.longdouble) @ Pl).astype(np.float64)
+        assert np.max(np.abs(y - want) / want) <= 2.3e-16
+    for i in (0, N // 3, N - 1):
+        e = np.zeros(N)
+        e[i] = 1.0
+        assert np.array_equal(oracle.left_matvec_streamed(f, td, e), P[i])
+    X = rng.uniform(0.0, 1.0, (3, N))
+    want = (X.astype(np.longdouble) @ Pl).astype(np.float64)
+    assert np.max(np.abs(oracle.left_matvec_streamed_multi(f, td, X) - want) / want) <= 2.3e-16
+    x = rng.uniform(0.0, 1.0, N)
+    prev = oracle.max_threads()
+    try:
+        oracle.set_threads(1)
+        y1 = oracle.left_matvec_streamed(f, td, x)
+        oracle.set_threads(4)
+        y4 = oracle.left_matvec_streamed(f, td, x)
+    finally:
+        oracle.set_threads(prev)
+    assert np.max(np.abs(y1 - y4)) <= 1e-15 * max(1.0, float(np.max(np.abs(y1))))
 
 
 # ------------------------------------------ P5 constant flux (S = 0): closed-form circulant chain
