@@ -218,6 +218,8 @@ def shift_l(flux, t_d: float) -> int:
     fmod(t_d, t_r) * N / t_r (reading R4). Used by oracle-side pins only."""
     import math
     u = math.fmod(float(t_d), flux.t_r) * flux.n_bins / flux.t_r
+    if abs(u - round(u)) <= 8.0 * 2.220446049250313e-16 * max(1.0, abs(u)):
+        u = float(round(u))                      # whole bins in decimal land on a bin centre (R4)
     return int(math.ceil(u)) % flux.n_bins
 
 

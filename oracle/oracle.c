@@ -21,7 +21,8 @@
  * Readings where the paper is silent (DESIGN.md §3 lists them all):
  *   R5  Lambda := F(t_r) (the integral of the one-period flux), so the periodic replica is exact.
  *   R6  lambda~ is the one-period lambda repeated (not a wrapped Gaussian).
- *   R4  x_d / Delta is evaluated as u = fmod(t_d, t_r) * N / t_r; ceilings are taken in bin units
+ *   R4  x_d / Delta is evaluated as u = fmod(t_d, t_r) * N / t_r, read as the integer it is within
+ *       8 ulps of (a dead time of whole bins in decimal lands on a bin centre); ceilings are taken in bin units
  *       so integer cases stay exact.
  *   R8  the 1/(1-exp(-Lambda)) prefactor of Eq. 3 is dropped: rows are divided by their sums.
  *   Parity pins: none unpinned (see tests/test_oracle_pins.py); the MC pin is statistical.
@@ -91,7 +92,8 @@ static double centre(const oracle_flux *f, int64_t j) { return ((double)j + 0.5)
 double oracle_entry_eq4_unnorm(const oracle_flux *f, double t_d, int32_t i, int32_t j) {
     const int64_t N = f->n_bins;
     const double x_d = fmod(t_d, f->t_r);                 /* P:102 */
-    const double u = x_d * (double)N / f->t_r;            /* x_d / Delta (reading R4) */
+    double u = x_d * (double)N / f->t_r;                  /* x_d / Delta (reading R4) */
+    if (fabs(u - nearbyint(u)) <= 8.0 * 2.220446049250313e-16 * fmax(1.0, fabs(u))) u = nearbyint(u);
     /* lower limit D(a): a / Delta = i + 1/2 + u; ceil -> 1-based bin index k_a on the unrolled line */
     const int64_t k_a = (int64_t)ceil((double)i + 0.5 + u);   /* >= 1 since u >= 0 */
     const int64_t qa = (k_a - 1) / N;

@@ -179,6 +179,17 @@ static splidar_status check_item(double sig_sum, double S, double B) {
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
+// u = x_d / Delta = fmod(t_d, t_r) N / t_r (x_d P:102, Thm 2; reading R4), snapped to the
+// nearest integer when it is within a few ulps of one: a dead time that is a whole number of bins in
+// decimal (t_d = 0.3 with Delta = 0.1) lands on a bin centre (l = u, E = 1 at zero distance), and
+// binary rounding of t_d, Delta or the fmod must not push it a whole bin further.
+static double shift_u(double t_r, int32_t n_bins, double t_d) {
+    double u = std::fmod(t_d, t_r) * (double)n_bins / t_r;
+    const double r = std::nearbyint(u);
+    if (std::fabs(u - r) <= 8.0 * 2.220446049250313e-16 * std::fmax(1.0, std::fabs(u))) u = r;
+    return u;
+}
+
 static splidar_status check_matrix(const void *P, int N, int64_t ld, int dt) {
     if (!P) return SPLIDAR_EINVAL;
     if (dt != SPLIDAR_F64 && dt != SPLIDAR_F32) return SPLIDAR_EINVAL;
@@ -196,7 +207,7 @@ extern "C" {
 
 splidar_status splidar_shift(double t_r, int32_t n_bins, double t_d, int32_t *l_out) {
     if (!l_out || !finite_pos(t_r) || n_bins < 2 || !std::isfinite(t_d) || t_d < 0.0) return SPLIDAR_EINVAL;
-    const double u = std::fmod(t_d, t_r) * (double)n_bins / t_r;   // x_d / Delta (Thm 2)
+    const double u = shift_u(t_r, n_bins, t_d);   // x_d / Delta (Thm 2)
     long l = (long)std::ceil(u);
     l %= n_bins;
     *l_out = (int32_t)l;
@@ -303,7 +314,7 @@ splidar_status splidar_build_eq4(const splidar_flux *flux, double t_d, splidar_d
     if (st) return st;
     if (!std::isfinite(t_d) || t_d < 0.0) return SPLIDAR_EINVAL;
     if ((st = check_matrix(P, flux->n_bins, ld, dt))) return st;
-    const double u = std::fmod(t_d, flux->t_r) * (double)flux->n_bins / flux->t_r;   // x_d / Delta (R4)
+    const double u = shift_u(flux->t_r, flux->n_bins, t_d);   // x_d / Delta (R4)
     return cuda_status(launch_build_eq4(to_dev(flux), u, dt, P, ld, (cudaStream_t)stream));
 }
 

@@ -12,9 +12,10 @@ namespace spl {
 constexpr int kMaxPulses = SPLIDAR_MAX_PULSES;
 constexpr int kMaxVectors = 32;      // dead times per matrix in one multi-vector GEMV pass
 constexpr int kStripCols = 512;      // columns per GEMV / build CTA (4 KB of an fp64 row)
-constexpr int kNumSMs = 148;
+constexpr int kNumSMsDefault = 148; // B200; only used if the device query fails
+constexpr int kMaxSMs = 160;        // workspace bound for the persistent GEMV grid (SM count queried per device)
 constexpr int kCheckChunk = 2048;   // elements per CTA of the convergence-check kernel
-constexpr int kGemvCtas = 2 * kNumSMs;  // largest persistent GEMV grid (two 256-thread CTAs per SM)
+constexpr int kGemvCtas = 2 * kMaxSMs;  // largest persistent GEMV grid (two 256-thread CTAs per SM)
 constexpr int kMinRowsPerCta = 64;      // smallest row range a GEMV CTA is given
 
 // theta without t_d, device copy. Eq. 1 with K pulses.
@@ -62,6 +63,13 @@ struct WsLayout {
 
 WsLayout ws_layout(int N, int M, int V);
 int pad_vectors(int V);
+
+// ---- per-device host state (device.cu) -------------------------------------------------------
+int current_device();
+int device_sm_count();              // SMs of the current device (cached per device ordinal)
+// cudaFuncSetAttribute once per (device, kernel, value): max dynamic shared memory (if > 0) and
+// non-portable cluster sizes (if requested).
+cudaError_t func_attrs_once(const void *fn, int max_dyn_smem, bool nonportable_cluster);
 
 // ---- kernels launch wrappers (host) -------------------------------------------------------
 cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs base, int64_t vstride,

@@ -479,12 +479,8 @@ cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs bas
         int threads = N + 1 < kST ? N + 1 : kST;     // one element per thread for the transcendentals
         threads = (threads + 31) / 32 * 32;          // (the scans need only (N + 1) / 8 of them)
         const int smem = (int)(sizeof(double) * threads * kSEl * 2);
-        static std::once_flag once;         // once per process (thread-safe; not in captured launches)
-        static cudaError_t attr = cudaSuccess;
-        std::call_once(once, [] {
-            attr = cudaFuncSetAttribute((const void *)k_vec_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)(sizeof(double) * kST * kSEl * 2));
-        });
+        // once per device (thread-safe; not in captured launches)
+        const cudaError_t attr = func_attrs_once((const void *)k_vec_small, (int)(sizeof(double) * kST * kSEl * 2), false);
         if (attr != cudaSuccess) return attr;
         k_vec_small<<<M, threads, smem, s>>>(d_flux, N, base, vstride);
         return cudaGetLastError();

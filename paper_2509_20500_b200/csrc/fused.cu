@@ -289,23 +289,18 @@ void *fused_fn_q(int N) {
     return (void *)k_power_fused<T, 4>;
 }
 
-// the kernel instance for (dtype, N); its attributes are set once per process for all instances
+// the kernel instance for (dtype, N); its attributes are set once per device for all instances
 // (thread-safe; never inside a captured launch)
 cudaError_t fused_fn(int dtype, int N, void **fn) {
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
-    std::call_once(once, [] {
-        void *all[] = {(void *)k_power_fused<double, 1>, (void *)k_power_fused<double, 2>,
-                       (void *)k_power_fused<double, 4>, (void *)k_power_fused<float, 1>,
-                       (void *)k_power_fused<float, 2>, (void *)k_power_fused<float, 4>};
-        for (void *f : all) {
-            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            if (e != cudaSuccess) { attr = e; return; }
-        }
-    });
+    const void *all[] = {(void *)k_power_fused<double, 1>, (void *)k_power_fused<double, 2>,
+                         (void *)k_power_fused<double, 4>, (void *)k_power_fused<float, 1>,
+                         (void *)k_power_fused<float, 2>, (void *)k_power_fused<float, 4>};
+    for (const void *f : all) {
+        const cudaError_t e = func_attrs_once(f, 220 * 1024, true);
+        if (e != cudaSuccess) return e;
+    }
     *fn = dtype == SPLIDAR_F64 ? fused_fn_q<double>(N) : fused_fn_q<float>(N);
-    return attr;
+    return cudaSuccess;
 }
 
 int fused_resident(int N, int R, int dtype) { return fused_slice_bytes(N, R, dtype) <= kFResidentMax; }

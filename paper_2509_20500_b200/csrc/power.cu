@@ -556,7 +556,7 @@ void *step_entry(size_t *smem, int *ctas_per_sm) {
     *smem = StepSmem<T, NV>::BYTES;
     *ctas_per_sm = StepSmem<T, NV>::MINB;
     void *fn = (void *)k_power_step<T, NV>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+    if (func_attrs_once(fn, (int)*smem, false) != cudaSuccess) return nullptr;
     return fn;
 }
 
@@ -604,7 +604,10 @@ int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a) {
     out->init_block = dim3(256);
     out->finish_grid = dim3(gx, a.M * a.V);
     out->finish_block = dim3(256);
-    out->step_grid = dim3(kNumSMs * cps);   // persistent: every resident CTA slot, once
+    // persistent: every resident CTA slot of the current device once (<= kGemvCtas, the workspace's
+    // partial-sum slots)
+    const int sms = device_sm_count() < kMaxSMs ? device_sm_count() : kMaxSMs;
+    out->step_grid = dim3(sms * cps);
     out->step_block = dim3(kThreads);
     out->check_grid = dim3(a.chunks, a.M * a.V);
     out->check_block = dim3(256);

@@ -28,6 +28,7 @@
 
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -1057,15 +1058,7 @@ int shape_for(int N, int E, int *C, int *threads) {
 // Kernel attributes once per kernel (keyed by its address: every team kernel has the same type), at
 // the largest dynamic shared memory it can request; thread-safe, never inside a captured launch.
 cudaError_t team_attrs_once(const void *fn, size_t max_smem) {
-    static std::mutex mu;
-    static std::vector<const void *> done;
-    std::lock_guard<std::mutex> lock(mu);
-    for (const void *d : done)
-        if (d == fn) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e == cudaSuccess) done.push_back(fn);
-    return e;
+    return func_attrs_once(fn, (int)max_smem, true);   // once per (device, kernel)
 }
 
 template <typename K>
@@ -1097,9 +1090,10 @@ cudaError_t launch_team(K kernel, StructArgs a, int n_units, int E, int nbuf, cu
 // Clusters of C CTAs x T threads with `smem` dynamic bytes resident at once (cached per kernel, C).
 int resident_clusters(const void *fn, int C, int T, size_t smem) {
     static std::mutex mu;
-    static std::map<std::pair<const void *, int>, int> cache;
+    static std::map<std::tuple<int, const void *, int, int, size_t>, int> cache;   // per device
+    const int dev = current_device();
     std::lock_guard<std::mutex> lock(mu);
-    const auto key = std::make_pair(fn, C);
+    const auto key = std::make_tuple(dev, fn, C, T, smem);
     const auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     cudaLaunchConfig_t cfg = {};

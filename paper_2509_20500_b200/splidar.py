@@ -6,7 +6,10 @@ load, every call raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
+import functools
+import inspect
 import math
 import os
 from dataclasses import dataclass
@@ -138,6 +141,22 @@ def _stream(stream=None) -> int:
     return s.cuda_stream
 
 
+def _allocates_on_stream(fn):
+    """Runs fn with `stream` (when given) as torch's current stream, so that every workspace, output
+    and temporary fn allocates belongs to the stream its kernels are enqueued on: the caching
+    allocator then never hands a temporary that kernels on `stream` still read to another stream's
+    allocation after fn returns."""
+    sig = inspect.signature(fn)
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        st = sig.bind_partial(*args, **kwargs).arguments.get("stream")
+        ctx = torch.cuda.stream(st) if isinstance(st, torch.cuda.Stream) else contextlib.nullcontext()
+        with ctx:
+            return fn(*args, **kwargs)
+    return wrapper
+
+
 class _FluxArg:
     """Marshals any object with t_r, n_bins, tau, sigma, signal, background into splidar_flux."""
 
@@ -190,6 +209,7 @@ def _matrix_args(P: torch.Tensor):
     return P.data_ptr(), P.shape[-1], P.stride(-2), _DTYPES[P.dtype]
 
 
+@_allocates_on_stream
 def flux_vectors(flux, ws: torch.Tensor | None = None, stream=None) -> dict:
     """Step 1 on the device: F(s_j), lambda(s_j), w_j, 1/D_j and Lambda (fp64 device tensors)."""
     N = int(flux.n_bins)
@@ -203,6 +223,7 @@ def flux_vectors(flux, ws: torch.Tensor | None = None, stream=None) -> dict:
     return {"F": F, "lam": lam, "w": w, "inv_d": invd, "Lambda": L}
 
 
+@_allocates_on_stream
 def build_base(flux, dtype=torch.float64, mode: str = "factored", out: torch.Tensor | None = None,
                ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Step 2: P~0 (N x N view of [N, ld] storage) on the current CUDA device (async)."""
@@ -216,6 +237,7 @@ def build_base(flux, dtype=torch.float64, mode: str = "factored", out: torch.Ten
     return P
 
 
+@_allocates_on_stream
 def build_base_batched(fluxes, dtype=torch.float64, mode: str = "factored", out: torch.Tensor | None = None,
                        ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Step 2 for M fluxes sharing N: P~0 [M, N, N] view of [M, N, ld] storage (async)."""
@@ -231,6 +253,7 @@ def build_base_batched(fluxes, dtype=torch.float64, mode: str = "factored", out:
     return P
 
 
+@_allocates_on_stream
 def build_eq4(flux, t_d: float, dtype=torch.float64, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """P~ element by element from Eq. 4 (the construction Theorem 2 replaces), async."""
     N = int(flux.n_bins)
@@ -241,6 +264,7 @@ def build_eq4(flux, t_d: float, dtype=torch.float64, out: torch.Tensor | None = 
     return P
 
 
+@_allocates_on_stream
 def apply_deadtime(P0: torch.Tensor, t_r: float, t_d: float, out: torch.Tensor | None = None,
                    stream=None) -> torch.Tensor:
     """Step 3 materialised: P[i] = P0[(i + l) mod N] (async)."""
@@ -254,6 +278,7 @@ def apply_deadtime(P0: torch.Tensor, t_r: float, t_d: float, out: torch.Tensor |
     return P
 
 
+@_allocates_on_stream
 def stationary(P0: torch.Tensor, t_r: float, t_d: float, tol: float = 1e-12, max_iter: int = 10 ** 6,
                out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None,
                check: bool = True):
@@ -268,6 +293,7 @@ def stationary(P0: torch.Tensor, t_r: float, t_d: float, tol: float = 1e-12, max
     return pi, info.as_dict()
 
 
+@_allocates_on_stream
 def sweep(shape, S, B, t_d, dtype=torch.float64, mode: str = "factored", tol: float = 1e-12,
           max_iter: int = 10 ** 6, n_store: int | None = None, P0_store: torch.Tensor | None = None,
           ws: torch.Tensor | None = None, stream=None, check: bool = True, matrix_free: bool = False):
@@ -423,6 +449,7 @@ def lambda2_of(rec) -> complex:
     return complex(float(rec["lambda2_re"]), float(rec["lambda2_im"]))
 
 
+@_allocates_on_stream
 def stationary_structured(shape, S, B, t_d, tol: float = 1e-12, max_iter: int = 10 ** 6,
                           ws: torch.Tensor | None = None, stream=None, check: bool = True):
     """f2: pi for (S[m], B[m], t_d[m]) items by power iteration on the matrix-free operator (no P~0 is
@@ -440,6 +467,7 @@ def stationary_structured(shape, S, B, t_d, tol: float = 1e-12, max_iter: int = 
     return pi, _records(infos)
 
 
+@_allocates_on_stream
 def second_eigenvalue(shape, S, B, t_d, pi: torch.Tensor, tol: float = 1e-13, max_iter: int = 10 ** 5,
                       ws: torch.Tensor | None = None, stream=None, check: bool = True) -> list:
     """f1: lambda_2 of P~ per item (modulus, phase in [0, pi], gap); pi = the items' stationary vectors
@@ -459,6 +487,7 @@ def second_eigenvalue(shape, S, B, t_d, pi: torch.Tensor, tol: float = 1e-13, ma
     return _records(infos)
 
 
+@_allocates_on_stream
 def second_eigenvalue_dense(P0: torch.Tensor, t_r: float, t_d: float, pi: torch.Tensor, tol: float = 1e-13,
                             max_iter: int = 10 ** 5, ws: torch.Tensor | None = None, stream=None,
                             check: bool = True) -> dict:
@@ -481,6 +510,7 @@ def second_eigenvalue_dense(P0: torch.Tensor, t_r: float, t_d: float, pi: torch.
     return info.as_dict()
 
 
+@_allocates_on_stream
 def mixing_steps(flux, t_d: float, pi: torch.Tensor, eps: float = 1e-3, max_steps: int = 10 ** 5,
                  ws: torch.Tensor | None = None, stream=None, check: bool = True):
     """f1: smallest n with max_i 1/2 ||e_i P~^n - pi||_1 <= eps. Returns (n, per-start n_i int32 tensor)."""
@@ -497,6 +527,7 @@ def mixing_steps(flux, t_d: float, pi: torch.Tensor, eps: float = 1e-3, max_step
     return out.value, per
 
 
+@_allocates_on_stream
 def bin_trajectory(flux, t_d: float, start: torch.Tensor, bin: int, steps: int, ws: torch.Tensor | None = None,
                    stream=None):
     """f1: (start P~^n)[bin] for n = 0..steps. Returns (traj [steps + 1], start P~^steps [N])."""
@@ -571,6 +602,7 @@ class StructPlan:
             pass
 
 
+@_allocates_on_stream
 def monte_carlo(shape, S, B, t_d, seed: int, n_runs: int, n_hist: int, n_burn: int = 100, n_regs: int = 0,
                 n_cycles: int = 0, n_record: int = 0, n_split: int = 1, stream=None):
     """histograms [M, n_runs, n_hist] (int64 CUDA tensor) of simulated detection timestamps

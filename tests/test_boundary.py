@@ -83,6 +83,13 @@ def test_shift_rule_matches_oracle_and_edges(spl):
     assert spl.shift(100.0, 4, 99.0) == 0               # l = N wraps to 0
     assert spl.shift(100.0, 4, 25.0) == 1               # exact integer: ceil(1) = 1
     assert spl.shift(100.0, 4, 25.0001) == 2
+    # whole bins written in decimal (Delta = 0.1, 0.01 not binary fractions): the re-arm point lands
+    # on a bin centre (reading R4), never one bin further; l = N wraps to 0
+    assert spl.shift(1.0, 10, 0.3) == 3                 # 0.3 * 10 / 1 = 3.0000000000000004 in fp64
+    assert spl.shift(0.1, 10, 0.3) == 0                 # fmod(0.3, 0.1) = 0.0999..: u ~ N -> l = 0
+    for k in (1, 3, 7, 29, 113, 4321):
+        td = float(f"{k / 100:.2f}")                    # k Delta, Delta = 0.01 (t_r = 100, N = 10000)
+        assert spl.shift(100.0, 10000, td) == k == oracle.shift_l(_F(100.0, 10000), td)
 
 
 class _F:

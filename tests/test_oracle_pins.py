@@ -101,6 +101,31 @@ def test_p3_raw_dead_time_and_whole_periods(oracle_lib, m):
     assert m * f.t_r <= Da < b < Da + f.t_r + d
 
 
+def test_p3b_decimal_whole_bins_land_on_a_bin_centre(oracle_lib):
+    """t_d = k Delta written in decimal (Delta = 0.1 or 0.01, not binary fractions): the re-arm time
+    s_i + t_d is exactly the bin centre s_{i+k}, reachable at zero distance, so the
+    raw-bound integral (exact decimal rationals) is 0 for j = i + k and the entry is lambda(s_j)
+    (E = 1). A shift rule that lets binary rounding push u = x_d / Delta above k moves that entry a
+    whole period away (integral Lambda); reading R4 snaps u to k."""
+    for t_r, N, tds in ((1.0, 10, ("0.3", "0.7", "1.3", "2.9")), (100.0, 10000, ("0.07", "1.13", "27.3"))):
+        rng = np.random.default_rng(N)
+        f = random_flux(rng, N, 1, t_r=t_r, sigma_bins=(2, 8))
+        d = Fraction(str(t_r)) / N
+        for td_s in tds:
+            td = float(td_s)
+            k = int(Fraction(td_s) / d) % N
+            assert oracle.shift_l(f, td) == k
+            for i in (0, 3, N // 2, N - 1):
+                j = (i + k) % N
+                a = (i + Fraction(1, 2)) * d + Fraction(td_s)
+                s_j = (j + Fraction(1, 2)) * d
+                Da = (math.ceil(a / d) - Fraction(1, 2)) * d
+                b = math.ceil((a - s_j) / Fraction(str(t_r))) * Fraction(str(t_r)) + s_j
+                assert b == Da                                   # zero distance, exactly
+                got = oracle.entry_eq4_unnorm(f, td, i, j)
+                assert got == oracle.lam(f, (j + 0.5) * (t_r / N)), (t_r, N, td_s, i)   # exp(-0) = 1
+
+
 # -------------------------- P13 streamed x^T P~ (the only oracle route to pi P~ at N >= 16384)
 @pytest.mark.parametrize("N,K,td_frac", [(97, 1, 0.37), (97, 2, 1.71), (256, 1, 2.42), (256, 2, 0.61)])
 def test_p13_streamed_left_matvec(oracle_lib, N, K, td_frac):
