@@ -120,13 +120,16 @@ __device__ __forceinline__ void mma_groups(double (&acc)[NG][8][2], const double
     }
 }
 
-// NVM vectors on tensor cores (groups of 8, running mask GM bits [0, NVM/8)) and NVF <= 2 leftover
-// vectors on DFMA (running mask bits [NVM/8, NVM/8 + NVF)) that reuse the B fragments already in
+// NVM slots on tensor cores (groups of 8, running mask GM bits [0, NVM/8)) and NVF <= 2 leftover
+// slots on DFMA (running mask bits [NVM/8, NVM/8 + NVF)) that reuse the B fragments already in
 // registers: lane (g, t) accumulates x_f[k = t] * P[t][64 w + 8 nt + g] into accf[f][nt]; the 4 t-lanes
-// of a column are added with shuffles when the piece ends.
+// of a column are added with shuffles when the piece ends. Slots are the running vectors in
+// compacted order: slot s reads the x column xc of vector s_vmap[s] (xc < 0: an empty slot of the
+// last, partly filled group, fed zeros), so converged vectors free their tensor-core group.
 template <typename T, int NVM, int NVF, int RS, int XST, unsigned GM>
 __device__ __forceinline__ void stage_mma_fixed(double (&acc)[NVM / 8][8][2], double (&accf)[NVF > 0 ? NVF : 1][8],
-                                                const T *seg, const double *xs, int nr, int lane, int warp) {
+                                                const T *seg, const double *xs, int nr, int lane, int warp,
+                                                const int (&xc)[NVM / 8], const int (&fc)[NVF > 0 ? NVF : 1]) {
     constexpr int SROW = GemvCfg<T>::SROW;
     constexpr int NG = NVM / 8;
     const int g = lane >> 2, t = lane & 3;
@@ -135,12 +138,13 @@ __device__ __forceinline__ void stage_mma_fixed(double (&acc)[NVM / 8][8][2], do
     for (int kb = 0; kb < RS; kb += 4) {
         const int k = kb + t;
         const bool kin = k < nr;
-        double a[NG];                                   // A fragments: X[k][8 q + g]
+        double a[NG];                                   // A fragments: X[k][slot 8 q + g]
 #pragma unroll
-        for (int q = 0; q < NG; ++q) a[q] = (kin && ((GM >> q) & 1u)) ? xs[k * XST + q * 8 + g] : 0.0;
+        for (int q = 0; q < NG; ++q)
+            a[q] = (kin && ((GM >> q) & 1u) && xc[q] >= 0) ? xs[k * XST + xc[q]] : 0.0;
         double xf[NVF > 0 ? NVF : 1];
 #pragma unroll
-        for (int f = 0; f < NVF; ++f) xf[f] = kin ? xs[k * XST + NVM + f] : 0.0;
+        for (int f = 0; f < NVF; ++f) xf[f] = (kin && ((GM >> (NG + f)) & 1u)) ? xs[k * XST + fc[f]] : 0.0;
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt) {
             const double bv = kin ? (double)sb[k * SROW + nt * 8] : 0.0;
@@ -152,13 +156,33 @@ __device__ __forceinline__ void stage_mma_fixed(double (&acc)[NVM / 8][8][2], do
     }
 }
 
-// Runtime running mask -> the compile-time specialisation (2^(NG + NVF) - 1 cases; uniform branch).
+// Running masks of compacted slots: the first G groups, and leftovers only behind all NG groups.
+template <int NG, int NVF>
+__host__ __device__ constexpr unsigned slot_mask(int nact) {
+    const int G = nact >= 8 * NG ? NG : (nact + 7) / 8;
+    const int F = nact > 8 * NG ? (nact - 8 * NG < NVF ? nact - 8 * NG : NVF) : 0;
+    return ((1u << G) - 1u) | (((1u << F) - 1u) << NG);
+}
+template <int NG, int NVF>
+__host__ __device__ constexpr bool is_slot_mask(unsigned m) {
+    for (int n = 1; n <= 8 * NG + NVF; ++n)
+        if (slot_mask<NG, NVF>(n) == m) return true;
+    return false;
+}
+
+// Runtime running mask -> the compile-time specialisation (one per reachable slot mask; uniform branch).
 template <typename T, int NVM, int NVF, int RS, int XST, unsigned GM = 1>
 __device__ __forceinline__ void stage_mma(double (&acc)[NVM / 8][8][2], double (&accf)[NVF > 0 ? NVF : 1][8],
-                                          const T *seg, const double *xs, int nr, int lane, int warp, unsigned mask) {
+                                          const T *seg, const double *xs, int nr, int lane, int warp, unsigned mask,
+                                          const int (&xc)[NVM / 8], const int (&fc)[NVF > 0 ? NVF : 1]) {
     if constexpr (GM < (1u << (NVM / 8 + NVF))) {
-        if (mask == GM) stage_mma_fixed<T, NVM, NVF, RS, XST, GM>(acc, accf, seg, xs, nr, lane, warp);
-        else stage_mma<T, NVM, NVF, RS, XST, GM + 1>(acc, accf, seg, xs, nr, lane, warp, mask);
+        if constexpr (is_slot_mask<NVM / 8, NVF>(GM)) {
+            if (mask == GM) {
+                stage_mma_fixed<T, NVM, NVF, RS, XST, GM>(acc, accf, seg, xs, nr, lane, warp, xc, fc);
+                return;
+            }
+        }
+        stage_mma<T, NVM, NVF, RS, XST, GM + 1>(acc, accf, seg, xs, nr, lane, warp, mask, xc, fc);
     }
 }
 
@@ -226,27 +250,37 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
         const int r_hi = (int)((u_end < strip_end ? u_end : strip_end) - g64 * N);
         u = g64 * N + r_hi;
 
-        // running vectors of matrix m, compacted into slots
+        // running vectors of matrix m, compacted into slots (slot s = the s-th running vector)
         if (tid == 0) {
             int n = 0;
-            unsigned gm = 0, vm = 0;
+            unsigned vm = 0;
             for (int v = 0; v < NV; ++v) {
                 const SolveState s = a.st[(size_t)m * NV + v];
                 if (!s.done) {
                     s_vmap[n] = v; s_cur[n] = s.cur; ++n;
                     vm |= 1u << v;
-                    // MMA groups of 8 in bits [0, NVM/8), DFMA leftovers in the bits after them
-                    gm |= (SM::MMA && v >= SM::NVM) ? (1u << (SM::NVM / 8 + v - SM::NVM)) : (1u << (v >> 3));
                 }
             }
             s_nact = n;
-            s_gmask = gm;
+            // MMA path: the first ceil(n / 8) groups of 8 slots, DFMA leftovers only behind all groups
+            s_gmask = SM::MMA ? slot_mask<SM::NVM / 8, SM::NVF>(n) : 0u;
             s_vmask = vm;
         }
         __syncthreads();
         const int nact = s_nact;
         const unsigned gmask = s_gmask;             // running MMA groups + DFMA leftovers
         const unsigned vmask = s_vmask;             // running vectors
+        constexpr int NGX = SM::MMA ? SM::NVM / 8 : 1;
+        constexpr int NFX = SM::NVF > 0 ? SM::NVF : 1;
+        int xc[NGX];                                // x column of this lane's slot 8 q + (lane / 4)
+        int fc[NFX];                                // x column of leftover slot NVM + f
+        {
+            const int gl = (tid & 31) >> 2;
+#pragma unroll
+            for (int q = 0; q < NGX; ++q) xc[q] = q * 8 + gl < nact ? s_vmap[q * 8 + gl] : -1;
+#pragma unroll
+            for (int f = 0; f < NFX; ++f) fc[f] = SM::NVM + f < nact ? s_vmap[SM::NVM + f] : 0;
+        }
 
         const int cols = min(kStripCols, N - c * kStripCols);
         const uint32_t seg_bytes = (uint32_t)(((size_t)cols * sizeof(T) + 15) & ~(size_t)15);
@@ -299,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
             __syncthreads();
             if (tid == 0 && k + kStages - 1 < nstages) issue(k + kStages - 1);
             if constexpr (SM::MMA) {
-                stage_mma<T, SM::NVM, SM::NVF, RS, SM::XST>(accm, accf, segb, xs, nr, lane, warp, gmask);
+                stage_mma<T, SM::NVM, SM::NVF, RS, SM::XST>(accm, accf, segb, xs, nr, lane, warp, gmask, xc, fc);
             } else {
                 if (2 * tid < cols) stage_fma<T, NV, NV, RS>(acc, segb, xs, SM::XST, nr, tid);
             }
@@ -314,12 +348,13 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
         if constexpr (SM::MMA) {
             // rows of D of the running groups (converged vectors are never read back)
             const int lane = tid & 31, w = tid >> 5, gq = lane >> 2, tq = lane & 3;
+            // slot rows go to their vector's partial row
 #pragma unroll
             for (int q = 0; q < NG; ++q) {
-                if (!((gmask >> q) & 1u)) continue;
+                if (!((gmask >> q) & 1u) || xc[q] < 0) continue;
 #pragma unroll
                 for (int nt = 0; nt < 8; ++nt)
-                    *reinterpret_cast<double2 *>(part + (size_t)(q * 8 + gq) * kStripCols + w * 64 + nt * 8 + 2 * tq) =
+                    *reinterpret_cast<double2 *>(part + (size_t)xc[q] * kStripCols + w * 64 + nt * 8 + 2 * tq) =
                         make_double2(accm[q][nt][0], accm[q][nt][1]);
             }
             if constexpr (SM::NVF > 0) {
@@ -332,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
                         double v = accf[f][nt];
                         v += __shfl_xor_sync(0xffffffffu, v, 1);
                         v += __shfl_xor_sync(0xffffffffu, v, 2);
-                        if (tq == 0) part[(size_t)(SM::NVM + f) * kStripCols + w * 64 + nt * 8 + gq] = v;
+                        if (tq == 0) part[(size_t)fc[f] * kStripCols + w * 64 + nt * 8 + gq] = v;
                     }
                 }
             }
