@@ -44,13 +44,19 @@ WsLayout ws_layout(int N, int M, int V) {
     L.y = o;    o = a256(o + sizeof(double) * MV * 2 * N);
     L.X = o;    o = a256(o + sizeof(double) * (size_t)M * N * L.xstride);
     L.part = o; o = a256(o + sizeof(double) * (size_t)L.pieces * L.V * kStripCols);
-    L.ssum = o; o = a256(o + sizeof(double) * MV * L.strips);
+    const size_t tiles64 = ((size_t)N + 63) / 64;        // column tiles of the int8 GEMV (>= 64 columns)
+    L.ssum = o; o = a256(o + sizeof(double) * MV * (tiles64 > (size_t)L.strips ? tiles64 : (size_t)L.strips));
     L.l1part = o; o = a256(o + sizeof(double) * MV * L.chunks);
     L.state = o; o = a256(o + sizeof(SolveState) * MV);
-    L.strip_cnt = o; o = a256(o + sizeof(unsigned) * (size_t)M * L.strips);
+    L.strip_cnt = o; o = a256(o + sizeof(unsigned) * (size_t)M * (tiles64 > (size_t)L.strips ? tiles64 : (size_t)L.strips));
     L.mv_cnt = o; o = a256(o + sizeof(unsigned) * MV);
     L.act = o; o = a256(o + sizeof(int) * (size_t)M);
     L.glob = o; o = a256(o + sizeof(unsigned) * 4);
+    // int8 tensor-core GEMV: x-slice image (128 bytes per row), column exponents, tile maxima, x scales
+    L.ximg = o; o = a256(o + (size_t)M * tiles64 * 64 * 128);
+    L.colexp = o; o = a256(o + sizeof(int) * (size_t)M * N);
+    L.smax = o; o = a256(o + sizeof(double) * MV * tiles64);
+    L.xtau = o; o = a256(o + sizeof(int) * MV);
     L.total = o;
     return L;
 }
@@ -341,6 +347,7 @@ struct splidar_plan_s {
     bool fused = false;
     int dt = 0;
     FusedArgs fargs;
+    I8Kernels q;       // int8 tensor-core GEMV (args.i8)
 };
 
 static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws, cudaStream_t s) {
@@ -363,6 +370,18 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     a.strips = L.strips;
     a.chunks = L.chunks;
     a.xstride = L.xstride;
+    a.ximg = reinterpret_cast<unsigned char *>(ws + L.ximg);
+    a.colexp = reinterpret_cast<int *>(ws + L.colexp);
+    a.smax = reinterpret_cast<double *>(ws + L.smax);
+    a.xtau = reinterpret_cast<int *>(ws + L.xtau);
+    a.i8 = 0;
+    {   // the int8 tensor-core GEMV (SPLIDAR_I8=0 keeps the DMMA / DFMA kernels only)
+        const char *e = getenv("SPLIDAR_I8");
+        if (!(e && e[0] == '0') && i8_supported(dt, a)) {
+            a.i8 = 1;
+            a.strips_i8 = L.N / i8_tile_cols(dt);
+        }
+    }
 
     SPL_CUDA(spl::upload_async(ws + L.lsh, p->lsh.data(), sizeof(int) * p->lsh.size(), s));
     SPL_CUDA(spl::upload_async(ws + L.oidx, p->out_idx.data(), sizeof(int) * p->out_idx.size(), s));
@@ -409,15 +428,31 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
         p->eager = e && e[0] == '1';
     }
 
+    I8Kernels &q = p->q;
+    if (a.i8) SPL_CUDA(i8_kernels(dt, &q, a));
+
     cudaKernelNodeParams kp;
     memset(&kp, 0, sizeof(kp));
     void *init_args[] = {&a};
+    cudaGraphNode_t n_init, n_while, n_step, n_fin, n_prev = nullptr;
+    if (a.i8) {   // range test of the stored matrix: flag = 1, then every column may clear it
+        cudaGraphNode_t n_flag, n_col;
+        kp.func = q.flag_fn;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = init_args;
+        SPL_CUDA(cudaGraphAddKernelNode(&n_flag, p->graph, nullptr, 0, &kp));
+        kp.func = q.colexp_fn;
+        kp.gridDim = q.colexp_grid;
+        kp.blockDim = q.colexp_block;
+        SPL_CUDA(cudaGraphAddKernelNode(&n_col, p->graph, &n_flag, 1, &kp));
+        n_prev = n_col;
+    }
     kp.func = k.init_fn;
     kp.gridDim = k.init_grid;
     kp.blockDim = k.init_block;
     kp.kernelParams = init_args;
-    cudaGraphNode_t n_init, n_while, n_step, n_fin;
-    SPL_CUDA(cudaGraphAddKernelNode(&n_init, p->graph, nullptr, 0, &kp));
+    SPL_CUDA(cudaGraphAddKernelNode(&n_init, p->graph, n_prev ? &n_prev : nullptr, n_prev ? 1 : 0, &kp));
 
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
@@ -428,12 +463,22 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     cudaGraph_t body = cp.conditional.phGraph_out[0];
 
     void *step_args[] = {&a};
+    cudaGraphNode_t n_i8 = nullptr;
+    if (a.i8) {
+        void *i8_args[] = {&a, q.tmap};
+        kp.func = q.step_fn;
+        kp.gridDim = q.step_grid;
+        kp.blockDim = q.step_block;
+        kp.sharedMemBytes = q.step_smem;
+        kp.kernelParams = i8_args;
+        SPL_CUDA(cudaGraphAddKernelNode(&n_i8, body, nullptr, 0, &kp));
+    }
     kp.func = k.step_fn;
     kp.gridDim = k.step_grid;
     kp.blockDim = k.step_block;
     kp.sharedMemBytes = k.step_smem;
     kp.kernelParams = step_args;
-    SPL_CUDA(cudaGraphAddKernelNode(&n_step, body, nullptr, 0, &kp));
+    SPL_CUDA(cudaGraphAddKernelNode(&n_step, body, n_i8 ? &n_i8 : nullptr, n_i8 ? 1 : 0, &kp));
     void *check_args[] = {&a};
     kp.func = k.check_fn;
     kp.gridDim = k.check_grid;
@@ -523,9 +568,16 @@ splidar_status splidar_plan_create(splidar_plan *plan, const void *P0, int32_t n
 static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
     if (!p->host_flag) SPL_CUDA(cudaMallocHost(&p->host_flag, sizeof(unsigned)));
     const SolverKernels &k = p->k;
+    const I8Kernels &q = p->q;
     void *args[] = {&p->eager_args};
+    if (p->args.i8) {
+        SPL_CUDA(cudaLaunchKernel(q.flag_fn, dim3(1), dim3(1), args, 0, s));
+        SPL_CUDA(cudaLaunchKernel(q.colexp_fn, q.colexp_grid, q.colexp_block, args, 0, s));
+    }
     SPL_CUDA(cudaLaunchKernel(k.init_fn, k.init_grid, k.init_block, args, 0, s));
+    void *i8_args[] = {&p->eager_args, const_cast<unsigned char *>(q.tmap)};
     for (int it = 0; it < p->args.max_iter; ++it) {
+        if (p->args.i8) SPL_CUDA(cudaLaunchKernel(q.step_fn, q.step_grid, q.step_block, i8_args, q.step_smem, s));
         SPL_CUDA(cudaLaunchKernel(k.step_fn, k.step_grid, k.step_block, args, k.step_smem, s));
         SPL_CUDA(cudaLaunchKernel(k.check_fn, k.check_grid, k.check_block, args, 0, s));
         SPL_CUDA(cudaMemcpyAsync(p->host_flag, p->eager_args.glob + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));

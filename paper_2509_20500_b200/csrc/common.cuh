@@ -58,7 +58,8 @@ struct __align__(16) SolveState {
 struct WsLayout {
     int N, M, V;    // V padded to a power of two
     int strips, chunks, xstride, pieces;
-    size_t flux, vec, lsh, oidx, y, X, part, ssum, l1part, state, strip_cnt, mv_cnt, act, glob, total;
+    size_t flux, vec, lsh, oidx, y, X, part, ssum, l1part, state, strip_cnt, mv_cnt, act, glob;
+    size_t ximg, colexp, smax, xtau, total;
 };
 
 WsLayout ws_layout(int N, int M, int V);
@@ -100,6 +101,13 @@ struct PowerArgs {
     int max_iter;
     int use_handle;
     cudaGraphConditionalHandle handle;
+    // tcgen05 int8 GEMV (power_i8.cu); glob[3] = 1 when it runs (range test passed)
+    int i8;                  // the plan has the int8 kernels in its loop
+    int strips_i8;           // column tiles of the int8 GEMV (N / TN)
+    unsigned char *ximg;     // [M][N / 64][8192]     x slices in the MMA's K-major image
+    int *colexp;             // [M][N]                column exponents E_j
+    double *smax;            // [M][V][N / 64]        tile maxima of y
+    int *xtau;               // [M][V]                x scale exponents tau_v
 };
 
 // Kernel node parameters for the three solver kernels (for graph construction).
@@ -115,6 +123,16 @@ struct SolverKernels {
     size_t step_smem;
 };
 int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a);
+// int8 tensor-core GEMV (power_i8.cu)
+struct I8Kernels {
+    alignas(64) unsigned char tmap[128];   // CUtensorMap of the stored matrices (a kernel parameter)
+    void *step_fn, *colexp_fn, *flag_fn;
+    dim3 step_grid, step_block, colexp_grid, colexp_block;
+    size_t step_smem;
+};
+int i8_supported(int dtype, const PowerArgs &a);
+cudaError_t i8_kernels(int dtype, I8Kernels *k, const PowerArgs &a);
+int i8_tile_cols(int dtype);
 size_t finish_args_size();
 // pi output: out_idx[mv] >= 0 selects row out_idx[mv] of pi ([*, N]); < 0 skips the vector.
 void make_finish_args(void *dst, const PowerArgs &a, double *pi, const int *out_idx);

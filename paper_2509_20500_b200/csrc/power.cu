@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
 
     const int tid = threadIdx.x, b = blockIdx.x, G = gridDim.x;
     const int N = a.N, S = a.strips;
+    if (a.i8 && a.glob[3]) return;                  // the int8 tensor-core GEMV runs this plan
     const int n_act = (int)a.glob[2];
     const int64_t T_units = (int64_t)n_act * S * N;
     if (T_units == 0) return;
@@ -444,23 +445,58 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
         const int m = mv / a.V, v = mv % a.V;
         // s = the strip sums added by every warp in the same fixed order (lane-strided, xor tree), so
         // all CTAs of (matrix, vector) hold the bitwise-same s
+        const bool i8 = a.i8 && a.glob[3];
+        const int nstrips = i8 ? a.strips_i8 : a.strips;
         double S = 0.0;
-        const double *ss = a.ssum + (size_t)mv * a.strips;
-        for (int k = tid & 31; k < a.strips; k += 32) S += __ldcg(ss + k);
+        const double *ss = a.ssum + (size_t)mv * nstrips;
+        for (int k = tid & 31; k < nstrips; k += 32) S += __ldcg(ss + k);
         S = warp_sum(S);
         const double inv_new = 1.0 / S, inv_old = 1.0 / st.s;
         const double *yn = a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
         const double *yo = a.y + ((size_t)mv * 2 + st.cur) * N;
-        double *X = a.X + (size_t)m * N * a.xstride + v;
         const int l = st.l < 0 ? 0 : st.l;
         double l1 = 0.0;
-        const int j1 = min(N, (c + 1) * kCheckChunk);
-        for (int j = c * kCheckChunk + tid; j < j1; j += 256) {
-            const double pn = __ldcg(yn + j) * inv_new;
-            l1 += fabs(pn - yo[j] * inv_old);
-            int r = j + l;
-            if (r >= N) r -= N;
-            X[(size_t)r * a.xstride] = pn;
+        if (i8) {
+            // next x in the int8 GEMV's form: x~ = floor(pi^{k+1} 2^tau) in 7 bytes (power_i8.cu),
+            // tau from the largest y (tile maxima), written at the gathered row r = (j + l) mod N
+            double ym = 0.0;
+            const double *sm = a.smax + (size_t)mv * nstrips;
+            for (int k = tid & 31; k < nstrips; k += 32) ym = fmax(ym, __ldcg(sm + k));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ym = fmax(ym, __shfl_xor_sync(0xffffffffu, ym, o));
+            const double pmax = ym * inv_new;
+            const int tau = pmax > 0.0 ? 55 - ilogb(pmax) : 0;
+            if (c == 0 && tid == 0) a.xtau[mv] = tau;
+            const int r0 = c * kCheckChunk + tid * 8;         // 8 consecutive gathered rows
+            if (r0 < N) {
+                uint64_t wq[7] = {0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    int j = r0 + e - l;
+                    if (j < 0) j += N;
+                    const double pn = __ldcg(yn + j) * inv_new;
+                    l1 += fabs(pn - yo[j] * inv_old);
+                    const uint64_t xt = (uint64_t)ldexp(pn, tau);
+#pragma unroll
+                    for (int q = 0; q < 7; ++q) wq[q] |= ((xt >> (8 * (6 - q))) & 0xFFull) << (8 * e);
+                }
+                unsigned char *img = a.ximg + ((size_t)m * (N / 64) + r0 / 64) * 8192 + ((r0 % 64) / 16) * 128 + (r0 % 16);
+#pragma unroll
+                for (int q = 0; q < 7; ++q) {
+                    const int row = q * a.V + v;
+                    *reinterpret_cast<uint64_t *>(img + (row / 8) * 512 + (row % 8) * 16) = wq[q];
+                }
+            }
+        } else {
+            double *X = a.X + (size_t)m * N * a.xstride + v;
+            const int j1 = min(N, (c + 1) * kCheckChunk);
+            for (int j = c * kCheckChunk + tid; j < j1; j += 256) {
+                const double pn = __ldcg(yn + j) * inv_new;
+                l1 += fabs(pn - yo[j] * inv_old);
+                int r = j + l;
+                if (r >= N) r -= N;
+                X[(size_t)r * a.xstride] = pn;
+            }
         }
         l1 = warp_sum(l1);
         if ((tid & 31) == 0) red[tid >> 5] = l1;
@@ -535,6 +571,24 @@ __global__ void k_power_init(const PowerArgs a) {
         y[j] = u;
         X[(size_t)j * a.xstride + v] = u;
         if (a.V == 1) X[(size_t)j * a.xstride + 1] = 0.0;   // padding column of the 16-byte x row
+    }
+    if (a.i8 && a.glob[3]) {
+        // x^0 = 1/N in the int8 GEMV's slices (rows q V + v; zero for unused vectors), and v = 0
+        // zeroes the image rows 7 V .. 127 that no vector owns
+        const int tau = 55 - ilogb(u);
+        const uint64_t xt = a.lsh[mv] >= 0 ? (uint64_t)ldexp(u, tau) : 0ull;
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.xtau[mv] = tau;
+        for (int r0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8; r0 < N; r0 += gridDim.x * blockDim.x * 8) {
+            unsigned char *img = a.ximg + ((size_t)m * (N / 64) + r0 / 64) * 8192 + ((r0 % 64) / 16) * 128 + (r0 % 16);
+            for (int q = 0; q < 7; ++q) {
+                const uint64_t b = (xt >> (8 * (6 - q))) & 0xFFull;
+                const int row = q * a.V + v;
+                *reinterpret_cast<uint64_t *>(img + (row / 8) * 512 + (row % 8) * 16) = b * 0x0101010101010101ull;
+            }
+            if (v == 0)
+                for (int row = 7 * a.V; row < 128; ++row)
+                    *reinterpret_cast<uint64_t *>(img + (row / 8) * 512 + (row % 8) * 16) = 0ull;
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         SolveState s;
