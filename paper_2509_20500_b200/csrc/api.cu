@@ -55,6 +55,7 @@ WsLayout ws_layout(int N, int M, int V) {
     // int8 tensor-core GEMV: x-slice image (128 bytes per row), column exponents, tile maxima, x scales
     L.ximg = o; o = a256(o + (size_t)M * tiles64 * 64 * 128);
     L.colexp = o; o = a256(o + sizeof(int) * (size_t)M * N);
+    L.colmin = o; o = a256(o + sizeof(int) * (size_t)M * N);
     L.smax = o; o = a256(o + sizeof(double) * MV * tiles64);
     L.xtau = o; o = a256(o + sizeof(int) * MV);
     L.total = o;
@@ -372,6 +373,7 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     a.xstride = L.xstride;
     a.ximg = reinterpret_cast<unsigned char *>(ws + L.ximg);
     a.colexp = reinterpret_cast<int *>(ws + L.colexp);
+    a.colmin = reinterpret_cast<int *>(ws + L.colmin);
     a.smax = reinterpret_cast<double *>(ws + L.smax);
     a.xtau = reinterpret_cast<int *>(ws + L.xtau);
     a.i8 = 0;
@@ -379,6 +381,8 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
         const char *e = getenv("SPLIDAR_I8");
         if (!(e && e[0] == '0') && i8_supported(dt, a)) {
             a.i8 = 1;
+            const char *d = getenv("SPLIDAR_I8_DBG");
+            a.i8_dbg = d ? atoi(d) : 0;
             a.strips_i8 = L.N / i8_tile_cols(dt);
         }
     }
@@ -435,18 +439,26 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     memset(&kp, 0, sizeof(kp));
     void *init_args[] = {&a};
     cudaGraphNode_t n_init, n_while, n_step, n_fin, n_prev = nullptr;
+    int rows_per_cta = q.rows_per_cta;
+    void *colexp_args[] = {&a, &rows_per_cta};
     if (a.i8) {   // range test of the stored matrix: flag = 1, then every column may clear it
-        cudaGraphNode_t n_flag, n_col;
-        kp.func = q.flag_fn;
-        kp.gridDim = dim3(1);
-        kp.blockDim = dim3(1);
+        cudaGraphNode_t n_prep, n_col, n_chk;
+        kp.func = q.prep_fn;
+        kp.gridDim = q.small_grid;
+        kp.blockDim = dim3(256);
         kp.kernelParams = init_args;
-        SPL_CUDA(cudaGraphAddKernelNode(&n_flag, p->graph, nullptr, 0, &kp));
+        SPL_CUDA(cudaGraphAddKernelNode(&n_prep, p->graph, nullptr, 0, &kp));
         kp.func = q.colexp_fn;
         kp.gridDim = q.colexp_grid;
         kp.blockDim = q.colexp_block;
-        SPL_CUDA(cudaGraphAddKernelNode(&n_col, p->graph, &n_flag, 1, &kp));
-        n_prev = n_col;
+        kp.kernelParams = colexp_args;
+        SPL_CUDA(cudaGraphAddKernelNode(&n_col, p->graph, &n_prep, 1, &kp));
+        kp.func = q.check_fn;
+        kp.gridDim = q.small_grid;
+        kp.blockDim = dim3(256);
+        kp.kernelParams = init_args;
+        SPL_CUDA(cudaGraphAddKernelNode(&n_chk, p->graph, &n_col, 1, &kp));
+        n_prev = n_chk;
     }
     kp.func = k.init_fn;
     kp.gridDim = k.init_grid;
@@ -571,8 +583,11 @@ static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
     const I8Kernels &q = p->q;
     void *args[] = {&p->eager_args};
     if (p->args.i8) {
-        SPL_CUDA(cudaLaunchKernel(q.flag_fn, dim3(1), dim3(1), args, 0, s));
-        SPL_CUDA(cudaLaunchKernel(q.colexp_fn, q.colexp_grid, q.colexp_block, args, 0, s));
+        int rpc = q.rows_per_cta;
+        void *cargs[] = {&p->eager_args, &rpc};
+        SPL_CUDA(cudaLaunchKernel(q.prep_fn, q.small_grid, dim3(256), args, 0, s));
+        SPL_CUDA(cudaLaunchKernel(q.colexp_fn, q.colexp_grid, q.colexp_block, cargs, 0, s));
+        SPL_CUDA(cudaLaunchKernel(q.check_fn, q.small_grid, dim3(256), args, 0, s));
     }
     SPL_CUDA(cudaLaunchKernel(k.init_fn, k.init_grid, k.init_block, args, 0, s));
     void *i8_args[] = {&p->eager_args, const_cast<unsigned char *>(q.tmap)};
@@ -582,7 +597,7 @@ static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
         SPL_CUDA(cudaLaunchKernel(k.check_fn, k.check_grid, k.check_block, args, 0, s));
         SPL_CUDA(cudaMemcpyAsync(p->host_flag, p->eager_args.glob + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
         SPL_CUDA(cudaStreamSynchronize(s));
-        if (!*p->host_flag) break;
+        if (!*p->host_flag && !p->args.i8_dbg) break;
     }
     void *fargs[] = {p->fin_args.data()};
     SPL_CUDA(cudaLaunchKernel(k.finish_fn, k.finish_grid, k.finish_block, fargs, 0, s));

@@ -59,7 +59,7 @@ struct WsLayout {
     int N, M, V;    // V padded to a power of two
     int strips, chunks, xstride, pieces;
     size_t flux, vec, lsh, oidx, y, X, part, ssum, l1part, state, strip_cnt, mv_cnt, act, glob;
-    size_t ximg, colexp, smax, xtau, total;
+    size_t ximg, colexp, colmin, smax, xtau, total;
 };
 
 WsLayout ws_layout(int N, int M, int V);
@@ -106,8 +106,10 @@ struct PowerArgs {
     int strips_i8;           // column tiles of the int8 GEMV (N / TN)
     unsigned char *ximg;     // [M][N / 64][8192]     x slices in the MMA's K-major image
     int *colexp;             // [M][N]                column exponents E_j
+    int *colmin;             // [M][N]                smallest exponent of a non-zero entry (range test)
     double *smax;            // [M][V][N / 64]        tile maxima of y
     int *xtau;               // [M][V]                x scale exponents tau_v
+    int i8_dbg;              // timing experiments only (SPLIDAR_I8_DBG): 1 skip conversion, 2 skip MMA
 };
 
 // Kernel node parameters for the three solver kernels (for graph construction).
@@ -126,9 +128,10 @@ int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a);
 // int8 tensor-core GEMV (power_i8.cu)
 struct I8Kernels {
     alignas(64) unsigned char tmap[128];   // CUtensorMap of the stored matrices (a kernel parameter)
-    void *step_fn, *colexp_fn, *flag_fn;
-    dim3 step_grid, step_block, colexp_grid, colexp_block;
+    void *step_fn, *colexp_fn, *check_fn, *prep_fn;
+    dim3 step_grid, step_block, colexp_grid, colexp_block, small_grid;
     size_t step_smem;
+    int rows_per_cta;
 };
 int i8_supported(int dtype, const PowerArgs &a);
 cudaError_t i8_kernels(int dtype, I8Kernels *k, const PowerArgs &a);

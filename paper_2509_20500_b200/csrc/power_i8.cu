@@ -20,17 +20,23 @@
 // k_power_step_i8<T>: persistent, one CTA per SM (TMEM: NP x TN = 512 columns). Work units are
 // (active matrix, column tile of TN = 128 (fp32) / 64 (fp64) columns, k-block of 64 rows), split
 // into equal contiguous ranges (stream-K). Warp roles:
-//   warp 0      TMA producer: the unit's 64 x 512-byte tile of P~0 as 4 tensor-map boxes of 64 rows
-//               x 128 B (cp.async.bulk.tensor, 128-byte swizzle) into a 3-stage ring, and its 8 KB
-//               x-slice image (written by k_power_check, cp.async.bulk) into the MMA buffer;
-//   warp 1      MMA issuer (one thread): per unit 2 k-steps x NP tcgen05.mma (M = 128 rows
-//               (q, v) of x slices, N = TN columns, K = 32), D_p in TMEM columns [p TN, (p+1) TN);
+//   warp 3      TMA producer: the unit's 64 x 512-byte tile of P~0 as 4 tensor-map boxes of 64 rows
+//               x 128 B (cp.async.bulk.tensor, 128-byte swizzle) into a 3-stage ring;
+//   warp 0      x-slice producer: the unit's 8 KB image (written by k_power_check) with one
+//               cp.async.bulk into the MMA buffer, once the MMA has freed it (3 buffers);
+//   warp 1      MMA issuer (one thread): per unit 2 k-steps x 2 tcgen05.mma of M = 128 rows (q, v)
+//               of x slices, N = 256 columns (2 fp32 / 4 fp64 byte planes side by side), K = 32;
+//               D_p in TMEM columns [p TN, (p+1) TN);
 //   warp 2      TMEM allocator;
-//   warps 4-11  converters: each unit's fp32/fp64 tile -> NP byte planes in the canonical MN-major
-//               layout (byte transposes with PRMT), then at the end of a piece the epilogue:
+//   warps 4-11  converters: each unit's tile -> NP byte planes in the canonical MN-major layout
+//               (byte transposes with PRMT); shared-memory bandwidth (TMA write, converter read and
+//               write, MMA operand reads: ~152 KB per 32 KB unit) is the budget the layout is cut
+//               for -- N = 256 MMAs read the x slices once per 2 (fp32) / 4 (fp64) planes. At the
+//               end of a piece the epilogue:
 //               TMEM -> registers (tcgen05.ld), sum over p and q in fp64, per-piece partial sums;
 //               the last piece of a tile adds the pieces in fixed order (deterministic), writes y,
 //               the tile's sum and max of y (the next x scale).
+#include <climits>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -46,9 +52,7 @@ constexpr int kI8Conv0 = 4;              // first converter warp
 constexpr int kI8ConvThreads = 256;      // 8 converter warps
 constexpr int kKB = 64;                  // rows per unit
 constexpr int kRowBytes = 512;           // bytes of a row segment per unit (128 fp32 / 64 fp64)
-constexpr int kBoxBytes = kKB * 128;     // one tensor-map box: 64 rows x 128 B (128-byte swizzle)
-constexpr int kAStages = 3;
-constexpr int kABytes = kKB * kRowBytes;     // 4 boxes = 32 KB
+constexpr int kSBuf = 3;                 // slice + x buffers between the converters and the MMA
 constexpr int kSBytes = kKB * kRowBytes;     // byte planes of one unit: NP x 64 x TN = 32 KB
 constexpr int kXBytes = 128 * kKB;           // x-slice image of one unit: 8 KB
 constexpr int kXQ = 7;                       // x slices
@@ -62,20 +66,13 @@ template <> struct I8Cfg<double> {
 };
 
 struct __align__(8) I8Bars {
-    uint64_t a_full[kAStages], a_empty[kAStages];
-    uint64_t s_full[2], x_full[2], s_empty[2];
+    uint64_t a_full[3], a_empty[3];
+    uint64_t s_full[kSBuf], x_full[kSBuf], s_empty[kSBuf];
     uint64_t t_full, t_empty;
 };
 
-constexpr size_t kI8Smem = 1024 + (size_t)kAStages * kABytes + 2 * (size_t)kSBytes + 2 * (size_t)kXBytes + 1024;
+constexpr size_t kI8Smem = 1024 + 3 * 32768 + kSBuf * (size_t)kSBytes + kSBuf * (size_t)kXBytes + 1024;
 
-// 2-D / 3-D tensor-map copy global -> shared (box at coordinates {c0 elements, c1 rows, c2 matrix}).
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-        ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -103,17 +100,22 @@ __device__ __forceinline__ void transpose4(uint32_t w0, uint32_t w1, uint32_t w2
 // PTX shl clamps the shift amount to the register width, so a zero entry (e = 0, shift e - base
 // < 0, i.e. huge as unsigned) gives 0 without a select; k_i8_colexp guarantees base > 0 for every
 // column with a non-zero entry and sets E_j = 255 / 2047 (base > 0 as well) for all-zero columns.
-__device__ __forceinline__ uint32_t fx32(uint32_t u, int base) {
-    const uint32_t m = (u & 0x7FFFFFu) | 0x800000u;
+// fp32: the significand 1.m left-aligned as the 64-bit value (1 : m << 9) = 2^9 sig, shifted left
+// by s = sh + 23 with a clamping funnel shift; the high word is sig << sh (3 integer ops per entry).
+// For a zero entry s < 0 (huge as unsigned) clamps to 32 and the funnel returns the low word, 0.
+__device__ __forceinline__ uint32_t fx32(uint32_t u, int base23) {
+    const uint32_t s = (uint32_t)((int)(u >> 23) - base23);          // e - base + 23
     uint32_t r;
-    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(m), "r"((uint32_t)((int)(u >> 23) - base)));
+    asm("shf.l.clamp.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(u << 9), "r"(1u), "r"(s));
     return r;
 }
-__device__ __forceinline__ uint64_t fx64(uint64_t u, int base) {
-    const uint64_t m = (u & 0xFFFFFFFFFFFFFull) | (1ull << 52);
-    uint64_t r;
-    asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(m), "r"((uint32_t)((int)(u >> 52) - base)));
-    return r;
+// fp64: 53-bit significand (hi 21 bits : lo 32 bits) << sh, sh <= 11, as two clamping shifts; a zero
+// entry has sh < 0: both clamp to 0 (the funnel returns the zero low word).
+__device__ __forceinline__ void fx64(uint32_t lo, uint32_t hi, int base, uint32_t &rlo, uint32_t &rhi) {
+    const uint32_t sh = (uint32_t)((int)(hi >> 20) - base);
+    const uint32_t sig_hi = (hi & 0xFFFFFu) | 0x100000u;
+    asm("shf.l.clamp.b32 %0, %1, %2, %3;" : "=r"(rhi) : "r"(lo), "r"(sig_hi), "r"(sh));
+    asm("shl.b32 %0, %1, %2;" : "=r"(rlo) : "r"(lo), "r"(sh));
 }
 
 // Walks the units (active matrix ai, column tile c, k-block kb) of a CTA's range without divisions.
@@ -144,23 +146,41 @@ struct Ring {
     }
 };
 
-// Byte-plane image of a unit: plane p at p * (64 TN); within a plane the MN-major canonical
-// layout: (r / 8) * (TN / 16) * 128 + (j / 16) * 128 + (r % 8) * 16 + j % 16.
-// The unit's tile in shared memory is 4 boxes of [64 rows][128 B] with the 128-byte swizzle: the
-// 16-byte chunk c of row r sits at chunk c ^ (r % 8) (so the 8 rows of one core matrix read
-// their chunks from 8 different bank groups).
+// Byte-plane image of a unit (the MMA's B operand, MN-major SWIZZLE_NONE): core matrices of
+// 8 rows x 16 columns, all NP planes of one 8-row group side by side, so that one MMA with N = 256
+// spans 256 / TN consecutive planes (their accumulators are adjacent in TMEM):
+//   offset(p, r, j) = (r / 8) * 4096 + (p * TN / 16 + j / 16) * 128 + (r % 8) * 16 + j % 16.
+// LBO (next 8 rows) = 4096 B, SBO (next 16 columns) = 128 B.
+constexpr int kKGroup = 4096;
+
+// The unit's tile arrives in shared memory as 4 tensor-map boxes of [64 rows][128 B] with the
+// 128-byte swizzle (the 16-byte chunk c of row r sits at chunk c ^ (r % 8), so the 8 rows of one
+// core matrix read their chunks from 8 different bank groups). Converter item = (row r, 16-column
+// block jb): 16 entries -> NP plane rows of 16 bytes (one 16-byte store each; the 8 rows of a
+// core matrix are 8 consecutive lanes: conflict-free).
+constexpr int kBoxBytes = kKB * 128;
+constexpr int kAStages = 3;
+constexpr int kABytes = 4 * kBoxBytes;       // 32 KB
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ void convert_item(const unsigned char *tile, unsigned char *splanes, int r, int jb,
                                              const int (&base)[16]) {
     using C = I8Cfg<T>;
-    constexpr int PLANE = kKB * C::TN;
-    unsigned char *dst = splanes + (r >> 3) * (C::TN / 16) * 128 + jb * 128 + (r & 7) * 16;
+    constexpr int CB = C::TN / 16;
+    unsigned char *dst = splanes + (r >> 3) * kKGroup + jb * 128 + (r & 7) * 16;   // plane p: + p * CB * 128
     const int sw = r & 7;
     if constexpr (sizeof(T) == 4) {
         // columns 16 jb .. 16 jb + 15: box jb / 2, chunks 4 (jb % 2) .. + 3
         const unsigned char *row = tile + (jb >> 1) * kBoxBytes + r * 128;
         const int c0 = (jb & 1) * 4;
-        uint32_t pw[4][4];                              // [plane byte k][word g]
+        uint32_t pw[4][4];                              // [byte k][word g]
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
             const uint4 v = *reinterpret_cast<const uint4 *>(row + (((c0 + g) ^ sw) << 4));
@@ -172,7 +192,7 @@ __device__ __forceinline__ void convert_item(const unsigned char *tile, unsigned
         }
 #pragma unroll
         for (int p = 0; p < 4; ++p)                    // plane p = byte 3 - p
-            *reinterpret_cast<uint4 *>(dst + p * PLANE) = make_uint4(pw[3 - p][0], pw[3 - p][1], pw[3 - p][2], pw[3 - p][3]);
+            *reinterpret_cast<uint4 *>(dst + p * CB * 128) = make_uint4(pw[3 - p][0], pw[3 - p][1], pw[3 - p][2], pw[3 - p][3]);
     } else {
         // columns 16 jb .. 16 jb + 15: box jb, chunks 0 .. 7
         const unsigned char *row = tile + jb * kBoxBytes + r * 128;
@@ -181,13 +201,14 @@ __device__ __forceinline__ void convert_item(const unsigned char *tile, unsigned
         for (int g = 0; g < 4; ++g) {                   // 4 entries per word group
             const uint4 v0 = *reinterpret_cast<const uint4 *>(row + (((2 * g) ^ sw) << 4));
             const uint4 v1 = *reinterpret_cast<const uint4 *>(row + (((2 * g + 1) ^ sw) << 4));
-            const uint64_t e0 = fx64(((uint64_t)v0.y << 32) | v0.x, base[4 * g]);
-            const uint64_t e1 = fx64(((uint64_t)v0.w << 32) | v0.z, base[4 * g + 1]);
-            const uint64_t e2 = fx64(((uint64_t)v1.y << 32) | v1.x, base[4 * g + 2]);
-            const uint64_t e3 = fx64(((uint64_t)v1.w << 32) | v1.z, base[4 * g + 3]);
+            uint32_t l0, h0, l1, h1, l2, h2, l3, h3;
+            fx64(v0.x, v0.y, base[4 * g], l0, h0);
+            fx64(v0.z, v0.w, base[4 * g + 1], l1, h1);
+            fx64(v1.x, v1.y, base[4 * g + 2], l2, h2);
+            fx64(v1.z, v1.w, base[4 * g + 3], l3, h3);
             uint32_t lo[4], hi[4];
-            transpose4((uint32_t)e0, (uint32_t)e1, (uint32_t)e2, (uint32_t)e3, lo);
-            transpose4((uint32_t)(e0 >> 32), (uint32_t)(e1 >> 32), (uint32_t)(e2 >> 32), (uint32_t)(e3 >> 32), hi);
+            transpose4(l0, l1, l2, l3, lo);
+            transpose4(h0, h1, h2, h3, hi);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 pw[k][g] = lo[k];
@@ -196,8 +217,132 @@ __device__ __forceinline__ void convert_item(const unsigned char *tile, unsigned
         }
 #pragma unroll
         for (int p = 0; p < 8; ++p)                    // plane p = byte 7 - p
-            *reinterpret_cast<uint4 *>(dst + p * PLANE) = make_uint4(pw[7 - p][0], pw[7 - p][1], pw[7 - p][2], pw[7 - p][3]);
+            *reinterpret_cast<uint4 *>(dst + p * CB * 128) = make_uint4(pw[7 - p][0], pw[7 - p][1], pw[7 - p][2], pw[7 - p][3]);
     }
+}
+
+struct PieceCtx {
+    int m, c;
+    int64_t g;
+};
+
+// Epilogue of a piece (matrix m, tile c): TMEM -> fp64 partial sums of y per running vector; the
+// last piece of the tile adds the pieces in fixed order (deterministic), writes y and the tile's
+// sum and maximum of y. Executed by the 256 converter threads.
+template <typename T>
+__device__ __forceinline__ void epilogue(const PowerArgs &a, const PieceCtx &pc, uint32_t tmem, unsigned char *sS,
+                                         I8Bars *bars, int piece, int64_t U, int b, int *s_vmap, int *s_cur,
+                                         int *s_tau, int *s_nact, int *s_last) {
+    using C = I8Cfg<T>;
+    constexpr int NP = C::NP, TN = C::TN;
+    const int ct = threadIdx.x - kI8Conv0 * 32, cw = ct >> 5, lane = threadIdx.x & 31;
+    const int N = a.N, kbs = N / kKB, VP = a.V, m = pc.m, c = pc.c;
+    const int64_t g = pc.g;
+    if (ct == 0) {
+        int n = 0;
+        for (int v = 0; v < VP; ++v) {
+            const SolveState st = a.st[(size_t)m * VP + v];
+            if (!st.done) { s_vmap[n] = v; s_cur[n] = st.cur; ++n; }
+            s_tau[v] = a.xtau[(size_t)m * VP + v];
+        }
+        *s_nact = n;
+    }
+    mbar_wait(&bars->t_full, piece & 1);
+    tc05::fence_after();
+    named_sync(1, kI8ConvThreads);
+    const int quad = cw & 3, half = cw >> 2;
+    const int row = 32 * quad + lane;                       // TMEM lane = x-slice row (q, v)
+    const int q = row / VP;
+    const bool live = q < kXQ;
+    double *stage = reinterpret_cast<double *>(sS);         // [2 halves][16 cols][128 rows]
+    constexpr int CW = 16;                                  // columns per chunk
+    constexpr int CHUNKS = TN / 2 / CW;                     // chunks per warp (its half of the tile)
+    const int64_t gN = g * kbs;
+    double *part = a.part + (size_t)(b + g) * VP * TN;
+    const int nact = *s_nact;
+    for (int ch = 0; ch < CHUNKS; ++ch) {
+        const int col0 = half * (TN / 2) + ch * CW;
+        double acc[CW];
+#pragma unroll
+        for (int i = 0; i < CW; ++i) acc[i] = 0.0;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            uint32_t r[CW];
+            tc05::ld32x16(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(p * TN + col0), r);
+            tc05::wait_ld();
+            const double w = ldexp(1.0, 8 * (NP - 1 - p) + 8 * (kXQ - 1 - (live ? q : 0)));
+#pragma unroll
+            for (int i = 0; i < CW; ++i) acc[i] = fma((double)(int)r[i], w, acc[i]);
+        }
+        double *st = stage + (size_t)half * CW * 128;
+#pragma unroll
+        for (int i = 0; i < CW; ++i) st[i * 128 + row] = live ? acc[i] : 0.0;
+        named_sync(2 + half, 128);
+        // y partial for (v, col0 + i): sum over q (fixed order, largest slice first)
+        const int t = ct & 127;
+        for (int o = t; o < nact * CW; o += 128) {
+            const int sl = o / CW, i = o % CW;
+            const int v = s_vmap[sl];
+            double ysum = 0.0;
+#pragma unroll
+            for (int qq = 0; qq < kXQ; ++qq) ysum += st[i * 128 + qq * VP + v];
+            const int j = c * TN + col0 + i;
+            const int ex = a.colexp[(size_t)m * N + j] - C::BIAS_MBITS - C::R - s_tau[v];
+            part[(size_t)v * TN + col0 + i] = ldexp(ysum, ex);
+        }
+        named_sync(2 + half, 128);
+    }
+    tc05::fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars->t_empty);
+    // ---- last piece of the tile: add the pieces in fixed order, write y, tile sum / max ----
+    __threadfence();
+    named_sync(1, kI8ConvThreads);
+    const int first_p = (int)(gN / U), last_p = (int)((gN + kbs - 1) / U);
+    if (ct == 0) {
+        const unsigned prev = atomicAdd(&a.strip_cnt[g], 1u);
+        *s_last = prev == (unsigned)(last_p - first_p);
+    }
+    named_sync(1, kI8ConvThreads);
+    if (*s_last) {
+        __threadfence();
+        double *red = reinterpret_cast<double *>(sS);                  // [8 warps][2][32] (stage is free)
+        for (int sl = 0; sl < nact; ++sl) {
+            const int v = s_vmap[sl];
+            double ysum = 0.0, ymax = 0.0;
+            if (ct < TN) {
+                double yv = 0.0;
+                for (int pcs = first_p; pcs <= last_p; ++pcs)
+                    yv += __ldcg(a.part + ((size_t)(pcs + g) * VP + v) * TN + ct);
+                a.y[(((size_t)m * VP + v) * 2 + (1 - s_cur[sl])) * N + (size_t)c * TN + ct] = yv;
+                ysum = yv;
+                ymax = yv;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
+                ymax = fmax(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
+            }
+            if (lane == 0) {
+                red[(cw * 2 + 0) * kMaxVectors + sl] = ysum;
+                red[(cw * 2 + 1) * kMaxVectors + sl] = ymax;
+            }
+        }
+        named_sync(1, kI8ConvThreads);
+        if (ct < nact) {
+            double ssum = 0.0, smax = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                ssum += red[(w * 2 + 0) * kMaxVectors + ct];
+                smax = fmax(smax, red[(w * 2 + 1) * kMaxVectors + ct]);
+            }
+            const size_t mv = (size_t)m * VP + s_vmap[ct];
+            a.ssum[mv * a.strips_i8 + c] = ssum;
+            a.smax[mv * a.strips_i8 + c] = smax;
+        }
+        if (ct == 0) a.strip_cnt[g] = 0u;
+    }
+    named_sync(1, kI8ConvThreads);
 }
 
 template <typename T>
@@ -207,7 +352,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
     if (!a.glob[3]) return;                             // range test failed: the DMMA kernel runs
     const int N = a.N;
     const int tiles = N / TN, kbs = N / kKB;
-    const int n_act = (int)a.glob[2];
+    const int n_act = a.i8_dbg ? a.M : (int)a.glob[2];      // timing experiments: every matrix, always
     const int64_t T_units = (int64_t)n_act * tiles * kbs;
     if (T_units == 0) return;
     const int G = gridDim.x, b = blockIdx.x;
@@ -218,11 +363,11 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
     const int64_t u_end = u_begin + U < T_units ? u_begin + U : T_units;
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);   // swizzle atoms: 1 KB aligned
+    unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     unsigned char *sA = smem;                                       // [3][4 boxes][64][128]
-    unsigned char *sS = sA + kAStages * kABytes;                    // [2][NP planes][64 x TN]
-    unsigned char *sX = sS + 2 * kSBytes;                           // [2][8 KB]
-    I8Bars *bars = reinterpret_cast<I8Bars *>(sX + 2 * kXBytes);
+    unsigned char *sS = sA + kAStages * kABytes;                    // [kSBuf][64 rows x NP planes x TN]
+    unsigned char *sX = sS + kSBuf * kSBytes;                       // [kSBuf][8 KB]
+    I8Bars *bars = reinterpret_cast<I8Bars *>(sX + kSBuf * kXBytes);
     __shared__ uint32_t s_tmem;
     __shared__ int s_vmap[kMaxVectors], s_cur[kMaxVectors], s_tau[kMaxVectors], s_nact, s_last;
 
@@ -232,7 +377,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
             mbar_init(&bars->a_full[i], 1);
             mbar_init(&bars->a_empty[i], 8);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kSBuf; ++i) {
             mbar_init(&bars->s_full[i], 8);
             mbar_init(&bars->x_full[i], 1);
             mbar_init(&bars->s_empty[i], 1);
@@ -247,15 +392,14 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
     tc05::fence_after();
     const uint32_t tmem = s_tmem;
 
-    if (warp == 0) {
-        // ------------------------------------------------------------------ TMA producer
+    if (warp == 3) {
+        // ------------------------------------------------------------------ TMA producer of P~0 tiles
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
             UnitCursor cu(u_begin, kbs, tiles);
             Ring<kAStages> ra;
-            Ring<2> rb;
-            for (int64_t u = u_begin; u < u_end; ++u, cu.next(kbs, tiles), ra.next(), rb.next()) {
-                const int m = a.act[cu.ai];
+            for (int64_t u = u_begin; u < u_end; ++u, cu.next(kbs, tiles), ra.next()) {
+                const int m = a.i8_dbg ? cu.ai : a.act[cu.ai];
                 mbar_wait(&bars->a_empty[ra.i], ra.ph ^ 1);
                 mbar_expect_tx(&bars->a_full[ra.i], kABytes);
                 unsigned char *dst = sA + ra.i * kABytes;
@@ -263,6 +407,15 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
 #pragma unroll
                 for (int bx = 0; bx < 4; ++bx)
                     tma_load_3d(dst + bx * kBoxBytes, &tmap, cu.c * TN + bx * BOXC, cu.kb * kKB, m, &bars->a_full[ra.i]);
+            }
+        }
+    } else if (warp == 0) {
+        // ------------------------------------------------------------------ x-slice producer
+        if (lane == 0) {
+            UnitCursor cu(u_begin, kbs, tiles);
+            Ring<kSBuf> rb;
+            for (int64_t u = u_begin; u < u_end; ++u, cu.next(kbs, tiles), rb.next()) {
+                const int m = a.i8_dbg ? cu.ai : a.act[cu.ai];
                 mbar_wait(&bars->s_empty[rb.i], rb.ph ^ 1);
                 mbar_expect_tx(&bars->x_full[rb.i], kXBytes);
                 bulk_g2s(sX + rb.i * kXBytes, a.ximg + ((size_t)m * kbs + cu.kb) * kXBytes, kXBytes, &bars->x_full[rb.i]);
@@ -271,31 +424,32 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
     } else if (warp == 1) {
         // ------------------------------------------------------------------ MMA issuer
         if (lane == 0) {
-            const uint32_t idesc = tc05::idesc_i8(128, TN, true);
+            const uint32_t idesc = tc05::idesc_i8(128, 256, true);
             const uint32_t sS_u = smem_u32(sS), sX_u = smem_u32(sX);
             int piece = 0;
             UnitCursor cu(u_begin, kbs, tiles);
-            Ring<2> rb;
+            Ring<kSBuf> rb;
             for (int64_t u = u_begin; u < u_end; ++u, cu.next(kbs, tiles), rb.next()) {
                 const bool first = u == u_begin || cu.kb == 0;
                 const bool last = u + 1 == u_end || cu.kb + 1 == kbs;
                 const int sb = rb.i;
-                const uint32_t ph = rb.ph;
                 if (first) {
                     mbar_wait(&bars->t_empty, (piece & 1) ^ 1);
                     tc05::fence_after();
                 }
-                mbar_wait(&bars->x_full[sb], ph);
-                mbar_wait(&bars->s_full[sb], ph);
+                mbar_wait(&bars->x_full[sb], rb.ph);
+                mbar_wait(&bars->s_full[sb], rb.ph);
                 tc05::fence_after();
+                // per k-step of 32 rows, NP * TN / 256 = 2 MMAs of N = 256 (2 fp32 / 4 fp64 planes each)
 #pragma unroll
-                for (int s = 0; s < kKB / 32; ++s) {
-                    const uint64_t ad = tc05::smem_desc(sX_u + sb * kXBytes + s * 256, 128, 512);
+                for (int h = 0; h < NP * TN / 256; ++h) {
+                    if (a.i8_dbg & 2) break;
 #pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        const uint64_t bd = tc05::smem_desc(sS_u + sb * kSBytes + p * (kKB * TN) + s * 4 * (TN / 16) * 128,
-                                                            (TN / 16) * 128, 128);
-                        tc05::mma_i8(tmem + (uint32_t)(p * TN), ad, bd, idesc, (first && s == 0) ? 0u : 1u);
+                    for (int s = 0; s < kKB / 32; ++s) {
+                        const uint64_t ad = tc05::smem_desc(sX_u + sb * kXBytes + s * 256, 128, 512);
+                        const uint64_t bd = tc05::smem_desc(sS_u + sb * kSBytes + s * 4 * kKGroup + h * 256 / 16 * 128,
+                                                            kKGroup, 128);
+                        tc05::mma_i8(tmem + (uint32_t)(h * 256), ad, bd, idesc, (first && s == 0) ? 0u : 1u);
                     }
                 }
                 tc05::commit(&bars->s_empty[sb]);
@@ -308,156 +462,50 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
     } else if (warp >= kI8Conv0) {
         // ------------------------------------------------------------------ converters + epilogue
         const int ct = threadIdx.x - kI8Conv0 * 32;                // 0..255
-        const int cw = ct >> 5;                                     // converter warp 0..7
         constexpr int JB = TN / 16;                                 // 16-column blocks per row
         constexpr int ITEMS = kKB * JB / kI8ConvThreads;            // 2 (fp32) / 1 (fp64)
         const int jb = (ct >> 3) % JB;
         int base[16];
         int piece = 0;
-        const int VP = a.V;
-        UnitCursor cu(u_begin, kbs, tiles);
+        UnitCursor cc(u_begin, kbs, tiles);
         Ring<kAStages> ra;
-        Ring<2> rb;
-        for (int64_t u = u_begin; u < u_end; ++u, cu.next(kbs, tiles), ra.next(), rb.next()) {
-            const int64_t g = cu.g;
-            const int c = cu.c;
-            const int m = a.act[cu.ai];
-            const bool last = u + 1 == u_end || cu.kb + 1 == kbs;
-            if (u == u_begin || cu.kb == 0) {                       // new piece: column bases
-                const int4 *E = reinterpret_cast<const int4 *>(a.colexp + (size_t)m * N + (size_t)c * TN + jb * 16);
+        Ring<kSBuf> rb;
+        for (int64_t u = u_begin; u < u_end; ++u, cc.next(kbs, tiles), ra.next(), rb.next()) {
+            const int m = a.i8_dbg ? cc.ai : a.act[cc.ai];
+            const bool last = u + 1 == u_end || cc.kb + 1 == kbs;
+            if (u == u_begin || cc.kb == 0) {                       // new piece: column bases
+                const int4 *E = reinterpret_cast<const int4 *>(a.colexp + (size_t)m * N + (size_t)cc.c * TN + jb * 16);
+                constexpr int OFF = C::R + (sizeof(T) == 4 ? 23 : 0);   // fp32 funnel: s = e - E + R + 23
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int4 e4 = E[i];
-                    base[4 * i] = e4.x - C::R;
-                    base[4 * i + 1] = e4.y - C::R;
-                    base[4 * i + 2] = e4.z - C::R;
-                    base[4 * i + 3] = e4.w - C::R;
+                    base[4 * i] = e4.x - OFF;
+                    base[4 * i + 1] = e4.y - OFF;
+                    base[4 * i + 2] = e4.z - OFF;
+                    base[4 * i + 3] = e4.w - OFF;
                 }
             }
-            const int sa = ra.i, sb = rb.i;
-            mbar_wait(&bars->a_full[sa], ra.ph);
-            mbar_wait(&bars->s_empty[sb], rb.ph ^ 1);
-            const unsigned char *At = sA + sa * kABytes;
+            mbar_wait(&bars->a_full[ra.i], ra.ph);
+            mbar_wait(&bars->s_empty[rb.i], rb.ph ^ 1);
+            const unsigned char *At = sA + ra.i * kABytes;
 #pragma unroll
             for (int h = 0; h < ITEMS; ++h) {
+                if (a.i8_dbg & 1) break;
                 const int it = ct + kI8ConvThreads * h;
                 const int r = (it & 7) + 8 * (it / (8 * JB));
-                convert_item<T>(At, sS + sb * kSBytes, r, jb, base);
+                convert_item<T>(At, sS + rb.i * kSBytes, r, jb, base);
             }
             tc05::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&bars->a_empty[sa]);
-                mbar_arrive(&bars->s_full[sb]);
+                mbar_arrive(&bars->a_empty[ra.i]);
+                mbar_arrive(&bars->s_full[rb.i]);
             }
-            if (!last) continue;
-
-            // ---- epilogue of the piece (matrix m, tile c): TMEM -> fp64 partial sums ----------
-            if (ct == 0) {
-                int n = 0;
-                for (int v = 0; v < VP; ++v) {
-                    const SolveState s = a.st[(size_t)m * VP + v];
-                    if (!s.done) { s_vmap[n] = v; s_cur[n] = s.cur; ++n; }
-                    s_tau[v] = a.xtau[(size_t)m * VP + v];
-                }
-                s_nact = n;
+            if (last) {
+                const PieceCtx pc{m, cc.c, cc.g};
+                epilogue<T>(a, pc, tmem, sS, bars, piece, U, b, s_vmap, s_cur, s_tau, &s_nact, &s_last);
+                ++piece;
             }
-            mbar_wait(&bars->t_full, piece & 1);
-            tc05::fence_after();
-            named_sync(1, kI8ConvThreads);
-            const int quad = cw & 3, half = cw >> 2;
-            const int row = 32 * quad + lane;                       // TMEM lane = x-slice row (q, v)
-            const int q = row / VP;
-            const bool live = q < kXQ;
-            double *stage = reinterpret_cast<double *>(sS);         // [2 halves][32 cols][128 rows]
-            constexpr int CHUNKS = TN / 64;                         // 32-column chunks per warp
-            const int64_t gN = g * kbs;
-            double *part = a.part + (size_t)(b + g) * VP * TN;
-            for (int ch = 0; ch < CHUNKS; ++ch) {
-                const int col0 = half * (TN / 2) + ch * 32;
-                double acc[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) acc[i] = 0.0;
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    uint32_t r[32];
-                    tc05::ld32x32(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(p * TN + col0), r);
-                    tc05::wait_ld();
-                    const double w = ldexp(1.0, 8 * (NP - 1 - p) + 8 * (kXQ - 1 - (live ? q : 0)));
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) acc[i] = fma((double)(int)r[i], w, acc[i]);
-                }
-                double *st = stage + (size_t)half * 32 * 128;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) st[i * 128 + row] = live ? acc[i] : 0.0;
-                named_sync(2 + half, 128);
-                // y partial for (v, col0 + i): sum over q (fixed order, largest slice first)
-                const int t = ct & 127;
-                for (int o = t; o < s_nact * 32; o += 128) {
-                    const int sl = o >> 5, i = o & 31;
-                    const int v = s_vmap[sl];
-                    double ysum = 0.0;
-#pragma unroll
-                    for (int qq = 0; qq < kXQ; ++qq) ysum += st[i * 128 + qq * VP + v];
-                    const int j = c * TN + col0 + i;
-                    const int ex = a.colexp[(size_t)m * N + j] - C::BIAS_MBITS - C::R - s_tau[v];
-                    part[(size_t)v * TN + col0 + i] = ldexp(ysum, ex);
-                }
-                named_sync(2 + half, 128);
-            }
-            tc05::fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->t_empty);
-            ++piece;
-            // ---- last piece of the tile: add the pieces in fixed order, write y, tile sum / max --
-            __threadfence();
-            named_sync(1, kI8ConvThreads);
-            if (ct == 0) {
-                const int first_p = (int)(gN / U), last_p = (int)((gN + kbs - 1) / U);
-                const unsigned prev = atomicAdd(&a.strip_cnt[g], 1u);
-                s_last = prev == (unsigned)(last_p - first_p);
-            }
-            named_sync(1, kI8ConvThreads);
-            if (s_last) {
-                __threadfence();
-                const int first_p = (int)(gN / U), last_p = (int)((gN + kbs - 1) / U);
-                double *red = reinterpret_cast<double *>(sS);                  // [8 warps][2][32] (stage is free)
-                for (int sl = 0; sl < s_nact; ++sl) {
-                    const int v = s_vmap[sl];
-                    double ysum = 0.0, ymax = 0.0;
-                    if (ct < TN) {
-                        double yv = 0.0;
-                        for (int pc = first_p; pc <= last_p; ++pc)
-                            yv += __ldcg(a.part + ((size_t)(pc + g) * VP + v) * TN + ct);
-                        a.y[(((size_t)m * VP + v) * 2 + (1 - s_cur[sl])) * N + (size_t)c * TN + ct] = yv;
-                        ysum = yv;
-                        ymax = yv;
-                    }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
-                        ymax = fmax(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
-                    }
-                    if (lane == 0) {
-                        red[(cw * 2 + 0) * kMaxVectors + sl] = ysum;
-                        red[(cw * 2 + 1) * kMaxVectors + sl] = ymax;
-                    }
-                }
-                named_sync(1, kI8ConvThreads);
-                if (ct < s_nact) {
-                    double ssum = 0.0, smax = 0.0;
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) {
-                        ssum += red[(w * 2 + 0) * kMaxVectors + ct];
-                        smax = fmax(smax, red[(w * 2 + 1) * kMaxVectors + ct]);
-                    }
-                    const size_t mv = (size_t)m * VP + s_vmap[ct];
-                    a.ssum[mv * a.strips_i8 + c] = ssum;
-                    a.smax[mv * a.strips_i8 + c] = smax;
-                }
-                if (ct == 0) a.strip_cnt[g] = 0u;
-            }
-            named_sync(1, kI8ConvThreads);
         }
     }
     tc05::fence_before();
@@ -468,66 +516,85 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
     }
 }
 
-// Column exponents E_j (largest biased exponent of column j) and the range test, one CTA per
-// 32 columns of one matrix; flag glob[3] is cleared if some non-zero entry lies more than 2^R
-// below its column maximum, or is subnormal.
+// Column exponents E_j (largest biased exponent of column j) and the range test, in three steps:
+// k_i8_prep (flag = 1, E_j = 0, e_min_j = INT_MAX), k_i8_colexp (a CTA per 128 columns x a chunk of
+// rows: one warp reads 512 B / 1 KB of a row, every lane 4 consecutive columns; atomicMax / atomicMin
+// per column), k_i8_colcheck (per column: the range test clears glob[3] when some non-zero entry
+// lies more than 2^R below its column maximum, or the maximum itself is <= R; all-zero columns get
+// E_j = the largest exponent so that every shift is negative). Subnormal or negative entries clear
+// the flag in k_i8_colexp.
 template <typename T>
-__global__ void __launch_bounds__(256) k_i8_colexp(const PowerArgs a) {
-    using C = I8Cfg<T>;
-    const int N = a.N, m = blockIdx.y;
-    const int j0 = blockIdx.x * 32;
-    const int tid = threadIdx.x;
-    constexpr int PER = 16 / sizeof(T);              // entries per 16-byte load
-    constexpr int LANES = 32 / PER;                  // threads per row segment of 32 columns
-    const int jl = (tid % LANES) * PER, rl = tid / LANES, RSTEP = 256 / LANES;
-    int emax[PER], emin[PER];
-#pragma unroll
-    for (int i = 0; i < PER; ++i) { emax[i] = 0; emin[i] = 1 << 20; }
-    const T *P = reinterpret_cast<const T *>(a.P) + (size_t)m * a.mstride + j0 + jl;
-    bool sub = false;
+__global__ void __launch_bounds__(256) k_i8_colexp(const PowerArgs a, int rows_per_cta) {
+    const int N = a.N, m = blockIdx.z;
+    const int j0 = blockIdx.x * 128 + (threadIdx.x & 31) * 4;
+    const int r0 = blockIdx.y * rows_per_cta, r1 = min(N, r0 + rows_per_cta);
+    const int w = threadIdx.x >> 5;
+    int emax[4] = {0, 0, 0, 0}, emin[4] = {1 << 20, 1 << 20, 1 << 20, 1 << 20};
+    bool bad = false;
+    const T *P = reinterpret_cast<const T *>(a.P) + (size_t)m * a.mstride + j0;
 #pragma unroll 4
-    for (int r = rl; r < N; r += RSTEP) {
-        const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(P + (size_t)r * a.ld));
+    for (int r = r0 + w; r < r1; r += 8) {
         if constexpr (sizeof(T) == 4) {
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(P + (size_t)r * a.ld));
+            const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int e = (int)((w[i] >> 23) & 0xFF);
-                sub |= (e == 0 && (w[i] & 0x7FFFFFu)) || (w[i] >> 31);      // subnormal or negative
-                if (w[i] & 0x7FFFFFFFu) { emax[i] = max(emax[i], e); emin[i] = min(emin[i], e); }
+                const int e = (int)((x[i] >> 23) & 0xFF);
+                bad |= (e == 0 && (x[i] & 0x7FFFFFu)) || (x[i] >> 31);      // subnormal or negative
+                if (x[i] & 0x7FFFFFFFu) { emax[i] = max(emax[i], e); emin[i] = min(emin[i], e); }
             }
         } else {
-            const uint64_t w[2] = {((uint64_t)v.y << 32) | v.x, ((uint64_t)v.w << 32) | v.z};
+            const uint4 v0 = __ldcs(reinterpret_cast<const uint4 *>(P + (size_t)r * a.ld));
+            const uint4 v1 = __ldcs(reinterpret_cast<const uint4 *>(P + (size_t)r * a.ld + 2));
+            const uint64_t x[4] = {((uint64_t)v0.y << 32) | v0.x, ((uint64_t)v0.w << 32) | v0.z,
+                                   ((uint64_t)v1.y << 32) | v1.x, ((uint64_t)v1.w << 32) | v1.z};
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int e = (int)((w[i] >> 52) & 0x7FF);
-                sub |= (e == 0 && (w[i] & 0xFFFFFFFFFFFFFull)) || (w[i] >> 63);   // subnormal or negative
-                if (w[i] & 0x7FFFFFFFFFFFFFFFull) { emax[i] = max(emax[i], e); emin[i] = min(emin[i], e); }
+            for (int i = 0; i < 4; ++i) {
+                const int e = (int)((x[i] >> 52) & 0x7FF);
+                bad |= (e == 0 && (x[i] & 0xFFFFFFFFFFFFFull)) || (x[i] >> 63);
+                if (x[i] & 0x7FFFFFFFFFFFFFFFull) { emax[i] = max(emax[i], e); emin[i] = min(emin[i], e); }
             }
         }
     }
-    __shared__ int s_max[256][PER], s_min[256][PER];
-    __shared__ int s_bad;
-    if (tid == 0) s_bad = 0;
+    __shared__ int s_max[8][128], s_min[8][128];
 #pragma unroll
-    for (int i = 0; i < PER; ++i) { s_max[tid][i] = emax[i]; s_min[tid][i] = emin[i]; }
-    __syncthreads();
-    if (sub) s_bad = 1;
-    if (tid < 32) {
-        const int l = tid / PER, i = tid % PER;       // column j0 + tid = lane l's entry i
-        int mx = 0, mn = 1 << 20;
-        for (int t = l; t < 256; t += LANES) { mx = max(mx, s_max[t][i]); mn = min(mn, s_min[t][i]); }
-        // all-zero column: E_j = the largest exponent, so that every shift is negative (zero out);
-        // a column whose largest exponent is <= R (entries ~ the subnormal range) fails the test
-        const bool any = mn < (1 << 20);
-        a.colexp[(size_t)m * N + j0 + tid] = any ? mx : (sizeof(T) == 4 ? 255 : 2047);
-        if (any && (mx - mn > C::R || mx <= C::R)) s_bad = 1;
+    for (int i = 0; i < 4; ++i) {
+        s_max[w][(threadIdx.x & 31) * 4 + i] = emax[i];
+        s_min[w][(threadIdx.x & 31) * 4 + i] = emin[i];
     }
-    __syncthreads();
-    if (tid == 0 && s_bad) atomicAnd(&a.glob[3], 0u);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAnd(&a.glob[3], 0u);
+    if (threadIdx.x < 128) {
+        int mx = 0, mn = 1 << 20;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { mx = max(mx, s_max[k][threadIdx.x]); mn = min(mn, s_min[k][threadIdx.x]); }
+        const size_t j = (size_t)m * N + blockIdx.x * 128 + threadIdx.x;
+        if (mx > 0) atomicMax(&a.colexp[j], mx);
+        if (mn < (1 << 20)) atomicMin(&a.colmin[j], mn);
+    }
 }
 
-__global__ void k_i8_flag_set(const PowerArgs a) { a.glob[3] = 1u; }
+template <typename T>
+__global__ void k_i8_colcheck(const PowerArgs a) {
+    using C = I8Cfg<T>;
+    const size_t n = (size_t)a.M * a.N;
+    bool bad = false;
+    for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (size_t)gridDim.x * blockDim.x) {
+        const int mx = a.colexp[j], mn = a.colmin[j];
+        if (mn == INT_MAX) a.colexp[j] = sizeof(T) == 4 ? 255 : 2047;   // all-zero column
+        else bad |= mx - mn > C::R || mx <= C::R;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAnd(&a.glob[3], 0u);
+}
+
+__global__ void k_i8_prep(const PowerArgs a) {
+    const size_t n = (size_t)a.M * a.N;
+    for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (size_t)gridDim.x * blockDim.x) {
+        a.colexp[j] = 0;
+        a.colmin[j] = INT_MAX;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.glob[3] = 1u;
+}
+
 
 }  // namespace
 
@@ -567,13 +634,20 @@ cudaError_t i8_kernels(int dtype, I8Kernels *k, const PowerArgs &a) {
     if (e != cudaSuccess) return e;
     k->step_fn = f64 ? (void *)k_power_step_i8<double> : (void *)k_power_step_i8<float>;
     k->colexp_fn = f64 ? (void *)k_i8_colexp<double> : (void *)k_i8_colexp<float>;
-    k->flag_fn = (void *)k_i8_flag_set;
+    k->check_fn = f64 ? (void *)k_i8_colcheck<double> : (void *)k_i8_colcheck<float>;
+    k->prep_fn = (void *)k_i8_prep;
     k->step_smem = kI8Smem;
     k->step_block = dim3(kI8Threads);
     const int sms = device_sm_count() < kMaxSMs ? device_sm_count() : kMaxSMs;
     k->step_grid = dim3(sms);
-    k->colexp_grid = dim3(a.N / 32, a.M);
+    // colexp: column tiles x row chunks, about 8 CTAs per SM in all
+    const int ct = a.N / 128;
+    int rc = (8 * sms + ct * a.M - 1) / (ct * a.M);
+    rc = rc < 1 ? 1 : (rc > a.N / 8 ? a.N / 8 : rc);
+    k->rows_per_cta = (a.N + rc - 1) / rc;
+    k->colexp_grid = dim3(ct, rc, a.M);
     k->colexp_block = dim3(256);
+    k->small_grid = dim3(2 * sms);
     return func_attrs_once(k->step_fn, (int)kI8Smem, false);
 }
 
