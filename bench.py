@@ -33,6 +33,8 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "stationary solves/s (with transition-matrix entries/s; % of HBM roofline)"
+GEMV_KERNELS = {"tensor_i8": "k_power_step_i8 (tcgen05 kind::i8 exact split, TMEM accumulators)",
+                "fp64": "k_power_step (FP64 tensor cores / DFMA)", "fused": "k_power_fused (cluster, small N)"}
 UNIT = "solves/s"
 
 
@@ -255,6 +257,7 @@ def run_ours(args, rank, world, dev):
         t_build = sum(a.elapsed_time(b) for a, b, _ in ev) / 1e3
         t_solve = sum(b.elapsed_time(c) for _, b, c in ev) / 1e3
     infos = st.infos()
+    gemv_kinds = sorted({p.gemv() for p in st.plans})
     from paper_2509_20500_b200.shard import max_over_ranks
     t_total, t_build, t_solve = max_over_ranks([t_total, t_build, t_solve], device="cuda")
 
@@ -273,8 +276,12 @@ def run_ours(args, rank, world, dev):
     if graphed:
         per_step_launches = prelude + len(st.plans)
     else:
-        per_step_launches = prelude + sum(2 + 2 * int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
-                                          for pi, p in zip(infos, st.plans))
+        # graph plans: init + finish, and per iteration GEMV + check; int8 plans add the range test
+        # (prep, column exponents, column check) and per iteration the FP64 GEMV's early exit
+        def plan_launches(pi, p):
+            it = int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
+            return 2 + 2 * it if p.gemv() != "tensor_i8" else 5 + 3 * it
+        per_step_launches = prelude + sum(plan_launches(pi, p) for pi, p in zip(infos, st.plans))
     hbm, hbm_src = load_peaks()
     traffic = load_traffic(args.workload, args.dtype)
     K = args.steps
@@ -299,6 +306,7 @@ def run_ours(args, rank, world, dev):
                                    if world > 1 else "single GPU"),
                    "solver": "fused (one clustered launch per plan, N <= 2048)" if all(p.fused for p in st.plans)
                    else "graph (GEMV + check in a conditional WHILE node)",
+                   "gemv": gemv_kinds,
                    "step_as_cuda_graph": bool(graphed)},
         "entries_per_s": st.entries * K * world / t_build,
         "solves_per_s_solve_only": st.n_solves * K * world / t_solve,
@@ -307,7 +315,8 @@ def run_ours(args, rank, world, dev):
                           "same_gpu_ratio": "bench.py --path eq4 (Theorem 2 vs element-wise Eq. 4 on this B200)"},
         "ms_build_per_step": t_build / K * 1e3, "ms_solve_per_step": t_solve / K * 1e3,
         "iterations": [[i["iters"] for i in pi] for pi in infos],
-        "roofline": {"bound": "hbm", "kernel": "k_power_step (power-iteration GEMV)", "achieved": gemv_gbs,
+        "roofline": {"bound": "hbm", "kernel": GEMV_KERNELS.get(gemv_kinds[0], gemv_kinds[0]) + " (power-iteration GEMV)"
+                     if len(gemv_kinds) == 1 else "+".join(gemv_kinds), "achieved": gemv_gbs,
                      "peak": hbm, "unit": "GB/s", "frac": gemv_gbs / hbm,
                      "traffic": traffic.get("k_power_step") if traffic else None,
                      "algorithmic_bytes_per_launch": N * N * b,

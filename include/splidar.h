@@ -188,6 +188,21 @@ void splidar_plan_destroy(splidar_plan plan);
 #define SPLIDAR_PLAN_GRAPH 0
 #define SPLIDAR_PLAN_FUSED 1
 int splidar_plan_kind(splidar_plan plan);
+/* Which GEMV kernel ran the plan's last launch (synchronises the stream once):
+ *   SPLIDAR_GEMV_TENSOR_I8 (2): the exact int8 split on the 5th-generation tensor cores
+ *     (tcgen05.mma kind::i8, TMEM accumulators): P~0 in u8 planes with one exponent per column,
+ *     x in 7 u8 slices (truncation < 2^-56 of the largest x); used for fp32 storage when the plan
+ *     has 8..18 dead times per matrix, N % 128 == 0 and N >= 1024 (fp64 storage only with
+ *     SPLIDAR_I8=2 in the environment at plan creation), and only if every column of every matrix
+ *     passes the range test of each launch (every non-zero entry within 2^8 (fp32) / 2^11 (fp64) of
+ *     its column's largest, no subnormal or negative entry) -- else the FP64 kernel runs;
+ *   SPLIDAR_GEMV_FP64 (1): FP64 tensor cores (DMMA) / DFMA (k_power_step);
+ *   SPLIDAR_GEMV_FUSED (0): the fused small-N solver (SPLIDAR_PLAN_FUSED);
+ *   -1: NULL plan or CUDA error. SPLIDAR_I8=0 at plan creation disables the int8 kernel. */
+#define SPLIDAR_GEMV_FUSED 0
+#define SPLIDAR_GEMV_FP64 1
+#define SPLIDAR_GEMV_TENSOR_I8 2
+int splidar_plan_gemv(splidar_plan plan, void *stream);
 
 /* ---------------------------------------------------------------------------------------------
  * Matrix-free (structured) operator: SURVEY §8(f) rows f2 and f1.

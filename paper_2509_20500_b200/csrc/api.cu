@@ -379,7 +379,8 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     a.i8 = 0;
     {   // the int8 tensor-core GEMV (SPLIDAR_I8=0 keeps the DMMA / DFMA kernels only)
         const char *e = getenv("SPLIDAR_I8");
-        if (!(e && e[0] == '0') && i8_supported(dt, a)) {
+        const bool allow = !(e && e[0] == '0') && (dt == SPLIDAR_F32 || (e && e[0] == '2'));
+        if (allow && i8_supported(dt, a)) {
             a.i8 = 1;
             const char *d = getenv("SPLIDAR_I8_DBG");
             a.i8_dbg = d ? atoi(d) : 0;
@@ -605,6 +606,20 @@ static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
 }
 
 int splidar_plan_kind(splidar_plan plan) { return !plan ? -1 : plan->fused ? SPLIDAR_PLAN_FUSED : SPLIDAR_PLAN_GRAPH; }
+
+int splidar_plan_gemv(splidar_plan plan, void *stream) {
+    if (!plan) return -1;
+    if (plan->fused) return SPLIDAR_GEMV_FUSED;
+    if (!plan->args.i8) return SPLIDAR_GEMV_FP64;
+    unsigned flag = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(&flag, plan->args.glob + 3, sizeof(unsigned), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        g_last_cuda_error = (int)cudaGetLastError();
+        return -1;
+    }
+    return flag ? SPLIDAR_GEMV_TENSOR_I8 : SPLIDAR_GEMV_FP64;
+}
 
 splidar_status splidar_plan_launch(splidar_plan plan, void *stream) {
     if (!plan) return SPLIDAR_EINVAL;

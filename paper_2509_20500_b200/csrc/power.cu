@@ -605,7 +605,7 @@ __global__ void k_power_init(const PowerArgs a) {
         a.mv_cnt[mv] = 0u;
     }
     if (mv == 0) {
-        const int ncnt = a.M * a.strips;
+        const int ncnt = a.M * (a.i8 && a.strips_i8 > a.strips ? a.strips_i8 : a.strips);   // int8 GEMV: column tiles
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ncnt; i += gridDim.x * blockDim.x)
             a.strip_cnt[i] = 0u;
         if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -94,6 +94,7 @@ def _lib():
             "splidar_plan_info": (st, [p, pinfo, p]),
             "splidar_plan_destroy": (None, [p]),
             "splidar_plan_kind": (C.c_int, [p]),
+            "splidar_plan_gemv": (C.c_int, [p, p]),
             "splidar_structured_workspace_bytes": (sz, [i32, i32, i32]),
             "splidar_stationary_structured": (st, [fp, i32, p, p, p, d, i32, p, p, sz, pinfo, p]),
             "splidar_second_eigenvalue": (st, [fp, i32, p, p, p, p, d, i32, p, sz, C.POINTER(SpectralInfo), p]),
@@ -372,6 +373,16 @@ class Plan:
     def fused(self) -> bool:
         """True when the plan is one clustered launch (N <= 2048), capturable into a CUDA graph."""
         return _lib().splidar_plan_kind(self._h) == 1
+
+    GEMV_NAMES = {0: "fused", 1: "fp64", 2: "tensor_i8"}
+
+    def gemv(self, stream=None) -> str:
+        """The GEMV kernel of the last launch: 'tensor_i8' (tcgen05 int8 split), 'fp64' (DMMA / DFMA)
+        or 'fused' (small-N single launch). Synchronises the stream."""
+        k = _lib().splidar_plan_gemv(self._h, _stream(stream))
+        if k < 0:
+            raise SplidarError(ECUDA, "splidar_plan_gemv")
+        return self.GEMV_NAMES[k]
 
     def info(self, stream=None, check: bool = True) -> list:
         infos = (SolveInfo * (self.M * self.V))()

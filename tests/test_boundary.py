@@ -332,3 +332,4 @@ def test_build_eq4_rejects(spl):
 
 def test_plan_kind_null(spl):
     assert spl._lib().splidar_plan_kind(None) == -1
+    assert spl._lib().splidar_plan_gemv(None, None) == -1
