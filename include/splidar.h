@@ -205,6 +205,35 @@ int splidar_plan_kind(splidar_plan plan);
 int splidar_plan_gemv(splidar_plan plan, void *stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * Row shards of one matrix over several GPUs: the power iteration of P:79 with
+ * P~ = J_l P~0 (Thm 2) split by rows. Rank g stores rows [row0, row0 + n_rows) of P~0
+ * (n_rows x ld, row-major, built by splidar_build_base_rows: the same entries as rows row0.. of
+ * splidar_build_base) and computes the partial product y_g^T = x^T P~0[rows, :], x_r = pi[(r - l) mod N]
+ * gathered from the replicated iterate; the caller sums the partials over the ranks (one all-reduce of
+ * N x n_vectors doubles per iteration, e.g. NCCL over NVLink) and every rank then runs the identical
+ * normalisation / L1-change / next-gather step, so the iterate stays replicated and the dead-time
+ * offset is applied after the collective. One iteration:
+ *     splidar_plan_shard_gemv(plan)            -> ypart [n_vectors][N] fp64 holds this rank's partial
+ *     all-reduce(ypart, SUM)                   (caller, same stream order)
+ *     splidar_plan_shard_check(plan, &more)    -> more = 0 when every vector converged / stopped
+ * preceded once by splidar_plan_shard_init and followed by splidar_plan_shard_finish (writes pi
+ * [n_vectors][N] and info, synchronises). ypart: device fp64 [n_vectors * N], 16-byte aligned, owned
+ * by the caller. ws: splidar_workspace_bytes(N, 1, n_vectors). The FP64 GEMV (DMMA / DFMA) runs the
+ * shard. EINVAL for a row range outside [0, N) or a NULL ypart; other errors as splidar_plan_create. */
+splidar_status splidar_build_base_rows(const splidar_flux *f, splidar_dtype dt, splidar_entry mode,
+                                       void *P0_rows, int64_t ld, int32_t row0, int32_t n_rows, void *ws,
+                                       size_t ws_bytes, void *stream);
+splidar_status splidar_plan_create_rows(splidar_plan *plan, const void *P0_rows, int32_t row0,
+                                        int32_t n_rows, int32_t n_bins, int64_t ld, splidar_dtype dt,
+                                        double t_r, const double *t_d, int32_t n_vectors, double tol,
+                                        int32_t max_iter, double *pi, double *ypart, void *ws,
+                                        size_t ws_bytes, void *stream);
+splidar_status splidar_plan_shard_init(splidar_plan plan, void *stream);
+splidar_status splidar_plan_shard_gemv(splidar_plan plan, void *stream);
+splidar_status splidar_plan_shard_check(splidar_plan plan, int32_t *more, void *stream);
+splidar_status splidar_plan_shard_finish(splidar_plan plan, splidar_solve_info *info, void *stream);
+
+/* ---------------------------------------------------------------------------------------------
  * Matrix-free (structured) operator: SURVEY §8(f) rows f2 and f1.
  *
  * From §3.4 (E_base = exp.(-Lambda L - D); P = (1 lambda^T) . E; row

@@ -12,5 +12,5 @@ from .splidar import (  # noqa: F401
     lib_path, shift, solve_host, stationary, sweep, workspace, workspace_bytes,
     SpectralInfo, bin_trajectory, flux_items, mixing_steps, second_eigenvalue, second_eigenvalue_dense,
     stationary_structured,
-    structured_workspace, StructPlan, build_eq4, monte_carlo, lambda2_of,
+    structured_workspace, StructPlan, build_eq4, monte_carlo, lambda2_of, build_base_rows, ShardPlan,
 )

@@ -349,6 +349,7 @@ struct splidar_plan_s {
     int dt = 0;
     FusedArgs fargs;
     I8Kernels q;       // int8 tensor-core GEMV (args.i8)
+    bool shard = false;   // row shard (splidar_plan_create_rows): stepped by the caller
 };
 
 static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws, cudaStream_t s) {
@@ -366,6 +367,7 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     a.act = reinterpret_cast<int *>(ws + L.act);
     a.glob = reinterpret_cast<unsigned *>(ws + L.glob);
     a.N = L.N;
+    if (a.rows == 0) a.rows = L.N;      // a row shard sets rows / row0 / ypart before plan_build
     a.M = L.M;
     a.V = L.V;
     a.strips = L.strips;
@@ -377,7 +379,7 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     a.smax = reinterpret_cast<double *>(ws + L.smax);
     a.xtau = reinterpret_cast<int *>(ws + L.xtau);
     a.i8 = 0;
-    {   // the int8 tensor-core GEMV (SPLIDAR_I8=0 keeps the DMMA / DFMA kernels only)
+    if (!p->shard) {   // the int8 tensor-core GEMV (SPLIDAR_I8=0 keeps the DMMA / DFMA kernels only)
         const char *e = getenv("SPLIDAR_I8");
         const bool allow = !(e && e[0] == '0') && (dt == SPLIDAR_F32 || (e && e[0] == '2'));
         if (allow && i8_supported(dt, a)) {
@@ -394,7 +396,7 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     {   // small N: the fused single-launch solver (SPLIDAR_FUSED=0 forces the general path)
         const char *e = getenv("SPLIDAR_FUSED");
         int C, R;
-        if (!(e && e[0] == '0') && !fused_shape(L.N, &C, &R)) {
+        if (!p->shard && !(e && e[0] == '0') && !fused_shape(L.N, &C, &R)) {
             p->fused = true;
             p->dt = dt;
             FusedArgs &f = p->fargs;
@@ -418,6 +420,14 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
         }
     }
 
+    if (p->shard) {   // row shard: the caller steps the kernels around its all-reduce (no graph)
+        if (solver_kernels(dt, L.V, &p->k, a)) return SPLIDAR_EINVAL;
+        p->eager_args = a;
+        p->eager_args.use_handle = 0;
+        p->fin_args.resize(finish_args_size());
+        make_finish_args(p->fin_args.data(), p->eager_args, pi, reinterpret_cast<const int *>(ws + L.oidx));
+        return SPLIDAR_OK;
+    }
     SPL_CUDA(cudaGraphCreate(&p->graph, 0));
     cudaGraphConditionalHandle h;
     SPL_CUDA(cudaGraphConditionalHandleCreate(&h, p->graph, 1, cudaGraphCondAssignDefault));
@@ -527,7 +537,8 @@ void splidar_plan_destroy(splidar_plan plan) {
 // Internal: plan with explicit shifts (l < 0 = unused vector) and output rows.
 static splidar_status plan_create_l(splidar_plan *out, const void *P0, int M, int64_t mstride, int N, int64_t ld,
                                     int dt, const int *l, int V, double tol, int max_iter, double *pi,
-                                    const int *out_idx, void *ws, size_t ws_bytes, cudaStream_t s) {
+                                    const int *out_idx, void *ws, size_t ws_bytes, cudaStream_t s,
+                                    int row0 = 0, int n_rows = -1, double *ypart = nullptr) {
     *out = nullptr;
     splidar_status st;
     if ((st = check_matrix(P0, N, ld, dt))) return st;
@@ -554,6 +565,12 @@ static splidar_status plan_create_l(splidar_plan *out, const void *P0, int M, in
     p->args.mstride = mstride;
     p->args.tol = tol;
     p->args.max_iter = max_iter;
+    if (n_rows >= 0) {
+        p->shard = true;
+        p->args.rows = n_rows;
+        p->args.row0 = row0;
+        p->args.ypart = ypart;
+    }
     if ((st = plan_build(p, dt, pi, static_cast<char *>(ws), s))) {
         splidar_plan_destroy(p);
         return st;
@@ -670,6 +687,84 @@ splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, sp
     return st;
 }
 
+// ------------------------------------------------ row shards ---------------
+
+splidar_status splidar_build_base_rows(const splidar_flux *flux, splidar_dtype dt, splidar_entry mode, void *P0_rows,
+                                       int64_t ld, int32_t row0, int32_t n_rows, void *ws, size_t ws_bytes,
+                                       void *stream) {
+    splidar_status st = check_flux(flux);
+    if (st) return st;
+    if (mode != SPLIDAR_ENTRY_FACTORED && mode != SPLIDAR_ENTRY_EXP) return SPLIDAR_EINVAL;
+    const int N = flux->n_bins;
+    if (row0 < 0 || n_rows < 1 || row0 + n_rows > N) return SPLIDAR_EINVAL;
+    if ((st = check_matrix(P0_rows, N, ld, dt))) return st;
+    const WsLayout L = ws_layout(N, 1, 1);
+    if ((st = check_ws(ws, ws_bytes, L))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *wsb = static_cast<char *>(ws);
+    FluxDev d = to_dev(flux);
+    SPL_CUDA(upload_async(wsb + L.flux, &d, sizeof(FluxDev), s));
+    VecPtrs vp = vec_ptrs(wsb, L);
+    SPL_CUDA(launch_flux_vectors(reinterpret_cast<const FluxDev *>(wsb + L.flux), 1, N, vp, N, s));
+    SPL_CUDA(launch_build(vp, N, 1, N, dt, mode, P0_rows, ld, (int64_t)n_rows * ld, s, row0, n_rows));
+    return SPLIDAR_OK;
+}
+
+splidar_status splidar_plan_create_rows(splidar_plan *plan, const void *P0_rows, int32_t row0, int32_t n_rows,
+                                        int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r, const double *t_d,
+                                        int32_t n_vectors, double tol, int32_t max_iter, double *pi, double *ypart,
+                                        void *ws, size_t ws_bytes, void *stream) {
+    if (!plan || !t_d || !ypart || n_vectors < 1 || n_vectors > kMaxVectors) return SPLIDAR_EINVAL;
+    if (row0 < 0 || n_rows < 1 || n_bins < 2 || row0 + n_rows > n_bins) return SPLIDAR_EINVAL;
+    if (((uintptr_t)ypart & 15u) != 0) return SPLIDAR_ENOSPACE;
+    std::vector<int> l((size_t)n_vectors);
+    for (int v = 0; v < n_vectors; ++v) {
+        int32_t li;
+        splidar_status st = splidar_shift(t_r, n_bins, t_d[v], &li);
+        if (st) return st;
+        l[(size_t)v] = li;
+    }
+    return plan_create_l(plan, P0_rows, 1, (int64_t)n_rows * ld, n_bins, ld, dt, l.data(), n_vectors, tol, max_iter,
+                         pi, nullptr, ws, ws_bytes, (cudaStream_t)stream, row0, n_rows, ypart);
+}
+
+splidar_status splidar_plan_shard_init(splidar_plan p, void *stream) {
+    if (!p || !p->shard) return SPLIDAR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    void *args[] = {&p->eager_args};
+    SPL_CUDA(cudaLaunchKernel(p->k.init_fn, p->k.init_grid, p->k.init_block, args, 0, s));
+    return SPLIDAR_OK;
+}
+
+splidar_status splidar_plan_shard_gemv(splidar_plan p, void *stream) {
+    if (!p || !p->shard) return SPLIDAR_EINVAL;
+    void *args[] = {&p->eager_args};
+    SPL_CUDA(cudaLaunchKernel(p->k.step_fn, p->k.step_grid, p->k.step_block, args, p->k.step_smem,
+                              (cudaStream_t)stream));
+    return SPLIDAR_OK;
+}
+
+splidar_status splidar_plan_shard_check(splidar_plan p, int32_t *more, void *stream) {
+    if (!p || !p->shard || !more) return SPLIDAR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    void *args[] = {&p->eager_args};
+    const dim3 sgrid((unsigned)p->L.strips, (unsigned)(p->M * p->V));
+    SPL_CUDA(cudaLaunchKernel(p->k.ssum_fn, sgrid, dim3(256), args, 0, s));
+    SPL_CUDA(cudaLaunchKernel(p->k.check_fn, p->k.check_grid, p->k.check_block, args, 0, s));
+    if (!p->host_flag) SPL_CUDA(cudaMallocHost(&p->host_flag, sizeof(unsigned)));
+    SPL_CUDA(cudaMemcpyAsync(p->host_flag, p->eager_args.glob + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    SPL_CUDA(cudaStreamSynchronize(s));
+    *more = *p->host_flag ? 1 : 0;
+    return SPLIDAR_OK;
+}
+
+splidar_status splidar_plan_shard_finish(splidar_plan p, splidar_solve_info *info, void *stream) {
+    if (!p || !p->shard) return SPLIDAR_EINVAL;
+    void *fargs[] = {p->fin_args.data()};
+    SPL_CUDA(cudaLaunchKernel(p->k.finish_fn, p->k.finish_grid, p->k.finish_block, fargs, 0, (cudaStream_t)stream));
+    return splidar_plan_info(p, info, stream);
+}
+
 // ------------------------------------------------ f1 on a stored matrix (spectral_dense.cu) ---
 
 static size_t sd_extra(int N, size_t *o_part, size_t *o_qsum, size_t *o_state, size_t *o_cnt) {
@@ -712,6 +807,7 @@ splidar_status splidar_second_eigenvalue_dense(const void *P0, int32_t n_bins, i
     p.ld = ld;
     p.mstride = (int64_t)N * ld;
     p.N = N;
+    p.rows = N;
     p.M = 1;
     p.V = L.V;
     p.strips = L.strips;

@@ -22,7 +22,8 @@ template <> struct Vec16<float> { using type = float4; static constexpr int n = 
 
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kStripCols / Vec16<T>::n)
-k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t ld, int64_t mstride) {
+k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t ld, int64_t mstride, int row0,
+        int nrows) {
     constexpr int VEC = Vec16<T>::n;
     using V = typename Vec16<T>::type;
     const int m = blockIdx.z;
@@ -37,8 +38,9 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
 
     const int j0 = blockIdx.x * kStripCols + threadIdx.x * VEC;
     if (j0 >= N) return;
-    const int r0 = blockIdx.y * kRowsPerCta;
-    const int r1 = min(N, r0 + kRowsPerCta);
+    // rows [row0, row0 + nrows) of P~0 (a row shard); stored from row 0 of P0
+    const int r0 = row0 + blockIdx.y * kRowsPerCta;
+    const int r1 = min(row0 + nrows, r0 + kRowsPerCta);
     const bool full = j0 + VEC <= N;
 
     // column operands in registers
@@ -79,7 +81,7 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
                 }
             }
         }
-        T *row = out + (int64_t)r * ld + j0;
+        T *row = out + (int64_t)(r - row0) * ld + j0;
         if (full) {
             V v;
             if constexpr (VEC == 2) { v.x = val[0]; v.y = val[1]; }
@@ -107,20 +109,21 @@ __global__ void __launch_bounds__(256) k_apply_deadtime(const uint4 *__restrict_
 }  // namespace
 
 cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
-                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s) {
-    dim3 grid((N + kStripCols - 1) / kStripCols, (N + kRowsPerCta - 1) / kRowsPerCta, M);
+                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0, int nrows) {
+    if (nrows < 0) nrows = N;
+    dim3 grid((N + kStripCols - 1) / kStripCols, (nrows + kRowsPerCta - 1) / kRowsPerCta, M);
     if (dtype == SPLIDAR_F64) {
         dim3 block(kStripCols / 2);
         if (mode == SPLIDAR_ENTRY_EXP)
-            k_build<double, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride);
+            k_build<double, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows);
         else
-            k_build<double, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride);
+            k_build<double, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows);
     } else {
         dim3 block(kStripCols / 4);
         if (mode == SPLIDAR_ENTRY_EXP)
-            k_build<float, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride);
+            k_build<float, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows);
         else
-            k_build<float, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride);
+            k_build<float, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows);
     }
     return cudaGetLastError();
 }

@@ -76,7 +76,7 @@ cudaError_t func_attrs_once(const void *fn, int max_dyn_smem, bool nonportable_c
 cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs base, int64_t vstride,
                                 cudaStream_t s);
 cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
-                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s);
+                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0 = 0, int nrows = -1);
 cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, int dtype, int l,
                                   cudaStream_t s);
 cudaError_t launch_build_eq4(const FluxDev &f, double u, int dtype, void *P, int64_t ld, cudaStream_t s);
@@ -110,6 +110,10 @@ struct PowerArgs {
     double *smax;            // [M][V][N / 64]        tile maxima of y
     int *xtau;               // [M][V]                x scale exponents tau_v
     int i8_dbg;              // timing experiments only (SPLIDAR_I8_DBG): 1 skip conversion, 2 skip MMA
+    // row shard: the stored block holds rows [row0, row0 + rows) of P~0; the GEMV
+    // writes its partial y^T = x_g^T P~0[rows, :] to ypart [M][V][N] for the caller's all-reduce
+    int rows, row0;
+    double *ypart;
 };
 
 // Kernel node parameters for the three solver kernels (for graph construction).
@@ -118,6 +122,7 @@ struct SolverKernels {
     void *step_fn;
     void *check_fn;
     void *finish_fn;
+    void *ssum_fn;           // row shard: strip sums of the all-reduced y
     dim3 init_grid, init_block;
     dim3 step_grid, step_block;
     dim3 check_grid, check_block;

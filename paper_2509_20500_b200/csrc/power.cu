@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
     const int N = a.N, S = a.strips;
     if (a.i8 && a.glob[3]) return;                  // the int8 tensor-core GEMV runs this plan
     const int n_act = (int)a.glob[2];
-    const int64_t T_units = (int64_t)n_act * S * N;
+    const int R = a.rows;                           // rows of the stored block (N, or a row shard)
+    const int64_t T_units = (int64_t)n_act * S * R;
     if (T_units == 0) return;
     int64_t U = (T_units + G - 1) / G;
     if (U < kMinRowsPerCta) U = kMinRowsPerCta;
@@ -242,14 +243,14 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
     uint32_t q_issue = 0, q_cons = 0;   // stage sequence numbers (buffer q % S, parity (q / S) & 1)
     int64_t u = u_begin;
     while (u < u_end) {
-        const int64_t g64 = u / N;                       // strip index in active order
+        const int64_t g64 = u / R;                       // strip index in active order
         const int g = (int)g64;
         const int ai = g / S, c = g % S;
         const int m = a.act[ai];
-        const int r_lo = (int)(u - g64 * N);
-        const int64_t strip_end = (g64 + 1) * N;
-        const int r_hi = (int)((u_end < strip_end ? u_end : strip_end) - g64 * N);
-        u = g64 * N + r_hi;
+        const int r_lo = (int)(u - g64 * R);
+        const int64_t strip_end = (g64 + 1) * R;
+        const int r_hi = (int)((u_end < strip_end ? u_end : strip_end) - g64 * R);
+        u = g64 * R + r_hi;
 
         // running vectors of matrix m, compacted into slots (slot s = the s-th running vector)
         if (tid == 0) {
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
         const int cols = min(kStripCols, N - c * kStripCols);
         const uint32_t seg_bytes = (uint32_t)(((size_t)cols * sizeof(T) + 15) & ~(size_t)15);
         const T *pbase = reinterpret_cast<const T *>(a.P) + (size_t)m * a.mstride + (size_t)c * kStripCols;
-        const double *xg = a.X + (size_t)m * N * SM::XST;
+        const double *xg = a.X + ((size_t)m * N + a.row0) * SM::XST;   // gathered x of the block's rows
         const int nstages = (r_hi - r_lo + RS - 1) / RS;
 
         auto issue = [&](int k) {   // stage k of this piece into buffer q_issue % S (thread 0)
@@ -342,9 +343,9 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
         }
 
         // ---- piece done: partial column sums into slot (b + g); the last piece of the strip reduces
-        const int64_t gN = g64 * N;
+        const int64_t gN = g64 * R;
         const int first = (int)(gN / U);
-        const int last = (int)((gN + N - 1) / U);
+        const int last = (int)((gN + R - 1) / U);
         double *part = a.part + (size_t)(b + g) * NV * kStripCols;
         if constexpr (SM::MMA) {
             // rows of D of the running groups (converged vectors are never read back)
@@ -403,7 +404,10 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
                         y0 += t.x;
                         y1 += t.y;
                     }
-                    double *yv = a.y + (((size_t)m * NV + v) * 2 + (1 - s_cur[sl])) * N + c * kStripCols + 2 * tid;
+                    // row shard: the partial y goes to the contiguous buffer the caller all-reduces
+                    double *yv = (a.ypart ? a.ypart + ((size_t)m * NV + v) * N
+                                          : a.y + (((size_t)m * NV + v) * 2 + (1 - s_cur[sl])) * N) +
+                                 c * kStripCols + 2 * tid;
                     yv[0] = y0;
                     if (2 * tid + 1 < cols) yv[1] = y1;
                     else y1 = 0.0;
@@ -441,6 +445,10 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
     const int c = blockIdx.x, mv = blockIdx.y, tid = threadIdx.x;
     const int N = a.N;
     const SolveState st = a.st[mv];
+    if (st.done && a.ypart) {   // row shard: a frozen vector's partial stays zero through the all-reduces
+        const int j1 = min(N, (c + 1) * kCheckChunk);
+        for (int j = c * kCheckChunk + tid; j < j1; j += 256) a.ypart[(size_t)mv * N + j] = 0.0;
+    }
     if (!st.done) {
         const int m = mv / a.V, v = mv % a.V;
         // s = the strip sums added by every warp in the same fixed order (lane-strided, xor tree), so
@@ -452,8 +460,15 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
         for (int k = tid & 31; k < nstrips; k += 32) S += __ldcg(ss + k);
         S = warp_sum(S);
         const double inv_new = 1.0 / S, inv_old = 1.0 / st.s;
-        const double *yn = a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
+        // row shard: y = the all-reduced partial products (a.ypart); it is also kept in y[1 - cur] as
+        // the next iterate (finish kernel, next change)
+        const double *yn = a.ypart ? a.ypart + (size_t)mv * N : a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
         const double *yo = a.y + ((size_t)mv * 2 + st.cur) * N;
+        if (a.ypart) {
+            double *yw = a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
+            const int j1 = min(N, (c + 1) * kCheckChunk);
+            for (int j = c * kCheckChunk + tid; j < j1; j += 256) yw[j] = __ldcg(yn + j);
+        }
         const int l = st.l < 0 ? 0 : st.l;
         double l1 = 0.0;
         if (i8) {
@@ -556,6 +571,27 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
                 if (a.use_handle) cudaGraphSetConditional(a.handle, n_act > 0 ? 1u : 0u);
             }
         }
+    }
+}
+
+// Row shard: strip sums of the all-reduced partial products, fixed order (the GEMV's own strip sums
+// cover only the shard's rows). CTA (strip, mv).
+__global__ void __launch_bounds__(256) k_shard_ssum(const PowerArgs a) {
+    __shared__ double red[8];
+    const int c = blockIdx.x, mv = blockIdx.y, tid = threadIdx.x;
+    const int N = a.N;
+    const double *yp = a.ypart + (size_t)mv * N + (size_t)c * kStripCols;
+    const int cols = min(kStripCols, N - c * kStripCols);
+    double t = 0.0;
+    for (int j = tid; j < cols; j += 256) t += __ldcg(yp + j);
+    t = warp_sum(t);
+    if ((tid & 31) == 0) red[tid >> 5] = t;
+    __syncthreads();
+    if (tid == 0) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sum += red[w];
+        a.ssum[(size_t)mv * a.strips + c] = sum;
     }
 }
 
@@ -687,6 +723,7 @@ int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a) {
     out->step_fn = step_fn(dtype, V, &out->step_smem, &cps);
     out->check_fn = (void *)k_power_check;
     out->finish_fn = (void *)k_power_finish;
+    out->ssum_fn = (void *)k_shard_ssum;
     if (!out->step_fn) return 1;
     const int gx = (a.N + 255) / 256 < 64 ? (a.N + 255) / 256 : 64;
     out->init_grid = dim3(gx, a.M * a.V);

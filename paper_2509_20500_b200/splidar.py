@@ -95,6 +95,13 @@ def _lib():
             "splidar_plan_destroy": (None, [p]),
             "splidar_plan_kind": (C.c_int, [p]),
             "splidar_plan_gemv": (C.c_int, [p, p]),
+            "splidar_build_base_rows": (st, [fp, st, st, p, i64, i32, i32, p, sz, p]),
+            "splidar_plan_create_rows": (st, [C.POINTER(p), p, i32, i32, i32, i64, st, d, p, i32, d, i32, p, p, p,
+                                              sz, p]),
+            "splidar_plan_shard_init": (st, [p, p]),
+            "splidar_plan_shard_gemv": (st, [p, p]),
+            "splidar_plan_shard_check": (st, [p, C.POINTER(i32), p]),
+            "splidar_plan_shard_finish": (st, [p, pinfo, p]),
             "splidar_structured_workspace_bytes": (sz, [i32, i32, i32]),
             "splidar_stationary_structured": (st, [fp, i32, p, p, p, d, i32, p, p, sz, pinfo, p]),
             "splidar_second_eigenvalue": (st, [fp, i32, p, p, p, p, d, i32, p, sz, C.POINTER(SpectralInfo), p]),
@@ -393,6 +400,75 @@ class Plan:
     def execute(self, stream=None, check: bool = True) -> list:
         self.launch(stream)
         return self.info(stream, check)
+
+    def close(self):
+        if self._h:
+            _lib().splidar_plan_destroy(self._h)
+            self._h = C.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@_allocates_on_stream
+def build_base_rows(flux, row0: int, n_rows: int, dtype=torch.float64, mode: str = "factored",
+                    out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Rows [row0, row0 + n_rows) of P~0 ([n_rows, N] view of [n_rows, ld] storage), the same entries
+    as those rows of build_base (SURVEY §8(e)(ii) row shard)."""
+    N = int(flux.n_bins)
+    ld = leading_dim(N, dtype)
+    P = out if out is not None else torch.empty((n_rows, ld), dtype=dtype, device="cuda")[:, :N]
+    ptr, n, ldp, dt = _matrix_args(P)
+    ws = ws if ws is not None else workspace(N)
+    fa = _FluxArg(flux)
+    _check(_lib().splidar_build_base_rows(C.byref(fa.s), dt, _MODES[mode], ptr, ldp, int(row0), int(n_rows),
+                                          ws.data_ptr(), ws.numel(), _stream(stream)), "splidar_build_base_rows")
+    return P
+
+
+class ShardPlan:
+    """One rank's part of a row-sharded power iteration (include/splidar.h): P0_rows
+    holds rows [row0, row0 + n_rows) of the N x N P~0; t_d: V dead times. ypart [V, N] is this rank's
+    partial product, to be summed over the ranks between gemv() and check(); pi [V, N] after finish().
+    See shard.sharded_solve for the loop."""
+
+    def __init__(self, P0_rows: torch.Tensor, row0: int, n_bins: int, t_r: float, t_d, tol: float = 1e-12,
+                 max_iter: int = 10 ** 6, ws: torch.Tensor | None = None, stream=None):
+        ptr, n, ld, dt = _matrix_args(P0_rows)
+        if n != n_bins:
+            raise SplidarError(EINVAL, "ShardPlan: P0_rows must have N columns")
+        T = np.ascontiguousarray(t_d, dtype=np.float64).reshape(-1)
+        self.V, self.N, self.stream = T.size, n_bins, stream
+        self.pi = torch.empty((self.V, n_bins), dtype=torch.float64, device=P0_rows.device)
+        self.ypart = torch.zeros((self.V, n_bins), dtype=torch.float64, device=P0_rows.device)
+        self.ws = ws if ws is not None else workspace(n_bins, 1, self.V, device=P0_rows.device)
+        self.P0_rows, self._T = P0_rows, T
+        self._h = C.c_void_p(None)
+        _check(_lib().splidar_plan_create_rows(C.byref(self._h), ptr, int(row0), int(P0_rows.shape[0]), n_bins, ld,
+                                               dt, float(t_r), T.ctypes.data, self.V, float(tol), int(max_iter),
+                                               self.pi.data_ptr(), self.ypart.data_ptr(), self.ws.data_ptr(),
+                                               self.ws.numel(), _stream(stream)), "splidar_plan_create_rows")
+
+    def init(self):
+        _check(_lib().splidar_plan_shard_init(self._h, _stream(self.stream)), "splidar_plan_shard_init")
+
+    def gemv(self):
+        _check(_lib().splidar_plan_shard_gemv(self._h, _stream(self.stream)), "splidar_plan_shard_gemv")
+
+    def check(self) -> bool:
+        more = C.c_int32(0)
+        _check(_lib().splidar_plan_shard_check(self._h, C.byref(more), _stream(self.stream)),
+               "splidar_plan_shard_check")
+        return bool(more.value)
+
+    def finish(self, check: bool = True) -> list:
+        infos = (SolveInfo * self.V)()
+        st = _lib().splidar_plan_shard_finish(self._h, infos, _stream(self.stream))
+        _check(st, "splidar_plan_shard_finish", allow=() if check else (ENOCONV,))
+        return [i.as_dict() for i in infos]
 
     def close(self):
         if self._h:
