@@ -57,6 +57,10 @@ def parse():
     p.add_argument("--mc-split", type=int, default=None, help="--path mc: sub-chains per run (default: auto)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="dense path: never replay the step as a CUDA graph")
+    p.add_argument("--shard", default="items", choices=["items", "rows"],
+                   help="multi-GPU split (SURVEY 8(e)): items = independent items per rank, no collective (weak "
+                        "scaling); rows = one matrix split by rows, one NCCL all-reduce of N x V doubles per "
+                        "iteration (strong scaling; dense path, c4 / c5)")
     return p.parse_args()
 
 
@@ -383,6 +387,97 @@ def run_e2e(args, w, groups, st, world):
             "d2h_bytes_per_step": n_solves * N * 8,
             "note": "host wall clock; includes plan (CUDA graph) instantiation, the theta upload and the pi "
                     "copy to pinned host memory every step"}
+
+
+# ------------------------------------------------------------------------------- row shards (8(e)(ii))
+def run_rows(args, rank, world, dev):
+    """One matrix split by rows over the ranks: rank g builds rows row_block(N, g, W)
+    of P~0 and the power iteration all-reduces the N x V partial products once per iteration over NCCL
+    (the gather offset is applied after the collective, in the replicated check). The workload is the
+    config's own (c5: t_d = 430 + the 16-value sweep, 17 vectors; c4: one solve), so the total work is
+    fixed: strong scaling. Device time by CUDA events around each step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2509_20500_b200 as spl
+    from paper_2509_20500_b200.shard import max_over_ranks, row_block, sharded_solve
+    w, groups = workload_items(args.workload, 0, 1)            # every rank: the whole item list
+    if len(groups) != 1:
+        raise SystemExit("--shard rows: one matrix per step (c4, c5)")
+    f, tds = groups[0]
+    N = f.n_bins
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    r0, n = row_block(N, rank, world)
+    ld = spl.leading_dim(N, dt)
+    rows = torch.empty((n, ld), dtype=dt, device="cuda")[:, :N]
+    ws_b = spl.workspace(N)
+    plan = spl.ShardPlan(rows, r0, N, f.t_r, tds, tol=1e-12)
+    reduce = (lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM)) if world > 1 else (lambda t: None)
+    n_ar = [0]
+
+    def counted(t):
+        n_ar[0] += 1
+        reduce(t)
+
+    def step():
+        spl.build_base_rows(f, r0, n, dt, args.mode, out=rows, ws=ws_b)
+        return sharded_solve(plan, counted)
+
+    for _ in range(args.warmup):
+        infos = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev)
+    time.sleep(0.25)
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    n_ar[0] = 0
+    for e0, e1 in ev:
+        e0.record(stream)
+        infos = step()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    K = args.steps
+    ar_per_step = n_ar[0] // K
+    t_total = max_over_ranks([sum(a.elapsed_time(b) for a, b in ev) / 1e3], device="cuda")[0]
+    iters = [i["iters"] for i in infos]
+    b = 8 if args.dtype == "f64" else 4
+    passes = max(iters)
+    hbm, hbm_src = load_peaks()
+    # every rank reads its n x N block once per pass: the job reads N^2 b per pass
+    gemv_gbs = passes * N * N * b * K / t_total / 1e9
+    pi_host = torch.empty((len(tds), N), dtype=torch.float64, pin_memory=True)
+    t0 = time.perf_counter()                           # e2e: theta from the host, pi to pinned host memory
+    for _ in range(K):
+        step()
+        pi_host.copy_(plan.pi, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    t_e2e = max_over_ranks([time.perf_counter() - t0], device="cuda")[0]
+    value = len(tds) * K / t_total
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": t_total / K * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic (seeded BASELINE.json flux parameters; inputs are theta only)",
+        "config": {"workload": f"{args.workload}: {w.description}", "n_bins": N, "solves_per_step": len(tds),
+                   "parallelism": f"rows{world}: P~0 split by rows over {world} ranks, one NCCL all-reduce of "
+                                  f"N x {len(tds)} fp64 per iteration" if world > 1 else "single GPU (row shard of 1)",
+                   "rows_per_rank": n, "allreduces_per_step": ar_per_step,
+                   "l2": "matrix > 126 MB L2: no flush needed" if N * N * b > 126e6 else "fits in L2"},
+        "iterations": iters,
+        "roofline": {"bound": "hbm", "kernel": "k_power_step (row shard) + NCCL all-reduce", "achieved": gemv_gbs,
+                     "peak": hbm * world, "unit": "GB/s", "frac": gemv_gbs / (hbm * world),
+                     "traffic": None, "peak_source": hbm_src + f" x {world} GPUs",
+                     "note": "job-wide algorithmic bytes (N^2 b per pass) / step time (build, GEMV, all-reduce, "
+                             "check, host loop)"},
+        "clocks": clk,
+        "e2e": {"value": len(tds) * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * (3 * len(f.tau) + 3 + len(tds)),
+                "d2h_bytes_per_step": len(tds) * N * 8},
+        "gpu_launches": K * (2 + 5 + 1 + 3 * passes + 1), "impl": "ours", "lib": spl.lib_path(),
+    }
 
 
 # ------------------------------------------------------------------------------- stored-matrix lambda_2
@@ -872,11 +967,29 @@ def run_oracle_sample(args, iters_per_item=None):
             "solve_products_entries_per_s_one_core": N / tm, "host": host_info()}
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not started by torchrun: launch one rank per GPU ourselves (rank 0 prints the line)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        return subprocess.call(cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
 
     if args.impl == "reference":
         if rank != 0:
@@ -908,7 +1021,9 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    if args.path == "dense":
+    if args.path == "dense" and args.shard == "rows":
+        line = run_rows(args, rank, world, dev)
+    elif args.path == "dense":
         line = run_ours(args, rank, world, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             its = line["iterations"]

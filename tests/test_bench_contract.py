@@ -52,3 +52,24 @@ def test_our_line(extra):
         assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
     if not extra:                        # the default line: c5, HBM-bound GEMV near the roofline
         assert d["config"]["workload"].startswith("c5") and r["frac"] > 0.7 and d["roofline_build"]["frac"] > 0.7
+
+
+def test_gpus_flag_must_match_world():
+    """--gpus N under a launcher with a different WORLD_SIZE is an error (exit 2), never a silent
+    single-rank run; without WORLD_SIZE, --gpus N > 1 re-launches itself through torch.distributed.run."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE=1" in out.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload,dtype", [("c5", "f64"), ("c4", "f32")])
+def test_row_shard_line(workload, dtype):
+    """--shard rows on one GPU: a row shard of 1, strong scaling, same solves."""
+    d = _run("--shard", "rows", "--workload", workload, "--dtype", dtype, "--steps", "2", "--warmup", "3",
+             "--no-cpu-baseline")
+    assert BASE <= set(d) and d["scaling"] == "strong" and d["n_gpus"] == 1 and d["value"] > 0
+    assert d["config"]["rows_per_rank"] == d["config"]["n_bins"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(d["roofline"])
+    assert d["roofline"]["frac"] > 0.5
