@@ -146,6 +146,31 @@ splidar_status splidar_build_eq4(const splidar_flux *flux, double t_d, splidar_d
 splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, splidar_dtype dt,
                                   double t_r, double t_d, double tol, int32_t max_iter, double *pi,
                                   void *ws, size_t ws_bytes, splidar_solve_info *info, void *stream);
+/* Step 4 for n_matrices matrices (P0 + m * matrix_stride) x n_vectors dead times each
+ * (t_d[n_matrices * n_vectors], matrix-major), one multi-vector GEMV per matrix and pass; pi: device
+ * fp64 [n_matrices * n_vectors * N]; info: host [n_matrices * n_vectors] or NULL; ws:
+ * splidar_workspace_bytes(N, n_matrices, n_vectors). Synchronises stream once.
+ * splidar_stationary is the case n_matrices = n_vectors = 1. Both keep the instantiated solver
+ * (a plan) in a library cache keyed by (device, P0, strides, N, dtype, n_matrices, n_vectors, tol,
+ * max_iter, pi, ws): a repeated call with the same buffers replays it (the shifts and output rows
+ * go back into the workspace with one small upload, since the workspace is scratch between calls)
+ * instead of building a CUDA graph per call. The cache holds at most 16 plans,
+ * least recently used first out; splidar_plan_cache_clear() destroys them (call it before freeing
+ * the CUDA context, or to return their pinned host memory). The same contract as plans applies:
+ * one call at a time per workspace. */
+splidar_status splidar_stationary_multi(const void *P0, int32_t n_matrices, int64_t matrix_stride,
+                                        int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r,
+                                        const double *t_d, int32_t n_vectors, double tol,
+                                        int32_t max_iter, double *pi, void *ws, size_t ws_bytes,
+                                        splidar_solve_info *info, void *stream);
+/* As splidar_stationary_multi, and pi is also copied to pi_host (host [n_matrices * n_vectors * N],
+ * pinned for an asynchronous copy) before the one stream synchronisation: host out in one call. */
+splidar_status splidar_stationary_multi_host(const void *P0, int32_t n_matrices, int64_t matrix_stride,
+                                             int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r,
+                                             const double *t_d, int32_t n_vectors, double tol,
+                                             int32_t max_iter, double *pi, double *pi_host, void *ws,
+                                             size_t ws_bytes, splidar_solve_info *info, void *stream);
+void splidar_plan_cache_clear(void);
 
 /* Steps 1-4 for a batch of (signal, background, dead-time) triples (synchronises stream once):
  * item m has pulses (shape.tau, shape.sigma, S[m] * shape.signal[k]) and background B[m], dead time

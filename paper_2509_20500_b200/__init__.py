@@ -13,4 +13,5 @@ from .splidar import (  # noqa: F401
     SpectralInfo, bin_trajectory, flux_items, mixing_steps, second_eigenvalue, second_eigenvalue_dense,
     stationary_structured,
     structured_workspace, StructPlan, build_eq4, monte_carlo, lambda2_of, build_base_rows, ShardPlan,
+    stationary_multi, plan_cache_clear,
 )

@@ -4,7 +4,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <list>
 #include <map>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -91,8 +93,26 @@ __global__ void k_upload(const UpChunk c, unsigned char *dst) {
 }
 }  // namespace
 
+// Small uploads (one flux record, a plan's shifts) as a 1 KB parameter block: the launch copies its
+// whole parameter block, so a 32 KB block for a few hundred bytes costs microseconds per call.
+constexpr int kUpSmall = 1024;
+struct UpSmall {
+    unsigned char data[kUpSmall];
+    int n;
+};
+__global__ void k_upload_small(const UpSmall c, unsigned char *dst) {
+    for (int i = threadIdx.x; i < c.n; i += blockDim.x) dst[i] = c.data[i];
+}
+
 static cudaError_t upload_async(void *dst, const void *src, size_t n, cudaStream_t s) {
     const unsigned char *p = static_cast<const unsigned char *>(src);
+    if (n <= (size_t)kUpSmall) {
+        UpSmall c;
+        c.n = (int)n;
+        memcpy(c.data, p, n);
+        k_upload_small<<<1, 128, 0, s>>>(c, static_cast<unsigned char *>(dst));
+        return cudaGetLastError();
+    }
     for (size_t o = 0; o < n; o += kUpChunk) {
         UpChunk c;
         c.n = (int)((n - o) < (size_t)kUpChunk ? (n - o) : (size_t)kUpChunk);
@@ -675,16 +695,123 @@ splidar_status splidar_plan_execute(splidar_plan plan, splidar_solve_info *info,
     return splidar_plan_info(plan, info, stream);
 }
 
+// ---- plan cache of the one-shot calls (splidar_stationary, splidar_stationary_multi) ----------
+// A plan binds pointers (P0, pi, workspace), sizes, dtype, tol and max_iter; the shifts l and output
+// rows live in the workspace and are re-uploaded (one small upload) by every launch of a cached plan. A
+// one-shot call with the same binding as an earlier one therefore replays that call's instantiated
+// graph instead of building, instantiating and destroying one (the host cost that dominated small N).
+// Keyed by the current device too. LRU of kPlanCache entries; splidar_plan_cache_clear frees them.
+namespace {
+struct PlanKey {
+    int dev, M, N, V, dt, max_iter;
+    const void *P0;
+    int64_t mstride, ld;
+    double tol;
+    double *pi;
+    void *ws;
+    size_t ws_bytes;
+    bool operator==(const PlanKey &o) const {
+        return dev == o.dev && M == o.M && N == o.N && V == o.V && dt == o.dt && max_iter == o.max_iter &&
+               P0 == o.P0 && mstride == o.mstride && ld == o.ld && tol == o.tol && pi == o.pi && ws == o.ws &&
+               ws_bytes == o.ws_bytes;
+    }
+};
+struct CachedPlan {
+    PlanKey key;
+    splidar_plan plan;
+    std::vector<int> l;
+};
+constexpr size_t kPlanCache = 16;
+std::mutex g_cache_mu;
+std::list<CachedPlan> g_cache;   // most recently used first
+}  // namespace
+
+static splidar_status cached_execute(const void *P0, int M, int64_t mstride, int N, int64_t ld, int dt,
+                                     const int *l, int V, double tol, int max_iter, double *pi, void *ws,
+                                     size_t ws_bytes, splidar_solve_info *info, cudaStream_t s,
+                                     double *pi_host = nullptr) {
+    PlanKey key{current_device(), M, N, V, dt, max_iter, P0, mstride, ld, tol, pi, ws, ws_bytes};
+    const std::vector<int> lv(l, l + (size_t)M * V);
+    splidar_plan plan = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(g_cache_mu);
+        for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+            if (it->key == key) {
+                plan = it->plan;
+                for (int m = 0; m < M; ++m)
+                    for (int v = 0; v < V; ++v) plan->lsh[(size_t)m * plan->V + v] = lv[(size_t)m * V + v];
+                it->l = lv;
+                // the workspace is scratch between calls (the caller may have used it for anything):
+                // the plan's shifts and output rows go back in with one upload per launch
+                const WsLayout &L = plan->L;
+                std::vector<unsigned char> blob(L.oidx + sizeof(int) * plan->out_idx.size() - L.lsh, 0);
+                memcpy(blob.data(), plan->lsh.data(), sizeof(int) * plan->lsh.size());
+                memcpy(blob.data() + (L.oidx - L.lsh), plan->out_idx.data(), sizeof(int) * plan->out_idx.size());
+                SPL_CUDA(spl::upload_async(static_cast<char *>(ws) + L.lsh, blob.data(), blob.size(), s));
+                g_cache.splice(g_cache.begin(), g_cache, it);
+                break;
+            }
+    }
+    if (!plan) {
+        splidar_status st = plan_create_l(&plan, P0, M, mstride, N, ld, dt, l, V, tol, max_iter, pi, nullptr, ws,
+                                          ws_bytes, s);
+        if (st) return st;
+        std::lock_guard<std::mutex> lock(g_cache_mu);
+        g_cache.push_front(CachedPlan{key, plan, lv});
+        while (g_cache.size() > kPlanCache) {
+            splidar_plan_destroy(g_cache.back().plan);
+            g_cache.pop_back();
+        }
+    }
+    // the cached plan is used under the cache lock's protection only for lookup; like any plan it
+    // must not be launched concurrently on two streams with the same workspace (the caller's contract)
+    splidar_status st = splidar_plan_launch(plan, s);
+    if (st) return st;
+    if (pi_host)   // the result's copy to the host rides on the same stream sync as the info
+        SPL_CUDA(cudaMemcpyAsync(pi_host, pi, sizeof(double) * (size_t)M * V * N, cudaMemcpyDeviceToHost, s));
+    return splidar_plan_info(plan, info, s);
+}
+
+void splidar_plan_cache_clear(void) {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    for (auto &c : g_cache) splidar_plan_destroy(c.plan);
+    g_cache.clear();
+}
+
 splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r,
                                   double t_d, double tol, int32_t max_iter, double *pi, void *ws,
                                   size_t ws_bytes, splidar_solve_info *info, void *stream) {
-    splidar_plan p;
-    splidar_status st = splidar_plan_create(&p, P0, 1, (int64_t)n_bins * ld, n_bins, ld, dt, t_r, &t_d, 1, tol,
-                                            max_iter, pi, ws, ws_bytes, stream);
-    if (st) return st;
-    st = splidar_plan_execute(p, info, stream);
-    splidar_plan_destroy(p);
-    return st;
+    return splidar_stationary_multi(P0, 1, (int64_t)n_bins * ld, n_bins, ld, dt, t_r, &t_d, 1, tol, max_iter, pi,
+                                    ws, ws_bytes, info, stream);
+}
+
+splidar_status splidar_stationary_multi(const void *P0, int32_t n_matrices, int64_t matrix_stride, int32_t n_bins,
+                                        int64_t ld, splidar_dtype dt, double t_r, const double *t_d,
+                                        int32_t n_vectors, double tol, int32_t max_iter, double *pi, void *ws,
+                                        size_t ws_bytes, splidar_solve_info *info, void *stream) {
+    return splidar_stationary_multi_host(P0, n_matrices, matrix_stride, n_bins, ld, dt, t_r, t_d, n_vectors, tol,
+                                         max_iter, pi, nullptr, ws, ws_bytes, info, stream);
+}
+
+splidar_status splidar_stationary_multi_host(const void *P0, int32_t n_matrices, int64_t matrix_stride,
+                                             int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r,
+                                             const double *t_d, int32_t n_vectors, double tol, int32_t max_iter,
+                                             double *pi, double *pi_host, void *ws, size_t ws_bytes,
+                                             splidar_solve_info *info, void *stream) {
+    splidar_status st;
+    if (!t_d || n_matrices < 1 || n_vectors < 1 || n_vectors > kMaxVectors) return SPLIDAR_EINVAL;
+    if ((st = check_matrix(P0, n_bins, ld, dt))) return st;
+    if (n_matrices > 1 && (matrix_stride < (int64_t)n_bins * ld || matrix_stride % ld != 0)) return SPLIDAR_EINVAL;
+    if (!(tol > 0.0) || !std::isfinite(tol) || max_iter < 1 || !pi) return SPLIDAR_EINVAL;
+    std::vector<int> l((size_t)n_matrices * n_vectors);
+    for (size_t i = 0; i < l.size(); ++i) {
+        int32_t li;
+        if ((st = splidar_shift(t_r, n_bins, t_d[i], &li))) return st;
+        l[i] = li;
+    }
+    if ((st = check_ws(ws, ws_bytes, ws_layout(n_bins, n_matrices, n_vectors)))) return st;
+    return cached_execute(P0, n_matrices, n_matrices > 1 ? matrix_stride : (int64_t)n_bins * ld, n_bins, ld, dt,
+                          l.data(), n_vectors, tol, max_iter, pi, ws, ws_bytes, info, (cudaStream_t)stream, pi_host);
 }
 
 // ------------------------------------------------ row shards ---------------

@@ -86,6 +86,10 @@ def _lib():
             "splidar_build_base_batched": (st, [fp, i32, st, st, p, i64, i64, p, sz, p]),
             "splidar_apply_deadtime": (st, [p, p, i32, i64, st, d, d, p]),
             "splidar_stationary": (st, [p, i32, i64, st, d, d, d, i32, p, p, sz, pinfo, p]),
+            "splidar_stationary_multi": (st, [p, i32, i64, i32, i64, st, d, p, i32, d, i32, p, p, sz, pinfo, p]),
+            "splidar_stationary_multi_host": (st, [p, i32, i64, i32, i64, st, d, p, i32, d, i32, p, p, p, sz, pinfo,
+                                                   p]),
+            "splidar_plan_cache_clear": (None, []),
             "splidar_sweep": (st, [fp, i32, p, p, p, st, st, d, i32, p, p, i32, i64, p, sz, pinfo, p]),
             "splidar_plan_create": (st, [C.POINTER(p), p, i32, i64, i32, i64, st, d, p, i32, d, i32, p, p,
                                          sz, p]),
@@ -144,29 +148,38 @@ def _check(status: int, where: str, allow=()):
     return status
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    if _RAW_STREAM is not None:                 # the current stream's handle without a Stream object
+        return _RAW_STREAM(torch.cuda.current_device())
+    return torch.cuda.current_stream().cuda_stream
 
 
 def _allocates_on_stream(fn):
     """Runs fn with `stream` (when given) as torch's current stream, so that every workspace, output
     and temporary fn allocates belongs to the stream its kernels are enqueued on: the caching
     allocator then never hands a temporary that kernels on `stream` still read to another stream's
-    allocation after fn returns."""
-    sig = inspect.signature(fn)
+    allocation after fn returns. (The position of `stream` is looked up once, not per call.)"""
+    names = list(inspect.signature(fn).parameters)
+    pos = names.index("stream")
 
     @functools.wraps(fn)
     def wrapper(*args, **kwargs):
-        st = sig.bind_partial(*args, **kwargs).arguments.get("stream")
-        ctx = torch.cuda.stream(st) if isinstance(st, torch.cuda.Stream) else contextlib.nullcontext()
-        with ctx:
-            return fn(*args, **kwargs)
+        st = kwargs.get("stream") if len(args) <= pos else args[pos]
+        if isinstance(st, torch.cuda.Stream):
+            with torch.cuda.stream(st):
+                return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
     return wrapper
 
 
 class _FluxArg:
-    """Marshals any object with t_r, n_bins, tau, sigma, signal, background into splidar_flux."""
+    """Marshals any object with t_r, n_bins, tau, sigma, signal, background into splidar_flux.
+    Hashable (frozen) flux objects are marshalled once and reused (see _flux_arg)."""
 
     def __init__(self, flux):
         self.tau = np.ascontiguousarray(flux.tau, dtype=np.float64).reshape(-1)
@@ -185,6 +198,22 @@ def shift(t_r: float, n_bins: int, t_d: float) -> int:
     return out.value
 
 
+_FLUX_CACHE: dict = {}
+
+
+def _flux_arg(flux) -> "_FluxArg":
+    params = getattr(flux, "__dataclass_params__", None)
+    if params is None or not params.frozen:             # only immutable fluxes are marshalled once
+        return _FluxArg(flux)
+    fa = _FLUX_CACHE.get(flux)
+    if fa is None:
+        if len(_FLUX_CACHE) > 4096:
+            _FLUX_CACHE.clear()
+        fa = _FLUX_CACHE[flux] = _FluxArg(flux)
+    return fa
+
+
+@functools.lru_cache(maxsize=1024)
 def workspace_bytes(n_bins: int, n_matrices: int = 1, n_vectors: int = 1) -> int:
     return int(_lib().splidar_workspace_bytes(int(n_bins), int(n_matrices), int(n_vectors)))
 
@@ -196,6 +225,24 @@ def workspace(n_bins: int, n_matrices: int = 1, n_vectors: int = 1, device=None)
     t = torch.empty(n + 256, dtype=torch.uint8, device=device or "cuda")
     off = (-t.data_ptr()) % 256
     return t[off:off + n]
+
+
+_SCRATCH: dict = {}
+
+
+def _scratch_workspace(n_bins: int, n_matrices: int, n_vectors: int, device, stream) -> torch.Tensor:
+    """The workspace of a one-shot solve when the caller passes none: kept per (device, stream, sizes)
+    and reused, so repeated calls allocate nothing and hit the library's plan cache (which keys on
+    the workspace pointer). Calls on different streams never share one."""
+    dev = device if isinstance(device, torch.device) else (
+        torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device()))
+    key = (dev.index, _stream(stream), n_bins, n_matrices, n_vectors)
+    ws = _SCRATCH.get(key)
+    if ws is None:
+        if len(_SCRATCH) > 64:
+            _SCRATCH.clear()
+        ws = _SCRATCH[key] = workspace(n_bins, n_matrices, n_vectors, device=dev)
+    return ws
 
 
 def leading_dim(n_bins: int, dtype=torch.float64) -> int:
@@ -224,7 +271,7 @@ def flux_vectors(flux, ws: torch.Tensor | None = None, stream=None) -> dict:
     ws = ws if ws is not None else workspace(N)
     F, lam, w, invd = (torch.empty(N, dtype=torch.float64, device=ws.device) for _ in range(4))
     L = torch.empty(1, dtype=torch.float64, device=ws.device)
-    fa = _FluxArg(flux)
+    fa = _flux_arg(flux)
     _check(_lib().splidar_flux_vectors(C.byref(fa.s), F.data_ptr(), lam.data_ptr(), w.data_ptr(), invd.data_ptr(),
                                        L.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)),
            "splidar_flux_vectors")
@@ -239,7 +286,7 @@ def build_base(flux, dtype=torch.float64, mode: str = "factored", out: torch.Ten
     P = out if out is not None else empty_matrix(N, dtype)
     ptr, n, ld, dt = _matrix_args(P)
     ws = ws if ws is not None else workspace(N)
-    fa = _FluxArg(flux)
+    fa = _flux_arg(flux)
     _check(_lib().splidar_build_base(C.byref(fa.s), dt, _MODES[mode], ptr, ld, ws.data_ptr(), ws.numel(),
                                      _stream(stream)), "splidar_build_base")
     return P
@@ -254,7 +301,7 @@ def build_base_batched(fluxes, dtype=torch.float64, mode: str = "factored", out:
     P = out if out is not None else empty_matrix(N, dtype, n_matrices=M)
     ptr, n, ld, dt = _matrix_args(P)
     ws = ws if ws is not None else workspace(N, M)
-    fas = [_FluxArg(f) for f in fluxes]
+    fas = [_flux_arg(f) for f in fluxes]
     arr = (_Flux * M)(*[fa.s for fa in fas])
     _check(_lib().splidar_build_base_batched(arr, M, dt, _MODES[mode], ptr, ld, P.stride(0), ws.data_ptr(),
                                              ws.numel(), _stream(stream)), "splidar_build_base_batched")
@@ -267,7 +314,7 @@ def build_eq4(flux, t_d: float, dtype=torch.float64, out: torch.Tensor | None = 
     N = int(flux.n_bins)
     P = out if out is not None else empty_matrix(N, dtype)
     ptr, n, ld, dt = _matrix_args(P)
-    fa = _FluxArg(flux)
+    fa = _flux_arg(flux)
     _check(_lib().splidar_build_eq4(C.byref(fa.s), float(t_d), dt, ptr, ld, _stream(stream)), "splidar_build_eq4")
     return P
 
@@ -293,12 +340,44 @@ def stationary(P0: torch.Tensor, t_r: float, t_d: float, tol: float = 1e-12, max
     """Step 4: pi with pi (J_l P~0) = pi by on-device power iteration. Returns (pi, info dict)."""
     ptr, n, ld, dt = _matrix_args(P0)
     pi = out if out is not None else torch.empty(n, dtype=torch.float64, device=P0.device)
-    ws = ws if ws is not None else workspace(n)
+    ws = ws if ws is not None else _scratch_workspace(n, 1, 1, P0.device, stream)
     info = SolveInfo()
     st = _lib().splidar_stationary(ptr, n, ld, dt, float(t_r), float(t_d), float(tol), int(max_iter),
                                    pi.data_ptr(), ws.data_ptr(), ws.numel(), C.byref(info), _stream(stream))
     _check(st, "splidar_stationary", allow=() if check else (ENOCONV,))
     return pi, info.as_dict()
+
+
+@_allocates_on_stream
+def stationary_multi(P0: torch.Tensor, t_r: float, t_d, tol: float = 1e-12, max_iter: int = 10 ** 6,
+                     out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None,
+                     check: bool = True, out_host: torch.Tensor | None = None):
+    """Step 4 for M matrices ([M, N, N] view) x V dead times each (t_d [M, V]) in one call; the
+    instantiated solver is cached in the library per (buffers, sizes) and replayed by repeated calls.
+    out_host (pinned CPU fp64 [M, V, N], optional) also receives pi within the same synchronisation.
+    Returns (pi [M, V, N], list of M * V info dicts)."""
+    ptr, n, ld, dt = _matrix_args(P0)
+    M = P0.shape[0] if P0.dim() == 3 else 1
+    mstride = P0.stride(0) if P0.dim() == 3 else n * ld
+    T = np.ascontiguousarray(t_d, dtype=np.float64).reshape(M, -1)
+    V = T.shape[1]
+    pi = out if out is not None else torch.empty((M, V, n), dtype=torch.float64, device=P0.device)
+    ws = ws if ws is not None else _scratch_workspace(n, M, V, P0.device, stream)
+    infos = (SolveInfo * (M * V))()
+    if out_host is not None and (out_host.is_cuda or out_host.dtype != torch.float64 or not out_host.is_contiguous()
+                                 or out_host.numel() != M * V * n):
+        raise SplidarError(EINVAL, "stationary_multi: out_host must be a contiguous CPU fp64 tensor of M*V*N")
+    st = _lib().splidar_stationary_multi_host(ptr, M, mstride, n, ld, dt, float(t_r), T.ctypes.data, V, float(tol),
+                                              int(max_iter), pi.data_ptr(),
+                                              out_host.data_ptr() if out_host is not None else None,
+                                              ws.data_ptr(), ws.numel(), infos, _stream(stream))
+    _check(st, "splidar_stationary_multi", allow=() if check else (ENOCONV,))
+    return pi, [i.as_dict() for i in infos]
+
+
+def plan_cache_clear() -> None:
+    """Destroy the library's cached one-shot solvers (splidar_plan_cache_clear)."""
+    _lib().splidar_plan_cache_clear()
 
 
 @_allocates_on_stream
@@ -320,7 +399,7 @@ def sweep(shape, S, B, t_d, dtype=torch.float64, mode: str = "factored", tol: fl
         ws = ws if ws is not None else structured_workspace(N, n_unique, M)
         pi = torch.empty((M, N), dtype=torch.float64, device=ws.device)
         infos = (SolveInfo * M)()
-        fa = _FluxArg(shape)
+        fa = _flux_arg(shape)
         st = _lib().splidar_sweep(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data, F64,
                                   _MODES[mode], float(tol), int(max_iter), pi.data_ptr(), None, 0, 0,
                                   ws.data_ptr(), ws.numel(), infos, _stream(stream))
@@ -342,7 +421,7 @@ def sweep(shape, S, B, t_d, dtype=torch.float64, mode: str = "factored", tol: fl
         ws = workspace(N, min(n_store, n_unique), max_items, device=P0_store.device)
     pi = torch.empty((M, N), dtype=torch.float64, device=P0_store.device)
     infos = (SolveInfo * M)()
-    fa = _FluxArg(shape)
+    fa = _flux_arg(shape)
     st = _lib().splidar_sweep(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data, dt, _MODES[mode],
                               float(tol), int(max_iter), pi.data_ptr(), ptr, int(n_store), ld, ws.data_ptr(),
                               ws.numel(), infos, _stream(stream))
@@ -423,7 +502,7 @@ def build_base_rows(flux, row0: int, n_rows: int, dtype=torch.float64, mode: str
     P = out if out is not None else torch.empty((n_rows, ld), dtype=dtype, device="cuda")[:, :N]
     ptr, n, ldp, dt = _matrix_args(P)
     ws = ws if ws is not None else workspace(N)
-    fa = _FluxArg(flux)
+    fa = _flux_arg(flux)
     _check(_lib().splidar_build_base_rows(C.byref(fa.s), dt, _MODES[mode], ptr, ldp, int(row0), int(n_rows),
                                           ws.data_ptr(), ws.numel(), _stream(stream)), "splidar_build_base_rows")
     return P
@@ -546,7 +625,7 @@ def stationary_structured(shape, S, B, t_d, tol: float = 1e-12, max_iter: int = 
     ws = ws if ws is not None else structured_workspace(N, n_prof, M)
     pi = torch.empty((M, N), dtype=torch.float64, device=ws.device)
     infos = (SolveInfo * M)()
-    fa = _FluxArg(shape)
+    fa = _flux_arg(shape)
     st = _lib().splidar_stationary_structured(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data,
                                               float(tol), int(max_iter), pi.data_ptr(), ws.data_ptr(), ws.numel(),
                                               infos, _stream(stream))
@@ -566,7 +645,7 @@ def second_eigenvalue(shape, S, B, t_d, pi: torch.Tensor, tol: float = 1e-13, ma
         raise SplidarError(EINVAL, "second_eigenvalue: pi must be a contiguous CUDA fp64 [M, N] tensor")
     ws = ws if ws is not None else structured_workspace(N, n_prof, M, device=pi.device)
     infos = (SpectralInfo * M)()
-    fa = _FluxArg(shape)
+    fa = _flux_arg(shape)
     st = _lib().splidar_second_eigenvalue(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data,
                                           pi.data_ptr(), float(tol), int(max_iter), ws.data_ptr(), ws.numel(),
                                           infos, _stream(stream))
@@ -607,7 +686,7 @@ def mixing_steps(flux, t_d: float, pi: torch.Tensor, eps: float = 1e-3, max_step
     ws = ws if ws is not None else structured_workspace(N, 1, N, device=pi.device)
     per = torch.empty(N, dtype=torch.int32, device=pi.device)
     out = C.c_int32(0)
-    fa = _FluxArg(flux)
+    fa = _flux_arg(flux)
     st = _lib().splidar_mixing_steps(C.byref(fa.s), float(t_d), pi.data_ptr(), float(eps), int(max_steps),
                                      per.data_ptr(), C.byref(out), ws.data_ptr(), ws.numel(), _stream(stream))
     _check(st, "splidar_mixing_steps", allow=() if check else (ENOCONV,))
@@ -624,7 +703,7 @@ def bin_trajectory(flux, t_d: float, start: torch.Tensor, bin: int, steps: int, 
     ws = ws if ws is not None else structured_workspace(N, 1, 1, device=start.device)
     traj = torch.empty(int(steps) + 1, dtype=torch.float64, device=start.device)
     fin = torch.empty(N, dtype=torch.float64, device=start.device)
-    fa = _FluxArg(flux)
+    fa = _flux_arg(flux)
     _check(_lib().splidar_bin_trajectory(C.byref(fa.s), float(t_d), start.data_ptr(), int(bin), int(steps),
                                          traj.data_ptr(), fin.data_ptr(), ws.data_ptr(), ws.numel(),
                                          _stream(stream)), "splidar_bin_trajectory")
@@ -657,7 +736,7 @@ class StructPlan:
         self.ws = ws if ws is not None else structured_workspace(self.N, n_prof, self.M, device=pi.device)
         self._keep = (S, B, T)
         self._h = C.c_void_p(None)
-        fa = _FluxArg(shape)
+        fa = _flux_arg(shape)
         _check(_lib().splidar_splan_create(C.byref(self._h), self.kind, C.byref(fa.s), self.M, S.ctypes.data,
                                            B.ctypes.data, T.ctypes.data, float(tol), int(max_iter), pi.data_ptr(),
                                            self.ws.data_ptr(), self.ws.numel(), _stream(stream)),
@@ -705,7 +784,7 @@ def monte_carlo(shape, S, B, t_d, seed: int, n_runs: int, n_hist: int, n_burn: i
     nr = max(0, int(n_record))
     q_rec = torch.empty((M * int(n_runs) * int(n_split), max(nr, 1)), dtype=torch.int64, device="cuda")
     t_rec = torch.empty((M * int(n_runs) * int(n_split), max(nr, 1)), dtype=torch.float64, device="cuda")
-    fa = _FluxArg(shape)
+    fa = _flux_arg(shape)
     _check(_lib().splidar_monte_carlo(C.byref(fa.s), M, S.ctypes.data, B.ctypes.data, T.ctypes.data,
                                       int(seed) & (2 ** 64 - 1), int(n_runs), int(n_split), int(n_burn), int(n_regs),
                                       int(n_cycles), int(n_hist), hist.data_ptr(), nr,
