@@ -322,7 +322,8 @@ def run_ours(args, rank, world, dev):
         "roofline": {"bound": "hbm", "kernel": GEMV_KERNELS.get(gemv_kinds[0], gemv_kinds[0]) + " (power-iteration GEMV)"
                      if len(gemv_kinds) == 1 else "+".join(gemv_kinds), "achieved": gemv_gbs,
                      "peak": hbm, "unit": "GB/s", "frac": gemv_gbs / hbm,
-                     "traffic": traffic.get("k_power_step") if traffic else None,
+                     "traffic": (traffic.get("k_power_step_i8" if gemv_kinds == ["tensor_i8"] else "k_power_step")
+                                 if traffic else None),
                      "algorithmic_bytes_per_launch": N * N * b,
                      "traffic_source": traffic.get("source") if traffic else None,
                      "peak_source": hbm_src,

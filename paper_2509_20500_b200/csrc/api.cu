@@ -269,9 +269,11 @@ const char *splidar_build_info(void) {
 static splidar_status vectors_and_build(const FluxDev *fl, int M, int N, int dt, int mode, void *P0,
                                         int64_t ld, int64_t mstride, char *ws, const WsLayout &L,
                                         cudaStream_t s) {
-    SPL_CUDA(upload_async(ws + L.flux, fl, sizeof(FluxDev) * (size_t)M, s));
+    const bool single = M == 1 && N + 1 <= kSmallVecMax;   // the profile travels in the parameters
+    if (!single) SPL_CUDA(upload_async(ws + L.flux, fl, sizeof(FluxDev) * (size_t)M, s));
     VecPtrs vp = vec_ptrs(ws, L);
-    SPL_CUDA(launch_flux_vectors(reinterpret_cast<const FluxDev *>(ws + L.flux), M, N, vp, N, s));
+    SPL_CUDA(launch_flux_vectors(reinterpret_cast<const FluxDev *>(ws + L.flux), M, N, vp, N, s,
+                                 single ? fl : nullptr));
     if (P0) SPL_CUDA(launch_build(vp, N, M, N, dt, mode, P0, ld, mstride, s));
     return SPLIDAR_OK;
 }
@@ -432,6 +434,11 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
             f.resident = fused_resident(L.N, R, dt);
             f.lsh = reinterpret_cast<const int *>(ws + L.lsh);
             f.out_idx = reinterpret_cast<const int *>(ws + L.oidx);
+            f.n_inline = (size_t)L.M * L.V <= (size_t)kFusedInline ? 1 : 0;
+            for (size_t i = 0; f.n_inline && i < p->lsh.size(); ++i) {
+                f.lsh_in[i] = p->lsh[i];
+                f.oidx_in[i] = p->out_idx[i];
+            }
             f.pi = pi;
             f.st = a.st;
             f.tol = a.tol;
@@ -741,6 +748,11 @@ static splidar_status cached_execute(const void *P0, int M, int64_t mstride, int
                 for (int m = 0; m < M; ++m)
                     for (int v = 0; v < V; ++v) plan->lsh[(size_t)m * plan->V + v] = lv[(size_t)m * V + v];
                 it->l = lv;
+                if (plan->fused && plan->fargs.n_inline) {   // small N: the shifts ride in the parameters
+                    for (size_t i = 0; i < plan->lsh.size(); ++i) plan->fargs.lsh_in[i] = plan->lsh[i];
+                    g_cache.splice(g_cache.begin(), g_cache, it);
+                    break;
+                }
                 // the workspace is scratch between calls (the caller may have used it for anything):
                 // the plan's shifts and output rows go back in with one upload per launch
                 const WsLayout &L = plan->L;

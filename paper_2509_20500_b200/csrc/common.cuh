@@ -73,8 +73,10 @@ int device_sm_count();              // SMs of the current device (cached per dev
 cudaError_t func_attrs_once(const void *fn, int max_dyn_smem, bool nonportable_cluster);
 
 // ---- kernels launch wrappers (host) -------------------------------------------------------
+// single (M = 1, N + 1 <= 8192): the profile by value, so d_flux need not be uploaded first
 cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs base, int64_t vstride,
-                                cudaStream_t s);
+                                cudaStream_t s, const FluxDev *single = nullptr);
+constexpr int kSmallVecMax = 8192;   // N + 1 <= this: the one-launch vector kernel (k_vec_small)
 cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
                          void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0 = 0, int nrows = -1);
 cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, int dtype, int l,
@@ -173,6 +175,7 @@ int struct_shape(int N, int *C, int *threads);
 cudaError_t launch_struct(int kind, const StructArgs &a, int n_units, cudaStream_t s);
 
 // ---- fused small-N dense solve (fused.cu): all iterations of one (matrix, vector) in one cluster
+constexpr int kFusedInline = 64;
 struct FusedArgs {
     const void *P;
     int64_t ld, mstride;
@@ -180,6 +183,8 @@ struct FusedArgs {
     int resident;               // rows of P~0 copied to shared memory once
     const int *lsh;             // [M][V]
     const int *out_idx;         // [M][V]
+    int n_inline;               // M V <= kFusedInline: shifts / output rows passed in the parameters
+    int lsh_in[64], oidx_in[64];
     double *pi;
     SolveState *st;             // [M][V]
     double tol;

@@ -25,6 +25,8 @@
 // prefix offsets, 4 w tile suffix offsets.
 #include <mutex>
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace spl {
@@ -339,7 +341,7 @@ __device__ double small_scan(double (&v)[kSEl], double *wt) {
 }
 
 __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ fluxes, int N, VecPtrs b,
-                                                   int64_t vstride) {
+                                                   int64_t vstride, const FluxDev single, int use_single) {
     __shared__ double wt[65];
     __shared__ FluxDev fs;               // the profile's parameters: shared-memory loads in the erfc loops
     extern __shared__ double rev[];      // [blockDim * 8]: w reversed, then its inclusive scan; then
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
     const int nslot = (int)blockDim.x * kSEl;
     double *lams = rev + nslot;
     const int m = blockIdx.x;
-    if (threadIdx.x == 0) fs = fluxes[m];
+    if (threadIdx.x == 0) fs = use_single ? single : fluxes[m];   // one profile: passed by value
     __syncthreads();
     const FluxDev &f = fs;
     const int e0 = threadIdx.x * kSEl;
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
 }  // namespace
 
 cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs base, int64_t vstride,
-                                cudaStream_t s) {
+                                cudaStream_t s, const FluxDev *single) {
     const int nt = base.ntile;                         // tiles over the N + 1 masses
     const int ntN = (N + kScanTile - 1) / kScanTile;   // tiles over the N bins
     if (nt > 4096) return cudaErrorInvalidValue;
@@ -482,7 +484,10 @@ cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs bas
         // once per device (thread-safe; not in captured launches)
         const cudaError_t attr = func_attrs_once((const void *)k_vec_small, (int)(sizeof(double) * kST * kSEl * 2), false);
         if (attr != cudaSuccess) return attr;
-        k_vec_small<<<M, threads, smem, s>>>(d_flux, N, base, vstride);
+        FluxDev one;
+        if (single) one = *single;
+        else memset(&one, 0, sizeof(one));
+        k_vec_small<<<M, threads, smem, s>>>(d_flux, N, base, vstride, one, single ? 1 : 0);
         return cudaGetLastError();
     }
     k_vec_a<<<dim3(nt, M), kT, 0, s>>>(d_flux, N, M, base, vstride);

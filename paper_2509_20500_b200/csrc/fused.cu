@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     const int mv = blockIdx.x / C;
     const int N = a.N, R = a.R;                      // rows / owned columns per CTA
     const int m = mv / a.V;
-    const int l = a.lsh[mv];
+    const int l = a.n_inline ? a.lsh_in[mv] : a.lsh[mv];
     double *xb = fsm;                                // [R]      gathered x of my rows
     double *recv = fsm + R;                          // [C][R]   partials of my columns from every CTA
     double *yp = recv + (size_t)C * R;               // [R]      previous y of my columns
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
         ++k;
     }
     // pi^k = y / s over my columns
-    const int o = a.out_idx[mv];
+    const int o = a.n_inline ? a.oidx_in[mv] : a.out_idx[mv];
     if (o >= 0) {
         const int j = c * R + (int)threadIdx.x;
         if ((int)threadIdx.x < R && j < N) a.pi[(size_t)o * N + j] = yp[threadIdx.x] / s_prev;

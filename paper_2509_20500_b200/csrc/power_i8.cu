@@ -254,8 +254,9 @@ __device__ __forceinline__ void epilogue(const PowerArgs &a, const PieceCtx &pc,
     const int row = 32 * quad + lane;                       // TMEM lane = x-slice row (q, v)
     const int q = row / VP;
     const bool live = q < kXQ;
-    double *stage = reinterpret_cast<double *>(sS);         // [2 halves][16 cols][128 rows]
+    double *stage = reinterpret_cast<double *>(sS);         // [2 halves][16 cols][SROW]
     constexpr int CW = 16;                                  // columns per chunk
+    constexpr int SROW = 129;   // odd row stride: the q-sum below reads 16 columns at once, conflict-free
     constexpr int CHUNKS = TN / 2 / CW;                     // chunks per warp (its half of the tile)
     const int64_t gN = g * kbs;
     double *part = a.part + (size_t)(b + g) * VP * TN;
@@ -274,9 +275,9 @@ __device__ __forceinline__ void epilogue(const PowerArgs &a, const PieceCtx &pc,
 #pragma unroll
             for (int i = 0; i < CW; ++i) acc[i] = fma((double)(int)r[i], w, acc[i]);
         }
-        double *st = stage + (size_t)half * CW * 128;
+        double *st = stage + (size_t)half * CW * SROW;
 #pragma unroll
-        for (int i = 0; i < CW; ++i) st[i * 128 + row] = live ? acc[i] : 0.0;
+        for (int i = 0; i < CW; ++i) st[i * SROW + row] = live ? acc[i] : 0.0;
         named_sync(2 + half, 128);
         // y partial for (v, col0 + i): sum over q (fixed order, largest slice first)
         const int t = ct & 127;
@@ -285,7 +286,7 @@ __device__ __forceinline__ void epilogue(const PowerArgs &a, const PieceCtx &pc,
             const int v = s_vmap[sl];
             double ysum = 0.0;
 #pragma unroll
-            for (int qq = 0; qq < kXQ; ++qq) ysum += st[i * 128 + qq * VP + v];
+            for (int qq = 0; qq < kXQ; ++qq) ysum += st[i * SROW + qq * VP + v];
             const int j = c * TN + col0 + i;
             const int ex = a.colexp[(size_t)m * N + j] - C::BIAS_MBITS - C::R - s_tau[v];
             part[(size_t)v * TN + col0 + i] = ldexp(ysum, ex);
