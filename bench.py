@@ -510,6 +510,9 @@ def run_spectral_dense(args, rank, world, dev):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    pinfo = plan.info()                                  # raises unless pi converged
+    if not res["l2"]["converged"]:
+        raise SystemExit("spectral_dense: lambda_2 did not converge")
     if world > 1:
         torch.distributed.barrier()
     clocks = ClockSampler(dev)
@@ -546,7 +549,11 @@ def run_spectral_dense(args, rank, world, dev):
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": hbm_src,
                      "algorithmic_bytes_per_launch": N * N * b, "lambda2_ms_per_step": statistics.mean(l2_ms)},
         "clocks": clk, "e2e": None,
-        "gpu_launches": K * ((1 + (1 if N + 1 <= 8192 else 5) + 1) + 0 + 3 * int(info["iters"]) + 1),
+        # build: (flux upload unless one small profile) + vectors + k_build; pi plan: one fused launch, or
+        # init + (GEMV + check) per iteration + finish; lambda_2: init + 3 per product
+        "gpu_launches": K * ((0 if N + 1 <= 8192 else 1) + (1 if N + 1 <= 8192 else 5) + 1
+                             + (1 if plan.fused else 2 + 2 * int(pinfo[0]["iters"]))
+                             + 1 + 3 * int(info["iters"])),
         "impl": "ours", "lib": spl.lib_path(),
     }
 

@@ -733,6 +733,22 @@ std::mutex g_cache_mu;
 std::list<CachedPlan> g_cache;   // most recently used first
 }  // namespace
 
+// Instantiated lambda_2 graphs of earlier calls, keyed by everything baked into their kernel
+// parameters (device, matrix, sizes, shift, pi, tolerances, workspace); LRU of 8, cleared with the
+// plan cache. A repeated call replays the graph instead of building and instantiating it again.
+namespace {
+struct SdCached {
+    int dev, dt;
+    SdArgs a;
+    cudaGraphExec_t x;
+};
+std::list<SdCached> g_sd_cache;
+bool sd_same(const SdArgs &u, const SdArgs &v) {
+    return u.p.P == v.p.P && u.p.ld == v.p.ld && u.p.N == v.p.N && u.p.y == v.p.y && u.l == v.l && u.pi == v.pi &&
+           u.tol == v.tol && u.max_iter == v.max_iter && u.sd == v.sd && u.part == v.part;
+}
+}  // namespace
+
 static splidar_status cached_execute(const void *P0, int M, int64_t mstride, int N, int64_t ld, int dt,
                                      const int *l, int V, double tol, int max_iter, double *pi, void *ws,
                                      size_t ws_bytes, splidar_solve_info *info, cudaStream_t s,
@@ -788,6 +804,8 @@ void splidar_plan_cache_clear(void) {
     std::lock_guard<std::mutex> lock(g_cache_mu);
     for (auto &c : g_cache) splidar_plan_destroy(c.plan);
     g_cache.clear();
+    for (auto &c : g_sd_cache) cudaGraphExecDestroy(c.x);
+    g_sd_cache.clear();
 }
 
 splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r,
@@ -921,6 +939,26 @@ size_t splidar_spectral_dense_workspace_bytes(int32_t n_bins) {
     return ws_layout(n_bins, 1, 2).total + sd_extra(n_bins, &a, &b, &c, &d);
 }
 
+static cudaGraphExec_t sd_cache_find(const SdArgs &a, int dt) {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    const int dev = current_device();
+    for (auto it = g_sd_cache.begin(); it != g_sd_cache.end(); ++it)
+        if (it->dev == dev && it->dt == dt && sd_same(it->a, a)) {
+            g_sd_cache.splice(g_sd_cache.begin(), g_sd_cache, it);
+            return it->x;
+        }
+    return nullptr;
+}
+
+static void sd_cache_put(const SdArgs &a, int dt, cudaGraphExec_t x) {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    g_sd_cache.push_front(SdCached{current_device(), dt, a, x});
+    while (g_sd_cache.size() > 8) {
+        cudaGraphExecDestroy(g_sd_cache.back().x);
+        g_sd_cache.pop_back();
+    }
+}
+
 splidar_status splidar_second_eigenvalue_dense(const void *P0, int32_t n_bins, int64_t ld, splidar_dtype dt,
                                                double t_r, double t_d, const double *pi, double tol,
                                                int32_t max_iter, void *ws, size_t ws_bytes,
@@ -995,6 +1033,8 @@ splidar_status splidar_second_eigenvalue_dense(const void *P0, int32_t n_bins, i
             SPL_CUDA(cudaStreamSynchronize(s));
             if (h.done) break;
         }
+    } else if (cudaGraphExec_t cx = sd_cache_find(a, dt)) {   // the same call before: replay its graph
+        SPL_CUDA(cudaGraphLaunch(cx, s));
     } else {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t x = nullptr;
@@ -1038,10 +1078,11 @@ splidar_status splidar_second_eigenvalue_dense(const void *P0, int32_t n_bins, i
             kp.gridDim = q.update_grid;
             if ((err = cudaGraphAddKernelNode(&n_upd, body, &n_dots, 1, &kp))) break;
             if ((err = cudaGraphInstantiate(&x, g, 0))) break;
-            if (!(err = cudaGraphLaunch(x, s))) err = cudaStreamSynchronize(s);   // before destroying
+            err = cudaGraphLaunch(x, s);
         } while (0);
-        if (x) cudaGraphExecDestroy(x);
         if (g) cudaGraphDestroy(g);
+        if (err == cudaSuccess) sd_cache_put(a, dt, x);   // kept for the next identical call
+        else if (x) cudaGraphExecDestroy(x);
         SPL_CUDA(err);
     }
     SdState h;
