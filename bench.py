@@ -274,9 +274,10 @@ def run_ours(args, rank, world, dev):
         per_m = np.array([i["iters"] for i in plan_info]).reshape(p.M, p.V).max(axis=1)
         launches_gemv += int(per_m.max())
         gemv_bytes += int(per_m.sum()) * N * N * b
-    # parameter upload + step-1 vector kernels (k_vec_small when N + 1 <= 8192, else k_vec_a..e) +
-    # k_build, then per plan: one fused launch, or init + (GEMV + check) per iteration + finish
-    prelude = 1 + (1 if N + 1 <= 8192 else 5) + 1
+    # parameter upload (none for one small profile, passed by value) + step-1 vector kernels (k_vec_small
+    # when N + 1 <= 8192, else k_vec_a..e) + k_build, then per plan: one fused launch, or init + (GEMV + check) per iteration + finish
+    small = N + 1 <= 8192
+    prelude = (0 if small and len(st.fluxes) == 1 else 1) + (1 if small else 5) + 1
     if graphed:
         per_step_launches = prelude + len(st.plans)
     else:
