@@ -424,6 +424,40 @@ def test_p10_mc_constant_flux_uniform(oracle_lib):
     assert np.all(np.abs(m - 1.0 / 16) <= 4.5 * se)
 
 
+def test_p10_mc_timestamps_dead_time_and_renewal(oracle_lib):
+    """One chain's registrations (the stream the GPU Monte Carlo is replayed against): offsets in
+    [0, t_r), absolute times T = q t_r + t strictly increasing with every gap >= t_d (the SPAD is dead
+    for t_d after each registration), and at constant flux (S = 0, rate B / t_r) the gaps are
+    t_d + Exp(B / t_r): mean t_d + t_r / B and variance (t_r / B)^2 within 5 standard errors (renewal
+    process, S:326)."""
+    f = Flux(100.0, 16, (40.0,), (5.0,), (0.0,), 2.0)
+    td = 37.5
+    q, t = oracle.mc_timestamps(f, td, 99, 200000)
+    assert np.all((t >= 0.0) & (t < f.t_r))
+    T = q.astype(np.float64) * f.t_r + t
+    gaps = np.diff(T)
+    assert np.all(gaps >= td * (1 - 1e-12))
+    mean_exp, n = f.t_r / f.background, gaps.size
+    assert abs(gaps.mean() - (td + mean_exp)) <= 5 * mean_exp / math.sqrt(n)
+    assert abs(gaps.var() - mean_exp ** 2) <= 5 * mean_exp ** 2 * math.sqrt(8.0 / n)   # Var(X^2) = 8 m^4 - m^4
+    g = config(1).items[0].flux                         # a pulsed flux: the gating holds there too
+    q, t = oracle.mc_timestamps(g, 75.0, 7, 20000)
+    assert np.all(np.diff(q.astype(np.float64) * g.t_r + t) >= 75.0 * (1 - 1e-12))
+
+
+def test_p14_left_matvec(oracle_lib):
+    """oracle.left_matvec (the product inside stationary_power and the CPU baseline's timing) equals
+    the extended-precision library product x @ rows, and e_i picks row i."""
+    rng = np.random.default_rng(14)
+    rows = rng.uniform(0.0, 1.0, (300, 77))
+    x = rng.uniform(0.0, 1.0, 300)
+    want = (x.astype(np.longdouble) @ rows.astype(np.longdouble)).astype(np.float64)
+    assert np.max(np.abs(oracle.left_matvec(rows, x) - want) / want) <= 2.3e-16
+    e = np.zeros(300)
+    e[123] = 1.0
+    assert np.array_equal(oracle.left_matvec(rows, e), rows[123])
+
+
 @pytest.mark.parametrize("td", [75.0, 130.0])
 def test_p10_mc_vs_chain(oracle_lib, td):
     """The chain's pi (fine N, aggregated to 16 comparison bins) against the continuous-time MC
