@@ -28,8 +28,8 @@
 //               of x slices, N = 256 columns (2 fp32 / 4 fp64 byte planes side by side), K = 32;
 //               D_p in TMEM columns [p TN, (p+1) TN);
 //   warp 2      TMEM allocator;
-//   warps 4-11  converters: each unit's tile -> NP byte planes in the canonical MN-major layout
-//               (byte transposes with PRMT); shared-memory bandwidth (TMA write, converter read and
+//   warps 4-11  converters: each unit's tile -> its scaled integers in the canonical MN-major layout
+//               (the tensor core reads every byte as its own u8 column: no transposes); shared-memory bandwidth (TMA write, converter read and
 //               write, MMA operand reads: ~152 KB per 32 KB unit) is the budget the layout is cut
 //               for -- N = 256 MMAs read the x slices once per 2 (fp32) / 4 (fp64) planes. At the
 //               end of a piece the epilogue:
@@ -80,23 +80,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 __device__ __forceinline__ void named_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
-    uint32_t r;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(s));
-    return r;
-}
-// 4 x 32-bit words -> 4 byte planes: out[k] = byte k of (w0, w1, w2, w3) (w0 in the low byte)
-__device__ __forceinline__ void transpose4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&o)[4]) {
-    const uint32_t t0 = prmt(w0, w1, 0x5140), t1 = prmt(w2, w3, 0x5140);   // b0: w0 w1 | b1: w0 w1
-    const uint32_t t2 = prmt(w0, w1, 0x7362), t3 = prmt(w2, w3, 0x7362);   // b2 | b3
-    o[0] = prmt(t0, t1, 0x5410);
-    o[1] = prmt(t0, t1, 0x7632);
-    o[2] = prmt(t2, t3, 0x5410);
-    o[3] = prmt(t2, t3, 0x7632);
-}
-
-// Scaled integer of one entry: mantissa << (e - base); zero stays zero (the range test guarantees
-// 0 <= e - base <= R for every non-zero entry when the plan runs this kernel).
 // PTX shl clamps the shift amount to the register width, so a zero entry (e = 0, shift e - base
 // < 0, i.e. huge as unsigned) gives 0 without a select; k_i8_colexp guarantees base > 0 for every
 // column with a non-zero entry and sets E_j = 255 / 2047 (base > 0 as well) for all-zero columns.
@@ -170,54 +153,36 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 }
 
 template <typename T>
-__device__ __forceinline__ void convert_item(const unsigned char *tile, unsigned char *splanes, int r, int jb,
+__device__ __forceinline__ void convert_item(const unsigned char *tile, unsigned char *sw_img, int r, int jb,
                                              const int (&base)[16]) {
-    using C = I8Cfg<T>;
-    constexpr int CB = C::TN / 16;
-    unsigned char *dst = splanes + (r >> 3) * kKGroup + jb * 128 + (r & 7) * 16;   // plane p: + p * CB * 128
+    // the 16 scaled integers of row r, columns 16 jb .. 16 jb + 15, little-endian, as they are:
+    // byte n = sizeof(T) j + p of the MMA's B row is byte p of column j (4 / 8 core-matrix rows of
+    // 16 bytes; the 8 rows r % 8 of one core matrix are 8 consecutive lanes: conflict-free stores)
+    constexpr int W = sizeof(T);                     // bytes (planes) per entry
+    unsigned char *dst = sw_img + (r >> 3) * kKGroup + jb * W * 128 + (r & 7) * 16;
     const int sw = r & 7;
     if constexpr (sizeof(T) == 4) {
         // columns 16 jb .. 16 jb + 15: box jb / 2, chunks 4 (jb % 2) .. + 3
         const unsigned char *row = tile + (jb >> 1) * kBoxBytes + r * 128;
         const int c0 = (jb & 1) * 4;
-        uint32_t pw[4][4];                              // [byte k][word g]
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
             const uint4 v = *reinterpret_cast<const uint4 *>(row + (((c0 + g) ^ sw) << 4));
-            uint32_t o[4];
-            transpose4(fx32(v.x, base[4 * g]), fx32(v.y, base[4 * g + 1]), fx32(v.z, base[4 * g + 2]),
-                       fx32(v.w, base[4 * g + 3]), o);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) pw[k][g] = o[k];
+            *reinterpret_cast<uint4 *>(dst + g * 128) =
+                make_uint4(fx32(v.x, base[4 * g]), fx32(v.y, base[4 * g + 1]), fx32(v.z, base[4 * g + 2]),
+                           fx32(v.w, base[4 * g + 3]));
         }
-#pragma unroll
-        for (int p = 0; p < 4; ++p)                    // plane p = byte 3 - p
-            *reinterpret_cast<uint4 *>(dst + p * CB * 128) = make_uint4(pw[3 - p][0], pw[3 - p][1], pw[3 - p][2], pw[3 - p][3]);
     } else {
-        // columns 16 jb .. 16 jb + 15: box jb, chunks 0 .. 7
+        // columns 16 jb .. 16 jb + 15: box jb, chunks 0 .. 7 (2 entries each)
         const unsigned char *row = tile + jb * kBoxBytes + r * 128;
-        uint32_t pw[8][4];                              // [byte k][word g]
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {                   // 4 entries per word group
-            const uint4 v0 = *reinterpret_cast<const uint4 *>(row + (((2 * g) ^ sw) << 4));
-            const uint4 v1 = *reinterpret_cast<const uint4 *>(row + (((2 * g + 1) ^ sw) << 4));
-            uint32_t l0, h0, l1, h1, l2, h2, l3, h3;
-            fx64(v0.x, v0.y, base[4 * g], l0, h0);
-            fx64(v0.z, v0.w, base[4 * g + 1], l1, h1);
-            fx64(v1.x, v1.y, base[4 * g + 2], l2, h2);
-            fx64(v1.z, v1.w, base[4 * g + 3], l3, h3);
-            uint32_t lo[4], hi[4];
-            transpose4(l0, l1, l2, l3, lo);
-            transpose4(h0, h1, h2, h3, hi);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                pw[k][g] = lo[k];
-                pw[4 + k][g] = hi[k];
-            }
+        for (int g = 0; g < 8; ++g) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(row + ((g ^ sw) << 4));
+            uint4 o;
+            fx64(v.x, v.y, base[2 * g], o.x, o.y);
+            fx64(v.z, v.w, base[2 * g + 1], o.z, o.w);
+            *reinterpret_cast<uint4 *>(dst + g * 128) = o;
         }
-#pragma unroll
-        for (int p = 0; p < 8; ++p)                    // plane p = byte 7 - p
-            *reinterpret_cast<uint4 *>(dst + p * CB * 128) = make_uint4(pw[7 - p][0], pw[7 - p][1], pw[7 - p][2], pw[7 - p][3]);
     }
 }
 
@@ -263,17 +228,21 @@ __device__ __forceinline__ void epilogue(const PowerArgs &a, const PieceCtx &pc,
     const int nact = *s_nact;
     for (int ch = 0; ch < CHUNKS; ++ch) {
         const int col0 = half * (TN / 2) + ch * CW;
+        // D column n = NP j + p holds byte p (weight 2^(8 p)) of column j's scaled integers
         double acc[CW];
+        const double wq = ldexp(1.0, 8 * (kXQ - 1 - (live ? q : 0)));
 #pragma unroll
-        for (int i = 0; i < CW; ++i) acc[i] = 0.0;
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            uint32_t r[CW];
-            tc05::ld32x16(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(p * TN + col0), r);
+        for (int c4 = 0; c4 < CW * NP / 16; ++c4) {
+            uint32_t r[16];
+            tc05::ld32x16(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(NP * col0 + 16 * c4), r);
             tc05::wait_ld();
-            const double w = ldexp(1.0, 8 * (NP - 1 - p) + 8 * (kXQ - 1 - (live ? q : 0)));
 #pragma unroll
-            for (int i = 0; i < CW; ++i) acc[i] = fma((double)(int)r[i], w, acc[i]);
+            for (int e = 0; e < 16 / NP; ++e) {
+                double t = 0.0;
+#pragma unroll
+                for (int p = NP - 1; p >= 0; --p) t = fma((double)(int)r[e * NP + p], ldexp(1.0, 8 * p), t);
+                acc[c4 * (16 / NP) + e] = t * wq;
+            }
         }
         double *st = stage + (size_t)half * CW * SROW;
 #pragma unroll
