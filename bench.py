@@ -161,20 +161,21 @@ class OurStep:
         self.P0 = spl.empty_matrix(self.N, self.dt, n_matrices=M)
         self.ws_build = spl.workspace(self.N, M, 1)
         self.plans = []
+        # building plans: every launch runs steps 1-2 for its matrices and the power iteration, the
+        # first product taken from the build's column sums (include/splidar.h: splidar_plan_create_build)
         if len(groups) == M and all(len(t) == 1 for _, t in groups):
             # one dead time per matrix (c1-c4): one plan over all M matrices
             tds = np.array([[t[0]] for _, t in groups])
-            self.plans.append(spl.Plan(self.P0, fl[0].t_r, tds, tol=1e-12))
+            self.plans.append(spl.Plan(self.P0, fl[0].t_r, tds, tol=1e-12, build=fl, mode=mode))
         else:                    # c5: dead-time groups sharing a matrix, one multi-vector plan each
             for f, tds in groups:
                 m = fl.index(f)
-                self.plans.append(spl.Plan(self.P0[m], f.t_r, np.array([tds]), tol=1e-12))
+                self.plans.append(spl.Plan(self.P0[m], f.t_r, np.array([tds]), tol=1e-12, build=[f], mode=mode))
         self.n_solves = sum(len(t) for _, t in groups)
         self.entries = M * self.N * self.N
 
     def step(self):
-        self.build()
-        self.solve()
+        self.solve()             # the plans build their matrices
 
     def capture(self):
         """Small N (every plan fused = single launches): the whole step captured once as a CUDA graph and
@@ -220,8 +221,7 @@ def run_ours(args, rank, world, dev):
         if graphed:
             st.graph.replay()
         else:
-            st.build()
-            st.solve()
+            st.step()
     torch.cuda.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -235,31 +235,31 @@ def run_ours(args, rank, world, dev):
         e0.record(stream)
         if graphed:                      # one replay = build + solve; the split is not observable
             st.graph.replay()
-        else:
-            st.build()
-            e1.record(stream)
-            st.solve()
+        else:                            # one launch per plan = build + solve (building plans)
+            st.step()
         e2.record(stream)
     torch.cuda.synchronize()
-    if graphed:                          # build share: replays of the build-only graph (build roofline)
+    # build share (build roofline): the same builds alone, timed after the steps
+    if graphed:
         st.graph_build.replay()
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        b0.record(stream)
-        for _ in range(len(ev)):
+    else:
+        st.build()
+    b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b0.record(stream)
+    for _ in range(len(ev)):
+        if graphed:
             st.graph_build.replay()
-        b1.record(stream)
-        torch.cuda.synchronize()
-        t_b = b0.elapsed_time(b1) / 1e3 / len(ev)
+        else:
+            st.build()
+    b1.record(stream)
+    torch.cuda.synchronize()
+    t_b = b0.elapsed_time(b1) / 1e3 / len(ev)
     if world > 1:
         torch.distributed.barrier()
     clk = clocks.stop()
     t_total = sum(a.elapsed_time(c) for a, _, c in ev) / 1e3
-    if graphed:
-        t_build = min(t_b * len(ev), t_total)
-        t_solve = t_total - t_build
-    else:
-        t_build = sum(a.elapsed_time(b) for a, b, _ in ev) / 1e3
-        t_solve = sum(b.elapsed_time(c) for _, b, c in ev) / 1e3
+    t_build = min(t_b * len(ev), t_total)
+    t_solve = t_total - t_build
     infos = st.infos()
     gemv_kinds = sorted({p.gemv() for p in st.plans})
     from paper_2509_20500_b200.shard import max_over_ranks
@@ -269,9 +269,12 @@ def run_ours(args, rank, world, dev):
     N = st.N
     # algorithmic GEMV bytes: every launch reads each still-active matrix once (N^2 b); launches =
     # iterations of the longest vector in each plan; matrices whose vectors all converged are skipped
+    # (a building graph plan takes iteration 1 from the build's column sums: one GEMV launch fewer)
     launches_gemv, gemv_bytes = 0, 0
     for plan_info, p in zip(infos, st.plans):
         per_m = np.array([i["iters"] for i in plan_info]).reshape(p.M, p.V).max(axis=1)
+        if not p.fused:
+            per_m = np.maximum(per_m - 1, 0)
         launches_gemv += int(per_m.max())
         gemv_bytes += int(per_m.sum()) * N * N * b
     # parameter upload (none for one small profile, passed by value) + step-1 vector kernels (k_vec_small
@@ -283,9 +286,13 @@ def run_ours(args, rank, world, dev):
     else:
         # graph plans: init + finish, and per iteration GEMV + check; int8 plans add the range test
         # (prep, column exponents, column check) and per iteration the FP64 GEMV's early exit
+        # building graph plans: the build (prelude) + column-sum reduce, init, ssum + check (iteration 1),
+        # then per further iteration GEMV + check, finish; int8 plans add the range test (3) and the
+        # FP64 GEMV's early exit per iteration
         def plan_launches(pi, p):
             it = int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
-            return 2 + 2 * it if p.gemv() != "tensor_i8" else 5 + 3 * it
+            n = 1 + 1 + 2 + 2 * (it - 1) + 1
+            return n if p.gemv() != "tensor_i8" else n + 3 + (it - 1)
         per_step_launches = prelude + sum(plan_launches(pi, p) for pi, p in zip(infos, st.plans))
     hbm, hbm_src = load_peaks()
     traffic = load_traffic(args.workload, args.dtype)
@@ -341,9 +348,9 @@ def run_ours(args, rank, world, dev):
 
 
 def run_e2e(args, w, groups, st, world):
-    """Same metric through the public one-shot calls a user makes, with host buffers: theta from the
-    host (build_base / build_base_batched), spl.stationary_multi (the library replays its cached
-    solver for repeated calls with the same buffers), pi copied to pinned host memory, every step."""
+    """Same metric through the public Plan API a user re-solving with new parameters makes, with host
+    buffers: theta from the host every step (Plan.set_fluxes), the building plan's launch (build +
+    solve), pi copied to pinned host memory and Plan.info's one synchronisation."""
     import torch
     import paper_2509_20500_b200 as spl
     N = st.N
@@ -354,18 +361,20 @@ def run_e2e(args, w, groups, st, world):
     for f, tds in groups:
         h2d += 8 * (3 * len(f.tau) + 3) + 8 * len(tds)
     one_per_matrix = len(groups) == len(st.fluxes) and all(len(t) == 1 for _, t in groups)
-    T = np.array([[t[0]] for _, t in groups]) if one_per_matrix else None
 
     def one():
-        st.build()
-        if one_per_matrix:
-            spl.stationary_multi(st.P0, groups[0][0].t_r, T, tol=1e-12, out_host=pi_host)
-        else:
-            row = 0
-            for f, tds in groups:
-                spl.stationary_multi(st.P0[st.fluxes.index(f)], f.t_r, np.array([tds]), tol=1e-12,
-                                     out_host=pi_host[row:row + len(tds)])
-                row += len(tds)
+        # theta host -> device every step (set_fluxes), build + solve (one launch per plan), pi to
+        # pinned host memory, one synchronisation (Plan.info)
+        row = 0
+        for p in st.plans:
+            fl = st.fluxes if one_per_matrix else [st.fluxes[st.plans.index(p)]]
+            p.set_fluxes(fl)
+            p.launch()
+            n = p.M * p.V
+            pi_host[row:row + n].copy_(p.pi.reshape(n, N), non_blocking=True)
+            row += n
+        for p in st.plans:
+            p.info()
 
     for _ in range(max(1, args.warmup)):
         one()
@@ -381,8 +390,8 @@ def run_e2e(args, w, groups, st, world):
     dt_s = max_over_ranks([dt_s], device="cuda")[0]
     return {"value": n_solves * args.steps * world / dt_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": n_solves * N * 8,
-            "note": "host wall clock; public one-shot calls (build_base, stationary_multi) with the theta upload "
-                    "and the pi copy to pinned host memory every step"}
+            "note": "host wall clock; the public Plan API (set_fluxes: theta to the device, launch: build + solve, "
+                    "pi copied to pinned host memory, info: one synchronisation) every step"}
 
 
 # ------------------------------------------------------------------------------- row shards (8(e)(ii))

@@ -201,6 +201,23 @@ splidar_status splidar_plan_create(splidar_plan *plan, const void *P0, int32_t n
                                    void *stream);
 splidar_status splidar_plan_execute(splidar_plan plan, splidar_solve_info *info /* host [M*V] */,
                                     void *stream);
+/* A plan that also BUILDS its matrices: every launch runs steps 1-2 (flux vectors, entries of
+ * P~0 for fluxes[m] into P0 + m * matrix_stride, as splidar_build_base_batched) and then the power
+ * iteration. The build also sums the stored entries of every column: from the uniform start the
+ * first product is x^0 P~ = (1/N) 1^T J_l P~0 = (1/N) 1^T P~0 -- the row permutation leaves column
+ * sums unchanged (Thm 2) -- so iteration 1 of every dead time comes from those sums and the
+ * GEMV passes start at iteration 2 (one matrix pass fewer per solve; same iterates up to the order
+ * of the column sums). All fluxes share N and t_r. ws: splidar_workspace_bytes(N, n_matrices,
+ * n_vectors); otherwise as splidar_plan_create. */
+splidar_status splidar_plan_create_build(splidar_plan *plan, const splidar_flux *fluxes, int32_t n_matrices,
+                                         splidar_entry mode, splidar_dtype dt, void *P0, int64_t matrix_stride,
+                                         int64_t ld, const double *t_d, int32_t n_vectors, double tol,
+                                         int32_t max_iter, double *pi, void *ws, size_t ws_bytes,
+                                         void *stream);
+/* New flux parameters for a building plan's next launches (same N, same t_r as at creation, the same
+ * number of matrices); enqueued on stream (a small upload), EINVAL otherwise. The dead times stay. */
+splidar_status splidar_plan_set_fluxes(splidar_plan plan, const splidar_flux *fluxes, int32_t n_matrices,
+                                       void *stream);
 /* As execute, but only enqueues (async); read results later with splidar_plan_info. */
 splidar_status splidar_plan_launch(splidar_plan plan, void *stream);
 splidar_status splidar_plan_info(splidar_plan plan, splidar_solve_info *info, void *stream);

@@ -60,6 +60,9 @@ WsLayout ws_layout(int N, int M, int V) {
     L.colmin = o; o = a256(o + sizeof(int) * (size_t)M * N);
     L.smax = o; o = a256(o + sizeof(double) * MV * tiles64);
     L.xtau = o; o = a256(o + sizeof(int) * MV);
+    // plans that build their matrix: the build's partial column sums and the column sums (iteration 1)
+    L.cpart = o; o = a256(o + sizeof(double) * (size_t)M * kColsumChunks * N);
+    L.csum = o; o = a256(o + sizeof(double) * (size_t)M * N);
     L.total = o;
     return L;
 }
@@ -372,11 +375,44 @@ struct splidar_plan_s {
     FusedArgs fargs;
     I8Kernels q;       // int8 tensor-core GEMV (args.i8)
     bool shard = false;   // row shard (splidar_plan_create_rows): stepped by the caller
+    // plans that build their matrices (splidar_plan_create_build): steps 1-2 run inside every launch,
+    // and the build also reduces the column sums of the stored entries = the first power-iteration
+    // product from the uniform start, shared by every dead time of a matrix (x^0 = 1/N is invariant
+    // under the row permutation J_l): the solve starts at iteration 1 without a GEMV pass
+    bool with_build = false;
+    int bmode = 0;
+    std::vector<FluxDev> bflux;
+    char *ws = nullptr;
 };
+
+// Enqueue steps 1-2 of a building plan (flux vectors, entries + column sums) on s.
+static cudaError_t plan_enqueue_build(const splidar_plan_s *p, int dt, cudaStream_t s) {
+    const WsLayout &L = p->L;
+    const int M = p->M, N = L.N;
+    VecPtrs vp;
+    {
+        double *b = reinterpret_cast<double *>(p->ws + L.vec);
+        const size_t MN = (size_t)L.M * L.N;
+        vp.F = b; vp.lam = b + MN; vp.w = b + 2 * MN; vp.invD = b + 3 * MN; vp.invZ = b + 4 * MN;
+        vp.scal = b + 5 * MN;
+        vp.ntile = (L.N + 1 + kScanTile - 1) / kScanTile;
+        vp.tiles = vp.scal + (size_t)L.M * 8;
+    }
+    // the fluxes are read from the plan's workspace (splidar_plan_set_fluxes replaces them there)
+    cudaError_t e = launch_flux_vectors(reinterpret_cast<const FluxDev *>(p->ws + L.flux), M, N, vp, N, s, nullptr);
+    if (e != cudaSuccess) return e;
+    return launch_build(vp, N, M, N, dt, p->bmode, const_cast<void *>(p->args.P), p->args.ld, p->args.mstride, s, 0,
+                        N, p->fused ? nullptr : reinterpret_cast<double *>(p->ws + L.cpart),
+                        p->fused ? nullptr : reinterpret_cast<double *>(p->ws + L.csum));
+}
 
 static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws, cudaStream_t s) {
     const WsLayout &L = p->L;
     PowerArgs &a = p->args;
+    p->ws = ws;
+    p->dt = dt;
+    if (p->with_build)   // the fluxes stay in the plan's workspace
+        SPL_CUDA(spl::upload_async(ws + L.flux, p->bflux.data(), sizeof(FluxDev) * p->bflux.size(), s));
     a.y = reinterpret_cast<double *>(ws + L.y);
     a.X = reinterpret_cast<double *>(ws + L.X);
     a.part = reinterpret_cast<double *>(ws + L.part);
@@ -477,6 +513,21 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     memset(&kp, 0, sizeof(kp));
     void *init_args[] = {&a};
     cudaGraphNode_t n_init, n_while, n_step, n_fin, n_prev = nullptr;
+    if (p->with_build) {   // steps 1-2 as a child graph captured from the same launch code
+        cudaStream_t cs;
+        SPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t bg = nullptr;
+        cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            const cudaError_t eb = plan_enqueue_build(p, dt, cs);
+            e = cudaStreamEndCapture(cs, &bg);
+            if (e == cudaSuccess) e = eb;
+        }
+        if (e == cudaSuccess) e = cudaGraphAddChildGraphNode(&n_prev, p->graph, nullptr, 0, bg);
+        if (bg) cudaGraphDestroy(bg);
+        cudaStreamDestroy(cs);
+        SPL_CUDA(e);
+    }
     int rows_per_cta = q.rows_per_cta;
     void *colexp_args[] = {&a, &rows_per_cta};
     if (a.i8) {   // range test of the stored matrix: flag = 1, then every column may clear it
@@ -485,7 +536,7 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
         kp.gridDim = q.small_grid;
         kp.blockDim = dim3(256);
         kp.kernelParams = init_args;
-        SPL_CUDA(cudaGraphAddKernelNode(&n_prep, p->graph, nullptr, 0, &kp));
+        SPL_CUDA(cudaGraphAddKernelNode(&n_prep, p->graph, n_prev ? &n_prev : nullptr, n_prev ? 1 : 0, &kp));
         kp.func = q.colexp_fn;
         kp.gridDim = q.colexp_grid;
         kp.blockDim = q.colexp_block;
@@ -503,13 +554,32 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     kp.blockDim = k.init_block;
     kp.kernelParams = init_args;
     SPL_CUDA(cudaGraphAddKernelNode(&n_init, p->graph, n_prev ? &n_prev : nullptr, n_prev ? 1 : 0, &kp));
+    cudaGraphNode_t n_loop_dep = n_init;
+    PowerArgs ac = a;      // iteration 1 from the build's column sums (no GEMV pass)
+    if (p->with_build) {
+        ac.ypart = reinterpret_cast<double *>(ws + L.csum);
+        ac.ypart_shared = 1;
+        void *cargs[] = {&ac};
+        cudaGraphNode_t n_ss, n_ck;
+        kp.func = k.ssum_fn;
+        kp.gridDim = dim3((unsigned)(L.strips > a.strips_i8 ? L.strips : a.strips_i8), (unsigned)(L.M * L.V));
+        kp.blockDim = dim3(256);
+        kp.sharedMemBytes = 0;
+        kp.kernelParams = cargs;
+        SPL_CUDA(cudaGraphAddKernelNode(&n_ss, p->graph, &n_init, 1, &kp));
+        kp.func = k.check_fn;
+        kp.gridDim = k.check_grid;
+        kp.blockDim = k.check_block;
+        SPL_CUDA(cudaGraphAddKernelNode(&n_ck, p->graph, &n_ss, 1, &kp));
+        n_loop_dep = n_ck;
+    }
 
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = h;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
-    SPL_CUDA(cudaGraphAddNode(&n_while, p->graph, &n_init, 1, &cp));
+    SPL_CUDA(cudaGraphAddNode(&n_while, p->graph, &n_loop_dep, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
 
     void *step_args[] = {&a};
@@ -565,7 +635,8 @@ void splidar_plan_destroy(splidar_plan plan) {
 static splidar_status plan_create_l(splidar_plan *out, const void *P0, int M, int64_t mstride, int N, int64_t ld,
                                     int dt, const int *l, int V, double tol, int max_iter, double *pi,
                                     const int *out_idx, void *ws, size_t ws_bytes, cudaStream_t s,
-                                    int row0 = 0, int n_rows = -1, double *ypart = nullptr) {
+                                    int row0 = 0, int n_rows = -1, double *ypart = nullptr,
+                                    const FluxDev *bflux = nullptr, int bmode = 0) {
     *out = nullptr;
     splidar_status st;
     if ((st = check_matrix(P0, N, ld, dt))) return st;
@@ -592,6 +663,11 @@ static splidar_status plan_create_l(splidar_plan *out, const void *P0, int M, in
     p->args.mstride = mstride;
     p->args.tol = tol;
     p->args.max_iter = max_iter;
+    if (bflux) {
+        p->with_build = true;
+        p->bmode = bmode;
+        p->bflux.assign(bflux, bflux + M);
+    }
     if (n_rows >= 0) {
         p->shard = true;
         p->args.rows = n_rows;
@@ -622,11 +698,52 @@ splidar_status splidar_plan_create(splidar_plan *plan, const void *P0, int32_t n
                          pi, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+splidar_status splidar_plan_create_build(splidar_plan *plan, const splidar_flux *fluxes, int32_t n_matrices,
+                                         splidar_entry mode, splidar_dtype dt, void *P0, int64_t matrix_stride,
+                                         int64_t ld, const double *t_d, int32_t n_vectors, double tol,
+                                         int32_t max_iter, double *pi, void *ws, size_t ws_bytes, void *stream) {
+    if (!plan || !fluxes || !t_d || n_matrices < 1 || n_matrices > 65535 || n_vectors < 1 ||
+        n_vectors > kMaxVectors)
+        return SPLIDAR_EINVAL;
+    if (mode != SPLIDAR_ENTRY_FACTORED && mode != SPLIDAR_ENTRY_EXP) return SPLIDAR_EINVAL;
+    const int N = fluxes[0].n_bins;
+    splidar_status st;
+    std::vector<FluxDev> d((size_t)n_matrices);
+    for (int m = 0; m < n_matrices; ++m) {
+        if ((st = check_flux(&fluxes[m], N))) return st;
+        if (fluxes[m].t_r != fluxes[0].t_r) return SPLIDAR_EINVAL;     // one shift rule per plan
+        d[(size_t)m] = to_dev(&fluxes[m]);
+    }
+    std::vector<int> l((size_t)n_matrices * n_vectors);
+    for (size_t i = 0; i < l.size(); ++i) {
+        int32_t li;
+        if ((st = splidar_shift(fluxes[0].t_r, N, t_d[i], &li))) return st;
+        l[i] = li;
+    }
+    return plan_create_l(plan, P0, n_matrices, n_matrices > 1 ? matrix_stride : (int64_t)N * ld, N, ld, dt, l.data(),
+                         n_vectors, tol, max_iter, pi, nullptr, ws, ws_bytes, (cudaStream_t)stream, 0, -1, nullptr,
+                         d.data(), mode);
+}
+
+splidar_status splidar_plan_set_fluxes(splidar_plan plan, const splidar_flux *fluxes, int32_t n_matrices,
+                                       void *stream) {
+    if (!plan || !plan->with_build || !fluxes || n_matrices != plan->M) return SPLIDAR_EINVAL;
+    splidar_status st;
+    for (int m = 0; m < n_matrices; ++m) {
+        if ((st = check_flux(&fluxes[m], plan->L.N))) return st;
+        if (fluxes[m].t_r != fluxes[0].t_r) return SPLIDAR_EINVAL;
+        plan->bflux[(size_t)m] = to_dev(&fluxes[m]);
+    }
+    return cuda_status(spl::upload_async(plan->ws + plan->L.flux, plan->bflux.data(),
+                                         sizeof(FluxDev) * plan->bflux.size(), (cudaStream_t)stream));
+}
+
 static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
     if (!p->host_flag) SPL_CUDA(cudaMallocHost(&p->host_flag, sizeof(unsigned)));
     const SolverKernels &k = p->k;
     const I8Kernels &q = p->q;
     void *args[] = {&p->eager_args};
+    if (p->with_build) SPL_CUDA(plan_enqueue_build(p, p->dt, s));
     if (p->args.i8) {
         int rpc = q.rows_per_cta;
         void *cargs[] = {&p->eager_args, &rpc};
@@ -635,8 +752,21 @@ static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
         SPL_CUDA(cudaLaunchKernel(q.check_fn, q.small_grid, dim3(256), args, 0, s));
     }
     SPL_CUDA(cudaLaunchKernel(k.init_fn, k.init_grid, k.init_block, args, 0, s));
+    bool more = true;
+    if (p->with_build) {   // iteration 1 from the build's column sums
+        PowerArgs ac = p->eager_args;
+        ac.ypart = reinterpret_cast<double *>(p->ws + p->L.csum);
+        ac.ypart_shared = 1;
+        void *cargs[] = {&ac};
+        const dim3 sgrid((unsigned)(p->L.strips > ac.strips_i8 ? p->L.strips : ac.strips_i8), (unsigned)(p->M * p->V));
+        SPL_CUDA(cudaLaunchKernel(k.ssum_fn, sgrid, dim3(256), cargs, 0, s));
+        SPL_CUDA(cudaLaunchKernel(k.check_fn, k.check_grid, k.check_block, cargs, 0, s));
+        SPL_CUDA(cudaMemcpyAsync(p->host_flag, p->eager_args.glob + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        SPL_CUDA(cudaStreamSynchronize(s));
+        more = *p->host_flag != 0;
+    }
     void *i8_args[] = {&p->eager_args, const_cast<unsigned char *>(q.tmap)};
-    for (int it = 0; it < p->args.max_iter; ++it) {
+    for (int it = 0; more && it < p->args.max_iter; ++it) {
         if (p->args.i8) SPL_CUDA(cudaLaunchKernel(q.step_fn, q.step_grid, q.step_block, i8_args, q.step_smem, s));
         SPL_CUDA(cudaLaunchKernel(k.step_fn, k.step_grid, k.step_block, args, k.step_smem, s));
         SPL_CUDA(cudaLaunchKernel(k.check_fn, k.check_grid, k.check_block, args, 0, s));
@@ -667,7 +797,10 @@ int splidar_plan_gemv(splidar_plan plan, void *stream) {
 
 splidar_status splidar_plan_launch(splidar_plan plan, void *stream) {
     if (!plan) return SPLIDAR_EINVAL;
-    if (plan->fused) return cuda_status(launch_fused(plan->dt, plan->fargs, (cudaStream_t)stream));
+    if (plan->fused) {
+        if (plan->with_build) SPL_CUDA(plan_enqueue_build(plan, plan->dt, (cudaStream_t)stream));
+        return cuda_status(launch_fused(plan->dt, plan->fargs, (cudaStream_t)stream));
+    }
     if (plan->eager) return plan_launch_eager(plan, (cudaStream_t)stream);
     return cuda_status(cudaGraphLaunch(plan->exec, (cudaStream_t)stream));
 }

@@ -23,7 +23,7 @@ template <> struct Vec16<float> { using type = float4; static constexpr int n = 
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kStripCols / Vec16<T>::n)
 k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t ld, int64_t mstride, int row0,
-        int nrows) {
+        int nrows, int rows_per_cta, double *__restrict__ colsum_part) {
     constexpr int VEC = Vec16<T>::n;
     using V = typename Vec16<T>::type;
     const int m = blockIdx.z;
@@ -39,8 +39,8 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
     const int j0 = blockIdx.x * kStripCols + threadIdx.x * VEC;
     if (j0 >= N) return;
     // rows [row0, row0 + nrows) of P~0 (a row shard); stored from row 0 of P0
-    const int r0 = row0 + blockIdx.y * kRowsPerCta;
-    const int r1 = min(row0 + nrows, r0 + kRowsPerCta);
+    const int r0 = row0 + blockIdx.y * rows_per_cta;
+    const int r1 = min(row0 + nrows, r0 + rows_per_cta);
     const bool full = j0 + VEC <= N;
 
     // column operands in registers
@@ -57,6 +57,9 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
         }
     }
 
+    double cs[VEC];              // column sums of the STORED entries over this CTA's rows (colsum_part)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) cs[e] = 0.0;
 #pragma unroll 4
     for (int r = r0; r < r1; ++r) {
         T val[VEC];
@@ -81,6 +84,10 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
                 }
             }
         }
+        if (colsum_part) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) cs[e] += (double)val[e];
+        }
         T *row = out + (int64_t)(r - row0) * ld + j0;
         if (full) {
             V v;
@@ -92,6 +99,23 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
             for (int e = 0; e < VEC; ++e)
                 if (j0 + e < N) row[e] = val[e];
         }
+    }
+    if (colsum_part) {           // [M][row chunk][N]: summed over the chunks in fixed order later
+        double *cp = colsum_part + ((size_t)m * gridDim.y + blockIdx.y) * N;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+            if (j0 + e < N) cp[j0 + e] = cs[e];
+    }
+}
+
+// colsum[m][j] = sum over the row chunks (fixed order) of the build's partial column sums.
+__global__ void __launch_bounds__(256) k_colsum_reduce(const double *__restrict__ part, int nch, int N, int M,
+                                                       double *__restrict__ colsum) {
+    const int m = blockIdx.y;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+        double t = 0.0;
+        for (int c = 0; c < nch; ++c) t += part[((size_t)m * nch + c) * N + j];
+        colsum[(size_t)m * N + j] = t;
     }
 }
 
@@ -108,24 +132,36 @@ __global__ void __launch_bounds__(256) k_apply_deadtime(const uint4 *__restrict_
 
 }  // namespace
 
+int colsum_chunks(int N) { return N / kRowsPerCta < kColsumChunks ? (N + kRowsPerCta - 1) / kRowsPerCta : kColsumChunks; }
+
 cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
-                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0, int nrows) {
+                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0, int nrows,
+                         double *colsum_part, double *colsum) {
     if (nrows < 0) nrows = N;
-    dim3 grid((N + kStripCols - 1) / kStripCols, (nrows + kRowsPerCta - 1) / kRowsPerCta, M);
+    // with column sums: at most kColsumChunks row chunks per matrix (deterministic fixed-order sum)
+    const int nch = colsum_part ? colsum_chunks(nrows) : (nrows + kRowsPerCta - 1) / kRowsPerCta;
+    const int rpc = (nrows + nch - 1) / nch;
+    dim3 grid((N + kStripCols - 1) / kStripCols, nch, M);
     if (dtype == SPLIDAR_F64) {
         dim3 block(kStripCols / 2);
         if (mode == SPLIDAR_ENTRY_EXP)
-            k_build<double, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows);
+            k_build<double, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part);
         else
-            k_build<double, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows);
+            k_build<double, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part);
     } else {
         dim3 block(kStripCols / 4);
         if (mode == SPLIDAR_ENTRY_EXP)
-            k_build<float, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows);
+            k_build<float, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part);
         else
-            k_build<float, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows);
+            k_build<float, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part);
     }
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && colsum_part) {
+        k_colsum_reduce<<<dim3((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, M), 256, 0, s>>>(colsum_part, nch, N, M,
+                                                                                          colsum);
+        e = cudaGetLastError();
+    }
+    return e;
 }
 
 cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, int dtype, int l,

@@ -59,7 +59,7 @@ struct WsLayout {
     int N, M, V;    // V padded to a power of two
     int strips, chunks, xstride, pieces;
     size_t flux, vec, lsh, oidx, y, X, part, ssum, l1part, state, strip_cnt, mv_cnt, act, glob;
-    size_t ximg, colexp, colmin, smax, xtau, total;
+    size_t ximg, colexp, colmin, smax, xtau, cpart, csum, total;
 };
 
 WsLayout ws_layout(int N, int M, int V);
@@ -77,8 +77,13 @@ cudaError_t func_attrs_once(const void *fn, int max_dyn_smem, bool nonportable_c
 cudaError_t launch_flux_vectors(const FluxDev *d_flux, int M, int N, VecPtrs base, int64_t vstride,
                                 cudaStream_t s, const FluxDev *single = nullptr);
 constexpr int kSmallVecMax = 8192;   // N + 1 <= this: the one-launch vector kernel (k_vec_small)
+// colsum_part ([M][colsum_chunks(N)][N]) / colsum ([M][N]): optional column sums of the stored
+// entries (the first power-iteration product from the uniform start, fused into the build)
+constexpr int kColsumChunks = 32;
+int colsum_chunks(int N);
 cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
-                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0 = 0, int nrows = -1);
+                         void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0 = 0, int nrows = -1,
+                         double *colsum_part = nullptr, double *colsum = nullptr);
 cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, int dtype, int l,
                                   cudaStream_t s);
 cudaError_t launch_build_eq4(const FluxDev &f, double u, int dtype, void *P, int64_t ld, cudaStream_t s);
@@ -116,6 +121,7 @@ struct PowerArgs {
     // writes its partial y^T = x_g^T P~0[rows, :] to ypart [M][V][N] for the caller's all-reduce
     int rows, row0;
     double *ypart;
+    int ypart_shared;        // ypart is [M][N], one y for every vector of a matrix (fused-build column sums)
 };
 
 // Kernel node parameters for the three solver kernels (for graph construction).

@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
     const int c = blockIdx.x, mv = blockIdx.y, tid = threadIdx.x;
     const int N = a.N;
     const SolveState st = a.st[mv];
-    if (st.done && a.ypart) {   // row shard: a frozen vector's partial stays zero through the all-reduces
+    if (st.done && a.ypart && !a.ypart_shared) {   // row shard: a frozen vector's partial stays zero
         const int j1 = min(N, (c + 1) * kCheckChunk);
         for (int j = c * kCheckChunk + tid; j < j1; j += 256) a.ypart[(size_t)mv * N + j] = 0.0;
     }
@@ -462,7 +462,8 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
         const double inv_new = 1.0 / S, inv_old = 1.0 / st.s;
         // row shard: y = the all-reduced partial products (a.ypart); it is also kept in y[1 - cur] as
         // the next iterate (finish kernel, next change)
-        const double *yn = a.ypart ? a.ypart + (size_t)mv * N : a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
+        const double *yn = a.ypart ? a.ypart + (size_t)(a.ypart_shared ? m : mv) * N
+                                   : a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
         const double *yo = a.y + ((size_t)mv * 2 + st.cur) * N;
         if (a.ypart) {
             double *yw = a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
@@ -574,24 +575,39 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
     }
 }
 
-// Row shard: strip sums of the all-reduced partial products, fixed order (the GEMV's own strip sums
-// cover only the shard's rows). CTA (strip, mv).
+// Strip sums (and, for the int8 GEMV, tile maxima) of an externally supplied y (a.ypart): the
+// all-reduced partial products of a row shard, or the column sums the fused build produced (the
+// first power-iteration product from the uniform start, shared by every vector of a matrix:
+// a.ypart_shared). The GEMV's own strip sums do not exist for such a y. CTA (strip, mv), fixed order;
+// the strip width follows the GEMV that runs this plan (512 columns, or the int8 GEMV's tiles).
 __global__ void __launch_bounds__(256) k_shard_ssum(const PowerArgs a) {
-    __shared__ double red[8];
+    __shared__ double red[8], mx[8];
     const int c = blockIdx.x, mv = blockIdx.y, tid = threadIdx.x;
     const int N = a.N;
-    const double *yp = a.ypart + (size_t)mv * N + (size_t)c * kStripCols;
-    const int cols = min(kStripCols, N - c * kStripCols);
-    double t = 0.0;
-    for (int j = tid; j < cols; j += 256) t += __ldcg(yp + j);
+    const bool i8 = a.i8 && a.glob[3];
+    const int nstrips = i8 ? a.strips_i8 : a.strips;
+    if (c >= nstrips) return;
+    const int width = i8 ? N / a.strips_i8 : kStripCols;
+    const int m = mv / a.V;
+    const double *yp = a.ypart + (size_t)(a.ypart_shared ? m : mv) * N + (size_t)c * width;
+    const int cols = min(width, N - c * width);
+    double t = 0.0, x = 0.0;
+    for (int j = tid; j < cols; j += 256) {
+        const double v = __ldcg(yp + j);
+        t += v;
+        x = fmax(x, v);
+    }
     t = warp_sum(t);
-    if ((tid & 31) == 0) red[tid >> 5] = t;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if ((tid & 31) == 0) { red[tid >> 5] = t; mx[tid >> 5] = x; }
     __syncthreads();
     if (tid == 0) {
-        double sum = 0.0;
+        double sum = 0.0, smx = 0.0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) sum += red[w];
-        a.ssum[(size_t)mv * a.strips + c] = sum;
+        for (int w = 0; w < 8; ++w) { sum += red[w]; smx = fmax(smx, mx[w]); }
+        a.ssum[(size_t)mv * nstrips + c] = sum;
+        if (i8) a.smax[(size_t)mv * nstrips + c] = smx;
     }
 }
 

@@ -93,6 +93,9 @@ def _lib():
             "splidar_sweep": (st, [fp, i32, p, p, p, st, st, d, i32, p, p, i32, i64, p, sz, pinfo, p]),
             "splidar_plan_create": (st, [C.POINTER(p), p, i32, i64, i32, i64, st, d, p, i32, d, i32, p, p,
                                          sz, p]),
+            "splidar_plan_set_fluxes": (st, [p, fp, i32, p]),
+            "splidar_plan_create_build": (st, [C.POINTER(p), fp, i32, st, st, p, i64, i64, p, i32, d, i32, p, p, sz,
+                                               p]),
             "splidar_plan_execute": (st, [p, pinfo, p]),
             "splidar_plan_launch": (st, [p, p]),
             "splidar_plan_info": (st, [p, pinfo, p]),
@@ -436,7 +439,9 @@ class Plan:
     execute() reruns the solve from pi^0 and returns the infos; launch() only enqueues."""
 
     def __init__(self, P0: torch.Tensor, t_r: float, t_d, tol: float = 1e-12, max_iter: int = 10 ** 6,
-                 ws: torch.Tensor | None = None, stream=None):
+                 ws: torch.Tensor | None = None, stream=None, build=None, mode: str = "factored"):
+        """build: fluxes (one per matrix) -> every launch also builds P0 (splidar_plan_create_build):
+        steps 1-2 and the column sums that give iteration 1 without a GEMV pass."""
         ptr, n, ld, dt = _matrix_args(P0)
         M = P0.shape[0] if P0.dim() == 3 else 1
         mstride = P0.stride(0) if P0.dim() == 3 else n * ld
@@ -448,12 +453,31 @@ class Plan:
         self.ws = ws if ws is not None else workspace(n, M, V, device=P0.device)
         self._T = T
         self._h = C.c_void_p(None)
+        if build is not None:
+            fl = list(build) if isinstance(build, (list, tuple)) else [build]
+            if len(fl) != M:
+                raise SplidarError(EINVAL, "Plan(build=...): one flux per matrix")
+            self._fas = [_flux_arg(f) for f in fl]
+            arr = (_Flux * M)(*[fa.s for fa in self._fas])
+            self._farr = arr
+            _check(_lib().splidar_plan_create_build(C.byref(self._h), arr, M, _MODES[mode], dt, ptr, mstride, ld,
+                                                    T.ctypes.data, V, float(tol), int(max_iter), self.pi.data_ptr(),
+                                                    self.ws.data_ptr(), self.ws.numel(), _stream(stream)),
+                   "splidar_plan_create_build")
+            return
         _check(_lib().splidar_plan_create(C.byref(self._h), ptr, M, mstride, n, ld, dt, float(t_r), T.ctypes.data,
                                           V, float(tol), int(max_iter), self.pi.data_ptr(), self.ws.data_ptr(),
                                           self.ws.numel(), _stream(stream)), "splidar_plan_create")
 
     def launch(self, stream=None):
         _check(_lib().splidar_plan_launch(self._h, _stream(stream)), "splidar_plan_launch")
+
+    def set_fluxes(self, fluxes, stream=None):
+        """New theta for a building plan (Plan(build=...)): same N and t_r, one flux per matrix."""
+        fl = list(fluxes) if isinstance(fluxes, (list, tuple)) else [fluxes]
+        fas = [_flux_arg(f) for f in fl]
+        arr = (_Flux * len(fl))(*[fa.s for fa in fas])
+        _check(_lib().splidar_plan_set_fluxes(self._h, arr, len(fl), _stream(stream)), "splidar_plan_set_fluxes")
 
     @property
     def fused(self) -> bool:

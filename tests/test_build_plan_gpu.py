@@ -1,0 +1,94 @@
+"""Building plans (splidar_plan_create_build): every launch builds P~0 and solves, the first product
+taken from the build's column sums (x^0 = 1/N: (1/N) 1^T J_l P~0 = (1/N) 1^T P~0, the row
+permutation leaves column sums unchanged -- Thm 2). Against the separate build + plan:
+the same iteration counts and pi to rounding, on every GEMV kind (fused, FP64, int8), in graph and
+eager mode, for several matrices, and after new parameters (set_fluxes); against the oracle's Eq. 4
+residual."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workloads import Flux, config, random_flux
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spl():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2509_20500_b200 import build
+    build.build()
+    import paper_2509_20500_b200 as s
+    return s
+
+
+def _pair(spl, fl, T, dtype, mode="factored"):
+    N = fl[0].n_bins
+    P0 = spl.empty_matrix(N, dtype, n_matrices=len(fl))
+    pa = spl.Plan(P0, fl[0].t_r, T, tol=1e-12, build=fl, mode=mode)
+    ia = pa.execute()
+    pia = pa.pi.detach().cpu().numpy().copy()
+    kind = pa.gemv()
+    spl.build_base_batched(fl, dtype, mode, out=P0)
+    pb = spl.Plan(P0, fl[0].t_r, T, tol=1e-12)
+    ib = pb.execute()
+    pib = pb.pi.detach().cpu().numpy().copy()
+    pa.close()
+    pb.close()
+    return pia, ia, pib, ib, kind
+
+
+def _c5(N):
+    f0 = config(5).items[0].flux
+    return Flux(f0.t_r, N, f0.tau, f0.sigma, f0.signal, f0.background)
+
+
+@pytest.mark.parametrize("N,V,dtype,eager", [(256, 1, torch.float64, "0"), (4096, 17, torch.float64, "0"),
+                                             (4096, 17, torch.float32, "0"), (4096, 17, torch.float32, "1"),
+                                             (5000, 2, torch.float64, "1"), (9001, 1, torch.float32, "0")])
+def test_building_plan_equals_separate(spl, monkeypatch, N, V, dtype, eager):
+    monkeypatch.setenv("SPLIDAR_EAGER", eager)
+    f = _c5(N)
+    w = config(5)
+    T = np.array([([w.items[0].t_d] + [it.t_d for it in w.sweep])[:V]])
+    pia, ia, pib, ib, kind = _pair(spl, [f], T, dtype)
+    assert [i["iters"] for i in ia] == [i["iters"] for i in ib]
+    assert all(i["converged"] for i in ia)
+    assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-14
+    if dtype == torch.float32 and V >= 8:
+        assert kind == "tensor_i8"
+    y = oracle.left_matvec_streamed(f, T[0, 0], pia[0, 0])
+    assert np.sum(np.abs(y - pia[0, 0])) <= (1e-11 if dtype == torch.float64 else 1e-5)
+
+
+def test_building_plan_batched_and_exp(spl):
+    rng = np.random.default_rng(21)
+    fl = [random_flux(rng, 4096, 1) for _ in range(5)]
+    fl = [Flux(100.0, 4096, f.tau, f.sigma, f.signal, f.background) for f in fl]
+    T = rng.uniform(0, 250, (5, 1))
+    for mode in ("factored", "exp"):
+        pia, ia, pib, ib, _ = _pair(spl, fl, T, torch.float64, mode)
+        assert [i["iters"] for i in ia] == [i["iters"] for i in ib]
+        assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-14
+
+
+def test_set_fluxes(spl):
+    """New theta through set_fluxes gives the plan built for that theta."""
+    c4 = config(4).items[0]
+    f = c4.flux
+    g = Flux(f.t_r, f.n_bins, (60.0,), (0.2,), (1.5,), 0.7)
+    P0 = spl.empty_matrix(f.n_bins, torch.float64)
+    plan = spl.Plan(P0, f.t_r, [[c4.t_d]], tol=1e-12, build=[f])
+    plan.execute()
+    plan.set_fluxes([g])
+    ig = plan.execute()
+    got = plan.pi[0, 0].detach().cpu().numpy().copy()
+    plan.close()
+    P1 = spl.build_base(g, torch.float64)
+    ref, ir = spl.stationary(P1, g.t_r, c4.t_d)
+    assert ig[0]["iters"] == ir["iters"]
+    assert np.sum(np.abs(got - ref.cpu().numpy())) <= 1e-14
+    with pytest.raises(spl.SplidarError):
+        plan2 = spl.Plan(P0, f.t_r, [[c4.t_d]], build=[f])
+        plan2.set_fluxes([Flux(f.t_r, 1024, f.tau, f.sigma, f.signal, f.background)])   # other N
