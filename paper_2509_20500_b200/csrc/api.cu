@@ -63,6 +63,7 @@ WsLayout ws_layout(int N, int M, int V) {
     // plans that build their matrix: the build's partial column sums and the column sums (iteration 1)
     L.cpart = o; o = a256(o + sizeof(double) * (size_t)M * kColsumChunks * N);
     L.csum = o; o = a256(o + sizeof(double) * (size_t)M * N);
+    L.epart = o; o = a256(o + 2 * sizeof(int) * (size_t)M * kColsumChunks * N);   // exponent max / min per chunk
     L.total = o;
     return L;
 }
@@ -401,9 +402,19 @@ static cudaError_t plan_enqueue_build(const splidar_plan_s *p, int dt, cudaStrea
     // the fluxes are read from the plan's workspace (splidar_plan_set_fluxes replaces them there)
     cudaError_t e = launch_flux_vectors(reinterpret_cast<const FluxDev *>(p->ws + L.flux), M, N, vp, N, s, nullptr);
     if (e != cudaSuccess) return e;
+    ColStats cst{};
+    if (p->args.i8) {   // the int8 GEMV's column exponents and range test come from the build too
+        int *ep = reinterpret_cast<int *>(p->ws + L.epart);
+        cst.emax_part = ep;
+        cst.emin_part = ep + (size_t)M * colsum_chunks(N) * N;
+        cst.colexp = p->args.colexp;
+        cst.flag = p->args.glob + 3;
+        cst.R = i8_range_bits(dt);
+        cst.zero_col_exp = dt == SPLIDAR_F64 ? 2047 : 255;
+    }
     return launch_build(vp, N, M, N, dt, p->bmode, const_cast<void *>(p->args.P), p->args.ld, p->args.mstride, s, 0,
                         N, p->fused ? nullptr : reinterpret_cast<double *>(p->ws + L.cpart),
-                        p->fused ? nullptr : reinterpret_cast<double *>(p->ws + L.csum));
+                        p->fused ? nullptr : reinterpret_cast<double *>(p->ws + L.csum), cst);
 }
 
 static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws, cudaStream_t s) {
@@ -530,7 +541,7 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     }
     int rows_per_cta = q.rows_per_cta;
     void *colexp_args[] = {&a, &rows_per_cta};
-    if (a.i8) {   // range test of the stored matrix: flag = 1, then every column may clear it
+    if (a.i8 && !p->with_build) {   // range test of the stored matrix: flag = 1, then every column may clear it
         cudaGraphNode_t n_prep, n_col, n_chk;
         kp.func = q.prep_fn;
         kp.gridDim = q.small_grid;
@@ -744,7 +755,7 @@ static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
     const I8Kernels &q = p->q;
     void *args[] = {&p->eager_args};
     if (p->with_build) SPL_CUDA(plan_enqueue_build(p, p->dt, s));
-    if (p->args.i8) {
+    if (p->args.i8 && !p->with_build) {
         int rpc = q.rows_per_cta;
         void *cargs[] = {&p->eager_args, &rpc};
         SPL_CUDA(cudaLaunchKernel(q.prep_fn, q.small_grid, dim3(256), args, 0, s));

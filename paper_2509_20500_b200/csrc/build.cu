@@ -23,7 +23,7 @@ template <> struct Vec16<float> { using type = float4; static constexpr int n = 
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kStripCols / Vec16<T>::n)
 k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t ld, int64_t mstride, int row0,
-        int nrows, int rows_per_cta, double *__restrict__ colsum_part) {
+        int nrows, int rows_per_cta, double *__restrict__ colsum_part, const ColStats cst) {
     constexpr int VEC = Vec16<T>::n;
     using V = typename Vec16<T>::type;
     const int m = blockIdx.z;
@@ -58,8 +58,15 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
     }
 
     double cs[VEC];              // column sums of the STORED entries over this CTA's rows (colsum_part)
+    int emx[VEC], emn[VEC];      // largest / smallest exponent of a non-zero stored entry (cst: the int8
+                                 // GEMV's range test; -1: a subnormal or negative entry)
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) cs[e] = 0.0;
+    for (int e = 0; e < VEC; ++e) {
+        cs[e] = 0.0;
+        emx[e] = 0;
+        emn[e] = 1 << 20;
+    }
+    if (cst.emax_part && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *cst.flag = 1u;
 #pragma unroll 4
     for (int r = r0; r < r1; ++r) {
         T val[VEC];
@@ -88,6 +95,29 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
 #pragma unroll
             for (int e = 0; e < VEC; ++e) cs[e] += (double)val[e];
         }
+        if (cst.emax_part) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                int ex;
+                bool nz, bad;
+                if constexpr (sizeof(T) == 4) {
+                    const uint32_t u = __float_as_uint(val[e]);
+                    ex = (int)((u >> 23) & 0xFF);
+                    nz = (u & 0x7FFFFFFFu) != 0;
+                    bad = (ex == 0 && nz) || (u >> 31);
+                } else {
+                    const uint64_t u = (uint64_t)__double_as_longlong(val[e]);
+                    ex = (int)((u >> 52) & 0x7FF);
+                    nz = (u & 0x7FFFFFFFFFFFFFFFull) != 0;
+                    bad = (ex == 0 && nz) || (u >> 63);
+                }
+                if (nz) {
+                    emx[e] = max(emx[e], ex);
+                    emn[e] = min(emn[e], ex);
+                }
+                if (bad) emn[e] = -1;
+            }
+        }
         T *row = out + (int64_t)(r - row0) * ld + j0;
         if (full) {
             V v;
@@ -106,17 +136,44 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
         for (int e = 0; e < VEC; ++e)
             if (j0 + e < N) cp[j0 + e] = cs[e];
     }
+    if (cst.emax_part) {
+        const size_t o = ((size_t)m * gridDim.y + blockIdx.y) * N;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+            if (j0 + e < N) {
+                cst.emax_part[o + j0 + e] = emx[e];
+                cst.emin_part[o + j0 + e] = emn[e];
+            }
+    }
 }
 
 // colsum[m][j] = sum over the row chunks (fixed order) of the build's partial column sums.
+// With cst: E_j (the column's largest exponent; all-zero columns get the largest representable, so
+// every shift of the int8 GEMV is negative) and the range test of the int8 GEMV (power_i8.cu): clear
+// *cst.flag if a non-zero entry lies more than 2^R below its column maximum, the maximum is <= R, or an
+// entry is subnormal / negative. The same test as k_i8_colexp / k_i8_colcheck, from the build's
+// registers instead of a second read of the matrix.
 __global__ void __launch_bounds__(256) k_colsum_reduce(const double *__restrict__ part, int nch, int N, int M,
-                                                       double *__restrict__ colsum) {
+                                                       double *__restrict__ colsum, const ColStats cst) {
     const int m = blockIdx.y;
+    bool bad = false;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
         double t = 0.0;
         for (int c = 0; c < nch; ++c) t += part[((size_t)m * nch + c) * N + j];
         colsum[(size_t)m * N + j] = t;
+        if (cst.emax_part) {
+            int mx = 0, mn = 1 << 20;
+            for (int c = 0; c < nch; ++c) {
+                const size_t o = ((size_t)m * nch + c) * N + j;
+                mx = max(mx, cst.emax_part[o]);
+                mn = min(mn, cst.emin_part[o]);
+            }
+            const bool any = mn < (1 << 20);
+            cst.colexp[(size_t)m * N + j] = any ? mx : cst.zero_col_exp;
+            bad |= mn < 0 || (any && (mx - mn > cst.R || mx <= cst.R));
+        }
     }
+    if (cst.emax_part && __syncthreads_or(bad) && threadIdx.x == 0) atomicAnd(cst.flag, 0u);
 }
 
 // P[i][:] = P0[(i + l) mod N][:] (Thm 2; J_l), 16-byte vectors, one row per CTA row.
@@ -136,7 +193,7 @@ int colsum_chunks(int N) { return N / kRowsPerCta < kColsumChunks ? (N + kRowsPe
 
 cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
                          void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0, int nrows,
-                         double *colsum_part, double *colsum) {
+                         double *colsum_part, double *colsum, ColStats cst) {
     if (nrows < 0) nrows = N;
     // with column sums: at most kColsumChunks row chunks per matrix (deterministic fixed-order sum)
     const int nch = colsum_part ? colsum_chunks(nrows) : (nrows + kRowsPerCta - 1) / kRowsPerCta;
@@ -145,20 +202,20 @@ cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int 
     if (dtype == SPLIDAR_F64) {
         dim3 block(kStripCols / 2);
         if (mode == SPLIDAR_ENTRY_EXP)
-            k_build<double, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part);
+            k_build<double, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
         else
-            k_build<double, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part);
+            k_build<double, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
     } else {
         dim3 block(kStripCols / 4);
         if (mode == SPLIDAR_ENTRY_EXP)
-            k_build<float, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part);
+            k_build<float, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
         else
-            k_build<float, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part);
+            k_build<float, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
     }
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && colsum_part) {
         k_colsum_reduce<<<dim3((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, M), 256, 0, s>>>(colsum_part, nch, N, M,
-                                                                                          colsum);
+                                                                                          colsum, cst);
         e = cudaGetLastError();
     }
     return e;

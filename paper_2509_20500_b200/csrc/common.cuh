@@ -59,7 +59,7 @@ struct WsLayout {
     int N, M, V;    // V padded to a power of two
     int strips, chunks, xstride, pieces;
     size_t flux, vec, lsh, oidx, y, X, part, ssum, l1part, state, strip_cnt, mv_cnt, act, glob;
-    size_t ximg, colexp, colmin, smax, xtau, cpart, csum, total;
+    size_t ximg, colexp, colmin, smax, xtau, cpart, csum, epart, total;
 };
 
 WsLayout ws_layout(int N, int M, int V);
@@ -81,9 +81,16 @@ constexpr int kSmallVecMax = 8192;   // N + 1 <= this: the one-launch vector ker
 // entries (the first power-iteration product from the uniform start, fused into the build)
 constexpr int kColsumChunks = 32;
 int colsum_chunks(int N);
+// optional (with colsum): the int8 GEMV's column exponents and range test from the build
+struct ColStats {
+    int *emax_part, *emin_part;   // [M][chunks][N] (null: not wanted)
+    int *colexp;                  // [M][N]
+    unsigned *flag;               // set to 1 by the build, cleared by a failing column
+    int R, zero_col_exp;
+};
 cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
                          void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0 = 0, int nrows = -1,
-                         double *colsum_part = nullptr, double *colsum = nullptr);
+                         double *colsum_part = nullptr, double *colsum = nullptr, ColStats cst = ColStats{});
 cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, int dtype, int l,
                                   cudaStream_t s);
 cudaError_t launch_build_eq4(const FluxDev &f, double u, int dtype, void *P, int64_t ld, cudaStream_t s);
@@ -149,6 +156,7 @@ struct I8Kernels {
 int i8_supported(int dtype, const PowerArgs &a);
 cudaError_t i8_kernels(int dtype, I8Kernels *k, const PowerArgs &a);
 int i8_tile_cols(int dtype);
+int i8_range_bits(int dtype);      // R: non-zero entries within 2^R of their column maximum
 size_t finish_args_size();
 // pi output: out_idx[mv] >= 0 selects row out_idx[mv] of pi ([*, N]); < 0 skips the vector.
 void make_finish_args(void *dst, const PowerArgs &a, double *pi, const int *out_idx);

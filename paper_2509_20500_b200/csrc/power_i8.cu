@@ -621,6 +621,8 @@ cudaError_t i8_kernels(int dtype, I8Kernels *k, const PowerArgs &a) {
     return func_attrs_once(k->step_fn, (int)kI8Smem, false);
 }
 
+int i8_range_bits(int dtype) { return dtype == SPLIDAR_F64 ? I8Cfg<double>::R : I8Cfg<float>::R; }
+
 int i8_tile_cols(int dtype) { return dtype == SPLIDAR_F64 ? I8Cfg<double>::TN : I8Cfg<float>::TN; }
 
 }  // namespace spl

@@ -92,3 +92,16 @@ def test_set_fluxes(spl):
     with pytest.raises(spl.SplidarError):
         plan2 = spl.Plan(P0, f.t_r, [[c4.t_d]], build=[f])
         plan2.set_fluxes([Flux(f.t_r, 1024, f.tau, f.sigma, f.signal, f.background)])   # other N
+
+
+def test_building_plan_range_test(spl):
+    """The int8 GEMV's column exponents and range test come from the build of a building plan: a
+    flux whose columns span more than 2^8 (Lambda = 61) must run the FP64 GEMV, a moderate one the
+    int8 GEMV, both equal to the separate build + plan."""
+    tds = [[10.0, 30.0, 50.0, 70.0, 90.0, 110.0, 130.0, 150.0]]
+    for sig, want in ((60.0, "fp64"), (1.0, "tensor_i8")):
+        f = Flux(200.0, 4096, (60.0,), (0.5,), (sig,), 1.0)
+        pia, ia, pib, ib, kind = _pair(spl, [f], np.array(tds), torch.float32)
+        assert kind == want
+        assert [i["iters"] for i in ia] == [i["iters"] for i in ib]
+        assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-13
