@@ -105,3 +105,16 @@ def test_building_plan_range_test(spl):
         assert kind == want
         assert [i["iters"] for i in ia] == [i["iters"] for i in ib]
         assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-13
+
+
+def test_building_plan_batched_int8(spl, monkeypatch):
+    """M = 3 matrices x 8 dead times on the int8 GEMV, matrices and exponents built by the plan."""
+    rng = np.random.default_rng(33)
+    fl = [random_flux(rng, 2048, 2, sigma_bins=(1, 10), s_range=(0.5, 1.5), b_range=(0.2, 1.0)) for _ in range(3)]
+    fl = [Flux(100.0, 2176, f.tau, f.sigma, f.signal, f.background) for f in fl]
+    T = rng.uniform(0, 300, (3, 8))
+    monkeypatch.setenv("SPLIDAR_FUSED", "0")
+    pia, ia, pib, ib, kind = _pair(spl, fl, T, torch.float32)
+    assert kind == "tensor_i8"
+    assert [i["iters"] for i in ia] == [i["iters"] for i in ib]
+    assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-13
