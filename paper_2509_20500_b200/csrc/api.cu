@@ -10,9 +10,22 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 namespace spl {
+
+// One NVTX range per public entry point, named after it (header-only NVTX3: a no-op unless a tool is
+// attached; `ncu --nvtx --nvtx-include "splidar_plan_launch/"` profiles only the kernels one call
+// launches, and a timeline tool shows host calls against their kernels).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define SPL_NVTX_RANGE() ::spl::NvtxRange spl_nvtx_range_(__func__)
 
 static inline size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -285,6 +298,7 @@ static splidar_status vectors_and_build(const FluxDev *fl, int M, int N, int dt,
 splidar_status splidar_flux_vectors(const splidar_flux *flux, double *F, double *lam, double *w,
                                     double *inv_d, double *lambda_total, void *ws, size_t ws_bytes,
                                     void *stream) {
+    SPL_NVTX_RANGE();
     splidar_status st = check_flux(flux);
     if (st) return st;
     const int N = flux->n_bins;
@@ -307,6 +321,7 @@ splidar_status splidar_flux_vectors(const splidar_flux *flux, double *F, double 
 splidar_status splidar_build_base_batched(const splidar_flux *fluxes, int32_t n_matrices, splidar_dtype dt,
                                           splidar_entry mode, void *P0, int64_t ld, int64_t matrix_stride,
                                           void *ws, size_t ws_bytes, void *stream) {
+    SPL_NVTX_RANGE();
     if (!fluxes || n_matrices < 1 || n_matrices > 65535) return SPLIDAR_EINVAL;
     if (mode != SPLIDAR_ENTRY_FACTORED && mode != SPLIDAR_ENTRY_EXP) return SPLIDAR_EINVAL;
     const int N = fluxes[0].n_bins;
@@ -325,12 +340,14 @@ splidar_status splidar_build_base_batched(const splidar_flux *fluxes, int32_t n_
 
 splidar_status splidar_build_base(const splidar_flux *flux, splidar_dtype dt, splidar_entry mode, void *P0,
                                   int64_t ld, void *ws, size_t ws_bytes, void *stream) {
+    SPL_NVTX_RANGE();
     return splidar_build_base_batched(flux, 1, dt, mode, P0, ld, flux ? (int64_t)flux->n_bins * ld : 0, ws,
                                       ws_bytes, stream);
 }
 
 splidar_status splidar_apply_deadtime(const void *P0, void *P, int32_t n_bins, int64_t ld, splidar_dtype dt,
                                       double t_r, double t_d, void *stream) {
+    SPL_NVTX_RANGE();
     int32_t l;
     splidar_status st = splidar_shift(t_r, n_bins, t_d, &l);
     if (st) return st;
@@ -697,6 +714,7 @@ splidar_status splidar_plan_create(splidar_plan *plan, const void *P0, int32_t n
                                    int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r, const double *t_d,
                                    int32_t n_vectors, double tol, int32_t max_iter, double *pi, void *ws,
                                    size_t ws_bytes, void *stream) {
+    SPL_NVTX_RANGE();
     if (!plan || !t_d || n_matrices < 1 || n_vectors < 1 || n_vectors > kMaxVectors) return SPLIDAR_EINVAL;
     std::vector<int> l((size_t)n_matrices * n_vectors);
     for (size_t i = 0; i < l.size(); ++i) {
@@ -713,6 +731,7 @@ splidar_status splidar_plan_create_build(splidar_plan *plan, const splidar_flux 
                                          splidar_entry mode, splidar_dtype dt, void *P0, int64_t matrix_stride,
                                          int64_t ld, const double *t_d, int32_t n_vectors, double tol,
                                          int32_t max_iter, double *pi, void *ws, size_t ws_bytes, void *stream) {
+    SPL_NVTX_RANGE();
     if (!plan || !fluxes || !t_d || n_matrices < 1 || n_matrices > 65535 || n_vectors < 1 ||
         n_vectors > kMaxVectors)
         return SPLIDAR_EINVAL;
@@ -738,6 +757,7 @@ splidar_status splidar_plan_create_build(splidar_plan *plan, const splidar_flux 
 
 splidar_status splidar_plan_set_fluxes(splidar_plan plan, const splidar_flux *fluxes, int32_t n_matrices,
                                        void *stream) {
+    SPL_NVTX_RANGE();
     if (!plan || !plan->with_build || !fluxes || n_matrices != plan->M) return SPLIDAR_EINVAL;
     splidar_status st;
     for (int m = 0; m < n_matrices; ++m) {
@@ -807,6 +827,7 @@ int splidar_plan_gemv(splidar_plan plan, void *stream) {
 }
 
 splidar_status splidar_plan_launch(splidar_plan plan, void *stream) {
+    SPL_NVTX_RANGE();
     if (!plan) return SPLIDAR_EINVAL;
     if (plan->fused) {
         if (plan->with_build) SPL_CUDA(plan_enqueue_build(plan, plan->dt, (cudaStream_t)stream));
@@ -841,6 +862,7 @@ splidar_status splidar_plan_info(splidar_plan plan, splidar_solve_info *info, vo
 }
 
 splidar_status splidar_plan_execute(splidar_plan plan, splidar_solve_info *info, void *stream) {
+    SPL_NVTX_RANGE();
     splidar_status st = splidar_plan_launch(plan, stream);
     if (st) return st;
     return splidar_plan_info(plan, info, stream);
@@ -955,6 +977,7 @@ void splidar_plan_cache_clear(void) {
 splidar_status splidar_stationary(const void *P0, int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r,
                                   double t_d, double tol, int32_t max_iter, double *pi, void *ws,
                                   size_t ws_bytes, splidar_solve_info *info, void *stream) {
+    SPL_NVTX_RANGE();
     return splidar_stationary_multi(P0, 1, (int64_t)n_bins * ld, n_bins, ld, dt, t_r, &t_d, 1, tol, max_iter, pi,
                                     ws, ws_bytes, info, stream);
 }
@@ -963,6 +986,7 @@ splidar_status splidar_stationary_multi(const void *P0, int32_t n_matrices, int6
                                         int64_t ld, splidar_dtype dt, double t_r, const double *t_d,
                                         int32_t n_vectors, double tol, int32_t max_iter, double *pi, void *ws,
                                         size_t ws_bytes, splidar_solve_info *info, void *stream) {
+    SPL_NVTX_RANGE();
     return splidar_stationary_multi_host(P0, n_matrices, matrix_stride, n_bins, ld, dt, t_r, t_d, n_vectors, tol,
                                          max_iter, pi, nullptr, ws, ws_bytes, info, stream);
 }
@@ -972,6 +996,7 @@ splidar_status splidar_stationary_multi_host(const void *P0, int32_t n_matrices,
                                              const double *t_d, int32_t n_vectors, double tol, int32_t max_iter,
                                              double *pi, double *pi_host, void *ws, size_t ws_bytes,
                                              splidar_solve_info *info, void *stream) {
+    SPL_NVTX_RANGE();
     splidar_status st;
     if (!t_d || n_matrices < 1 || n_vectors < 1 || n_vectors > kMaxVectors) return SPLIDAR_EINVAL;
     if ((st = check_matrix(P0, n_bins, ld, dt))) return st;
@@ -993,6 +1018,7 @@ splidar_status splidar_stationary_multi_host(const void *P0, int32_t n_matrices,
 splidar_status splidar_build_base_rows(const splidar_flux *flux, splidar_dtype dt, splidar_entry mode, void *P0_rows,
                                        int64_t ld, int32_t row0, int32_t n_rows, void *ws, size_t ws_bytes,
                                        void *stream) {
+    SPL_NVTX_RANGE();
     splidar_status st = check_flux(flux);
     if (st) return st;
     if (mode != SPLIDAR_ENTRY_FACTORED && mode != SPLIDAR_ENTRY_EXP) return SPLIDAR_EINVAL;
@@ -1015,6 +1041,7 @@ splidar_status splidar_plan_create_rows(splidar_plan *plan, const void *P0_rows,
                                         int32_t n_bins, int64_t ld, splidar_dtype dt, double t_r, const double *t_d,
                                         int32_t n_vectors, double tol, int32_t max_iter, double *pi, double *ypart,
                                         void *ws, size_t ws_bytes, void *stream) {
+    SPL_NVTX_RANGE();
     if (!plan || !t_d || !ypart || n_vectors < 1 || n_vectors > kMaxVectors) return SPLIDAR_EINVAL;
     if (row0 < 0 || n_rows < 1 || n_bins < 2 || row0 + n_rows > n_bins) return SPLIDAR_EINVAL;
     if (((uintptr_t)ypart & 15u) != 0) return SPLIDAR_ENOSPACE;
@@ -1030,6 +1057,7 @@ splidar_status splidar_plan_create_rows(splidar_plan *plan, const void *P0_rows,
 }
 
 splidar_status splidar_plan_shard_init(splidar_plan p, void *stream) {
+    SPL_NVTX_RANGE();
     if (!p || !p->shard) return SPLIDAR_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     void *args[] = {&p->eager_args};
@@ -1038,6 +1066,7 @@ splidar_status splidar_plan_shard_init(splidar_plan p, void *stream) {
 }
 
 splidar_status splidar_plan_shard_gemv(splidar_plan p, void *stream) {
+    SPL_NVTX_RANGE();
     if (!p || !p->shard) return SPLIDAR_EINVAL;
     void *args[] = {&p->eager_args};
     SPL_CUDA(cudaLaunchKernel(p->k.step_fn, p->k.step_grid, p->k.step_block, args, p->k.step_smem,
@@ -1046,6 +1075,7 @@ splidar_status splidar_plan_shard_gemv(splidar_plan p, void *stream) {
 }
 
 splidar_status splidar_plan_shard_check(splidar_plan p, int32_t *more, void *stream) {
+    SPL_NVTX_RANGE();
     if (!p || !p->shard || !more) return SPLIDAR_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     void *args[] = {&p->eager_args};
@@ -1060,6 +1090,7 @@ splidar_status splidar_plan_shard_check(splidar_plan p, int32_t *more, void *str
 }
 
 splidar_status splidar_plan_shard_finish(splidar_plan p, splidar_solve_info *info, void *stream) {
+    SPL_NVTX_RANGE();
     if (!p || !p->shard) return SPLIDAR_EINVAL;
     void *fargs[] = {p->fin_args.data()};
     SPL_CUDA(cudaLaunchKernel(p->k.finish_fn, p->k.finish_grid, p->k.finish_block, fargs, 0, (cudaStream_t)stream));
@@ -1107,6 +1138,7 @@ splidar_status splidar_second_eigenvalue_dense(const void *P0, int32_t n_bins, i
                                                double t_r, double t_d, const double *pi, double tol,
                                                int32_t max_iter, void *ws, size_t ws_bytes,
                                                splidar_spectral_info *info, void *stream) {
+    SPL_NVTX_RANGE();
     splidar_status st;
     if (n_bins < 2 || !pi) return SPLIDAR_EINVAL;
     if ((st = check_matrix(P0, n_bins, ld, dt))) return st;
@@ -1251,6 +1283,7 @@ splidar_status splidar_sweep(const splidar_flux *shape, int32_t n_items, const d
                              const double *t_d, splidar_dtype dt, splidar_entry mode, double tol, int32_t max_iter,
                              double *pi, void *P0_store, int32_t n_store, int64_t ld, void *ws, size_t ws_bytes,
                              splidar_solve_info *info, void *stream) {
+    SPL_NVTX_RANGE();
     if (!shape || n_items < 1 || !S || !B || !t_d || !pi) return SPLIDAR_EINVAL;
     if (!P0_store)   // matrix-free: the same items on the structured operator (f2), no N^2 storage
         return splidar_stationary_structured(shape, n_items, S, B, t_d, tol, max_iter, pi, ws, ws_bytes, info,
@@ -1533,6 +1566,7 @@ void splidar_splan_destroy(splidar_splan plan) {
 splidar_status splidar_splan_create(splidar_splan *plan, int32_t kind, const splidar_flux *shape, int32_t n_items,
                                     const double *S, const double *B, const double *t_d, double tol,
                                     int32_t max_iter, double *pi, void *ws, size_t ws_bytes, void *stream) {
+    SPL_NVTX_RANGE();
     if (!plan) return SPLIDAR_EINVAL;
     *plan = nullptr;
     if ((kind != SPLIDAR_SPLAN_SOLVE && kind != SPLIDAR_SPLAN_LAMBDA2) || !pi || !(tol > 0.0) ||
@@ -1555,6 +1589,7 @@ splidar_status splidar_splan_create(splidar_splan *plan, int32_t kind, const spl
 }
 
 splidar_status splidar_splan_launch(splidar_splan plan, void *stream) {
+    SPL_NVTX_RANGE();
     if (!plan) return SPLIDAR_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     if (!plan->gexec && plan->launches == 1 && !plan->graph_tried) {   // a reused plan: capture it once
@@ -1623,6 +1658,7 @@ splidar_status splidar_stationary_structured(const splidar_flux *shape, int32_t 
                                              const double *B, const double *t_d, double tol, int32_t max_iter,
                                              double *pi, void *ws, size_t ws_bytes, splidar_solve_info *info,
                                              void *stream) {
+    SPL_NVTX_RANGE();
     splidar_splan pl;
     splidar_status st = splidar_splan_create(&pl, SPLIDAR_SPLAN_SOLVE, shape, n_items, S, B, t_d, tol, max_iter,
                                              pi, ws, ws_bytes, stream);
@@ -1637,6 +1673,7 @@ splidar_status splidar_second_eigenvalue(const splidar_flux *shape, int32_t n_it
                                          const double *B, const double *t_d, const double *pi, double tol,
                                          int32_t max_iter, void *ws, size_t ws_bytes, splidar_spectral_info *info,
                                          void *stream) {
+    SPL_NVTX_RANGE();
     splidar_splan pl;
     splidar_status st = splidar_splan_create(&pl, SPLIDAR_SPLAN_LAMBDA2, shape, n_items, S, B, t_d, tol,
                                              max_iter, const_cast<double *>(pi), ws, ws_bytes, stream);
@@ -1650,6 +1687,7 @@ splidar_status splidar_second_eigenvalue(const splidar_flux *shape, int32_t n_it
 splidar_status splidar_mixing_steps(const splidar_flux *flux, double t_d, const double *pi, double eps,
                                     int32_t max_steps, int32_t *steps_per_start, int32_t *mixing_steps, void *ws,
                                     size_t ws_bytes, void *stream) {
+    SPL_NVTX_RANGE();
     if (!flux || !pi || !mixing_steps || !(eps > 0.0) || !std::isfinite(eps) || max_steps < 1) return SPLIDAR_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     const double one = 1.0, bg = flux->background;
@@ -1680,6 +1718,7 @@ splidar_status splidar_mixing_steps(const splidar_flux *flux, double t_d, const 
 splidar_status splidar_bin_trajectory(const splidar_flux *flux, double t_d, const double *start, int32_t bin,
                                       int32_t steps, double *traj, double *final_vec, void *ws, size_t ws_bytes,
                                       void *stream) {
+    SPL_NVTX_RANGE();
     if (!flux || !start || !traj || steps < 0 || bin < 0 || bin >= flux->n_bins) return SPLIDAR_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     const double one = 1.0, bg = flux->background;
@@ -1719,6 +1758,7 @@ splidar_status splidar_monte_carlo(const splidar_flux *shape, int32_t n_items, c
                                    const double *t_d, uint64_t seed, int32_t n_runs, int32_t n_split, int64_t n_burn,
                                    int64_t n_regs, int64_t n_cycles, int32_t n_hist, uint64_t *hist, int32_t n_record,
                                    int64_t *q_rec, double *t_rec, void *ws, size_t ws_bytes, void *stream) {
+    SPL_NVTX_RANGE();
     if (!shape || n_items < 1 || n_items > 65535 || !S || !B || !t_d || !hist) return SPLIDAR_EINVAL;
     if (n_runs < 1 || n_split < 1 || (int64_t)n_runs * n_split > (1 << 30) || n_hist < 1 || n_burn < 0 ||
         n_record < 0 || (n_regs < 1 && n_cycles < 1))
