@@ -399,6 +399,10 @@ struct splidar_plan_s {
     // under the row permutation J_l): the solve starts at iteration 1 without a GEMV pass
     bool with_build = false;
     int bmode = 0;
+    // fp32 factored building plans on the int8 GEMV store P~0 ENCODED when every column is in range:
+    // each entry as its column's scaled integer (fixpt.cuh), so the GEMV needs no converters
+    // (k_power_step_i8e); the column exponents come from launch_enc_colexp before the build
+    bool enc = false;
     std::vector<FluxDev> bflux;
     char *ws = nullptr;
 };
@@ -420,7 +424,14 @@ static cudaError_t plan_enqueue_build(const splidar_plan_s *p, int dt, cudaStrea
     cudaError_t e = launch_flux_vectors(reinterpret_cast<const FluxDev *>(p->ws + L.flux), M, N, vp, N, s, nullptr);
     if (e != cudaSuccess) return e;
     ColStats cst{};
-    if (p->args.i8) {   // the int8 GEMV's column exponents and range test come from the build too
+    if (p->enc) {       // column exponents and range test first, then the build encodes (or not)
+        e = launch_enc_colexp(vp, N, M, N, p->args.colexp, p->args.colmin, p->args.glob + 3, s);
+        if (e != cudaSuccess) return e;
+        cst.colexp = p->args.colexp;
+        cst.flag = p->args.glob + 3;
+        cst.R = i8_range_bits(dt);
+        cst.enc = 1;
+    } else if (p->args.i8) {   // the int8 GEMV's column exponents and range test come from the build too
         int *ep = reinterpret_cast<int *>(p->ws + L.epart);
         cst.emax_part = ep;
         cst.emin_part = ep + (size_t)M * colsum_chunks(N) * N;
@@ -473,6 +484,8 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
             const char *d = getenv("SPLIDAR_I8_DBG");
             a.i8_dbg = d ? atoi(d) : 0;
             a.strips_i8 = L.N / i8_tile_cols(dt);
+            const char *ev = getenv("SPLIDAR_I8_ENC");
+            p->enc = p->with_build && dt == SPLIDAR_F32 && p->bmode == SPLIDAR_ENTRY_FACTORED && !(ev && ev[0] == '0');
         }
     }
 
@@ -614,10 +627,10 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     cudaGraphNode_t n_i8 = nullptr;
     if (a.i8) {
         void *i8_args[] = {&a, q.tmap};
-        kp.func = q.step_fn;
+        kp.func = p->enc ? q.step_enc_fn : q.step_fn;
         kp.gridDim = q.step_grid;
         kp.blockDim = q.step_block;
-        kp.sharedMemBytes = q.step_smem;
+        kp.sharedMemBytes = p->enc ? q.step_enc_smem : q.step_smem;
         kp.kernelParams = i8_args;
         SPL_CUDA(cudaGraphAddKernelNode(&n_i8, body, nullptr, 0, &kp));
     }
@@ -798,7 +811,9 @@ static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
     }
     void *i8_args[] = {&p->eager_args, const_cast<unsigned char *>(q.tmap)};
     for (int it = 0; more && it < p->args.max_iter; ++it) {
-        if (p->args.i8) SPL_CUDA(cudaLaunchKernel(q.step_fn, q.step_grid, q.step_block, i8_args, q.step_smem, s));
+        if (p->args.i8)
+            SPL_CUDA(cudaLaunchKernel(p->enc ? q.step_enc_fn : q.step_fn, q.step_grid, q.step_block, i8_args,
+                                      p->enc ? q.step_enc_smem : q.step_smem, s));
         SPL_CUDA(cudaLaunchKernel(k.step_fn, k.step_grid, k.step_block, args, k.step_smem, s));
         SPL_CUDA(cudaLaunchKernel(k.check_fn, k.check_grid, k.check_block, args, 0, s));
         SPL_CUDA(cudaMemcpyAsync(p->host_flag, p->eager_args.glob + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));

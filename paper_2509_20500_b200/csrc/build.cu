@@ -10,6 +10,7 @@
 // lambda, F) in registers and streams 128-bit stores down the rows. Per row it reads one
 // broadcast scalar (1/D_r or 1/Z_r, F_r). The kernel is a pure HBM write stream: N^2 * b bytes.
 #include "common.cuh"
+#include "fixpt.cuh"
 
 namespace spl {
 namespace {
@@ -67,6 +68,16 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
         emn[e] = 1 << 20;
     }
     if (cst.emax_part && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *cst.flag = 1u;
+    // encoded storage: entry -> scaled integer of its column (fixpt.cuh; launch_enc_colexp set E_j)
+    bool enc = false;
+    int base23[VEC];
+    if constexpr (sizeof(T) == 4 && MODE == SPLIDAR_ENTRY_FACTORED) {
+        enc = cst.enc && *cst.flag;
+        if (enc) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) base23[e] = j0 + e < N ? cst.colexp[(size_t)m * N + j0 + e] - cst.R - 23 : 255;
+        }
+    }
 #pragma unroll 4
     for (int r = r0; r < r1; ++r) {
         T val[VEC];
@@ -119,6 +130,21 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
             }
         }
         T *row = out + (int64_t)(r - row0) * ld + j0;
+        if constexpr (sizeof(T) == 4 && MODE == SPLIDAR_ENTRY_FACTORED) {
+            if (enc) {
+                uint32_t wd[VEC];
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) wd[e] = fx32(__float_as_uint((float)val[e]), base23[e]);
+                if (full) {
+                    *reinterpret_cast<uint4 *>(row) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e)
+                        if (j0 + e < N) reinterpret_cast<uint32_t *>(row)[e] = wd[e];
+                }
+                continue;
+            }
+        }
         if (full) {
             V v;
             if constexpr (VEC == 2) { v.x = val[0]; v.y = val[1]; }
@@ -176,6 +202,91 @@ __global__ void __launch_bounds__(256) k_colsum_reduce(const double *__restrict_
     if (cst.emax_part && __syncthreads_or(bad) && threadIdx.x == 0) atomicAnd(cst.flag, 0u);
 }
 
+// Column exponents for encoded storage, before the build writes anything. Factored entries are
+// P~0[r][j] = fl32(w_j * h_r) with h_r = 1/D_r for r <= j and fl(e^{-Lambda} / D_r) for r > j (k_build),
+// and fl(w * x) is non-decreasing in x, so column j's largest / smallest entries are w_j times the
+// extremes of 1/D over r <= j (prefix) and e^{-Lambda} times those over r > j (suffix). One CTA walks
+// the matrices: thread t owns columns [t C, t C + C); warp shuffles and the warp totals give each
+// thread the extremes before and after its chunk; a forward pass leaves the prefix-side extremes of
+// every column in colexp / scratch (as fp32 bits), a backward pass combines them with the suffix side
+// and writes E_j. The range test is k_i8_colcheck's (a column fails if its smallest entry is not a
+// normal fp32 number, lies more than 2^R below the largest, or the largest exponent is <= R); an
+// all-zero column (w_j = 0) gets E_j = 255.
+__global__ void __launch_bounds__(1024) k_enc_colexp(const VecPtrs base, int64_t vstride, int N, int M, int R,
+                                                     int *__restrict__ colexp, int *__restrict__ scratch,
+                                                     unsigned *__restrict__ flag) {
+    __shared__ double s_wmx[32], s_wmn[32];
+    const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+    const int C = (N + 1023) / 1024;
+    const int j0 = min(N, t * C), j1 = min(N, j0 + C);
+    bool bad = false;
+    for (int m = 0; m < M; ++m) {
+        const double *__restrict__ invD = base.invD + m * vstride;
+        const double *__restrict__ w = base.w + m * vstride;
+        const double eL = base.scal[m * 8 + 1];
+        int *__restrict__ E = colexp + (size_t)m * N;
+        int *__restrict__ Sx = scratch + (size_t)m * N;
+        double cmx = 0.0, cmn = INFINITY;                  // this chunk's extremes of 1/D
+        for (int j = j0; j < j1; ++j) {
+            const double h = invD[j];
+            cmx = fmax(cmx, h);
+            cmn = fmin(cmn, h);
+        }
+        // exclusive extremes of the chunks before (p*) and after (s*) this one
+        double pmx = cmx, pmn = cmn, smx = cmx, smn = cmn;  // inclusive warp scans
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double a = __shfl_up_sync(0xffffffffu, pmx, o), b2 = __shfl_up_sync(0xffffffffu, pmn, o);
+            const double c = __shfl_down_sync(0xffffffffu, smx, o), d = __shfl_down_sync(0xffffffffu, smn, o);
+            if (lane >= o) { pmx = fmax(pmx, a); pmn = fmin(pmn, b2); }
+            if (lane + o < 32) { smx = fmax(smx, c); smn = fmin(smn, d); }
+        }
+        __syncthreads();                                   // previous matrix done with s_w*
+        if (lane == 31) { s_wmx[wp] = pmx; s_wmn[wp] = pmn; }
+        double epmx = __shfl_up_sync(0xffffffffu, pmx, 1), epmn = __shfl_up_sync(0xffffffffu, pmn, 1);
+        double esmx = __shfl_down_sync(0xffffffffu, smx, 1), esmn = __shfl_down_sync(0xffffffffu, smn, 1);
+        if (lane == 0) { epmx = 0.0; epmn = INFINITY; }
+        if (lane == 31) { esmx = 0.0; esmn = INFINITY; }
+        __syncthreads();
+        for (int k = 0; k < 32; ++k) {
+            if (k < wp) { epmx = fmax(epmx, s_wmx[k]); epmn = fmin(epmn, s_wmn[k]); }
+            if (k > wp) { esmx = fmax(esmx, s_wmx[k]); esmn = fmin(esmn, s_wmn[k]); }
+        }
+        // forward: rows r <= j
+        double rmx = epmx, rmn = epmn;
+        for (int j = j0; j < j1; ++j) {
+            const double h = invD[j];
+            rmx = fmax(rmx, h);
+            rmn = fmin(rmn, h);
+            E[j] = (int)__float_as_uint((float)(w[j] * rmx));
+            Sx[j] = (int)__float_as_uint((float)(w[j] * rmn));
+        }
+        // backward: rows r > j, combined with the forward side
+        rmx = esmx;
+        rmn = esmn;
+        for (int j = j1 - 1; j >= j0; --j) {
+            float vmx = __uint_as_float((uint32_t)E[j]), vmn = __uint_as_float((uint32_t)Sx[j]);
+            if (j + 1 < N) {                               // some row lies below the diagonal
+                vmx = fmaxf(vmx, (float)(w[j] * (eL * rmx)));
+                vmn = fminf(vmn, (float)(w[j] * (eL * rmn)));
+            }
+            const uint32_t ux = __float_as_uint(vmx), un = __float_as_uint(vmn);
+            const int ex = (int)(ux >> 23), en = (int)(un >> 23);   // biased exponents (sign bit 0 if >= 0)
+            if (ux == 0u && un == 0u) {
+                E[j] = 255;                                // all-zero column
+            } else {
+                bad |= !(en >= 1 && ex <= 254 && ex - en <= R && ex > R);   // +0 / subnormal / inf / NaN fail
+                E[j] = ex;
+            }
+            const double h = invD[j];
+            rmx = fmax(rmx, h);
+            rmn = fmin(rmn, h);
+        }
+    }
+    bad = __syncthreads_or(bad);
+    if (t == 0) *flag = bad ? 0u : 1u;
+}
+
 // P[i][:] = P0[(i + l) mod N][:] (Thm 2; J_l), 16-byte vectors, one row per CTA row.
 __global__ void __launch_bounds__(256) k_apply_deadtime(const uint4 *__restrict__ P0, uint4 *__restrict__ P,
                                                         int N, int64_t ld_vec, int row_vecs, int l) {
@@ -219,6 +330,12 @@ cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int 
         e = cudaGetLastError();
     }
     return e;
+}
+
+cudaError_t launch_enc_colexp(const VecPtrs base, int64_t vstride, int M, int N, int *colexp, int *scratch,
+                              unsigned *flag, cudaStream_t s) {
+    k_enc_colexp<<<1, 1024, 0, s>>>(base, vstride, N, M, 8, colexp, scratch, flag);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, int dtype, int l,

@@ -87,7 +87,16 @@ struct ColStats {
     int *colexp;                  // [M][N]
     unsigned *flag;               // set to 1 by the build, cleared by a failing column
     int R, zero_col_exp;
+    // encoded storage (fp32, factored entries; emax_part null): colexp and *flag come from
+    // launch_enc_colexp before the build, which then stores every entry as its scaled integer
+    // (fixpt.cuh) when *flag is set, and as fp32 otherwise
+    int enc;
 };
+// Column exponents of the matrices a factored fp32 build is about to write, from the O(N) row
+// normalisers (prefix / suffix extremes of 1/D), and the int8 range test: *flag = every column of
+// every matrix in range (the condition for encoded storage).
+cudaError_t launch_enc_colexp(const VecPtrs base, int64_t vstride, int M, int N, int *colexp, int *scratch,
+                              unsigned *flag, cudaStream_t s);
 cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int dtype, int mode,
                          void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0 = 0, int nrows = -1,
                          double *colsum_part = nullptr, double *colsum = nullptr, ColStats cst = ColStats{});
@@ -149,6 +158,8 @@ int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a);
 struct I8Kernels {
     alignas(64) unsigned char tmap[128];   // CUtensorMap of the stored matrices (a kernel parameter)
     void *step_fn, *colexp_fn, *check_fn, *prep_fn;
+    void *step_enc_fn;        // fp32 matrices stored encoded by a building plan (k_power_step_i8e)
+    size_t step_enc_smem;
     dim3 step_grid, step_block, colexp_grid, colexp_block, small_grid;
     size_t step_smem;
     int rows_per_cta;

@@ -41,6 +41,7 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "fixpt.cuh"
 #include "ptx.cuh"
 #include "tc05.cuh"
 
@@ -65,8 +66,10 @@ template <> struct I8Cfg<double> {
     static constexpr int NP = 8, TN = 64, R = 11, BIAS_MBITS = 1075;
 };
 
+constexpr int kEStages = 4;              // encoded-storage kernel: TMA stages (tile + x image)
+
 struct __align__(8) I8Bars {
-    uint64_t a_full[3], a_empty[3];
+    uint64_t a_full[kEStages], a_empty[kEStages];
     uint64_t s_full[kSBuf], x_full[kSBuf], s_empty[kSBuf];
     uint64_t t_full, t_empty;
 };
@@ -80,27 +83,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 __device__ __forceinline__ void named_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-// PTX shl clamps the shift amount to the register width, so a zero entry (e = 0, shift e - base
-// < 0, i.e. huge as unsigned) gives 0 without a select; k_i8_colexp guarantees base > 0 for every
-// column with a non-zero entry and sets E_j = 255 / 2047 (base > 0 as well) for all-zero columns.
-// fp32: the significand 1.m left-aligned as the 64-bit value (1 : m << 9) = 2^9 sig, shifted left
-// by s = sh + 23 with a clamping funnel shift; the high word is sig << sh (3 integer ops per entry).
-// For a zero entry s < 0 (huge as unsigned) clamps to 32 and the funnel returns the low word, 0.
-__device__ __forceinline__ uint32_t fx32(uint32_t u, int base23) {
-    const uint32_t s = (uint32_t)((int)(u >> 23) - base23);          // e - base + 23
-    uint32_t r;
-    asm("shf.l.clamp.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(u << 9), "r"(1u), "r"(s));
-    return r;
-}
-// fp64: 53-bit significand (hi 21 bits : lo 32 bits) << sh, sh <= 11, as two clamping shifts; a zero
-// entry has sh < 0: both clamp to 0 (the funnel returns the zero low word).
-__device__ __forceinline__ void fx64(uint32_t lo, uint32_t hi, int base, uint32_t &rlo, uint32_t &rhi) {
-    const uint32_t sh = (uint32_t)((int)(hi >> 20) - base);
-    const uint32_t sig_hi = (hi & 0xFFFFFu) | 0x100000u;
-    asm("shf.l.clamp.b32 %0, %1, %2, %3;" : "=r"(rhi) : "r"(lo), "r"(sig_hi), "r"(sh));
-    asm("shl.b32 %0, %1, %2;" : "=r"(rlo) : "r"(lo), "r"(sh));
-}
-
 // Walks the units (active matrix ai, column tile c, k-block kb) of a CTA's range without divisions.
 struct UnitCursor {
     int64_t g;     // ai * tiles + c
@@ -129,11 +111,12 @@ struct Ring {
     }
 };
 
-// Byte-plane image of a unit (the MMA's B operand, MN-major SWIZZLE_NONE): core matrices of
-// 8 rows x 16 columns, all NP planes of one 8-row group side by side, so that one MMA with N = 256
-// spans 256 / TN consecutive planes (their accumulators are adjacent in TMEM):
-//   offset(p, r, j) = (r / 8) * 4096 + (p * TN / 16 + j / 16) * 128 + (r % 8) * 16 + j % 16.
-// LBO (next 8 rows) = 4096 B, SBO (next 16 columns) = 128 B.
+// Byte image of a unit (the MMA's B operand, MN-major SWIZZLE_NONE) in the "word layout": B column
+// n = W j + p is byte p (little-endian) of column j's scaled integer, so a row of B is the row of
+// scaled integers as they sit in memory. Core matrices of 8 rows x 16 bytes:
+//   offset(r, n) = (r / 8) * 4096 + (n / 16) * 128 + (r % 8) * 16 + n % 16,
+// LBO (next 8 rows) = 4096 B, SBO (next 16 bytes of n) = 128 B; one MMA with N = 256 spans 64 fp32 /
+// 32 fp64 columns (their accumulators are adjacent in TMEM).
 constexpr int kKGroup = 4096;
 
 // The unit's tile arrives in shared memory as 4 tensor-map boxes of [64 rows][128 B] with the
@@ -144,6 +127,8 @@ constexpr int kKGroup = 4096;
 constexpr int kBoxBytes = kKB * 128;
 constexpr int kAStages = 3;
 constexpr int kABytes = 4 * kBoxBytes;       // 32 KB
+constexpr int kEStaging = 2 * 16 * 129 * 8 + 1024;   // the epilogue's staging (stage[2][16][129] doubles)
+constexpr size_t kI8eSmem = 1024 + kEStages * (size_t)(kABytes + kXBytes) + kEStaging + 1024;
 
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar) {
     asm volatile(
@@ -486,6 +471,129 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
     }
 }
 
+// k_power_step_i8e: the same GEMV for a matrix a building plan stored ENCODED (build.cu, fp32 storage
+// with every column in range): each 4-byte entry already holds its scaled integer a~_rj (fixpt.cuh),
+// so the TMA boxes of a unit ARE the MMA's B operand -- MN-major with the 128-byte swizzle the tensor
+// map applies (CuTe's canonical ((T,8,m),(8,k)):((1,T,LBO),(8T,SBO)) layout: LBO = the next 128-byte
+// column span = the next box, SBO = the next 8 rows = 1024 B; tools/probe/umma_sw128_probe.cu). No
+// converters: per unit the producer loads the tile and the x-slice image into one of 4 stages, the MMA
+// issuer consumes it, and the epilogue is the converter kernel's. Warps 4-11 only run the epilogue.
+__global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8e(const PowerArgs a, const __grid_constant__ CUtensorMap tmap) {
+    using T = float;
+    using C = I8Cfg<T>;
+    constexpr int NP = C::NP, TN = C::TN;
+    if (!a.glob[3]) return;                             // range test failed: stored as fp32, DMMA runs
+    const int N = a.N;
+    const int tiles = N / TN, kbs = N / kKB;
+    const int n_act = a.i8_dbg ? a.M : (int)a.glob[2];
+    const int64_t T_units = (int64_t)n_act * tiles * kbs;
+    if (T_units == 0) return;
+    const int G = gridDim.x, b = blockIdx.x;
+    int64_t U = (T_units + G - 1) / G;
+    if (U < 2) U = 2;
+    const int64_t u_begin = (int64_t)b * U;
+    if (u_begin >= T_units) return;
+    const int64_t u_end = u_begin + U < T_units ? u_begin + U : T_units;
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    unsigned char *sA = smem;                                       // [4][4 boxes][64][128]
+    unsigned char *sX = sA + kEStages * kABytes;                    // [4][8 KB]
+    unsigned char *sS = sX + kEStages * kXBytes;                    // epilogue staging
+    I8Bars *bars = reinterpret_cast<I8Bars *>(sS + kEStaging);
+    __shared__ uint32_t s_tmem;
+    __shared__ int s_vmap[kMaxVectors], s_cur[kMaxVectors], s_tau[kMaxVectors], s_nact, s_last;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kEStages; ++i) {
+            mbar_init(&bars->a_full[i], 1);
+            mbar_init(&bars->a_empty[i], 1);
+        }
+        mbar_init(&bars->t_full, 1);
+        mbar_init(&bars->t_empty, 8);
+        fence_mbar_init();
+    }
+    if (warp == 2) tc05::alloc<512>(&s_tmem);
+    tc05::fence_before();
+    __syncthreads();
+    tc05::fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 3) {
+        // ------------------------------------------------------------------ TMA producer (tile + x)
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+            UnitCursor cu(u_begin, kbs, tiles);
+            Ring<kEStages> ra;
+            for (int64_t u = u_begin; u < u_end; ++u, cu.next(kbs, tiles), ra.next()) {
+                const int m = a.i8_dbg ? cu.ai : a.act[cu.ai];
+                mbar_wait(&bars->a_empty[ra.i], ra.ph ^ 1);
+                mbar_expect_tx(&bars->a_full[ra.i], kABytes + kXBytes);
+                unsigned char *dst = sA + ra.i * kABytes;
+#pragma unroll
+                for (int bx = 0; bx < 4; ++bx)
+                    tma_load_3d(dst + bx * kBoxBytes, &tmap, cu.c * TN + bx * 32, cu.kb * kKB, m, &bars->a_full[ra.i]);
+                bulk_g2s(sX + ra.i * kXBytes, a.ximg + ((size_t)m * kbs + cu.kb) * kXBytes, kXBytes, &bars->a_full[ra.i]);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = tc05::idesc_i8(128, 256, true);
+            const uint32_t sA_u = smem_u32(sA), sX_u = smem_u32(sX);
+            int piece = 0;
+            UnitCursor cu(u_begin, kbs, tiles);
+            Ring<kEStages> ra;
+            for (int64_t u = u_begin; u < u_end; ++u, cu.next(kbs, tiles), ra.next()) {
+                const bool first = u == u_begin || cu.kb == 0;
+                const bool last = u + 1 == u_end || cu.kb + 1 == kbs;
+                if (first) {
+                    mbar_wait(&bars->t_empty, (piece & 1) ^ 1);
+                    tc05::fence_after();
+                }
+                mbar_wait(&bars->a_full[ra.i], ra.ph);
+                tc05::fence_after();
+                // per k-step of 32 rows, 2 MMAs of N = 256 bytes (64 columns = boxes 2h, 2h + 1)
+#pragma unroll
+                for (int h = 0; h < NP * TN / 256; ++h) {
+                    if (a.i8_dbg & 2) break;
+#pragma unroll
+                    for (int s = 0; s < kKB / 32; ++s) {
+                        const uint64_t ad = tc05::smem_desc(sX_u + ra.i * kXBytes + s * 256, 128, 512);
+                        const uint64_t bd = tc05::smem_desc(sA_u + ra.i * kABytes + 2 * h * kBoxBytes + s * 32 * 128,
+                                                            kBoxBytes, 1024) | (2ull << 61);   // SWIZZLE_128B
+                        tc05::mma_i8(tmem + (uint32_t)(h * 256), ad, bd, idesc, (first && s == 0) ? 0u : 1u);
+                    }
+                }
+                tc05::commit(&bars->a_empty[ra.i]);
+                if (last) {
+                    tc05::commit(&bars->t_full);
+                    ++piece;
+                }
+            }
+        }
+    } else if (warp >= kI8Conv0) {
+        // ------------------------------------------------------------------ epilogue
+        int piece = 0;
+        UnitCursor cc(u_begin, kbs, tiles);
+        for (int64_t u = u_begin; u < u_end; ++u, cc.next(kbs, tiles)) {
+            if (u + 1 == u_end || cc.kb + 1 == kbs) {
+                const int m = a.i8_dbg ? cc.ai : a.act[cc.ai];
+                const PieceCtx pc{m, cc.c, cc.g};
+                epilogue<T>(a, pc, tmem, sS, bars, piece, U, b, s_vmap, s_cur, s_tau, &s_nact, &s_last);
+                ++piece;
+            }
+        }
+    }
+    tc05::fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc05::fence_after();
+        tc05::dealloc<512>(tmem);
+    }
+}
+
 // Column exponents E_j (largest biased exponent of column j) and the range test, in three steps:
 // k_i8_prep (flag = 1, E_j = 0, e_min_j = INT_MAX), k_i8_colexp (a CTA per 128 columns x a chunk of
 // rows: one warp reads 512 B / 1 KB of a row, every lane 4 consecutive columns; atomicMax / atomicMin
@@ -607,6 +715,8 @@ cudaError_t i8_kernels(int dtype, I8Kernels *k, const PowerArgs &a) {
     k->check_fn = f64 ? (void *)k_i8_colcheck<double> : (void *)k_i8_colcheck<float>;
     k->prep_fn = (void *)k_i8_prep;
     k->step_smem = kI8Smem;
+    k->step_enc_fn = f64 ? nullptr : (void *)k_power_step_i8e;
+    k->step_enc_smem = kI8eSmem;
     k->step_block = dim3(kI8Threads);
     const int sms = device_sm_count() < kMaxSMs ? device_sm_count() : kMaxSMs;
     k->step_grid = dim3(sms);
@@ -618,7 +728,9 @@ cudaError_t i8_kernels(int dtype, I8Kernels *k, const PowerArgs &a) {
     k->colexp_grid = dim3(ct, rc, a.M);
     k->colexp_block = dim3(256);
     k->small_grid = dim3(2 * sms);
-    return func_attrs_once(k->step_fn, (int)kI8Smem, false);
+    e = func_attrs_once(k->step_fn, (int)kI8Smem, false);
+    if (e == cudaSuccess && k->step_enc_fn) e = func_attrs_once(k->step_enc_fn, (int)kI8eSmem, false);
+    return e;
 }
 
 int i8_range_bits(int dtype) { return dtype == SPLIDAR_F64 ? I8Cfg<double>::R : I8Cfg<float>::R; }

@@ -118,3 +118,71 @@ def test_building_plan_batched_int8(spl, monkeypatch):
     assert kind == "tensor_i8"
     assert [i["iters"] for i in ia] == [i["iters"] for i in ib]
     assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-13
+
+
+def _encode_ref(P):
+    """Test-side encoding of an fp32 matrix: column j's entries as sig << (e - E_j + 8), E_j the
+    column's largest biased exponent (the int8 GEMV's scaled integers); None if out of range."""
+    u = P.view(np.uint32).astype(np.uint64)
+    e = ((u >> 23) & 0xFF).astype(np.int64)
+    nz = (u & 0x7FFFFFFF) != 0
+    E = np.where(nz, e, 0).max(axis=0)
+    emin = np.where(nz, e, 1 << 20).min(axis=0)
+    if np.any((E - emin > 8) & (emin < (1 << 20))) or np.any(E <= 8):
+        return None
+    sig = (u & 0x7FFFFF) | 0x800000
+    sh = e - E[None, :] + 8
+    w = np.where(nz, sig << np.clip(sh, 0, 63).astype(np.uint64), 0)
+    assert np.all(w < 2 ** 32)
+    return w.astype(np.uint32)
+
+
+@pytest.mark.parametrize("enc_env", ["1", "0"])
+def test_building_plan_encoded_storage(spl, monkeypatch, enc_env):
+    """fp32 factored building plans on the int8 GEMV store P~0 encoded: every entry as its column's
+    scaled integer, with the column exponents derived from 1/D before the build (k_enc_colexp). The
+    stored words must equal the test-side encoding of the separately built fp32 matrix, bit for bit
+    (SPLIDAR_I8_ENC=0: plain fp32), and pi must equal the separate plan's."""
+    monkeypatch.setenv("SPLIDAR_I8_ENC", enc_env)
+    rng = np.random.default_rng(5)
+    w = config(5)
+    for N, f in ((4096, _c5(4096)), (2176, random_flux(rng, 2176, 2, sigma_bins=(1, 10), s_range=(0.5, 1.5),
+                                                       b_range=(0.2, 1.0)))):
+        f = Flux(f.t_r, N, f.tau, f.sigma, f.signal, f.background)
+        T = np.array([([w.items[0].t_d] + [it.t_d for it in w.sweep])[:17]])
+        monkeypatch.setenv("SPLIDAR_FUSED", "0")
+        P0 = spl.empty_matrix(N, torch.float32, n_matrices=1)
+        pa = spl.Plan(P0, f.t_r, T, tol=1e-12, build=[f])
+        ia = pa.execute()
+        assert pa.gemv() == "tensor_i8"
+        stored = P0[0].contiguous().cpu().numpy()
+        pia = pa.pi.detach().cpu().numpy().copy()
+        pa.close()
+        ref = spl.build_base(f, torch.float32).cpu().numpy()
+        want = _encode_ref(ref)
+        assert want is not None
+        if enc_env == "1":
+            assert np.array_equal(stored.view(np.uint32), want)
+        else:
+            assert np.array_equal(stored.view(np.uint32), ref.view(np.uint32))
+        pb = spl.Plan(spl.build_base(f, torch.float32), f.t_r, T, tol=1e-12)
+        ib = pb.execute()
+        pib = pb.pi.detach().cpu().numpy().copy()
+        pb.close()
+        assert [i["iters"] for i in ia] == [i["iters"] for i in ib]
+        assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-13
+
+
+def test_building_plan_encoded_out_of_range(spl):
+    """A flux whose columns span more than 2^8 (Lambda = 61): the encoded build falls back to plain
+    fp32 storage and the FP64 GEMV (the stored matrix equals the separate fp32 build)."""
+    f = Flux(200.0, 4096, (60.0,), (0.5,), (60.0,), 1.0)
+    T = np.array([[10.0, 30.0, 50.0, 70.0, 90.0, 110.0, 130.0, 150.0]])
+    P0 = spl.empty_matrix(4096, torch.float32, n_matrices=1)
+    pa = spl.Plan(P0, f.t_r, T, tol=1e-12, build=[f])
+    pa.execute()
+    assert pa.gemv() == "fp64"
+    ref = spl.build_base(f, torch.float32).cpu().numpy()
+    assert _encode_ref(ref) is None
+    assert np.array_equal(P0[0].contiguous().cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    pa.close()
