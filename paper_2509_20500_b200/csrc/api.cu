@@ -485,7 +485,8 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
             a.i8_dbg = d ? atoi(d) : 0;
             a.strips_i8 = L.N / i8_tile_cols(dt);
             const char *ev = getenv("SPLIDAR_I8_ENC");
-            p->enc = p->with_build && dt == SPLIDAR_F32 && p->bmode == SPLIDAR_ENTRY_FACTORED && !(ev && ev[0] == '0');
+            p->enc = p->with_build && dt == SPLIDAR_F32 && p->bmode == SPLIDAR_ENTRY_FACTORED && L.N <= 131072 &&
+                     !(ev && ev[0] == '0');
         }
     }
 

@@ -205,86 +205,86 @@ __global__ void __launch_bounds__(256) k_colsum_reduce(const double *__restrict_
 // Column exponents for encoded storage, before the build writes anything. Factored entries are
 // P~0[r][j] = fl32(w_j * h_r) with h_r = 1/D_r for r <= j and fl(e^{-Lambda} / D_r) for r > j (k_build),
 // and fl(w * x) is non-decreasing in x, so column j's largest / smallest entries are w_j times the
-// extremes of 1/D over r <= j (prefix) and e^{-Lambda} times those over r > j (suffix). One CTA walks
-// the matrices: thread t owns columns [t C, t C + C); warp shuffles and the warp totals give each
-// thread the extremes before and after its chunk; a forward pass leaves the prefix-side extremes of
-// every column in colexp / scratch (as fp32 bits), a backward pass combines them with the suffix side
-// and writes E_j. The range test is k_i8_colcheck's (a column fails if its smallest entry is not a
-// normal fp32 number, lies more than 2^R below the largest, or the largest exponent is <= R); an
-// all-zero column (w_j = 0) gets E_j = 255.
-__global__ void __launch_bounds__(1024) k_enc_colexp(const VecPtrs base, int64_t vstride, int N, int M, int R,
-                                                     int *__restrict__ colexp, int *__restrict__ scratch,
-                                                     unsigned *__restrict__ flag) {
-    __shared__ double s_wmx[32], s_wmn[32];
+// extremes of 1/D over r <= j (prefix) and e^{-Lambda} times those over r > j (suffix). Grid
+// (column blocks of 1024, matrices); a thread per column. Every CTA first reduces the extremes of all
+// blocks (one warp per block, coalesced: the 1/D vector is L2-resident), then a warp-shuffle scan plus
+// the warp and block totals give its columns the inclusive prefix and exclusive suffix extremes. The
+// range test is k_i8_colcheck's (a column fails if its smallest entry is not a normal fp32 number, lies
+// more than 2^R below the largest, or the largest exponent is <= R); an all-zero column (w_j = 0) gets
+// E_j = 255. Each CTA writes whether one of its columns failed; k_enc_flag folds those into the flag.
+constexpr int kEncBlock = 1024;
+constexpr int kEncMaxBlocks = 128;        // N <= 131072
+
+__global__ void __launch_bounds__(kEncBlock) k_enc_colexp(const VecPtrs base, int64_t vstride, int N, int R,
+                                                          int *__restrict__ colexp, int *__restrict__ bad_out) {
+    __shared__ double s_bmx[kEncMaxBlocks], s_bmn[kEncMaxBlocks], s_wmx[32], s_wmn[32];
+    const int m = blockIdx.y, nb = gridDim.x, bk = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
-    const int C = (N + 1023) / 1024;
-    const int j0 = min(N, t * C), j1 = min(N, j0 + C);
-    bool bad = false;
-    for (int m = 0; m < M; ++m) {
-        const double *__restrict__ invD = base.invD + m * vstride;
-        const double *__restrict__ w = base.w + m * vstride;
-        const double eL = base.scal[m * 8 + 1];
-        int *__restrict__ E = colexp + (size_t)m * N;
-        int *__restrict__ Sx = scratch + (size_t)m * N;
-        double cmx = 0.0, cmn = INFINITY;                  // this chunk's extremes of 1/D
-        for (int j = j0; j < j1; ++j) {
+    const double *__restrict__ invD = base.invD + m * vstride;
+    const double *__restrict__ w = base.w + m * vstride;
+    const double eL = base.scal[m * 8 + 1];
+    for (int b2 = wp; b2 < nb; b2 += kEncBlock / 32) {          // extremes of every block
+        double mx = 0.0, mn = INFINITY;
+        for (int j = b2 * kEncBlock + lane; j < min(N, (b2 + 1) * kEncBlock); j += 32) {
             const double h = invD[j];
-            cmx = fmax(cmx, h);
-            cmn = fmin(cmn, h);
+            mx = fmax(mx, h);
+            mn = fmin(mn, h);
         }
-        // exclusive extremes of the chunks before (p*) and after (s*) this one
-        double pmx = cmx, pmn = cmn, smx = cmx, smn = cmn;  // inclusive warp scans
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double a = __shfl_up_sync(0xffffffffu, pmx, o), b2 = __shfl_up_sync(0xffffffffu, pmn, o);
-            const double c = __shfl_down_sync(0xffffffffu, smx, o), d = __shfl_down_sync(0xffffffffu, smn, o);
-            if (lane >= o) { pmx = fmax(pmx, a); pmn = fmin(pmn, b2); }
-            if (lane + o < 32) { smx = fmax(smx, c); smn = fmin(smn, d); }
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         }
-        __syncthreads();                                   // previous matrix done with s_w*
-        if (lane == 31) { s_wmx[wp] = pmx; s_wmn[wp] = pmn; }
-        double epmx = __shfl_up_sync(0xffffffffu, pmx, 1), epmn = __shfl_up_sync(0xffffffffu, pmn, 1);
-        double esmx = __shfl_down_sync(0xffffffffu, smx, 1), esmn = __shfl_down_sync(0xffffffffu, smn, 1);
-        if (lane == 0) { epmx = 0.0; epmn = INFINITY; }
-        if (lane == 31) { esmx = 0.0; esmn = INFINITY; }
-        __syncthreads();
-        for (int k = 0; k < 32; ++k) {
-            if (k < wp) { epmx = fmax(epmx, s_wmx[k]); epmn = fmin(epmn, s_wmn[k]); }
-            if (k > wp) { esmx = fmax(esmx, s_wmx[k]); esmn = fmin(esmn, s_wmn[k]); }
+        if (lane == 0) { s_bmx[b2] = mx; s_bmn[b2] = mn; }
+    }
+    const int j = bk * kEncBlock + t;
+    const double h = j < N ? invD[j] : 0.0;
+    double pmx = h, pmn = j < N ? h : INFINITY, smx = pmx, smn = pmn;   // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double a = __shfl_up_sync(0xffffffffu, pmx, o), b2 = __shfl_up_sync(0xffffffffu, pmn, o);
+        const double c = __shfl_down_sync(0xffffffffu, smx, o), d = __shfl_down_sync(0xffffffffu, smn, o);
+        if (lane >= o) { pmx = fmax(pmx, a); pmn = fmin(pmn, b2); }
+        if (lane + o < 32) { smx = fmax(smx, c); smn = fmin(smn, d); }
+    }
+    if (lane == 31) { s_wmx[wp] = pmx; s_wmn[wp] = pmn; }       // warp totals
+    double xsmx = __shfl_down_sync(0xffffffffu, smx, 1), xsmn = __shfl_down_sync(0xffffffffu, smn, 1);
+    if (lane == 31) { xsmx = 0.0; xsmn = INFINITY; }            // exclusive suffix within the warp
+    __syncthreads();
+    for (int k = 0; k < 32; ++k) {
+        if (k < wp) { pmx = fmax(pmx, s_wmx[k]); pmn = fmin(pmn, s_wmn[k]); }
+        if (k > wp) { xsmx = fmax(xsmx, s_wmx[k]); xsmn = fmin(xsmn, s_wmn[k]); }
+    }
+    for (int k = 0; k < nb; ++k) {
+        if (k < bk) { pmx = fmax(pmx, s_bmx[k]); pmn = fmin(pmn, s_bmn[k]); }
+        if (k > bk) { xsmx = fmax(xsmx, s_bmx[k]); xsmn = fmin(xsmn, s_bmn[k]); }
+    }
+    bool bad = false;
+    if (j < N) {
+        float vmx = (float)(w[j] * pmx), vmn = (float)(w[j] * pmn);    // rows r <= j
+        if (j + 1 < N) {                                                 // rows r > j
+            vmx = fmaxf(vmx, (float)(w[j] * (eL * xsmx)));
+            vmn = fminf(vmn, (float)(w[j] * (eL * xsmn)));
         }
-        // forward: rows r <= j
-        double rmx = epmx, rmn = epmn;
-        for (int j = j0; j < j1; ++j) {
-            const double h = invD[j];
-            rmx = fmax(rmx, h);
-            rmn = fmin(rmn, h);
-            E[j] = (int)__float_as_uint((float)(w[j] * rmx));
-            Sx[j] = (int)__float_as_uint((float)(w[j] * rmn));
-        }
-        // backward: rows r > j, combined with the forward side
-        rmx = esmx;
-        rmn = esmn;
-        for (int j = j1 - 1; j >= j0; --j) {
-            float vmx = __uint_as_float((uint32_t)E[j]), vmn = __uint_as_float((uint32_t)Sx[j]);
-            if (j + 1 < N) {                               // some row lies below the diagonal
-                vmx = fmaxf(vmx, (float)(w[j] * (eL * rmx)));
-                vmn = fminf(vmn, (float)(w[j] * (eL * rmn)));
-            }
-            const uint32_t ux = __float_as_uint(vmx), un = __float_as_uint(vmn);
-            const int ex = (int)(ux >> 23), en = (int)(un >> 23);   // biased exponents (sign bit 0 if >= 0)
-            if (ux == 0u && un == 0u) {
-                E[j] = 255;                                // all-zero column
-            } else {
-                bad |= !(en >= 1 && ex <= 254 && ex - en <= R && ex > R);   // +0 / subnormal / inf / NaN fail
-                E[j] = ex;
-            }
-            const double h = invD[j];
-            rmx = fmax(rmx, h);
-            rmn = fmin(rmn, h);
+        const uint32_t ux = __float_as_uint(vmx), un = __float_as_uint(vmn);
+        const int ex = (int)(ux >> 23), en = (int)(un >> 23);           // biased exponents (entries >= 0)
+        if (ux == 0u && un == 0u) {
+            colexp[(size_t)m * N + j] = 255;                             // all-zero column
+        } else {
+            bad = !(en >= 1 && ex <= 254 && ex - en <= R && ex > R);     // +0 / subnormal / inf / NaN fail
+            colexp[(size_t)m * N + j] = ex;
         }
     }
     bad = __syncthreads_or(bad);
-    if (t == 0) *flag = bad ? 0u : 1u;
+    if (t == 0) bad_out[m * nb + bk] = bad ? 1 : 0;
+}
+
+// flag = no CTA of k_enc_colexp saw a failing column.
+__global__ void k_enc_flag(const int *__restrict__ bad, int n, unsigned *__restrict__ flag) {
+    int any = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) any |= bad[i];
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) *flag = any ? 0u : 1u;
 }
 
 // P[i][:] = P0[(i + l) mod N][:] (Thm 2; J_l), 16-byte vectors, one row per CTA row.
@@ -334,7 +334,10 @@ cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int 
 
 cudaError_t launch_enc_colexp(const VecPtrs base, int64_t vstride, int M, int N, int *colexp, int *scratch,
                               unsigned *flag, cudaStream_t s) {
-    k_enc_colexp<<<1, 1024, 0, s>>>(base, vstride, N, M, 8, colexp, scratch, flag);
+    const int nb = (N + kEncBlock - 1) / kEncBlock;
+    if (nb > kEncMaxBlocks) return cudaErrorInvalidValue;
+    k_enc_colexp<<<dim3(nb, M), kEncBlock, 0, s>>>(base, vstride, N, 8, colexp, scratch);
+    k_enc_flag<<<1, 256, 0, s>>>(scratch, nb * M, flag);
     return cudaGetLastError();
 }
 
