@@ -34,6 +34,8 @@ import numpy as np  # noqa: E402
 
 METRIC = "stationary solves/s (with transition-matrix entries/s; % of HBM roofline)"
 GEMV_KERNELS = {"tensor_i8": "k_power_step_i8 (tcgen05 kind::i8 exact split, TMEM accumulators)",
+                "tensor_i8_encoded": "k_power_step_i8e (tcgen05 kind::i8 on encoded fp32 storage: TMA tiles are "
+                                     "the MMA operand, TMEM accumulators)",
                 "fp64": "k_power_step (FP64 tensor cores / DFMA)", "fused": "k_power_fused (cluster, small N)"}
 UNIT = "solves/s"
 
@@ -261,7 +263,8 @@ def run_ours(args, rank, world, dev):
     t_build = min(t_b * len(ev), t_total)
     t_solve = t_total - t_build
     infos = st.infos()
-    gemv_kinds = sorted({p.gemv() for p in st.plans})
+    gemv_kinds = sorted({p.gemv() + ("_encoded" if p.gemv() == "tensor_i8" and p.storage() == "encoded" else "")
+                         for p in st.plans})
     from paper_2509_20500_b200.shard import max_over_ranks
     t_total, t_build, t_solve = max_over_ranks([t_total, t_build, t_solve], device="cuda")
 
@@ -277,23 +280,24 @@ def run_ours(args, rank, world, dev):
             per_m = np.maximum(per_m - 1, 0)
         launches_gemv += int(per_m.max())
         gemv_bytes += int(per_m.sum()) * N * N * b
-    # parameter upload (none for one small profile, passed by value) + step-1 vector kernels (k_vec_small
-    # when N + 1 <= 8192, else k_vec_a..e) + k_build, then per plan: one fused launch, or init + (GEMV + check) per iteration + finish
+    # every plan builds its matrices (fluxes stay in the plan's workspace: no upload): the step-1 vector
+    # kernels (k_vec_small when N + 1 <= 8192, else k_vec_a..e) + k_build; encoded fp32 storage adds the
+    # column-exponent pass before the build (k_enc_colexp + k_enc_flag). Then a fused plan is one launch;
+    # a graph plan: column-sum reduce, init, ssum + check (iteration 1 from the column sums), GEMV + check
+    # per further iteration, finish; int8 plans add the FP64 GEMV's early exit per iteration
     small = N + 1 <= 8192
-    prelude = (0 if small and len(st.fluxes) == 1 else 1) + (1 if small else 5) + 1
-    if graphed:
-        per_step_launches = prelude + len(st.plans)
-    else:
-        # graph plans: init + finish, and per iteration GEMV + check; int8 plans add the range test
-        # (prep, column exponents, column check) and per iteration the FP64 GEMV's early exit
-        # building graph plans: the build (prelude) + column-sum reduce, init, ssum + check (iteration 1),
-        # then per further iteration GEMV + check, finish; int8 plans add the FP64 GEMV's early exit per
-        # iteration (their range test comes from the build)
-        def plan_launches(pi, p):
-            it = int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
-            n = 1 + 1 + 2 + 2 * (it - 1) + 1
-            return n if p.gemv() != "tensor_i8" else n + (it - 1)
-        per_step_launches = prelude + sum(plan_launches(pi, p) for pi, p in zip(infos, st.plans))
+    prelude = (1 if small else 5) + 1
+    storages = [p.storage() for p in st.plans]
+
+    def plan_launches(pi, p, storage):
+        if p.fused:
+            return prelude + 1
+        it = int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
+        n = prelude + 1 + 1 + 2 + 2 * (it - 1) + 1
+        if p.gemv() == "tensor_i8":
+            n += it - 1
+        return n + (2 if storage == "encoded" else 0)
+    per_step_launches = sum(plan_launches(pi, p, sg) for pi, p, sg in zip(infos, st.plans, storages))
     hbm, hbm_src = load_peaks()
     traffic = load_traffic(args.workload, args.dtype)
     K = args.steps
@@ -330,7 +334,8 @@ def run_ours(args, rank, world, dev):
         "roofline": {"bound": "hbm", "kernel": GEMV_KERNELS.get(gemv_kinds[0], gemv_kinds[0]) + " (power-iteration GEMV)"
                      if len(gemv_kinds) == 1 else "+".join(gemv_kinds), "achieved": gemv_gbs,
                      "peak": hbm, "unit": "GB/s", "frac": gemv_gbs / hbm,
-                     "traffic": (traffic.get("k_power_step_i8" if gemv_kinds == ["tensor_i8"] else "k_power_step")
+                     "traffic": (traffic.get({"tensor_i8": "k_power_step_i8",
+                                              "tensor_i8_encoded": "k_power_step_i8e"}.get(gemv_kinds[0], "k_power_step"))
                                  if traffic else None),
                      "algorithmic_bytes_per_launch": N * N * b,
                      "traffic_source": traffic.get("source") if traffic else None,

@@ -208,7 +208,15 @@ splidar_status splidar_plan_execute(splidar_plan plan, splidar_solve_info *info 
  * sums unchanged (Thm 2) -- so iteration 1 of every dead time comes from those sums and the
  * GEMV passes start at iteration 2 (one matrix pass fewer per solve; same iterates up to the order
  * of the column sums). All fluxes share N and t_r. ws: splidar_workspace_bytes(N, n_matrices,
- * n_vectors); otherwise as splidar_plan_create. */
+ * n_vectors); otherwise as splidar_plan_create.
+ * Encoded storage: an fp32 plan with factored entries that runs the int8 GEMV (see splidar_plan_gemv)
+ * and N <= 131072 first derives every column's largest exponent E_j from the row normalisers (the
+ * column's extreme entries are w_j times the extremes of 1/D above and below the diagonal); when
+ * every column passes the int8 range test it stores each entry of P0 not as fp32 but as its column's
+ * scaled integer, the u32 word sig << (e - E_j + 8) (sig = the 24-bit significand, e = the biased
+ * exponent; the same value, exactly), and the GEMV feeds those words to the tensor cores as they
+ * arrive (no conversion pass). Such a P0 is an internal buffer: splidar_plan_storage tells which
+ * form the last launch left; SPLIDAR_I8_ENC=0 at plan creation keeps fp32. */
 splidar_status splidar_plan_create_build(splidar_plan *plan, const splidar_flux *fluxes, int32_t n_matrices,
                                          splidar_entry mode, splidar_dtype dt, void *P0, int64_t matrix_stride,
                                          int64_t ld, const double *t_d, int32_t n_vectors, double tol,
@@ -245,6 +253,12 @@ int splidar_plan_kind(splidar_plan plan);
 #define SPLIDAR_GEMV_FP64 1
 #define SPLIDAR_GEMV_TENSOR_I8 2
 int splidar_plan_gemv(splidar_plan plan, void *stream);
+/* The form of P0 after the plan's last launch (synchronises the stream once): SPLIDAR_STORAGE_IEEE
+ * (the dtype's numbers) or SPLIDAR_STORAGE_ENCODED (a building plan's per-column scaled integers, see
+ * splidar_plan_create_build); -1: NULL plan or CUDA error. */
+#define SPLIDAR_STORAGE_IEEE 0
+#define SPLIDAR_STORAGE_ENCODED 1
+int splidar_plan_storage(splidar_plan plan, void *stream);
 
 /* ---------------------------------------------------------------------------------------------
  * Row shards of one matrix over several GPUs: the power iteration of P:79 with

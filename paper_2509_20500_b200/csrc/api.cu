@@ -842,6 +842,13 @@ int splidar_plan_gemv(splidar_plan plan, void *stream) {
     return flag ? SPLIDAR_GEMV_TENSOR_I8 : SPLIDAR_GEMV_FP64;
 }
 
+int splidar_plan_storage(splidar_plan plan, void *stream) {
+    if (!plan) return -1;
+    if (!plan->enc) return SPLIDAR_STORAGE_IEEE;
+    const int g = splidar_plan_gemv(plan, stream);   // encoded exactly when the range test passed
+    return g < 0 ? -1 : g == SPLIDAR_GEMV_TENSOR_I8 ? SPLIDAR_STORAGE_ENCODED : SPLIDAR_STORAGE_IEEE;
+}
+
 splidar_status splidar_plan_launch(splidar_plan plan, void *stream) {
     SPL_NVTX_RANGE();
     if (!plan) return SPLIDAR_EINVAL;

@@ -102,6 +102,7 @@ def _lib():
             "splidar_plan_destroy": (None, [p]),
             "splidar_plan_kind": (C.c_int, [p]),
             "splidar_plan_gemv": (C.c_int, [p, p]),
+            "splidar_plan_storage": (C.c_int, [p, p]),
             "splidar_build_base_rows": (st, [fp, st, st, p, i64, i32, i32, p, sz, p]),
             "splidar_plan_create_rows": (st, [C.POINTER(p), p, i32, i32, i32, i64, st, d, p, i32, d, i32, p, p, p,
                                               sz, p]),
@@ -493,6 +494,14 @@ class Plan:
         if k < 0:
             raise SplidarError(ECUDA, "splidar_plan_gemv")
         return self.GEMV_NAMES[k]
+
+    def storage(self, stream=None) -> str:
+        """The form of P0 after the last launch: 'ieee' or 'encoded' (a building plan's per-column
+        scaled integers, splidar_plan_create_build). Synchronises the stream."""
+        k = _lib().splidar_plan_storage(self._h, _stream(stream))
+        if k < 0:
+            raise SplidarError(ECUDA, "splidar_plan_storage")
+        return ("ieee", "encoded")[k]
 
     def info(self, stream=None, check: bool = True) -> list:
         infos = (SolveInfo * (self.M * self.V))()

@@ -155,6 +155,7 @@ def test_building_plan_encoded_storage(spl, monkeypatch, enc_env):
         pa = spl.Plan(P0, f.t_r, T, tol=1e-12, build=[f])
         ia = pa.execute()
         assert pa.gemv() == "tensor_i8"
+        assert pa.storage() == ("encoded" if enc_env == "1" else "ieee")
         stored = P0[0].contiguous().cpu().numpy()
         pia = pa.pi.detach().cpu().numpy().copy()
         pa.close()
@@ -181,7 +182,7 @@ def test_building_plan_encoded_out_of_range(spl):
     P0 = spl.empty_matrix(4096, torch.float32, n_matrices=1)
     pa = spl.Plan(P0, f.t_r, T, tol=1e-12, build=[f])
     pa.execute()
-    assert pa.gemv() == "fp64"
+    assert pa.gemv() == "fp64" and pa.storage() == "ieee"
     ref = spl.build_base(f, torch.float32).cpu().numpy()
     assert _encode_ref(ref) is None
     assert np.array_equal(P0[0].contiguous().cpu().numpy().view(np.uint32), ref.view(np.uint32))

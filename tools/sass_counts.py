@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2509_20500_b200", "lib", "libsplidar.so")
 OPS = ["UTCIMMA", "LDTM", "UTCBAR", "UTMALDG", "UBLKCP", "DMMA", "DFMA", "DADD", "DMUL", "SYNCS", "PRMT",
        "LDS", "STS", "LDG", "STG", "SHFL", "BAR", "MUFU", "F2F"]
-WANT = ["k_power_step_i8IfE", "k_power_step_i8IdE", "k_power_stepIdLi17E", "k_power_stepIfLi17E", "k_power_stepIdLi1E",
+WANT = ["k_power_step_i8IfE", "k_power_step_i8e", "k_enc_colexp", "k_power_step_i8IdE", "k_power_stepIdLi17E", "k_power_stepIfLi17E", "k_power_stepIdLi1E",
         "k_power_check", "k_i8_colexpIfE", "k_buildIdLi0E", "k_power_fusedIdLi1E", "k_struct_solve_c1", "k_mc"]
 
 sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
