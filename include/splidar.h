@@ -242,7 +242,7 @@ int splidar_plan_kind(splidar_plan plan);
  *   SPLIDAR_GEMV_TENSOR_I8 (2): the exact int8 split on the 5th-generation tensor cores
  *     (tcgen05.mma kind::i8, TMEM accumulators): P~0 in u8 planes with one exponent per column,
  *     x in 7 u8 slices (truncation < 2^-56 of the largest x); used for fp32 storage when the plan
- *     has 8..18 dead times per matrix, N % 128 == 0 and N >= 1024 (fp64 storage only with
+ *     has 8..18 dead times per matrix, N % 128 == 0 and 1024 <= N <= 66048 (fp64 storage only with
  *     SPLIDAR_I8=2 in the environment at plan creation), and only if every column of every matrix
  *     passes the range test of each launch (every non-zero entry within 2^8 (fp32) / 2^11 (fp64) of
  *     its column's largest, no subnormal or negative entry) -- else the FP64 kernel runs;

@@ -221,11 +221,20 @@ __device__ __forceinline__ void epilogue(const PowerArgs &a, const PieceCtx &pc,
             uint32_t r[16];
             tc05::ld32x16(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(NP * col0 + 16 * c4), r);
             tc05::wait_ld();
+            // D is read as UNSIGNED: every product is >= 0 and a column's sum over <= 66048 rows is
+            // < 2^32 (i8_supported bounds N), so the s32 accumulator's wrap-around is exact mod 2^32
 #pragma unroll
             for (int e = 0; e < 16 / NP; ++e) {
-                double t = 0.0;
+                double t;
+                if constexpr (NP == 4) {     // fp32: sum_p D_p 2^(8p) < 2^56, exact in 64-bit integers
+                    const uint64_t t64 = (uint64_t)r[e * 4] + ((uint64_t)r[e * 4 + 1] << 8) +
+                                         ((uint64_t)r[e * 4 + 2] << 16) + ((uint64_t)r[e * 4 + 3] << 24);
+                    t = (double)t64;
+                } else {                     // fp64: 8 planes (up to 2^88): fp64, most significant last
+                    t = 0.0;
 #pragma unroll
-                for (int p = NP - 1; p >= 0; --p) t = fma((double)(int)r[e * NP + p], ldexp(1.0, 8 * p), t);
+                    for (int p = NP - 1; p >= 0; --p) t = fma((double)r[e * NP + p], ldexp(1.0, 8 * p), t);
+                }
                 acc[c4 * (16 / NP) + e] = t * wq;
             }
         }
@@ -243,7 +252,9 @@ __device__ __forceinline__ void epilogue(const PowerArgs &a, const PieceCtx &pc,
             for (int qq = 0; qq < kXQ; ++qq) ysum += st[i * SROW + qq * VP + v];
             const int j = c * TN + col0 + i;
             const int ex = a.colexp[(size_t)m * N + j] - C::BIAS_MBITS - C::R - s_tau[v];
-            part[(size_t)v * TN + col0 + i] = ldexp(ysum, ex);
+            // ysum 2^ex: a multiply by the exact power of two (same rounding as ldexp) when 2^ex is normal
+            part[(size_t)v * TN + col0 + i] =
+                ex >= -1022 && ex <= 1023 ? ysum * __longlong_as_double((long long)(ex + 1023) << 52) : ldexp(ysum, ex);
         }
         named_sync(2 + half, 128);
     }
@@ -679,7 +690,8 @@ __global__ void k_i8_prep(const PowerArgs a) {
 // Host side: the i8 kernels of a plan (nullptr when the plan cannot use them).
 int i8_supported(int dtype, const PowerArgs &a) {
     const int TN = dtype == SPLIDAR_F64 ? I8Cfg<double>::TN : I8Cfg<float>::TN;
-    return a.V >= 8 && 7 * a.V <= 128 && a.N % 128 == 0 && a.N % TN == 0 && a.N >= 1024;
+    // N <= 66048: a column's u8 x u8 sum over N rows stays below 2^32 (the accumulator read unsigned)
+    return a.V >= 8 && 7 * a.V <= 128 && a.N % 128 == 0 && a.N % TN == 0 && a.N >= 1024 && a.N <= 66048;
 }
 
 // Tensor map of the stored matrices: dims {N columns, N rows, M matrices}, strides {ld, mstride}

@@ -128,7 +128,8 @@ def _encode_ref(P):
     nz = (u & 0x7FFFFFFF) != 0
     E = np.where(nz, e, 0).max(axis=0)
     emin = np.where(nz, e, 1 << 20).min(axis=0)
-    if np.any((E - emin > 8) & (emin < (1 << 20))) or np.any(E <= 8):
+    has = emin < (1 << 20)                          # columns with a non-zero entry (all-zero ones encode as 0)
+    if np.any(has & (E - emin > 8)) or np.any(has & (E <= 8)) or np.any(nz & (e == 0)):
         return None
     sig = (u & 0x7FFFFF) | 0x800000
     sh = e - E[None, :] + 8
@@ -174,16 +175,26 @@ def test_building_plan_encoded_storage(spl, monkeypatch, enc_env):
         assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-13
 
 
-def test_building_plan_encoded_out_of_range(spl):
-    """A flux whose columns span more than 2^8 (Lambda = 61): the encoded build falls back to plain
-    fp32 storage and the FP64 GEMV (the stored matrix equals the separate fp32 build)."""
-    f = Flux(200.0, 4096, (60.0,), (0.5,), (60.0,), 1.0)
+@pytest.mark.parametrize("sig,bg,want_enc", [(60.0, 1.0, False), (5.0, 0.05, None), (5.5, 0.01, None), (1.0, 1.0, True)])
+def test_building_plan_encoded_range(spl, sig, bg, want_enc):
+    """The range test from 1/D (before the build) agrees with the range test of the stored fp32
+    matrix: columns spanning more than 2^8 (Lambda = 61; Lambda ~ 5 sits near the edge, either way)
+    fall back to plain fp32 storage and the FP64 GEMV (the stored matrix equals the separate fp32
+    build, bit for bit); otherwise the words equal the test-side encoding."""
+    f = Flux(200.0, 4096, (60.0,), (0.5,), (sig,), bg)
     T = np.array([[10.0, 30.0, 50.0, 70.0, 90.0, 110.0, 130.0, 150.0]])
+    ref = spl.build_base(f, torch.float32).cpu().numpy()
+    want = _encode_ref(ref)
+    if want_enc is not None:
+        assert (want is not None) == want_enc
     P0 = spl.empty_matrix(4096, torch.float32, n_matrices=1)
     pa = spl.Plan(P0, f.t_r, T, tol=1e-12, build=[f])
     pa.execute()
-    assert pa.gemv() == "fp64" and pa.storage() == "ieee"
-    ref = spl.build_base(f, torch.float32).cpu().numpy()
-    assert _encode_ref(ref) is None
-    assert np.array_equal(P0[0].contiguous().cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    stored = P0[0].contiguous().cpu().numpy().view(np.uint32)
+    if want is None:
+        assert pa.gemv() == "fp64" and pa.storage() == "ieee"
+        assert np.array_equal(stored, ref.view(np.uint32))
+    else:
+        assert pa.gemv() == "tensor_i8" and pa.storage() == "encoded"
+        assert np.array_equal(stored, want)
     pa.close()

@@ -149,3 +149,48 @@ def test_i8_not_used_where_unsupported(spl, monkeypatch):
     P0r = spl.build_base(g, torch.float32)
     _, _, k = _solve(spl, P0r, g.t_r, [10.0 * i for i in range(8)], "1", monkeypatch)
     assert k == "fp64"
+
+
+def test_i8_largest_n(spl, monkeypatch):
+    """N = 66048, the largest N the int8 kernels take (u8 x u8 sums over N rows < 2^32), on a nearly
+    flat flux: the encoded building plan, the converter kernel on the IEEE matrix and the FP64 GEMV
+    agree."""
+    N = 66048
+    f = Flux(100.0, N, (50.0,), (1.0,), (1e-4,), 0.1)
+    T = np.array([[10.0, 30.0, 50.0, 70.0, 90.0, 110.0, 130.0, 150.0]])
+    monkeypatch.setenv("SPLIDAR_FUSED", "0")
+    P0 = spl.empty_matrix(N, torch.float32, n_matrices=1)
+    pe = spl.Plan(P0, f.t_r, T, tol=1e-12, build=[f])
+    ie = pe.execute()
+    assert pe.gemv() == "tensor_i8" and pe.storage() == "encoded"
+    pie = pe.pi.detach().cpu().numpy().copy()
+    pe.close()
+    spl.build_base(f, torch.float32, out=P0[0])
+    pic, ic, kc = _solve(spl, P0[0], f.t_r, T, "1", monkeypatch)
+    pif, iff, kf = _solve(spl, P0[0], f.t_r, T, "0", monkeypatch)
+    assert kc == "tensor_i8" and kf == "fp64"
+    assert [i["iters"] for i in ie] == [i["iters"] for i in ic]
+    assert all(abs(a["iters"] - b["iters"]) <= 1 for a, b in zip(ic, iff))
+    assert np.max(np.sum(np.abs(pie - pic), axis=-1)) <= 1e-14
+    assert np.max(np.sum(np.abs(pic - pif), axis=-1)) <= 1e-12
+
+
+def test_i8_accumulator_beyond_2_31(spl, monkeypatch):
+    """A constant matrix c = 1.99 2^-17 at N = 66048 from the uniform start: the top byte of every
+    scaled entry (sig << 8) is 254 and so is the top byte of every x slice (1/N = 0.992 2^-16), so the
+    most significant plane-times-slice sum is 254^2 N = 4.26e9: above 2^31 (where a signed read of the
+    s32 accumulator goes wrong), below 2^32. y = c sum(x) for every column: pi stays uniform."""
+    N = 66048
+    c = np.float32(1.99 * 2.0 ** -17)
+    assert ((int(np.array([c]).view(np.uint32)[0]) & 0x7FFFFF | 0x800000) >> 16) == 254
+    P0 = spl.empty_matrix(N, torch.float32)
+    P0.fill_(float(c))
+    monkeypatch.setenv("SPLIDAR_I8", "1")
+    plan = spl.Plan(P0, 100.0, np.array([[10.0, 30.0, 50.0, 70.0, 90.0, 110.0, 130.0, 150.0]]), tol=1e-12,
+                    max_iter=20)                # a wrong product fails fast instead of iterating on
+    i8 = plan.execute(check=False)
+    assert plan.gemv() == "tensor_i8"
+    pi8 = plan.pi.detach().cpu().numpy().copy()
+    plan.close()
+    assert all(i["converged"] for i in i8)
+    assert np.max(np.abs(pi8 - 1.0 / N)) <= 1e-18
