@@ -49,8 +49,9 @@ __device__ __forceinline__ double phi_diff(double zl, double zh) {
     return 0.5 * (erf(zh * r2) + erf(-zl * r2));
 }
 
-// int_lo^hi lambda(t) dt for 0 <= lo <= hi <= t_r (Eq. 1; S = alpha E, lambda_b = B/t_r).
-__device__ double flux_mass(const FluxDev &f, double lo, double hi) {
+// int_lo^hi lambda(t) dt for 0 <= lo <= hi <= t_r (Eq. 1; S = alpha E, lambda_b = B/t_r). The
+// reference form of the masses k_vec_a / k_vec_small compute with shared bin-edge erfc evaluations.
+[[maybe_unused]] __device__ double flux_mass(const FluxDev &f, double lo, double hi) {
     double v = f.B * ((hi - lo) / f.t_r);
     for (int k = 0; k < f.k; ++k) {
         const double is = 1.0 / f.sigma[k];
