@@ -33,10 +33,16 @@ def spl():
 
 
 def _bench_plan_pis(spl, f, tds, dtype):
-    """The bench's c5 step: one P~0, all dead times as one multi-vector plan."""
-    P0 = spl.build_base(f, dtype)
-    plan = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-12)
+    """The bench's c5 step: one building plan (build P~0 + iteration 1 from its column sums + the
+    power iteration), all dead times as one multi-vector plan; fp32 runs on the encoded storage and
+    the int8 tensor-core GEMV, fp64 on the FP64 tensor cores."""
+    P0 = spl.empty_matrix(f.n_bins, dtype, n_matrices=1)
+    plan = spl.Plan(P0, f.t_r, np.array([tds]), tol=1e-12, build=[f])
     infos = plan.execute(check=dtype == torch.float64)
+    if dtype == torch.float32:
+        assert plan.gemv() == "tensor_i8" and plan.storage() == "encoded"
+    else:
+        assert plan.gemv() == "fp64" and plan.storage() == "ieee"
     pis = plan.pi[0].detach().cpu().numpy().copy()
     plan.close()
     del P0
