@@ -306,8 +306,15 @@ cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int 
                          void *P0, int64_t ld, int64_t mstride, cudaStream_t s, int row0, int nrows,
                          double *colsum_part, double *colsum, ColStats cst) {
     if (nrows < 0) nrows = N;
-    // with column sums: at most kColsumChunks row chunks per matrix (deterministic fixed-order sum)
-    const int nch = colsum_part ? colsum_chunks(nrows) : (nrows + kRowsPerCta - 1) / kRowsPerCta;
+    // with column sums: at most kColsumChunks row chunks per matrix (deterministic fixed-order sum);
+    // without: chunks of 32 rows, or fewer rows per CTA when that leaves the grid below two CTAs per
+    // SM (small N: c1's N = 256 was 8 CTAs of 32 rows)
+    int nch = colsum_part ? colsum_chunks(nrows) : (nrows + kRowsPerCta - 1) / kRowsPerCta;
+    if (!colsum_part) {
+        const int strips = (N + kStripCols - 1) / kStripCols;
+        const int want = (2 * device_sm_count() + strips * M - 1) / (strips * M);
+        if (nch < want) nch = want < nrows ? want : nrows;
+    }
     const int rpc = (nrows + nch - 1) / nch;
     dim3 grid((N + kStripCols - 1) / kStripCols, nch, M);
     if (dtype == SPLIDAR_F64) {
