@@ -22,8 +22,9 @@ def _run(*args, timeout=900):
 
 
 def test_reference_arm_line():
-    d = _run("--impl", "reference", "--workload", "c1", "--steps", "1", "--warmup", "3")
+    d = _run("--impl", "reference", "--workload", "c1", "--steps", "2", "--warmup", "3")
     assert BASE <= set(d) and d["impl"] == "reference"
+    assert d["steps"] == 2 and d["warmup"] == 3 and d["ms_per_step"] < 60e3   # a step = one bounded sample
     assert d["value"] > 0 and d["higher_is_better"] is True
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["sample"] and cb["value"] == d["value"]
