@@ -174,3 +174,36 @@ def test_spectral_dense_and_shards_guarded(spl):
     out = _run_poisoned(run, [ws_d] + ws_r)
     assert np.array_equal(out[1], out[2])
     A.check()
+
+
+@pytest.mark.parametrize("N,V,M,dtype", [(4096, 17, 1, torch.float32), (2176, 8, 2, torch.float32),
+                                         (3000, 17, 1, torch.float64), (1024, 3, 2, torch.float64)])
+def test_building_plans_guarded(spl, monkeypatch, N, V, M, dtype):
+    """Building plans (steps 1-2 inside the launch, iteration 1 from the column sums; fp32 with >= 8
+    dead times on the encoded storage + int8 GEMV): matrix and workspace between guard bands, both
+    poisoned before the plan is created (a plan binds its workspace: the fluxes and shifts live there
+    between launches)."""
+    monkeypatch.setenv("SPLIDAR_FUSED", "0" if N > 1024 else "1")
+    rng = np.random.default_rng(N + V + M)
+    fl = [random_flux(rng, N, 2, sigma_bins=(1, 10), s_range=(0.5, 1.5), b_range=(0.2, 1.0)) for _ in range(M)]
+    fl = [Flux(100.0, N, f.tau, f.sigma, f.signal, f.background) for f in fl]
+    A = Arena()
+    P0 = A.matrix(spl, N, dtype, M)
+    ws = _ws(A, spl, spl.workspace_bytes(N, M, V))
+    T = rng.uniform(0, 300, (M, V))
+    kinds = []
+
+    def run():
+        P0.fill_(float("nan"))
+        plan = spl.Plan(P0, 100.0, T, tol=1e-12, ws=ws, build=fl)
+        plan.execute()
+        kinds.append((plan.gemv(), plan.storage()))
+        out = plan.pi.detach().clone()
+        plan.close()
+        return [out]
+
+    out = _run_poisoned(run, [ws])
+    A.check()
+    assert np.all(np.isfinite(out[0])) and np.allclose(out[0].sum(axis=-1), 1.0)
+    if dtype == torch.float32 and V >= 8:
+        assert set(kinds) == {("tensor_i8", "encoded")}
