@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(kEncBlock) k_enc_colexp(const VecPtrs base, in
     const double eL = base.scal[m * 8 + 1];
     for (int b2 = wp; b2 < nb; b2 += kEncBlock / 32) {          // extremes of every block
         double mx = 0.0, mn = INFINITY;
-        for (int j = b2 * kEncBlock + lane; j < min(N, (b2 + 1) * kEncBlock); j += 32) {
+        const int jend = min(N, (b2 + 1) * kEncBlock);
+#pragma unroll 8
+        for (int j = b2 * kEncBlock + lane; j < jend; j += 32) {    // 8 loads in flight per lane
             const double h = invD[j];
             mx = fmax(mx, h);
             mn = fmin(mn, h);
