@@ -25,8 +25,8 @@
 //   warp 0      x-slice producer: the unit's 8 KB image (written by k_power_check) with one
 //               cp.async.bulk into the MMA buffer, once the MMA has freed it (3 buffers);
 //   warp 1      MMA issuer (one thread): per unit 2 k-steps x 2 tcgen05.mma of M = 128 rows (q, v)
-//               of x slices, N = 256 columns (2 fp32 / 4 fp64 byte planes side by side), K = 32;
-//               D_p in TMEM columns [p TN, (p+1) TN);
+//               of x slices, N = 256 bytes of scaled integers (64 fp32 / 32 fp64 columns, byte n =
+//               W j + p of column j's word), K = 32; D in TMEM column (W j + p) of the tile;
 //   warp 2      TMEM allocator;
 //   warps 4-11  converters: each unit's tile -> its scaled integers in the canonical MN-major layout
 //               (the tensor core reads every byte as its own u8 column: no transposes); shared-memory bandwidth (TMA write, converter read and
@@ -36,6 +36,9 @@
 //               TMEM -> registers (tcgen05.ld), sum over p and q in fp64, per-piece partial sums;
 //               the last piece of a tile adds the pieces in fixed order (deterministic), writes y,
 //               the tile's sum and max of y (the next x scale).
+// k_power_step_i8e: fp32 matrices a building plan stored already ENCODED (each entry its scaled
+// integer; build.cu): the TMA boxes are the MMA's B operand as they land, so it has no converters
+// (4 stages of tile + x image, the same MMA issue and epilogue).
 #include <climits>
 #include <cuda.h>
 #include <cudaTypedefs.h>
