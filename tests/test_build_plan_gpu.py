@@ -198,3 +198,20 @@ def test_building_plan_encoded_range(spl, sig, bg, want_enc):
         assert pa.gemv() == "tensor_i8" and pa.storage() == "encoded"
         assert np.array_equal(stored, want)
     pa.close()
+
+
+@pytest.mark.parametrize("N,V,M", [(1152, 18, 1), (2176, 19, 1), (1024, 8, 4), (8192, 12, 2)])
+def test_building_plan_fp32_shapes(spl, monkeypatch, N, V, M):
+    """fp32 building plans at the edges of the int8 path: the most dead times it takes (18), one more
+    (19: the FP64 kernel with 24 slots), the smallest N (1024) with several matrices, and 12 dead
+    times on two larger matrices; each equal to the separate build + plan."""
+    monkeypatch.setenv("SPLIDAR_FUSED", "0")
+    rng = np.random.default_rng(N + V + M)
+    fl = [random_flux(rng, N, 2, sigma_bins=(1, 10), s_range=(0.5, 1.5), b_range=(0.2, 1.0)) for _ in range(M)]
+    fl = [Flux(100.0, N, f.tau, f.sigma, f.signal, f.background) for f in fl]
+    T = rng.uniform(0, 300, (M, V))
+    pia, ia, pib, ib, kind = _pair(spl, fl, T, torch.float32)
+    assert kind == ("tensor_i8" if V <= 18 else "fp64")
+    assert [i["iters"] for i in ia] == [i["iters"] for i in ib]
+    assert all(i["converged"] for i in ia)
+    assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-13
