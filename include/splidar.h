@@ -256,6 +256,14 @@ int splidar_plan_gemv(splidar_plan plan, void *stream);
 /* The form of P0 after the plan's last launch (synchronises the stream once): SPLIDAR_STORAGE_IEEE
  * (the dtype's numbers) or SPLIDAR_STORAGE_ENCODED (a building plan's per-column scaled integers, see
  * splidar_plan_create_build); -1: NULL plan or CUDA error. */
+/* Device time of the plan's GEMV launches since the last reset: each GEMV kernel stamps the device
+ * clock (%globaltimer) when its first CTA starts and its last CTA ends, and the convergence check that
+ * follows adds the difference, so *seconds / *launches is the GEMV kernel's own average launch duration
+ * inside the CUDA-graph loop (where events cannot bracket a single kernel). The int8 plans' FP64
+ * kernel returns at once without stamping; iteration 1 of a building plan has no GEMV launch. reset
+ * != 0 zeroes the counters after reading. Synchronises the stream. Fused plans report 0 launches. */
+splidar_status splidar_plan_gemv_time(splidar_plan plan, int32_t reset, double *seconds, int64_t *launches,
+                                      void *stream);
 #define SPLIDAR_STORAGE_IEEE 0
 #define SPLIDAR_STORAGE_ENCODED 1
 int splidar_plan_storage(splidar_plan plan, void *stream);

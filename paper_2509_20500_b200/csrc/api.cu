@@ -463,6 +463,9 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     a.mv_cnt = reinterpret_cast<unsigned *>(ws + L.mv_cnt);
     a.act = reinterpret_cast<int *>(ws + L.act);
     a.glob = reinterpret_cast<unsigned *>(ws + L.glob);
+    // GEMV launch timer in the glob block's spare bytes (ptx.cuh; read by splidar_plan_gemv_time)
+    a.ktime = reinterpret_cast<unsigned long long *>(ws + L.glob + 64);
+    SPL_CUDA(cudaMemsetAsync(a.ktime, 0, 4 * sizeof(unsigned long long), s));
     a.N = L.N;
     if (a.rows == 0) a.rows = L.N;      // a row shard sets rows / row0 / ypart before plan_build
     a.M = L.M;
@@ -840,6 +843,23 @@ int splidar_plan_gemv(splidar_plan plan, void *stream) {
         return -1;
     }
     return flag ? SPLIDAR_GEMV_TENSOR_I8 : SPLIDAR_GEMV_FP64;
+}
+
+splidar_status splidar_plan_gemv_time(splidar_plan plan, int32_t reset, double *seconds, int64_t *launches,
+                                      void *stream) {
+    SPL_NVTX_RANGE();
+    if (!plan || !seconds || !launches) return SPLIDAR_EINVAL;
+    *seconds = 0.0;
+    *launches = 0;
+    if (plan->fused || !plan->args.ktime) return SPLIDAR_OK;
+    unsigned long long h[2] = {0ull, 0ull};
+    cudaStream_t s = (cudaStream_t)stream;
+    SPL_CUDA(cudaMemcpyAsync(h, plan->args.ktime + 2, sizeof(h), cudaMemcpyDeviceToHost, s));
+    if (reset) SPL_CUDA(cudaMemsetAsync(plan->args.ktime + 2, 0, sizeof(h), s));
+    SPL_CUDA(cudaStreamSynchronize(s));
+    *seconds = (double)h[0] * 1e-9;
+    *launches = (int64_t)h[1];
+    return SPLIDAR_OK;
 }
 
 int splidar_plan_storage(splidar_plan plan, void *stream) {

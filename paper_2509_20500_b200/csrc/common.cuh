@@ -138,6 +138,8 @@ struct PowerArgs {
     int rows, row0;
     double *ypart;
     int ypart_shared;        // ypart is [M][N], one y for every vector of a matrix (fused-build column sums)
+    unsigned long long *ktime;   // GEMV launch timer (ptx.cuh): [0] first start, [1] last end, [2] sum of
+                                 // launch durations (ns), [3] launches; null: not timed
 };
 
 // Kernel node parameters for the three solver kernels (for graph construction).

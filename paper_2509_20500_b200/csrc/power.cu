@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
     const int64_t u_end = u_begin + U < T_units ? u_begin + U : T_units;
 
     if (tid == 0) {
+        ktime_start(a.ktime);
         for (int i = 0; i < kStages; ++i) {
             mbar_init(&full[i], 1);
         }
@@ -432,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
         }
         __syncthreads();
     }
+    if (tid == 0) ktime_end(a.ktime);
 }
 
 // Convergence check of one iteration (after k_power_step in the WHILE body). CTA (chunk, mv):
@@ -566,6 +568,15 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
                 n_act += __popc(b);
             }
             if (tid == 0) {
+                if (a.ktime) {   // the GEMV launch of this iteration (none before iteration 2 of a building plan)
+                    const unsigned long long t0 = __ldcg(a.ktime), t1 = __ldcg(a.ktime + 1);
+                    if (t1 > t0) {
+                        a.ktime[2] += t1 - t0;
+                        a.ktime[3] += 1ull;
+                    }
+                    a.ktime[0] = ~0ull;
+                    a.ktime[1] = 0ull;
+                }
                 a.glob[0] = 0u;
                 a.glob[1] = n_act > 0 ? 1u : 0u;
                 a.glob[2] = (unsigned)n_act;
@@ -641,6 +652,10 @@ __global__ void k_power_init(const PowerArgs a) {
                 for (int row = 7 * a.V; row < 128; ++row)
                     *reinterpret_cast<uint64_t *>(img + (row / 8) * 512 + (row % 8) * 16) = 0ull;
         }
+    }
+    if (mv == 0 && blockIdx.x == 0 && threadIdx.x == 0 && a.ktime) {
+        a.ktime[0] = ~0ull;
+        a.ktime[1] = 0ull;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         SolveState s;

@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
         fence_mbar_init();
     }
     if (warp == 2) tc05::alloc<512>(&s_tmem);
+    if (threadIdx.x == 0) ktime_start(a.ktime);
     tc05::fence_before();
     __syncthreads();
     tc05::fence_after();
@@ -479,6 +480,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8(const PowerArgs
     }
     tc05::fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) ktime_end(a.ktime);
     if (warp == 2) {
         tc05::fence_after();
         tc05::dealloc<512>(tmem);
@@ -529,6 +531,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8e(const PowerArg
         fence_mbar_init();
     }
     if (warp == 2) tc05::alloc<512>(&s_tmem);
+    if (threadIdx.x == 0) ktime_start(a.ktime);
     tc05::fence_before();
     __syncthreads();
     tc05::fence_after();
@@ -602,6 +605,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) k_power_step_i8e(const PowerArg
     }
     tc05::fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) ktime_end(a.ktime);
     if (warp == 2) {
         tc05::fence_after();
         tc05::dealloc<512>(tmem);

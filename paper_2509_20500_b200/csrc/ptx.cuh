@@ -8,6 +8,21 @@ namespace spl {
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// Device clock (ns) and the GEMV launch timer (PowerArgs::ktime): the first CTA to start lowers
+// ktime[0], the last to finish raises ktime[1]; k_power_check adds ktime[1] - ktime[0] to ktime[2]
+// and counts the launch in ktime[3] (the kernel's own duration, measured on the device).
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void ktime_start(unsigned long long *kt) {
+    if (kt) atomicMin(kt, global_ns());
+}
+__device__ __forceinline__ void ktime_end(unsigned long long *kt) {
+    if (kt) atomicMax(kt + 1, global_ns());
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }

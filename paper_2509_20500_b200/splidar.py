@@ -103,6 +103,7 @@ def _lib():
             "splidar_plan_kind": (C.c_int, [p]),
             "splidar_plan_gemv": (C.c_int, [p, p]),
             "splidar_plan_storage": (C.c_int, [p, p]),
+            "splidar_plan_gemv_time": (st, [p, i32, C.POINTER(d), C.POINTER(i64), p]),
             "splidar_build_base_rows": (st, [fp, st, st, p, i64, i32, i32, p, sz, p]),
             "splidar_plan_create_rows": (st, [C.POINTER(p), p, i32, i32, i32, i64, st, d, p, i32, d, i32, p, p, p,
                                               sz, p]),
@@ -494,6 +495,14 @@ class Plan:
         if k < 0:
             raise SplidarError(ECUDA, "splidar_plan_gemv")
         return self.GEMV_NAMES[k]
+
+    def gemv_time(self, reset: bool = False, stream=None):
+        """(seconds, launches) of the plan's GEMV kernel since the last reset, measured on the device
+        (splidar_plan_gemv_time). Synchronises the stream."""
+        sec, n = C.c_double(0.0), C.c_int64(0)
+        _check(_lib().splidar_plan_gemv_time(self._h, int(reset), C.byref(sec), C.byref(n), _stream(stream)),
+               "splidar_plan_gemv_time")
+        return sec.value, n.value
 
     def storage(self, stream=None) -> str:
         """The form of P0 after the last launch: 'ieee' or 'encoded' (a building plan's per-column

@@ -53,6 +53,11 @@ def test_our_line(extra):
         assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
     if not extra:                        # the default line: c5, HBM-bound GEMV near the roofline
         assert d["config"]["workload"].startswith("c5") and r["frac"] > 0.7 and d["roofline_build"]["frac"] > 0.7
+        # the GEMV's own device time (splidar_plan_gemv_time): one timed launch per GEMV pass, shorter than
+        # the solve phase per pass, so the kernel's rate is at least the solve phase's
+        its = max(d["iterations"][0])
+        assert r["kernel_launches"] == 2 * (its - 1) and r["kernel_ms_per_launch"] > 0
+        assert r["frac"] >= r["frac_solve_phase"]
 
 
 def test_gpus_flag_must_match_world():
