@@ -71,6 +71,9 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
     // encoded storage: entry -> scaled integer of its column (fixpt.cuh; launch_enc_colexp set E_j)
     bool enc = false;
     int base23[VEC];
+    uint64_t csi[VEC];           // encoded storage: column sums of the stored integers (exact)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) csi[e] = 0;
     if constexpr (sizeof(T) == 4 && MODE == SPLIDAR_ENTRY_FACTORED) {
         enc = cst.enc && *cst.flag;
         if (enc) {
@@ -102,7 +105,7 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
                 }
             }
         }
-        if (colsum_part) {
+        if (colsum_part && !enc) {
 #pragma unroll
             for (int e = 0; e < VEC; ++e) cs[e] += (double)val[e];
         }
@@ -134,7 +137,10 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
             if (enc) {
                 uint32_t wd[VEC];
 #pragma unroll
-                for (int e = 0; e < VEC; ++e) wd[e] = fx32(__float_as_uint((float)val[e]), base23[e]);
+                for (int e = 0; e < VEC; ++e) {
+                    wd[e] = fx32(__float_as_uint((float)val[e]), base23[e]);
+                    csi[e] += wd[e];
+                }
                 if (full) {
                     *reinterpret_cast<uint4 *>(row) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
                 } else {
@@ -158,6 +164,10 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
     }
     if (colsum_part) {           // [M][row chunk][N]: summed over the chunks in fixed order later
         double *cp = colsum_part + ((size_t)m * gridDim.y + blockIdx.y) * N;
+        if (enc) {   // stored value = integer x 2^(base23 - 127) (fixpt.cuh); a chunk's sum < 2^53: exact
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) cs[e] = ldexp((double)csi[e], base23[e] - 127);
+        }
 #pragma unroll
         for (int e = 0; e < VEC; ++e)
             if (j0 + e < N) cp[j0 + e] = cs[e];
