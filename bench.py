@@ -36,7 +36,8 @@ METRIC = "stationary solves/s (with transition-matrix entries/s; % of HBM roofli
 GEMV_KERNELS = {"tensor_i8": "k_power_step_i8 (tcgen05 kind::i8 exact split, TMEM accumulators)",
                 "tensor_i8_encoded": "k_power_step_i8e (tcgen05 kind::i8 on encoded fp32 storage: TMA tiles are "
                                      "the MMA operand, TMEM accumulators)",
-                "fp64": "k_power_step (FP64 tensor cores / DFMA)", "fused": "k_power_fused (cluster, small N)"}
+                "fp64": "k_power_step (FP64 tensor cores / DFMA)", "fused": "k_power_fused (cluster, small N)",
+                "fp64_loop": "k_power_loop GEMV phase (FP64 tensor cores / DFMA; persistent GEMV + check kernel)"}
 UNIT = "solves/s"
 
 
@@ -269,7 +270,7 @@ def run_ours(args, rank, world, dev):
     t_solve = t_total - t_build
     infos = st.infos()
     gemv_kinds = sorted({p.gemv() + ("_encoded" if p.gemv() == "tensor_i8" and p.storage() == "encoded" else "")
-                         for p in st.plans})
+                         + ("_loop" if p.kind == "loop" else "") for p in st.plans})
     from paper_2509_20500_b200.shard import max_over_ranks
     t_total, t_build, t_solve, t_kernel = max_over_ranks([t_total, t_build, t_solve, t_kernel], device="cuda")
 
@@ -298,7 +299,8 @@ def run_ours(args, rank, world, dev):
         if p.fused:
             return prelude + 1
         it = int(np.array([i["iters"] for i in pi]).reshape(p.M, p.V).max())
-        n = prelude + 1 + 1 + 2 + 2 * (it - 1) + 1
+        # the iterations after the first: GEMV + check each, or one persistent loop launch
+        n = prelude + 1 + 1 + 2 + (1 if p.kind == "loop" else 2 * (it - 1)) + 1
         if p.gemv() == "tensor_i8":
             n += it - 1
         return n + (2 if storage == "encoded" else 0)
@@ -330,6 +332,8 @@ def run_ours(args, rank, world, dev):
                    "parallelism": (f"dp{world}: items sharded over {world} ranks, no collective on the data path"
                                    if world > 1 else "single GPU"),
                    "solver": "fused (one clustered launch per plan, N <= 2048)" if all(p.fused for p in st.plans)
+                   else "loop (every iteration in one cooperative launch of the persistent GEMV + check kernel)"
+                   if all(p.kind == "loop" for p in st.plans)
                    else "graph (GEMV + check in a conditional WHILE node)",
                    "gemv": gemv_kinds,
                    "step_as_cuda_graph": bool(graphed)},
@@ -353,7 +357,7 @@ def run_ours(args, rank, world, dev):
                      "kernel_ms_per_launch": t_kernel / n_kernel * 1e3 if kernel_timed else None,
                      "kernel_launches": n_kernel,
                      "note": ("achieved = algorithmic bytes (N^2 b per launch per active matrix) / the GEMV "
-                              "launches' own duration, measured on the device over the timed region (each launch "
+                              "launches' own duration, measured on the device over the timed region (each launch, or each pass of the persistent loop kernel, "
                               "stamps %globaltimer at its first CTA's start and last CTA's end: "
                               "splidar_plan_gemv_time; CUDA events cannot bracket one kernel inside the graph's "
                               "WHILE loop); achieved_solve_phase divides by the whole solve phase (GEMV + check "

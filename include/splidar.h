@@ -231,12 +231,18 @@ splidar_status splidar_plan_launch(splidar_plan plan, void *stream);
 splidar_status splidar_plan_info(splidar_plan plan, splidar_solve_info *info, void *stream);
 void splidar_plan_destroy(splidar_plan plan);
 /* How a plan runs: SPLIDAR_PLAN_GRAPH (instantiated CUDA graph: [GEMV -> check] in a conditional WHILE
- * node; N > 2048) or SPLIDAR_PLAN_FUSED (N <= 2048: one clustered launch runs every iteration of every
- * (matrix, dead time) pair, P~0 rows staged in shared memory or streamed from L2; a single kernel
- * launch, so splidar_plan_launch may be captured into a caller's CUDA graph). -1 for NULL.
- * SPLIDAR_FUSED=0 in the environment at plan creation forces the graph form. */
+ * node; N > 2048), SPLIDAR_PLAN_LOOP (opt-in, SPLIDAR_PERSIST=1 at plan creation; N > 2048, GEMV not on
+ * the int8 tensor cores: instantiated CUDA graph whose iterations are ONE cooperative launch of a
+ * persistent kernel -- GEMV pass, grid barrier, convergence check, grid barrier, until every vector is
+ * done (P:79 iterated on the device with no launch between iterations); same arithmetic in the same
+ * order as the WHILE form, bit-identical results) or
+ * SPLIDAR_PLAN_FUSED (N <= 2048: one clustered launch runs every iteration of every (matrix, dead
+ * time) pair, P~0 rows staged in shared memory or streamed from L2; a single kernel launch, so
+ * splidar_plan_launch may be captured into a caller's CUDA graph). -1 for NULL.
+ * SPLIDAR_FUSED=0 in the environment at plan creation forces the graph forms. */
 #define SPLIDAR_PLAN_GRAPH 0
 #define SPLIDAR_PLAN_FUSED 1
+#define SPLIDAR_PLAN_LOOP 2
 int splidar_plan_kind(splidar_plan plan);
 /* Which GEMV kernel ran the plan's last launch (synchronises the stream once):
  *   SPLIDAR_GEMV_TENSOR_I8 (2): the exact int8 split on the 5th-generation tensor cores

@@ -389,6 +389,8 @@ struct splidar_plan_s {
     unsigned *host_flag = nullptr;
     // small N: every iteration of every (matrix, vector) in one clustered launch (fused.cu)
     bool fused = false;
+    // graph plans: the iterations are one cooperative k_power_loop launch (else the WHILE node)
+    bool persist = false;
     int dt = 0;
     FusedArgs fargs;
     I8Kernels q;       // int8 tensor-core GEMV (args.i8)
@@ -537,13 +539,34 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
         return SPLIDAR_OK;
     }
     SPL_CUDA(cudaGraphCreate(&p->graph, 0));
-    cudaGraphConditionalHandle h;
-    SPL_CUDA(cudaGraphConditionalHandleCreate(&h, p->graph, 1, cudaGraphCondAssignDefault));
-    a.use_handle = 1;
-    a.handle = h;
-
     SolverKernels &k = p->k;
     if (solver_kernels(dt, L.V, &k, a)) return SPLIDAR_EINVAL;
+    // SPLIDAR_PERSIST=1: the iterations as ONE cooperative launch of k_power_loop (GEMV + check fused,
+    // grid barriers) when the plan is not on the int8 GEMV and the whole persistent grid can be
+    // resident at once. Opt-in: measured against the conditional WHILE node of [k_power_step ->
+    // k_power_check] (same box, alternating), it gained 0.3 % at c4 (DFMA) and lost 1.6 % at c5
+    // (DMMA: the inlined GEMV pass itself runs ~1.8 % slower in the larger kernel), DESIGN.md §6.
+    p->persist = false;
+    if (!a.i8 && k.loop_fn) {
+        const char *e = getenv("SPLIDAR_PERSIST");
+        int nb = 0;
+        if (e && e[0] == '1') {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k.loop_fn, (int)k.step_block.x, k.step_smem) !=
+                cudaSuccess) {
+                (void)cudaGetLastError();
+                nb = 0;
+            }
+            p->persist = (long)nb * device_sm_count() >= (long)k.step_grid.x;
+        }
+    }
+    if (p->persist) {
+        a.use_handle = 0;
+    } else {
+        cudaGraphConditionalHandle h;
+        SPL_CUDA(cudaGraphConditionalHandleCreate(&h, p->graph, 1, cudaGraphCondAssignDefault));
+        a.use_handle = 1;
+        a.handle = h;
+    }
     p->eager_args = a;
     p->eager_args.use_handle = 0;
     {
@@ -619,9 +642,33 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
         n_loop_dep = n_ck;
     }
 
+    if (p->persist) {
+        void *loop_args[] = {&a};
+        kp.func = k.loop_fn;
+        kp.gridDim = k.step_grid;
+        kp.blockDim = k.step_block;
+        kp.sharedMemBytes = k.step_smem;
+        kp.kernelParams = loop_args;
+        SPL_CUDA(cudaGraphAddKernelNode(&n_while, p->graph, &n_loop_dep, 1, &kp));
+        cudaKernelNodeAttrValue coop = {};
+        coop.cooperative = 1;
+        SPL_CUDA(cudaGraphKernelNodeSetAttribute(n_while, cudaLaunchAttributeCooperative, &coop));
+        std::vector<unsigned char> &fa = p->fin_args;
+        fa.resize(finish_args_size());
+        make_finish_args(fa.data(), a, pi, reinterpret_cast<const int *>(ws + L.oidx));
+        void *fin_args[] = {fa.data()};
+        kp.func = k.finish_fn;
+        kp.gridDim = k.finish_grid;
+        kp.blockDim = k.finish_block;
+        kp.sharedMemBytes = 0;
+        kp.kernelParams = fin_args;
+        SPL_CUDA(cudaGraphAddKernelNode(&n_fin, p->graph, &n_while, 1, &kp));
+        SPL_CUDA(cudaGraphInstantiate(&p->exec, p->graph, 0));
+        return SPLIDAR_OK;
+    }
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h;
+    cp.conditional.handle = a.handle;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
     SPL_CUDA(cudaGraphAddNode(&n_while, p->graph, &n_loop_dep, 1, &cp));
@@ -829,7 +876,9 @@ static splidar_status plan_launch_eager(splidar_plan_s *p, cudaStream_t s) {
     return SPLIDAR_OK;
 }
 
-int splidar_plan_kind(splidar_plan plan) { return !plan ? -1 : plan->fused ? SPLIDAR_PLAN_FUSED : SPLIDAR_PLAN_GRAPH; }
+int splidar_plan_kind(splidar_plan plan) {
+    return !plan ? -1 : plan->fused ? SPLIDAR_PLAN_FUSED : plan->persist && !plan->eager ? SPLIDAR_PLAN_LOOP : SPLIDAR_PLAN_GRAPH;
+}
 
 int splidar_plan_gemv(splidar_plan plan, void *stream) {
     if (!plan) return -1;

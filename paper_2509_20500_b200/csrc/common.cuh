@@ -104,6 +104,8 @@ cudaError_t launch_apply_deadtime(const void *P0, void *P, int N, int64_t ld, in
                                   cudaStream_t s);
 cudaError_t launch_build_eq4(const FluxDev &f, double u, int dtype, void *P, int64_t ld, cudaStream_t s);
 
+constexpr int kGridBarWord = 32;   // glob[32..33]: k_power_loop's grid barrier (arrivals, generation)
+
 struct PowerArgs {
     const void *P;
     int64_t ld;
@@ -119,7 +121,8 @@ struct PowerArgs {
     unsigned *strip_cnt;     // [M * strips]       pieces finished per strip (active order)
     unsigned *mv_cnt;        // [M][V]             check-kernel CTA counters
     int *act;                // [M]                active matrices (any vector still running)
-    unsigned *glob;          // [0] check CTA counter, [1] any-active flag, [2] number of active matrices
+    unsigned *glob;          // [0] check CTA counter, [1] any-active flag, [2] number of active matrices,
+                             // [3] int8 GEMV on, [kGridBarWord..+1] k_power_loop grid barrier
     double tol;
     int max_iter;
     int use_handle;
@@ -149,6 +152,7 @@ struct SolverKernels {
     void *check_fn;
     void *finish_fn;
     void *ssum_fn;           // row shard: strip sums of the all-reduced y
+    void *loop_fn;           // k_power_loop: GEMV + check iterated in one cooperative launch (or null)
     dim3 init_grid, init_block;
     dim3 step_grid, step_block;
     dim3 check_grid, check_block;

@@ -205,13 +205,30 @@ struct StepSmem {
     static constexpr size_t BYTES = STAGES * (SEG + XB) + STAGES * sizeof(uint64_t);
 };
 
+// The state of (matrix, vector) mv through L2 (never a stale L1 line: the persistent loop kernel
+// reads states other CTAs wrote in the same launch).
+__device__ __forceinline__ SolveState load_state(const SolveState *p) {
+    static_assert(sizeof(SolveState) == 48, "SolveState is three 16-byte words");
+    SolveState s;
+    const int4 *q = reinterpret_cast<const int4 *>(p);
+    int4 *d = reinterpret_cast<int4 *>(&s);
+    d[0] = __ldcg(q);
+    d[1] = __ldcg(q + 1);
+    d[2] = __ldcg(q + 2);
+    return s;
+}
+
+// One GEMV pass of every active (matrix, vector) over the stored P~0 (the body of k_power_step and of
+// each iteration of k_power_loop). full[]: the CTA's ring mbarriers, initialised by the caller;
+// q_issue / q_cons: the ring's stage sequence numbers, continued across passes. Every cross-CTA
+// input (active list, states, partials) is read through L2.
 template <typename T, int NV>
-__global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(const PowerArgs a) {
+__device__ __forceinline__ void gemv_pass(const PowerArgs &a, unsigned char *smem, uint32_t &q_issue,
+                                          uint32_t &q_cons) {
     using SM = StepSmem<T, NV>;
     constexpr int RS = SM::RS;
     constexpr int kStages = SM::STAGES;
     constexpr int NWARPS = kThreads / 32;
-    extern __shared__ __align__(128) unsigned char smem[];
     T *segs = reinterpret_cast<T *>(smem);                                             // [S][RS][512]
     double *xbuf = reinterpret_cast<double *>(smem + kStages * SM::SEG);               // [S][RS][XST]
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * (SM::SEG + SM::XB));   // TMA landed
@@ -221,8 +238,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
 
     const int tid = threadIdx.x, b = blockIdx.x, G = gridDim.x;
     const int N = a.N, S = a.strips;
-    if (a.i8 && a.glob[3]) return;                  // the int8 tensor-core GEMV runs this plan
-    const int n_act = (int)a.glob[2];
+    const int n_act = (int)__ldcg(a.glob + 2);
     const int R = a.rows;                           // rows of the stored block (N, or a row shard)
     const int64_t T_units = (int64_t)n_act * S * R;
     if (T_units == 0) return;
@@ -231,23 +247,14 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
     const int64_t u_begin = (int64_t)b * U;
     if (u_begin >= T_units) return;
     const int64_t u_end = u_begin + U < T_units ? u_begin + U : T_units;
+    if (tid == 0) ktime_start(a.ktime);
 
-    if (tid == 0) {
-        ktime_start(a.ktime);
-        for (int i = 0; i < kStages; ++i) {
-            mbar_init(&full[i], 1);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    uint32_t q_issue = 0, q_cons = 0;   // stage sequence numbers (buffer q % S, parity (q / S) & 1)
     int64_t u = u_begin;
     while (u < u_end) {
         const int64_t g64 = u / R;                       // strip index in active order
         const int g = (int)g64;
         const int ai = g / S, c = g % S;
-        const int m = a.act[ai];
+        const int m = __ldcg(a.act + ai);
         const int r_lo = (int)(u - g64 * R);
         const int64_t strip_end = (g64 + 1) * R;
         const int r_hi = (int)((u_end < strip_end ? u_end : strip_end) - g64 * R);
@@ -258,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
             int n = 0;
             unsigned vm = 0;
             for (int v = 0; v < NV; ++v) {
-                const SolveState s = a.st[(size_t)m * NV + v];
+                const SolveState s = load_state(a.st + (size_t)m * NV + v);
                 if (!s.done) {
                     s_vmap[n] = v; s_cur[n] = s.cur; ++n;
                     vm |= 1u << v;
@@ -436,17 +443,39 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
     if (tid == 0) ktime_end(a.ktime);
 }
 
+template <typename T, int NV>
+__device__ __forceinline__ void ring_init(unsigned char *smem) {
+    using SM = StepSmem<T, NV>;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + SM::STAGES * (SM::SEG + SM::XB));
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < SM::STAGES; ++i) mbar_init(&full[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+}
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(const PowerArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (a.i8 && a.glob[3]) return;                  // the int8 tensor-core GEMV runs this plan
+    ring_init<T, NV>(smem);
+    uint32_t q_issue = 0, q_cons = 0;               // stage sequence numbers (buffer q % S, parity (q / S) & 1)
+    gemv_pass<T, NV>(a, smem, q_issue, q_cons);
+}
+
 // Convergence check of one iteration (after k_power_step in the WHILE body). CTA (chunk, mv):
 // s = sum of strip sums (fixed order); the chunk's part of ||y / s - pi^k||_1; the next gathered
 // x: X[m][(j + l) mod N][v] = y_j / s; the last CTA of each (matrix, vector) adds the chunks in
 // fixed order and updates the state; the last CTA of the grid rebuilds the active-matrix list and
 // sets the WHILE condition. Done vectors are skipped (their pi stays frozen).
-__global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
+// check_item: the work of CTA (chunk c, vector mv); n_items = chunks x M x V, the count after which the
+// last item rebuilds the active list (one item per CTA in k_power_check, grid-strided in k_power_loop).
+__device__ __forceinline__ void check_item(const PowerArgs &a, int c, int mv, unsigned n_items) {
     __shared__ double red[8];
     __shared__ int s_last;
-    const int c = blockIdx.x, mv = blockIdx.y, tid = threadIdx.x;
+    const int tid = threadIdx.x;
     const int N = a.N;
-    const SolveState st = a.st[mv];
+    const SolveState st = load_state(a.st + mv);
     if (st.done && a.ypart && !a.ypart_shared) {   // row shard: a frozen vector's partial stays zero
         const int j1 = min(N, (c + 1) * kCheckChunk);
         for (int j = c * kCheckChunk + tid; j < j1; j += 256) a.ypart[(size_t)mv * N + j] = 0.0;
@@ -493,7 +522,7 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
                     int j = r0 + e - l;
                     if (j < 0) j += N;
                     const double pn = __ldcg(yn + j) * inv_new;
-                    l1 += fabs(pn - yo[j] * inv_old);
+                    l1 += fabs(pn - __ldcg(yo + j) * inv_old);
                     const uint64_t xt = (uint64_t)ldexp(pn, tau);
 #pragma unroll
                     for (int q = 0; q < 7; ++q) wq[q] |= ((xt >> (8 * (6 - q))) & 0xFFull) << (8 * e);
@@ -510,7 +539,7 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
             const int j1 = min(N, (c + 1) * kCheckChunk);
             for (int j = c * kCheckChunk + tid; j < j1; j += 256) {
                 const double pn = __ldcg(yn + j) * inv_new;
-                l1 += fabs(pn - yo[j] * inv_old);
+                l1 += fabs(pn - __ldcg(yo + j) * inv_old);
                 int r = j + l;
                 if (r >= N) r -= N;
                 X[(size_t)r * a.xstride] = pn;
@@ -555,7 +584,7 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
             prev = atomicAdd(&a.glob[0], 1u);
         }
         prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev == gridDim.x * gridDim.y - 1) {
+        if (prev == n_items - 1) {
             __threadfence();
             int n_act = 0;
             for (int m0 = 0; m0 < a.M; m0 += 32) {
@@ -583,6 +612,56 @@ __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
                 if (a.use_handle) cudaGraphSetConditional(a.handle, n_act > 0 ? 1u : 0u);
             }
         }
+    }
+    __syncthreads();   // red / s_last free for the CTA's next item
+}
+
+__global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
+    check_item(a, blockIdx.x, blockIdx.y, gridDim.x * gridDim.y);
+}
+
+// Grid-wide barrier of a co-resident (cooperatively launched) grid: bar[0] arrivals, bar[1] the
+// generation. Generic-proxy global writes before it are made visible to the async proxy (the next
+// pass's TMA reads of the gathered x) and to every CTA's L2 reads after it.
+__device__ __forceinline__ void grid_sync(unsigned *bar) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // this thread's x writes -> later TMA reads
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned gen = *reinterpret_cast<volatile unsigned *>(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*reinterpret_cast<volatile unsigned *>(bar + 1) == gen) {
+            }
+        }
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+// The whole power iteration of a plan in ONE launch (a6 with the convergence check fused): a
+// cooperatively launched persistent grid (every CTA resident) runs, while any vector is running,
+// the GEMV pass (gemv_pass, as k_power_step), a grid barrier, the check of every (chunk, vector)
+// item grid-strided over the CTAs (check_item, as k_power_check: normalisation, L1 change, next
+// gathered x, states, active list), and a second grid barrier -- no launches, no graph nodes and
+// no host round trips between iterations. Same arithmetic in the same order as the two-kernel loop.
+template <typename T, int NV>
+__global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_loop(const PowerArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    ring_init<T, NV>(smem);
+    uint32_t q_issue = 0, q_cons = 0;
+    unsigned *bar = a.glob + kGridBarWord;
+    const unsigned n_items = (unsigned)(a.chunks * a.M * a.V);
+    while (__ldcg(a.glob + 1) != 0u) {
+        gemv_pass<T, NV>(a, smem, q_issue, q_cons);
+        grid_sync(bar);
+        for (unsigned it = blockIdx.x; it < n_items; it += gridDim.x)
+            check_item(a, (int)(it % (unsigned)a.chunks), (int)(it / (unsigned)a.chunks), n_items);
+        grid_sync(bar);
     }
 }
 
@@ -685,6 +764,7 @@ __global__ void k_power_init(const PowerArgs a) {
             a.glob[0] = 0u;
             a.glob[1] = n > 0 ? 1u : 0u;
             a.glob[2] = (unsigned)n;
+            a.glob[kGridBarWord] = 0u;        // k_power_loop's grid barrier: no arrivals
         }
     }
 }
@@ -708,38 +788,40 @@ __global__ void k_power_finish(const FinishArgs f) {
 }
 
 template <typename T, int NV>
-void *step_entry(size_t *smem, int *ctas_per_sm) {
+void *step_entry(size_t *smem, int *ctas_per_sm, void **loop) {
     *smem = StepSmem<T, NV>::BYTES;
     *ctas_per_sm = StepSmem<T, NV>::MINB;
     void *fn = (void *)k_power_step<T, NV>;
     if (func_attrs_once(fn, (int)*smem, false) != cudaSuccess) return nullptr;
+    *loop = (void *)k_power_loop<T, NV>;
+    if (func_attrs_once(*loop, (int)*smem, false) != cudaSuccess) *loop = nullptr;
     return fn;
 }
 
-void *step_fn(int dtype, int V, size_t *smem, int *cps) {
+void *step_fn(int dtype, int V, size_t *smem, int *cps, void **loop) {
     if (dtype == SPLIDAR_F64) {
         switch (V) {
-            case 1: return step_entry<double, 1>(smem, cps);
-            case 2: return step_entry<double, 2>(smem, cps);
-            case 4: return step_entry<double, 4>(smem, cps);
-            case 8: return step_entry<double, 8>(smem, cps);
-            case 16: return step_entry<double, 16>(smem, cps);
-            case 17: return step_entry<double, 17>(smem, cps);
-            case 18: return step_entry<double, 18>(smem, cps);
-            case 24: return step_entry<double, 24>(smem, cps);
-            case 32: return step_entry<double, 32>(smem, cps);
+            case 1: return step_entry<double, 1>(smem, cps, loop);
+            case 2: return step_entry<double, 2>(smem, cps, loop);
+            case 4: return step_entry<double, 4>(smem, cps, loop);
+            case 8: return step_entry<double, 8>(smem, cps, loop);
+            case 16: return step_entry<double, 16>(smem, cps, loop);
+            case 17: return step_entry<double, 17>(smem, cps, loop);
+            case 18: return step_entry<double, 18>(smem, cps, loop);
+            case 24: return step_entry<double, 24>(smem, cps, loop);
+            case 32: return step_entry<double, 32>(smem, cps, loop);
         }
     } else {
         switch (V) {
-            case 1: return step_entry<float, 1>(smem, cps);
-            case 2: return step_entry<float, 2>(smem, cps);
-            case 4: return step_entry<float, 4>(smem, cps);
-            case 8: return step_entry<float, 8>(smem, cps);
-            case 16: return step_entry<float, 16>(smem, cps);
-            case 17: return step_entry<float, 17>(smem, cps);
-            case 18: return step_entry<float, 18>(smem, cps);
-            case 24: return step_entry<float, 24>(smem, cps);
-            case 32: return step_entry<float, 32>(smem, cps);
+            case 1: return step_entry<float, 1>(smem, cps, loop);
+            case 2: return step_entry<float, 2>(smem, cps, loop);
+            case 4: return step_entry<float, 4>(smem, cps, loop);
+            case 8: return step_entry<float, 8>(smem, cps, loop);
+            case 16: return step_entry<float, 16>(smem, cps, loop);
+            case 17: return step_entry<float, 17>(smem, cps, loop);
+            case 18: return step_entry<float, 18>(smem, cps, loop);
+            case 24: return step_entry<float, 24>(smem, cps, loop);
+            case 32: return step_entry<float, 32>(smem, cps, loop);
         }
     }
     return nullptr;
@@ -751,7 +833,8 @@ void *step_fn(int dtype, int V, size_t *smem, int *cps) {
 int solver_kernels(int dtype, int V, SolverKernels *out, const PowerArgs &a) {
     out->init_fn = (void *)k_power_init;
     int cps = 2;
-    out->step_fn = step_fn(dtype, V, &out->step_smem, &cps);
+    out->loop_fn = nullptr;
+    out->step_fn = step_fn(dtype, V, &out->step_smem, &cps, &out->loop_fn);
     out->check_fn = (void *)k_power_check;
     out->finish_fn = (void *)k_power_finish;
     out->ssum_fn = (void *)k_shard_ssum;

@@ -486,6 +486,14 @@ class Plan:
         """True when the plan is one clustered launch (N <= 2048), capturable into a CUDA graph."""
         return _lib().splidar_plan_kind(self._h) == 1
 
+    KINDS = {0: "graph", 1: "fused", 2: "loop"}
+
+    @property
+    def kind(self) -> str:
+        """'fused' (N <= 2048, one clustered launch), 'loop' (a graph whose iterations are one cooperative
+        launch of the persistent GEMV + check kernel) or 'graph' (GEMV + check in a conditional WHILE node)."""
+        return self.KINDS[_lib().splidar_plan_kind(self._h)]
+
     GEMV_NAMES = {0: "fused", 1: "fp64", 2: "tensor_i8"}
 
     def gemv(self, stream=None) -> str:
