@@ -207,8 +207,10 @@ struct StepSmem {
 
 // The state of (matrix, vector) mv through L2 (never a stale L1 line: the persistent loop kernel
 // reads states other CTAs wrote in the same launch).
+template <bool CG>
 __device__ __forceinline__ SolveState load_state(const SolveState *p) {
     static_assert(sizeof(SolveState) == 48, "SolveState is three 16-byte words");
+    if constexpr (!CG) return *p;   // a kernel of its own: states from earlier launches only
     SolveState s;
     const int4 *q = reinterpret_cast<const int4 *>(p);
     int4 *d = reinterpret_cast<int4 *>(&s);
@@ -218,11 +220,19 @@ __device__ __forceinline__ SolveState load_state(const SolveState *p) {
     return s;
 }
 
+// A load that bypasses L1 in the persistent loop kernel (CG: values other CTAs wrote in the same
+// launch) and is a plain load in the two-kernel form.
+template <bool CG, typename V>
+__device__ __forceinline__ V ld_x(const V *p) {
+    if constexpr (CG) return __ldcg(p);
+    else return *p;
+}
+
 // One GEMV pass of every active (matrix, vector) over the stored P~0 (the body of k_power_step and of
 // each iteration of k_power_loop). full[]: the CTA's ring mbarriers, initialised by the caller;
 // q_issue / q_cons: the ring's stage sequence numbers, continued across passes. Every cross-CTA
 // input (active list, states, partials) is read through L2.
-template <typename T, int NV>
+template <typename T, int NV, bool CG>
 __device__ __forceinline__ void gemv_pass(const PowerArgs &a, unsigned char *smem, uint32_t &q_issue,
                                           uint32_t &q_cons) {
     using SM = StepSmem<T, NV>;
@@ -238,7 +248,7 @@ __device__ __forceinline__ void gemv_pass(const PowerArgs &a, unsigned char *sme
 
     const int tid = threadIdx.x, b = blockIdx.x, G = gridDim.x;
     const int N = a.N, S = a.strips;
-    const int n_act = (int)__ldcg(a.glob + 2);
+    const int n_act = (int)ld_x<CG>(a.glob + 2);
     const int R = a.rows;                           // rows of the stored block (N, or a row shard)
     const int64_t T_units = (int64_t)n_act * S * R;
     if (T_units == 0) return;
@@ -254,7 +264,7 @@ __device__ __forceinline__ void gemv_pass(const PowerArgs &a, unsigned char *sme
         const int64_t g64 = u / R;                       // strip index in active order
         const int g = (int)g64;
         const int ai = g / S, c = g % S;
-        const int m = __ldcg(a.act + ai);
+        const int m = ld_x<CG>(a.act + ai);
         const int r_lo = (int)(u - g64 * R);
         const int64_t strip_end = (g64 + 1) * R;
         const int r_hi = (int)((u_end < strip_end ? u_end : strip_end) - g64 * R);
@@ -265,7 +275,7 @@ __device__ __forceinline__ void gemv_pass(const PowerArgs &a, unsigned char *sme
             int n = 0;
             unsigned vm = 0;
             for (int v = 0; v < NV; ++v) {
-                const SolveState s = load_state(a.st + (size_t)m * NV + v);
+                const SolveState s = load_state<CG>(a.st + (size_t)m * NV + v);
                 if (!s.done) {
                     s_vmap[n] = v; s_cur[n] = s.cur; ++n;
                     vm |= 1u << v;
@@ -460,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
     if (a.i8 && a.glob[3]) return;                  // the int8 tensor-core GEMV runs this plan
     ring_init<T, NV>(smem);
     uint32_t q_issue = 0, q_cons = 0;               // stage sequence numbers (buffer q % S, parity (q / S) & 1)
-    gemv_pass<T, NV>(a, smem, q_issue, q_cons);
+    gemv_pass<T, NV, false>(a, smem, q_issue, q_cons);
 }
 
 // Convergence check of one iteration (after k_power_step in the WHILE body). CTA (chunk, mv):
@@ -470,12 +480,13 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(
 // sets the WHILE condition. Done vectors are skipped (their pi stays frozen).
 // check_item: the work of CTA (chunk c, vector mv); n_items = chunks x M x V, the count after which the
 // last item rebuilds the active list (one item per CTA in k_power_check, grid-strided in k_power_loop).
+template <bool CG>
 __device__ __forceinline__ void check_item(const PowerArgs &a, int c, int mv, unsigned n_items) {
     __shared__ double red[8];
     __shared__ int s_last;
     const int tid = threadIdx.x;
     const int N = a.N;
-    const SolveState st = load_state(a.st + mv);
+    const SolveState st = load_state<CG>(a.st + mv);
     if (st.done && a.ypart && !a.ypart_shared) {   // row shard: a frozen vector's partial stays zero
         const int j1 = min(N, (c + 1) * kCheckChunk);
         for (int j = c * kCheckChunk + tid; j < j1; j += 256) a.ypart[(size_t)mv * N + j] = 0.0;
@@ -522,7 +533,7 @@ __device__ __forceinline__ void check_item(const PowerArgs &a, int c, int mv, un
                     int j = r0 + e - l;
                     if (j < 0) j += N;
                     const double pn = __ldcg(yn + j) * inv_new;
-                    l1 += fabs(pn - __ldcg(yo + j) * inv_old);
+                    l1 += fabs(pn - ld_x<CG>(yo + j) * inv_old);
                     const uint64_t xt = (uint64_t)ldexp(pn, tau);
 #pragma unroll
                     for (int q = 0; q < 7; ++q) wq[q] |= ((xt >> (8 * (6 - q))) & 0xFFull) << (8 * e);
@@ -539,7 +550,7 @@ __device__ __forceinline__ void check_item(const PowerArgs &a, int c, int mv, un
             const int j1 = min(N, (c + 1) * kCheckChunk);
             for (int j = c * kCheckChunk + tid; j < j1; j += 256) {
                 const double pn = __ldcg(yn + j) * inv_new;
-                l1 += fabs(pn - __ldcg(yo + j) * inv_old);
+                l1 += fabs(pn - ld_x<CG>(yo + j) * inv_old);
                 int r = j + l;
                 if (r >= N) r -= N;
                 X[(size_t)r * a.xstride] = pn;
@@ -617,7 +628,7 @@ __device__ __forceinline__ void check_item(const PowerArgs &a, int c, int mv, un
 }
 
 __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
-    check_item(a, blockIdx.x, blockIdx.y, gridDim.x * gridDim.y);
+    check_item<false>(a, blockIdx.x, blockIdx.y, gridDim.x * gridDim.y);
 }
 
 // Grid-wide barrier of a co-resident (cooperatively launched) grid: bar[0] arrivals, bar[1] the
@@ -657,10 +668,10 @@ __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_loop(
     unsigned *bar = a.glob + kGridBarWord;
     const unsigned n_items = (unsigned)(a.chunks * a.M * a.V);
     while (__ldcg(a.glob + 1) != 0u) {
-        gemv_pass<T, NV>(a, smem, q_issue, q_cons);
+        gemv_pass<T, NV, true>(a, smem, q_issue, q_cons);
         grid_sync(bar);
         for (unsigned it = blockIdx.x; it < n_items; it += gridDim.x)
-            check_item(a, (int)(it % (unsigned)a.chunks), (int)(it / (unsigned)a.chunks), n_items);
+            check_item<true>(a, (int)(it % (unsigned)a.chunks), (int)(it / (unsigned)a.chunks), n_items);
         grid_sync(bar);
     }
 }
