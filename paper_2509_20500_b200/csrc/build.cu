@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(256) k_colsum_reduce(const double *__restrict_
     bool bad = false;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
         double t = 0.0;
-        for (int c = 0; c < nch; ++c) t += part[((size_t)m * nch + c) * N + j];
+#pragma unroll 8
+        for (int c = 0; c < nch; ++c) t += __ldcg(part + ((size_t)m * nch + c) * N + j);   // loads in flight, fixed-order adds
         colsum[(size_t)m * N + j] = t;
         if (cst.emax_part) {
             int mx = 0, mn = 1 << 20;

@@ -497,16 +497,29 @@ __device__ __forceinline__ void check_item(const PowerArgs &a, int c, int mv, un
         // all CTAs of (matrix, vector) hold the bitwise-same s
         const bool i8 = a.i8 && a.glob[3];
         const int nstrips = i8 ? a.strips_i8 : a.strips;
-        double S = 0.0;
-        const double *ss = a.ssum + (size_t)mv * nstrips;
-        for (int k = tid & 31; k < nstrips; k += 32) S += __ldcg(ss + k);
-        S = warp_sum(S);
-        const double inv_new = 1.0 / S, inv_old = 1.0 / st.s;
         // row shard: y = the all-reduced partial products (a.ypart); it is also kept in y[1 - cur] as
         // the next iterate (finish kernel, next change)
         const double *yn = a.ypart ? a.ypart + (size_t)(a.ypart_shared ? m : mv) * N
                                    : a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
         const double *yo = a.y + ((size_t)mv * 2 + st.cur) * N;
+        // the chunk's y loads (E per thread) go out before the strip-sum reduction and stay in flight
+        // together (the X stores below could alias them as far as the compiler knows)
+        constexpr int E = kCheckChunk / 256;
+        double yv[E], ov[E];
+        if (!i8) {
+            const int j1 = min(N, (c + 1) * kCheckChunk);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int j = c * kCheckChunk + tid + e * 256;
+                yv[e] = j < j1 ? __ldcg(yn + j) : 0.0;
+                ov[e] = j < j1 ? ld_x<CG>(yo + j) : 0.0;
+            }
+        }
+        double S = 0.0;
+        const double *ss = a.ssum + (size_t)mv * nstrips;
+        for (int k = tid & 31; k < nstrips; k += 32) S += __ldcg(ss + k);
+        S = warp_sum(S);
+        const double inv_new = 1.0 / S, inv_old = 1.0 / st.s;
         if (a.ypart) {
             double *yw = a.y + ((size_t)mv * 2 + (1 - st.cur)) * N;
             const int j1 = min(N, (c + 1) * kCheckChunk);
@@ -548,12 +561,16 @@ __device__ __forceinline__ void check_item(const PowerArgs &a, int c, int mv, un
         } else {
             double *X = a.X + (size_t)m * N * a.xstride + v;
             const int j1 = min(N, (c + 1) * kCheckChunk);
-            for (int j = c * kCheckChunk + tid; j < j1; j += 256) {
-                const double pn = __ldcg(yn + j) * inv_new;
-                l1 += fabs(pn - ld_x<CG>(yo + j) * inv_old);
-                int r = j + l;
-                if (r >= N) r -= N;
-                X[(size_t)r * a.xstride] = pn;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int j = c * kCheckChunk + tid + e * 256;
+                if (j < j1) {
+                    const double pn = yv[e] * inv_new;
+                    l1 += fabs(pn - ov[e] * inv_old);
+                    int r = j + l;
+                    if (r >= N) r -= N;
+                    X[(size_t)r * a.xstride] = pn;
+                }
             }
         }
         l1 = warp_sum(l1);
