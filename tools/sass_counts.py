@@ -13,7 +13,7 @@ LIB = os.path.join(ROOT, "paper_2509_20500_b200", "lib", "libsplidar.so")
 OPS = ["UTCIMMA", "LDTM", "UTCBAR", "UTMALDG", "UBLKCP", "DMMA", "DFMA", "DADD", "DMUL", "SYNCS", "PRMT",
        "LDS", "STS", "LDG", "STG", "SHFL", "BAR", "MUFU", "F2F"]
 WANT = ["k_power_step_i8IfE", "k_power_step_i8e", "k_enc_colexp", "k_power_step_i8IdE", "k_power_stepIdLi17E", "k_power_stepIfLi17E", "k_power_stepIdLi1E",
-        "k_power_check", "k_i8_colexpIfE", "k_buildIdLi0E", "k_power_fusedIdLi1E", "k_struct_solve_c1", "k_mc"]
+        "k_power_check", "k_power_loopIdLi17E", "k_power_loopIdLi1E", "k_i8_colexpIfE", "k_buildIdLi0E", "k_power_fusedIdLi1E", "k_struct_solve_c1", "k_mc"]
 
 sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s*Function : ", sass)
