@@ -526,6 +526,10 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
             f.st = a.st;
             f.tol = a.tol;
             f.max_iter = a.max_iter;
+            {
+                const char *e2 = getenv("SPLIDAR_FUSED_P2P");
+                f.p2p = (e2 && e2[0] == '0') ? 0 : 1;
+            }
             return SPLIDAR_OK;
         }
     }

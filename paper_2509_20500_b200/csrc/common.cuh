@@ -220,6 +220,7 @@ struct FusedArgs {
     SolveState *st;             // [M][V]
     double tol;
     int max_iter;
+    int p2p;                    // exchanges by st.async + per-CTA mbarriers (else barrier.cluster)
 };
 int fused_shape(int N, int *C, int *R);
 int fused_resident(int N, int R, int dtype);

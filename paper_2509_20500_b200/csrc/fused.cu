@@ -118,6 +118,19 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     }
     double s_prev = 1.0, dpart = 0.0, change = __longlong_as_double(0x7ff0000000000000ll);
     int k = 0, conv = 0;
+    // p2p exchanges: every value another CTA delivers is an st.async whose bytes complete a phase of
+    // my mbarrier xbar[0] (partials + change partials, A) or xbar[1] (y + sums, B); thread 0 arms each
+    // phase with the bytes it will receive, everyone waits on its parity. Single buffers suffice: a
+    // CTA only sends phase-A data of the next product after it has every CTA's phase-B data of this
+    // one, which each sends after it has read its own buffers (and the same for phase B).
+    __shared__ uint64_t xbar[2];
+    const int ncols = min(N, (c + 1) * R) - c * R;           // my owned columns == my rows
+    const uint32_t bytesA = 8u * (uint32_t)C * (uint32_t)(ncols + 1), bytesB = 8u * (uint32_t)(ncols + C);
+    if (a.p2p && threadIdx.x == 0) {
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
+        fence_mbar_init();
+    }
     cl.sync();
     for (;;) {
         // ---- A: partial y over my rows; column j = 2 t + 512 q + e. Resident rows: from shared
@@ -184,19 +197,39 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
             }
         }
         // push partials to the owners of the columns: recv[c][j - owner R] in the owner's smem
+        if (a.p2p) {
+            if (threadIdx.x == 0) mbar_expect_tx(&xbar[0], bytesA);
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
+            for (int q = 0; q < Q; ++q) {
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int j = 2 * threadIdx.x + 2 * kFT * q + e;
-                if (j < N) {
-                    const int ow = j / R;
-                    cl.map_shared_rank(recv, ow)[(size_t)c * R + (j - ow * R)] = acc[2 * q + e];
+                for (int e = 0; e < 2; ++e) {
+                    const int j = 2 * threadIdx.x + 2 * kFT * q + e;
+                    if (j < N) {
+                        const uint32_t ow = (uint32_t)(j / R);
+                        st_async_f64(mapa_u32(smem_u32(recv + (size_t)c * R + (j - (int)ow * R)), ow), acc[2 * q + e],
+                                     mapa_u32(smem_u32(&xbar[0]), ow));
+                    }
                 }
             }
+            if (threadIdx.x < C)
+                st_async_f64(mapa_u32(smem_u32(&sh.exA[kFMaxC + c]), threadIdx.x), dpart,
+                             mapa_u32(smem_u32(&xbar[0]), threadIdx.x));
+            mbar_wait(&xbar[0], (uint32_t)k & 1u);
+        } else {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = 2 * threadIdx.x + 2 * kFT * q + e;
+                    if (j < N) {
+                        const int ow = j / R;
+                        cl.map_shared_rank(recv, ow)[(size_t)c * R + (j - ow * R)] = acc[2 * q + e];
+                    }
+                }
+            }
+            if (threadIdx.x < C) cl.map_shared_rank(sh.exA, threadIdx.x)[kFMaxC + c] = dpart;
+            cl.sync();   // A
         }
-        if (threadIdx.x < C) cl.map_shared_rank(sh.exA, threadIdx.x)[kFMaxC + c] = dpart;
-        cl.sync();   // A
         if (k > 0) {
             double t = 0.0;
             for (int cc = 0; cc < C; ++cc) t += sh.exA[kFMaxC + cc];
@@ -208,17 +241,28 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
         double ys = 0.0, yj = 0.0;
         const int j = c * R + (int)threadIdx.x;
         const bool own = (int)threadIdx.x < R && j < N;
+        if (a.p2p && threadIdx.x == 0) mbar_expect_tx(&xbar[1], bytesB);
         if (own) {
             for (int cc = 0; cc < C; ++cc) yj += recv[(size_t)cc * R + threadIdx.x];
             ys = yj;
             int r = j + l;
             if (r >= N) r -= N;
             const int ow = r / R;
-            cl.map_shared_rank(xb, ow)[r - ow * R] = yj;
+            if (a.p2p)
+                st_async_f64(mapa_u32(smem_u32(xb + (r - ow * R)), (uint32_t)ow), yj,
+                             mapa_u32(smem_u32(&xbar[1]), (uint32_t)ow));
+            else
+                cl.map_shared_rank(xb, ow)[r - ow * R] = yj;
         }
         ys = fblock_sum(ys, sh.red);
-        if (threadIdx.x < C) cl.map_shared_rank(sh.exB, threadIdx.x)[c] = ys;
-        cl.sync();   // B
+        if (a.p2p) {
+            if (threadIdx.x < C)
+                st_async_f64(mapa_u32(smem_u32(&sh.exB[c]), threadIdx.x), ys, mapa_u32(smem_u32(&xbar[1]), threadIdx.x));
+            mbar_wait(&xbar[1], (uint32_t)k & 1u);
+        } else {
+            if (threadIdx.x < C) cl.map_shared_rank(sh.exB, threadIdx.x)[c] = ys;
+            cl.sync();   // B
+        }
         double s = 0.0;
         for (int cc = 0; cc < C; ++cc) s += sh.exB[cc];
         // ---- C: L1 change of the normalised iterates over my columns
@@ -231,6 +275,7 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
         s_prev = s;
         ++k;
     }
+    if (a.p2p) cl.sync();   // nothing is in flight to a CTA that exits (every phase was waited for)
     // pi^k = y / s over my columns
     const int o = a.n_inline ? a.oidx_in[mv] : a.out_idx[mv];
     if (o >= 0) {

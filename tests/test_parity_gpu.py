@@ -360,6 +360,27 @@ def test_fused_equals_general_path(spl, case, monkeypatch):
         general.close()
 
 
+@pytest.mark.parametrize("n", [2, 37, 256, 700, 1024, 1537, 2048])
+def test_fused_p2p_exchange_equals_cluster_barrier(spl, n, monkeypatch):
+    """The fused solver's exchanges by st.async + per-CTA mbarriers (default) against the same solver
+    with barrier.cluster exchanges (SPLIDAR_FUSED_P2P=0): the same sums in the same order, so pi is
+    bit-identical and the infos equal; resident (N <= 384) and L2-streamed rows, several dead times."""
+    f = random_flux(np.random.default_rng(4400 + n), n, 2)
+    P0 = spl.build_base(f, torch.float64)
+    T = np.array([[3.0, 61.5, 140.0]])
+    a = spl.Plan(P0, f.t_r, T, tol=1e-12)
+    monkeypatch.setenv("SPLIDAR_FUSED_P2P", "0")
+    b = spl.Plan(P0, f.t_r, T, tol=1e-12)
+    monkeypatch.delenv("SPLIDAR_FUSED_P2P")
+    assert a.fused and b.fused
+    ia, ib = a.execute(check=False), b.execute(check=False)
+    assert torch.equal(a.pi, b.pi) and ia == ib
+    a.execute(check=False)                       # relaunch: the mbarrier phases start again
+    assert torch.equal(a.pi, b.pi)
+    a.close()
+    b.close()
+
+
 def test_ragged_large_n(spl):
     """N = 9001 (> 8192: the tiled flux-vector scans; a ragged last 512-column strip for the build and
     the graph-path GEMV; a 3-CTA cluster with a ragged last CTA for the structured solve): sampled rows
