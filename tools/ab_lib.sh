@@ -9,8 +9,8 @@ for i in $(seq 1 $REPS); do
     cp ab/$v.so $LIB && touch $LIB
     timeout -s KILL 600 python bench.py $ARGS --no-cpu-baseline > gpurun_out/ab_$v.json 2> gpurun_out/ab_$v.err
     python -c "
-import json; d=json.load(open('gpurun_out/ab_$v.json')); r=d['roofline']
-print('$v', round(d['value'],2), 'build', round(d['ms_build_per_step'],4), 'solve', round(d['ms_solve_per_step'],4), d['clocks']['sm_mhz'], 'frac', round(r['frac'],4), 'e2e', round(d['e2e']['value'],1) if d.get('e2e') else None)"
+import json; d=json.load(open('gpurun_out/ab_$v.json')); r=d.get('roofline') or {}
+print('$v', round(d['value'],2), 'ms/step', round(d['ms_per_step'],4), 'build', d.get('ms_build_per_step'), 'solve', d.get('ms_solve_per_step'), d['clocks']['sm_mhz'], 'frac', round(r.get('frac') or 0,4), 'e2e', round(d['e2e']['value'],1) if d.get('e2e') else None)"
   done
 done
 cp ab/new.so $LIB && touch $LIB
