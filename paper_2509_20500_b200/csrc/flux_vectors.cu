@@ -341,16 +341,63 @@ __device__ double small_scan(double (&v)[kSEl], double *wt) {
     return tot;
 }
 
+// small_scan of two arrays at once (the same sums in the same order for each, one set of barriers)
+__device__ void small_scan2(double (&v)[kSEl], double (&u)[kSEl], double *wt, double *wu) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 1; i < kSEl; ++i) {
+        v[i] += v[i - 1];
+        u[i] += u[i - 1];
+    }
+    double x = v[kSEl - 1], y = u[kSEl - 1];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double a = __shfl_up_sync(0xffffffffu, x, o), c = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) { x += a; y += c; }
+    }
+    double ex = __shfl_up_sync(0xffffffffu, x, 1), ey = __shfl_up_sync(0xffffffffu, y, 1);
+    if (lane == 0) { ex = 0.0; ey = 0.0; }
+    if (lane == 31) { wt[warp] = x; wu[warp] = y; }
+    __syncthreads();
+    if (warp == 0) {
+        const bool in = lane < (int)(blockDim.x >> 5);
+        double z = in ? wt[lane] : 0.0, q = in ? wu[lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double a = __shfl_up_sync(0xffffffffu, z, o), c = __shfl_up_sync(0xffffffffu, q, o);
+            if (lane >= o) { z += a; q += c; }
+        }
+        double ze = __shfl_up_sync(0xffffffffu, z, 1), qe = __shfl_up_sync(0xffffffffu, q, 1);
+        if (lane == 0) { ze = 0.0; qe = 0.0; }
+        wt[32 + lane] = ze;
+        wu[32 + lane] = qe;
+    }
+    __syncthreads();
+    const double ov = wt[32 + warp] + ex, ou = wu[32 + warp] + ey;
+#pragma unroll
+    for (int i = 0; i < kSEl; ++i) {
+        v[i] += ov;
+        u[i] += ou;
+    }
+}
+
 __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ fluxes, int N, VecPtrs b,
-                                                   int64_t vstride, const FluxDev single, int use_single) {
-    __shared__ double wt[65];
+                                                   int64_t vstride, const __grid_constant__ FluxDev single,
+                                                   int use_single) {
+    __shared__ double wt[65], wu[65];
     __shared__ FluxDev fs;               // the profile's parameters: shared-memory loads in the erfc loops
     extern __shared__ double rev[];      // [blockDim * 8]: w reversed, then its inclusive scan; then
                                          // [blockDim * 8]: lambda_j (own slots)
     const int nslot = (int)blockDim.x * kSEl;
     double *lams = rev + nslot;
     const int m = blockIdx.x;
-    if (threadIdx.x == 0) fs = use_single ? single : fluxes[m];   // one profile: passed by value
+    {   // the profile's parameters (one profile: passed by value), one 8-byte word per thread
+        static_assert(sizeof(FluxDev) % 8 == 0, "FluxDev is copied as 8-byte words");
+        const unsigned long long *src = use_single ? reinterpret_cast<const unsigned long long *>(&single)
+                                                   : reinterpret_cast<const unsigned long long *>(fluxes + m);
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(&fs);
+        for (int i = threadIdx.x; i < (int)(sizeof(FluxDev) / 8); i += blockDim.x) dst[i] = src[i];
+    }
     __syncthreads();
     const FluxDev &f = fs;
     const int e0 = threadIdx.x * kSEl;
@@ -421,10 +468,11 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
         if (e < N) {
             const double Fe = rev[e];
             const double lm = flux_rate(f, bin_centre(f, e));
+            const double ef = exp(-Fe);
             F[e] = Fe;
             lam[e] = lm;
-            lams[e] = lm;
-            wj = lm * exp(-Fe);
+            lams[e] = ef;                        // e^{-F_j}: 1/Z_j = e^{-F_j} / D_j below
+            wj = lm * ef;
             w[e] = wj;
         }
         rev[e] = wj;
@@ -435,32 +483,37 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
     __syncthreads();                             // own slots read: rev[] now takes w reversed
 #pragma unroll
     for (int i = 0; i < kSEl; ++i) rev[nslot - 1 - (e0 + i)] = wv[i];
-    double pf[kSEl];
+    double pf[kSEl], sf[kSEl];
 #pragma unroll
     for (int i = 0; i < kSEl; ++i) pf[i] = wv[i];
-    small_scan(pf, wt);                          // prefix of w (its barriers publish rev[])
-    {
-        double sf[kSEl];
+    __syncthreads();                             // the reversed w is in rev[]
 #pragma unroll
-        for (int i = 0; i < kSEl; ++i) sf[i] = rev[e0 + i];
-        small_scan(sf, wt);                      // inclusive scan of the reversed w
+    for (int i = 0; i < kSEl; ++i) sf[i] = rev[e0 + i];
+    small_scan2(pf, sf, wt, wu);                 // prefix of w and inclusive scan of the reversed w
 #pragma unroll
-        for (int i = 0; i < kSEl; ++i) rev[e0 + i] = sf[i];
-    }
+    for (int i = 0; i < kSEl; ++i) rev[e0 + i] = sf[i];
     __syncthreads();
-    int bad = 0;
+    // D_r = U_r + e^{-Lambda} L_r at the owner's slots (rev[nslot - 1 - r] held U_r: only this thread
+    // reads it), then 1/D and 1/Z with one division per element strided over all threads (the
+    // owner-slot form ran up to 16 dependent divisions in the 32 threads that own the positions)
 #pragma unroll
     for (int i = 0; i < kSEl; ++i) {
         const int r = e0 + i;
         if (r < N) {
             const double L = pf[i] - wv[i];                   // sum_{j < r} w_j (exclusive prefix)
             const double U = rev[nslot - 1 - r];              // sum_{j >= r} w_j (inclusive suffix)
-            const double D = U + eL * L;
-            bad |= !(D > 0.0 && isfinite(D));
-            const double id = 1.0 / D;
-            invD[r] = id;
-            invZ[r] = id * (wv[i] / lams[e0 + i]);            // e^{-F_r} / D_r
+            rev[nslot - 1 - r] = U + eL * L;
         }
+    }
+    __syncthreads();
+    int bad = 0;
+#pragma unroll 1
+    for (int r = threadIdx.x; r < N; r += blockDim.x) {
+        const double D = rev[nslot - 1 - r];
+        bad |= !(D > 0.0 && isfinite(D));
+        const double id = 1.0 / D;
+        invD[r] = id;
+        invZ[r] = id * lams[r];                               // e^{-F_r} / D_r
     }
     if (threadIdx.x == 0) {
         b.scal[m * 8 + 0] = Lam;
