@@ -702,7 +702,15 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
     kp.sharedMemBytes = 0;
     kp.kernelParams = check_args;
     cudaGraphNode_t n_check;
-    SPL_CUDA(cudaGraphAddKernelNode(&n_check, body, &n_step, 1, &kp));
+    if (pdl_enabled()) {   // programmatic edge: the check's CTAs are scheduled while the GEMV runs
+        SPL_CUDA(cudaGraphAddKernelNode(&n_check, body, nullptr, 0, &kp));
+        cudaGraphEdgeData ed = {};
+        ed.from_port = cudaGraphKernelNodePortProgrammatic;
+        ed.type = cudaGraphDependencyTypeProgrammatic;
+        SPL_CUDA(cudaGraphAddDependencies_v2(body, &n_step, &n_check, &ed, 1));
+    } else {
+        SPL_CUDA(cudaGraphAddKernelNode(&n_check, body, &n_step, 1, &kp));
+    }
 
     std::vector<unsigned char> &fa = p->fin_args;
     fa.resize(finish_args_size());

@@ -11,6 +11,7 @@
 // broadcast scalar (1/D_r or 1/Z_r, F_r). The kernel is a pure HBM write stream: N^2 * b bytes.
 #include "common.cuh"
 #include "fixpt.cuh"
+#include "ptx.cuh"
 
 namespace spl {
 namespace {
@@ -27,6 +28,8 @@ k_build(const VecPtrs base, int64_t vstride, int N, T *__restrict__ P0, int64_t 
         int nrows, int rows_per_cta, double *__restrict__ colsum_part, const ColStats cst) {
     constexpr int VEC = Vec16<T>::n;
     using V = typename Vec16<T>::type;
+    pdl_wait();        // PDL secondary of the flux-vector kernel (launch_build); no-op otherwise
+    pdl_trigger();     // the consumer (fused solver / iteration graph) may be scheduled now
     const int m = blockIdx.z;
     const double *__restrict__ w = base.w + m * vstride;
     const double *__restrict__ lam = base.lam + m * vstride;
@@ -330,20 +333,29 @@ cudaError_t launch_build(const VecPtrs base, int64_t vstride, int M, int N, int 
     }
     const int rpc = (nrows + nch - 1) / nch;
     dim3 grid((N + kStripCols - 1) / kStripCols, nch, M);
+    // a PDL secondary of the kernel before it on s (k_build waits for it before any global access)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kStripCols / (dtype == SPLIDAR_F64 ? 2 : 4));
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaError_t e;
     if (dtype == SPLIDAR_F64) {
-        dim3 block(kStripCols / 2);
         if (mode == SPLIDAR_ENTRY_EXP)
-            k_build<double, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
+            e = cudaLaunchKernelEx(&cfg, k_build<double, SPLIDAR_ENTRY_EXP>, base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
         else
-            k_build<double, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
+            e = cudaLaunchKernelEx(&cfg, k_build<double, SPLIDAR_ENTRY_FACTORED>, base, vstride, N, (double *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
     } else {
-        dim3 block(kStripCols / 4);
         if (mode == SPLIDAR_ENTRY_EXP)
-            k_build<float, SPLIDAR_ENTRY_EXP><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
+            e = cudaLaunchKernelEx(&cfg, k_build<float, SPLIDAR_ENTRY_EXP>, base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
         else
-            k_build<float, SPLIDAR_ENTRY_FACTORED><<<grid, block, 0, s>>>(base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
+            e = cudaLaunchKernelEx(&cfg, k_build<float, SPLIDAR_ENTRY_FACTORED>, base, vstride, N, (float *)P0, ld, mstride, row0, nrows, rpc, colsum_part, cst);
     }
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess && colsum_part) {
         k_colsum_reduce<<<dim3((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, M), 256, 0, s>>>(colsum_part, nch, N, M,
                                                                                           colsum, cst);

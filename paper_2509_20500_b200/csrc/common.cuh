@@ -68,6 +68,10 @@ int pad_vectors(int V);
 // ---- per-device host state (device.cu) -------------------------------------------------------
 int current_device();
 int device_sm_count();              // SMs of the current device (cached per device ordinal)
+// Programmatic dependent launch between the library's own consecutive kernels (the build after the
+// flux vectors, the fused solver after the build, the check after the GEMV in the iteration graph):
+// on unless SPLIDAR_PDL=0 (read once per process).
+bool pdl_enabled();
 // cudaFuncSetAttribute once per (device, kernel, value): max dynamic shared memory (if > 0) and
 // non-portable cluster sizes (if requested).
 cudaError_t func_attrs_once(const void *fn, int max_dyn_smem, bool nonportable_cluster);

@@ -2,6 +2,7 @@
 // (device, context), so every cache here is keyed by the current device ordinal. A process that
 // drives several GPUs (cudaSetDevice / torch.cuda.set_device between calls) gets each kernel's
 // attributes set once on every device it launches on. Never called inside a stream capture.
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -34,6 +35,14 @@ int device_sm_count() {
     }
     cache[dev] = n;
     return n;
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("SPLIDAR_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 cudaError_t func_attrs_once(const void *fn, int max_dyn_smem, bool nonportable_cluster) {

@@ -28,6 +28,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace spl {
 namespace {
@@ -390,6 +391,7 @@ __global__ void __launch_bounds__(kST) k_vec_small(const FluxDev *__restrict__ f
                                          // [blockDim * 8]: lambda_j (own slots)
     const int nslot = (int)blockDim.x * kSEl;
     double *lams = rev + nslot;
+    pdl_trigger();     // the build (a PDL secondary) may be scheduled while the vectors are computed
     const int m = blockIdx.x;
     {   // the profile's parameters (one profile: passed by value), one 8-byte word per thread
         static_assert(sizeof(FluxDev) % 8 == 0, "FluxDev is copied as 8-byte words");

@@ -63,6 +63,7 @@ template <typename T, int Q>
 __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     constexpr int NC = 2 * Q;
     constexpr int RS = Q <= 2 ? 8 : 4;
+    pdl_wait();        // PDL secondary of the build (launch_fused); no-op otherwise
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double fsm[];
     __shared__ FusedShared sh;
@@ -356,13 +357,15 @@ cudaError_t launch_fused(int dtype, const FusedArgs &a, cudaStream_t s) {
     cfg.blockDim = dim3(kFT);
     cfg.dynamicSmemBytes = fused_smem(a, dtype);
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = (unsigned)a.C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL secondary of the build
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     void *fn = nullptr;
     cudaError_t e = fused_fn(dtype, a.N, &fn);
     if (e != cudaSuccess) return e;

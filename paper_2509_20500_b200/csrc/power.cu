@@ -467,6 +467,7 @@ __device__ __forceinline__ void ring_init(unsigned char *smem) {
 template <typename T, int NV>
 __global__ void __launch_bounds__(kThreads, StepSmem<T, NV>::MINB) k_power_step(const PowerArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
+    pdl_trigger();                                  // the check (programmatic graph edge) may be scheduled
     if (a.i8 && a.glob[3]) return;                  // the int8 tensor-core GEMV runs this plan
     ring_init<T, NV>(smem);
     uint32_t q_issue = 0, q_cons = 0;               // stage sequence numbers (buffer q % S, parity (q / S) & 1)
@@ -645,6 +646,7 @@ __device__ __forceinline__ void check_item(const PowerArgs &a, int c, int mv, un
 }
 
 __global__ void __launch_bounds__(256) k_power_check(const PowerArgs a) {
+    pdl_wait();        // PDL secondary of the GEMV in the iteration graph; no-op otherwise
     check_item<false>(a, blockIdx.x, blockIdx.y, gridDim.x * gridDim.y);
 }
 

@@ -23,6 +23,15 @@ __device__ __forceinline__ void ktime_end(unsigned long long *kt) {
     if (kt) atomicMax(kt + 1, global_ns());
 }
 
+// Programmatic dependent launch (PDL). pdl_trigger: this CTA lets the next kernel of the stream /
+// graph edge be scheduled now (its CTAs may become resident while this grid still runs); pdl_wait:
+// blocks until every prerequisite grid has completed and its memory operations are visible. Every
+// kernel that may be launched as a PDL secondary calls pdl_wait before its first global access
+// (read or write), so completion stays transitive along a chain of PDL edges. Both are no-ops in a
+// launch without the PDL attribute / programmatic edge.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
