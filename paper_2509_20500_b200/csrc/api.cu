@@ -529,6 +529,11 @@ static splidar_status plan_build(splidar_plan_s *p, int dt, double *pi, char *ws
             {
                 const char *e2 = getenv("SPLIDAR_FUSED_P2P");
                 f.p2p = (e2 && e2[0] == '0') ? 0 : 1;
+                const char *e3 = getenv("SPLIDAR_FUSED_LDG");   // 0: rows not resident stream through a TMA ring
+                f.ldg = (e3 && e3[0] == '0') ? 0 : 1;
+                const char *e4 = getenv("SPLIDAR_FUSED_1X");    // 0: two exchanges per product
+                // (the TMA ring leaves no shared memory for the double buffers at N = 2048)
+                f.one_x = (f.p2p && (f.resident || f.ldg) && !(e4 && e4[0] == '0')) ? 1 : 0;
             }
             return SPLIDAR_OK;
         }

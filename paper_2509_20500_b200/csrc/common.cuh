@@ -225,6 +225,9 @@ struct FusedArgs {
     double tol;
     int max_iter;
     int p2p;                    // exchanges by st.async + per-CTA mbarriers (else barrier.cluster)
+    int ldg;                    // non-resident rows: read-only global loads into registers (else TMA ring)
+    int one_x;                  // one exchange per product: partials go straight to the CTA whose rows
+                                // they feed (needs p2p); else owners sum and redistribute (two)
 };
 int fused_shape(int N, int *C, int *R);
 int fused_resident(int N, int R, int dtype);

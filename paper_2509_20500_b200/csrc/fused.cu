@@ -5,20 +5,25 @@
 //
 // Cluster of C CTAs (C = min(16, ceil(N / 32))): CTA c owns the rows [c R, (c + 1) R) of P~0 and the
 // output columns [c W, (c + 1) W) (R = W = ceil(N / C)). Its rows of P~0 are copied to shared memory
-// once when they fit in 96 KB (N <= 384 fp64 / 512 fp32 at R = 32), else streamed from L2 through a
-// 3-stage shared-memory ring of TMA bulk copies (64 KB per stage, issued by one thread). One product pi P~ = x P~0 with the gathered
-// x_r = v[(r - l) mod N] (Thm 2):
-//   A  partial y over the CTA's rows (x_r from shared memory, fp64 FMA) ->
-//      each partial column slice pushed to its owner over DSMEM; barrier.cluster
-//   B  owners add the C partials in fixed order -> y_j; sum of y; y_j pushed (unnormalised) to the
-//      x buffer of the CTA owning row (j + l) mod N; barrier.cluster
-//   C  s = sum y, the L1 change of the normalised iterates (published with the next A)
+// once when they fit in 96 KB (N <= 384 fp64 / 512 fp32 at R = 32), else read from L2 straight into
+// registers (16 rows of 16-byte loads in flight per thread; SPLIDAR_FUSED_LDG=0: a 3-stage
+// shared-memory ring of TMA bulk copies, 64 KB per stage). One product pi P~ = x P~0 with the
+// gathered x_r = v[(r - l) mod N] (Thm 2), default form (ONE exchange per product):
+//   A  partial y over the CTA's rows (x_r from shared memory, fp64 FMA) -> the partial of column j
+//      pushed (st.async, completing the receiver's mbarrier) to the CTA owning row (j + l) mod N, with
+//      the CTA's partial total and its change partial of the previous product
+//   B  every CTA adds the C partials of each of its rows in fixed CTA order -> x_r = y_{r-l}
+//      (unnormalised); s = sum of the C totals; the L1 change over its rows (published with the next A)
+// SPLIDAR_FUSED_1X=0: the two-exchange form (owners of columns add the partials, then push y_j to
+// row (j + l) mod N and the sums; barrier.cluster or st.async per exchange). Same y in the same order;
+// s is summed in another order, so the two forms agree to rounding.
 // Same definition as the general path: pi^0 = 1/N, pi^{k+1} = y / ||y||_1, stop after the first
 // product with ||pi^{k+1} - pi^k||_1 < tol (decided one exchange later, on identical sums in every
 // CTA), or after max_iter products. Deterministic: fixed-order sums, no atomics.
 #include <cooperative_groups.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -38,6 +43,8 @@ struct FusedShared {
     double exA[2 * kFMaxC];       // scan of nothing: [0] unused, change partials
     double exB[kFMaxC];           // sum partials
     double red[kFT / 32];
+    double tx[2][kFMaxC];         // one-exchange form: every CTA's partial-y total, by product parity
+    double dx[2][kFMaxC];         // and its change partial of the previous product
 };
 
 __device__ __forceinline__ double fwarp_sum(double x) {
@@ -63,6 +70,7 @@ template <typename T, int Q>
 __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     constexpr int NC = 2 * Q;
     constexpr int RS = Q <= 2 ? 8 : 4;
+    constexpr int RSG = Q <= 2 ? 16 : 8;     // direct global loads: twice the rows in flight
     pdl_wait();        // PDL secondary of the build (launch_fused); no-op otherwise
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double fsm[];
@@ -76,7 +84,9 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     double *recv = fsm + R;                          // [C][R]   partials of my columns from every CTA
     double *yp = recv + (size_t)C * R;               // [R]      previous y of my columns
     const int NP = (N + 3) & ~3;                     // row stride: 16-byte aligned rows for both dtypes
-    T *slice = reinterpret_cast<T *>(fsm + (((size_t)R * (C + 2) + 1) & ~(size_t)1));   // [R][NP] (a.resident)
+    // one-exchange form: [2][C][R] partials of my rows' x from every CTA in place of recv / yp
+    const size_t head = (size_t)R * (a.one_x ? 2 * C + 1 : C + 2);
+    T *slice = reinterpret_cast<T *>(fsm + ((head + 1) & ~(size_t)1));   // [R][NP] (a.resident)
     if (l < 0) {                                     // padding vector: nothing to solve
         if (c == 0 && threadIdx.x == 0) {
             SolveState st = {};
@@ -97,7 +107,7 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     __shared__ uint64_t rbar[kRing];
     uint32_t q_issue = 0, q_cons = 0;
     const double *xrow = nullptr;
-    if (!a.resident && threadIdx.x == 0) {
+    if (!a.resident && !a.ldg && threadIdx.x == 0) {
         for (int i = 0; i < kRing; ++i) mbar_init(&rbar[i], 1);
         fence_mbar_init();
     }
@@ -127,20 +137,23 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     __shared__ uint64_t xbar[2];
     const int ncols = min(N, (c + 1) * R) - c * R;           // my owned columns == my rows
     const uint32_t bytesA = 8u * (uint32_t)C * (uint32_t)(ncols + 1), bytesB = 8u * (uint32_t)(ncols + C);
-    if (a.p2p && threadIdx.x == 0) {
+    if ((a.p2p || a.one_x) && threadIdx.x == 0) {
         mbar_init(&xbar[0], 1);
         mbar_init(&xbar[1], 1);
         fence_mbar_init();
     }
     cl.sync();
-    for (;;) {
+    // one product: acc[2 q + e] = partial y of column j = 2 t + 2 kFT q + e over my rows (x = xb)
+    auto gemv = [&](double (&acc)[NC]) {
+#pragma unroll
+        for (int i = 0; i < NC; ++i) acc[i] = 0.0;
         // ---- A: partial y over my rows; column j = 2 t + 512 q + e. Resident rows: from shared
         // memory, RS rows per step. Otherwise rows stream through a 3-stage shared-memory ring filled by
         // TMA bulk copies (thread 0 issues, mbarrier complete_tx), so ~kRing x 64 KB are in flight.
-        double acc[NC];
-#pragma unroll
-        for (int i = 0; i < NC; ++i) acc[i] = 0.0;
-        auto rows_fma = [&](const T *base, int64_t rs, int n) {
+        // from_global: read-only loads from L2 straight into registers (no shared-memory staging)
+        // rows_c: rows whose loads are in flight together
+        auto rows_fma = [&](auto from_global, auto rows_c, const T *base, int64_t rs, int n) {
+            constexpr int RS = decltype(rows_c)::value;
             for (int r = 0; r < n; r += RS) {
                 double xr[RS];
                 double pv[RS][NC];
@@ -155,10 +168,14 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
                         pv[rr][2 * q] = pv[rr][2 * q + 1] = 0.0;
                         if (j < N) {
                             if constexpr (sizeof(T) == 8) {
-                                const double2 v = *reinterpret_cast<const double2 *>(row + j);
+                                const double2 v = decltype(from_global)::value
+                                                      ? __ldg(reinterpret_cast<const double2 *>(row + j))
+                                                      : *reinterpret_cast<const double2 *>(row + j);
                                 pv[rr][2 * q] = v.x; pv[rr][2 * q + 1] = v.y;
                             } else {
-                                const float2 v = *reinterpret_cast<const float2 *>(row + j);
+                                const float2 v = decltype(from_global)::value
+                                                     ? __ldg(reinterpret_cast<const float2 *>(row + j))
+                                                     : *reinterpret_cast<const float2 *>(row + j);
                                 pv[rr][2 * q] = v.x; pv[rr][2 * q + 1] = v.y;
                             }
                         }
@@ -172,7 +189,10 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
         };
         if (a.resident) {
             xrow = xb;
-            rows_fma(slice, NP, nrow);
+            rows_fma(std::false_type{}, std::integral_constant<int, RS>{}, slice, NP, nrow);
+        } else if (a.ldg) {
+            xrow = xb;
+            rows_fma(std::true_type{}, std::integral_constant<int, RSG>{}, P + (size_t)r0 * a.ld, a.ld, nrow);
         } else {
             const int nst = (nrow + ring_rows - 1) / ring_rows;
             auto issue = [&](int st) {                 // thread 0: stage st into buffer q_issue % kRing
@@ -193,95 +213,167 @@ __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
                 __syncthreads();                       // every thread is done with stage st - 1's buffer
                 if (threadIdx.x == 0 && st + kRing - 1 < nst) issue(st + kRing - 1);
                 xrow = xb + st * ring_rows;
-                rows_fma(ring + (size_t)buf * ring_rows * NP, NP, min(ring_rows, nrow - st * ring_rows));
+                rows_fma(std::false_type{}, std::integral_constant<int, RS>{}, ring + (size_t)buf * ring_rows * NP, NP, min(ring_rows, nrow - st * ring_rows));
                 ++q_cons;
             }
         }
-        // push partials to the owners of the columns: recv[c][j - owner R] in the owner's smem
-        if (a.p2p) {
-            if (threadIdx.x == 0) mbar_expect_tx(&xbar[0], bytesA);
+    };
+
+    if (a.one_x) {
+        // One exchange per product (st.async + mbarrier, double-buffered by product parity b): every
+        // CTA pushes its partial of column j straight to the CTA owning row r = (j + l) mod N (whose
+        // next x_r is y_j, Theorem 2's gather), with its partial total (-> s) and its change partial of
+        // the previous product. The owner sums the C partials of each row in CTA order. A CTA sends
+        // product k + 2 into buffer b only after it has every CTA's product k + 1, which each sends
+        // after reading its buffer b of product k, so two buffers suffice.
+        double *rx = fsm + R;
+        const uint32_t bytesX = 8u * ((uint32_t)C * (uint32_t)nrow + 2u * (uint32_t)C);
+        for (;;) {
+            double acc[NC];
+            gemv(acc);
+            double tp = 0.0;                            // (a pair's odd column may be row padding)
+            const int b = k & 1;
+            double *rb = rx + (size_t)b * C * R;
+            if (threadIdx.x == 0) mbar_expect_tx(&xbar[b], bytesX);
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int j = 2 * threadIdx.x + 2 * kFT * q + e;
                     if (j < N) {
-                        const uint32_t ow = (uint32_t)(j / R);
-                        st_async_f64(mapa_u32(smem_u32(recv + (size_t)c * R + (j - (int)ow * R)), ow), acc[2 * q + e],
-                                     mapa_u32(smem_u32(&xbar[0]), ow));
+                        int r = j + l;
+                        if (r >= N) r -= N;
+                        const uint32_t ow = (uint32_t)(r / R);
+                        st_async_f64(mapa_u32(smem_u32(rb + (size_t)c * R + (r - (int)ow * R)), ow), acc[2 * q + e],
+                                     mapa_u32(smem_u32(&xbar[b]), ow));
+                        tp += acc[2 * q + e];
                     }
                 }
             }
-            if (threadIdx.x < C)
-                st_async_f64(mapa_u32(smem_u32(&sh.exA[kFMaxC + c]), threadIdx.x), dpart,
-                             mapa_u32(smem_u32(&xbar[0]), threadIdx.x));
-            mbar_wait(&xbar[0], (uint32_t)k & 1u);
-        } else {
+            const double tot = fblock_sum(tp, sh.red);  // after the partials are on their way
+            if (threadIdx.x < C) {
+                const uint32_t bar = mapa_u32(smem_u32(&xbar[b]), threadIdx.x);
+                st_async_f64(mapa_u32(smem_u32(&sh.tx[b][c]), threadIdx.x), tot, bar);
+                st_async_f64(mapa_u32(smem_u32(&sh.dx[b][c]), threadIdx.x), dpart, bar);
+            }
+            mbar_wait(&xbar[b], (uint32_t)(k >> 1) & 1u);
+            if (k > 0) {
+                double t = 0.0;
+                for (int cc = 0; cc < C; ++cc) t += sh.dx[b][cc];
+                change = t;
+                if (change < a.tol) { conv = 1; break; }
+                if (k >= a.max_iter || !(s_prev > 0.0) || !isfinite(change)) break;
+            }
+            double s = 0.0;
+            for (int cc = 0; cc < C; ++cc) s += sh.tx[b][cc];
+            double d = 0.0;
+            if ((int)threadIdx.x < nrow) {              // y of the column feeding my row, its change
+                double yj = 0.0;
+                for (int cc = 0; cc < C; ++cc) yj += rb[(size_t)cc * R + threadIdx.x];
+                d = fabs(yj / s - xb[threadIdx.x] / s_prev);
+                xb[threadIdx.x] = yj;
+            }
+            dpart = fblock_sum(d, sh.red);
+            s_prev = s;
+            ++k;
+        }
+        cl.sync();   // nothing is in flight to a CTA that exits
+        const int o = a.n_inline ? a.oidx_in[mv] : a.out_idx[mv];
+        if (o >= 0 && (int)threadIdx.x < nrow) {     // pi^k over the columns feeding my rows
+            int j = r0 + (int)threadIdx.x - l;
+            if (j < 0) j += N;
+            a.pi[(size_t)o * N + j] = xb[threadIdx.x] / s_prev;
+        }
+    } else {
+        for (;;) {
+            double acc[NC];
+            gemv(acc);
+            // push partials to the owners of the columns: recv[c][j - owner R] in the owner's smem
+            if (a.p2p) {
+                if (threadIdx.x == 0) mbar_expect_tx(&xbar[0], bytesA);
 #pragma unroll
-            for (int q = 0; q < Q; ++q) {
+                for (int q = 0; q < Q; ++q) {
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int j = 2 * threadIdx.x + 2 * kFT * q + e;
-                    if (j < N) {
-                        const int ow = j / R;
-                        cl.map_shared_rank(recv, ow)[(size_t)c * R + (j - ow * R)] = acc[2 * q + e];
+                    for (int e = 0; e < 2; ++e) {
+                        const int j = 2 * threadIdx.x + 2 * kFT * q + e;
+                        if (j < N) {
+                            const uint32_t ow = (uint32_t)(j / R);
+                            st_async_f64(mapa_u32(smem_u32(recv + (size_t)c * R + (j - (int)ow * R)), ow), acc[2 * q + e],
+                                         mapa_u32(smem_u32(&xbar[0]), ow));
+                        }
                     }
                 }
+                if (threadIdx.x < C)
+                    st_async_f64(mapa_u32(smem_u32(&sh.exA[kFMaxC + c]), threadIdx.x), dpart,
+                                 mapa_u32(smem_u32(&xbar[0]), threadIdx.x));
+                mbar_wait(&xbar[0], (uint32_t)k & 1u);
+            } else {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int j = 2 * threadIdx.x + 2 * kFT * q + e;
+                        if (j < N) {
+                            const int ow = j / R;
+                            cl.map_shared_rank(recv, ow)[(size_t)c * R + (j - ow * R)] = acc[2 * q + e];
+                        }
+                    }
+                }
+                if (threadIdx.x < C) cl.map_shared_rank(sh.exA, threadIdx.x)[kFMaxC + c] = dpart;
+                cl.sync();   // A
             }
-            if (threadIdx.x < C) cl.map_shared_rank(sh.exA, threadIdx.x)[kFMaxC + c] = dpart;
-            cl.sync();   // A
+            if (k > 0) {
+                double t = 0.0;
+                for (int cc = 0; cc < C; ++cc) t += sh.exA[kFMaxC + cc];
+                change = t;
+                if (change < a.tol) { conv = 1; break; }
+                if (k >= a.max_iter || !(s_prev > 0.0) || !isfinite(change)) break;
+            }
+            // ---- B: owners add the partials (fixed order); push y to the x buffers; publish sum(y)
+            double ys = 0.0, yj = 0.0;
+            const int j = c * R + (int)threadIdx.x;
+            const bool own = (int)threadIdx.x < R && j < N;
+            if (a.p2p && threadIdx.x == 0) mbar_expect_tx(&xbar[1], bytesB);
+            if (own) {
+                for (int cc = 0; cc < C; ++cc) yj += recv[(size_t)cc * R + threadIdx.x];
+                ys = yj;
+                int r = j + l;
+                if (r >= N) r -= N;
+                const int ow = r / R;
+                if (a.p2p)
+                    st_async_f64(mapa_u32(smem_u32(xb + (r - ow * R)), (uint32_t)ow), yj,
+                                 mapa_u32(smem_u32(&xbar[1]), (uint32_t)ow));
+                else
+                    cl.map_shared_rank(xb, ow)[r - ow * R] = yj;
+            }
+            ys = fblock_sum(ys, sh.red);
+            if (a.p2p) {
+                if (threadIdx.x < C)
+                    st_async_f64(mapa_u32(smem_u32(&sh.exB[c]), threadIdx.x), ys, mapa_u32(smem_u32(&xbar[1]), threadIdx.x));
+                mbar_wait(&xbar[1], (uint32_t)k & 1u);
+            } else {
+                if (threadIdx.x < C) cl.map_shared_rank(sh.exB, threadIdx.x)[c] = ys;
+                cl.sync();   // B
+            }
+            double s = 0.0;
+            for (int cc = 0; cc < C; ++cc) s += sh.exB[cc];
+            // ---- C: L1 change of the normalised iterates over my columns
+            double d = 0.0;
+            if (own) {
+                d = fabs(yj / s - yp[threadIdx.x] / s_prev);
+                yp[threadIdx.x] = yj;
+            }
+            dpart = fblock_sum(d, sh.red);
+            s_prev = s;
+            ++k;
         }
-        if (k > 0) {
-            double t = 0.0;
-            for (int cc = 0; cc < C; ++cc) t += sh.exA[kFMaxC + cc];
-            change = t;
-            if (change < a.tol) { conv = 1; break; }
-            if (k >= a.max_iter || !(s_prev > 0.0) || !isfinite(change)) break;
+        if (a.p2p) cl.sync();   // nothing is in flight to a CTA that exits (every phase was waited for)
+        // pi^k = y / s over my columns
+        const int o = a.n_inline ? a.oidx_in[mv] : a.out_idx[mv];
+        if (o >= 0) {
+            const int j = c * R + (int)threadIdx.x;
+            if ((int)threadIdx.x < R && j < N) a.pi[(size_t)o * N + j] = yp[threadIdx.x] / s_prev;
         }
-        // ---- B: owners add the partials (fixed order); push y to the x buffers; publish sum(y)
-        double ys = 0.0, yj = 0.0;
-        const int j = c * R + (int)threadIdx.x;
-        const bool own = (int)threadIdx.x < R && j < N;
-        if (a.p2p && threadIdx.x == 0) mbar_expect_tx(&xbar[1], bytesB);
-        if (own) {
-            for (int cc = 0; cc < C; ++cc) yj += recv[(size_t)cc * R + threadIdx.x];
-            ys = yj;
-            int r = j + l;
-            if (r >= N) r -= N;
-            const int ow = r / R;
-            if (a.p2p)
-                st_async_f64(mapa_u32(smem_u32(xb + (r - ow * R)), (uint32_t)ow), yj,
-                             mapa_u32(smem_u32(&xbar[1]), (uint32_t)ow));
-            else
-                cl.map_shared_rank(xb, ow)[r - ow * R] = yj;
-        }
-        ys = fblock_sum(ys, sh.red);
-        if (a.p2p) {
-            if (threadIdx.x < C)
-                st_async_f64(mapa_u32(smem_u32(&sh.exB[c]), threadIdx.x), ys, mapa_u32(smem_u32(&xbar[1]), threadIdx.x));
-            mbar_wait(&xbar[1], (uint32_t)k & 1u);
-        } else {
-            if (threadIdx.x < C) cl.map_shared_rank(sh.exB, threadIdx.x)[c] = ys;
-            cl.sync();   // B
-        }
-        double s = 0.0;
-        for (int cc = 0; cc < C; ++cc) s += sh.exB[cc];
-        // ---- C: L1 change of the normalised iterates over my columns
-        double d = 0.0;
-        if (own) {
-            d = fabs(yj / s - yp[threadIdx.x] / s_prev);
-            yp[threadIdx.x] = yj;
-        }
-        dpart = fblock_sum(d, sh.red);
-        s_prev = s;
-        ++k;
-    }
-    if (a.p2p) cl.sync();   // nothing is in flight to a CTA that exits (every phase was waited for)
-    // pi^k = y / s over my columns
-    const int o = a.n_inline ? a.oidx_in[mv] : a.out_idx[mv];
-    if (o >= 0) {
-        const int j = c * R + (int)threadIdx.x;
-        if ((int)threadIdx.x < R && j < N) a.pi[(size_t)o * N + j] = yp[threadIdx.x] / s_prev;
     }
     if (c == 0 && threadIdx.x == 0) {
         SolveState st;
@@ -323,8 +415,8 @@ size_t fused_ring_bytes(int N, int dtype) {
     return kRing * rows * row;
 }
 size_t fused_smem(const FusedArgs &a, int dtype) {
-    return sizeof(double) * (((size_t)a.R * (a.C + 2) + 1) & ~(size_t)1) +
-           (a.resident ? fused_slice_bytes(a.N, a.R, dtype) : fused_ring_bytes(a.N, dtype));
+    return sizeof(double) * (((size_t)a.R * (a.one_x ? 2 * a.C + 1 : a.C + 2) + 1) & ~(size_t)1) +
+           (a.resident ? fused_slice_bytes(a.N, a.R, dtype) : a.ldg ? 0 : fused_ring_bytes(a.N, dtype));
 }
 
 template <typename T>

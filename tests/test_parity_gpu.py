@@ -368,17 +368,52 @@ def test_fused_p2p_exchange_equals_cluster_barrier(spl, n, monkeypatch):
     f = random_flux(np.random.default_rng(4400 + n), n, 2)
     P0 = spl.build_base(f, torch.float64)
     T = np.array([[3.0, 61.5, 140.0]])
+    monkeypatch.setenv("SPLIDAR_FUSED_1X", "0")          # both in the two-exchange form
     a = spl.Plan(P0, f.t_r, T, tol=1e-12)
     monkeypatch.setenv("SPLIDAR_FUSED_P2P", "0")
     b = spl.Plan(P0, f.t_r, T, tol=1e-12)
     monkeypatch.delenv("SPLIDAR_FUSED_P2P")
-    assert a.fused and b.fused
-    ia, ib = a.execute(check=False), b.execute(check=False)
+    monkeypatch.setenv("SPLIDAR_FUSED_LDG", "0")         # L2-streamed rows through the TMA ring
+    c = spl.Plan(P0, f.t_r, T, tol=1e-12)
+    monkeypatch.delenv("SPLIDAR_FUSED_LDG")
+    monkeypatch.delenv("SPLIDAR_FUSED_1X")
+    assert a.fused and b.fused and c.fused
+    ia, ib, ic = a.execute(check=False), b.execute(check=False), c.execute(check=False)
     assert torch.equal(a.pi, b.pi) and ia == ib
+    assert torch.equal(a.pi, c.pi) and ia == ic           # register loads == ring: same FMA order
     a.execute(check=False)                       # relaunch: the mbarrier phases start again
     assert torch.equal(a.pi, b.pi)
-    a.close()
-    b.close()
+    for x in (a, b, c):
+        x.close()
+
+
+@pytest.mark.parametrize("n", [2, 37, 256, 700, 1024, 1537, 2048])
+def test_fused_one_exchange_equals_two(spl, n, monkeypatch):
+    """The default fused solver (one exchange per product: partials pushed straight to the CTA whose
+    row they feed, s from the CTAs' partial totals) against the two-exchange form (owners sum and
+    redistribute y, SPLIDAR_FUSED_1X=0): the same y in the same order, s summed in another order, so
+    pi agrees to rounding (<= 1e-14 L1; 2e-12 if a count differs) and the iteration counts to +-1;
+    relaunches are bit-identical."""
+    f = random_flux(np.random.default_rng(4500 + n), n, 2)
+    for dt in (torch.float64, torch.float32):
+        P0 = spl.build_base(f, dt)
+        T = np.array([[3.0, 61.5, 140.0, 250.0]])
+        a = spl.Plan(P0, f.t_r, T, tol=1e-12)
+        monkeypatch.setenv("SPLIDAR_FUSED_1X", "0")
+        b = spl.Plan(P0, f.t_r, T, tol=1e-12)
+        monkeypatch.delenv("SPLIDAR_FUSED_1X")
+        assert a.fused and b.fused
+        ia, ib = a.execute(check=False), b.execute(check=False)
+        for v in range(T.shape[1]):
+            assert abs(ia[v]["iters"] - ib[v]["iters"]) <= 1
+            assert ia[v]["shift_l"] == ib[v]["shift_l"]
+            # equal counts: rounding only; one more product: the last L1 change (< tol) on top
+            bound = 1e-14 if ia[v]["iters"] == ib[v]["iters"] else 2e-12
+            assert np.sum(np.abs(_np(a.pi[0, v]) - _np(b.pi[0, v]))) <= bound
+        p1 = a.pi.clone()
+        assert a.execute(check=False) == ia and torch.equal(a.pi, p1)
+        a.close()
+        b.close()
 
 
 def test_ragged_large_n(spl):
