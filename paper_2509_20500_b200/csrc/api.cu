@@ -378,6 +378,11 @@ struct splidar_plan_s {
     int M = 0, V = 0, Vreal = 0;
     std::vector<int> lsh;          // [M * V] (padded)
     std::vector<SolveState> host;  // [M * V]
+    SolveState *host_pinned = nullptr;   // [M * V] page-locked copy target of splidar_plan_info (lazy)
+    // fused building plans: steps 1-4 (flux vectors, build, fused solver) captured once as a graph,
+    // replayed by launches on a stream that is not capturing; re-captured when fargs change
+    cudaGraphExec_t fexec = nullptr;
+    FusedArgs fargs_cap;
     std::vector<int> out_idx;      // [M * V]
     // eager mode (SPLIDAR_EAGER=1 at plan creation): the same kernels launched from a host loop that
     // reads the any-active flag after each iteration; for profilers that do not descend into
@@ -736,6 +741,8 @@ void splidar_plan_destroy(splidar_plan plan) {
     if (!plan) return;
     if (plan->exec) cudaGraphExecDestroy(plan->exec);
     if (plan->host_flag) cudaFreeHost(plan->host_flag);
+    if (plan->host_pinned) cudaFreeHost(plan->host_pinned);
+    if (plan->fexec) cudaGraphExecDestroy(plan->fexec);
     if (plan->graph) cudaGraphDestroy(plan->graph);
     delete plan;
 }
@@ -939,6 +946,36 @@ splidar_status splidar_plan_launch(splidar_plan plan, void *stream) {
     SPL_NVTX_RANGE();
     if (!plan) return SPLIDAR_EINVAL;
     if (plan->fused) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        SPL_CUDA(cudaStreamIsCapturing((cudaStream_t)stream, &cap));
+        if (plan->with_build && cap == cudaStreamCaptureStatusNone && !plan->eager) {
+            // one graph launch instead of three kernel launches (host cost of the small-N step)
+            if (plan->fexec && memcmp(&plan->fargs_cap, &plan->fargs, sizeof(FusedArgs)) != 0) {
+                cudaGraphExecDestroy(plan->fexec);
+                plan->fexec = nullptr;
+            }
+            if (!plan->fexec) {
+                void *fn = nullptr;   // kernel attributes are set outside the capture
+                SPL_CUDA(fused_fn(plan->dt, plan->fargs.N, &fn));
+                cudaStream_t cs;
+                SPL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+                cudaGraph_t g = nullptr;
+                cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+                if (e == cudaSuccess) {
+                    cudaError_t eb = plan_enqueue_build(plan, plan->dt, cs);
+                    if (eb == cudaSuccess) eb = launch_fused(plan->dt, plan->fargs, cs);
+                    e = cudaStreamEndCapture(cs, &g);
+                    if (e == cudaSuccess) e = eb;
+                }
+                if (e == cudaSuccess) e = cudaGraphInstantiate(&plan->fexec, g, 0);
+                if (g) cudaGraphDestroy(g);
+                cudaStreamDestroy(cs);
+                if (e != cudaSuccess) plan->fexec = nullptr;
+                SPL_CUDA(e);
+                memcpy(&plan->fargs_cap, &plan->fargs, sizeof(FusedArgs));
+            }
+            return cuda_status(cudaGraphLaunch(plan->fexec, (cudaStream_t)stream));
+        }
         if (plan->with_build) SPL_CUDA(plan_enqueue_build(plan, plan->dt, (cudaStream_t)stream));
         return cuda_status(launch_fused(plan->dt, plan->fargs, (cudaStream_t)stream));
     }
@@ -949,13 +986,20 @@ splidar_status splidar_plan_launch(splidar_plan plan, void *stream) {
 splidar_status splidar_plan_info(splidar_plan plan, splidar_solve_info *info, void *stream) {
     if (!plan) return SPLIDAR_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
-    SPL_CUDA(cudaMemcpyAsync(plan->host.data(), plan->args.st, sizeof(SolveState) * plan->host.size(),
-                             cudaMemcpyDeviceToHost, s));
+    // page-locked target: an asynchronous copy ordered behind the launch, then the one synchronisation
+    // (a pageable target would stage through a driver buffer)
+    if (!plan->host_pinned &&
+        cudaMallocHost(reinterpret_cast<void **>(&plan->host_pinned), sizeof(SolveState) * plan->host.size()) != cudaSuccess) {
+        (void)cudaGetLastError();
+        plan->host_pinned = nullptr;
+    }
+    SolveState *hs = plan->host_pinned ? plan->host_pinned : plan->host.data();
+    SPL_CUDA(cudaMemcpyAsync(hs, plan->args.st, sizeof(SolveState) * plan->host.size(), cudaMemcpyDeviceToHost, s));
     SPL_CUDA(cudaStreamSynchronize(s));
     bool all = true;
     for (int m = 0; m < plan->M; ++m)
         for (int v = 0; v < plan->Vreal; ++v) {
-            const SolveState &h = plan->host[(size_t)m * plan->V + v];
+            const SolveState &h = hs[(size_t)m * plan->V + v];
             all = all && h.converged;
             if (info) {
                 splidar_solve_info &o = info[(size_t)m * plan->Vreal + v];

@@ -232,6 +232,7 @@ struct FusedArgs {
 int fused_shape(int N, int *C, int *R);
 int fused_resident(int N, int R, int dtype);
 cudaError_t launch_fused(int dtype, const FusedArgs &a, cudaStream_t s);
+cudaError_t fused_fn(int dtype, int N, void **fn);   // the kernel instance; sets its attributes (not in a capture)
 
 // ---- second eigenvalue of a stored matrix (spectral_dense.cu; SURVEY §8(f) f1 on K6) -----------
 struct SdState {

@@ -478,7 +478,13 @@ class Plan:
         """New theta for a building plan (Plan(build=...)): same N and t_r, one flux per matrix."""
         fl = list(fluxes) if isinstance(fluxes, (list, tuple)) else [fluxes]
         fas = [_flux_arg(f) for f in fl]
-        arr = (_Flux * len(fl))(*[fa.s for fa in fas])
+        key = tuple(id(fa) for fa in fas)          # the marshalled array of the last call, reused
+        last = getattr(self, "_flux_arr", None)
+        if last is not None and last[0] == key:
+            arr = last[1]
+        else:
+            arr = (_Flux * len(fl))(*[fa.s for fa in fas])
+            self._flux_arr = (key, arr, fas)       # fas keeps the parameter arrays arr points into alive
         _check(_lib().splidar_plan_set_fluxes(self._h, arr, len(fl), _stream(stream)), "splidar_plan_set_fluxes")
 
     @property

@@ -215,3 +215,36 @@ def test_building_plan_fp32_shapes(spl, monkeypatch, N, V, M):
     assert [i["iters"] for i in ia] == [i["iters"] for i in ib]
     assert all(i["converged"] for i in ia)
     assert np.max(np.sum(np.abs(pia - pib), axis=-1)) <= 1e-13
+
+
+@pytest.mark.parametrize("N,dtype", [(256, torch.float64), (1024, torch.float64), (700, torch.float32)])
+def test_fused_building_plan_graph_replay(spl, N, dtype):
+    """Small-N building plans launch steps 1-4 as one cached graph on a stream that is not capturing,
+    and as kernels into a caller's capture: both equal the separate build + plan, across replays and
+    after set_fluxes (the graph reads theta from the workspace, so it is not re-captured)."""
+    f = _c5(N)
+    g = Flux(f.t_r, N, (37.0, 120.0), (0.3, 0.2), (1.2, 0.4), 0.3)
+    T = np.array([[55.0, 430.0]])
+    P0 = spl.empty_matrix(N, dtype)
+    plan = spl.Plan(P0, f.t_r, T, tol=1e-12, build=[f])
+    assert plan.fused
+    for flux in (f, g, f):
+        plan.set_fluxes([flux])
+        i1 = plan.execute()
+        p1 = plan.pi.clone()
+        i2 = plan.execute()                                   # replay
+        assert i1 == i2 and torch.equal(p1, plan.pi)
+        st = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()                        # the caller's capture: direct kernels
+        with torch.cuda.graph(graph, stream=st):
+            plan.launch(stream=st)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert plan.info() == i1 and torch.equal(p1, plan.pi)
+        P1 = spl.build_base(flux, dtype)
+        ref = spl.Plan(P1, flux.t_r, T, tol=1e-12)
+        ir = ref.execute()
+        assert [i["iters"] for i in ir] == [i["iters"] for i in i1]
+        assert torch.sum(torch.abs(ref.pi - plan.pi)).item() <= 1e-14
+        ref.close()
+    plan.close()
