@@ -70,7 +70,9 @@ template <typename T, int Q>
 __global__ void __launch_bounds__(kFT, 1) k_power_fused(const FusedArgs a) {
     constexpr int NC = 2 * Q;
     constexpr int RS = Q <= 2 ? 8 : 4;
-    constexpr int RSG = Q <= 2 ? 16 : 8;     // direct global loads: twice the rows in flight
+    // direct global loads: twice the rows in flight at Q = 2 (N = 513..1024, the c2 shape); at Q = 1
+    // (mostly rows resident in shared memory) the register budget of RS keeps 2x more clusters resident
+    constexpr int RSG = Q == 2 ? 16 : 8;
     pdl_wait();        // PDL secondary of the build (launch_fused); no-op otherwise
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double fsm[];
